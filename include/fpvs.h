@@ -1,0 +1,200 @@
+/*
+ * fpvs.h — C ABI of libfpvs.so, the B200 (sm_100a) NeuralPVS hot path.
+ *
+ * The reference (pkg/src/froxelpvs) is pure Python/numpy and has no FFI of
+ * its own; its boundary is the Python API of froxelpvs.interleave and
+ * froxelpvs.neural.  Each entry point below states the
+ * reference function it replaces.  The Python package
+ * paper_2509_24677_b200 binds these through ctypes and re-exposes the
+ * reference names; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - every pointer argument is a DEVICE pointer unless named host_*;
+ *  - every call takes a cudaStream_t passed as void* and is stream-ordered,
+ *    never synchronises and never allocates (graph-capturable);
+ *  - row counts produced on the device (active cells) are passed back as
+ *    device int32 pointers ("n_*_dev"), so kernels size their work from
+ *    device memory and a whole frame runs with no host round trip; buffers
+ *    are sized by a host-known capacity ("cap_*");
+ *  - return 0 on success, FPVS_EINVAL (1) on bad arguments, FPVS_ESHAPE (2)
+ *    on shape mismatch, FPVS_ECUDA (3) on a CUDA launch error;
+ *    fpvs_last_error() returns a thread-local message.  The Python layer maps
+ *    1/2 to ValueError, as the reference raises ValueError
+ *    (interleave.py:58-59, 78-79; neural.py:203-205, 518-522).
+ *
+ * Layouts (HBM)
+ *  - packed grid: B x (Nz, Ny, Nx/8) bytes, x-fastest LSB-first, the FPVS
+ *    payload of froxel.py:3-4 / 96-104, one grid after another;
+ *  - dense grid: (B, Nx, Ny, Nz) C-order, as the reference's ndarray;
+ *  - cells: (B, X, Y, Z, d^3) channels-last, channel k = lx + d*(ly + d*lz)
+ *    (interleave.py:54-65);
+ *  - sparse features: rows of active cells in C-order of (b, x, y, z),
+ *    row stride ld (elements) so concatenation is a column offset;
+ *  - coords: int32 [cap][4] = (b, x, y, z);
+ *  - neighbour tables: int32 [cap][K] row index or -1; subm K = 27 with
+ *    offset j = 9a + 3b + c <-> (a-1, b-1, c-1) (neural.py:187-199),
+ *    down K = 8 with child = 2*parent + (a, b, c), j = 4a + 2b + c,
+ *    up K = 8 with only the fine cell's own parity slot set;
+ *  - weights (reference layout): f32 (K*Cin, Cout), row = j*Cin + ci
+ *    (neural.py:163-166); the tensor-core path takes them pre-packed by
+ *    fpvs_pack_weights_tc.
+ */
+#ifndef FPVS_H_
+#define FPVS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { FPVS_OK = 0, FPVS_EINVAL = 1, FPVS_ESHAPE = 2, FPVS_ECUDA = 3 };
+enum { FPVS_IN_PACKED = 0, FPVS_IN_U8 = 1, FPVS_IN_F32 = 2 };
+enum { FPVS_F32 = 0, FPVS_BF16 = 1 };
+enum { FPVS_ACT_NONE = 0, FPVS_ACT_RELU = 1, FPVS_ACT_SIGMOID = 2 };
+
+const char* fpvs_last_error(void);
+int fpvs_abi_version(void);
+
+/* ---- (1) interleave / deinterleave ------------------------------------ */
+
+/* Replaces interleave(grid, d) (interleave.py:54-65) for B grids at once.
+ * in: packed bits, u8 or f32 dense; out: (B, Nx/d, Ny/d, Nz/d, d^3) f32/bf16;
+ * cell_active (nullable): u8 (B, X, Y, Z), 1 iff the block holds a nonzero. */
+int fpvs_interleave(const void* in, int in_fmt, int B, int Nx, int Ny, int Nz, int d,
+                    void* out, int out_dtype, uint8_t* cell_active, void* stream);
+
+/* Replaces deinterleave(t, d, threshold) (interleave.py:68-85).
+ * in: (B, X, Y, Z, d^3) f32/bf16.  If tau is NaN, out is f32 dense
+ * (B, X*d, Y*d, Z*d); else out is packed bits of [value >= tau]. */
+int fpvs_deinterleave(const void* in, int in_dtype, int B, int X, int Y, int Z, int d,
+                      float tau, void* out, void* stream);
+
+/* ---- (2) kernel maps --------------------------------------------------- */
+
+/* Scratch bytes for fpvs_kmap_compact over a (B, X, Y, Z) cell grid. */
+size_t fpvs_kmap_workspace_size(int B, int X, int Y, int Z);
+
+/* Active cells straight from packed bits (fused interleave): cell_active[c] =
+ * any bit of the d^3 block is set. */
+int fpvs_cell_active_from_bits(const uint8_t* bits, int B, int Nx, int Ny, int Nz, int d,
+                               uint8_t* cell_active, void* stream);
+
+/* Stream compaction of cell_active in C-order: coords[rank] = (b,x,y,z),
+ * index_vol[cell] = rank or -1, *n_active_dev = count (clamped to cap). */
+int fpvs_kmap_compact(const uint8_t* cell_active, int B, int X, int Y, int Z,
+                      int32_t* coords, int32_t* index_vol, int32_t* n_active_dev, int cap,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* Submanifold 3x3x3 neighbour table: nbr[i][j] = index_vol[coords[i] + o_j]. */
+int fpvs_kmap_subm(const int32_t* coords, const int32_t* n_active_dev, int cap,
+                   const int32_t* index_vol, int B, int X, int Y, int Z,
+                   int32_t* nbr, void* stream);
+
+/* Parent flags of a k2s2 down-conv: coarse_active[b, x>>1, y>>1, z>>1] = 1.
+ * coarse_active must be zeroed first (fine dims X, Y, Z must be even). */
+int fpvs_kmap_coarsen(const int32_t* coords, const int32_t* n_active_dev, int cap,
+                      int B, int X, int Y, int Z, uint8_t* coarse_active, void* stream);
+
+/* down[p][j] = fine row of child 2*coarse[p] + (a,b,c) or -1. */
+int fpvs_kmap_down(const int32_t* coarse_coords, const int32_t* n_coarse_dev, int cap_coarse,
+                   const int32_t* fine_index_vol, int B, int X, int Y, int Z,
+                   int32_t* down, void* stream);
+
+/* up[i][j] = parent row if j == parity(fine[i]) else -1 (fine dims X, Y, Z). */
+int fpvs_kmap_up(const int32_t* fine_coords, const int32_t* n_fine_dev, int cap_fine,
+                 const int32_t* coarse_index_vol, int B, int X, int Y, int Z,
+                 int32_t* up, void* stream);
+
+/* Open-addressing GPU hash alternative to index_vol (general, unbounded
+ * grids): capacity slots of (key int64, value int32); key = linear cell id. */
+int fpvs_hash_build(const int32_t* coords, const int32_t* n_active_dev, int cap,
+                    int B, int X, int Y, int Z, int64_t* keys, int32_t* vals,
+                    int hash_capacity, void* stream);
+int fpvs_kmap_subm_hash(const int32_t* coords, const int32_t* n_active_dev, int cap,
+                        const int64_t* keys, const int32_t* vals, int hash_capacity,
+                        int B, int X, int Y, int Z, int32_t* nbr, void* stream);
+
+/* Features of active cells from packed bits (the sparse interleave):
+ * x[i][k] = bit of (b, x*d + lx, y*d + ly, z*d + lz), k = lx + d*(ly + d*lz). */
+int fpvs_gather_cells_bits(const uint8_t* bits, int B, int Nx, int Ny, int Nz, int d,
+                           const int32_t* coords, const int32_t* n_active_dev, int cap,
+                           void* x, int ldx, int dtype, void* stream);
+
+/* ---- (3) sparse convolution ------------------------------------------- */
+
+/* Implicit gather-GEMM: y[i][col_off + c] = act(bias[c] + sum_j x[nbr[i][j]] . W_j[:, c]).
+ * nbr may be NULL with K == 1 (identity gather, 1x1x1 conv).
+ * SIMT FFMA path (fp32 mode, correctness anchor): w f32 (K*Cin, Cout). */
+int fpvs_spconv_simt(const void* x, int ldx, int in_dtype, const int32_t* nbr, int K,
+                     const int32_t* n_out_dev, int cap_out, const float* w, const float* bias,
+                     int cin, int cout, int act, void* y, int ldy, int col_off, int out_dtype,
+                     void* stream);
+
+/* Bytes of the packed tensor-core weight image for (K, Cin, Cout). */
+size_t fpvs_pack_weights_tc_size(int K, int cin, int cout);
+/* Pack f32 (K*Cin, Cout) weights into the bf16 SW128 K-major smem image. */
+int fpvs_pack_weights_tc(const float* w, int K, int cin, int cout, void* packed, void* stream);
+
+/* tcgen05 path: bf16 in, fp32 TMEM accumulate, fused bias + act, bf16 out. */
+int fpvs_spconv_tc(const void* x, int ldx, const int32_t* nbr, int K,
+                   const int32_t* n_out_dev, int cap_out, const void* w_packed,
+                   const float* bias, int cin, int cout, int act,
+                   void* y, int ldy, int col_off, void* stream);
+
+/* Fused head (replaces the final Conv3d + sigmoid + deinterleave(tau),
+ * neural.py:513-526): 1x1x1 conv Cin -> d^3, sigmoid, [p >= tau], packed-bit
+ * scatter into out_bits (zeroed first; u32-aligned).  probs (nullable):
+ * f32 [cap][d^3] per-active-cell probabilities; logits likewise. */
+int fpvs_head_simt(const void* x, int ldx, int in_dtype, const int32_t* coords,
+                   const int32_t* n_dev, int cap, const float* w, const float* bias,
+                   int cin, int d, int B, int Nx, int Ny, int Nz, float tau,
+                   uint8_t* out_bits, float* probs, float* logits, void* stream);
+int fpvs_head_tc(const void* x, int ldx, const int32_t* coords, const int32_t* n_dev, int cap,
+                 const void* w_packed, const float* bias, int cin, int d,
+                 int B, int Nx, int Ny, int Nz, float tau,
+                 uint8_t* out_bits, float* probs, float* logits, void* stream);
+
+/* ---- (4) training ------------------------------------------------------ */
+
+/* Per-sample soft counts over active-cell probabilities (ConfusionCounts,
+ * neural.py:130-144): sums[3b..3b+2] = (sum p*g, sum p, sum g) in f64, sum g
+ * over the whole label grid.  p: f32 [cap][C]; gt_bits: packed label grids.
+ * sums must hold fpvs_loss_sums_size(B, cap) bytes (results, then per-row
+ * scratch); reductions run in a fixed order (deterministic). */
+size_t fpvs_loss_sums_size(int B, int cap);
+int fpvs_loss_counts(const float* probs, int C, const int32_t* coords, const int32_t* n_dev,
+                     int cap, const uint8_t* gt_bits, int d, int B, int Nx, int Ny, int Nz,
+                     double* sums, void* stream);
+/* dL/dlogit for combined_loss (neural.py:353-399) averaged over the batch,
+ * written as f32 [cap][C]; loss_out[0] = batch-mean loss (f64). */
+int fpvs_loss_grad(const float* probs, int C, const int32_t* coords, const int32_t* n_dev,
+                   int cap, const uint8_t* gt_bits, int d, int B, int Nx, int Ny, int Nz,
+                   const double* sums, double alpha, double lam, float* dlogits,
+                   double* loss_out, void* stream);
+
+/* dgrad: dx[n] += dz[i] . W_j^T over pairs n = nbr[i][j] (mirrored gather:
+ * dx[n] = sum_j dz[nbr[n][K-1-j]] . W_j^T for the symmetric subm map), then
+ * optionally times (ymask[n] > 0) (relu' with z > 0, neural.py:227-228). */
+int fpvs_spconv_dgrad_simt(const float* dz, int lddz, const int32_t* nbr, int K,
+                           const int32_t* n_dev, int cap, const float* w, int cin, int cout,
+                           const float* ymask, int ldm, float* dx, int lddx, void* stream);
+/* wgrad: dw[j*Cin + ci][co] = sum_i x[nbr[i][j]][ci] * dz[i][co]; db = sum_i dz.
+ * Deterministic (fixed split + fixed-order reduction, no float atomics). */
+size_t fpvs_wgrad_workspace_size(int K, int cin, int cout, int cap);
+int fpvs_spconv_wgrad_simt(const float* x, int ldx, const float* dz, int lddz,
+                           const int32_t* nbr, int K, const int32_t* n_dev, int cap,
+                           int cin, int cout, float* dw, float* db,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* Synthetic PVS labels (row LBL): first occupied froxel of any column within
+ * +-radius in x/y; packed in, packed out. */
+int fpvs_first_hit_labels(const uint8_t* bits, int B, int Nx, int Ny, int Nz, int radius,
+                          uint8_t* out_bits, int32_t* zfirst_ws, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FPVS_H_ */

@@ -1,0 +1,118 @@
+"""ctypes binding of libfpvs.so (include/fpvs.h) — the only way into the kernels.
+
+There is no CPU fallback: importing a compute entry point without the built
+library, or calling it without a CUDA device, raises.  Status codes map to
+the reference's exceptions: FPVS_EINVAL / FPVS_ESHAPE -> ValueError (as
+pkg/src/froxelpvs/interleave.py:58-59, neural.py:203-205 raise), FPVS_ECUDA
+-> RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("FPVS_LIB", os.path.join(HERE, "libfpvs.so"))
+
+F32, BF16 = 0, 1
+IN_PACKED, IN_U8, IN_F32 = 0, 1, 2
+ACT = {"none": 0, "relu": 1, "sigmoid": 2}
+
+_i, _f, _d, _p, _z = C.c_int, C.c_float, C.c_double, C.c_void_p, C.c_size_t
+
+# name -> (restype, argtypes); mirrors include/fpvs.h one to one
+SIGNATURES = {
+    "fpvs_last_error": (C.c_char_p, []),
+    "fpvs_abi_version": (_i, []),
+    "fpvs_interleave": (_i, [_p, _i, _i, _i, _i, _i, _i, _p, _i, _p, _p]),
+    "fpvs_deinterleave": (_i, [_p, _i, _i, _i, _i, _i, _i, _f, _p, _p]),
+    "fpvs_kmap_workspace_size": (_z, [_i, _i, _i, _i]),
+    "fpvs_cell_active_from_bits": (_i, [_p, _i, _i, _i, _i, _i, _p, _p]),
+    "fpvs_kmap_compact": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _i, _p, _z, _p]),
+    "fpvs_kmap_subm": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _p, _p]),
+    "fpvs_kmap_coarsen": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p]),
+    "fpvs_kmap_down": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _p, _p]),
+    "fpvs_kmap_up": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _p, _p]),
+    "fpvs_hash_build": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _i, _p]),
+    "fpvs_kmap_subm_hash": (_i, [_p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _p, _p]),
+    "fpvs_gather_cells_bits": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _i, _p, _i, _i, _p]),
+    "fpvs_spconv_simt": (_i, [_p, _i, _i, _p, _i, _p, _i, _p, _p, _i, _i, _i, _p, _i, _i, _i, _p]),
+    "fpvs_pack_weights_tc_size": (_z, [_i, _i, _i]),
+    "fpvs_pack_weights_tc": (_i, [_p, _i, _i, _i, _p, _p]),
+    "fpvs_spconv_tc": (_i, [_p, _i, _p, _i, _p, _i, _p, _p, _i, _i, _i, _p, _i, _i, _p]),
+    "fpvs_head_simt": (_i, [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p, _p]),
+    "fpvs_head_tc": (_i, [_p, _i, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p, _p]),
+    "fpvs_loss_sums_size": (_z, [_i, _i]),
+    "fpvs_loss_counts": (_i, [_p, _i, _p, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p]),
+    "fpvs_loss_grad": (_i, [_p, _i, _p, _p, _i, _p, _i, _i, _i, _i, _i, _p, _d, _d, _p, _p, _p]),
+    "fpvs_spconv_dgrad_simt": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _p, _i, _p, _i, _p]),
+    "fpvs_wgrad_workspace_size": (_z, [_i, _i, _i, _i]),
+    "fpvs_spconv_wgrad_simt": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _p, _p, _p, _z, _p]),
+    "fpvs_first_hit_labels": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p]),
+}
+
+_LIB = None
+
+
+def load():
+    """dlopen libfpvs.so once; raise loudly when it is missing."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libfpvs.so not built at {LIB_PATH}; run python -m paper_2509_24677_b200.build")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def exported_symbols():
+    return list(SIGNATURES)
+
+
+class FpvsError(RuntimeError):
+    pass
+
+
+def call(name: str, *args):
+    """Invoke a status-returning entry point; map status to Python errors."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.fpvs_last_error().decode(errors="replace")
+        if rc in (1, 2):
+            raise ValueError(msg)
+        raise FpvsError(f"{name}: {msg}")
+    return rc
+
+
+def size(name: str, *args) -> int:
+    return int(getattr(load(), name)(*args))
+
+
+# ---- torch plumbing --------------------------------------------------------
+
+def ptr(t) -> int | None:
+    """Device pointer of a CUDA tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("fpvs kernels take CUDA tensors")
+    return t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2509_24677_b200 runs on a CUDA (sm_100a) device; none is visible")
+    load()

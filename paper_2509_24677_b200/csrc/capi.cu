@@ -1,0 +1,19 @@
+// Error reporting and version of the C ABI (include/fpvs.h).
+#include "common.cuh"
+
+namespace fpvs {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+}  // namespace fpvs
+
+extern "C" const char* fpvs_last_error(void) { return fpvs::g_err; }
+extern "C" int fpvs_abi_version(void) { return 1; }

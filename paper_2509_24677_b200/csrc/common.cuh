@@ -1,0 +1,79 @@
+// Shared helpers for libfpvs (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+
+#include "../../include/fpvs.h"
+
+namespace fpvs {
+
+constexpr int kNumSMs = 148;
+
+// thread-local error text behind fpvs_last_error()
+int set_error(int code, const char* fmt, ...);
+
+#define FPVS_CHECK_ARG(cond, ...)                                   \
+  do {                                                              \
+    if (!(cond)) return ::fpvs::set_error(FPVS_EINVAL, __VA_ARGS__); \
+  } while (0)
+
+#define FPVS_CHECK_LAUNCH(name)                                                      \
+  do {                                                                               \
+    cudaError_t e_ = cudaGetLastError();                                             \
+    if (e_ != cudaSuccess)                                                           \
+      return ::fpvs::set_error(FPVS_ECUDA, "%s: %s", name, cudaGetErrorString(e_)); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int grid_for(long long work, int block, int per_sm = 8) {
+  long long g = (work + block - 1) / block;
+  long long cap = (long long)kNumSMs * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// -------- numeric conversion --------------------------------------------
+template <typename T> __device__ __forceinline__ float to_f32(T v);
+template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+template <> __device__ __forceinline__ float to_f32<uint8_t>(uint8_t v) { return (float)v; }
+
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+// split-branch stable sigmoid, as neural.py:151-157
+__device__ __forceinline__ float sigmoidf_stable(float z) {
+  if (z >= 0.f) return 1.f / (1.f + expf(-z));
+  float e = expf(z);
+  return e / (1.f + e);
+}
+
+__device__ __forceinline__ float apply_act(float z, int act) {
+  if (act == FPVS_ACT_RELU) return fmaxf(z, 0.f);
+  if (act == FPVS_ACT_SIGMOID) return sigmoidf_stable(z);
+  return z;
+}
+
+// bit address of froxel (b, x, y, z) in a batch of packed grids
+__device__ __forceinline__ long long bit_byte(int b, int x, int y, int z, int Nx, int Ny, int Nz) {
+  return (long long)b * ((long long)(Nx >> 3) * Ny * Nz) + (x >> 3) +
+         (long long)(Nx >> 3) * (y + (long long)Ny * z);
+}
+
+__device__ __forceinline__ void atomic_or_bit(uint8_t* bits, long long byte, int bit) {
+  uint32_t* word = reinterpret_cast<uint32_t*>(bits + (byte & ~3LL));
+  atomicOr(word, 1u << (((int)(byte & 3)) * 8 + bit));
+}
+
+}  // namespace fpvs

@@ -1,0 +1,493 @@
+"""Drop-in NeuralPVS estimator API (pkg/src/froxelpvs/neural.py) on B200 kernels.
+
+Same names, argument order and error behaviour as the reference:
+``ConvSpec``, ``ModelConfig``, ``TrainConfig``, ``ConfusionCounts``,
+``TrainingDiverged``, ``Conv3d``, ``PvsNet`` (forward / save / load, FPVW),
+``dice_loss``, ``rvl_loss``, ``combined_loss``, ``predict_pvs``; ``train`` lives
+in ``paper_2509_24677_b200.train`` and is re-exported here.
+
+Semantics: the convolution is SUBMANIFOLD — outputs exist on the active cells
+(any nonzero channel) and inactive cells read as zero / predict p = 0.  This is
+the masked form of the reference's dense Conv3d (neural.py:201-219) that
+SURVEY.md §7.3 item 5 fixes as the parity target; the unmasked dense
+reference is not.
+
+Numerics: ``precision="fp32"`` runs the SIMT FFMA kernels (logits within 1e-4
+of the float64 oracle); ``precision="bf16"`` runs the tcgen05 kernels (bf16
+activations and weights, fp32 accumulation in TMEM).
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import _lib
+from . import sparse as sp
+from .froxel import FroxelGrid
+
+FPVW_MAGIC = b"FPVW"
+FPVW_VERSION = 1
+ACTIVATIONS = ("relu", "sigmoid", "none")
+INITS = ("he", "identity", "kaiming_uniform")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class TrainingDiverged(RuntimeError):
+    """Raised when a non-finite loss shows up; carries the batch index (neural.py:30-35)."""
+
+    def __init__(self, batch_index: int, value: float):
+        super().__init__(f"non-finite loss {value!r} at batch {batch_index}")
+        self.batch_index = batch_index
+
+
+# ---------------------------------------------------------------------------
+# configuration (neural.py:42-127)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class ConvSpec:
+    kernel: int
+    in_channels: int
+    out_channels: int
+    activation: str = "relu"
+
+    def __post_init__(self):
+        if self.kernel < 1 or self.kernel % 2 == 0:
+            raise ValueError("kernel size must be odd so spatial dims are preserved")
+        if self.in_channels < 1 or self.out_channels < 1:
+            raise ValueError("channel counts must be positive")
+        if self.activation not in ACTIVATIONS:
+            raise ValueError(f"unknown activation {self.activation!r}")
+
+
+@dataclass
+class ModelConfig:
+    d: int
+    layers: list
+    init: str = "he"
+
+    def __post_init__(self):
+        if self.d < 1:
+            raise ValueError("interleave factor must be >= 1")
+        if not self.layers:
+            raise ValueError("model needs at least one layer")
+        if self.init not in INITS:
+            raise ValueError(f"unknown init {self.init!r}")
+        want = self.d ** 3
+        if self.layers[0].in_channels != want:
+            raise ValueError(f"first layer must take d^3 = {want} channels")
+        for prev, cur in zip(self.layers, self.layers[1:]):
+            if cur.in_channels != prev.out_channels:
+                raise ValueError("layer channel chain is inconsistent")
+        last = self.layers[-1]
+        if last.out_channels != want or last.activation != "sigmoid":
+            raise ValueError(f"final layer must emit d^3 = {want} channels with sigmoid")
+        if self.init == "identity":
+            for spec in self.layers:
+                if spec.out_channels < want and spec is not self.layers[-1]:
+                    raise ValueError("identity init needs >= d^3 channels per hidden layer")
+        for spec in self.layers:
+            if spec.kernel not in (1, 3):
+                raise ValueError("the sparse kernels support kernel sizes 1 and 3")
+        if last.kernel != 1:
+            raise ValueError("the fused head needs a 1x1x1 final layer")
+
+    @classmethod
+    def default(cls, d: int = 4, hidden: int = 32, init: str = "he") -> "ModelConfig":
+        c = d ** 3
+        return cls(d, [ConvSpec(3, c, hidden, "relu"), ConvSpec(3, hidden, hidden, "relu"),
+                       ConvSpec(1, hidden, c, "sigmoid")], init)
+
+    @classmethod
+    def config1(cls, init: str = "kaiming_uniform") -> "ModelConfig":
+        """BASELINE config 1: d=2; 4 x subm 3^3 at 32 ch + ReLU; 1^3 conv to 8 ch; sigmoid."""
+        return cls(2, [ConvSpec(3, 8, 32, "relu")] + [ConvSpec(3, 32, 32, "relu") for _ in range(3)]
+                   + [ConvSpec(1, 32, 8, "sigmoid")], init)
+
+
+@dataclass
+class TrainConfig:
+    alpha: float = 0.1
+    lam: float = 0.99
+    tau: float = 0.5
+    lr: float = 1e-3
+    decay: float = 1e-10
+    batch_size: int = 3
+    epochs: int = 50
+    seed: int = 0
+    optimizer: str = "sgd"        # "sgd" (reference, neural.py:481) | "adamw" (BASELINE config 5)
+    weight_decay: float = 0.01
+
+    def __post_init__(self):
+        for name in ("alpha", "lam", "tau"):
+            v = getattr(self, name)
+            if not 0.0 <= v <= 1.0:
+                raise ValueError(f"{name} must lie in [0, 1], got {v}")
+        if self.lr <= 0:
+            raise ValueError("learning rate must be positive")
+        if not 0.0 <= self.decay < 1.0:
+            raise ValueError("decay must lie in [0, 1)")
+        if self.batch_size < 1 or self.epochs < 0:
+            raise ValueError("batch size must be >= 1 and epochs >= 0")
+        if self.seed < 0:
+            raise ValueError("seed must be nonnegative")
+        if self.optimizer not in ("sgd", "adamw"):
+            raise ValueError(f"unknown optimizer {self.optimizer!r}")
+
+
+@dataclass
+class ConfusionCounts:
+    tp: float
+    fp: float
+    fn: float
+    gtp: float
+
+    @staticmethod
+    def from_soft(pred, gt) -> "ConfusionCounts":
+        """TP = sum p*g, FP = sum p*(1-g), FN = sum (1-p)*g, GTP = sum g (neural.py:139-144)."""
+        p = _as_cuda64(pred)
+        g = _as_cuda64(gt)
+        tp = float((p * g).sum())
+        ps = float(p.sum())
+        gs = float(g.sum())
+        return ConfusionCounts(tp, ps - tp, gs - tp, gs)
+
+
+def _as_cuda64(a):
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=torch.float64)
+    return torch.as_tensor(np.asarray(a, dtype=np.float64), device="cuda")
+
+
+# ---------------------------------------------------------------------------
+# layers
+# ---------------------------------------------------------------------------
+
+class Conv3d:
+    """Submanifold 3-D conv (k = 1 or 3) + bias + activation with device weights.
+
+    ``w`` is the reference's (k^3 * Cin, Cout) matrix, row ((a*k + b)*k + c)*Cin
+    + ci (neural.py:163-166), held as float32 on the GPU; ``packed()`` is the
+    bf16 128B-swizzled image the tcgen05 kernel streams (built once).
+    """
+
+    def __init__(self, spec: ConvSpec, rng: np.random.Generator | None = None, init: str = "he",
+                 device: str = "cuda"):
+        torch = _torch()
+        self.spec = spec
+        k3c = spec.kernel ** 3 * spec.in_channels
+        gain = 2.0 if spec.activation == "relu" else 1.0
+        if rng is None:
+            w = np.zeros((k3c, spec.out_channels))
+        elif init == "kaiming_uniform":
+            bound = np.sqrt(3.0 * gain / k3c)
+            w = rng.uniform(-bound, bound, size=(k3c, spec.out_channels))
+        else:  # reference He-normal draw (neural.py:174-175); identity re-seeds below
+            w = rng.normal(0.0, np.sqrt(gain / k3c), size=(k3c, spec.out_channels))
+        self.w = torch.tensor(w, dtype=torch.float32, device=device)
+        self.b = torch.zeros(spec.out_channels, dtype=torch.float32, device=device)
+        self._packed = None
+
+    @property
+    def taps(self) -> int:
+        return self.spec.kernel ** 3
+
+    def seed_identity(self, rng: np.random.Generator, gain: float, noise: float = 0.02):
+        """Centre-tap identity plus small noise, drawn as neural.py:178-185."""
+        torch = _torch()
+        k3, cin, cout = self.taps, self.spec.in_channels, self.spec.out_channels
+        w = rng.normal(0.0, noise / np.sqrt(k3 * cin), size=(k3, cin, cout))
+        for j in range(min(cin, cout)):
+            w[k3 // 2, j, j] += gain
+        self.w = torch.tensor(w.reshape(k3 * cin, cout), dtype=torch.float32, device=self.w.device)
+        self._packed = None
+
+    def set_weights(self, w, b):
+        torch = _torch()
+        self.w = torch.as_tensor(np.asarray(w, dtype=np.float32) if not isinstance(w, torch.Tensor) else w,
+                                 dtype=torch.float32).to(self.w.device).contiguous()
+        self.b = torch.as_tensor(np.asarray(b, dtype=np.float32) if not isinstance(b, torch.Tensor) else b,
+                                 dtype=torch.float32).to(self.w.device).contiguous()
+        self._packed = None
+
+    def invalidate(self):
+        self._packed = None
+
+    def packed(self, stream=None):
+        if self._packed is None:
+            self._packed = pack_tc(self.w, self.taps, self.spec.in_channels, self.spec.out_channels, stream)
+        return self._packed
+
+
+def pack_tc(w, taps: int, cin: int, cout: int, stream=None):
+    torch = _torch()
+    nbytes = _lib.size("fpvs_pack_weights_tc_size", taps, cin, cout)
+    if nbytes == 0:
+        raise ValueError(f"no tensor-core packing for taps={taps}, Cin={cin}, Cout={cout}")
+    out = torch.empty(nbytes, dtype=torch.uint8, device=w.device)
+    _lib.call("fpvs_pack_weights_tc", _lib.ptr(w.contiguous()), taps, cin, cout, _lib.ptr(out),
+              _lib.stream_ptr(stream))
+    return out
+
+
+def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int, col_off: int = 0,
+             precision: str = "fp32", act: str | None = None, stream=None):
+    """One sparse conv launch: y[:, col_off:col_off+Cout] = act(gather-GEMM(x, table) + b)."""
+    torch = _torch()
+    spec = layer.spec
+    a = _lib.ACT[act or spec.activation]
+    s = _lib.stream_ptr(stream)
+    if precision == "bf16":
+        _lib.call("fpvs_spconv_tc", _lib.ptr(x), ldx, _lib.ptr(table), K, _lib.ptr(n), cap,
+                  _lib.ptr(layer.packed(stream)), _lib.ptr(layer.b), spec.in_channels, spec.out_channels, a,
+                  _lib.ptr(y), ldy, col_off, s)
+    else:
+        idt = _lib.BF16 if x.dtype == torch.bfloat16 else _lib.F32
+        odt = _lib.BF16 if y.dtype == torch.bfloat16 else _lib.F32
+        _lib.call("fpvs_spconv_simt", _lib.ptr(x), ldx, idt, _lib.ptr(table), K, _lib.ptr(n), cap,
+                  _lib.ptr(layer.w), _lib.ptr(layer.b), spec.in_channels, spec.out_channels, a, _lib.ptr(y), ldy,
+                  col_off, odt, s)
+
+
+def run_head(layer: Conv3d, x, ldx: int, lv: sp.Level, d: int, grid_dims, tau: float, out_bits=None,
+             probs=None, logits=None, precision: str = "fp32", stream=None):
+    """Fused 1x1x1 conv + sigmoid + [p >= tau] + deinterleave bit-pack (neural.py:513-526)."""
+    torch = _torch()
+    nx, ny, nz = grid_dims
+    s = _lib.stream_ptr(stream)
+    spec = layer.spec
+    if precision == "bf16":
+        _lib.call("fpvs_head_tc", _lib.ptr(x), ldx, _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap,
+                  _lib.ptr(layer.packed(stream)), _lib.ptr(layer.b), spec.in_channels, d, lv.B, nx, ny, nz,
+                  float(tau), _lib.ptr(out_bits), _lib.ptr(probs), _lib.ptr(logits), s)
+    else:
+        idt = _lib.BF16 if x.dtype == torch.bfloat16 else _lib.F32
+        _lib.call("fpvs_head_simt", _lib.ptr(x), ldx, idt, _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap,
+                  _lib.ptr(layer.w), _lib.ptr(layer.b), spec.in_channels, d, lv.B, nx, ny, nz, float(tau),
+                  _lib.ptr(out_bits), _lib.ptr(probs), _lib.ptr(logits), s)
+
+
+# ---------------------------------------------------------------------------
+# network
+# ---------------------------------------------------------------------------
+
+class PvsNet:
+    """Stack of submanifold convs mapping interleaved cells to probabilities (neural.py:260-346)."""
+
+    OUTPUT_GAIN = 3.0
+
+    def __init__(self, cfg: ModelConfig, rng: np.random.Generator | None = None, device: str = "cuda",
+                 precision: str = "fp32"):
+        _lib.require_cuda()
+        if precision not in ("fp32", "bf16"):
+            raise ValueError(f"unknown precision {precision!r}")
+        self.cfg = cfg
+        self.precision = precision
+        self.layers = [Conv3d(spec, rng, cfg.init, device) for spec in cfg.layers]
+        if cfg.init == "identity" and rng is not None:
+            for layer in self.layers[:-1]:
+                layer.seed_identity(rng, 1.0)
+            self.layers[-1].seed_identity(rng, self.OUTPUT_GAIN)
+            self.layers[-1].b.fill_(-self.OUTPUT_GAIN / 2.0)
+
+    # -- device path ---------------------------------------------------------
+    def forward_rows(self, feats, lv: sp.Level, grid_dims, tau: float = 0.5, out_bits=None, probs=None,
+                     logits=None, keep: bool = False, stream=None):
+        """Run the chain on active-cell rows; the head writes bits / probs / logits.
+
+        Returns the list of per-layer activations when ``keep`` (training).
+        """
+        torch = _torch()
+        d = self.cfg.d
+        bf16 = self.precision == "bf16"
+        dt = torch.bfloat16 if bf16 else torch.float32
+        x = feats
+        acts = [x]
+        for layer in self.layers[:-1]:
+            y = torch.empty((lv.cap, layer.spec.out_channels), dtype=dt, device=x.device)
+            table, K = (lv.nbr, 27) if layer.spec.kernel == 3 else (None, 1)
+            run_conv(layer, x, x.shape[1], table, K, lv.n, lv.cap, y, y.shape[1], 0, self.precision, stream=stream)
+            x = y
+            acts.append(x)
+        run_head(self.layers[-1], x, x.shape[1], lv, d, grid_dims, tau, out_bits, probs, logits,
+                 self.precision, stream)
+        return acts if keep else None
+
+    def predict_bits(self, bits, B: int, grid_dims, tau: float = 0.5, stream=None, level: sp.Level | None = None):
+        """Packed PVS bits of B packed grids, all on the device (no host sync)."""
+        torch = _torch()
+        d = self.cfg.d
+        lv = level or sp.level_from_bits(bits, B, grid_dims, d, stream=stream)
+        dt = torch.bfloat16 if self.precision == "bf16" else torch.float32
+        feats = sp.gather_features(bits, lv, grid_dims, d, dt, stream=stream)
+        nx, ny, nz = grid_dims
+        out = torch.zeros(B * nx * ny * nz // 8, dtype=torch.uint8, device=bits.device)
+        self.forward_rows(feats, lv, grid_dims, tau, out_bits=out, stream=stream)
+        return out
+
+    # -- reference-shaped dense API ------------------------------------------
+    def forward(self, x):
+        """(B, X, Y, Z, d^3) -> probabilities of the same shape; inactive cells -> 0."""
+        torch = _torch()
+        host = not isinstance(x, torch.Tensor)
+        xt = torch.as_tensor(np.asarray(x), dtype=torch.float32).cuda() if host else x.to("cuda", torch.float32)
+        if xt.dim() != 5 or xt.shape[4] != self.cfg.layers[0].in_channels:
+            raise ValueError(f"expected (B, D, H, W, {self.cfg.layers[0].in_channels}) input, got {tuple(xt.shape)}")
+        B, X, Y, Z, C = xt.shape
+        lv = sp.new_level(B, (X, Y, Z))
+        lv.active.copy_((xt != 0).any(-1).reshape(-1).to(torch.uint8))
+        sp.compact(lv)
+        sp.build_subm(lv)
+        n = lv.count()
+        rows = xt.reshape(-1, C)[lv.coords[:n, 0].long() * (X * Y * Z) + (lv.coords[:n, 1].long() * Y
+                                 + lv.coords[:n, 2].long()) * Z + lv.coords[:n, 3].long()]
+        feats = torch.zeros((lv.cap, C), dtype=torch.bfloat16 if self.precision == "bf16" else torch.float32,
+                            device="cuda")
+        feats[:n] = rows.to(feats.dtype)
+        d3 = self.cfg.layers[-1].out_channels
+        probs = torch.zeros((lv.cap, d3), dtype=torch.float32, device="cuda")
+        grid_dims = (X * self.cfg.d, Y * self.cfg.d, Z * self.cfg.d)
+        self.forward_rows(feats, lv, grid_dims, 0.5, probs=probs)
+        out = torch.zeros((B * X * Y * Z, d3), dtype=torch.float32, device="cuda")
+        lin = ((lv.coords[:n, 0].long() * X + lv.coords[:n, 1].long()) * Y + lv.coords[:n, 2].long()) * Z \
+            + lv.coords[:n, 3].long()
+        out[lin] = probs[:n]
+        out = out.reshape(B, X, Y, Z, d3)
+        return out.cpu().numpy().astype(np.float64) if host else out
+
+    def parameters(self):
+        out = []
+        for layer in self.layers:
+            out += [layer.w, layer.b]
+        return out
+
+    def invalidate(self):
+        for layer in self.layers:
+            layer.invalidate()
+
+    # -- checkpoint format (neural.py:299-346) -------------------------------
+    def save(self, path):
+        lines = [f"d={self.cfg.d}"]
+        for spec in self.cfg.layers:
+            lines.append(f"layer={spec.kernel}:{spec.in_channels}:{spec.out_channels}:{spec.activation}")
+        text = "\n".join(lines).encode()
+        with open(path, "wb") as fh:
+            fh.write(FPVW_MAGIC + struct.pack("<II", FPVW_VERSION, len(text)))
+            fh.write(text)
+            for layer in self.layers:
+                fh.write(layer.w.detach().cpu().numpy().astype("<f4").tobytes())
+                fh.write(layer.b.detach().cpu().numpy().astype("<f4").tobytes())
+
+    @classmethod
+    def load(cls, path, precision: str = "fp32") -> "PvsNet":
+        d, specs, arrays = read_fpvw(path)
+        net = cls(ModelConfig(d, specs), precision=precision)
+        for layer, (w, b) in zip(net.layers, arrays):
+            layer.set_weights(w, b)
+        return net
+
+
+def read_fpvw(path):
+    """Parse an FPVW checkpoint: (d, [ConvSpec], [(w (k^3 Cin, Cout) f32, b f32)]) (neural.py:316-346)."""
+    raw = Path(path).read_bytes()
+    if raw[:4] != FPVW_MAGIC:
+        raise ValueError(f"{path}: not an FPVW checkpoint")
+    version, textlen = struct.unpack_from("<II", raw, 4)
+    if version != FPVW_VERSION:
+        raise ValueError(f"{path}: unsupported FPVW version {version}")
+    text = raw[12:12 + textlen].decode()
+    d, specs = None, []
+    for line in text.splitlines():
+        key, val = line.split("=", 1)
+        if key == "d":
+            d = int(val)
+        elif key == "layer":
+            k, cin, cout, act = val.split(":")
+            specs.append(ConvSpec(int(k), int(cin), int(cout), act))
+    off = 12 + textlen
+    arrays = []
+    for s in specs:
+        nw = s.kernel ** 3 * s.in_channels * s.out_channels
+        w = np.frombuffer(raw, "<f4", nw, off).reshape(s.kernel ** 3 * s.in_channels, s.out_channels).copy()
+        off += 4 * nw
+        b = np.frombuffer(raw, "<f4", s.out_channels, off).copy()
+        off += 4 * s.out_channels
+        arrays.append((w, b))
+    return d, specs, arrays
+
+
+# ---------------------------------------------------------------------------
+# losses (neural.py:353-399), evaluated on the GPU
+# ---------------------------------------------------------------------------
+
+def dice_loss(pred, gt, alpha: float):
+    """Weighted Dice 1 - 2TP/(2TP + alpha FP + (1-alpha) FN); returns (value, grad)."""
+    p, g = _as_cuda64(pred), _as_cuda64(gt)
+    if p.shape != g.shape:
+        raise ValueError("prediction and ground truth shapes differ")
+    tp = (p * g).sum()
+    fp = p.sum() - tp
+    fn = g.sum() - tp
+    num = 2.0 * tp
+    den = 2.0 * tp + alpha * fp + (1.0 - alpha) * fn
+    if float(den) == 0.0:
+        return 0.0, _like(pred, np.zeros(tuple(p.shape)))
+    dden = 2.0 * g + alpha * (1.0 - g) - (1.0 - alpha) * g
+    grad = -(2.0 * g * den - num * dden) / (den * den)
+    return float((den - num) / den), _like(pred, grad)
+
+
+def rvl_loss(pred, gt):
+    """Repulsive visibility loss (1 - TP/GTP) + FP/GTP; returns (value, grad)."""
+    p, g = _as_cuda64(pred), _as_cuda64(gt)
+    if p.shape != g.shape:
+        raise ValueError("prediction and ground truth shapes differ")
+    gtp = float(g.sum())
+    if gtp == 0.0:
+        return 0.0, _like(pred, np.zeros(tuple(p.shape)))
+    tp = float((p * g).sum())
+    fp = float(p.sum()) - tp
+    return (1.0 - tp / gtp) + fp / gtp, _like(pred, (1.0 - 2.0 * g) / gtp)
+
+
+def combined_loss(pred, gt, cfg: TrainConfig):
+    dv, dg = dice_loss(pred, gt, cfg.alpha)
+    rv, rg = rvl_loss(pred, gt)
+    return cfg.lam * dv + (1.0 - cfg.lam) * rv, cfg.lam * dg + (1.0 - cfg.lam) * rg
+
+
+def _like(ref, val):
+    torch = _torch()
+    if isinstance(ref, torch.Tensor):
+        return val if isinstance(val, torch.Tensor) else torch.as_tensor(val)
+    return val.cpu().numpy() if isinstance(val, torch.Tensor) else np.asarray(val)
+
+
+# ---------------------------------------------------------------------------
+# inference entry (neural.py:513-526)
+# ---------------------------------------------------------------------------
+
+def predict_pvs(grid: FroxelGrid, net, tau: float = 0.5) -> FroxelGrid:
+    """Interleave, run the network, deinterleave with threshold tau — one device pass."""
+    torch = _torch()
+    if isinstance(net, (str, Path)):
+        net = PvsNet.load(net)
+    d = net.cfg.d
+    if any(dim % d for dim in grid.dims):
+        raise ValueError(f"grid dims {grid.dims} not divisible by interleave factor {d}")
+    if net.cfg.layers[0].in_channels != d ** 3:
+        raise ValueError("grid/channel mismatch against the checkpoint")
+    bits = torch.from_numpy(grid.bits).cuda()
+    out = net.predict_bits(bits, 1, grid.dims, tau)
+    res = FroxelGrid(grid.dims, role="predicted_pvs", bits=out.cpu().numpy())
+    res.supersample = grid.supersample
+    return res

@@ -1,0 +1,170 @@
+"""Sparse active-cell sets and kernel maps on the device (row KM).
+
+A ``Level`` is one resolution of a batch of interleaved grids: the active
+cells of a (B, X, Y, Z) cell grid in canonical C-order, the direct-mapped
+index volume (row of each cell or -1), the submanifold neighbour table, and —
+between levels — the k2s2 down / up tables.  Counts live on the device
+(``n``, int32[1]) and every buffer is sized by a host capacity, so building a
+frame's maps issues only kernels: no host round trip, CUDA-graph capturable.
+
+The canonical form is the one the oracle pins (oracle/sparse.py): rows in
+np.nonzero order, nbr[i][j] for o_j = (a-1, b-1, c-1), j = 9a + 3b + c
+(the tap order of pkg/src/froxelpvs/neural.py:187-199).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import _lib
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class Level:
+    B: int
+    dims: tuple               # (X, Y, Z) cells
+    cap: int
+    coords: object = None      # int32 [cap, 4] (b, x, y, z)
+    index_vol: object = None   # int32 [B*X*Y*Z]
+    n: object = None           # int32 [1] on device
+    nbr: object = None         # int32 [cap, 27]
+    active: object = None      # u8 [B*X*Y*Z]
+    hash_keys: object = None
+    hash_vals: object = None
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def ncells(self) -> int:
+        X, Y, Z = self.dims
+        return self.B * X * Y * Z
+
+    def count(self) -> int:
+        """Active row count (host sync — for tests and reporting only)."""
+        return min(int(self.n.item()), self.cap)
+
+
+def new_level(B: int, dims, cap: int | None = None, device="cuda") -> Level:
+    torch = _torch()
+    X, Y, Z = dims
+    ncell = B * X * Y * Z
+    cap = ncell if cap is None else min(cap, ncell)
+    lv = Level(B, (X, Y, Z), cap)
+    lv.coords = torch.empty((cap, 4), dtype=torch.int32, device=device)
+    lv.index_vol = torch.empty(ncell, dtype=torch.int32, device=device)
+    lv.n = torch.zeros(1, dtype=torch.int32, device=device)
+    lv.nbr = torch.empty((cap, 27), dtype=torch.int32, device=device)
+    lv.active = torch.empty(ncell, dtype=torch.uint8, device=device)
+    lv.extra["ws"] = torch.empty(_lib.size("fpvs_kmap_workspace_size", B, X, Y, Z), dtype=torch.uint8,
+                                 device=device)
+    return lv
+
+
+def compact(lv: Level, stream=None):
+    s = _lib.stream_ptr(stream)
+    X, Y, Z = lv.dims
+    ws = lv.extra["ws"]
+    _lib.call("fpvs_kmap_compact", _lib.ptr(lv.active), lv.B, X, Y, Z, _lib.ptr(lv.coords), _lib.ptr(lv.index_vol),
+              _lib.ptr(lv.n), lv.cap, _lib.ptr(ws), ws.numel(), s)
+
+
+def build_subm(lv: Level, stream=None):
+    X, Y, Z = lv.dims
+    _lib.call("fpvs_kmap_subm", _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap, _lib.ptr(lv.index_vol), lv.B, X, Y, Z,
+              _lib.ptr(lv.nbr), _lib.stream_ptr(stream))
+
+
+def build_subm_hash(lv: Level, hash_capacity: int | None = None, stream=None):
+    """Same table through the open-addressing hash instead of the index volume."""
+    torch = _torch()
+    X, Y, Z = lv.dims
+    if hash_capacity is None:
+        hash_capacity = 1 << max(4, (2 * lv.cap - 1).bit_length())
+    keys = torch.empty(hash_capacity, dtype=torch.int64, device=lv.coords.device)
+    vals = torch.empty(hash_capacity, dtype=torch.int32, device=lv.coords.device)
+    s = _lib.stream_ptr(stream)
+    _lib.call("fpvs_hash_build", _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap, lv.B, X, Y, Z, _lib.ptr(keys),
+              _lib.ptr(vals), hash_capacity, s)
+    nbr = torch.empty((lv.cap, 27), dtype=torch.int32, device=lv.coords.device)
+    _lib.call("fpvs_kmap_subm_hash", _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap, _lib.ptr(keys), _lib.ptr(vals),
+              hash_capacity, lv.B, X, Y, Z, _lib.ptr(nbr), s)
+    lv.hash_keys, lv.hash_vals = keys, vals
+    return nbr
+
+
+def fill_level_from_bits(lv: Level, bits, grid_dims, d: int, stream=None, with_nbr: bool = True) -> Level:
+    """Level 0 of a batch of packed grids: active cells = blocks with any bit set."""
+    nx, ny, nz = grid_dims
+    if nx % 8:
+        raise ValueError(f"N_x must be divisible by 8, got {nx}")
+    if d < 1 or nx % d or ny % d or nz % d:
+        raise ValueError(f"grid dims {tuple(grid_dims)} not divisible by interleave factor {d}")
+    if lv.dims != (nx // d, ny // d, nz // d):
+        raise ValueError("level dims do not match the grid")
+    _lib.call("fpvs_cell_active_from_bits", _lib.ptr(bits), lv.B, nx, ny, nz, d, _lib.ptr(lv.active),
+              _lib.stream_ptr(stream))
+    compact(lv, stream)
+    if with_nbr:
+        build_subm(lv, stream)
+    return lv
+
+
+def level_from_bits(bits, B: int, grid_dims, d: int, cap: int | None = None, stream=None,
+                    with_nbr: bool = True) -> Level:
+    nx, ny, nz = grid_dims
+    if d < 1 or nx % d or ny % d or nz % d:
+        raise ValueError(f"grid dims {tuple(grid_dims)} not divisible by interleave factor {d}")
+    lv = new_level(B, (nx // d, ny // d, nz // d), cap, device=bits.device)
+    return fill_level_from_bits(lv, bits, grid_dims, d, stream, with_nbr)
+
+
+def new_coarse(fine: Level, cap: int | None = None):
+    """Allocate the next level plus its (down, up) tables."""
+    torch = _torch()
+    X, Y, Z = fine.dims
+    if X % 2 or Y % 2 or Z % 2:
+        raise ValueError(f"k2s2 needs even cell dims, got {fine.dims}")
+    coarse = new_level(fine.B, (X // 2, Y // 2, Z // 2), cap, device=fine.coords.device)
+    down = torch.empty((coarse.cap, 8), dtype=torch.int32, device=fine.coords.device)
+    up = torch.empty((fine.cap, 8), dtype=torch.int32, device=fine.coords.device)
+    return coarse, down, up
+
+
+def fill_coarse(fine: Level, coarse: Level, down, up, stream=None, with_nbr: bool = True):
+    """Active set of a k2s2 down-conv (parents of active cells) and its maps."""
+    X, Y, Z = fine.dims
+    s = _lib.stream_ptr(stream)
+    coarse.active.zero_()
+    _lib.call("fpvs_kmap_coarsen", _lib.ptr(fine.coords), _lib.ptr(fine.n), fine.cap, fine.B, X, Y, Z,
+              _lib.ptr(coarse.active), s)
+    compact(coarse, stream)
+    if with_nbr:
+        build_subm(coarse, stream)
+    _lib.call("fpvs_kmap_down", _lib.ptr(coarse.coords), _lib.ptr(coarse.n), coarse.cap, _lib.ptr(fine.index_vol),
+              fine.B, X, Y, Z, _lib.ptr(down), s)
+    _lib.call("fpvs_kmap_up", _lib.ptr(fine.coords), _lib.ptr(fine.n), fine.cap, _lib.ptr(coarse.index_vol),
+              fine.B, X, Y, Z, _lib.ptr(up), s)
+
+
+def coarsen(fine: Level, cap: int | None = None, stream=None, with_nbr: bool = True):
+    coarse, down, up = new_coarse(fine, cap)
+    fill_coarse(fine, coarse, down, up, stream, with_nbr)
+    return coarse, down, up
+
+
+def gather_features(bits, lv: Level, grid_dims, d: int, dtype, ld: int | None = None, out=None, stream=None):
+    """Sparse interleave: (cap, ld) features of the active cells straight from packed bits."""
+    torch = _torch()
+    d3 = d ** 3
+    ld = ld or d3
+    if out is None:
+        out = torch.zeros((lv.cap, ld), dtype=dtype, device=bits.device)
+    nx, ny, nz = grid_dims
+    dt = _lib.BF16 if dtype == torch.bfloat16 else _lib.F32
+    _lib.call("fpvs_gather_cells_bits", _lib.ptr(bits), lv.B, nx, ny, nz, d, _lib.ptr(lv.coords), _lib.ptr(lv.n),
+              lv.cap, _lib.ptr(out), ld, dt, _lib.stream_ptr(stream))
+    return out

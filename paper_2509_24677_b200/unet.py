@@ -1,0 +1,185 @@
+"""Config-2 network: 3-level sparse U-Net over 256^3 froxel grids (row UNET).
+
+Not in the reference (its estimator is a dense 3-layer chain,
+pkg/src/froxelpvs/neural.py:95-99); BASELINE.json config 2 asks for it and
+SURVEY.md §8(a) row UNET pins the architecture, restated in the oracle
+(oracle/sparse.py ``unet_forward``):
+
+    L0 (d^3 = 64 ch): subm 64->64, subm 64->64                 = E0
+    down k2s2 64->128 -> L1: subm 128->128 x2                  = E1
+    down k2s2 128->256 -> L2: subm 256->256 x2
+    up k2s2^T 256->128 onto L1 = U1; [E1, U1] -> subm 256->128, 128->128
+    up k2s2^T 128->64 onto L0 = U0;  [E0, U0] -> subm 128->64, 64->64
+    head 1^3 64->64 + sigmoid + [p >= tau] + deinterleave bit-pack
+
+ReLU after every conv except the head.  Skip concatenation costs nothing:
+the encoder output and the up-conv output are written by their producing
+kernels into the two column halves of one [rows, 2C] buffer.
+
+A ``UNetPlan`` owns every device buffer for a (B, grid) shape, sized by the
+cell-count capacities, so ``run`` is pure kernel launches — no host sync, no
+allocation — and can be captured into a CUDA graph.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from . import sparse as sp
+from .neural import pack_tc, run_conv, run_head
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def layer_table(widths=(64, 128, 256), d3: int = 64):
+    c0, c1, c2 = widths
+    return (("enc0a", "subm", d3, c0), ("enc0b", "subm", c0, c0), ("down01", "down", c0, c1),
+            ("enc1a", "subm", c1, c1), ("enc1b", "subm", c1, c1), ("down12", "down", c1, c2),
+            ("enc2a", "subm", c2, c2), ("enc2b", "subm", c2, c2), ("up21", "up", c2, c1),
+            ("dec1a", "subm", 2 * c1, c1), ("dec1b", "subm", c1, c1), ("up10", "up", c1, c0),
+            ("dec0a", "subm", 2 * c0, c0), ("dec0b", "subm", c0, c0), ("head", "head", c0, d3))
+
+
+TAPS = {"subm": 27, "down": 8, "up": 8, "head": 1}
+
+
+class _Spec:
+    def __init__(self, cin, cout, act):
+        self.in_channels, self.out_channels, self.activation = cin, cout, act
+
+
+class SparseLayer:
+    """Weights of one U-Net conv: w (taps*Cin, Cout) f32, row j*Cin + ci."""
+
+    def __init__(self, name, kind, cin, cout, w, b, device="cuda"):
+        torch = _torch()
+        self.name, self.kind, self.taps = name, kind, TAPS[kind]
+        self.spec = _Spec(cin, cout, "sigmoid" if kind == "head" else "relu")
+        self.w = torch.as_tensor(np.asarray(w, np.float32)).to(device).contiguous()
+        self.b = torch.as_tensor(np.asarray(b, np.float32)).to(device).contiguous()
+        self._packed = None
+        self._w_bf16r = None
+
+    def packed(self, stream=None):
+        if self._packed is None:
+            self._packed = pack_tc(self.w, self.taps, self.spec.in_channels, self.spec.out_channels, stream)
+        return self._packed
+
+
+class PvsUNet:
+    """Sparse U-Net (BASELINE config 2) with Kaiming-uniform init from ``seed``."""
+
+    def __init__(self, seed: int = 1, widths=(64, 128, 256), d: int = 4, precision: str = "bf16",
+                 device: str = "cuda", params=None):
+        _lib.require_cuda()
+        if precision not in ("bf16", "fp32"):
+            raise ValueError(f"unknown precision {precision!r}")
+        self.d, self.widths, self.precision = d, tuple(widths), precision
+        table = layer_table(widths, d ** 3)
+        if params is None:
+            params = init_params(seed, widths, d ** 3)
+        self.layers = {name: SparseLayer(name, kind, cin, cout, *params[name], device=device)
+                       for name, kind, cin, cout in table}
+
+    def plan(self, B: int, grid_dims, device="cuda") -> "UNetPlan":
+        return UNetPlan(self, B, grid_dims, device)
+
+    def predict_bits(self, bits, B: int, grid_dims, tau: float = 0.5, plan=None, probs=None, logits=None):
+        plan = plan or self.plan(B, grid_dims, bits.device)
+        out = _torch().empty(B * int(np.prod(grid_dims)) // 8, dtype=_torch().uint8, device=bits.device)
+        plan.run(bits, out, tau, probs=probs, logits=logits)
+        return out, plan
+
+
+def init_params(seed: int, widths=(64, 128, 256), d3: int = 64):
+    """Kaiming-uniform U(+-sqrt(3 gain / fan_in)) per layer, Generator(PCG64(seed)), layer order."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = {}
+    for name, kind, cin, cout in layer_table(widths, d3):
+        fan_in = TAPS[kind] * cin
+        gain = 1.0 if kind == "head" else 2.0
+        bound = np.sqrt(3.0 * gain / fan_in)
+        out[name] = (rng.uniform(-bound, bound, size=(fan_in, cout)), np.zeros(cout))
+    return out
+
+
+class UNetPlan:
+    """All device buffers of one (B, grid) frame shape; ``run`` only launches kernels."""
+
+    def __init__(self, net: PvsUNet, B: int, grid_dims, device="cuda"):
+        torch = _torch()
+        self.net, self.B, self.grid_dims = net, B, tuple(grid_dims)
+        d = net.d
+        nx, ny, nz = grid_dims
+        if nx % 8 or nx % (4 * d) or ny % (4 * d) or nz % (4 * d):
+            raise ValueError(f"grid dims {tuple(grid_dims)} must be divisible by 4*d = {4 * d} (and N_x by 8)")
+        c0, c1, c2 = net.widths
+        self.L0 = sp.new_level(B, (nx // d, ny // d, nz // d), device=device)
+        self.L1, self.down01, self.up10 = sp.new_coarse(self.L0)
+        self.L2, self.down12, self.up21 = sp.new_coarse(self.L1)
+        dt = torch.bfloat16 if net.precision == "bf16" else torch.float32
+        e = lambda rows, cols: torch.empty((rows, cols), dtype=dt, device=device)  # noqa: E731
+        k0, k1, k2 = self.L0.cap, self.L1.cap, self.L2.cap
+        self.x0 = e(k0, d ** 3)
+        self.t0a, self.t0b, self.buf0 = e(k0, c0), e(k0, c0), e(k0, 2 * c0)
+        self.t1a, self.t1b, self.buf1 = e(k1, c1), e(k1, c1), e(k1, 2 * c1)
+        self.t2a, self.t2b = e(k2, c2), e(k2, c2)
+
+    def build_maps(self, bits):
+        sp.fill_level_from_bits(self.L0, bits, self.grid_dims, self.net.d)
+        sp.fill_coarse(self.L0, self.L1, self.down01, self.up10)
+        sp.fill_coarse(self.L1, self.L2, self.down12, self.up21)
+
+    def run(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, maps: bool = True):
+        """One frame: maps, sparse interleave, 14 convs, fused head into ``out_bits`` (zeroed here)."""
+        net, P = self.net, self.net.precision
+        L = net.layers
+        L0, L1, L2 = self.L0, self.L1, self.L2
+        c0, c1, c2 = net.widths
+        if maps:
+            self.build_maps(bits)
+        sp.gather_features(bits, L0, self.grid_dims, net.d, self.x0.dtype, out=self.x0)
+
+        def conv(name, x, ldx, table, K, lv, y, ldy, off=0):
+            run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu")
+
+        d3 = net.d ** 3
+        conv("enc0a", self.x0, d3, L0.nbr, 27, L0, self.t0a, c0)
+        conv("enc0b", self.t0a, c0, L0.nbr, 27, L0, self.buf0, 2 * c0, 0)             # E0 -> buf0[:, :c0]
+        conv("down01", self.buf0, 2 * c0, self.down01, 8, L1, self.t1a, c1)
+        conv("enc1a", self.t1a, c1, L1.nbr, 27, L1, self.t1b, c1)
+        conv("enc1b", self.t1b, c1, L1.nbr, 27, L1, self.buf1, 2 * c1, 0)             # E1 -> buf1[:, :c1]
+        conv("down12", self.buf1, 2 * c1, self.down12, 8, L2, self.t2a, c2)
+        conv("enc2a", self.t2a, c2, L2.nbr, 27, L2, self.t2b, c2)
+        conv("enc2b", self.t2b, c2, L2.nbr, 27, L2, self.t2a, c2)
+        conv("up21", self.t2a, c2, self.up21, 8, L1, self.buf1, 2 * c1, c1)           # U1 -> buf1[:, c1:]
+        conv("dec1a", self.buf1, 2 * c1, L1.nbr, 27, L1, self.t1a, c1)
+        conv("dec1b", self.t1a, c1, L1.nbr, 27, L1, self.t1b, c1)
+        conv("up10", self.t1b, c1, self.up10, 8, L0, self.buf0, 2 * c0, c0)           # U0 -> buf0[:, c0:]
+        conv("dec0a", self.buf0, 2 * c0, L0.nbr, 27, L0, self.t0a, c0)
+        conv("dec0b", self.t0a, c0, L0.nbr, 27, L0, self.t0b, c0)
+        out_bits.zero_()
+        run_head(L["head"], self.t0b, c0, L0, net.d, self.grid_dims, tau, out_bits, probs, logits, P)
+
+    def counts(self):
+        return self.L0.count(), self.L1.count(), self.L2.count()
+
+    def useful_flops(self):
+        """Algorithmic FLOPs of one frame: 2 * pairs * Cin * Cout per conv (no zero-fill counted)."""
+        n0, n1, n2 = self.counts()
+        p0 = int((self.L0.nbr[:n0] >= 0).sum())
+        p1 = int((self.L1.nbr[:n1] >= 0).sum())
+        p2 = int((self.L2.nbr[:n2] >= 0).sum())
+        c0, c1, c2 = self.net.widths
+        d3 = self.net.d ** 3
+        f = 2 * p0 * (d3 * c0 + c0 * c0 + 2 * c0 * c0 + c0 * c0)
+        f += 2 * p1 * (c1 * c1 * 2 + 2 * c1 * c1 + c1 * c1)
+        f += 2 * p2 * (c2 * c2 * 2)
+        f += 2 * n0 * c0 * c1 + 2 * n1 * c1 * c2          # down convs: one pair per fine cell
+        f += 2 * n1 * c2 * c1 + 2 * n0 * c1 * c0          # up convs: one pair per fine cell
+        f += 2 * n0 * c0 * d3                              # head
+        return f

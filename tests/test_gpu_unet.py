@@ -1,0 +1,90 @@
+"""Config-2 sparse U-Net on the tcgen05 path vs the oracle's bf16 emulation."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import sparse as osp
+from paper_2509_24677_b200 import synth
+from paper_2509_24677_b200.froxel import FroxelGrid
+
+pytestmark = pytest.mark.gpu
+
+BF16_LOGIT_TOL = 2e-2
+BAND = 1e-3
+
+
+def _run(occ, seed=1, precision="bf16"):
+    import torch
+    from paper_2509_24677_b200.unet import PvsUNet
+    net = PvsUNet(seed=seed, precision=precision)
+    bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+    plan = net.plan(1, occ.shape)
+    out = torch.empty(occ.size // 8, dtype=torch.uint8, device="cuda")
+    logits = torch.zeros((plan.L0.cap, 64), device="cuda")
+    plan.run(bits, out, 0.5, logits=logits)
+    torch.cuda.synchronize()
+    return plan, out, logits
+
+
+def _check(occ, plan, out, logits, bf16=True):
+    cells = osp.interleave(occ.astype(np.float64), 4)[None]
+    params = osp.unet_init(1)
+    coords, z = osp.unet_forward(cells, params, bf16=bf16, return_logits=True)
+    n = plan.L0.count()
+    assert n == len(coords)
+    assert np.array_equal(plan.L0.coords[:n].cpu().numpy(), coords)
+    err = np.abs(logits[:n].cpu().numpy() - z).max()
+    prob = osp.sigmoid(z)
+    dense = osp.deinterleave(osp.scatter_cells(coords, prob, (1,) + plan.L0.dims)[0], 4)
+    got = FroxelGrid(occ.shape, bits=out.cpu().numpy()).to_dense()
+    diff = got != (dense >= 0.5)
+    hard = int((diff & (np.abs(dense - 0.5) >= BAND)).sum())
+    return err, hard, int(diff.sum()), int((dense >= 0.5).sum())
+
+
+def test_unet_small_grid():
+    occ = synth.box_grid((64, 64, 64), 60, 1, 8, 5)
+    plan, out, logits = _run(occ)
+    err, hard, soft, vis = _check(occ, plan, out, logits)
+    assert err <= BF16_LOGIT_TOL, err
+    assert hard == 0, (hard, soft)
+    assert vis > 0
+
+
+def test_unet_fp32_mode_small_grid():
+    occ = synth.box_grid((64, 64, 64), 60, 1, 8, 6)
+    plan, out, logits = _run(occ, precision="fp32")
+    err, hard, soft, _ = _check(occ, plan, out, logits, bf16=False)
+    assert err <= 1e-4, err
+    assert hard == 0, (hard, soft)
+
+
+def test_unet_empty_and_tiny_grids():
+    import torch
+    for occ in (np.zeros((64, 64, 64), bool), _single_froxel()):
+        plan, out, logits = _run(occ)
+        if not occ.any():
+            assert plan.L0.count() == 0 and not out.any()
+        else:
+            _, hard, _, _ = _check(occ, plan, out, logits)
+            assert hard == 0
+        del torch
+
+
+def _single_froxel():
+    o = np.zeros((64, 64, 64), bool)
+    o[63, 0, 17] = True
+    return o
+
+
+@pytest.mark.slow
+def test_unet_config2_full_size():
+    """BASELINE config 2 (256^3, 4000 boxes, seed 1) end to end."""
+    occ = synth.config2_grid(1)
+    plan, out, logits = _run(occ)
+    err, hard, soft, vis = _check(occ, plan, out, logits)
+    print(f"cfg2: logits max-abs {err:.3g}, mask diffs {soft} (outside band {hard}), visible {vis}")
+    assert err <= BF16_LOGIT_TOL, err
+    assert hard == 0, (hard, soft)
