@@ -62,7 +62,6 @@ def test_unet_fp32_mode_small_grid():
 
 
 def test_unet_empty_and_tiny_grids():
-    import torch
     for occ in (np.zeros((64, 64, 64), bool), _single_froxel()):
         plan, out, logits = _run(occ)
         if not occ.any():
@@ -70,7 +69,6 @@ def test_unet_empty_and_tiny_grids():
         else:
             _, hard, _, _ = _check(occ, plan, out, logits)
             assert hard == 0
-        del torch
 
 
 def _single_froxel():
