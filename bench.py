@@ -1,0 +1,346 @@
+"""NeuralPVS hot-path benchmark (BASELINE.json metric: froxel grids/s and
+ms/frame at 256^3, bs1, per GPU count; % of tensor-pipe peak).
+
+Workload (BASELINE config 2): one 256^3 froxel grid per step per GPU (4000
+seeded boxes, edges 1-12, seed 1), interleave d=4 -> 64^3 cells x 64 ch,
+3-level sparse U-Net (64/128/256 ch), bf16 activations/weights with fp32
+accumulation, fused sigmoid + threshold + deinterleave bit-pack.  A step is
+one whole frame: kernel maps (3 levels), sparse interleave, 14 convs, head.
+
+* ``value``: frames with the packed input already in HBM, each step replayed
+  from one CUDA graph; L2 is flushed (256 MiB memset, untimed) before every
+  step; device time from CUDA events on the launching stream, max over ranks.
+* ``e2e``: the same frames through ``FramePipeline.infer`` — pinned host
+  packed grid -> H2D -> frame -> D2H packed PVS — every copy inside the
+  timed region.
+* ``roofline``: the dominant kernel (the tcgen05 gather-GEMM, spconv_tc)
+  from an event-instrumented eager frame: algorithmic FLOPs (2*pairs*Cin*Cout,
+  zero-fill not counted) / its summed launch time vs the measured bf16 peak.
+* ``cpu_baseline``: the numpy sparse restatement (oracle/, fp64) of the same
+  frame on this host's cores (rank 0, N=1).
+
+Multi-GPU: one process per GPU (torchrun); frames are independent ("replicas
+only" per frame): each rank runs its own frames, no
+collective on the data path; value = total frames / max-rank time.
+
+``--impl reference`` times the CPU reference path (the oracle port) instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "froxel grids/sec and ms/frame (256^3, bs1); % tensor-pipe peak"
+UNIT = "grids/s"
+WORKLOAD = "config2: 256^3 froxels, 4000 boxes (edges 1-12, seed 1), d=4, 3-level sparse U-Net 64/128/256, bf16"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_frame_time(occ, seed=1):
+    """One config-2 frame through the numpy sparse restatement (oracle, float64)."""
+    from oracle import sparse as osp
+    params = osp.unet_init(seed)
+    t0 = time.perf_counter()
+    cells = osp.interleave(occ.astype(np.float64), 4)[None]
+    coords, prob = osp.unet_forward(cells, params, bf16=False)
+    dense = osp.deinterleave(osp.scatter_cells(coords, prob, (1,) + cells.shape[1:4])[0], 4)
+    np.packbits((dense >= 0.5).transpose(2, 1, 0), axis=2, bitorder="little")
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2509_24677_b200 import synth
+    occ = synth.config2_grid(1)
+    cores = os.cpu_count()
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
+        cpu_frame_time(occ)
+    times = [cpu_frame_time(occ) for _ in range(args.steps)]
+    total = sum(times)
+    value = args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": warm, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded boxes; paper scenes unavailable)",
+        "config": {"workload": WORKLOAD, "parallelism": "cpu, rank 0 only", "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": "one full config-2 frame per step: numpy sparse restatement of the reference "
+                                   "arithmetic (oracle/sparse.py, float64, OpenBLAS on all host threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# number of our kernels each C-ABI entry point launches
+KERNELS_PER_CALL = {"fpvs_kmap_compact": 3, "fpvs_hash_build": 1}
+
+
+def count_launches(fn):
+    """Run fn once while counting libfpvs kernel launches (via the C-ABI calls)."""
+    from paper_2509_24677_b200 import _lib
+    orig = _lib.call
+    n = [0]
+
+    def counting(name, *a):
+        n[0] += KERNELS_PER_CALL.get(name, 1)
+        return orig(name, *a)
+    _lib.call = counting
+    try:
+        fn()
+    finally:
+        _lib.call = orig
+    return n[0]
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2509_24677_b200 import synth
+    from paper_2509_24677_b200.froxel import FroxelGrid
+    from paper_2509_24677_b200.pipeline import FramePipeline, stage_times
+    from paper_2509_24677_b200.unet import PvsUNet
+
+    dims = (256, 256, 256)
+    occ = synth.config2_grid(1)
+    host_bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).pin_memory()
+    nbytes = host_bits.numel()
+    net = PvsUNet(seed=1, precision="bf16")
+    pipe = FramePipeline(net, 1, dims, tau=0.5, graph=True)
+    pipe.load(host_bits.cuda())
+    pipe.capture()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    # ---- instrumented eager frame: per-stage events, FLOPs, launch count
+    events = []
+    pipe.plan.run(pipe.in_bits, pipe.out_bits, 0.5, events=events)
+    torch.cuda.synchronize()
+    stages = stage_times(events)
+    layer_flops = pipe.plan.layer_flops()
+    n0, n1, n2 = pipe.plan.counts()
+    launches_per_frame = count_launches(lambda: pipe.plan.run(pipe.in_bits, pipe.out_bits, 0.5))
+    torch.cuda.synchronize()
+    # repeat instrumented frames for stable per-kernel averages
+    conv_ms = {k: [] for k in layer_flops}
+    stage_acc = {}
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        ev = []
+        pipe.plan.run(pipe.in_bits, pipe.out_bits, 0.5, events=ev)
+        torch.cuda.synchronize()
+        for name, ms in stage_times(ev):
+            stage_acc.setdefault(name, []).append(ms)
+            if name in conv_ms:
+                conv_ms[name].append(ms)
+
+    # ---- warm-up graph replays
+    for _ in range(args.warmup):
+        flush.zero_()
+        pipe.run_device()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    # ---- timed: device-resident input, graph replay per step
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        starts[i].record(stream)
+        pipe.run_device()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+
+    # ---- timed e2e: pinned host in -> device -> pinned host out, every step
+    host_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    e_starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for _ in range(2):
+        pipe.infer(host_bits, host_out)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()
+        e_starts[i].record(stream)
+        pipe.infer(host_bits, host_out)
+        e_ends[i].record(stream)
+    torch.cuda.synchronize()
+    wall_e2e = time.perf_counter() - wall0
+    if ws > 1:
+        dist.barrier()
+    e2e_ms = sum(s.elapsed_time(e) for s, e in zip(e_starts, e_ends))
+    time.sleep(0.2)
+    clocks = sampler.stop()
+
+    # correctness guard: the timed output equals the eager output
+    check = pipe.out_bits.clone()
+    pipe.plan.run(pipe.in_bits, pipe.out_bits, 0.5)
+    torch.cuda.synchronize()
+    if not torch.equal(check, pipe.out_bits) or not torch.equal(host_out.cuda(), check):
+        raise RuntimeError("graph replay / e2e output differs from the eager frame")
+
+    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_ms = float(t[0]), float(t[1])
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return 0
+
+    hbm_peak, tf_peak, peak_kind = peaks()
+    tc_ms = sum(statistics.median(v) for v in conv_ms.values())
+    tc_flops = sum(layer_flops.values())
+    achieved = tc_flops / (tc_ms * 1e-3) / 1e12
+    n_tc_launches = len(conv_ms)
+    per_layer = {k: {"ms": round(statistics.median(conv_ms[k]), 5),
+                     "tflops": round(layer_flops[k] / (statistics.median(conv_ms[k]) * 1e-3) / 1e12, 2)}
+                 for k in conv_ms}
+    stage_ms = {k: round(statistics.median(v), 5) for k, v in stage_acc.items()}
+
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        t_cpu = cpu_frame_time(occ)
+        cpu = {"value": 1.0 / t_cpu, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": "one config-2 frame (interleave, maps, U-Net, threshold) through the numpy sparse "
+                         "restatement oracle/sparse.py in float64 on all host threads (OpenBLAS)"}
+
+    value = ws * args.steps / (dev_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded boxes; paper scenes unavailable)",
+        "config": {"workload": WORKLOAD, "global_batch": ws, "grid": list(dims), "parallelism": f"replicas x{ws}",
+                   "l2": "flushed before every step (256 MiB memset, untimed)",
+                   "active_cells": [n0, n1, n2], "density": float(occ.mean()), "cuda_graph": True},
+        "e2e": {"value": ws * args.steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes,
+                "d2h_bytes_per_step": nbytes, "ms_per_step": e2e_ms / args.steps,
+                "wall_ms_per_step": 1e3 * wall_e2e / args.steps},
+        "roofline": {"bound": "tensor", "kernel": "spconv_tc (tcgen05 gather-GEMM, 14 convs + head / frame)",
+                     "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s", "frac": achieved / tf_peak,
+                     "peak_kind": f"{peak_kind} bf16 burst", "traffic": None,
+                     "flops_per_frame": tc_flops, "launches_per_frame": n_tc_launches,
+                     "kernel_ms_per_frame": tc_ms, "per_layer": per_layer},
+        "stages_ms": stage_ms,
+        "gpu_launches": launches_per_frame * args.steps,
+        "clocks": clocks,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,145 @@
+"""Frame pipelines: preallocated plans replayed as CUDA graphs.
+
+``predict_pvs`` (pkg/src/froxelpvs/neural.py:513-526) is interleave ->
+forward -> deinterleave(tau) per grid.  On the device that is ~35 kernel
+launches per frame (maps, sparse interleave, convs, fused head), each a few
+microseconds, so the host would dominate if it launched them one by one.  A
+``FramePipeline`` allocates every buffer once for a (B, grid) shape, runs the
+frame eagerly once (warm-up: lazily packed weights, kernel attributes), then
+captures it into one CUDA graph.  ``run_device`` replays the graph on
+device-resident packed bits; ``infer`` adds the pinned host <-> device copies
+of the packed input and output grids (Nx*Ny*Nz/8 bytes each way).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import sparse as sp
+from .neural import PvsNet, run_conv, run_head
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class ChainPlan:
+    """Buffers for a linear PvsNet (configs 1, 3, 4, 5) over B packed grids."""
+
+    def __init__(self, net: PvsNet, B: int, grid_dims, device="cuda", cap: int | None = None):
+        torch = _torch()
+        self.net, self.B, self.grid_dims = net, B, tuple(grid_dims)
+        d = net.cfg.d
+        nx, ny, nz = grid_dims
+        if nx % 8 or nx % d or ny % d or nz % d:
+            raise ValueError(f"grid dims {tuple(grid_dims)} not divisible by interleave factor {d} (N_x by 8)")
+        self.L0 = sp.new_level(B, (nx // d, ny // d, nz // d), cap, device=device)
+        dt = torch.bfloat16 if net.precision == "bf16" else torch.float32
+        widest = max(s.out_channels for s in net.cfg.layers[:-1]) if len(net.cfg.layers) > 1 else 1
+        k = self.L0.cap
+        self.x0 = torch.empty((k, d ** 3), dtype=dt, device=device)
+        self.ping = torch.empty((k, widest), dtype=dt, device=device)
+        self.pong = torch.empty((k, widest), dtype=dt, device=device)
+
+    def run(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, events=None):
+        net, lv = self.net, self.L0
+        d = net.cfg.d
+        _ev(events, "maps")
+        sp.fill_level_from_bits(lv, bits, self.grid_dims, d)
+        sp.gather_features(bits, lv, self.grid_dims, d, self.x0.dtype, out=self.x0)
+        x, ldx = self.x0, d ** 3
+        bufs = (self.ping, self.pong)
+        for i, layer in enumerate(net.layers[:-1]):
+            _ev(events, f"conv{i}")
+            y = bufs[i % 2]
+            table, K = (lv.nbr, 27) if layer.spec.kernel == 3 else (None, 1)
+            run_conv(layer, x, ldx, table, K, lv.n, lv.cap, y, y.shape[1], 0, net.precision)
+            x, ldx = y, y.shape[1]
+        _ev(events, "head")
+        out_bits.zero_()
+        run_head(net.layers[-1], x, ldx, lv, d, self.grid_dims, tau, out_bits, probs, logits, net.precision)
+        _ev(events, "end")
+
+    def counts(self):
+        return (self.L0.count(),)
+
+    def useful_flops(self):
+        n = self.L0.count()
+        p = int((self.L0.nbr[:n] >= 0).sum())
+        f = 0
+        for layer in self.net.layers:
+            s = layer.spec
+            f += 2 * (p if s.kernel == 3 else n) * s.in_channels * s.out_channels
+        return f
+
+
+def _ev(events, name):
+    """Record a CUDA event named ``name`` on the current stream (stage timing)."""
+    if events is None:
+        return
+    torch = _torch()
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    events.append((name, e))
+
+
+def stage_times(events):
+    """[(stage, ms)] between consecutive recorded events."""
+    return [(a[0], a[1].elapsed_time(b[1])) for a, b in zip(events, events[1:])]
+
+
+class FramePipeline:
+    """CUDA-graph replay of one frame for a fixed (B, grid) shape.
+
+    ``net`` is a PvsUNet (config 2) or a PvsNet (configs 1/3/4).  The input
+    is ``self.in_bits`` (packed grids, device), the output ``self.out_bits``.
+    """
+
+    def __init__(self, net, B: int, grid_dims, tau: float = 0.5, graph: bool = True, device="cuda"):
+        torch = _torch()
+        self.net, self.B, self.grid_dims, self.tau = net, B, tuple(grid_dims), float(tau)
+        nbytes = B * int(np.prod(grid_dims)) // 8
+        self.plan = net.plan(B, grid_dims, device) if hasattr(net, "plan") else ChainPlan(net, B, grid_dims, device)
+        self.in_bits = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        self.out_bits = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        self.graph = None
+        self._use_graph = graph
+
+    def load(self, bits):
+        self.in_bits.copy_(bits, non_blocking=True)
+
+    def capture(self):
+        """Warm up eagerly once, then capture the frame into a CUDA graph."""
+        torch = _torch()
+        self.plan.run(self.in_bits, self.out_bits, self.tau)
+        torch.cuda.synchronize()
+        if not self._use_graph:
+            return
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self.plan.run(self.in_bits, self.out_bits, self.tau)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = g
+
+    def run_device(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.plan.run(self.in_bits, self.out_bits, self.tau)
+        return self.out_bits
+
+    def infer(self, host_bits, host_out=None):
+        """Host packed grids in, host packed PVS out (pinned buffers avoid staging)."""
+        torch = _torch()
+        src = torch.as_tensor(host_bits)
+        self.in_bits.copy_(src, non_blocking=True)
+        self.run_device()
+        if host_out is None:
+            host_out = torch.empty(self.out_bits.numel(), dtype=torch.uint8, pin_memory=True)
+        host_out.copy_(self.out_bits, non_blocking=True)
+        return host_out

@@ -134,17 +134,24 @@ class UNetPlan:
         sp.fill_coarse(self.L0, self.L1, self.down01, self.up10)
         sp.fill_coarse(self.L1, self.L2, self.down12, self.up21)
 
-    def run(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, maps: bool = True):
-        """One frame: maps, sparse interleave, 14 convs, fused head into ``out_bits`` (zeroed here)."""
+    def run(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, maps: bool = True, events=None):
+        """One frame: maps, sparse interleave, 14 convs, fused head into ``out_bits`` (zeroed here).
+
+        ``events`` (a list) receives (stage, cuda.Event) marks for per-stage timing.
+        """
+        from .pipeline import _ev
         net, P = self.net, self.net.precision
         L = net.layers
         L0, L1, L2 = self.L0, self.L1, self.L2
         c0, c1, c2 = net.widths
         if maps:
+            _ev(events, "maps")
             self.build_maps(bits)
+        _ev(events, "gather")
         sp.gather_features(bits, L0, self.grid_dims, net.d, self.x0.dtype, out=self.x0)
 
         def conv(name, x, ldx, table, K, lv, y, ldy, off=0):
+            _ev(events, name)
             run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu")
 
         d3 = net.d ** 3
@@ -162,24 +169,27 @@ class UNetPlan:
         conv("up10", self.t1b, c1, self.up10, 8, L0, self.buf0, 2 * c0, c0)           # U0 -> buf0[:, c0:]
         conv("dec0a", self.buf0, 2 * c0, L0.nbr, 27, L0, self.t0a, c0)
         conv("dec0b", self.t0a, c0, L0.nbr, 27, L0, self.t0b, c0)
+        _ev(events, "head")
         out_bits.zero_()
         run_head(L["head"], self.t0b, c0, L0, net.d, self.grid_dims, tau, out_bits, probs, logits, P)
+        _ev(events, "end")
 
-    def counts(self):
-        return self.L0.count(), self.L1.count(), self.L2.count()
-
-    def useful_flops(self):
-        """Algorithmic FLOPs of one frame: 2 * pairs * Cin * Cout per conv (no zero-fill counted)."""
+    def layer_flops(self):
+        """Algorithmic FLOPs per conv of the last frame (2 * pairs * Cin * Cout; no zero-fill)."""
         n0, n1, n2 = self.counts()
         p0 = int((self.L0.nbr[:n0] >= 0).sum())
         p1 = int((self.L1.nbr[:n1] >= 0).sum())
         p2 = int((self.L2.nbr[:n2] >= 0).sum())
         c0, c1, c2 = self.net.widths
         d3 = self.net.d ** 3
-        f = 2 * p0 * (d3 * c0 + c0 * c0 + 2 * c0 * c0 + c0 * c0)
-        f += 2 * p1 * (c1 * c1 * 2 + 2 * c1 * c1 + c1 * c1)
-        f += 2 * p2 * (c2 * c2 * 2)
-        f += 2 * n0 * c0 * c1 + 2 * n1 * c1 * c2          # down convs: one pair per fine cell
-        f += 2 * n1 * c2 * c1 + 2 * n0 * c1 * c0          # up convs: one pair per fine cell
-        f += 2 * n0 * c0 * d3                              # head
-        return f
+        return {"enc0a": 2 * p0 * d3 * c0, "enc0b": 2 * p0 * c0 * c0, "down01": 2 * n0 * c0 * c1,
+                "enc1a": 2 * p1 * c1 * c1, "enc1b": 2 * p1 * c1 * c1, "down12": 2 * n1 * c1 * c2,
+                "enc2a": 2 * p2 * c2 * c2, "enc2b": 2 * p2 * c2 * c2, "up21": 2 * n1 * c2 * c1,
+                "dec1a": 2 * p1 * 2 * c1 * c1, "dec1b": 2 * p1 * c1 * c1, "up10": 2 * n0 * c1 * c0,
+                "dec0a": 2 * p0 * 2 * c0 * c0, "dec0b": 2 * p0 * c0 * c0, "head": 2 * n0 * c0 * d3}
+
+    def counts(self):
+        return self.L0.count(), self.L1.count(), self.L2.count()
+
+    def useful_flops(self):
+        return sum(self.layer_flops().values())
