@@ -153,7 +153,7 @@ def run_reference(args):
 
 
 # number of our kernels each C-ABI entry point launches
-KERNELS_PER_CALL = {"fpvs_kmap_compact": 3, "fpvs_hash_build": 1}
+KERNELS_PER_CALL = {"fpvs_kmap_compact": 1, "fpvs_hash_build": 1}
 
 
 def count_launches(fn):

@@ -132,14 +132,20 @@ int fpvs_spconv_simt(const void* x, int ldx, int in_dtype, const int32_t* nbr, i
                      int cin, int cout, int act, void* y, int ldy, int col_off, int out_dtype,
                      void* stream);
 
-/* Bytes of the packed tensor-core weight image for (K, Cin, Cout). */
-size_t fpvs_pack_weights_tc_size(int K, int cin, int cout);
-/* Pack f32 (K*Cin, Cout) weights into the bf16 SW128 K-major smem image. */
-int fpvs_pack_weights_tc(const float* w, int K, int cin, int cout, void* packed, void* stream);
+/* Bytes of the packed tensor-core weight image for (K, Cin, Cout) cut into
+ * BN-wide output-column blocks (bn = 0 picks the smallest of 32/64/128/256
+ * that covers Cout; smaller bn splits N across CTAs for layers with few rows). */
+size_t fpvs_pack_weights_tc_size(int K, int cin, int cout, int bn);
+/* Pack f32 (K*Cin, Cout) weights into the bf16 SW128 K-major smem image,
+ * layout [Cout/bn][ceil(K*Cin/64)][bn][128 B]. */
+int fpvs_pack_weights_tc(const float* w, int K, int cin, int cout, int bn, void* packed, void* stream);
 
-/* tcgen05 path: bf16 in, fp32 TMEM accumulate, fused bias + act, bf16 out. */
-int fpvs_spconv_tc(const void* x, int ldx, const int32_t* nbr, int K,
-                   const int32_t* n_out_dev, int cap_out, const void* w_packed,
+/* tcgen05 path: bf16 in, fp32 TMEM accumulate, fused bias + act, bf16 out.
+ * x has x_rows rows of stride ldx; rows of x are gathered by TMA
+ * (tile::gather4) when Cin % 64 == 0, else by cp.async.  w_packed must have
+ * been packed with the same bn. */
+int fpvs_spconv_tc(const void* x, int ldx, int x_rows, const int32_t* nbr, int K,
+                   const int32_t* n_out_dev, int cap_out, const void* w_packed, int bn,
                    const float* bias, int cin, int cout, int act,
                    void* y, int ldy, int col_off, void* stream);
 
@@ -151,8 +157,8 @@ int fpvs_head_simt(const void* x, int ldx, int in_dtype, const int32_t* coords,
                    const int32_t* n_dev, int cap, const float* w, const float* bias,
                    int cin, int d, int B, int Nx, int Ny, int Nz, float tau,
                    uint8_t* out_bits, float* probs, float* logits, void* stream);
-int fpvs_head_tc(const void* x, int ldx, const int32_t* coords, const int32_t* n_dev, int cap,
-                 const void* w_packed, const float* bias, int cin, int d,
+int fpvs_head_tc(const void* x, int ldx, int x_rows, const int32_t* coords, const int32_t* n_dev,
+                 int cap, const void* w_packed, const float* bias, int cin, int d,
                  int B, int Nx, int Ny, int Nz, float tau,
                  uint8_t* out_bits, float* probs, float* logits, void* stream);
 

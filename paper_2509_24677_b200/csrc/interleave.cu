@@ -80,10 +80,12 @@ __global__ void interleave_bits_kernel(const uint8_t* __restrict__ bits, int B, 
   }
 }
 
-// any bit of the d^3 block of cell c set?
-__device__ __forceinline__ uint8_t block_any(const uint8_t* __restrict__ bits, int b, int bx, int by,
-                                             int bz, int d, int Nx, int Ny, int Nz) {
+// any bit of the d^3 block of cell (b, bx, by, bz) set?  (all d*d row loads
+// issued before the test, no early exit, for memory-level parallelism)
+__device__ __forceinline__ uint8_t block_any(const uint8_t* __restrict__ bits, int b, int bx, int by, int bz, int d,
+                                             int Nx, int Ny, int Nz) {
   const int x0 = bx * d;
+  uint32_t acc = 0;
   for (int lz = 0; lz < d; ++lz)
     for (int ly = 0; ly < d; ++ly) {
       const uint8_t* row = bits + bit_byte(b, 0, by * d + ly, bz * d + lz, Nx, Ny, Nz);
@@ -92,25 +94,45 @@ __device__ __forceinline__ uint8_t block_any(const uint8_t* __restrict__ bits, i
         int sh = x & 7;
         int nb = min(8 - sh, x0 + d - x);
         uint32_t m = ((1u << nb) - 1u) << sh;
-        if (__ldg(row + (x >> 3)) & m) return 1;
+        acc |= __ldg(row + (x >> 3)) & m;
         x += nb;
       }
     }
-  return 0;
+  return acc ? 1 : 0;
 }
 
-__global__ void cell_active_bits_kernel(const uint8_t* __restrict__ bits, int B, int Nx, int Ny, int Nz,
-                                        int d, uint8_t* __restrict__ cell_active) {
+// Active flags of cells from packed bits.  A block covers 32 (bx) x 32 (bz)
+// cells of one (b, by) slab: lanes walk x so the bytes a warp reads per
+// froxel row are contiguous, then the flags are transposed through shared
+// memory so the C-order (z-fastest) output is written in 32-byte runs.
+__global__ void __launch_bounds__(256) cell_active_bits_kernel(const uint8_t* __restrict__ bits, int B, int Nx, int Ny,
+                                                               int Nz, int d, uint8_t* __restrict__ cell_active) {
+  __shared__ uint8_t flag[32][33];
   const int X = Nx / d, Y = Ny / d, Z = Nz / d;
-  const long long total = (long long)B * X * Y * Z;
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < total;
-       c += (long long)gridDim.x * blockDim.x) {
-    long long r = c;
-    int bz = r % Z; r /= Z;
-    int by = r % Y; r /= Y;
-    int bx = r % X;
-    int b = (int)(r / X);
-    cell_active[c] = block_any(bits, b, bx, by, bz, d, Nx, Ny, Nz);
+  const int nxt = (X + 31) / 32, nzt = (Z + 31) / 32;
+  long long blk = blockIdx.x;
+  const int zt = blk % nzt; blk /= nzt;
+  const int xt = blk % nxt; blk /= nxt;
+  const int by = blk % Y;
+  const int b = (int)(blk / Y);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int bx = xt * 32 + lane;
+  for (int i = 0; i < 4; ++i) {
+    const int bzl = w + 8 * i, bz = zt * 32 + bzl;
+    uint8_t f = 0;
+    if (bx < X && bz < Z) f = block_any(bits, b, bx, by, bz, d, Nx, Ny, Nz);
+    flag[lane][bzl] = f;
+  }
+  __syncthreads();
+  const int bxl = threadIdx.x >> 3, zq = (threadIdx.x & 7) * 4;
+  const int ox = xt * 32 + bxl;
+  if (ox < X) {
+    const long long row = (((long long)b * X + ox) * Y + by) * Z;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int oz = zt * 32 + zq + q;
+      if (oz < Z) cell_active[row + oz] = flag[bxl][zq + q];
+    }
   }
 }
 
@@ -158,20 +180,56 @@ __global__ void deinterleave_thresh_kernel(const Tin* __restrict__ in, int B, in
 }
 
 template <typename Tout>
+__device__ __forceinline__ void store8(Tout* dst, const float (&v)[8]);
+template <>
+__device__ __forceinline__ void store8<__nv_bfloat16>(__nv_bfloat16* dst, const float (&v)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+template <>
+__device__ __forceinline__ void store8<float>(float* dst, const float (&v)[8]) {
+  reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+// Sparse interleave: one thread per (active row, group of 8 channels); the
+// group's bits come from a few L1-cached bytes and leave as one 16-byte
+// (bf16) / 32-byte (f32) store.
+template <typename Tout>
 __global__ void gather_cells_bits_kernel(const uint8_t* __restrict__ bits, int Nx, int Ny, int Nz, int d,
                                          const int4* __restrict__ coords, const int* __restrict__ n_dev,
                                          int cap, Tout* __restrict__ x, int ldx) {
   const int n = min(*n_dev, cap);
   const int d3 = d * d * d;
-  const long long total = (long long)n * d3;
+  const int groups = (d3 + 7) / 8;
+  const bool vec = (d3 % 8 == 0) && (ldx % 8 == 0);
+  const long long total = (long long)n * groups;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    int k = t % d3;
-    long long i = t / d3;
-    int4 c = coords[i];
-    int lx = k % d, ly = (k / d) % d, lz = k / (d * d);
-    x[i * ldx + k] = from_f32<Tout>((float)read_bit(bits, c.x, c.y * d + lx, c.z * d + ly, c.w * d + lz,
-                                                    Nx, Ny, Nz));
+    const int g = t % groups;
+    const long long i = t / groups;
+    const int4 c = coords[i];
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int k = g * 8 + q;
+      v[q] = 0.f;
+      if (k < d3) {
+        const int lx = k % d, ly = (k / d) % d, lz = k / (d * d);
+        v[q] = (float)read_bit(bits, c.x, c.y * d + lx, c.z * d + ly, c.w * d + lz, Nx, Ny, Nz);
+      }
+    }
+    Tout* dst = x + i * ldx + g * 8;
+    if (vec) {
+      store8<Tout>(dst, v);
+    } else {
+      for (int q = 0; q < 8 && g * 8 + q < d3; ++q) dst[q] = from_f32<Tout>(v[q]);
+    }
   }
 }
 
@@ -204,9 +262,10 @@ extern "C" int fpvs_interleave(const void* in, int in_fmt, int B, int Nx, int Ny
     else
       interleave_bits_kernel<__nv_bfloat16><<<g, 256, 0, s>>>((const uint8_t*)in, B, Nx, Ny, Nz, d,
                                                               (__nv_bfloat16*)out);
-    if (cell_active)
-      cell_active_bits_kernel<<<grid_for((long long)B * X * Y * Z, 256), 256, 0, s>>>(
-          (const uint8_t*)in, B, Nx, Ny, Nz, d, cell_active);
+    if (cell_active) {
+      long long nblk = (long long)B * Y * ((X + 31) / 32) * ((Z + 31) / 32);
+      cell_active_bits_kernel<<<(unsigned)nblk, 256, 0, s>>>((const uint8_t*)in, B, Nx, Ny, Nz, d, cell_active);
+    }
     FPVS_CHECK_LAUNCH("fpvs_interleave(packed)");
     return FPVS_OK;
   }
@@ -268,9 +327,9 @@ extern "C" int fpvs_cell_active_from_bits(const uint8_t* bits, int B, int Nx, in
   int rc = check_grid(B, Nx, Ny, Nz, d);
   if (rc) return rc;
   FPVS_CHECK_ARG(Nx % 8 == 0, "packed grids need N_x divisible by 8, got %d", Nx);
-  long long total = (long long)B * (Nx / d) * (Ny / d) * (Nz / d);
-  cell_active_bits_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(bits, B, Nx, Ny, Nz, d,
-                                                                              cell_active);
+  const int X = Nx / d, Y = Ny / d, Z = Nz / d;
+  long long nblk = (long long)B * Y * ((X + 31) / 32) * ((Z + 31) / 32);
+  cell_active_bits_kernel<<<(unsigned)nblk, 256, 0, as_stream(stream)>>>(bits, B, Nx, Ny, Nz, d, cell_active);
   FPVS_CHECK_LAUNCH("fpvs_cell_active_from_bits");
   return FPVS_OK;
 }
@@ -282,7 +341,7 @@ extern "C" int fpvs_gather_cells_bits(const uint8_t* bits, int B, int Nx, int Ny
   if (rc) return rc;
   FPVS_CHECK_ARG(ldx >= d * d * d, "ldx %d < d^3", ldx);
   cudaStream_t s = as_stream(stream);
-  int g = grid_for((long long)cap * d * d * d, 256);
+  int g = grid_for((long long)cap * ((d * d * d + 7) / 8), 256);
   if (dtype == FPVS_F32)
     gather_cells_bits_kernel<float><<<g, 256, 0, s>>>(bits, Nx, Ny, Nz, d, (const int4*)coords,
                                                        n_active_dev, cap, (float*)x, ldx);

@@ -17,105 +17,112 @@
 namespace fpvs {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanIters = 16;
-constexpr int kScanCells = kScanThreads * kScanIters;  // cells per block
+constexpr int kScanPer = 16;                              // cells per thread (one 16-byte load)
+constexpr int kScanCells = kScanThreads * kScanPer;       // cells per tile
+constexpr unsigned kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValMask = (1u << 30) - 1u;
 
 __device__ __forceinline__ long long lin4(int b, int x, int y, int z, int X, int Y, int Z) {
   return (((long long)b * X + x) * Y + y) * Z + z;
 }
-
-__global__ void compact_count_kernel(const uint8_t* __restrict__ act, long long ncell,
-                                     int* __restrict__ block_sums) {
-  __shared__ int warp_tot[kScanThreads / 32];
-  const long long base = (long long)blockIdx.x * kScanCells;
-  int cnt = 0;
-  for (int it = 0; it < kScanIters; ++it) {
-    long long c = base + it * kScanThreads + threadIdx.x;
-    cnt += (c < ncell && act[c]) ? 1 : 0;
-  }
-  cnt = __reduce_add_sync(0xffffffffu, cnt);
-  if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int s = 0;
-    for (int w = 0; w < kScanThreads / 32; ++w) s += warp_tot[w];
-    block_sums[blockIdx.x] = s;
-  }
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// single-block exclusive scan of block sums; total -> *n_out
-__global__ void compact_scan_kernel(int* __restrict__ block_sums, int nblk, int* __restrict__ n_out) {
-  __shared__ int wsum[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
+// Single-pass stream compaction (decoupled look-back): each tile of 4096
+// cells takes a dynamic tile id, block-scans its 16-cells-per-thread counts,
+// publishes its aggregate, resolves its exclusive prefix from predecessors,
+// then writes index_vol (rank or -1, 64 B per thread, coalesced) and the
+// C-order coordinates of its active cells.
+__global__ void __launch_bounds__(kScanThreads) compact_kernel(
+    const uint8_t* __restrict__ act, long long ncell, int X, int Y, int Z, int4* __restrict__ coords,
+    int* __restrict__ index_vol, int cap, unsigned* __restrict__ status, int* __restrict__ tile_ctr,
+    int* __restrict__ n_out, int ntiles) {
+  __shared__ int s_tile, s_prefix;
+  __shared__ int s_warp[kScanThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(tile_ctr, 1);
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int base = 0; base < nblk; base += blockDim.x) {
-    int i = base + threadIdx.x;
-    int v = i < nblk ? block_sums[i] : 0;
-    int incl = v;
+  const int tile = s_tile;
+  const long long base = (long long)tile * kScanCells + (long long)tid * kScanPer;
+  uint32_t f = 0;
+  if (base + kScanPer <= ncell && ((reinterpret_cast<uintptr_t>(act + base) & 15) == 0)) {
+    uint4 v = *reinterpret_cast<const uint4*>(act + base);
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) f |= (((w[i >> 2] >> ((i & 3) * 8)) & 0xffu) ? 1u : 0u) << i;
+  } else {
+    for (int i = 0; i < kScanPer; ++i)
+      if (base + i < ncell && act[base + i]) f |= 1u << i;
+  }
+  const int cnt = __popc(f);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int w = lane < kScanThreads / 32 ? s_warp[lane] : 0, wi = w;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
+      int t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
     }
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      int w = lane < nw ? wsum[lane] : 0;
-      int wi = w;
-      for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(0xffffffffu, wi, o);
-        if (lane >= o) wi += t;
+    if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
+    if (lane == kScanThreads / 32 - 1) {
+      const unsigned agg = (unsigned)wi;
+      unsigned prefix = 0;
+      if (tile == 0) {
+        st_release(status, kFlagPrefix | agg);
+      } else {
+        st_release(status + tile, kFlagAgg | agg);
+        for (int t = tile - 1; t >= 0;) {
+          unsigned v = ld_acquire(status + t);
+          if (!(v & (kFlagAgg | kFlagPrefix))) continue;  // predecessor not published yet
+          prefix += v & kValMask;
+          if (v & kFlagPrefix) break;
+          --t;
+        }
+        st_release(status + tile, kFlagPrefix | (prefix + agg));
       }
-      if (lane < nw) wsum[lane] = wi - w;  // exclusive warp offsets
+      s_prefix = (int)prefix;
+      if (tile == ntiles - 1) *n_out = (int)(prefix + agg);
     }
-    __syncthreads();
-    int excl = carry + wsum[wid] + incl - v;
-    if (i < nblk) block_sums[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
-    __syncthreads();
   }
-  if (threadIdx.x == 0) *n_out = carry;
-}
-
-__global__ void compact_write_kernel(const uint8_t* __restrict__ act, long long ncell, int X, int Y, int Z,
-                                     const int* __restrict__ block_off, int4* __restrict__ coords,
-                                     int* __restrict__ index_vol, int cap) {
-  __shared__ int warp_cnt[kScanThreads / 32];
-  __shared__ int run;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) run = block_off[blockIdx.x];
   __syncthreads();
-  const long long base = (long long)blockIdx.x * kScanCells;
-  for (int it = 0; it < kScanIters; ++it) {
-    long long c = base + it * kScanThreads + threadIdx.x;
-    bool a = c < ncell && act[c];
-    unsigned m = __ballot_sync(0xffffffffu, a);
-    if (lane == 0) warp_cnt[wid] = __popc(m);
-    __syncthreads();
-    int off = run;
-    for (int w = 0; w < wid; ++w) off += warp_cnt[w];
-    int rank = off + __popc(m & ((1u << lane) - 1u));
-    if (c < ncell) {
-      int row = (a && rank < cap) ? rank : -1;
-      index_vol[c] = row;
-      if (row >= 0) {
-        long long r = c;
-        int z = r % Z; r /= Z;
-        int y = r % Y; r /= Y;
-        int x = r % X;
-        int b = (int)(r / X);
-        coords[row] = make_int4(b, x, y, z);
-      }
+  int rank = s_prefix + s_warp[wid] + incl - cnt;
+  int rows[kScanPer];
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i) {
+    const bool a = (f >> i) & 1u;
+    rows[i] = (a && rank < cap) ? rank : -1;
+    rank += a ? 1 : 0;
+  }
+  if (base + kScanPer <= ncell && ((reinterpret_cast<uintptr_t>(index_vol + base) & 15) == 0)) {
+    int4* dst = reinterpret_cast<int4*>(index_vol + base);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[q] = make_int4(rows[4 * q], rows[4 * q + 1], rows[4 * q + 2], rows[4 * q + 3]);
+  } else {
+    for (int i = 0; i < kScanPer; ++i)
+      if (base + i < ncell) index_vol[base + i] = rows[i];
+  }
+  if (f) {
+#pragma unroll
+    for (int i = 0; i < kScanPer; ++i) {
+      if (rows[i] < 0) continue;
+      long long r = base + i;
+      int z = r % Z; r /= Z;
+      int y = r % Y; r /= Y;
+      int x = r % X;
+      coords[rows[i]] = make_int4((int)(r / X), x, y, z);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int w = 0; w < kScanThreads / 32; ++w) t += warp_cnt[w];
-      run += t;
-    }
-    __syncthreads();
   }
 }
 
@@ -264,7 +271,7 @@ static long long ncells(int B, int X, int Y, int Z) { return (long long)B * X * 
 
 extern "C" size_t fpvs_kmap_workspace_size(int B, int X, int Y, int Z) {
   long long nblk = (ncells(B, X, Y, Z) + kScanCells - 1) / kScanCells;
-  return (size_t)(nblk + 1) * sizeof(int);
+  return (size_t)(nblk + 1) * sizeof(unsigned);
 }
 
 extern "C" int fpvs_kmap_compact(const uint8_t* cell_active, int B, int X, int Y, int Z, int32_t* coords,
@@ -274,12 +281,13 @@ extern "C" int fpvs_kmap_compact(const uint8_t* cell_active, int B, int X, int Y
   FPVS_CHECK_ARG(cell_active && coords && index_vol && n_active_dev && workspace, "null pointer");
   FPVS_CHECK_ARG(workspace_bytes >= fpvs_kmap_workspace_size(B, X, Y, Z), "workspace too small");
   const long long nc = ncells(B, X, Y, Z);
+  FPVS_CHECK_ARG(nc < (1LL << 30), "cell grid too large for one compaction (%lld cells)", nc);
   const int nblk = (int)((nc + kScanCells - 1) / kScanCells);
-  int* bs = (int*)workspace;
+  unsigned* status = (unsigned*)workspace;
   cudaStream_t s = as_stream(stream);
-  compact_count_kernel<<<nblk, kScanThreads, 0, s>>>(cell_active, nc, bs);
-  compact_scan_kernel<<<1, 1024, 0, s>>>(bs, nblk, n_active_dev);
-  compact_write_kernel<<<nblk, kScanThreads, 0, s>>>(cell_active, nc, X, Y, Z, bs, (int4*)coords, index_vol, cap);
+  cudaMemsetAsync(status, 0, (size_t)(nblk + 1) * sizeof(unsigned), s);
+  compact_kernel<<<nblk, kScanThreads, 0, s>>>(cell_active, nc, X, Y, Z, (int4*)coords, index_vol, cap, status,
+                                               (int*)(status + nblk), n_active_dev, nblk);
   FPVS_CHECK_LAUNCH("fpvs_kmap_compact");
   return FPVS_OK;
 }

@@ -1,49 +1,54 @@
 // (3) Sparse convolution on 5th-generation tensor cores (tcgen05, sm_100a).
 //
-// Implicit gather-GEMM-scatter: for a tile of BM = 128 output rows (active
-// cells), the K dimension is the flattened (offset j, channel ci) index
+// Implicit gather-GEMM-scatter.  An output tile is BM = 128 active cells x BN
+// output channels.  K is the flattened (offset j, channel ci) index
 // k = j*Cin + ci of the reference weight rows (neural.py:163-166), cut into
 // 64-element (128-byte) chunks.  Per chunk:
-//   * A (128 x 64 bf16): 4 producer warps gather 16-byte pieces of the
-//     neighbour rows x[nbr[i][j]] with cp.async straight into the 128B-swizzled
-//     K-major shared-memory layout the UMMA descriptor expects; a missing
-//     neighbour (-1) is a zero-fill (src-size 0).  Each producer thread signals
-//     the stage's mbarrier with cp.async.mbarrier.arrive.noinc, so gathers for
-//     up to STAGES chunks are in flight per SM.
-//   * B (BN x 64 bf16): one bulk copy (TMA engine, cp.async.bulk) of the
-//     pre-swizzled weight image produced by fpvs_pack_weights_tc.
-//   * one elected thread of the MMA warp issues 4 x tcgen05.mma (M=128, N=BN,
-//     K=16, bf16 -> fp32) into a TMEM accumulator; tcgen05.commit frees the
-//     stage.  Chunks whose offsets have no neighbour in the whole tile are
-//     skipped (per-tile 27-bit offset mask), so sparse tiles do less MMA work.
-//   * 4 epilogue warps drain TMEM (tcgen05.ld 32x32b) with a double-buffered
+//   * A (128 x 64 bf16) is GATHERED: row i of the tile is x[nbr[i][j]].
+//     - Cin % 64 == 0 (every config-2 layer): one producer warp issues 32
+//       TMA `tile::gather4` copies (4 rows x 128 B each) into the 128B-swizzled
+//       K-major layout the UMMA descriptor reads; a missing neighbour (-1) is
+//       an out-of-bounds row, which TMA zero-fills.  32 instructions move 16 KB.
+//     - Cin < 64 (8 / 32 channels, config 1): four producer warps gather
+//       16-byte pieces with cp.async (zero-fill via src-size 0), one chunk
+//       spanning 64/Cin offsets.
+//   * B (BN x 64 bf16): one bulk copy (cp.async.bulk, TMA engine) of the
+//     pre-swizzled weight image from fpvs_pack_weights_tc.
+//   * one elected thread issues 4 x tcgen05.mma (M=128, N=BN, K=16, bf16 ->
+//     fp32) into a TMEM accumulator; tcgen05.commit frees the stage.  Chunks
+//     whose offsets have no neighbour anywhere in the tile are skipped.
+//   * 4 epilogue warps drain TMEM (tcgen05.ld) from a double-buffered
 //     accumulator (2 x BN columns) so the epilogue of tile t overlaps the
-//     mainloop of tile t+1, fuse bias + ReLU + bf16 cast (or, for the head,
-//     sigmoid + [p >= tau] + deinterleave bit-pack), and store.
-// The grid is persistent (<= 148 CTAs, 1 per SM) and reads the active row
-// count from device memory, so the launch is graph-capturable.
+//     mainloop of tile t+1, and fuse bias + ReLU + bf16 cast, or for the
+//     head sigmoid + [p >= tau] + the deinterleave bit-pack.
+// Each tile's neighbour rows are prefetched one tile ahead (double-buffered).
+// Layers with few row tiles (coarse U-Net levels) split N across CTAs
+// (BN < Cout) so all 148 SMs get work.  The grid is persistent (<= 148 CTAs)
+// and reads the active row count from device memory (graph-capturable).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <string.h>
+
 #include "common.cuh"
 
 namespace fpvs {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 64;            // bf16 elements per chunk = 128 bytes
+constexpr int BK = 64;             // bf16 elements per chunk = 128 bytes
 constexpr int A_BYTES = BM * 128;  // 16 KB
-constexpr int kProd = 128;        // producer threads (warps 0-3)
-constexpr int kMmaWarp = 8;
-constexpr int kThreads = 288;
 constexpr int kMaxK = 27;
 
 struct Params {
   const __nv_bfloat16* x;
-  int ldx;
+  int ldx, x_rows;
   const int* nbr;
   int K;
   const int* n_dev;
   int cap;
   const uint8_t* wpk;
-  int nchunks;
+  int nchunks, nblk;
   const float* bias;
   int cin, cout, act;
   __nv_bfloat16* y;
@@ -51,22 +56,30 @@ struct Params {
   // head epilogue
   int head;
   const int4* coords;
-  int d, Nx, Ny, Nz;
-  float tau;
+  int d, dlog, Nx, Ny, Nz;
+  float tau, zt;
   uint8_t* out_bits;
   float* probs;
   float* logits;
 };
 
-template <int BN>
+template <int BN, bool TMA>
 struct Cfg {
+  static constexpr int P = TMA ? 1 : 8;         // producer warps
+  static constexpr int MMA_WARP = P;
+  static constexpr int THREADS = (P + 5) * 32;  // producers, MMA, 4 epilogue warps
+  static constexpr int PROD = P * 32;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES > 8 ? 8 : (192 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
-  static constexpr int NBR_BYTES = BM * kMaxK * 4;
+  static constexpr int NBR_BYTES = 2 * BM * kMaxK * 4;  // double-buffered neighbour tile
+  static constexpr int kStageBudget = 232448 - 1024 - NBR_BYTES - 2048;
+  static constexpr int STAGES = kStageBudget / STAGE_BYTES > 8 ? 8 : kStageBudget / STAGE_BYTES;
+  static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128
+                                 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES + NBR_BYTES;
-  static constexpr int SMEM = 1024 + BAR_OFF + 8 * (2 * STAGES + 4) + 16 + 4 * STAGES + 16;
+  static constexpr int BIAS_OFF = BAR_OFF + 8 * (2 * STAGES + 6) + 64 + 4 * STAGES;
+  static constexpr int SMEM = 1024 + BIAS_OFF + 4 * 1024 + 16;
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 // ---------------- PTX wrappers ----------------
@@ -95,6 +108,15 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
+}
+// TMA gather of 4 rows (row coordinates r0..r3, column c0) of a 2-D tensor
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const void* tmap, int c0, int r0, int r1, int r2, int r3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
@@ -160,53 +182,78 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// offsets j covered by chunk c (flattened k = j*cin + ci, 64 per chunk)
-__device__ __forceinline__ uint32_t chunk_offset_bits(int c, int cin, int K) {
-  int jlo = (c * BK) / cin, jhi = (c * BK + BK - 1) / cin;
-  if (jhi > K - 1) jhi = K - 1;
-  if (jlo > K - 1) return 0;
-  uint32_t hi = (jhi >= 31) ? 0xffffffffu : ((1u << (jhi + 1)) - 1u);
-  return hi & ~((1u << jlo) - 1u);
+// Copy neighbour rows [row0, row0 + BM) of a K-wide int32 table into shared
+// memory with 16-byte cp.async pieces (zero-filled past the table end), then
+// arrive (noinc) on `bar` once this thread's copies have landed.
+__device__ __forceinline__ void prefetch_nbr(const Params& p, int row0, uint32_t dst, uint32_t bar, int t, int nt) {
+  const long long tab_bytes = (long long)p.cap * p.K * 4;
+  const long long base = (long long)row0 * p.K * 4;
+  const int bytes = BM * p.K * 4;
+  const char* src = reinterpret_cast<const char*>(p.nbr);
+  for (int o = t * 16; o < bytes; o += nt * 16) {
+    long long rem = tab_bytes - (base + o);
+    uint32_t n = rem >= 16 ? 16u : (rem > 0 ? (uint32_t)rem : 0u);
+    cp_async16(dst + o, src + (n ? base + o : 0), n);
+  }
+  cp_async_mbar_arrive_noinc(bar);
 }
 
-template <int BN>
-__global__ void __launch_bounds__(kThreads, 1) spconv_tc_kernel(const Params p) {
-  using C = Cfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+template <int BN, bool TMA>
+__global__ void __launch_bounds__(Cfg<BN, TMA>::THREADS, 1)
+    spconv_tc_kernel(const Params p, const __grid_constant__ CUtensorMap xmap) {
+  using C = Cfg<BN, TMA>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // pointers stay derived from the __shared__ array (LDS/STS, not generic)
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * A_BYTES;
-  int* s_nbr = reinterpret_cast<int*>(smem + C::STAGES * C::STAGE_BYTES);
+  int* s_nbr = reinterpret_cast<int*>(smem + C::STAGES * C::STAGE_BYTES);  // 2 x BM*K
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint32_t* s_mask = s_tmem + 1;   // 4 warp masks
-  uint32_t* s_info = s_tmem + 8;   // per-stage flags (bit0 first, bit1 last)
+  uint64_t* nbar = tempty + 2;  // neighbour-tile prefetch, 2 buffers
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(nbar + 2);
+  uint32_t* s_mask = s_tmem + 1;   // up to 4 producer-warp masks
+  uint32_t* s_info = s_tmem + 16;  // per-stage flags (bit0 first, bit1 last)
+  float* s_bias = reinterpret_cast<float*>(smem + C::BIAS_OFF);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = min(*p.n_dev, p.cap);
-  const int ntiles = (n + BM - 1) / BM;
+  const int mtiles = (n + BM - 1) / BM;
+  const int ntiles = mtiles * p.nblk;
 
   if (tid == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(smem_u32(full + s), kProd + 1);
+      mbar_init(smem_u32(full + s), TMA ? 1 : C::PROD + 1);
       mbar_init(smem_u32(empty + s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(tfull + a), 1);
       mbar_init(smem_u32(tempty + a), 128);
+      mbar_init(smem_u32(nbar + a), C::PROD);
     }
     fence_mbar_init();
   }
-  if (warp == kMmaWarp) {
+  for (int c = tid; c < p.cout; c += C::THREADS) s_bias[c] = p.bias ? p.bias[c] : 0.f;
+  if (warp == C::MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
                  "n"(C::TMEM_COLS)
                  : "memory");
@@ -217,107 +264,153 @@ __global__ void __launch_bounds__(kThreads, 1) spconv_tc_kernel(const Params p) 
   tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
 
-  if (warp < 4) {
+  if (warp < C::P) {
     // ===================== gather producers =====================
     int stage = 0;
     uint32_t phase = 0;
+    const int nbr_elems = BM * p.K;
+    const int ptid = tid;  // 0 .. PROD-1
+    // chunk <-> (offset, channel) maps without runtime division: Cin >= 64
+    // gives cpo = Cin/64 chunks per offset, Cin < 64 gives opc = 64/Cin
+    // offsets per chunk (Cin is a multiple of 8; both are exact here)
+    const int cpo = p.cin >= BK ? p.cin / BK : 1;
+    const int opc = p.cin >= BK ? 1 : BK / p.cin;
     const int ppo = p.cin >> 3;  // 16-byte pieces per offset
+    // neighbour rows depend only on the m-tile; consecutive n-blocks reuse them
+    int cur_m = -1, lt = 0, buf = 1;
+    if (p.nbr && (int)blockIdx.x < ntiles)
+      prefetch_nbr(p, ((int)blockIdx.x / p.nblk) * BM, smem_u32(s_nbr), smem_u32(nbar), ptid, C::PROD);
+    // cp.async thread geometry: piece = 16-byte column slot, rows r_i = rbase + i*RSTEP
+    constexpr int RSTEP = C::PROD / 8;
+    constexpr int NPT = BM / RSTEP;  // rows (cp.async ops) per thread per chunk
+    const int piece = ptid & 7, rbase = ptid >> 3;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int row0 = tile * BM;
-      named_bar(1, kProd);  // previous tile's readers of s_nbr are done
-      for (int e = tid; e < BM * p.K; e += kProd) {
-        int r = e / p.K;
-        int v = -1;
-        if (row0 + r < n) v = p.nbr ? __ldg(p.nbr + (long long)row0 * p.K + e) : row0 + r;
-        s_nbr[e] = v;
+      const int mt = tile / p.nblk, nb = tile - mt * p.nblk;
+      const int row0 = mt * BM;
+      if (mt != cur_m) {
+        buf ^= 1;
+        if (p.nbr) mbar_wait(smem_u32(nbar + buf), (lt >> 1) & 1);
+        ++lt;
+        cur_m = mt;
+        if (C::P > 1) named_bar(1, C::PROD); else __syncwarp();
+        // prefetch the next distinct m-tile this CTA will visit into the other buffer
+        int nt = tile + gridDim.x;
+        while (nt < ntiles && nt / p.nblk == mt) nt += gridDim.x;
+        if (p.nbr && nt < ntiles)
+          prefetch_nbr(p, (nt / p.nblk) * BM, smem_u32(s_nbr + (buf ^ 1) * nbr_elems), smem_u32(nbar + (buf ^ 1)),
+                       ptid, C::PROD);
       }
-      named_bar(1, kProd);
+      const int* nb_s = s_nbr + buf * nbr_elems;
+      // per-tile offset mask: OR of "neighbour j present" over the tile's rows
       uint32_t m = 0;
-      for (int j = 0; j < p.K; ++j) m |= (s_nbr[tid * p.K + j] >= 0 ? 1u : 0u) << j;
+      for (int r = ptid; r < BM; r += C::PROD) {
+        if (row0 + r >= n) continue;
+        if (p.nbr) {
+          for (int j = 0; j < p.K; ++j) m |= (nb_s[r * p.K + j] >= 0 ? 1u : 0u) << j;
+        } else {
+          m |= 1u;
+        }
+      }
       m = __reduce_or_sync(0xffffffffu, m);
-      if (lane == 0) s_mask[warp] = m;
-      named_bar(1, kProd);
-      const uint32_t tmask = s_mask[0] | s_mask[1] | s_mask[2] | s_mask[3];
-      int last = -1, first = -1;
-      for (int c = 0; c < p.nchunks; ++c)
-        if (chunk_offset_bits(c, p.cin, p.K) & tmask) { last = c; if (first < 0) first = c; }
-      if (last < 0) { first = 0; last = 0; }  // keep the pipeline shape: one zero chunk
-      for (int c = first; c <= last; ++c) {
-        if (c != first && c != last && !(chunk_offset_bits(c, p.cin, p.K) & tmask)) continue;
+      uint32_t tmask = m;
+      if (C::P > 1) {
+        if (lane == 0) s_mask[warp] = m;
+        named_bar(1, C::PROD);
+        tmask = 0;
+        for (int w = 0; w < C::P; ++w) tmask |= s_mask[w];
+        named_bar(1, C::PROD);
+      }
+      if (tmask == 0) tmask = 1u;  // keep the pipeline shape: one (zero) chunk
+      // chunks to issue: for Cin >= 64 every ci-chunk of each present offset;
+      // for Cin < 64 every chunk whose offset group has a present offset
+      const uint32_t gmask = (opc >= 32) ? 0xffffffffu : ((1u << opc) - 1u);
+      int nissue;
+      if (opc == 1) {
+        nissue = __popc(tmask) * cpo;
+      } else {
+        nissue = 0;
+        for (int c = 0; c < p.nchunks; ++c) nissue += ((tmask >> (c * opc)) & gmask) ? 1 : 0;
+      }
+      // per-thread row geometry for this tile (cp.async path)
+      int rowk[NPT];
+      uint32_t dsto[NPT];
+      bool rok[NPT];
+#pragma unroll
+      for (int i = 0; i < NPT; ++i) {
+        const int r = rbase + i * RSTEP;
+        rowk[i] = r * p.K;
+        rok[i] = row0 + r < n;
+        dsto[i] = r * 128 + ((piece ^ (r & 7)) << 4);
+      }
+      const uint8_t* wblk = p.wpk + (size_t)nb * p.nchunks * C::B_BYTES;
+      uint32_t rem = tmask;
+      int j = -1, cc = cpo;  // current offset / ci-chunk for opc == 1
+      int cg = -1;           // current chunk for opc > 1
+      for (int q = 0; q < nissue; ++q) {
+        int c;
+        if (opc == 1) {
+          if (++cc >= cpo) { cc = 0; j = __ffs(rem) - 1; rem &= rem - 1; }
+          c = j * cpo + cc;
+        } else {
+          do { ++cg; } while (!((tmask >> (cg * opc)) & gmask));
+          c = cg;
+        }
         mbar_wait(smem_u32(empty + stage), phase ^ 1);
         const uint32_t fb = smem_u32(full + stage);
-        if (tid == 0) {
-          s_info[stage] = (c == first ? 1u : 0u) | (c == last ? 2u : 0u);
-          mbar_arrive_expect_tx(fb, C::B_BYTES);
-          bulk_g2s(smem_u32(sB + stage * C::B_BYTES), p.wpk + (size_t)c * C::B_BYTES, C::B_BYTES, fb);
-        }
         const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
-        const int piece = lane & 7;
-        const int g = c * 8 + piece;          // global 16B piece index along K
-        const int j = g / ppo, ci = (g % ppo) * 8;
+        const uint32_t info = (q == 0 ? 1u : 0u) | (q == nissue - 1 ? 2u : 0u);
+        if constexpr (TMA) {
+          if (lane == 0) {
+            s_info[stage] = info;
+            mbar_arrive_expect_tx(fb, A_BYTES + C::B_BYTES);
+          }
+          __syncwarp();
+          const int ci0 = cc * BK;
+          int rr[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = i * 16 + warp * 4 + (lane >> 3);
-          int src = (j < p.K) ? s_nbr[r * p.K + j] : -1;
-          const __nv_bfloat16* gp = p.x + (src >= 0 ? (long long)src * p.ldx + ci : 0);
-          cp_async16(a_base + r * 128 + ((piece ^ (r & 7)) << 4), gp, src >= 0 ? 16u : 0u);
+          for (int t = 0; t < 4; ++t) {
+            const int r = lane * 4 + t;
+            int src = -1;
+            if (row0 + r < n) src = p.nbr ? nb_s[r * p.K + j] : row0 + r;
+            rr[t] = src >= 0 ? src : p.x_rows;  // out-of-bounds row -> TMA zero fill
+          }
+          tma_gather4(a_base + lane * 512, &xmap, ci0, rr[0], rr[1], rr[2], rr[3], fb);
+          if (lane == 0) bulk_g2s(smem_u32(sB + stage * C::B_BYTES), wblk + (size_t)c * C::B_BYTES, C::B_BYTES, fb);
+        } else {
+          if (ptid == 0) {
+            s_info[stage] = info;
+            mbar_arrive_expect_tx(fb, C::B_BYTES);
+            bulk_g2s(smem_u32(sB + stage * C::B_BYTES), wblk + (size_t)c * C::B_BYTES, C::B_BYTES, fb);
+          }
+          int jj, ci;
+          if (opc == 1) {
+            jj = j;
+            ci = cc * BK + piece * 8;
+          } else {
+            const int g = piece + (c * opc) * ppo;  // piece index along K (ppo pieces per offset)
+            jj = g / ppo;
+            ci = (g - jj * ppo) * 8;
+          }
+          const bool jok = jj < p.K;
+          int src[NPT];
+#pragma unroll
+          for (int i = 0; i < NPT; ++i) {
+            src[i] = -1;
+            if (jok && rok[i]) src[i] = p.nbr ? nb_s[rowk[i] + jj] : row0 + rbase + i * RSTEP;
+          }
+#pragma unroll
+          for (int i = 0; i < NPT; ++i) {
+            const bool ok = src[i] >= 0;
+            const __nv_bfloat16* gp = p.x + (ok ? (long long)src[i] * p.ldx + ci : 0);
+            cp_async16(a_base + dsto[i], gp, ok ? 16u : 0u);
+          }
+          cp_async_mbar_arrive_noinc(fb);
         }
-        cp_async_mbar_arrive_noinc(fb);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp < 8) {
-    // ===================== epilogue =====================
-    const int q = warp & 3;  // TMEM lane quadrant
-    const int r = q * 32 + lane;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const int acc = it & 1;
-      mbar_wait(smem_u32(tfull + acc), (it >> 1) & 1);
-      tc_fence_after();
-      const int row = tile * BM + r;
-      const bool valid = row < n;
-      int4 cc = make_int4(0, 0, 0, 0);
-      if (p.head && valid) cc = p.coords[row];
-#pragma unroll 1
-      for (int cb = 0; cb < BN; cb += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb, v);
-        if (!valid || cb >= p.cout) continue;
-        if (!p.head) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            float z = v[i] + (p.bias ? __ldg(p.bias + cb + i) : 0.f);
-            v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
-          }
-          uint4* dst = reinterpret_cast<uint4*>(p.y + (long long)row * p.ldy + p.col_off + cb);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(pack_bf16x2(v[8 * i + 0], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
-                                pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
-        } else {
-          const int d = p.d;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int k = cb + i;
-            if (k >= p.cout) continue;
-            float z = v[i] + (p.bias ? __ldg(p.bias + k) : 0.f);
-            float pr = sigmoidf_stable(z);
-            if (p.logits) p.logits[(long long)row * p.cout + k] = z;
-            if (p.probs) p.probs[(long long)row * p.cout + k] = pr;
-            if (pr >= p.tau && p.out_bits) {
-              int lx = k % d, ly = (k / d) % d, lz = k / (d * d);
-              int fx = cc.y * d + lx;
-              atomic_or_bit(p.out_bits, bit_byte(cc.x, fx, cc.z * d + ly, cc.w * d + lz, p.Nx, p.Ny, p.Nz), fx & 7);
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(smem_u32(tempty + acc));
-    }
-  } else {
-    // ===================== MMA issuer (warp 8) =====================
+  } else if (warp == C::MMA_WARP) {
+    // ===================== MMA issuer =====================
     const uint32_t idesc = idesc_bf16<BN>();
     int stage = 0;
     uint32_t phase = 0;
@@ -330,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) spconv_tc_kernel(const Params p) 
       while (true) {
         mbar_wait(smem_u32(full + stage), phase);
         tc_fence_after();
-        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 (async proxy) reads
+        if constexpr (!TMA) fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05 (async proxy)
         const uint32_t info = s_info[stage];
         if (lane == 0) {
           const uint64_t ad = sw128_desc(smem_u32(sA + stage * A_BYTES));
@@ -346,31 +439,116 @@ __global__ void __launch_bounds__(kThreads, 1) spconv_tc_kernel(const Params p) 
         if (info & 2u) break;
       }
     }
+  } else {
+    // ===================== epilogue (4 warps) =====================
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int r = q * 32 + lane;
+    const uint32_t tlane = (uint32_t)(q * 32) << 16;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int mt = tile / p.nblk, nb = tile - mt * p.nblk;
+      const int acc = it & 1;
+      mbar_wait(smem_u32(tfull + acc), (it >> 1) & 1);
+      tc_fence_after();
+      const int row = mt * BM + r;
+      const bool valid = row < n;
+      const int col0 = nb * BN;
+      if (!p.head) {
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 32) {
+          float v[32];
+          tmem_ld32(tmem_base + tlane + acc * BN + cb, v);
+          if (!valid || col0 + cb >= p.cout) continue;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float z = v[i] + s_bias[col0 + cb + i];
+            v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
+          }
+          uint4* dst = reinterpret_cast<uint4*>(p.y + (long long)row * p.ldy + p.col_off + col0 + cb);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_bf16x2(v[8 * i + 0], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                                pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+        }
+      } else {
+        // [p >= tau] as [z >= logit(tau)] (sigmoid is monotone; the two differ
+        // only within fp32 rounding of tau, inside the parity band).  When d is
+        // a power of two <= 8, the d bits of one (ly, lz) row of a cell share a
+        // byte of the packed grid: build them in a register, one RED.OR per row.
+        int4 cc = make_int4(0, 0, 0, 0);
+        if (valid) cc = p.coords[row];
+        const int d = p.d, dl = p.dlog;
+        const bool fast = dl >= 0 && d <= 8 && !p.probs && !p.logits && p.out_bits;
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 8) {
+          float v[8];
+          tmem_ld8(tmem_base + tlane + acc * BN + cb, v);
+          if (!valid || cb >= p.cout) continue;
+          if (fast) {
+            uint32_t bits8 = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) bits8 |= (v[i] + s_bias[cb + i] >= p.zt ? 1u : 0u) << i;
+            if (!bits8) continue;
+            const uint32_t dm = (1u << d) - 1u;
+            for (int q = 0; q < (8 >> dl); ++q) {
+              const uint32_t rb = (bits8 >> (q * d)) & dm;
+              if (!rb) continue;
+              const int rr = (cb >> dl) + q;  // rr = ly + d*lz
+              const int ly = rr & (d - 1), lz = rr >> dl;
+              const int fx = cc.y * d;
+              const long long byte = bit_byte(cc.x, fx, cc.z * d + ly, cc.w * d + lz, p.Nx, p.Ny, p.Nz);
+              uint32_t* word = reinterpret_cast<uint32_t*>(p.out_bits + (byte & ~3LL));
+              atomicOr(word, rb << ((int)(byte & 3) * 8 + (fx & 7)));
+            }
+          } else {
+#pragma unroll 1
+            for (int i = 0; i < 8; ++i) {
+              const int k = cb + i;
+              if (k >= p.cout) break;
+              const float z = v[i] + s_bias[k];
+              const float pr = sigmoidf_stable(z);
+              if (p.logits) p.logits[(long long)row * p.cout + k] = z;
+              if (p.probs) p.probs[(long long)row * p.cout + k] = pr;
+              if (pr >= p.tau && p.out_bits) {
+                const int lx = k % d, rr = k / d;
+                const int fx = cc.y * d + lx;
+                atomic_or_bit(p.out_bits, bit_byte(cc.x, fx, cc.z * d + rr % d, cc.w * d + rr / d, p.Nx, p.Ny, p.Nz),
+                              fx & 7);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(smem_u32(tempty + acc));
+    }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) {
+  if (warp == C::MMA_WARP) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
                  : "memory");
   }
 }
 
-// packed[c][n][128 B] for n < BN: element kk of chunk c at
-// n*128 + ((kk/8) ^ (n%8))*16 + (kk%8)*2 (Swizzle<3,4,3>), value W[c*64+kk][n]
-__global__ void pack_weights_kernel(const float* __restrict__ w, int Ktot, int cout, int BN, int nchunks,
+// packed[nb][c][n][128 B] for n < BN: element kk of chunk c at
+// n*128 + ((kk/8) ^ (n%8))*16 + (kk%8)*2 (Swizzle<3,4,3>), value W[c*64+kk][nb*BN + n]
+__global__ void pack_weights_kernel(const float* __restrict__ w, int Ktot, int cout, int BN, int nchunks, int nblk,
                                     __nv_bfloat16* __restrict__ out) {
-  const long long total = (long long)nchunks * BN * BK;
+  const long long total = (long long)nblk * nchunks * BN * BK;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     int kk = t % BK;
     long long r = t / BK;
     int nn = r % BN;
-    int c = (int)(r / BN);
-    int k = c * BK + kk;
-    float v = (k < Ktot && nn < cout) ? w[(long long)k * cout + nn] : 0.f;
-    long long byte = ((long long)c * BN + nn) * 128 + (((kk >> 3) ^ (nn & 7)) << 4) + (kk & 7) * 2;
+    r /= BN;
+    int c = r % nchunks;
+    int nb = (int)(r / nchunks);
+    int k = c * BK + kk, col = nb * BN + nn;
+    float v = (k < Ktot && col < cout) ? w[(long long)k * cout + col] : 0.f;
+    long long byte = (((long long)nb * nchunks + c) * BN + nn) * 128 + (((kk >> 3) ^ (nn & 7)) << 4) + (kk & 7) * 2;
     out[byte / 2] = __float2bfloat16_rn(v);
   }
 }
@@ -379,35 +557,75 @@ inline int pick_bn(int cout) {
   if (cout <= 32) return 32;
   if (cout <= 64) return 64;
   if (cout <= 128) return 128;
-  if (cout <= 256) return 256;
-  return -1;
+  return 256;
 }
 
-template <int BN>
+inline bool valid_bn(int bn) { return bn == 32 || bn == 64 || bn == 128 || bn == 256; }
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [x_rows, ldx] with a {64, 1} box, 128B swizzle, zero OOB fill
+static int make_xmap(CUtensorMap* m, const Params& p) {
+  auto enc = get_encode();
+  if (!enc) return set_error(FPVS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)p.ldx, (cuuint64_t)p.x_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)p.ldx * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(p.x), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(FPVS_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return FPVS_OK;
+}
+
+template <int BN, bool TMA>
 int launch(const Params& p, cudaStream_t s) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, TMA>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(spconv_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(spconv_tc_kernel<BN, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM);
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     configured = true;
   }
-  int tiles = (p.cap + BM - 1) / BM;
-  int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  alignas(64) CUtensorMap xmap;
+  memset(&xmap, 0, sizeof(xmap));
+  if (TMA) {
+    int rc = make_xmap(&xmap, p);
+    if (rc) return rc;
+  }
+  long long tiles = (long long)((p.cap + BM - 1) / BM) * p.nblk;
+  int grid = tiles < kNumSMs ? (int)tiles : kNumSMs;
   if (grid < 1) grid = 1;
-  spconv_tc_kernel<BN><<<grid, kThreads, C::SMEM, s>>>(p);
+  spconv_tc_kernel<BN, TMA><<<grid, C::THREADS, C::SMEM, s>>>(p, xmap);
   FPVS_CHECK_LAUNCH("spconv_tc");
   return FPVS_OK;
 }
 
-int dispatch(Params& p, cudaStream_t s) {
-  switch (pick_bn(p.cout)) {
-    case 32: return launch<32>(p, s);
-    case 64: return launch<64>(p, s);
-    case 128: return launch<128>(p, s);
-    case 256: return launch<256>(p, s);
+int dispatch(Params& p, int bn, bool allow_tma, cudaStream_t s) {
+  const bool tma = allow_tma && (p.cin % BK) == 0 && (p.ldx % 8) == 0 && p.x_rows > 0;
+#define FPVS_TC_CASE(BNV) \
+  case BNV:               \
+    return tma ? launch<BNV, true>(p, s) : launch<BNV, false>(p, s);
+  switch (bn) {
+    FPVS_TC_CASE(32)
+    FPVS_TC_CASE(64)
+    FPVS_TC_CASE(128)
+    FPVS_TC_CASE(256)
   }
-  return set_error(FPVS_EINVAL, "Cout %d > 256 not supported by the tcgen05 path", p.cout);
+#undef FPVS_TC_CASE
+  return set_error(FPVS_EINVAL, "bad tensor-core tile width %d", bn);
 }
 
 }  // namespace tc
@@ -415,53 +633,78 @@ int dispatch(Params& p, cudaStream_t s) {
 
 using namespace fpvs;
 
-extern "C" size_t fpvs_pack_weights_tc_size(int K, int cin, int cout) {
-  int bn = tc::pick_bn(cout);
-  if (bn < 0 || K < 1 || cin < 1) return 0;
-  size_t nchunks = ((size_t)K * cin + tc::BK - 1) / tc::BK;
-  return nchunks * bn * 128;
+static int resolve_bn(int bn, int cout) {
+  if (bn == 0) bn = tc::pick_bn(cout);
+  return tc::valid_bn(bn) ? bn : -1;
 }
 
-extern "C" int fpvs_pack_weights_tc(const float* w, int K, int cin, int cout, void* packed, void* stream) {
+static bool tma_gather_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    // cp.async producers by default; FPVS_TC_GATHER=tma selects the TMA
+    // tile::gather4 producer (measured slower on B200: the gather4 issue loop
+    // serialises on uniform registers, ~130 cycles per 512 B per SM)
+    const char* e = getenv("FPVS_TC_GATHER");
+    v = (e && e[0] == 't') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+extern "C" size_t fpvs_pack_weights_tc_size(int K, int cin, int cout, int bn) {
+  bn = resolve_bn(bn, cout);
+  if (bn < 0 || K < 1 || cin < 1 || cout < 1) return 0;
+  size_t nchunks = ((size_t)K * cin + tc::BK - 1) / tc::BK;
+  size_t nblk = ((size_t)cout + bn - 1) / bn;
+  return nblk * nchunks * bn * 128;
+}
+
+extern "C" int fpvs_pack_weights_tc(const float* w, int K, int cin, int cout, int bn, void* packed, void* stream) {
   FPVS_CHECK_ARG(w && packed, "null pointer");
-  int bn = tc::pick_bn(cout);
-  FPVS_CHECK_ARG(bn > 0, "Cout %d > 256 not supported by the tcgen05 path", cout);
+  bn = resolve_bn(bn, cout);
+  FPVS_CHECK_ARG(bn > 0, "tile width must be 0 (auto), 32, 64, 128 or 256");
   FPVS_CHECK_ARG(cin % 8 == 0, "tcgen05 path needs Cin %% 8 == 0, got %d", cin);
   int nchunks = (K * cin + tc::BK - 1) / tc::BK;
-  long long total = (long long)nchunks * bn * tc::BK;
-  tc::pack_weights_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(w, K * cin, cout, bn, nchunks,
+  int nblk = (cout + bn - 1) / bn;
+  long long total = (long long)nblk * nchunks * bn * tc::BK;
+  tc::pack_weights_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(w, K * cin, cout, bn, nchunks, nblk,
                                                                               (__nv_bfloat16*)packed);
   FPVS_CHECK_LAUNCH("fpvs_pack_weights_tc");
   return FPVS_OK;
 }
 
-static int tc_common(tc::Params& p, const void* x, int ldx, const int32_t* nbr, int K, const int32_t* n_dev, int cap,
-                     const void* w_packed, const float* bias, int cin, int cout) {
+static int tc_common(tc::Params& p, const void* x, int ldx, int x_rows, const int32_t* nbr, int K,
+                     const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin, int cout,
+                     int bn) {
   FPVS_CHECK_ARG(x && w_packed && n_dev, "null pointer");
   FPVS_CHECK_ARG(K >= 1 && K <= tc::kMaxK, "K must lie in [1, 27]");
   FPVS_CHECK_ARG(nbr || K == 1, "nbr may be NULL only for K == 1");
-  FPVS_CHECK_ARG(cin % 8 == 0 && ldx % 8 == 0, "tcgen05 path needs Cin and ldx multiples of 8");
-  FPVS_CHECK_ARG(tc::pick_bn(cout) > 0, "Cout %d > 256 not supported", cout);
+  FPVS_CHECK_ARG(cin % 8 == 0 && ldx % 8 == 0 && ldx >= cin, "tcgen05 path needs Cin and ldx multiples of 8");
+  FPVS_CHECK_ARG(cout >= 1 && cout <= 1024, "bad Cout %d", cout);
+  FPVS_CHECK_ARG(x_rows >= 1, "x_rows must be positive");
   p = tc::Params{};
   p.x = (const __nv_bfloat16*)x;
   p.ldx = ldx;
+  p.x_rows = x_rows;
   p.nbr = nbr;
   p.K = K;
   p.n_dev = n_dev;
   p.cap = cap;
   p.wpk = (const uint8_t*)w_packed;
   p.nchunks = (K * cin + tc::BK - 1) / tc::BK;
+  p.nblk = (cout + bn - 1) / bn;
   p.bias = bias;
   p.cin = cin;
   p.cout = cout;
   return FPVS_OK;
 }
 
-extern "C" int fpvs_spconv_tc(const void* x, int ldx, const int32_t* nbr, int K, const int32_t* n_out_dev,
-                              int cap_out, const void* w_packed, const float* bias, int cin, int cout, int act, void* y,
-                              int ldy, int col_off, void* stream) {
+extern "C" int fpvs_spconv_tc(const void* x, int ldx, int x_rows, const int32_t* nbr, int K, const int32_t* n_out_dev,
+                              int cap_out, const void* w_packed, int bn, const float* bias, int cin, int cout, int act,
+                              void* y, int ldy, int col_off, void* stream) {
   tc::Params p;
-  int rc = tc_common(p, x, ldx, nbr, K, n_out_dev, cap_out, w_packed, bias, cin, cout);
+  bn = resolve_bn(bn, cout);
+  FPVS_CHECK_ARG(bn > 0, "tile width must be 0 (auto), 32, 64, 128 or 256");
+  int rc = tc_common(p, x, ldx, x_rows, nbr, K, n_out_dev, cap_out, w_packed, bias, cin, cout, bn);
   if (rc) return rc;
   FPVS_CHECK_ARG(y, "null output");
   FPVS_CHECK_ARG(cout % 32 == 0, "tcgen05 store epilogue needs Cout %% 32 == 0, got %d", cout);
@@ -472,15 +715,17 @@ extern "C" int fpvs_spconv_tc(const void* x, int ldx, const int32_t* nbr, int K,
   p.y = (__nv_bfloat16*)y;
   p.ldy = ldy;
   p.col_off = col_off;
-  return tc::dispatch(p, as_stream(stream));
+  return tc::dispatch(p, bn, tma_gather_enabled(), as_stream(stream));
 }
 
-extern "C" int fpvs_head_tc(const void* x, int ldx, const int32_t* coords, const int32_t* n_dev, int cap,
+extern "C" int fpvs_head_tc(const void* x, int ldx, int x_rows, const int32_t* coords, const int32_t* n_dev, int cap,
                             const void* w_packed, const float* bias, int cin, int d, int B, int Nx, int Ny, int Nz,
                             float tau, uint8_t* out_bits, float* probs, float* logits, void* stream) {
   tc::Params p;
   const int d3 = d * d * d;
-  int rc = tc_common(p, x, ldx, nullptr, 1, n_dev, cap, w_packed, bias, cin, d3);
+  FPVS_CHECK_ARG(d3 <= 256, "head supports d^3 <= 256");
+  const int bn = tc::pick_bn(d3);
+  int rc = tc_common(p, x, ldx, x_rows, nullptr, 1, n_dev, cap, w_packed, bias, cin, d3, bn);
   if (rc) return rc;
   FPVS_CHECK_ARG(coords, "null coords");
   FPVS_CHECK_ARG(Nx % 8 == 0, "N_x must be divisible by 8");
@@ -489,6 +734,10 @@ extern "C" int fpvs_head_tc(const void* x, int ldx, const int32_t* coords, const
   p.head = 1;
   p.coords = (const int4*)coords;
   p.d = d;
+  p.dlog = (d & (d - 1)) == 0 ? __builtin_ctz(d) : -1;
+  // logit(tau) for the fast threshold; tau outside (0, 1) takes the sigmoid path
+  p.zt = (tau > 0.f && tau < 1.f) ? (float)log((double)tau / (1.0 - (double)tau)) : 0.f;
+  if (!(tau > 0.f && tau < 1.f)) p.dlog = -1;
   p.Nx = Nx;
   p.Ny = Ny;
   p.Nz = Nz;
@@ -496,5 +745,5 @@ extern "C" int fpvs_head_tc(const void* x, int ldx, const int32_t* coords, const
   p.out_bits = out_bits;
   p.probs = probs;
   p.logits = logits;
-  return tc::dispatch(p, as_stream(stream));
+  return tc::dispatch(p, bn, tma_gather_enabled(), as_stream(stream));
 }

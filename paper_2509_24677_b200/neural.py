@@ -222,33 +222,51 @@ class Conv3d:
     def invalidate(self):
         self._packed = None
 
-    def packed(self, stream=None):
-        if self._packed is None:
-            self._packed = pack_tc(self.w, self.taps, self.spec.in_channels, self.spec.out_channels, stream)
-        return self._packed
+    def packed(self, bn: int = 0, stream=None):
+        return packed_cache(self, bn, stream)
 
 
-def pack_tc(w, taps: int, cin: int, cout: int, stream=None):
+def packed_cache(layer, bn: int = 0, stream=None):
+    """The layer's bf16 weight image for tile width ``bn`` (built once per bn)."""
+    if layer._packed is None:
+        layer._packed = {}
+    if bn not in layer._packed:
+        layer._packed[bn] = pack_tc(layer.w, layer.taps, layer.spec.in_channels, layer.spec.out_channels, bn, stream)
+    return layer._packed[bn]
+
+
+def pack_tc(w, taps: int, cin: int, cout: int, bn: int = 0, stream=None):
     torch = _torch()
-    nbytes = _lib.size("fpvs_pack_weights_tc_size", taps, cin, cout)
+    nbytes = _lib.size("fpvs_pack_weights_tc_size", taps, cin, cout, bn)
     if nbytes == 0:
-        raise ValueError(f"no tensor-core packing for taps={taps}, Cin={cin}, Cout={cout}")
+        raise ValueError(f"no tensor-core packing for taps={taps}, Cin={cin}, Cout={cout}, bn={bn}")
     out = torch.empty(nbytes, dtype=torch.uint8, device=w.device)
-    _lib.call("fpvs_pack_weights_tc", _lib.ptr(w.contiguous()), taps, cin, cout, _lib.ptr(out),
+    _lib.call("fpvs_pack_weights_tc", _lib.ptr(w.contiguous()), taps, cin, cout, bn, _lib.ptr(out),
               _lib.stream_ptr(stream))
     return out
 
 
+def pick_bn(cout: int, rows: int, sms: int = 148) -> int:
+    """Output-tile width: split N until the layer has >= one wave of 128-row tiles."""
+    bn = 32 if cout <= 32 else 64 if cout <= 64 else 128 if cout <= 128 else 256
+    mtiles = max(1, (rows + 127) // 128)
+    # splitting N re-gathers A once per column block; measured on B200 it only
+    # pays when the layer has well under half a wave of row tiles
+    while bn > 64 and mtiles * ((cout + bn - 1) // bn) < sms // 4:
+        bn //= 2
+    return bn
+
+
 def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int, col_off: int = 0,
-             precision: str = "fp32", act: str | None = None, stream=None):
+             precision: str = "fp32", act: str | None = None, stream=None, bn: int = 0):
     """One sparse conv launch: y[:, col_off:col_off+Cout] = act(gather-GEMM(x, table) + b)."""
     torch = _torch()
     spec = layer.spec
     a = _lib.ACT[act or spec.activation]
     s = _lib.stream_ptr(stream)
     if precision == "bf16":
-        _lib.call("fpvs_spconv_tc", _lib.ptr(x), ldx, _lib.ptr(table), K, _lib.ptr(n), cap,
-                  _lib.ptr(layer.packed(stream)), _lib.ptr(layer.b), spec.in_channels, spec.out_channels, a,
+        _lib.call("fpvs_spconv_tc", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), K, _lib.ptr(n), cap,
+                  _lib.ptr(layer.packed(bn, stream)), bn, _lib.ptr(layer.b), spec.in_channels, spec.out_channels, a,
                   _lib.ptr(y), ldy, col_off, s)
     else:
         idt = _lib.BF16 if x.dtype == torch.bfloat16 else _lib.F32
@@ -266,8 +284,8 @@ def run_head(layer: Conv3d, x, ldx: int, lv: sp.Level, d: int, grid_dims, tau: f
     s = _lib.stream_ptr(stream)
     spec = layer.spec
     if precision == "bf16":
-        _lib.call("fpvs_head_tc", _lib.ptr(x), ldx, _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap,
-                  _lib.ptr(layer.packed(stream)), _lib.ptr(layer.b), spec.in_channels, d, lv.B, nx, ny, nz,
+        _lib.call("fpvs_head_tc", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap,
+                  _lib.ptr(layer.packed(0, stream)), _lib.ptr(layer.b), spec.in_channels, d, lv.B, nx, ny, nz,
                   float(tau), _lib.ptr(out_bits), _lib.ptr(probs), _lib.ptr(logits), s)
     else:
         idt = _lib.BF16 if x.dtype == torch.bfloat16 else _lib.F32

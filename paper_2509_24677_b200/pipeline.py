@@ -109,9 +109,11 @@ class FramePipeline:
     def load(self, bits):
         self.in_bits.copy_(bits, non_blocking=True)
 
-    def capture(self):
-        """Warm up eagerly once, then capture the frame into a CUDA graph."""
+    def capture(self, tune: bool = True):
+        """Tune tile widths on the loaded frame, warm up eagerly, capture a CUDA graph."""
         torch = _torch()
+        if tune and hasattr(self.plan, "tune"):
+            self.plan.tune(self.in_bits)
         self.plan.run(self.in_bits, self.out_bits, self.tau)
         torch.cuda.synchronize()
         if not self._use_graph:

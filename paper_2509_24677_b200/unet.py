@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _lib
 from . import sparse as sp
-from .neural import pack_tc, run_conv, run_head
+from .neural import packed_cache, pick_bn, run_conv, run_head
 
 
 def _torch():
@@ -62,12 +62,9 @@ class SparseLayer:
         self.w = torch.as_tensor(np.asarray(w, np.float32)).to(device).contiguous()
         self.b = torch.as_tensor(np.asarray(b, np.float32)).to(device).contiguous()
         self._packed = None
-        self._w_bf16r = None
 
-    def packed(self, stream=None):
-        if self._packed is None:
-            self._packed = pack_tc(self.w, self.taps, self.spec.in_channels, self.spec.out_channels, stream)
-        return self._packed
+    def packed(self, bn: int = 0, stream=None):
+        return packed_cache(self, bn, stream)
 
 
 class PvsUNet:
@@ -128,6 +125,20 @@ class UNetPlan:
         self.t0a, self.t0b, self.buf0 = e(k0, c0), e(k0, c0), e(k0, 2 * c0)
         self.t1a, self.t1b, self.buf1 = e(k1, c1), e(k1, c1), e(k1, 2 * c1)
         self.t2a, self.t2b = e(k2, c2), e(k2, c2)
+        self.bn = {}  # per-layer output-tile width (0 = auto from Cout); see tune()
+
+    def tune(self, bits):
+        """Pick per-layer tile widths from one frame's active counts (one host sync).
+
+        Layers whose rows make fewer than one wave of 128-row tiles split N
+        across CTAs; reuse the plan for frames of similar occupancy.
+        """
+        self.build_maps(bits)
+        n0, n1, n2 = self.counts()
+        rows = {"enc0a": n0, "enc0b": n0, "down01": n1, "enc1a": n1, "enc1b": n1, "down12": n2, "enc2a": n2,
+                "enc2b": n2, "up21": n1, "dec1a": n1, "dec1b": n1, "up10": n0, "dec0a": n0, "dec0b": n0}
+        self.bn = {k: pick_bn(self.net.layers[k].spec.out_channels, v) for k, v in rows.items()}
+        return self.bn
 
     def build_maps(self, bits):
         sp.fill_level_from_bits(self.L0, bits, self.grid_dims, self.net.d)
@@ -152,7 +163,7 @@ class UNetPlan:
 
         def conv(name, x, ldx, table, K, lv, y, ldy, off=0):
             _ev(events, name)
-            run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu")
+            run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu", bn=self.bn.get(name, 0))
 
         d3 = net.d ** 3
         conv("enc0a", self.x0, d3, L0.nbr, 27, L0, self.t0a, c0)

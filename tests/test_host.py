@@ -34,8 +34,10 @@ def test_library_exports_every_header_symbol():
     lib = _lib.load()
     assert lib.fpvs_abi_version() == 1
     # size queries are pure host arithmetic
-    assert _lib.size("fpvs_pack_weights_tc_size", 27, 64, 64) == 27 * 64 * 128
-    assert _lib.size("fpvs_pack_weights_tc_size", 27, 8, 32) == 4 * 32 * 128
+    assert _lib.size("fpvs_pack_weights_tc_size", 27, 64, 64, 0) == 27 * 64 * 128
+    assert _lib.size("fpvs_pack_weights_tc_size", 27, 8, 32, 0) == 4 * 32 * 128
+    assert _lib.size("fpvs_pack_weights_tc_size", 27, 256, 256, 64) == 4 * 108 * 64 * 128
+    assert _lib.size("fpvs_pack_weights_tc_size", 27, 64, 64, 48) == 0
     assert _lib.size("fpvs_kmap_workspace_size", 1, 64, 64, 64) > 0
 
 
@@ -44,7 +46,7 @@ def test_argument_errors_map_to_valueerror():
     with pytest.raises(ValueError, match="divide"):
         _lib.call("fpvs_interleave", 1, 0, 1, 6, 4, 4, 4, 1, 0, None, None)
     with pytest.raises(ValueError):
-        _lib.call("fpvs_spconv_tc", 1, 64, None, 27, 1, 10, 1, None, 64, 64, 1, 1, 64, 0, None)
+        _lib.call("fpvs_spconv_tc", 1, 64, 10, None, 27, 1, 10, 1, 0, None, 64, 64, 1, 1, 64, 0, None)
 
 
 # -------------------------------------------------------- FPVS boundary format

@@ -1,0 +1,22 @@
+"""Run config-2 frames eagerly (for ncu captures of individual kernels)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2509_24677_b200 import synth  # noqa: E402
+from paper_2509_24677_b200.froxel import FroxelGrid  # noqa: E402
+from paper_2509_24677_b200.unet import PvsUNet  # noqa: E402
+
+frames = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+occ = synth.config2_grid(1)
+bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+net = PvsUNet(seed=1, precision="bf16")
+plan = net.plan(1, occ.shape)
+out = torch.empty(occ.size // 8, dtype=torch.uint8, device="cuda")
+for _ in range(frames):
+    plan.run(bits, out, 0.5)
+torch.cuda.synchronize()
+print("frames ok", plan.counts())
