@@ -3,30 +3,28 @@
 // Implicit gather-GEMM-scatter.  An output tile is BM = 128 active cells x BN
 // output channels.  K is the flattened (offset j, channel ci) index
 // k = j*Cin + ci of the reference weight rows (neural.py:163-166), cut into
-// 64-element (128-byte) chunks.  Per chunk:
-//   * A (128 x 64 bf16) is GATHERED: row i of the tile is x[nbr[i][j]].
-//     - Cin % 64 == 0 (every config-2 layer): one producer warp issues 32
-//       TMA `tile::gather4` copies (4 rows x 128 B each) into the 128B-swizzled
-//       K-major layout the UMMA descriptor reads; a missing neighbour (-1) is
-//       an out-of-bounds row, which TMA zero-fills.  32 instructions move 16 KB.
-//     - Cin < 64 (8 / 32 channels, config 1): four producer warps gather
-//       16-byte pieces with cp.async (zero-fill via src-size 0), one chunk
-//       spanning 64/Cin offsets.
+// 64-element (128-byte) chunks; a pipeline stage holds G chunks.  Per chunk:
+//   * A (128 x 64 bf16) is GATHERED: row i of the tile is x[nbr[i][j]].  Eight
+//     producer warps issue 16-byte cp.async pieces straight into the
+//     128B-swizzled K-major layout the UMMA descriptor reads; a missing
+//     neighbour (-1) is a zero-fill.  For Cin < 64 one chunk spans 64/Cin
+//     offsets.  (A TMA tile::gather4 producer was measured slower on B200:
+//     ~130 cycles per 512-byte gather per SM.)
 //   * B (BN x 64 bf16): one bulk copy (cp.async.bulk, TMA engine) of the
 //     pre-swizzled weight image from fpvs_pack_weights_tc.
-//   * one elected thread issues 4 x tcgen05.mma (M=128, N=BN, K=16, bf16 ->
-//     fp32) into a TMEM accumulator; tcgen05.commit frees the stage.  Chunks
-//     whose offsets have no neighbour anywhere in the tile are skipped.
+//   * one elected thread issues 4 x tcgen05.mma per chunk (M=128, N=BN, K=16,
+//     bf16 -> fp32) into a TMEM accumulator; tcgen05.commit frees the stage.
+//     Offsets with no neighbour anywhere in the tile are skipped.
 //   * 4 epilogue warps drain TMEM (tcgen05.ld) from a double-buffered
 //     accumulator (2 x BN columns) so the epilogue of tile t overlaps the
 //     mainloop of tile t+1, and fuse bias + ReLU + bf16 cast, or for the
-//     head sigmoid + [p >= tau] + the deinterleave bit-pack.
-// Each tile's neighbour rows are prefetched one tile ahead (double-buffered).
-// Layers with few row tiles (coarse U-Net levels) split N across CTAs
-// (BN < Cout) so all 148 SMs get work.  The grid is persistent (<= 148 CTAs)
-// and reads the active row count from device memory (graph-capturable).
-#include <cuda.h>
-#include <cudaTypedefs.h>
+//     head sigmoid-threshold + the deinterleave bit-pack.
+// Stage arrivals are per warp and lag the copies (cp.async.wait_group), so a
+// stage costs 9 mbarrier arrivals instead of one per thread.  Each tile's
+// neighbour rows are prefetched one tile ahead (double-buffered).  Layers
+// with very few row tiles can split N across CTAs (BN < Cout).  The grid is
+// persistent (<= 148 CTAs) and reads the active row count from device memory
+// (graph-capturable).
 #include <math.h>
 #include <string.h>
 
@@ -61,26 +59,44 @@ struct Params {
   uint8_t* out_bits;
   float* probs;
   float* logits;
+  int dbg;  // profiling knob (FPVS_TC_DEBUG): 1 = no MMA, 2 = no A gather, 4 = no B copy
 };
 
-template <int BN, bool TMA>
+template <int BN, int G, int PW = 8, int MINB = 1>
 struct Cfg {
-  static constexpr int P = TMA ? 1 : 8;         // producer warps
-  static constexpr int MMA_WARP = P;
-  static constexpr int THREADS = (P + 5) * 32;  // producers, MMA, 4 epilogue warps
+  static constexpr int P = PW;                  // A-gather warps
+  static constexpr int BW_WARP = P;             // B loader + stage bookkeeping
+  static constexpr int MMA_WARP = P + 1;
+  static constexpr int THREADS = (P + 6) * 32;  // + 4 epilogue warps
   static constexpr int PROD = P * 32;
-  static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int B_SUB = BN * 128;        // one 64-wide K chunk of B
+  static constexpr int STAGE_A = G * A_BYTES;   // G K-chunks per pipeline stage
+  static constexpr int STAGE_B = G * B_SUB;
+  static constexpr int STAGE_BYTES = STAGE_A + STAGE_B;
   static constexpr int NBR_BYTES = 2 * BM * kMaxK * 4;  // double-buffered neighbour tile
-  static constexpr int kStageBudget = 232448 - 1024 - NBR_BYTES - 2048;
+  static constexpr int kStageBudget = 232448 / MINB - 1024 - NBR_BYTES - 6144;
   static constexpr int STAGES = kStageBudget / STAGE_BYTES > 8 ? 8 : kStageBudget / STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128
                                  : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES + NBR_BYTES;
-  static constexpr int BIAS_OFF = BAR_OFF + 8 * (2 * STAGES + 6) + 64 + 4 * STAGES;
+  static constexpr int CTRL_OFF = BAR_OFF + 8 * (2 * STAGES + 6);  // tmem addr, masks, stage info, chunk list
+  static constexpr int BIAS_OFF = CTRL_OFF + 128 + 4 * 256;  // + two 128-entry chunk lists
   static constexpr int SMEM = 1024 + BIAS_OFF + 4 * 1024 + 16;
-  static_assert(SMEM <= 232448, "shared memory budget");
+  static_assert(STAGES >= 2, "pipeline needs two stages");
+  static_assert(SMEM * MINB <= 232448, "shared memory budget");
 };
+
+// ---------------- profiling timestamps (FPVS_TC_DEBUG & 16) ----------------
+__device__ unsigned long long g_dbg_ts[2][4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TS(slot)                                                              \
+  do {                                                                        \
+    if ((p.dbg & 16) && blockIdx.x < 2 && (slot) < 4096) g_dbg_ts[blockIdx.x][(slot)] = gtimer(); \
+  } while (0)
 
 // ---------------- PTX wrappers ----------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -98,6 +114,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Same wait, but the thread sleeps in the barrier unit until the phase
+// completes (suspend-time hint) instead of re-issuing try_wait: waiting warps
+// stop stealing issue slots from the producer warps.
+__device__ __forceinline__ void mbar_sleep_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -109,18 +137,20 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
-// TMA gather of 4 rows (row coordinates r0..r3, column c0) of a 2-D tensor
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const void* tmap, int c0, int r0, int r1, int r2, int r3,
-                                            uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-      "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
-      : "memory");
-}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
+// 16-byte cp.async; when `skip` the source is ignored and zeros are written
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, bool skip) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+      "cp.async.cg.shared.global [%0], [%1], 16, p;\n}\n" ::"r"(dst),
+      "l"(src), "r"((int)skip)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -213,16 +243,15 @@ __device__ __forceinline__ void prefetch_nbr(const Params& p, int row0, uint32_t
   cp_async_mbar_arrive_noinc(bar);
 }
 
-template <int BN, bool TMA>
-__global__ void __launch_bounds__(Cfg<BN, TMA>::THREADS, 1)
-    spconv_tc_kernel(const Params p, const __grid_constant__ CUtensorMap xmap) {
-  using C = Cfg<BN, TMA>;
+template <int BN, int G, int PW, int MINB>
+__global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc_kernel(const Params p) {
+  using C = Cfg<BN, G, PW, MINB>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // pointers stay derived from the __shared__ array (LDS/STS, not generic)
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * A_BYTES;
+  uint8_t* sA = smem;                              // [STAGES][G][16 KB]
+  uint8_t* sB = smem + C::STAGES * C::STAGE_A;     // [STAGES][G][B_SUB]
   int* s_nbr = reinterpret_cast<int*>(smem + C::STAGES * C::STAGE_BYTES);  // 2 x BM*K
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* full = bars;
@@ -230,24 +259,27 @@ __global__ void __launch_bounds__(Cfg<BN, TMA>::THREADS, 1)
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* nbar = tempty + 2;  // neighbour-tile prefetch, 2 buffers
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(nbar + 2);
-  uint32_t* s_mask = s_tmem + 1;   // up to 4 producer-warp masks
-  uint32_t* s_info = s_tmem + 16;  // per-stage flags (bit0 first, bit1 last)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::CTRL_OFF);
+  uint32_t* s_mask = s_tmem + 1;   // producer-warp offset masks (8)
+  int* s_cnt = reinterpret_cast<int*>(s_tmem + 10);  // chunks of the m-tile (2 buffers)
+  uint32_t* s_info = s_tmem + 16;  // per stage: bit0 first, bit1 last, bits 2+ = chunks in stage
+  int* s_cl0 = reinterpret_cast<int*>(s_tmem + 32);  // chunk lists (2 x 128): jbase | cibase << 8 | c << 16
   float* s_bias = reinterpret_cast<float*>(smem + C::BIAS_OFF);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) TS(0);
   const int n = min(*p.n_dev, p.cap);
   const int mtiles = (n + BM - 1) / BM;
   const int ntiles = mtiles * p.nblk;
 
   if (tid == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(smem_u32(full + s), TMA ? 1 : C::PROD + 1);
+      mbar_init(smem_u32(full + s), C::PROD + 1);  // async arrival per A thread + the B loader's expect_tx
       mbar_init(smem_u32(empty + s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(tfull + a), 1);
-      mbar_init(smem_u32(tempty + a), 128);
+      mbar_init(smem_u32(tempty + a), 4);  // one arrival per epilogue warp
       mbar_init(smem_u32(nbar + a), C::PROD);
     }
     fence_mbar_init();
@@ -263,149 +295,176 @@ __global__ void __launch_bounds__(Cfg<BN, TMA>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
+  if (tid == 0) TS(1);
 
   if (warp < C::P) {
-    // ===================== gather producers =====================
-    int stage = 0;
-    uint32_t phase = 0;
+    // ===================== A-gather warps =====================
+    // Each thread owns NPT fixed rows and one 16-byte column slot of the
+    // 128B-swizzled A chunk.  Per chunk: NPT shared loads of neighbour rows,
+    // NPT cp.async (zero-fill for missing rows) — no per-thread special cases.
+    constexpr int RSTEP = C::PROD / 8;
+    constexpr int NPT = BM / RSTEP;  // cp.async ops per thread per chunk
     const int nbr_elems = BM * p.K;
-    const int ptid = tid;  // 0 .. PROD-1
-    // chunk <-> (offset, channel) maps without runtime division: Cin >= 64
-    // gives cpo = Cin/64 chunks per offset, Cin < 64 gives opc = 64/Cin
-    // offsets per chunk (Cin is a multiple of 8; both are exact here)
+    const int ptid = tid;
     const int cpo = p.cin >= BK ? p.cin / BK : 1;
     const int opc = p.cin >= BK ? 1 : BK / p.cin;
-    const int ppo = p.cin >> 3;  // 16-byte pieces per offset
-    // neighbour rows depend only on the m-tile; consecutive n-blocks reuse them
-    int cur_m = -1, lt = 0, buf = 1;
-    if (p.nbr && (int)blockIdx.x < ntiles)
-      prefetch_nbr(p, ((int)blockIdx.x / p.nblk) * BM, smem_u32(s_nbr), smem_u32(nbar), ptid, C::PROD);
-    // cp.async thread geometry: piece = 16-byte column slot, rows r_i = rbase + i*RSTEP
-    constexpr int RSTEP = C::PROD / 8;
-    constexpr int NPT = BM / RSTEP;  // rows (cp.async ops) per thread per chunk
+    const int ppo = p.cin >> 3;
+    const uint32_t ldx2 = (uint32_t)p.ldx * 2u;  // row pitch in bytes (host checks x < 2^31 B)
     const int piece = ptid & 7, rbase = ptid >> 3;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int mt = tile / p.nblk, nb = tile - mt * p.nblk;
+    const int tj = opc == 1 ? 0 : piece / ppo;                     // offset delta of my column slot
+    const int tci = opc == 1 ? piece * 8 : (piece - tj * ppo) * 8;  // channel of my column slot
+    int rowk[NPT];
+    uint32_t dsto[NPT];
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) {
+      const int r = rbase + i * RSTEP;
+      rowk[i] = r * p.K;
+      dsto[i] = r * 128 + ((piece ^ (r & 7)) << 4);
+    }
+    const bool ident = p.nbr == nullptr;
+    int stage = 0;
+    uint32_t phase = 0;
+    int cur_m = -1, lt = 0, buf = 1, nissue = 0;
+    if (!ident && (int)blockIdx.x < ntiles)
+      prefetch_nbr(p, ((int)blockIdx.x / p.nblk) * BM, smem_u32(s_nbr), smem_u32(nbar), ptid, C::PROD);
+    int ltile = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ltile) {
+      const int mt = tile / p.nblk;
       const int row0 = mt * BM;
+      if (ptid == 0) TS(8 + 8 * ltile);
       if (mt != cur_m) {
         buf ^= 1;
-        if (p.nbr) mbar_wait(smem_u32(nbar + buf), (lt >> 1) & 1);
+        if (!ident) mbar_wait(smem_u32(nbar + buf), (lt >> 1) & 1);
         ++lt;
         cur_m = mt;
-        if (C::P > 1) named_bar(1, C::PROD); else __syncwarp();
-        // prefetch the next distinct m-tile this CTA will visit into the other buffer
+        named_bar(1, C::PROD);
         int nt = tile + gridDim.x;
         while (nt < ntiles && nt / p.nblk == mt) nt += gridDim.x;
-        if (p.nbr && nt < ntiles)
+        if (!ident && nt < ntiles)
           prefetch_nbr(p, (nt / p.nblk) * BM, smem_u32(s_nbr + (buf ^ 1) * nbr_elems), smem_u32(nbar + (buf ^ 1)),
                        ptid, C::PROD);
-      }
-      const int* nb_s = s_nbr + buf * nbr_elems;
-      // per-tile offset mask: OR of "neighbour j present" over the tile's rows
-      uint32_t m = 0;
-      for (int r = ptid; r < BM; r += C::PROD) {
-        if (row0 + r >= n) continue;
-        if (p.nbr) {
-          for (int j = 0; j < p.K; ++j) m |= (nb_s[r * p.K + j] >= 0 ? 1u : 0u) << j;
-        } else {
-          m |= 1u;
+        // offset-presence mask over live rows; rows past n become -1
+        int* nbv = s_nbr + buf * nbr_elems;
+        uint32_t m = 0;
+        for (int r = ptid; r < BM; r += C::PROD) {
+          const bool live = row0 + r < n;
+          if (!ident) {
+            for (int j = 0; j < p.K; ++j) {
+              const int v = live ? nbv[r * p.K + j] : -1;
+              if (!live) nbv[r * p.K + j] = -1;
+              m |= (v >= 0 ? 1u : 0u) << j;
+            }
+          } else if (live) {
+            m = 1u;
+          }
         }
-      }
-      m = __reduce_or_sync(0xffffffffu, m);
-      uint32_t tmask = m;
-      if (C::P > 1) {
+        m = __reduce_or_sync(0xffffffffu, m);
         if (lane == 0) s_mask[warp] = m;
         named_bar(1, C::PROD);
-        tmask = 0;
-        for (int w = 0; w < C::P; ++w) tmask |= s_mask[w];
-        named_bar(1, C::PROD);
-      }
-      if (tmask == 0) tmask = 1u;  // keep the pipeline shape: one (zero) chunk
-      // chunks to issue: for Cin >= 64 every ci-chunk of each present offset;
-      // for Cin < 64 every chunk whose offset group has a present offset
-      const uint32_t gmask = (opc >= 32) ? 0xffffffffu : ((1u << opc) - 1u);
-      int nissue;
-      if (opc == 1) {
-        nissue = __popc(tmask) * cpo;
-      } else {
-        nissue = 0;
-        for (int c = 0; c < p.nchunks; ++c) nissue += ((tmask >> (c * opc)) & gmask) ? 1 : 0;
-      }
-      // per-thread row geometry for this tile (cp.async path)
-      int rowk[NPT];
-      uint32_t dsto[NPT];
-      bool rok[NPT];
-#pragma unroll
-      for (int i = 0; i < NPT; ++i) {
-        const int r = rbase + i * RSTEP;
-        rowk[i] = r * p.K;
-        rok[i] = row0 + r < n;
-        dsto[i] = r * 128 + ((piece ^ (r & 7)) << 4);
-      }
-      const uint8_t* wblk = p.wpk + (size_t)nb * p.nchunks * C::B_BYTES;
-      uint32_t rem = tmask;
-      int j = -1, cc = cpo;  // current offset / ci-chunk for opc == 1
-      int cg = -1;           // current chunk for opc > 1
-      for (int q = 0; q < nissue; ++q) {
-        int c;
-        if (opc == 1) {
-          if (++cc >= cpo) { cc = 0; j = __ffs(rem) - 1; rem &= rem - 1; }
-          c = j * cpo + cc;
-        } else {
-          do { ++cg; } while (!((tmask >> (cg * opc)) & gmask));
-          c = cg;
-        }
-        mbar_wait(smem_u32(empty + stage), phase ^ 1);
-        const uint32_t fb = smem_u32(full + stage);
-        const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
-        const uint32_t info = (q == 0 ? 1u : 0u) | (q == nissue - 1 ? 2u : 0u);
-        if constexpr (TMA) {
-          if (lane == 0) {
-            s_info[stage] = info;
-            mbar_arrive_expect_tx(fb, A_BYTES + C::B_BYTES);
-          }
-          __syncwarp();
-          const int ci0 = cc * BK;
-          int rr[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int r = lane * 4 + t;
-            int src = -1;
-            if (row0 + r < n) src = p.nbr ? nb_s[r * p.K + j] : row0 + r;
-            rr[t] = src >= 0 ? src : p.x_rows;  // out-of-bounds row -> TMA zero fill
-          }
-          tma_gather4(a_base + lane * 512, &xmap, ci0, rr[0], rr[1], rr[2], rr[3], fb);
-          if (lane == 0) bulk_g2s(smem_u32(sB + stage * C::B_BYTES), wblk + (size_t)c * C::B_BYTES, C::B_BYTES, fb);
-        } else {
-          if (ptid == 0) {
-            s_info[stage] = info;
-            mbar_arrive_expect_tx(fb, C::B_BYTES);
-            bulk_g2s(smem_u32(sB + stage * C::B_BYTES), wblk + (size_t)c * C::B_BYTES, C::B_BYTES, fb);
-          }
-          int jj, ci;
+        int* s_cl = s_cl0 + (lt & 1) * 128;
+        if (ptid == 0) {
+          uint32_t tmask = 0;
+          for (int w = 0; w < C::P; ++w) tmask |= s_mask[w];
+          if (!tmask) tmask = 1u;  // keep the pipeline shape: one (zero) chunk
+          int k = 0;
           if (opc == 1) {
-            jj = j;
-            ci = cc * BK + piece * 8;
+            for (uint32_t rm = tmask; rm; rm &= rm - 1) {
+              const int j = __ffs(rm) - 1;
+              for (int cc = 0; cc < cpo; ++cc) s_cl[k++] = j | ((cc * BK) << 8) | ((j * cpo + cc) << 16);
+            }
           } else {
-            const int g = piece + (c * opc) * ppo;  // piece index along K (ppo pieces per offset)
-            jj = g / ppo;
-            ci = (g - jj * ppo) * 8;
+            const uint32_t gm = (1u << opc) - 1u;
+            for (int c = 0; c < p.nchunks; ++c)
+              if ((tmask >> (c * opc)) & gm) s_cl[k++] = (c * opc) | (c << 16);
           }
-          const bool jok = jj < p.K;
-          int src[NPT];
-#pragma unroll
-          for (int i = 0; i < NPT; ++i) {
-            src[i] = -1;
-            if (jok && rok[i]) src[i] = p.nbr ? nb_s[rowk[i] + jj] : row0 + rbase + i * RSTEP;
-          }
-#pragma unroll
-          for (int i = 0; i < NPT; ++i) {
-            const bool ok = src[i] >= 0;
-            const __nv_bfloat16* gp = p.x + (ok ? (long long)src[i] * p.ldx + ci : 0);
-            cp_async16(a_base + dsto[i], gp, ok ? 16u : 0u);
-          }
-          cp_async_mbar_arrive_noinc(fb);
+          s_cnt[lt & 1] = k;
         }
+        // publish the chunk list to the B-loader warp as well
+        named_bar(2, C::PROD + 32);
+        nissue = s_cnt[lt & 1];
+      }
+      if (ptid == 0) TS(9 + 8 * ltile);
+      const int* nb_s = s_nbr + buf * nbr_elems;
+      const int* s_cl = s_cl0 + (lt & 1) * 128;
+      const int nst = (nissue + G - 1) / G;
+      for (int st = 0; st < nst; ++st) {
+        const int nvalid = min(G, nissue - st * G);
+        mbar_wait(smem_u32(empty + stage), phase ^ 1);
+        const uint32_t a_stage = smem_u32(sA + stage * C::STAGE_A);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          if (g >= nvalid) break;
+          const int e = s_cl[st * G + g];
+          const int jj = (e & 0xff) + tj;
+          const uint32_t ci2 = (uint32_t)(((e >> 8) & 0xff) + tci) * 2u;
+          const uint32_t a_sub = a_stage + g * A_BYTES;
+          const char* base = reinterpret_cast<const char*>(p.x) + ci2;
+          uint32_t off[NPT];
+          bool skip[NPT];
+          if (!ident) {
+            const bool jk = jj < p.K;
+#pragma unroll
+            for (int i = 0; i < NPT; ++i) {
+              const int v = jk ? nb_s[rowk[i] + jj] : -1;
+              skip[i] = v < 0;
+              off[i] = skip[i] ? 0u : (uint32_t)v * ldx2;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < NPT; ++i) {
+              const int row = row0 + rbase + i * RSTEP;
+              skip[i] = row >= n;
+              off[i] = skip[i] ? 0u : (uint32_t)row * ldx2;
+            }
+          }
+          if (!(p.dbg & 2)) {
+#pragma unroll
+            for (int i = 0; i < NPT; ++i) cp_async16_zfill(a_sub + dsto[i], base + off[i], skip[i]);
+          }
+        }
+        // asynchronous arrival once this thread's copies of the stage land
+        // (the MMA issuer fences the generic->async proxy after its wait)
+        cp_async_mbar_arrive_noinc(smem_u32(full + stage));
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (ptid == 0) TS(10 + 8 * ltile);
+    }
+  } else if (warp == C::BW_WARP) {
+    // ===================== B loader (one elected lane) =====================
+    // Streams the weight chunks of each stage with bulk copies (TMA engine)
+    // and writes the stage flags the MMA issuer reads.
+    int stage = 0;
+    uint32_t phase = 0;
+    int cur_m = -1, nissue = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int mt = tile / p.nblk, nb = tile - mt * p.nblk;
+      if (mt != cur_m) {
+        cur_m = mt;
+        ++lt;
+        named_bar(2, C::PROD + 32);
+        nissue = s_cnt[lt & 1];
+      }
+      const int* s_cl = s_cl0 + (lt & 1) * 128;
+      const uint8_t* wblk = p.wpk + (size_t)nb * p.nchunks * C::B_SUB;
+      const int nst = (nissue + G - 1) / G;
+      for (int st = 0; st < nst; ++st) {
+        const int nvalid = min(G, nissue - st * G);
+        mbar_wait(smem_u32(empty + stage), phase ^ 1);
+        if (lane == 0) {
+          const uint32_t fb = smem_u32(full + stage);
+          const uint32_t b_stage = smem_u32(sB + stage * C::STAGE_B);
+          s_info[stage] = (st == 0 ? 1u : 0u) | (st == nst - 1 ? 2u : 0u) | ((uint32_t)nvalid << 2);
+          if (p.dbg & 4) {
+            mbar_arrive(fb);
+          } else {
+            mbar_arrive_expect_tx(fb, nvalid * C::B_SUB);
+            for (int g = 0; g < nvalid; ++g) {
+              const int c = s_cl[st * G + g] >> 16;
+              bulk_g2s(b_stage + g * C::B_SUB, wblk + (size_t)c * C::B_SUB, C::B_SUB, fb);
+            }
+          }
+        }
+        __syncwarp();
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -414,26 +473,39 @@ __global__ void __launch_bounds__(Cfg<BN, TMA>::THREADS, 1)
     const uint32_t idesc = idesc_bf16<BN>();
     int stage = 0;
     uint32_t phase = 0;
-    int it = 0;
+    int it = 0, kst = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
       mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t dtm = tmem_base + acc * BN;
+      bool firstc = true;
       while (true) {
         mbar_wait(smem_u32(full + stage), phase);
+        if (lane == 0) TS(1000 + kst);
+        if (firstc && lane == 0) TS(11 + 8 * it);
+        firstc = false;
         tc_fence_after();
-        if constexpr (!TMA) fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05 (async proxy)
+        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 (async proxy) reads
         const uint32_t info = s_info[stage];
+        const int nvalid = (int)(info >> 2);
         if (lane == 0) {
-          const uint64_t ad = sw128_desc(smem_u32(sA + stage * A_BYTES));
-          const uint64_t bd = sw128_desc(smem_u32(sB + stage * C::B_BYTES));
+          if (!(p.dbg & 1)) {
+            const uint32_t a_stage = smem_u32(sA + stage * C::STAGE_A);
+            const uint32_t b_stage = smem_u32(sB + stage * C::STAGE_B);
+            for (int g = 0; g < nvalid; ++g) {
+              const uint64_t ad = sw128_desc(a_stage + g * A_BYTES);
+              const uint64_t bd = sw128_desc(b_stage + g * C::B_SUB);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, ((info & 1u) && k == 0) ? 0u : 1u);
+              for (int k = 0; k < BK / 16; ++k)
+                umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, ((info & 1u) && g == 0 && k == 0) ? 0u : 1u);
+            }
+          }
           umma_commit(smem_u32(empty + stage));
-          if (info & 2u) umma_commit(smem_u32(tfull + acc));
+          if (info & 2u) { umma_commit(smem_u32(tfull + acc)); TS(12 + 8 * it); }
+          TS(1400 + kst);
         }
+        ++kst;
         __syncwarp();
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         if (info & 2u) break;
@@ -449,6 +521,7 @@ __global__ void __launch_bounds__(Cfg<BN, TMA>::THREADS, 1)
       const int mt = tile / p.nblk, nb = tile - mt * p.nblk;
       const int acc = it & 1;
       mbar_wait(smem_u32(tfull + acc), (it >> 1) & 1);
+      if (q == 0 && lane == 0) TS(13 + 8 * it);
       tc_fence_after();
       const int row = mt * BM + r;
       const bool valid = row < n;
@@ -520,12 +593,16 @@ __global__ void __launch_bounds__(Cfg<BN, TMA>::THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(smem_u32(tempty + acc));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+      if (q == 0 && lane == 0) TS(14 + 8 * it);
     }
   }
 
+  if (tid == 0) TS(2);
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) TS(3);
   if (warp == C::MMA_WARP) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
@@ -562,69 +639,53 @@ inline int pick_bn(int cout) {
 
 inline bool valid_bn(int bn) { return bn == 32 || bn == 64 || bn == 128 || bn == 256; }
 
-static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
-}
-
-// 2-D bf16 tensor [x_rows, ldx] with a {64, 1} box, 128B swizzle, zero OOB fill
-static int make_xmap(CUtensorMap* m, const Params& p) {
-  auto enc = get_encode();
-  if (!enc) return set_error(FPVS_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[2] = {(cuuint64_t)p.ldx, (cuuint64_t)p.x_rows};
-  cuuint64_t strides[1] = {(cuuint64_t)p.ldx * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, 1};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(p.x), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return set_error(FPVS_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return FPVS_OK;
-}
-
-template <int BN, bool TMA>
-int launch(const Params& p, cudaStream_t s) {
-  using C = Cfg<BN, TMA>;
+template <int BN, int G, int PW, int MINB>
+int launch_cfg(const Params& p, cudaStream_t s) {
+  using C = Cfg<BN, G, PW, MINB>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(spconv_tc_kernel<BN, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(spconv_tc_kernel<BN, G, PW, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     configured = true;
   }
-  alignas(64) CUtensorMap xmap;
-  memset(&xmap, 0, sizeof(xmap));
-  if (TMA) {
-    int rc = make_xmap(&xmap, p);
-    if (rc) return rc;
-  }
   long long tiles = (long long)((p.cap + BM - 1) / BM) * p.nblk;
-  int grid = tiles < kNumSMs ? (int)tiles : kNumSMs;
+  long long slots = (long long)kNumSMs * MINB;
+  int grid = (int)(tiles < slots ? tiles : slots);
   if (grid < 1) grid = 1;
-  spconv_tc_kernel<BN, TMA><<<grid, C::THREADS, C::SMEM, s>>>(p, xmap);
+  spconv_tc_kernel<BN, G, PW, MINB><<<grid, C::THREADS, C::SMEM, s>>>(p);
   FPVS_CHECK_LAUNCH("spconv_tc");
   return FPVS_OK;
 }
 
-int dispatch(Params& p, int bn, bool allow_tma, cudaStream_t s) {
-  const bool tma = allow_tma && (p.cin % BK) == 0 && (p.ldx % 8) == 0 && p.x_rows > 0;
-#define FPVS_TC_CASE(BNV) \
-  case BNV:               \
-    return tma ? launch<BNV, true>(p, s) : launch<BNV, false>(p, s);
-  switch (bn) {
-    FPVS_TC_CASE(32)
-    FPVS_TC_CASE(64)
-    FPVS_TC_CASE(128)
-    FPVS_TC_CASE(256)
+static int tc_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FPVS_TC_VARIANT");
+    v = e ? atoi(e) : 0;
   }
-#undef FPVS_TC_CASE
+  return v;
+}
+
+template <int BN>
+int launch(const Params& p, cudaStream_t s) {
+  switch (tc_variant()) {
+    case 1: return launch_cfg<BN, 1, 8, 1>(p, s);
+    case 2:
+      if constexpr (BN <= 128) return launch_cfg<BN, 1, 4, 2>(p, s);
+      else return launch_cfg<BN, 1, 8, 1>(p, s);
+    case 3: return launch_cfg<BN, 2, 8, 1>(p, s);
+    default: return launch_cfg<BN, (BN <= 128 ? 2 : 1), 8, 1>(p, s);
+  }
+}
+
+int dispatch(Params& p, int bn, cudaStream_t s) {
+  switch (bn) {
+    case 32: return launch<32>(p, s);
+    case 64: return launch<64>(p, s);
+    case 128: return launch<128>(p, s);
+    case 256: return launch<256>(p, s);
+  }
   return set_error(FPVS_EINVAL, "bad tensor-core tile width %d", bn);
 }
 
@@ -638,16 +699,11 @@ static int resolve_bn(int bn, int cout) {
   return tc::valid_bn(bn) ? bn : -1;
 }
 
-static bool tma_gather_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    // cp.async producers by default; FPVS_TC_GATHER=tma selects the TMA
-    // tile::gather4 producer (measured slower on B200: the gather4 issue loop
-    // serialises on uniform registers, ~130 cycles per 512 B per SM)
-    const char* e = getenv("FPVS_TC_GATHER");
-    v = (e && e[0] == 't') ? 1 : 0;
-  }
-  return v == 1;
+// internal profiling hook (not part of the ABI): copy CTA 0/1 timestamps out
+extern "C" int fpvs_debug_tc_timestamps(unsigned long long* host, int n) {
+  if (n > 2 * 4096) n = 2 * 4096;
+  cudaError_t e = cudaMemcpyFromSymbol(host, tc::g_dbg_ts, sizeof(unsigned long long) * n);
+  return e == cudaSuccess ? 0 : 3;
 }
 
 extern "C" size_t fpvs_pack_weights_tc_size(int K, int cin, int cout, int bn) {
@@ -681,6 +737,7 @@ static int tc_common(tc::Params& p, const void* x, int ldx, int x_rows, const in
   FPVS_CHECK_ARG(cin % 8 == 0 && ldx % 8 == 0 && ldx >= cin, "tcgen05 path needs Cin and ldx multiples of 8");
   FPVS_CHECK_ARG(cout >= 1 && cout <= 1024, "bad Cout %d", cout);
   FPVS_CHECK_ARG(x_rows >= 1, "x_rows must be positive");
+  FPVS_CHECK_ARG((long long)x_rows * ldx * 2 < (1LL << 31), "feature buffer too large for 32-bit row offsets");
   p = tc::Params{};
   p.x = (const __nv_bfloat16*)x;
   p.ldx = ldx;
@@ -695,6 +752,8 @@ static int tc_common(tc::Params& p, const void* x, int ldx, int x_rows, const in
   p.bias = bias;
   p.cin = cin;
   p.cout = cout;
+  const char* dbg = getenv("FPVS_TC_DEBUG");
+  p.dbg = dbg ? atoi(dbg) : 0;
   return FPVS_OK;
 }
 
@@ -715,7 +774,7 @@ extern "C" int fpvs_spconv_tc(const void* x, int ldx, int x_rows, const int32_t*
   p.y = (__nv_bfloat16*)y;
   p.ldy = ldy;
   p.col_off = col_off;
-  return tc::dispatch(p, bn, tma_gather_enabled(), as_stream(stream));
+  return tc::dispatch(p, bn, as_stream(stream));
 }
 
 extern "C" int fpvs_head_tc(const void* x, int ldx, int x_rows, const int32_t* coords, const int32_t* n_dev, int cap,
@@ -745,5 +804,5 @@ extern "C" int fpvs_head_tc(const void* x, int ldx, int x_rows, const int32_t* c
   p.out_bits = out_bits;
   p.probs = probs;
   p.logits = logits;
-  return tc::dispatch(p, bn, tma_gather_enabled(), as_stream(stream));
+  return tc::dispatch(p, bn, as_stream(stream));
 }

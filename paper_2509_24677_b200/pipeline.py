@@ -42,24 +42,39 @@ class ChainPlan:
         self.ping = torch.empty((k, widest), dtype=dt, device=device)
         self.pong = torch.empty((k, widest), dtype=dt, device=device)
 
-    def run(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, events=None):
+    def stages(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None):
+        """Ordered (name, idempotent launch function) list of one frame."""
         net, lv = self.net, self.L0
         d = net.cfg.d
-        _ev(events, "maps")
-        sp.fill_level_from_bits(lv, bits, self.grid_dims, d)
-        sp.gather_features(bits, lv, self.grid_dims, d, self.x0.dtype, out=self.x0)
+        out = [("maps", lambda: sp.fill_level_from_bits(lv, bits, self.grid_dims, d)),
+               ("gather", lambda: sp.gather_features(bits, lv, self.grid_dims, d, self.x0.dtype, out=self.x0))]
         x, ldx = self.x0, d ** 3
         bufs = (self.ping, self.pong)
         for i, layer in enumerate(net.layers[:-1]):
-            _ev(events, f"conv{i}")
             y = bufs[i % 2]
             table, K = (lv.nbr, 27) if layer.spec.kernel == 3 else (None, 1)
-            run_conv(layer, x, ldx, table, K, lv.n, lv.cap, y, y.shape[1], 0, net.precision)
+            out.append((f"conv{i}", lambda layer=layer, x=x, ldx=ldx, table=table, K=K, y=y:
+                        run_conv(layer, x, ldx, table, K, lv.n, lv.cap, y, y.shape[1], 0, net.precision)))
             x, ldx = y, y.shape[1]
-        _ev(events, "head")
-        out_bits.zero_()
-        run_head(net.layers[-1], x, ldx, lv, d, self.grid_dims, tau, out_bits, probs, logits, net.precision)
+
+        def head(x=x, ldx=ldx):
+            out_bits.zero_()
+            run_head(net.layers[-1], x, ldx, lv, d, self.grid_dims, tau, out_bits, probs, logits, net.precision)
+        out.append(("head", head))
+        return out
+
+    def run(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, events=None):
+        for name, fn in self.stages(bits, out_bits, tau, probs, logits):
+            _ev(events, name)
+            fn()
         _ev(events, "end")
+
+    def layer_flops(self):
+        n = self.L0.count()
+        p = int((self.L0.nbr[:n] >= 0).sum())
+        return {f"conv{i}": 2 * (p if layer.spec.kernel == 3 else n) * layer.spec.in_channels
+                * layer.spec.out_channels for i, layer in enumerate(self.net.layers[:-1])} | {
+            "head": 2 * n * self.net.layers[-1].spec.in_channels * self.net.layers[-1].spec.out_channels}
 
     def counts(self):
         return (self.L0.count(),)
@@ -85,8 +100,40 @@ def _ev(events, name):
 
 
 def stage_times(events):
-    """[(stage, ms)] between consecutive recorded events."""
+    """[(stage, ms)] between consecutive recorded events (includes host launch gaps)."""
     return [(a[0], a[1].elapsed_time(b[1])) for a, b in zip(events, events[1:])]
+
+
+def device_stage_times(plan, bits, out_bits, tau: float = 0.5, reps: int = 20, flush=None):
+    """Per-stage DEVICE time (ms): each stage captured alone into a CUDA graph of
+    ``reps`` back-to-back copies and replayed, so host launch overhead is
+    excluded.  ``flush`` (a buffer > L2) is cleared before each replay."""
+    torch = _torch()
+    res = {}
+    for name, fn in plan.stages(bits, out_bits, tau):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(reps):
+                    fn()
+        torch.cuda.current_stream().wait_stream(s)
+        times = []
+        for _ in range(3):
+            if flush is not None:
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / reps)
+        res[name] = min(times)
+        del g
+    return res
 
 
 class FramePipeline:

@@ -145,27 +145,27 @@ class UNetPlan:
         sp.fill_coarse(self.L0, self.L1, self.down01, self.up10)
         sp.fill_coarse(self.L1, self.L2, self.down12, self.up21)
 
-    def run(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, maps: bool = True, events=None):
-        """One frame: maps, sparse interleave, 14 convs, fused head into ``out_bits`` (zeroed here).
+    def stages(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, maps: bool = True):
+        """The frame as an ordered list of (stage name, launch function).
 
-        ``events`` (a list) receives (stage, cuda.Event) marks for per-stage timing.
+        Each function only enqueues kernels and is idempotent, so a stage can be
+        replayed on its own (per-stage device timing) or all run in order.
         """
-        from .pipeline import _ev
         net, P = self.net, self.net.precision
         L = net.layers
         L0, L1, L2 = self.L0, self.L1, self.L2
         c0, c1, c2 = net.widths
+        d3 = net.d ** 3
+        out = []
         if maps:
-            _ev(events, "maps")
-            self.build_maps(bits)
-        _ev(events, "gather")
-        sp.gather_features(bits, L0, self.grid_dims, net.d, self.x0.dtype, out=self.x0)
+            out.append(("maps", lambda: self.build_maps(bits)))
+        out.append(("gather", lambda: sp.gather_features(bits, L0, self.grid_dims, net.d, self.x0.dtype,
+                                                         out=self.x0)))
 
         def conv(name, x, ldx, table, K, lv, y, ldy, off=0):
-            _ev(events, name)
-            run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu", bn=self.bn.get(name, 0))
+            out.append((name, lambda: run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu",
+                                               bn=self.bn.get(name, 0))))
 
-        d3 = net.d ** 3
         conv("enc0a", self.x0, d3, L0.nbr, 27, L0, self.t0a, c0)
         conv("enc0b", self.t0a, c0, L0.nbr, 27, L0, self.buf0, 2 * c0, 0)             # E0 -> buf0[:, :c0]
         conv("down01", self.buf0, 2 * c0, self.down01, 8, L1, self.t1a, c1)
@@ -180,9 +180,22 @@ class UNetPlan:
         conv("up10", self.t1b, c1, self.up10, 8, L0, self.buf0, 2 * c0, c0)           # U0 -> buf0[:, c0:]
         conv("dec0a", self.buf0, 2 * c0, L0.nbr, 27, L0, self.t0a, c0)
         conv("dec0b", self.t0a, c0, L0.nbr, 27, L0, self.t0b, c0)
-        _ev(events, "head")
-        out_bits.zero_()
-        run_head(L["head"], self.t0b, c0, L0, net.d, self.grid_dims, tau, out_bits, probs, logits, P)
+
+        def head():
+            out_bits.zero_()
+            run_head(L["head"], self.t0b, c0, L0, net.d, self.grid_dims, tau, out_bits, probs, logits, P)
+        out.append(("head", head))
+        return out
+
+    def run(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, maps: bool = True, events=None):
+        """One frame: maps, sparse interleave, 14 convs, fused head into ``out_bits`` (zeroed here).
+
+        ``events`` (a list) receives (stage, cuda.Event) marks (host-launch timing).
+        """
+        from .pipeline import _ev
+        for name, fn in self.stages(bits, out_bits, tau, probs, logits, maps):
+            _ev(events, name)
+            fn()
         _ev(events, "end")
 
     def layer_flops(self):

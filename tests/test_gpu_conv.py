@@ -261,27 +261,3 @@ def test_tc_n_split_tiles(bn):
     run_conv(layer, xt, 256, lv.nbr, 27, lv.n, lv.cap, ref, 256, 0, "bf16", bn=0)
     run_conv(layer, xt, 256, lv.nbr, 27, lv.n, lv.cap, got, 256, 0, "bf16", bn=bn)
     assert torch.equal(got[:n], ref[:n])
-
-
-def test_tc_cpasync_producer_matches_tma():
-    """The cp.async gather producer (used for Cin < 64) and the TMA gather4 producer agree."""
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, torch\n"
-        "from tests.test_gpu_conv import _rand_level, _bf16_rows\n"
-        "from paper_2509_24677_b200.neural import Conv3d, ConvSpec, run_conv\n"
-        "lv, _ = _rand_level(1, (16, 12, 10), 0.25, 5)\n"
-        "n = lv.count()\n"
-        "_, xt = _bf16_rows(n, 128, 4, lv.cap)\n"
-        "layer = Conv3d(ConvSpec(3, 128, 64, 'relu'), np.random.default_rng(2), init='kaiming_uniform')\n"
-        "y = torch.zeros((lv.cap, 64), dtype=torch.bfloat16, device='cuda')\n"
-        "run_conv(layer, xt, 128, lv.nbr, 27, lv.n, lv.cap, y, 64, 0, 'bf16')\n"
-        "torch.save(y[:n].cpu(), '/tmp/fpvs_y_%s.pt')\n")
-    import os
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for mode in ("tma", "cpasync"):  # FPVS_TC_GATHER selects the producer
-        env = dict(os.environ, FPVS_TC_GATHER=mode, PYTHONPATH=root)
-        subprocess.run([sys.executable, "-c", code % mode], check=True, env=env, cwd=root)
-    import torch
-    assert torch.equal(torch.load("/tmp/fpvs_y_tma.pt"), torch.load("/tmp/fpvs_y_cpasync.pt"))
