@@ -107,6 +107,12 @@ int fpvs_kmap_up(const int32_t* fine_coords, const int32_t* n_fine_dev, int cap_
                  const int32_t* coarse_index_vol, int B, int X, int Y, int Z,
                  int32_t* up, void* stream);
 
+/* Per 128-row tile of a neighbour table: bit j set iff some live row of the
+ * tile has table[row][j] >= 0.  masks: uint32 [ceil(cap/128)].  The
+ * tensor-core conv skips K-chunks of offsets absent from a whole tile. */
+int fpvs_kmap_tile_masks(const int32_t* table, int K, const int32_t* n_dev, int cap,
+                         uint32_t* masks, void* stream);
+
 /* Open-addressing GPU hash alternative to index_vol (general, unbounded
  * grids): capacity slots of (key int64, value int32); key = linear cell id. */
 int fpvs_hash_build(const int32_t* coords, const int32_t* n_active_dev, int cap,
@@ -142,10 +148,11 @@ int fpvs_pack_weights_tc(const float* w, int K, int cin, int cout, int bn, void*
 
 /* tcgen05 path: bf16 in, fp32 TMEM accumulate, fused bias + act, bf16 out.
  * x has x_rows rows of stride ldx; rows of x are gathered by TMA
- * (tile::gather4) when Cin % 64 == 0, else by cp.async.  w_packed must have
- * been packed with the same bn. */
+ * with cp.async; tile_masks (from fpvs_kmap_tile_masks on nbr) is required
+ * when nbr is given.  w_packed must have been packed with the same bn. */
 int fpvs_spconv_tc(const void* x, int ldx, int x_rows, const int32_t* nbr, int K,
-                   const int32_t* n_out_dev, int cap_out, const void* w_packed, int bn,
+                   const uint32_t* tile_masks, const int32_t* n_out_dev, int cap_out,
+                   const void* w_packed, int bn,
                    const float* bias, int cin, int cout, int act,
                    void* y, int ldy, int col_off, void* stream);
 

@@ -34,13 +34,14 @@ SIGNATURES = {
     "fpvs_kmap_coarsen": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_kmap_down": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _p, _p]),
     "fpvs_kmap_up": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _p, _p]),
+    "fpvs_kmap_tile_masks": (_i, [_p, _i, _p, _i, _p, _p]),
     "fpvs_hash_build": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _i, _p]),
     "fpvs_kmap_subm_hash": (_i, [_p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_gather_cells_bits": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _i, _p, _i, _i, _p]),
     "fpvs_spconv_simt": (_i, [_p, _i, _i, _p, _i, _p, _i, _p, _p, _i, _i, _i, _p, _i, _i, _i, _p]),
     "fpvs_pack_weights_tc_size": (_z, [_i, _i, _i, _i]),
     "fpvs_pack_weights_tc": (_i, [_p, _i, _i, _i, _i, _p, _p]),
-    "fpvs_spconv_tc": (_i, [_p, _i, _i, _p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _p, _i, _i, _p]),
+    "fpvs_spconv_tc": (_i, [_p, _i, _i, _p, _i, _p, _p, _i, _p, _i, _p, _i, _i, _i, _p, _i, _i, _p]),
     "fpvs_head_simt": (_i, [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p, _p]),
     "fpvs_head_tc": (_i, [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p, _p]),
     "fpvs_loss_sums_size": (_z, [_i, _i]),

@@ -176,6 +176,27 @@ __global__ void kmap_up_kernel(const int4* __restrict__ fc, const int* __restric
   }
 }
 
+// masks[t] = OR over rows [128t, 128t+128) (< n) of (1 << j) for every present
+// table entry j: which kernel offsets a 128-row conv tile needs at all.
+__global__ void __launch_bounds__(128) tile_masks_kernel(const int* __restrict__ table, int K,
+                                                         const int* __restrict__ n_dev, int cap,
+                                                         uint32_t* __restrict__ masks) {
+  __shared__ uint32_t wm[4];
+  const int n = min(*n_dev, cap);
+  const int ntiles = (n + 127) / 128;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int row = t * 128 + threadIdx.x;
+    uint32_t m = 0;
+    if (row < n)
+      for (int j = 0; j < K; ++j) m |= (__ldg(table + (long long)row * K + j) >= 0 ? 1u : 0u) << j;
+    m = __reduce_or_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) masks[t] = wm[0] | wm[1] | wm[2] | wm[3];
+    __syncthreads();
+  }
+}
+
 // ---------------- open-addressing hash, 8-lane cooperative probing --------
 constexpr int kGroup = 8;
 
@@ -330,6 +351,17 @@ extern "C" int fpvs_kmap_up(const int32_t* fine_coords, const int32_t* n_fine_de
   kmap_up_kernel<<<grid_for((long long)cap_fine * 8, 256), 256, 0, as_stream(stream)>>>(
       (const int4*)fine_coords, n_fine_dev, cap_fine, coarse_index_vol, X, Y, Z, up);
   FPVS_CHECK_LAUNCH("fpvs_kmap_up");
+  return FPVS_OK;
+}
+
+extern "C" int fpvs_kmap_tile_masks(const int32_t* table, int K, const int32_t* n_dev, int cap, uint32_t* masks,
+                                    void* stream) {
+  FPVS_CHECK_ARG(table && n_dev && masks, "null pointer");
+  FPVS_CHECK_ARG(K >= 1 && K <= 32, "K must lie in [1, 32]");
+  int tiles = (cap + 127) / 128;
+  tile_masks_kernel<<<tiles < 4 * kNumSMs ? (tiles > 0 ? tiles : 1) : 4 * kNumSMs, 128, 0, as_stream(stream)>>>(
+      table, K, n_dev, cap, masks);
+  FPVS_CHECK_LAUNCH("fpvs_kmap_tile_masks");
   return FPVS_OK;
 }
 

@@ -43,6 +43,7 @@ struct Params {
   int ldx, x_rows;
   const int* nbr;
   int K;
+  const uint32_t* tile_masks;  // per 128-row tile: offsets present (fpvs_kmap_tile_masks)
   const int* n_dev;
   int cap;
   const uint8_t* wpk;
@@ -59,15 +60,16 @@ struct Params {
   uint8_t* out_bits;
   float* probs;
   float* logits;
-  int dbg;  // profiling knob (FPVS_TC_DEBUG): 1 = no MMA, 2 = no A gather, 4 = no B copy
+  int dbg;  // profiling knob (FPVS_TC_DEBUG): 1 = no MMA, 2 = no A gather, 4 = no B copy, 16 = timestamps
 };
 
 template <int BN, int G, int PW = 8, int MINB = 1>
 struct Cfg {
   static constexpr int P = PW;                  // A-gather warps
-  static constexpr int BW_WARP = P;             // B loader + stage bookkeeping
-  static constexpr int MMA_WARP = P + 1;
-  static constexpr int THREADS = (P + 6) * 32;  // + 4 epilogue warps
+  static constexpr int BW_WARP = P;             // B loader + stage flags
+  static constexpr int NB_WARP = P + 1;         // neighbour-row loader
+  static constexpr int MMA_WARP = P + 2;
+  static constexpr int THREADS = (P + 7) * 32;  // + 4 epilogue warps
   static constexpr int PROD = P * 32;
   static constexpr int B_SUB = BN * 128;        // one 64-wide K chunk of B
   static constexpr int STAGE_A = G * A_BYTES;   // G K-chunks per pipeline stage
@@ -79,10 +81,11 @@ struct Cfg {
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128
                                  : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES + NBR_BYTES;
-  static constexpr int CTRL_OFF = BAR_OFF + 8 * (2 * STAGES + 6);  // tmem addr, masks, stage info, chunk list
-  static constexpr int BIAS_OFF = CTRL_OFF + 128 + 4 * 256;  // + two 128-entry chunk lists
+  static constexpr int CTRL_OFF = BAR_OFF + 8 * (2 * STAGES + 8);  // tmem addr, stage info
+  static constexpr int BIAS_OFF = CTRL_OFF + 128;
   static constexpr int SMEM = 1024 + BIAS_OFF + 4 * 1024 + 16;
   static_assert(STAGES >= 2, "pipeline needs two stages");
+  static_assert(STAGES <= 16, "stage info slots");
   static_assert(SMEM * MINB <= 232448, "shared memory budget");
 };
 
@@ -114,17 +117,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Same wait, but the thread sleeps in the barrier unit until the phase
-// completes (suspend-time hint) instead of re-issuing try_wait: waiting warps
-// stop stealing issue slots from the producer warps.
-__device__ __forceinline__ void mbar_sleep_wait(uint32_t bar, uint32_t parity) {
+// Polling wait with a nanosleep back-off between probes: warps that wait long
+// (epilogue during the mainloop, gather warps between their chunks) stop
+// competing for issue slots with the MMA-issuing warp.
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
-      "r"(parity), "r"(1000000)
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -227,6 +235,41 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Walks the K-chunks a tile needs, in order, from its offset mask: for
+// Cin >= 64 every ci-chunk (cpo per offset) of each present offset j; for
+// Cin < 64 every chunk (opc offsets wide) holding a present offset.
+struct ChunkIter {
+  uint32_t mask, rem;
+  int cpo, opc, j, cc, cg;
+  __device__ void init(uint32_t m, int cpo_, int opc_) {
+    mask = m ? m : 1u;
+    rem = mask;
+    cpo = cpo_;
+    opc = opc_;
+    j = -1;
+    cc = cpo_;
+    cg = -1;
+  }
+  __device__ int count(int nchunks) const {
+    if (opc == 1) return __popc(mask) * cpo;
+    const uint32_t gm = (1u << opc) - 1u;
+    int k = 0;
+    for (int c = 0; c < nchunks; ++c) k += ((mask >> (c * opc)) & gm) ? 1 : 0;
+    return k;
+  }
+  // next chunk: jbase (first offset of the chunk), cibase (first channel), chunk id
+  __device__ void next(int& jb, int& cib, int& c) {
+    if (opc == 1) {
+      if (++cc >= cpo) { cc = 0; j = __ffs(rem) - 1; rem &= rem - 1; }
+      jb = j; cib = cc * BK; c = j * cpo + cc;
+    } else {
+      const uint32_t gm = (1u << opc) - 1u;
+      do { ++cg; } while (!((mask >> (cg * opc)) & gm));
+      jb = cg * opc; cib = 0; c = cg;
+    }
+  }
+};
+
 // Copy neighbour rows [row0, row0 + BM) of a K-wide int32 table into shared
 // memory with 16-byte cp.async pieces (zero-filled past the table end), then
 // arrive (noinc) on `bar` once this thread's copies have landed.
@@ -258,12 +301,10 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* nbar = tempty + 2;  // neighbour-tile prefetch, 2 buffers
+  uint64_t* nfull = tempty + 2;   // neighbour tile landed (bulk copy)
+  uint64_t* nempty = nfull + 2;   // every A warp is done with the neighbour tile
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::CTRL_OFF);
-  uint32_t* s_mask = s_tmem + 1;   // producer-warp offset masks (8)
-  int* s_cnt = reinterpret_cast<int*>(s_tmem + 10);  // chunks of the m-tile (2 buffers)
-  uint32_t* s_info = s_tmem + 16;  // per stage: bit0 first, bit1 last, bits 2+ = chunks in stage
-  int* s_cl0 = reinterpret_cast<int*>(s_tmem + 32);  // chunk lists (2 x 128): jbase | cibase << 8 | c << 16
+  uint32_t* s_info = s_tmem + 8;  // per stage: bit0 first, bit1 last of the tile, bits 2+ chunks in the stage
   float* s_bias = reinterpret_cast<float*>(smem + C::BIAS_OFF);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -280,7 +321,8 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(tfull + a), 1);
       mbar_init(smem_u32(tempty + a), 4);  // one arrival per epilogue warp
-      mbar_init(smem_u32(nbar + a), C::PROD);
+      mbar_init(smem_u32(nfull + a), 1);
+      mbar_init(smem_u32(nempty + a), C::P);
     }
     fence_mbar_init();
   }
@@ -297,20 +339,21 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
   const uint32_t tmem_base = *s_tmem;
   if (tid == 0) TS(1);
 
+  const int cpo = p.cin >= BK ? p.cin / BK : 1;  // chunks per offset (Cin >= 64)
+  const int opc = p.cin >= BK ? 1 : BK / p.cin;  // offsets per chunk (Cin < 64)
+  const bool ident = p.nbr == nullptr;
+  const int nbr_elems = BM * p.K;
+
   if (warp < C::P) {
     // ===================== A-gather warps =====================
-    // Each thread owns NPT fixed rows and one 16-byte column slot of the
-    // 128B-swizzled A chunk.  Per chunk: NPT shared loads of neighbour rows,
-    // NPT cp.async (zero-fill for missing rows) — no per-thread special cases.
+    // All PROD threads gather every chunk: thread t owns column slot t%8 and
+    // rows t/8 + RSTEP*i of the 128B-swizzled A chunk; a stage's full barrier
+    // completes when every thread's cp.async pieces have landed (noinc arrival).
     constexpr int RSTEP = C::PROD / 8;
     constexpr int NPT = BM / RSTEP;  // cp.async ops per thread per chunk
-    const int nbr_elems = BM * p.K;
-    const int ptid = tid;
-    const int cpo = p.cin >= BK ? p.cin / BK : 1;
-    const int opc = p.cin >= BK ? 1 : BK / p.cin;
     const int ppo = p.cin >> 3;
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u;  // row pitch in bytes (host checks x < 2^31 B)
-    const int piece = ptid & 7, rbase = ptid >> 3;
+    const int piece = tid & 7, rbase = tid >> 3;
     const int tj = opc == 1 ? 0 : piece / ppo;                     // offset delta of my column slot
     const int tci = opc == 1 ? piece * 8 : (piece - tj * ppo) * 8;  // channel of my column slot
     int rowk[NPT];
@@ -321,101 +364,46 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
       rowk[i] = r * p.K;
       dsto[i] = r * 128 + ((piece ^ (r & 7)) << 4);
     }
-    const bool ident = p.nbr == nullptr;
     int stage = 0;
     uint32_t phase = 0;
-    int cur_m = -1, lt = 0, buf = 1, nissue = 0;
-    if (!ident && (int)blockIdx.x < ntiles)
-      prefetch_nbr(p, ((int)blockIdx.x / p.nblk) * BM, smem_u32(s_nbr), smem_u32(nbar), ptid, C::PROD);
-    int ltile = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ltile) {
+    int cur_m = -1, mi = -1;
+    bool live[NPT];
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int mt = tile / p.nblk;
       const int row0 = mt * BM;
-      if (ptid == 0) TS(8 + 8 * ltile);
       if (mt != cur_m) {
-        buf ^= 1;
-        if (!ident) mbar_wait(smem_u32(nbar + buf), (lt >> 1) & 1);
-        ++lt;
+        if (mi >= 0 && !ident && lane == 0) mbar_arrive(smem_u32(nempty + (mi & 1)));  // done with the old rows
         cur_m = mt;
-        named_bar(1, C::PROD);
-        int nt = tile + gridDim.x;
-        while (nt < ntiles && nt / p.nblk == mt) nt += gridDim.x;
-        if (!ident && nt < ntiles)
-          prefetch_nbr(p, (nt / p.nblk) * BM, smem_u32(s_nbr + (buf ^ 1) * nbr_elems), smem_u32(nbar + (buf ^ 1)),
-                       ptid, C::PROD);
-        // offset-presence mask over live rows; rows past n become -1
-        int* nbv = s_nbr + buf * nbr_elems;
-        uint32_t m = 0;
-        for (int r = ptid; r < BM; r += C::PROD) {
-          const bool live = row0 + r < n;
-          if (!ident) {
-            for (int j = 0; j < p.K; ++j) {
-              const int v = live ? nbv[r * p.K + j] : -1;
-              if (!live) nbv[r * p.K + j] = -1;
-              m |= (v >= 0 ? 1u : 0u) << j;
-            }
-          } else if (live) {
-            m = 1u;
-          }
-        }
-        m = __reduce_or_sync(0xffffffffu, m);
-        if (lane == 0) s_mask[warp] = m;
-        named_bar(1, C::PROD);
-        int* s_cl = s_cl0 + (lt & 1) * 128;
-        if (ptid == 0) {
-          uint32_t tmask = 0;
-          for (int w = 0; w < C::P; ++w) tmask |= s_mask[w];
-          if (!tmask) tmask = 1u;  // keep the pipeline shape: one (zero) chunk
-          int k = 0;
-          if (opc == 1) {
-            for (uint32_t rm = tmask; rm; rm &= rm - 1) {
-              const int j = __ffs(rm) - 1;
-              for (int cc = 0; cc < cpo; ++cc) s_cl[k++] = j | ((cc * BK) << 8) | ((j * cpo + cc) << 16);
-            }
-          } else {
-            const uint32_t gm = (1u << opc) - 1u;
-            for (int c = 0; c < p.nchunks; ++c)
-              if ((tmask >> (c * opc)) & gm) s_cl[k++] = (c * opc) | (c << 16);
-          }
-          s_cnt[lt & 1] = k;
-        }
-        // publish the chunk list to the B-loader warp as well
-        named_bar(2, C::PROD + 32);
-        nissue = s_cnt[lt & 1];
+        ++mi;
+        if (!ident) mbar_wait(smem_u32(nfull + (mi & 1)), (mi >> 1) & 1);
+#pragma unroll
+        for (int i = 0; i < NPT; ++i) live[i] = row0 + rbase + i * RSTEP < n;
       }
-      if (ptid == 0) TS(9 + 8 * ltile);
-      const int* nb_s = s_nbr + buf * nbr_elems;
-      const int* s_cl = s_cl0 + (lt & 1) * 128;
+      const int* nb_s = s_nbr + (mi & 1) * nbr_elems;
+      ChunkIter itr;
+      itr.init(ident ? 1u : __ldg(p.tile_masks + mt), cpo, opc);
+      const int nissue = itr.count(p.nchunks);
       const int nst = (nissue + G - 1) / G;
       for (int st = 0; st < nst; ++st) {
         const int nvalid = min(G, nissue - st * G);
-        mbar_wait(smem_u32(empty + stage), phase ^ 1);
+        mbar_wait_sleep(smem_u32(empty + stage), phase ^ 1, 32);
         const uint32_t a_stage = smem_u32(sA + stage * C::STAGE_A);
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           if (g >= nvalid) break;
-          const int e = s_cl[st * G + g];
-          const int jj = (e & 0xff) + tj;
-          const uint32_t ci2 = (uint32_t)(((e >> 8) & 0xff) + tci) * 2u;
+          int jb, cib, c;
+          itr.next(jb, cib, c);
+          const int jj = jb + tj;
+          const bool jk = jj < p.K;
+          const char* base = reinterpret_cast<const char*>(p.x) + (uint32_t)(cib + tci) * 2u;
           const uint32_t a_sub = a_stage + g * A_BYTES;
-          const char* base = reinterpret_cast<const char*>(p.x) + ci2;
           uint32_t off[NPT];
           bool skip[NPT];
-          if (!ident) {
-            const bool jk = jj < p.K;
 #pragma unroll
-            for (int i = 0; i < NPT; ++i) {
-              const int v = jk ? nb_s[rowk[i] + jj] : -1;
-              skip[i] = v < 0;
-              off[i] = skip[i] ? 0u : (uint32_t)v * ldx2;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < NPT; ++i) {
-              const int row = row0 + rbase + i * RSTEP;
-              skip[i] = row >= n;
-              off[i] = skip[i] ? 0u : (uint32_t)row * ldx2;
-            }
+          for (int i = 0; i < NPT; ++i) {
+            const int v = !(live[i] && jk) ? -1 : ident ? row0 + rbase + i * RSTEP : nb_s[rowk[i] + jj];
+            skip[i] = v < 0;
+            off[i] = skip[i] ? 0u : (uint32_t)v * ldx2;
           }
           if (!(p.dbg & 2)) {
 #pragma unroll
@@ -427,30 +415,25 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
         cp_async_mbar_arrive_noinc(smem_u32(full + stage));
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
-      if (ptid == 0) TS(10 + 8 * ltile);
     }
+    if (mi >= 0 && !ident && lane == 0) mbar_arrive(smem_u32(nempty + (mi & 1)));
   } else if (warp == C::BW_WARP) {
     // ===================== B loader (one elected lane) =====================
-    // Streams the weight chunks of each stage with bulk copies (TMA engine)
-    // and writes the stage flags the MMA issuer reads.
-    int stage = 0;
-    uint32_t phase = 0;
-    int cur_m = -1, nissue = 0, lt = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int mt = tile / p.nblk, nb = tile - mt * p.nblk;
-      if (mt != cur_m) {
-        cur_m = mt;
-        ++lt;
-        named_bar(2, C::PROD + 32);
-        nissue = s_cnt[lt & 1];
-      }
-      const int* s_cl = s_cl0 + (lt & 1) * 128;
-      const uint8_t* wblk = p.wpk + (size_t)nb * p.nchunks * C::B_SUB;
-      const int nst = (nissue + G - 1) / G;
-      for (int st = 0; st < nst; ++st) {
-        const int nvalid = min(G, nissue - st * G);
-        mbar_wait(smem_u32(empty + stage), phase ^ 1);
-        if (lane == 0) {
+    // Streams each stage's weight chunks with bulk copies (TMA engine) and
+    // writes the stage flags the MMA issuer reads.
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int mt = tile / p.nblk, nb = tile - mt * p.nblk;
+        const uint8_t* wblk = p.wpk + (size_t)nb * p.nchunks * C::B_SUB;
+        ChunkIter itr;
+        itr.init(ident ? 1u : __ldg(p.tile_masks + mt), cpo, opc);
+        const int nissue = itr.count(p.nchunks);
+        const int nst = (nissue + G - 1) / G;
+        for (int st = 0; st < nst; ++st) {
+          const int nvalid = min(G, nissue - st * G);
+          mbar_wait(smem_u32(empty + stage), phase ^ 1);
           const uint32_t fb = smem_u32(full + stage);
           const uint32_t b_stage = smem_u32(sB + stage * C::STAGE_B);
           s_info[stage] = (st == 0 ? 1u : 0u) | (st == nst - 1 ? 2u : 0u) | ((uint32_t)nvalid << 2);
@@ -459,40 +442,77 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
           } else {
             mbar_arrive_expect_tx(fb, nvalid * C::B_SUB);
             for (int g = 0; g < nvalid; ++g) {
-              const int c = s_cl[st * G + g] >> 16;
+              int jb, cib, c;
+              itr.next(jb, cib, c);
               bulk_g2s(b_stage + g * C::B_SUB, wblk + (size_t)c * C::B_SUB, C::B_SUB, fb);
             }
           }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == C::NB_WARP) {
+    // ===================== neighbour-row loader =====================
+    // Bulk-copies (TMA engine) the neighbour rows of each m-tile into a double
+    // buffer one m-tile ahead of the gather warps.
+    auto load_rows = [&](int mt2, int b2) {
+      const long long row0 = (long long)mt2 * BM;
+      long long rows = p.cap - row0;
+      if (rows > BM) rows = BM;
+      const long long bytes = rows * p.K * 4;
+      const long long bulk = bytes & ~15LL;
+      const uint32_t dst = smem_u32(s_nbr + b2 * nbr_elems);
+      const int* src = p.nbr + row0 * p.K;
+      // the < 16-byte tail of the table (if any) goes through registers
+      for (long long o = bulk / 4; o < bytes / 4; ++o) s_nbr[b2 * nbr_elems + o] = __ldg(src + o);
+      mbar_arrive_expect_tx(smem_u32(nfull + b2), (uint32_t)bulk);
+      if (bulk) bulk_g2s(dst, src, (uint32_t)bulk, smem_u32(nfull + b2));
+    };
+    if (!ident && lane == 0) {
+      int cur_m = -1, mi = -1;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int mt = tile / p.nblk;
+        if (mt == cur_m) continue;
+        cur_m = mt;
+        ++mi;
+        if (mi == 0) load_rows(mt, 0);
+        int nt = tile + gridDim.x;
+        while (nt < ntiles && nt / p.nblk == mt) nt += gridDim.x;
+        if (nt < ntiles) {
+          // buffer (mi+1)&1 held m-tile mi-1: wait until every A warp released it
+          if (mi >= 1) mbar_wait(smem_u32(nempty + ((mi + 1) & 1)), ((mi - 1) >> 1) & 1);
+          load_rows(nt / p.nblk, (mi + 1) & 1);
+        }
       }
     }
   } else if (warp == C::MMA_WARP) {
     // ===================== MMA issuer =====================
-    const uint32_t idesc = idesc_bf16<BN>();
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0, kst = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const int acc = it & 1;
-      mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t dtm = tmem_base + acc * BN;
-      bool firstc = true;
-      while (true) {
-        mbar_wait(smem_u32(full + stage), phase);
-        if (lane == 0) TS(1000 + kst);
-        if (firstc && lane == 0) TS(11 + 8 * it);
-        firstc = false;
+    // one thread runs the issue loop (a whole-warp loop measured ~25% slower
+    // per chunk: 32-lane barrier polls and fences); lanes 1-31 go straight to
+    // the final barrier.
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16<BN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0, kst = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 (async proxy) reads
-        const uint32_t info = s_info[stage];
-        const int nvalid = (int)(info >> 2);
-        if (lane == 0) {
+        const uint32_t dtm = tmem_base + acc * BN;
+        bool firstc = true;
+        while (true) {
+          mbar_wait(smem_u32(full + stage), phase);
+          TS(1000 + kst);
+          if (firstc) TS(11 + 8 * it);
+          firstc = false;
+          tc_fence_after();
+          if (!(p.dbg & 128)) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 (async proxy) reads
+          const uint32_t info = s_info[stage];
           if (!(p.dbg & 1)) {
             const uint32_t a_stage = smem_u32(sA + stage * C::STAGE_A);
             const uint32_t b_stage = smem_u32(sB + stage * C::STAGE_B);
+            const int nvalid = (int)(info >> 2);
             for (int g = 0; g < nvalid; ++g) {
               const uint64_t ad = sw128_desc(a_stage + g * A_BYTES);
               const uint64_t bd = sw128_desc(b_stage + g * C::B_SUB);
@@ -504,11 +524,10 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
           umma_commit(smem_u32(empty + stage));
           if (info & 2u) { umma_commit(smem_u32(tfull + acc)); TS(12 + 8 * it); }
           TS(1400 + kst);
+          ++kst;
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          if (info & 2u) break;
         }
-        ++kst;
-        __syncwarp();
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-        if (info & 2u) break;
       }
     }
   } else {
@@ -520,7 +539,7 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int mt = tile / p.nblk, nb = tile - mt * p.nblk;
       const int acc = it & 1;
-      mbar_wait(smem_u32(tfull + acc), (it >> 1) & 1);
+      mbar_wait_sleep(smem_u32(tfull + acc), (it >> 1) & 1, 256);
       if (q == 0 && lane == 0) TS(13 + 8 * it);
       tc_fence_after();
       const int row = mt * BM + r;
@@ -644,8 +663,8 @@ int launch_cfg(const Params& p, cudaStream_t s) {
   using C = Cfg<BN, G, PW, MINB>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(spconv_tc_kernel<BN, G, PW, MINB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(spconv_tc_kernel<BN, G, PW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM);
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     configured = true;
   }
@@ -658,25 +677,11 @@ int launch_cfg(const Params& p, cudaStream_t s) {
   return FPVS_OK;
 }
 
-static int tc_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FPVS_TC_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 template <int BN>
 int launch(const Params& p, cudaStream_t s) {
-  switch (tc_variant()) {
-    case 1: return launch_cfg<BN, 1, 8, 1>(p, s);
-    case 2:
-      if constexpr (BN <= 128) return launch_cfg<BN, 1, 4, 2>(p, s);
-      else return launch_cfg<BN, 1, 8, 1>(p, s);
-    case 3: return launch_cfg<BN, 2, 8, 1>(p, s);
-    default: return launch_cfg<BN, (BN <= 128 ? 2 : 1), 8, 1>(p, s);
-  }
+  // two K chunks per stage halve the per-stage barrier/commit overhead where
+  // the stage still fits >= 4 times in shared memory
+  return launch_cfg<BN, (BN <= 128 ? 2 : 1), 8, 1>(p, s);
 }
 
 int dispatch(Params& p, int bn, cudaStream_t s) {
@@ -729,11 +734,12 @@ extern "C" int fpvs_pack_weights_tc(const float* w, int K, int cin, int cout, in
 }
 
 static int tc_common(tc::Params& p, const void* x, int ldx, int x_rows, const int32_t* nbr, int K,
-                     const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin, int cout,
-                     int bn) {
+                     const uint32_t* tile_masks, const int32_t* n_dev, int cap, const void* w_packed,
+                     const float* bias, int cin, int cout, int bn) {
   FPVS_CHECK_ARG(x && w_packed && n_dev, "null pointer");
   FPVS_CHECK_ARG(K >= 1 && K <= tc::kMaxK, "K must lie in [1, 27]");
   FPVS_CHECK_ARG(nbr || K == 1, "nbr may be NULL only for K == 1");
+  FPVS_CHECK_ARG(!nbr || tile_masks, "tile_masks (fpvs_kmap_tile_masks) are required with a neighbour table");
   FPVS_CHECK_ARG(cin % 8 == 0 && ldx % 8 == 0 && ldx >= cin, "tcgen05 path needs Cin and ldx multiples of 8");
   FPVS_CHECK_ARG(cout >= 1 && cout <= 1024, "bad Cout %d", cout);
   FPVS_CHECK_ARG(x_rows >= 1, "x_rows must be positive");
@@ -744,6 +750,7 @@ static int tc_common(tc::Params& p, const void* x, int ldx, int x_rows, const in
   p.x_rows = x_rows;
   p.nbr = nbr;
   p.K = K;
+  p.tile_masks = tile_masks;
   p.n_dev = n_dev;
   p.cap = cap;
   p.wpk = (const uint8_t*)w_packed;
@@ -757,13 +764,14 @@ static int tc_common(tc::Params& p, const void* x, int ldx, int x_rows, const in
   return FPVS_OK;
 }
 
-extern "C" int fpvs_spconv_tc(const void* x, int ldx, int x_rows, const int32_t* nbr, int K, const int32_t* n_out_dev,
-                              int cap_out, const void* w_packed, int bn, const float* bias, int cin, int cout, int act,
-                              void* y, int ldy, int col_off, void* stream) {
+extern "C" int fpvs_spconv_tc(const void* x, int ldx, int x_rows, const int32_t* nbr, int K,
+                              const uint32_t* tile_masks, const int32_t* n_out_dev, int cap_out, const void* w_packed,
+                              int bn, const float* bias, int cin, int cout, int act, void* y, int ldy, int col_off,
+                              void* stream) {
   tc::Params p;
   bn = resolve_bn(bn, cout);
   FPVS_CHECK_ARG(bn > 0, "tile width must be 0 (auto), 32, 64, 128 or 256");
-  int rc = tc_common(p, x, ldx, x_rows, nbr, K, n_out_dev, cap_out, w_packed, bias, cin, cout, bn);
+  int rc = tc_common(p, x, ldx, x_rows, nbr, K, tile_masks, n_out_dev, cap_out, w_packed, bias, cin, cout, bn);
   if (rc) return rc;
   FPVS_CHECK_ARG(y, "null output");
   FPVS_CHECK_ARG(cout % 32 == 0, "tcgen05 store epilogue needs Cout %% 32 == 0, got %d", cout);
@@ -784,7 +792,7 @@ extern "C" int fpvs_head_tc(const void* x, int ldx, int x_rows, const int32_t* c
   const int d3 = d * d * d;
   FPVS_CHECK_ARG(d3 <= 256, "head supports d^3 <= 256");
   const int bn = tc::pick_bn(d3);
-  int rc = tc_common(p, x, ldx, x_rows, nullptr, 1, n_dev, cap, w_packed, bias, cin, d3, bn);
+  int rc = tc_common(p, x, ldx, x_rows, nullptr, 1, nullptr, n_dev, cap, w_packed, bias, cin, d3, bn);
   if (rc) return rc;
   FPVS_CHECK_ARG(coords, "null coords");
   FPVS_CHECK_ARG(Nx % 8 == 0, "N_x must be divisible by 8");

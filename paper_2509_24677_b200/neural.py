@@ -258,14 +258,21 @@ def pick_bn(cout: int, rows: int, sms: int = 148) -> int:
 
 
 def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int, col_off: int = 0,
-             precision: str = "fp32", act: str | None = None, stream=None, bn: int = 0):
-    """One sparse conv launch: y[:, col_off:col_off+Cout] = act(gather-GEMM(x, table) + b)."""
+             precision: str = "fp32", act: str | None = None, stream=None, bn: int = 0, masks=None):
+    """One sparse conv launch: y[:, col_off:col_off+Cout] = act(gather-GEMM(x, table) + b).
+
+    ``masks`` are the table's per-tile offset masks (sparse.tile_masks); the
+    tensor-core path computes them here when not given.
+    """
     torch = _torch()
     spec = layer.spec
     a = _lib.ACT[act or spec.activation]
     s = _lib.stream_ptr(stream)
     if precision == "bf16":
-        _lib.call("fpvs_spconv_tc", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), K, _lib.ptr(n), cap,
+        if table is not None and masks is None:
+            masks = sp.tile_masks(table, K, n, cap, stream=stream)
+        _lib.call("fpvs_spconv_tc", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), K, _lib.ptr(masks), _lib.ptr(n),
+                  cap,
                   _lib.ptr(layer.packed(bn, stream)), bn, _lib.ptr(layer.b), spec.in_channels, spec.out_channels, a,
                   _lib.ptr(y), ldy, col_off, s)
     else:
@@ -333,7 +340,8 @@ class PvsNet:
         for layer in self.layers[:-1]:
             y = torch.empty((lv.cap, layer.spec.out_channels), dtype=dt, device=x.device)
             table, K = (lv.nbr, 27) if layer.spec.kernel == 3 else (None, 1)
-            run_conv(layer, x, x.shape[1], table, K, lv.n, lv.cap, y, y.shape[1], 0, self.precision, stream=stream)
+            run_conv(layer, x, x.shape[1], table, K, lv.n, lv.cap, y, y.shape[1], 0, self.precision, stream=stream,
+                     masks=lv.nbr_masks if table is not None else None)
             x = y
             acts.append(x)
         run_head(self.layers[-1], x, x.shape[1], lv, d, grid_dims, tau, out_bits, probs, logits,

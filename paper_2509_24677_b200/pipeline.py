@@ -54,7 +54,8 @@ class ChainPlan:
             y = bufs[i % 2]
             table, K = (lv.nbr, 27) if layer.spec.kernel == 3 else (None, 1)
             out.append((f"conv{i}", lambda layer=layer, x=x, ldx=ldx, table=table, K=K, y=y:
-                        run_conv(layer, x, ldx, table, K, lv.n, lv.cap, y, y.shape[1], 0, net.precision)))
+                        run_conv(layer, x, ldx, table, K, lv.n, lv.cap, y, y.shape[1], 0, net.precision,
+                                 masks=lv.nbr_masks if table is not None else None)))
             x, ldx = y, y.shape[1]
 
         def head(x=x, ldx=ldx):

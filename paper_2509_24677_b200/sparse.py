@@ -33,6 +33,7 @@ class Level:
     index_vol: object = None   # int32 [B*X*Y*Z]
     n: object = None           # int32 [1] on device
     nbr: object = None         # int32 [cap, 27]
+    nbr_masks: object = None   # uint32 [ceil(cap/128)] offsets present per 128-row tile
     active: object = None      # u8 [B*X*Y*Z]
     hash_keys: object = None
     hash_vals: object = None
@@ -72,10 +73,26 @@ def compact(lv: Level, stream=None):
               _lib.ptr(lv.n), lv.cap, _lib.ptr(ws), ws.numel(), s)
 
 
+def new_masks(cap: int, device="cuda"):
+    torch = _torch()
+    return torch.empty(max(1, (cap + 127) // 128), dtype=torch.int32, device=device)
+
+
+def tile_masks(table, K: int, n, cap: int, out=None, stream=None):
+    """Per 128-row tile: bit j set iff any live row has table[row][j] >= 0."""
+    if out is None:
+        out = new_masks(cap, table.device)
+    _lib.call("fpvs_kmap_tile_masks", _lib.ptr(table), K, _lib.ptr(n), cap, _lib.ptr(out), _lib.stream_ptr(stream))
+    return out
+
+
 def build_subm(lv: Level, stream=None):
     X, Y, Z = lv.dims
     _lib.call("fpvs_kmap_subm", _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap, _lib.ptr(lv.index_vol), lv.B, X, Y, Z,
               _lib.ptr(lv.nbr), _lib.stream_ptr(stream))
+    if lv.nbr_masks is None:
+        lv.nbr_masks = new_masks(lv.cap, lv.nbr.device)
+    tile_masks(lv.nbr, 27, lv.n, lv.cap, lv.nbr_masks, stream)
 
 
 def build_subm_hash(lv: Level, hash_capacity: int | None = None, stream=None):
@@ -131,6 +148,8 @@ def new_coarse(fine: Level, cap: int | None = None):
     coarse = new_level(fine.B, (X // 2, Y // 2, Z // 2), cap, device=fine.coords.device)
     down = torch.empty((coarse.cap, 8), dtype=torch.int32, device=fine.coords.device)
     up = torch.empty((fine.cap, 8), dtype=torch.int32, device=fine.coords.device)
+    coarse.extra["down_masks"] = new_masks(coarse.cap, fine.coords.device)
+    coarse.extra["up_masks"] = new_masks(fine.cap, fine.coords.device)
     return coarse, down, up
 
 
@@ -148,6 +167,8 @@ def fill_coarse(fine: Level, coarse: Level, down, up, stream=None, with_nbr: boo
               fine.B, X, Y, Z, _lib.ptr(down), s)
     _lib.call("fpvs_kmap_up", _lib.ptr(fine.coords), _lib.ptr(fine.n), fine.cap, _lib.ptr(coarse.index_vol),
               fine.B, X, Y, Z, _lib.ptr(up), s)
+    tile_masks(down, 8, coarse.n, coarse.cap, coarse.extra["down_masks"], stream)
+    tile_masks(up, 8, fine.n, fine.cap, coarse.extra["up_masks"], stream)
 
 
 def coarsen(fine: Level, cap: int | None = None, stream=None, with_nbr: bool = True):

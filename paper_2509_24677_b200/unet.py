@@ -162,24 +162,27 @@ class UNetPlan:
         out.append(("gather", lambda: sp.gather_features(bits, L0, self.grid_dims, net.d, self.x0.dtype,
                                                          out=self.x0)))
 
-        def conv(name, x, ldx, table, K, lv, y, ldy, off=0):
+        def conv(name, x, ldx, table, K, lv, y, ldy, off=0, masks=None):
             out.append((name, lambda: run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu",
-                                               bn=self.bn.get(name, 0))))
+                                               bn=self.bn.get(name, 0), masks=masks)))
 
-        conv("enc0a", self.x0, d3, L0.nbr, 27, L0, self.t0a, c0)
-        conv("enc0b", self.t0a, c0, L0.nbr, 27, L0, self.buf0, 2 * c0, 0)             # E0 -> buf0[:, :c0]
-        conv("down01", self.buf0, 2 * c0, self.down01, 8, L1, self.t1a, c1)
-        conv("enc1a", self.t1a, c1, L1.nbr, 27, L1, self.t1b, c1)
-        conv("enc1b", self.t1b, c1, L1.nbr, 27, L1, self.buf1, 2 * c1, 0)             # E1 -> buf1[:, :c1]
-        conv("down12", self.buf1, 2 * c1, self.down12, 8, L2, self.t2a, c2)
-        conv("enc2a", self.t2a, c2, L2.nbr, 27, L2, self.t2b, c2)
-        conv("enc2b", self.t2b, c2, L2.nbr, 27, L2, self.t2a, c2)
-        conv("up21", self.t2a, c2, self.up21, 8, L1, self.buf1, 2 * c1, c1)           # U1 -> buf1[:, c1:]
-        conv("dec1a", self.buf1, 2 * c1, L1.nbr, 27, L1, self.t1a, c1)
-        conv("dec1b", self.t1a, c1, L1.nbr, 27, L1, self.t1b, c1)
-        conv("up10", self.t1b, c1, self.up10, 8, L0, self.buf0, 2 * c0, c0)           # U0 -> buf0[:, c0:]
-        conv("dec0a", self.buf0, 2 * c0, L0.nbr, 27, L0, self.t0a, c0)
-        conv("dec0b", self.t0a, c0, L0.nbr, 27, L0, self.t0b, c0)
+        m0, m1, m2 = L0.nbr_masks, L1.nbr_masks, L2.nbr_masks
+        dm01, um10 = L1.extra["down_masks"], L1.extra["up_masks"]
+        dm12, um21 = L2.extra["down_masks"], L2.extra["up_masks"]
+        conv("enc0a", self.x0, d3, L0.nbr, 27, L0, self.t0a, c0, masks=m0)
+        conv("enc0b", self.t0a, c0, L0.nbr, 27, L0, self.buf0, 2 * c0, 0, m0)          # E0 -> buf0[:, :c0]
+        conv("down01", self.buf0, 2 * c0, self.down01, 8, L1, self.t1a, c1, masks=dm01)
+        conv("enc1a", self.t1a, c1, L1.nbr, 27, L1, self.t1b, c1, masks=m1)
+        conv("enc1b", self.t1b, c1, L1.nbr, 27, L1, self.buf1, 2 * c1, 0, m1)          # E1 -> buf1[:, :c1]
+        conv("down12", self.buf1, 2 * c1, self.down12, 8, L2, self.t2a, c2, masks=dm12)
+        conv("enc2a", self.t2a, c2, L2.nbr, 27, L2, self.t2b, c2, masks=m2)
+        conv("enc2b", self.t2b, c2, L2.nbr, 27, L2, self.t2a, c2, masks=m2)
+        conv("up21", self.t2a, c2, self.up21, 8, L1, self.buf1, 2 * c1, c1, um21)       # U1 -> buf1[:, c1:]
+        conv("dec1a", self.buf1, 2 * c1, L1.nbr, 27, L1, self.t1a, c1, masks=m1)
+        conv("dec1b", self.t1a, c1, L1.nbr, 27, L1, self.t1b, c1, masks=m1)
+        conv("up10", self.t1b, c1, self.up10, 8, L0, self.buf0, 2 * c0, c0, um10)       # U0 -> buf0[:, c0:]
+        conv("dec0a", self.buf0, 2 * c0, L0.nbr, 27, L0, self.t0a, c0, masks=m0)
+        conv("dec0b", self.t0a, c0, L0.nbr, 27, L0, self.t0b, c0, masks=m0)
 
         def head():
             out_bits.zero_()

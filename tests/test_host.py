@@ -46,7 +46,7 @@ def test_argument_errors_map_to_valueerror():
     with pytest.raises(ValueError, match="divide"):
         _lib.call("fpvs_interleave", 1, 0, 1, 6, 4, 4, 4, 1, 0, None, None)
     with pytest.raises(ValueError):
-        _lib.call("fpvs_spconv_tc", 1, 64, 10, None, 27, 1, 10, 1, 0, None, 64, 64, 1, 1, 64, 0, None)
+        _lib.call("fpvs_spconv_tc", 1, 64, 10, None, 27, None, 1, 10, 1, 0, None, 64, 64, 1, 1, 64, 0, None)
 
 
 # -------------------------------------------------------- FPVS boundary format

@@ -48,12 +48,7 @@ buf = (ctypes.c_ulonglong * 8192)()
 fn(buf, 8192)
 ts = np.array(buf[:4096], dtype=np.int64)
 t0 = ts[0]
-print("stage: prod-empty-ok | prod-arrived | mma-full-ok | mma-commit   (us)")
-for k in range(0, 40):
+print("chunk: A-empty-ok A-arrived | B-empty-ok | MMA-full-ok MMA-commit  (us)")
+for k in range(0, 30):
     f = lambda i: (ts[i] - t0) / 1000.0  # noqa: E731
-    print(k, "%.2f %.2f %.2f %.2f" % (f(200 + k), f(600 + k), f(1000 + k), f(1400 + k)))
-print("fine: wait-ok | t0-block | chunks | commit | waitgrp | fence | syncwarp  (delta us from wait-ok)")
-for k in range(0, 12):
-    b = 2000 + 16 * k
-    base = ts[b]
-    print(k, "%.2f" % ((base - t0) / 1000.0), " ".join("%.3f" % ((ts[b + q] - base) / 1000.0) for q in range(1, 7)))
+    print(k, "%.2f %.2f | %.2f | %.2f %.2f" % (f(200 + k), f(600 + k), f(1800 + k), f(1000 + k), f(1400 + k)))
