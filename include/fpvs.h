@@ -113,6 +113,41 @@ int fpvs_kmap_up(const int32_t* fine_coords, const int32_t* n_fine_dev, int cap_
 int fpvs_kmap_tile_masks(const int32_t* table, int K, const int32_t* n_dev, int cap,
                          uint32_t* masks, void* stream);
 
+/* One frame's whole map hierarchy in three launches (levels.cu): level-0
+ * active cells from packed bits (cell = d^3 block), levels l > 0 = parents
+ * of level l-1 (k2s2), each compacted in C-order, plus every table below
+ * that is non-NULL.  Produces exactly what fpvs_cell_active_from_bits ->
+ * fpvs_kmap_compact -> fpvs_kmap_subm / coarsen / down / up / tile_masks
+ * produce step by step (the reference builds the same maps implicitly in
+ * neural.py:187-199 im2col and unet.py:26-64).
+ * Per level (device pointers, caps on the host):
+ *   coords [cap][4], index_vol [B*X*Y*Z], n (int32, device);
+ *   nbr [cap][27] + nbr_masks (NULL = skip);
+ *   level > 0: down [cap][8] rows of l -> children in l-1, down_masks;
+ *              up [cap(l-1)][8] rows of l-1 -> parent in l, up_masks.
+ * Optional: feat = level-0 features (fpvs_gather_cells_bits), clear_bits =
+ * clear_bytes to zero (the output grid of the fused head).
+ * workspace: fpvs_levels_workspace_size bytes, ZEROED once before first use
+ * (every call leaves it zeroed again).  d in {1, 2, 4, 8}, nlev <= 4. */
+typedef struct fpvs_level {
+  int32_t* coords;
+  int32_t* index_vol;
+  int32_t* n;
+  int cap;
+  int32_t* nbr;
+  uint32_t* nbr_masks;
+  int32_t* down;
+  uint32_t* down_masks;
+  int32_t* up;
+  uint32_t* up_masks;
+} fpvs_level;
+
+size_t fpvs_levels_workspace_size(int B, int Nx, int Ny, int Nz, int d, int nlev);
+int fpvs_levels_from_bits(const uint8_t* bits, int B, int Nx, int Ny, int Nz, int d, int nlev,
+                          const fpvs_level* levels, void* workspace, size_t workspace_bytes,
+                          void* feat, int feat_dtype, int ldf, uint8_t* clear_bits, size_t clear_bytes,
+                          void* stream);
+
 /* Open-addressing GPU hash alternative to index_vol (general, unbounded
  * grids): capacity slots of (key int64, value int32); key = linear cell id. */
 int fpvs_hash_build(const int32_t* coords, const int32_t* n_active_dev, int cap,

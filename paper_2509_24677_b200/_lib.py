@@ -35,6 +35,8 @@ SIGNATURES = {
     "fpvs_kmap_down": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _p, _p]),
     "fpvs_kmap_up": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _p, _p]),
     "fpvs_kmap_tile_masks": (_i, [_p, _i, _p, _i, _p, _p]),
+    "fpvs_levels_workspace_size": (_z, [_i, _i, _i, _i, _i, _i]),
+    "fpvs_levels_from_bits": (_i, [_p, _i, _i, _i, _i, _i, _i, _p, _p, _z, _p, _i, _i, _p, _z, _p]),
     "fpvs_hash_build": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _i, _p]),
     "fpvs_kmap_subm_hash": (_i, [_p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_gather_cells_bits": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _i, _p, _i, _i, _p]),
@@ -52,6 +54,14 @@ SIGNATURES = {
     "fpvs_spconv_wgrad_simt": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _p, _p, _p, _z, _p]),
     "fpvs_first_hit_labels": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p]),
 }
+
+
+
+class Level(C.Structure):
+    """struct fpvs_level (include/fpvs.h)."""
+    _fields_ = [("coords", _p), ("index_vol", _p), ("n", _p), ("cap", _i), ("nbr", _p), ("nbr_masks", _p),
+                ("down", _p), ("down_masks", _p), ("up", _p), ("up_masks", _p)]
+
 
 _LIB = None
 

@@ -171,6 +171,55 @@ def fill_coarse(fine: Level, coarse: Level, down, up, stream=None, with_nbr: boo
     tile_masks(up, 8, fine.n, fine.cap, coarse.extra["up_masks"], stream)
 
 
+class LevelMaps:
+    """A frame's level hierarchy built by one fused call (fpvs_levels_from_bits).
+
+    ``levels[0]`` comes from the packed bits, ``levels[l]`` (l > 0) is the k2s2
+    parent set of ``levels[l-1]`` with ``downs[l-1]`` / ``ups[l-1]`` between
+    them (allocated by ``new_coarse``).  Three launches replace the granular
+    sequence fill_level_from_bits -> fill_coarse -> ... and produce the same
+    tables and tile masks bit for bit.
+    """
+
+    def __init__(self, levels, downs, ups, grid_dims, d: int, with_nbr: bool = True):
+        import ctypes as C
+        torch = _torch()
+        self.levels, self.grid_dims, self.d = list(levels), tuple(grid_dims), d
+        lv0 = self.levels[0]
+        nx, ny, nz = self.grid_dims
+        nlev = len(self.levels)
+        ws = _lib.size("fpvs_levels_workspace_size", lv0.B, nx, ny, nz, d, nlev)
+        if ws == 0:
+            raise ValueError(f"fused level build does not support grid {self.grid_dims}, d={d}, {nlev} levels")
+        self.ws = torch.zeros(ws, dtype=torch.uint8, device=lv0.coords.device)  # must start zeroed
+        arr = (_lib.Level * nlev)()
+        for i, lv in enumerate(self.levels):
+            if with_nbr and lv.nbr_masks is None:
+                lv.nbr_masks = new_masks(lv.cap, lv.coords.device)
+            e = arr[i]
+            e.coords, e.index_vol, e.n, e.cap = _lib.ptr(lv.coords), _lib.ptr(lv.index_vol), _lib.ptr(lv.n), lv.cap
+            if with_nbr:
+                e.nbr, e.nbr_masks = _lib.ptr(lv.nbr), _lib.ptr(lv.nbr_masks)
+            if i > 0:
+                e.down, e.down_masks = _lib.ptr(downs[i - 1]), _lib.ptr(lv.extra["down_masks"])
+                e.up, e.up_masks = _lib.ptr(ups[i - 1]), _lib.ptr(lv.extra["up_masks"])
+        self._arr = arr
+        self._arr_ptr = C.addressof(arr)
+
+    def run(self, bits, feat=None, ldf: int = 0, clear=None, stream=None):
+        """Build every level; optionally gather level-0 features into ``feat`` and zero ``clear``."""
+        nx, ny, nz = self.grid_dims
+        lv0 = self.levels[0]
+        fdt = 0
+        if feat is not None:
+            torch = _torch()
+            fdt = _lib.BF16 if feat.dtype == torch.bfloat16 else _lib.F32
+            ldf = ldf or feat.shape[1]
+        _lib.call("fpvs_levels_from_bits", _lib.ptr(bits), lv0.B, nx, ny, nz, self.d, len(self.levels),
+                  self._arr_ptr, _lib.ptr(self.ws), self.ws.numel(), _lib.ptr(feat), fdt, ldf,
+                  _lib.ptr(clear), 0 if clear is None else clear.numel(), _lib.stream_ptr(stream))
+
+
 def coarsen(fine: Level, cap: int | None = None, stream=None, with_nbr: bool = True):
     coarse, down, up = new_coarse(fine, cap)
     fill_coarse(fine, coarse, down, up, stream, with_nbr)

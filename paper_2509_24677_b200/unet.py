@@ -126,6 +126,8 @@ class UNetPlan:
         self.t1a, self.t1b, self.buf1 = e(k1, c1), e(k1, c1), e(k1, 2 * c1)
         self.t2a, self.t2b = e(k2, c2), e(k2, c2)
         self.bn = {}  # per-layer output-tile width (0 = auto from Cout); see tune()
+        self.maps = sp.LevelMaps([self.L0, self.L1, self.L2], [self.down01, self.down12], [self.up10, self.up21],
+                                 self.grid_dims, d) if d in (1, 2, 4, 8) else None
 
     def tune(self, bits):
         """Pick per-layer tile widths from one frame's active counts (one host sync).
@@ -140,7 +142,12 @@ class UNetPlan:
         self.bn = {k: pick_bn(self.net.layers[k].spec.out_channels, v) for k, v in rows.items()}
         return self.bn
 
-    def build_maps(self, bits):
+    def build_maps(self, bits, gather: bool = False, clear=None):
+        """Level hierarchy + tables (three fused launches); with ``gather`` also the
+        level-0 features, and ``clear`` (the output grid) is zeroed on the way."""
+        if self.maps is not None:
+            self.maps.run(bits, self.x0 if gather else None, 0, clear)
+            return
         sp.fill_level_from_bits(self.L0, bits, self.grid_dims, self.net.d)
         sp.fill_coarse(self.L0, self.L1, self.down01, self.up10)
         sp.fill_coarse(self.L1, self.L2, self.down12, self.up21)
@@ -157,10 +164,15 @@ class UNetPlan:
         c0, c1, c2 = net.widths
         d3 = net.d ** 3
         out = []
-        if maps:
-            out.append(("maps", lambda: self.build_maps(bits)))
-        out.append(("gather", lambda: sp.gather_features(bits, L0, self.grid_dims, net.d, self.x0.dtype,
-                                                         out=self.x0)))
+        fused = maps and self.maps is not None
+        if fused:
+            # maps + level-0 features + clearing the output grid: three launches
+            out.append(("maps", lambda: self.build_maps(bits, gather=True, clear=out_bits)))
+        else:
+            if maps:
+                out.append(("maps", lambda: self.build_maps(bits)))
+            out.append(("gather", lambda: sp.gather_features(bits, L0, self.grid_dims, net.d, self.x0.dtype,
+                                                             out=self.x0)))
 
         def conv(name, x, ldx, table, K, lv, y, ldy, off=0, masks=None):
             out.append((name, lambda: run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu",
@@ -185,7 +197,8 @@ class UNetPlan:
         conv("dec0b", self.t0a, c0, L0.nbr, 27, L0, self.t0b, c0, masks=m0)
 
         def head():
-            out_bits.zero_()
+            if not fused:
+                out_bits.zero_()
             run_head(L["head"], self.t0b, c0, L0, net.d, self.grid_dims, tau, out_bits, probs, logits, P)
         out.append(("head", head))
         return out

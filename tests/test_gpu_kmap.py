@@ -98,3 +98,73 @@ def test_config2_level0_map_full_size():
     # property: nbr[nbr[i][j]][26-j] == i for every present pair
     i, j = torch.nonzero(got >= 0, as_tuple=True)
     assert torch.equal(got[got[i, j].long(), 26 - j], i.int())
+
+
+def _granular(bits, B, dims, d, nlev):
+    from paper_2509_24677_b200 import sparse as sp
+    levels = [sp.level_from_bits(bits, B, dims, d)]
+    downs, ups = [], []
+    for _ in range(nlev - 1):
+        c, dn, up = sp.coarsen(levels[-1])
+        levels.append(c)
+        downs.append(dn)
+        ups.append(up)
+    return levels, downs, ups
+
+
+FUSED_CASES = {
+    "cfg2": (lambda: [synth.config2_grid(1)], 4, 3),
+    "batch64": (lambda: [synth.box_grid((64, 64, 64), 80, 1, 10, s) for s in (1, 2)], 4, 3),
+    "cfg1": (lambda: [synth.config1_grid(0)], 2, 2),
+    "smallz": (lambda: [synth.box_grid((32, 16, 16), 30, 1, 4, s) for s in range(5)], 2, 1),
+    "d8": (lambda: [synth.box_grid((64, 64, 128), 60, 1, 12, 3)], 8, 2),
+    "d1": (lambda: [synth.box_grid((16, 16, 32), 10, 1, 3, 4)], 1, 3),
+    "empty": (lambda: [np.zeros((32, 32, 32), bool)], 4, 2),
+}
+
+
+@pytest.mark.parametrize("case", list(FUSED_CASES))
+def test_fused_levels_match_granular(case):
+    """fpvs_levels_from_bits == the granular kmap sequence, bit for bit (and
+    re-arms its workspace: a second frame on the same plan is exact too)."""
+    import torch
+    from paper_2509_24677_b200 import sparse as sp
+    make, d, nlev = FUSED_CASES[case]
+    occs = make()
+    B, dims = len(occs), occs[0].shape
+    X, Y, Z = (v // d for v in dims)
+    lv0 = sp.new_level(B, (X, Y, Z))
+    levels, downs, ups = [lv0], [], []
+    for _ in range(nlev - 1):
+        c, dn, up = sp.new_coarse(levels[-1])
+        levels.append(c)
+        downs.append(dn)
+        ups.append(up)
+    maps = sp.LevelMaps(levels, downs, ups, dims, d)
+    feat = torch.full((lv0.cap, d ** 3 + 8), 7.0, dtype=torch.bfloat16, device="cuda")
+    frames = [occs, [o[::-1].copy() for o in occs]]
+    for fr in frames:
+        bits = _bits(fr)
+        clear = torch.full((bits.numel(),), 255, dtype=torch.uint8, device="cuda")
+        maps.run(bits, feat=feat, clear=clear)
+        ref, rdowns, rups = _granular(bits, B, dims, d, nlev)
+        for lv, rl in zip(levels, ref):
+            n = rl.count()
+            assert lv.count() == n
+            assert torch.equal(lv.coords[:n], rl.coords[:n])
+            assert torch.equal(lv.index_vol, rl.index_vol)
+            assert torch.equal(lv.nbr[:n], rl.nbr[:n])
+            t = (n + 127) // 128
+            assert torch.equal(lv.nbr_masks[:t], rl.nbr_masks[:t])
+        for i in range(nlev - 1):
+            c, f, rc = levels[i + 1], levels[i], ref[i + 1]
+            nc, nf = c.count(), f.count()
+            assert torch.equal(downs[i][:nc], rdowns[i][:nc])
+            assert torch.equal(ups[i][:nf], rups[i][:nf])
+            assert torch.equal(c.extra["down_masks"][:(nc + 127) // 128], rc.extra["down_masks"][:(nc + 127) // 128])
+            assert torch.equal(c.extra["up_masks"][:(nf + 127) // 128], rc.extra["up_masks"][:(nf + 127) // 128])
+        n0 = ref[0].count()
+        want = sp.gather_features(bits, ref[0], dims, d, torch.bfloat16)
+        assert torch.equal(feat[:n0, :d ** 3], want[:n0])
+        assert bool((feat[:n0, d ** 3:] == 7).all())  # columns past d^3 untouched
+        assert int(clear.sum()) == 0
