@@ -13,9 +13,13 @@ one whole frame: kernel maps (3 levels), sparse interleave, 14 convs, head.
 * ``e2e``: the same frames through ``FramePipeline.infer`` — pinned host
   packed grid -> H2D -> frame -> D2H packed PVS — every copy inside the
   timed region.
-* ``roofline``: the dominant kernel (the tcgen05 gather-GEMM, spconv_tc)
-  from an event-instrumented eager frame: algorithmic FLOPs (2*pairs*Cin*Cout,
-  zero-fill not counted) / its summed launch time vs the measured bf16 peak.
+* ``roofline``: the dominant kernel (the tcgen05 gather-GEMM, spconv_tc, 14
+  launches per frame): algorithmic FLOPs (2 * present pairs * Cin * Cout;
+  zero-filled taps not counted) / its summed per-launch DEVICE time.  Each
+  stage of the frame is captured alone as a CUDA graph of 20 back-to-back
+  launches and timed with CUDA events on its stream (host launch gaps
+  excluded); peak = MEASURED_PEAKS.json bf16.  ``traffic`` = DRAM bytes per
+  launch from the committed ncu --set full capture (profiles/).
 * ``cpu_baseline``: the numpy sparse restatement (oracle/, fp64) of the same
   frame on this host's cores (rank 0, N=1).
 
@@ -153,7 +157,7 @@ def run_reference(args):
 
 
 # number of our kernels each C-ABI entry point launches
-KERNELS_PER_CALL = {"fpvs_kmap_compact": 1, "fpvs_hash_build": 1}
+KERNELS_PER_CALL = {"fpvs_kmap_compact": 1, "fpvs_hash_build": 1, "fpvs_levels_from_bits": 3}
 
 
 def count_launches(fn):
@@ -182,7 +186,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2509_24677_b200 import synth
     from paper_2509_24677_b200.froxel import FroxelGrid
-    from paper_2509_24677_b200.pipeline import FramePipeline, stage_times
+    from paper_2509_24677_b200.pipeline import FramePipeline, device_stage_times
     from paper_2509_24677_b200.unet import PvsUNet
 
     dims = (256, 256, 256)
@@ -196,27 +200,13 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
-    # ---- instrumented eager frame: per-stage events, FLOPs, launch count
-    events = []
-    pipe.plan.run(pipe.in_bits, pipe.out_bits, 0.5, events=events)
-    torch.cuda.synchronize()
-    stages = stage_times(events)
+    # ---- per-stage device times (graph-replayed stages), FLOPs, launch count
     layer_flops = pipe.plan.layer_flops()
     n0, n1, n2 = pipe.plan.counts()
     launches_per_frame = count_launches(lambda: pipe.plan.run(pipe.in_bits, pipe.out_bits, 0.5))
     torch.cuda.synchronize()
-    # repeat instrumented frames for stable per-kernel averages
-    conv_ms = {k: [] for k in layer_flops}
-    stage_acc = {}
-    for _ in range(max(3, args.warmup)):
-        flush.zero_()
-        ev = []
-        pipe.plan.run(pipe.in_bits, pipe.out_bits, 0.5, events=ev)
-        torch.cuda.synchronize()
-        for name, ms in stage_times(ev):
-            stage_acc.setdefault(name, []).append(ms)
-            if name in conv_ms:
-                conv_ms[name].append(ms)
+    stage_dev = device_stage_times(pipe.plan, pipe.in_bits, pipe.out_bits, 0.5, reps=20)
+    conv_ms = {k: stage_dev[k] for k in layer_flops if k != "head"}
 
     # ---- warm-up graph replays
     for _ in range(args.warmup):
@@ -283,14 +273,19 @@ def run_ours(args):
         return 0
 
     hbm_peak, tf_peak, peak_kind = peaks()
-    tc_ms = sum(statistics.median(v) for v in conv_ms.values())
-    tc_flops = sum(layer_flops.values())
+    tc_ms = sum(conv_ms.values())
+    tc_flops = sum(layer_flops[k] for k in conv_ms)
     achieved = tc_flops / (tc_ms * 1e-3) / 1e12
     n_tc_launches = len(conv_ms)
-    per_layer = {k: {"ms": round(statistics.median(conv_ms[k]), 5),
-                     "tflops": round(layer_flops[k] / (statistics.median(conv_ms[k]) * 1e-3) / 1e12, 2)}
+    per_layer = {k: {"ms": round(conv_ms[k], 5), "tflops": round(layer_flops[k] / (conv_ms[k] * 1e-3) / 1e12, 2)}
                  for k in conv_ms}
-    stage_ms = {k: round(statistics.median(v), 5) for k, v in stage_acc.items()}
+    stage_ms = {k: round(v, 5) for k, v in stage_dev.items()}
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh).get("spconv_tc_dram_bytes_per_launch")
+    except Exception:
+        pass
 
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
@@ -312,10 +307,12 @@ def run_ours(args):
                 "wall_ms_per_step": 1e3 * wall_e2e / args.steps},
         "roofline": {"bound": "tensor", "kernel": "spconv_tc (tcgen05 gather-GEMM, 14 convs + head / frame)",
                      "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s", "frac": achieved / tf_peak,
-                     "peak_kind": f"{peak_kind} bf16 burst", "traffic": None,
+                     "peak_kind": f"{peak_kind} bf16 burst", "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (mean over the 14 conv launches, ncu --set full)",
                      "flops_per_frame": tc_flops, "launches_per_frame": n_tc_launches,
                      "kernel_ms_per_frame": tc_ms, "per_layer": per_layer},
         "stages_ms": stage_ms,
+        "stages_total_ms": round(sum(stage_dev.values()), 5),
         "gpu_launches": launches_per_frame * args.steps,
         "clocks": clocks,
     }

@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
       rowk[i] = r * p.K;
       dsto[i] = r * 128 + ((piece ^ (r & 7)) << 4);
     }
-    int stage = 0;
+    int stage = 0, gst = 0;
     uint32_t phase = 0;
     int cur_m = -1, mi = -1;
     bool live[NPT];
@@ -387,6 +387,7 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
       for (int st = 0; st < nst; ++st) {
         const int nvalid = min(G, nissue - st * G);
         mbar_wait_sleep(smem_u32(empty + stage), phase ^ 1, 32);
+        if (tid == 0) TS(200 + gst);
         const uint32_t a_stage = smem_u32(sA + stage * C::STAGE_A);
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -413,6 +414,8 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
         // asynchronous arrival once this thread's copies of the stage land
         // (the MMA issuer fences the generic->async proxy after its wait)
         cp_async_mbar_arrive_noinc(smem_u32(full + stage));
+        if (tid == 0) TS(600 + gst);
+        ++gst;
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
