@@ -227,14 +227,31 @@ int fpvs_loss_grad(const float* probs, int C, const int32_t* coords, const int32
  * optionally times (ymask[n] > 0) (relu' with z > 0, neural.py:227-228). */
 int fpvs_spconv_dgrad_simt(const float* dz, int lddz, const int32_t* nbr, int K,
                            const int32_t* n_dev, int cap, const float* w, int cin, int cout,
-                           const float* ymask, int ldm, float* dx, int lddx, void* stream);
+                           const void* ymask, int mask_dtype, int ldm, float* dx, int lddx, void* stream);
 /* wgrad: dw[j*Cin + ci][co] = sum_i x[nbr[i][j]][ci] * dz[i][co]; db = sum_i dz.
  * Deterministic (fixed split + fixed-order reduction, no float atomics). */
 size_t fpvs_wgrad_workspace_size(int K, int cin, int cout, int cap);
-int fpvs_spconv_wgrad_simt(const float* x, int ldx, const float* dz, int lddz,
+int fpvs_spconv_wgrad_simt(const void* x, int ldx, int x_dtype, const float* dz, int lddz,
                            const int32_t* nbr, int K, const int32_t* n_dev, int cap,
                            int cin, int cout, float* dw, float* db,
                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* Optimizer steps over ONE flat fp32 parameter buffer (all layers' weights
+ * and biases back to back; the data-parallel gradient is one all-reduce of
+ * the matching flat gradient).  SGD replaces PvsNet.sgd_step
+ * (neural.py:293-297) with lr = lr0 * (1 - decay)^step (neural.py:481);
+ * AdamW (BASELINE config 5, fp32 master weights): m, v zero-initialised,
+ * step counts from 1, decoupled weight decay. */
+int fpvs_sgd_step(float* params, const float* grads, size_t n, float lr, void* stream);
+int fpvs_adamw_step(float* params, const float* grads, float* m, float* v, size_t n, float lr,
+                    float beta1, float beta2, float eps, float weight_decay, int step, void* stream);
+
+/* Hard confusion counts of thresholded predictions against labels, both as
+ * packed grids (replaces the hard-count loops of neural.py:423-439 and
+ * 485-490): counts[4b..4b+3] = (TP, FP, FN, GTP) as int64 for sample b. */
+size_t fpvs_bits_confusion_workspace_size(int B);
+int fpvs_bits_confusion(const uint8_t* pred_bits, const uint8_t* gt_bits, int B, long long grid_bytes,
+                        long long* counts, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Synthetic PVS labels (row LBL): first occupied froxel of any column within
  * +-radius in x/y; packed in, packed out. */

@@ -49,9 +49,13 @@ SIGNATURES = {
     "fpvs_loss_sums_size": (_z, [_i, _i]),
     "fpvs_loss_counts": (_i, [_p, _i, _p, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_loss_grad": (_i, [_p, _i, _p, _p, _i, _p, _i, _i, _i, _i, _i, _p, _d, _d, _p, _p, _p]),
-    "fpvs_spconv_dgrad_simt": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _p, _i, _p, _i, _p]),
+    "fpvs_spconv_dgrad_simt": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _p, _i, _i, _p, _i, _p]),
     "fpvs_wgrad_workspace_size": (_z, [_i, _i, _i, _i]),
-    "fpvs_spconv_wgrad_simt": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _p, _p, _p, _z, _p]),
+    "fpvs_spconv_wgrad_simt": (_i, [_p, _i, _i, _p, _i, _p, _i, _p, _i, _i, _i, _p, _p, _p, _z, _p]),
+    "fpvs_sgd_step": (_i, [_p, _p, _z, _f, _p]),
+    "fpvs_adamw_step": (_i, [_p, _p, _p, _p, _z, _f, _f, _f, _f, _f, _i, _p]),
+    "fpvs_bits_confusion_workspace_size": (_z, [_i]),
+    "fpvs_bits_confusion": (_i, [_p, _p, _i, C.c_longlong, _p, _p, _z, _p]),
     "fpvs_first_hit_labels": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p]),
 }
 

@@ -24,7 +24,7 @@ template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) spconv_simt_kernel(
     const Tin* __restrict__ x, int ldx, const int* __restrict__ nbr, int K, const int* __restrict__ n_dev, int cap,
     const float* __restrict__ w, int wmode, const float* __restrict__ bias, int cin, int cout, int act,
-    const float* __restrict__ ymask, int ldm, Tout* __restrict__ y, int ldy, int col_off) {
+    const void* __restrict__ ymask, int mask_bf16, int ldm, Tout* __restrict__ y, int ldy, int col_off) {
   __shared__ float As[kTK][kTM + 4];
   __shared__ float Bs[kTK][kTN];
   const int n = min(*n_dev, cap);
@@ -90,7 +90,12 @@ __global__ void __launch_bounds__(256) spconv_simt_kernel(
         if (co >= cout) continue;
         float z = acc[p][q] + (bias ? __ldg(bias + co) : 0.f);
         z = apply_act(z, act);
-        if (ymask && !(ymask[(long long)row * ldm + co] > 0.f)) z = 0.f;
+        if (ymask) {
+          const long long mi = (long long)row * ldm + co;
+          const float mv = mask_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(ymask)[mi])
+                                     : reinterpret_cast<const float*>(ymask)[mi];
+          if (!(mv > 0.f)) z = 0.f;
+        }
         y[(long long)row * ldy + col_off + co] = from_f32<Tout>(z);
       }
     }
@@ -135,8 +140,9 @@ constexpr int kWgSplits = 64;
 constexpr int kWgRows = 32;
 
 // partial[s][j][ci][co] = sum over rows of split s of x[nbr[i][j]][ci] * dz[i][co]
+template <typename Tx>
 __global__ void __launch_bounds__(256) wgrad_partial_kernel(
-    const float* __restrict__ x, int ldx, const float* __restrict__ dz, int lddz, const int* __restrict__ nbr, int K,
+    const Tx* __restrict__ x, int ldx, const float* __restrict__ dz, int lddz, const int* __restrict__ nbr, int K,
     const int* __restrict__ n_dev, int cap, int cin, int cout, float* __restrict__ part) {
   extern __shared__ float sm[];
   float* xs = sm;                      // kWgRows * cin
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(256) wgrad_partial_kernel(
       float v = 0.f;
       if (row < r1) {
         int src = nbr ? __ldg(nbr + (long long)row * K + j) : row;
-        if (src >= 0) v = x[(long long)src * ldx + ci];
+        if (src >= 0) v = to_f32<Tx>(x[(long long)src * ldx + ci]);
       }
       xs[e] = v;
     }
@@ -371,13 +377,13 @@ __global__ void first_hit_kernel(const uint8_t* __restrict__ bits, int B, int Nx
 using namespace fpvs;
 
 static int launch_simt(const void* x, int ldx, int in_dtype, const int32_t* nbr, int K, const int32_t* n_dev, int cap,
-                       const float* w, int wmode, const float* bias, int cin, int cout, int act, const float* ymask,
-                       int ldm, void* y, int ldy, int col_off, int out_dtype, cudaStream_t s) {
+                       const float* w, int wmode, const float* bias, int cin, int cout, int act, const void* ymask,
+                       int mask_bf16, int ldm, void* y, int ldy, int col_off, int out_dtype, cudaStream_t s) {
   const long long tiles = (long long)((cap + kTM - 1) / kTM) * ((cout + kTN - 1) / kTN);
   const int g = grid_for(tiles, 1, 4);
 #define FPVS_SIMT(TI, TO)                                                                                  \
   spconv_simt_kernel<TI, TO><<<g, 256, 0, s>>>((const TI*)x, ldx, nbr, K, n_dev, cap, w, wmode, bias, cin, \
-                                              cout, act, ymask, ldm, (TO*)y, ldy, col_off)
+                                              cout, act, ymask, mask_bf16, ldm, (TO*)y, ldy, col_off)
   if (in_dtype == FPVS_F32 && out_dtype == FPVS_F32) FPVS_SIMT(float, float);
   else if (in_dtype == FPVS_F32) FPVS_SIMT(float, __nv_bfloat16);
   else if (out_dtype == FPVS_F32) FPVS_SIMT(__nv_bfloat16, float);
@@ -395,7 +401,7 @@ extern "C" int fpvs_spconv_simt(const void* x, int ldx, int in_dtype, const int3
   FPVS_CHECK_ARG(nbr || K == 1, "nbr may be NULL only for K == 1");
   FPVS_CHECK_ARG(ldx >= cin && ldy >= col_off + cout, "bad leading dimension");
   if (cap_out <= 0) return FPVS_OK;
-  return launch_simt(x, ldx, in_dtype, nbr, K, n_out_dev, cap_out, w, 0, bias, cin, cout, act, nullptr, 0, y, ldy,
+  return launch_simt(x, ldx, in_dtype, nbr, K, n_out_dev, cap_out, w, 0, bias, cin, cout, act, nullptr, 0, 0, y, ldy,
                      col_off, out_dtype, as_stream(stream));
 }
 
@@ -423,15 +429,16 @@ extern "C" int fpvs_head_simt(const void* x, int ldx, int in_dtype, const int32_
 }
 
 extern "C" int fpvs_spconv_dgrad_simt(const float* dz, int lddz, const int32_t* nbr, int K, const int32_t* n_dev,
-                                      int cap, const float* w, int cin, int cout, const float* ymask, int ldm,
-                                      float* dx, int lddx, void* stream) {
+                                      int cap, const float* w, int cin, int cout, const void* ymask, int mask_dtype,
+                                      int ldm, float* dx, int lddx, void* stream) {
   FPVS_CHECK_ARG(dz && w && dx && n_dev, "null pointer");
   FPVS_CHECK_ARG(K == 27 || K == 1, "dgrad supports the symmetric subm map (K=27) and 1x1x1 (K=1)");
   FPVS_CHECK_ARG(nbr || K == 1, "nbr may be NULL only for K == 1");
   if (cap <= 0) return FPVS_OK;
   // effective conv: input dz (Cin_eff = cout), output dx (Cout_eff = cin)
-  return launch_simt(dz, lddz, FPVS_F32, nbr, K, n_dev, cap, w, 1, nullptr, cout, cin, FPVS_ACT_NONE, ymask, ldm, dx,
-                     lddx, 0, FPVS_F32, as_stream(stream));
+  FPVS_CHECK_ARG(mask_dtype == FPVS_F32 || mask_dtype == FPVS_BF16, "bad mask dtype");
+  return launch_simt(dz, lddz, FPVS_F32, nbr, K, n_dev, cap, w, 1, nullptr, cout, cin, FPVS_ACT_NONE, ymask,
+                     mask_dtype == FPVS_BF16, ldm, dx, lddx, 0, FPVS_F32, as_stream(stream));
 }
 
 extern "C" size_t fpvs_wgrad_workspace_size(int K, int cin, int cout, int cap) {
@@ -439,7 +446,8 @@ extern "C" size_t fpvs_wgrad_workspace_size(int K, int cin, int cout, int cap) {
   return sizeof(float) * (size_t)kWgSplits * K * cin * cout;
 }
 
-extern "C" int fpvs_spconv_wgrad_simt(const float* x, int ldx, const float* dz, int lddz, const int32_t* nbr, int K,
+extern "C" int fpvs_spconv_wgrad_simt(const void* x, int ldx, int x_dtype, const float* dz, int lddz,
+                                      const int32_t* nbr, int K,
                                       const int32_t* n_dev, int cap, int cin, int cout, float* dw, float* db,
                                       void* workspace, size_t workspace_bytes, void* stream) {
   FPVS_CHECK_ARG(x && dz && dw && n_dev && workspace, "null pointer");
@@ -448,8 +456,13 @@ extern "C" int fpvs_spconv_wgrad_simt(const float* x, int ldx, const float* dz, 
   FPVS_CHECK_ARG(workspace_bytes >= fpvs_wgrad_workspace_size(K, cin, cout, cap), "workspace too small");
   cudaStream_t s = as_stream(stream);
   size_t smem = sizeof(float) * kWgRows * (cin + cout);
-  wgrad_partial_kernel<<<K * kWgSplits, 256, smem, s>>>(x, ldx, dz, lddz, nbr, K, n_dev, cap, cin, cout,
-                                                        (float*)workspace);
+  FPVS_CHECK_ARG(x_dtype == FPVS_F32 || x_dtype == FPVS_BF16, "bad x dtype");
+  if (x_dtype == FPVS_F32)
+    wgrad_partial_kernel<float><<<K * kWgSplits, 256, smem, s>>>((const float*)x, ldx, dz, lddz, nbr, K, n_dev, cap,
+                                                                 cin, cout, (float*)workspace);
+  else
+    wgrad_partial_kernel<__nv_bfloat16><<<K * kWgSplits, 256, smem, s>>>((const __nv_bfloat16*)x, ldx, dz, lddz, nbr,
+                                                                         K, n_dev, cap, cin, cout, (float*)workspace);
   long long per = (long long)K * cin * cout;
   wgrad_reduce_kernel<<<grid_for(per, 256), 256, 0, s>>>((const float*)workspace, per, dw);
   if (db) bias_grad_kernel<<<cout < 148 ? cout : 148, 256, 0, s>>>(dz, lddz, n_dev, cap, cout, db);

@@ -517,3 +517,27 @@ def predict_pvs(grid: FroxelGrid, net, tau: float = 0.5) -> FroxelGrid:
     res = FroxelGrid(grid.dims, role="predicted_pvs", bits=out.cpu().numpy())
     res.supersample = grid.supersample
     return res
+
+
+# ---------------------------------------------------------------------------
+# training entry points (neural.py:405-510), implemented in .train
+# ---------------------------------------------------------------------------
+
+def train(pairs, mcfg: ModelConfig, tcfg: TrainConfig, eval_pairs=None, target_fnr=None, target_fpr=None,
+          checkpoint_path=None, log_path=None, verbose: bool = False, precision: str = "fp32"):
+    """Drop-in ``train`` (neural.py:442-510); see paper_2509_24677_b200.train.train."""
+    from .train import train as _train
+    return _train(pairs, mcfg, tcfg, eval_pairs, target_fnr, target_fpr, checkpoint_path, log_path, verbose,
+                  precision)
+
+
+def evaluate_pairs(net: PvsNet, pairs, tau: float):
+    """Hard FNR/FPR over (geometry, gt) pairs (neural.py:423-434)."""
+    from .train import evaluate_pairs as _ev
+    return _ev(net, pairs, tau)
+
+
+def load_pairs(manifest_path) -> list:
+    """(geometry, gt) pairs of a dataset manifest (neural.py:405-411)."""
+    from .train import load_pairs as _lp
+    return _lp(manifest_path)
