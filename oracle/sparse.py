@@ -1,5 +1,9 @@
 """numpy restatement of the NeuralPVS hot path (float64; test infrastructure).
 
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's CPU legs (cpu_baseline, --impl reference) as the checker / CPU
+baseline — never by the product package, which has no CPU fallback.
+
 Submanifold ("masked") semantics: a layer's output exists only on the active
 cells of its input set and inactive cells read as zero.
 shows this equals ``where(active, Conv3d.forward(h), 0)`` of the reference
