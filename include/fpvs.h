@@ -191,6 +191,42 @@ int fpvs_spconv_tc(const void* x, int ldx, int x_rows, const int32_t* nbr, int K
                    const float* bias, int cin, int cout, int act,
                    void* y, int ldy, int col_off, void* stream);
 
+/* Halo-cached submanifold conv (spconv_halo.cu), same math as
+ * fpvs_spconv_tc with K = 27 (neural.py:187-219 on the active set), for
+ * Cin and Cout multiples of 64.  Each 128-row tile's distinct neighbour rows
+ * (its halo) are staged once per 64-channel chunk in shared memory and the
+ * per-offset A operand is assembled in tensor memory.
+ * fpvs_kmap_halo builds, per tile of a K = 27 table: halo_rows
+ * int32 [tiles][FPVS_HALO_MAX] (sorted distinct rows), halo_n int32 [tiles],
+ * lnbr int16 [tiles][128][27] (slot in halo_rows, -1 = none, -2 = not
+ * cached: read directly; every row of a tile whose neighbours span more than
+ * 16384 rows is read directly); tiles = ceil(cap / 128).  fpvs_kmap_halo_size is
+ * the total bytes of the three arrays (each 256-byte aligned, in that order).
+ * fpvs_spconv_halo: bn in {0 (auto), 64, 128}; split >= 1 cuts each tile's K
+ * range across CTAs (fp32 partials in ws, reduced in a fixed order by the
+ * last CTA: deterministic).  ws = fpvs_spconv_halo_workspace_size bytes,
+ * ZEROED before its first use (the kernel leaves its counters at zero). */
+#define FPVS_HALO_MAX 512
+size_t fpvs_kmap_halo_size(int cap);
+int fpvs_kmap_halo(const int32_t* nbr, const int32_t* n_dev, int cap, int32_t* halo_rows,
+                   int32_t* halo_n, int16_t* lnbr, void* stream);
+/* The same tables for up to 4 levels in one launch. */
+typedef struct fpvs_halo_job {
+  const int32_t* nbr;
+  const int32_t* n_dev;
+  int cap;
+  int32_t* halo_rows;
+  int32_t* halo_n;
+  int16_t* lnbr;
+} fpvs_halo_job;
+int fpvs_kmap_halo_multi(const fpvs_halo_job* jobs, int njobs, void* stream);
+size_t fpvs_spconv_halo_workspace_size(int cap, int cout, int bn, int split);
+int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
+                     const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
+                     const int32_t* n_dev, int cap, const void* w_packed, int bn, int split,
+                     const float* bias, int cin, int cout, int act, void* y, int ldy, int col_off,
+                     void* ws, size_t ws_bytes, void* stream);
+
 /* Fused head (replaces the final Conv3d + sigmoid + deinterleave(tau),
  * neural.py:513-526): 1x1x1 conv Cin -> d^3, sigmoid, [p >= tau], packed-bit
  * scatter into out_bits (zeroed first; u32-aligned).  probs (nullable):

@@ -44,6 +44,12 @@ SIGNATURES = {
     "fpvs_pack_weights_tc_size": (_z, [_i, _i, _i, _i]),
     "fpvs_pack_weights_tc": (_i, [_p, _i, _i, _i, _i, _p, _p]),
     "fpvs_spconv_tc": (_i, [_p, _i, _i, _p, _i, _p, _p, _i, _p, _i, _p, _i, _i, _i, _p, _i, _i, _p]),
+    "fpvs_kmap_halo_size": (_z, [_i]),
+    "fpvs_kmap_halo": (_i, [_p, _p, _i, _p, _p, _p, _p]),
+    "fpvs_kmap_halo_multi": (_i, [_p, _i, _p]),
+    "fpvs_spconv_halo_workspace_size": (_z, [_i, _i, _i, _i]),
+    "fpvs_spconv_halo": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _i, _i, _p, _i, _i, _i, _p, _i, _i, _p,
+                              _z, _p]),
     "fpvs_head_simt": (_i, [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p, _p]),
     "fpvs_head_tc": (_i, [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p, _p]),
     "fpvs_loss_sums_size": (_z, [_i, _i]),
@@ -65,6 +71,11 @@ class Level(C.Structure):
     """struct fpvs_level (include/fpvs.h)."""
     _fields_ = [("coords", _p), ("index_vol", _p), ("n", _p), ("cap", _i), ("nbr", _p), ("nbr_masks", _p),
                 ("down", _p), ("down_masks", _p), ("up", _p), ("up_masks", _p)]
+
+
+class HaloJob(C.Structure):
+    """struct fpvs_halo_job (include/fpvs.h)."""
+    _fields_ = [("nbr", _p), ("n_dev", _p), ("cap", _i), ("halo_rows", _p), ("halo_n", _p), ("lnbr", _p)]
 
 
 _LIB = None

@@ -1,0 +1,706 @@
+// (3b) Submanifold 3x3x3 sparse convolution with a per-tile halo cache
+// (tcgen05, A operand in TMEM).  Replaces Conv3d.forward on the active set
+// (pkg/src/froxelpvs/neural.py:187-219) for Cin, Cout multiples of 64.
+//
+// Why: in the plain gather-GEMM (spconv_tc.cu) every 128-row output tile
+// fetches 27 x 128 neighbour rows from L2, but those rows are only ~370-450
+// distinct cells (rows are in C-order, so a tile is a compact slab): the
+// same feature rows are fetched ~8x, and the L2 -> SM path is the limiter.
+// Here each tile's DISTINCT neighbour rows (its halo, <= 512, listed by
+// fpvs_kmap_halo) are copied once per 64-channel chunk into shared memory,
+// and the per-offset A operand (128 rows x 64 bf16) is assembled from
+// shared memory straight into tensor memory:
+//   * 2 loader warps: cp.async the halo rows of (tile, channel chunk) into
+//     a double-buffered smem halo (16-byte pieces XOR-swizzled by row so the
+//     builders' row reads do not bank-conflict) + a bulk copy of the tile's
+//     local neighbour table (int16 halo slot per (row, offset));
+//   * 8 builder warps (two groups of 4, one warp per TMEM lane quadrant,
+//     alternating chunks): thread = tile row; 8 x 16-byte smem loads of the
+//     neighbour's row, one tcgen05.st (32x32b.x32) into an A slot in TMEM;
+//   * 1 warp: bulk copy (TMA engine) of the pre-swizzled weight chunk;
+//   * 1 thread issues tcgen05.mma kind::f16 with A from TMEM, B from smem
+//     (M=128, N=BN, K=16, bf16 -> fp32 TMEM), commits stages back;
+//   * 4 epilogue warps: tcgen05.ld, bias + ReLU + bf16 store; or, when the
+//     K range is split across CTAs (split > 1, for levels with few tiles),
+//     an fp32 partial per split and a deterministic fixed-order reduction by
+//     the last-arriving CTA of the tile.
+// Halo slots past 512 (pathological tiles) fall back to a direct global read
+// of that neighbour row, so the result never depends on the cache.
+#include <limits.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace fpvs {
+namespace halo {
+
+using namespace tc;
+
+constexpr int HMAX = FPVS_HALO_MAX;         // halo rows cached per tile
+constexpr int KOFF = 27;
+constexpr int LNBR_BYTES = BM * KOFF * 2;   // int16 [128][27]
+constexpr int HALO_BYTES = HMAX * 128;      // one 64-channel chunk of every halo row
+constexpr int ROWS_OFF = HALO_BYTES + LNBR_BYTES;   // the tile's halo row list (int32 [HMAX])
+constexpr int HBUF = (ROWS_OFF + HMAX * 4 + 1023) / 1024 * 1024;
+constexpr int WIN_WORDS = 512;              // 16384-row window of the build (wider tiles read directly)
+
+// ------------------------------------------------------------------------
+// Halo build: per 128-row tile, the sorted distinct neighbour rows and the
+// local table lnbr[r][j] = slot of nbr[r][j] in that list (-1 = no
+// neighbour, -2 = not cached -> direct read).
+// ------------------------------------------------------------------------
+struct HaloJob {
+  const int* nbr;
+  const int* n;
+  int cap;
+  int* rows;
+  int* hn;
+  int16_t* lnbr;
+};
+constexpr int kMaxHaloJobs = 4;
+struct HaloJobs {
+  HaloJob j[kMaxHaloJobs];
+  int count;
+};
+
+// One launch for every level's table: CTA b takes active tiles b, b + grid, ...
+// of the concatenated (level, tile) space (counts read on the device).
+__global__ void __launch_bounds__(256) halo_build_kernel(const HaloJobs J) {
+  __shared__ __align__(16) uint8_t s_flag[WIN_WORDS * 32];
+  __shared__ uint32_t s_bits[WIN_WORDS];
+  __shared__ int s_pre[WIN_WORDS];
+  __shared__ int s_red[2][8];
+  __shared__ int s_wsum[8];
+  __shared__ int s_base[kMaxHaloJobs + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    int acc = 0;
+    for (int l = 0; l < J.count; ++l) {
+      s_base[l] = acc;
+      acc += (min(*J.j[l].n, J.j[l].cap) + BM - 1) / BM;
+    }
+    s_base[J.count] = acc;
+  }
+  __syncthreads();
+  const int total = s_base[J.count];
+  for (int tt = blockIdx.x; tt < total; tt += gridDim.x) {
+    int l = 0;
+    while (tt >= s_base[l + 1]) ++l;
+    const int t = tt - s_base[l];
+    const int* __restrict__ nbr = J.j[l].nbr;
+    const int n = min(*J.j[l].n, J.j[l].cap);
+    int* __restrict__ halo_rows = J.j[l].rows;
+    int16_t* __restrict__ lnbr = J.j[l].lnbr;
+    const long long row0 = (long long)t * BM;
+    constexpr int PER = (BM * KOFF + 255) / 256;
+    int vals[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int e = tid + 256 * k;
+      vals[k] = (e < BM * KOFF && row0 + e / KOFF < n) ? __ldg(nbr + row0 * KOFF + e) : -1;
+    }
+    int lo = INT_MAX, hi = -1;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      if (vals[k] >= 0) {
+        lo = min(lo, vals[k]);
+        hi = max(hi, vals[k]);
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(~0u, lo, o));
+      hi = max(hi, __shfl_xor_sync(~0u, hi, o));
+    }
+    if (lane == 0) {
+      s_red[0][warp] = lo;
+      s_red[1][warp] = hi;
+    }
+    __syncthreads();
+    lo = INT_MAX;
+    hi = -1;
+    for (int w = 0; w < 8; ++w) {
+      lo = min(lo, s_red[0][w]);
+      hi = max(hi, s_red[1][w]);
+    }
+    const bool win = hi >= 0 && hi - lo < WIN_WORDS * 32;
+    const int nw = win ? ((hi - lo) >> 5) + 1 : 0;
+    // mark the window rows with plain byte stores (no atomics: equal values),
+    // then fold 32 flags into one bitmap word per thread
+    for (int i = tid; i < nw * 2; i += 256) reinterpret_cast<uint4*>(s_flag)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    if (win) {
+#pragma unroll
+      for (int k = 0; k < PER; ++k)
+        if (vals[k] >= 0) s_flag[vals[k] - lo] = 1;
+    }
+    __syncthreads();
+    for (int w = tid; w < nw; w += 256) {
+      const uint4 a = reinterpret_cast<const uint4*>(s_flag)[2 * w];
+      const uint4 b = reinterpret_cast<const uint4*>(s_flag)[2 * w + 1];
+      const uint32_t q[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t m = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        // bytes are 0/1: gather bit 0 of each byte
+        const uint32_t v = q[i];
+        m |= ((v & 1u) | ((v >> 7) & 2u) | ((v >> 14) & 4u) | ((v >> 21) & 8u)) << (4 * i);
+      }
+      s_bits[w] = m;
+    }
+    __syncthreads();
+    // exclusive scan of the word popcounts (one word per thread per round) and
+    // the sorted halo list: word w's set bits are rows lo + 32 w + b
+    int* hr = halo_rows + (long long)t * HMAX;
+    int H = 0;
+    for (int base = 0; base < nw; base += 256) {
+      const int w = base + tid;
+      const uint32_t bw = w < nw ? s_bits[w] : 0u;
+      const int c = __popc(bw);
+      int incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(~0u, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
+      int woff = 0, rtot = 0;
+      for (int i = 0; i < 8; ++i) {
+        if (i < warp) woff += s_wsum[i];
+        rtot += s_wsum[i];
+      }
+      int rk = H + woff + incl - c;
+      if (w < nw) s_pre[w] = rk;
+      uint32_t bits = bw;
+      while (bits && rk < HMAX) {
+        hr[rk++] = lo + w * 32 + (__ffs(bits) - 1);
+        bits &= bits - 1;
+      }
+      H += rtot;
+      __syncthreads();
+    }
+    if (tid == 0) J.j[l].hn[t] = win ? min(H, HMAX) : 0;
+    int16_t* ln = lnbr + (long long)t * BM * KOFF;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int e = tid + 256 * k;
+      if (e >= BM * KOFF) break;
+      const int v = vals[k];
+      int o = -1;
+      if (v >= 0) {
+        o = -2;
+        if (win) {
+          const int dd = v - lo;
+          const int rk = s_pre[dd >> 5] + __popc(s_bits[dd >> 5] & ((1u << (dd & 31)) - 1u));
+          if (rk < HMAX) o = rk;
+        }
+      }
+      ln[e] = (int16_t)o;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------
+// Conv kernel
+// ------------------------------------------------------------------------
+struct Params {
+  const __nv_bfloat16* x;
+  int ldx;
+  const int* nbr;
+  const int16_t* lnbr;
+  const int* halo_rows;
+  const int* halo_n;
+  const uint32_t* tile_masks;
+  const int* n_dev;
+  int cap;
+  const uint8_t* wpk;
+  int nchunks, nblk, split;
+  const float* bias;
+  int cin, cout, act;
+  __nv_bfloat16* y;
+  int ldy, col_off;
+  float* part;    // [tiles][nblk][split][128][BN] fp32 partials (split > 1)
+  int* counters;  // [tiles][nblk] arrival counters, zero between launches
+  int dbg;        // FPVS_HALO_DEBUG=1: per-role timestamps of CTAs 0/1 (profiling only)
+};
+
+// ---------------- profiling timestamps (FPVS_HALO_DEBUG) ----------------
+__device__ unsigned long long g_hts[2][8192];
+#define HTS(slot)                                                                        \
+  do {                                                                                   \
+    if (p.dbg && blockIdx.x < 2 && (slot) < 8192) {                                     \
+      unsigned long long t_;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+      g_hts[blockIdx.x][(slot)] = t_;                                                    \
+    }                                                                                    \
+  } while (0)
+
+constexpr int W_LOAD = 8;   // warps 8, 9: halo loaders
+constexpr int W_B = 10;     // weight loader
+constexpr int W_MMA = 11;   // MMA issuer, TMEM owner
+constexpr int W_EPI = 12;   // warps 12..15: epilogue
+constexpr int THREADS = 512;
+constexpr int LOADERS = 64;
+
+template <int BN>
+struct Cfg {
+  static constexpr int NS = BN == 64 ? 8 : 4;  // stages: TMEM A slot + smem B chunk
+  static constexpr int B_SUB = BN * 128;
+  static constexpr int ACOL = 2 * BN;          // TMEM: [acc0 | acc1 | A slots]
+  static constexpr int B_OFF = 2 * HBUF;
+  static constexpr int BAR_OFF = B_OFF + NS * B_SUB;
+  static constexpr int NBARS = 2 * NS + 10;
+  static constexpr int CTRL_OFF = BAR_OFF + 8 * NBARS;
+  static constexpr int BIAS_OFF = CTRL_OFF + 64;
+  static constexpr int SMEM = 1024 + BIAS_OFF + 4 * 1024;
+  static_assert(ACOL + NS * 32 <= 512, "TMEM columns");
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+struct Unit {
+  int mt, nb, s, npres, q0, q1;
+  uint32_t mask;
+};
+
+__device__ __forceinline__ void unit_of(const Params& p, int u, int cpo, Unit& U) {
+  const int per = p.nblk * p.split;
+  U.mt = u / per;
+  const int rem = u - U.mt * per;
+  U.nb = rem / p.split;
+  U.s = rem - U.nb * p.split;
+  U.mask = __ldg(p.tile_masks + U.mt);
+  if (!U.mask) U.mask = 1u << 13;
+  U.npres = __popc(U.mask);
+  const long long L = (long long)cpo * U.npres;
+  U.q0 = (int)(U.s * L / p.split);
+  U.q1 = (int)((U.s + 1) * L / p.split);
+}
+
+// offset of the q-th chunk inside channel chunk c: the (q - c*npres)-th set bit
+__device__ __forceinline__ int first_offset(uint32_t mask, int rank) { return (int)__fns(mask, 0, rank + 1); }
+__device__ __forceinline__ int next_offset(uint32_t mask, int j) { return __ffs(mask & ~((2u << j) - 1u)) - 1; }
+
+template <int BN>
+__global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  uint8_t* sB = smem + C::B_OFF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::NS;
+  uint64_t* tfull = bars + 2 * C::NS;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* hfull = tempty + 2;
+  uint64_t* hempty = hfull + 2;
+  uint64_t* hmeta = hempty + 2;  // the tile's local table + halo row list landed (bulk copy)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::CTRL_OFF);
+  volatile int* s_last = reinterpret_cast<volatile int*>(smem + C::CTRL_OFF + 16);
+  float* s_bias = reinterpret_cast<float*>(smem + C::BIAS_OFF);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) HTS(0);
+  const int n = min(*p.n_dev, p.cap);
+  const int mtiles = (n + BM - 1) / BM;
+  const int nunits = mtiles * p.nblk * p.split;
+  const int cpo = p.cin / BK;
+
+  if (tid == 0) {
+    for (int s = 0; s < C::NS; ++s) {
+      mbar_init(smem_u32(full + s), 4 + 1);  // one builder group (4 warps) + the weight loader
+      mbar_init(smem_u32(empty + s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(tfull + a), 1);
+      mbar_init(smem_u32(tempty + a), 4);
+      mbar_init(smem_u32(hfull + a), LOADERS);
+      mbar_init(smem_u32(hempty + a), 8);
+      mbar_init(smem_u32(hmeta + a), 1);
+    }
+    fence_mbar_init();
+  }
+  for (int c = tid; c < p.cout; c += THREADS) s_bias[c] = p.bias ? p.bias[c] : 0.f;
+  if (warp == W_MMA) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *s_tmem;
+  if (tid == 0) HTS(1);
+
+  if (warp < W_LOAD) {
+    // ===================== A builders =====================
+    const int bg = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
+    const uint32_t t_a = tmem_base + ((uint32_t)(q4 * 32) << 16) + C::ACOL;
+    const uint32_t ldx2 = (uint32_t)p.ldx * 2u;
+    uint32_t kc = 0, gc = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      unit_of(p, u, cpo, U);
+      for (int c = U.q0 / U.npres; U.q1 > U.q0 && c * U.npres < U.q1; ++c) {
+        const int qs = max(U.q0, c * U.npres), qe = min(U.q1, (c + 1) * U.npres);
+        const int hb = gc & 1;
+        mbar_wait(smem_u32(hmeta + hb), (gc >> 1) & 1);
+        mbar_wait(smem_u32(hfull + hb), (gc >> 1) & 1);
+        if (lane == 0 && q4 == 0) HTS(256 + 4 * gc + 2 * bg);
+        const uint8_t* hbuf = smem + hb * HBUF;
+        const int16_t* ln = reinterpret_cast<const int16_t*>(hbuf + HALO_BYTES) + r * KOFF;
+        int j = first_offset(U.mask, qs - c * U.npres);
+        for (int q = qs; q < qe; ++q, ++kc, j = next_offset(U.mask, j)) {
+          if ((int)(kc & 1) != bg) continue;
+          const int stage = (int)(kc % C::NS);
+          const uint32_t ph = (kc / C::NS) & 1;
+          const int li = ln[j];
+          uint32_t v[32];
+          if (li >= 0) {
+            const uint8_t* src = hbuf + li * 128;
+            const int sw = li & 7;
+#pragma unroll
+            for (int pc = 0; pc < 8; ++pc) {
+              const uint4 t4 = *reinterpret_cast<const uint4*>(src + ((pc ^ sw) << 4));
+              v[4 * pc] = t4.x; v[4 * pc + 1] = t4.y; v[4 * pc + 2] = t4.z; v[4 * pc + 3] = t4.w;
+            }
+          } else if (li == -1) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0u;
+          } else {
+            const int g = __ldg(p.nbr + ((long long)U.mt * BM + r) * KOFF + j);
+            const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(p.x) +
+                                                              (long long)g * ldx2 + c * 128);
+#pragma unroll
+            for (int pc = 0; pc < 8; ++pc) {
+              const uint4 t4 = __ldg(src + pc);
+              v[4 * pc] = t4.x; v[4 * pc + 1] = t4.y; v[4 * pc + 2] = t4.z; v[4 * pc + 3] = t4.w;
+            }
+          }
+          if (lane == 0 && q4 == 0) HTS(1024 + 3 * kc);
+          mbar_wait(smem_u32(empty + stage), ph ^ 1);
+          if (lane == 0 && q4 == 0) HTS(1025 + 3 * kc);
+          tc_fence_after();
+          tmem_st32(t_a + stage * 32, v);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(full + stage));
+          if (lane == 0 && q4 == 0) HTS(1026 + 3 * kc);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(hempty + hb));
+        if (lane == 0 && q4 == 0) HTS(257 + 4 * gc + 2 * bg);
+        ++gc;
+      }
+    }
+  } else if (warp < W_B) {
+    // ===================== halo loaders =====================
+    const int tl = tid - W_LOAD * 32;
+    const int pc = tl & 7;
+    const uint32_t ldx2 = (uint32_t)p.ldx * 2u;
+    uint32_t gc = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      Unit U;
+      unit_of(p, u, cpo, U);
+      for (int c = U.q0 / U.npres; U.q1 > U.q0 && c * U.npres < U.q1; ++c) {
+        const int hb = gc & 1;
+        mbar_wait_sleep(smem_u32(hempty + hb), ((gc >> 1) & 1) ^ 1, 64);
+        if (tl == 0) HTS(16 + 3 * gc);
+        uint8_t* hbuf = smem + hb * HBUF;
+        const int H = __ldg(p.halo_n + U.mt);
+        if (tl == 0) {
+          // the tile's local table and its halo row list, one bulk copy each
+          const uint32_t rb = (uint32_t)((H * 4 + 15) & ~15);
+          const uint32_t mb = smem_u32(hmeta + hb);
+          mbar_arrive_expect_tx(mb, LNBR_BYTES + rb);
+          bulk_g2s(smem_u32(hbuf + HALO_BYTES), p.lnbr + (long long)U.mt * BM * KOFF, LNBR_BYTES, mb);
+          if (rb) bulk_g2s(smem_u32(hbuf + ROWS_OFF), p.halo_rows + (long long)U.mt * HMAX, rb, mb);
+        }
+        mbar_wait(smem_u32(hmeta + hb), (gc >> 1) & 1);
+        if (tl == 0) HTS(17 + 3 * gc);
+        const int* hr = reinterpret_cast<const int*>(hbuf + ROWS_OFF);
+        const char* xb = reinterpret_cast<const char*>(p.x) + c * 128 + pc * 16;
+        const uint32_t hs = smem_u32(hbuf);
+#pragma unroll 4
+        for (int i = tl >> 3; i < H; i += LOADERS / 8) {
+          const int g = hr[i];
+          cp_async16(hs + i * 128 + ((pc ^ (i & 7)) << 4), xb + (long long)g * ldx2, 16);
+        }
+        cp_async_mbar_arrive_noinc(smem_u32(hfull + hb));
+        if (tl == 0) HTS(18 + 3 * gc);
+        ++gc;
+      }
+    }
+  } else if (warp == W_B) {
+    // ===================== weight loader =====================
+    if (lane == 0) {
+      uint32_t kc = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        Unit U;
+        unit_of(p, u, cpo, U);
+        const uint8_t* wblk = p.wpk + (size_t)U.nb * p.nchunks * C::B_SUB;
+        for (int c = U.q0 / U.npres; c * U.npres < U.q1; ++c) {
+          const int qs = max(U.q0, c * U.npres), qe = min(U.q1, (c + 1) * U.npres);
+          int j = first_offset(U.mask, qs - c * U.npres);
+          for (int q = qs; q < qe; ++q, ++kc, j = next_offset(U.mask, j)) {
+            const int stage = (int)(kc % C::NS);
+            mbar_wait(smem_u32(empty + stage), ((kc / C::NS) & 1) ^ 1);
+            const uint32_t fb = smem_u32(full + stage);
+            mbar_arrive_expect_tx(fb, C::B_SUB);
+            bulk_g2s(smem_u32(sB + stage * C::B_SUB), wblk + (size_t)(j * cpo + c) * C::B_SUB, C::B_SUB, fb);
+          }
+        }
+      }
+    }
+  } else if (warp == W_MMA) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16<BN>();
+      uint32_t kc = 0;
+      int it = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+        Unit U;
+        unit_of(p, u, cpo, U);
+        const int acc = it & 1;
+        mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
+        HTS(7000 + 2 * it);
+        tc_fence_after();
+        const uint32_t dtm = tmem_base + acc * BN;
+        bool first = true;
+        for (int q = U.q0; q < U.q1; ++q, ++kc) {
+          const int stage = (int)(kc % C::NS);
+          mbar_wait(smem_u32(full + stage), (kc / C::NS) & 1);
+          HTS(4096 + 2 * kc);
+          tc_fence_after();
+          const uint32_t ta = tmem_base + C::ACOL + stage * 32;
+          const uint64_t bd = sw128_desc(smem_u32(sB + stage * C::B_SUB));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) umma_bf16_ts(dtm, ta + 8 * k, bd + 2 * k, idesc, (first && k == 0) ? 0u : 1u);
+          first = false;
+          umma_commit(smem_u32(empty + stage));
+          HTS(4097 + 2 * kc);
+        }
+        umma_commit(smem_u32(tfull + acc));
+        HTS(7001 + 2 * it);
+      }
+    }
+  } else {
+    // ===================== epilogue (4 warps) =====================
+    const int q4 = warp & 3, r = q4 * 32 + lane;
+    const uint32_t tlane = (uint32_t)(q4 * 32) << 16;
+    int it = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+      Unit U;
+      unit_of(p, u, cpo, U);
+      const int acc = it & 1;
+      mbar_wait_sleep(smem_u32(tfull + acc), (it >> 1) & 1, 128);
+      if (q4 == 0 && lane == 0) HTS(7200 + 2 * it);
+      tc_fence_after();
+      const long long row = (long long)U.mt * BM + r;
+      const bool valid = row < n;
+      const int col0 = U.nb * BN;
+      if (p.split == 1) {
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 32) {
+          float v[32];
+          tmem_ld32(tmem_base + tlane + acc * BN + cb, v);
+          if (!valid) continue;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float z = v[i] + s_bias[col0 + cb + i];
+            v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
+          }
+          uint4* dst = reinterpret_cast<uint4*>(p.y + row * p.ldy + p.col_off + col0 + cb);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_bf16x2(v[8 * i + 0], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                                pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+      } else {
+        const long long slot = (long long)U.mt * p.nblk + U.nb;
+        float* mine = p.part + ((slot * p.split + U.s) * BM + r) * BN;
+        const bool has = U.q1 > U.q0;
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 32) {
+          float v[32];
+          tmem_ld32(tmem_base + tlane + acc * BN + cb, v);
+          float4* dst = reinterpret_cast<float4*>(mine + cb);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = has ? make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3])
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+        __threadfence();
+        named_bar(1, 128);
+        if (warp == W_EPI && lane == 0) *s_last = atomicAdd(p.counters + slot, 1) == p.split - 1;
+        named_bar(1, 128);
+        if (*s_last) {
+          __threadfence();
+          if (valid) {
+            const float* base = p.part + (slot * p.split * BM + r) * BN;
+#pragma unroll 1
+            for (int cb = 0; cb < BN; cb += 32) {
+              float v[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+              for (int ss = 0; ss < p.split; ++ss) {
+                const float4* src = reinterpret_cast<const float4*>(base + (long long)ss * BM * BN + cb);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float4 t4 = __ldcg(src + i);
+                  v[4 * i] += t4.x; v[4 * i + 1] += t4.y; v[4 * i + 2] += t4.z; v[4 * i + 3] += t4.w;
+                }
+              }
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float z = v[i] + s_bias[col0 + cb + i];
+                v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
+              }
+              uint4* dst = reinterpret_cast<uint4*>(p.y + row * p.ldy + p.col_off + col0 + cb);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                dst[i] = make_uint4(pack_bf16x2(v[8 * i + 0], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                                    pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+            }
+          }
+          if (warp == W_EPI && lane == 0) p.counters[slot] = 0;
+        }
+      }
+    }
+  }
+
+  if (tid == 0) HTS(2);
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) HTS(3);
+  if (warp == W_MMA) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  }
+}
+
+template <int BN>
+int launch(const Params& p, cudaStream_t s) {
+  using C = Cfg<BN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(spconv_halo_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  const long long units = (long long)((p.cap + BM - 1) / BM) * p.nblk * p.split;
+  const int grid = (int)(units < kNumSMs ? (units < 1 ? 1 : units) : kNumSMs);
+  spconv_halo_kernel<BN><<<grid, THREADS, C::SMEM, s>>>(p);
+  FPVS_CHECK_LAUNCH("spconv_halo");
+  return FPVS_OK;
+}
+
+inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+}  // namespace halo
+}  // namespace fpvs
+
+using namespace fpvs;
+
+// internal profiling hook (not part of the ABI): CTA 0/1 timestamps
+extern "C" int fpvs_debug_halo_timestamps(unsigned long long* host, int n) {
+  if (n > 2 * 8192) n = 2 * 8192;
+  return cudaMemcpyFromSymbol(host, halo::g_hts, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 3;
+}
+
+extern "C" size_t fpvs_kmap_halo_size(int cap) {
+  if (cap < 1) return 0;
+  const size_t tiles = (cap + tc::BM - 1) / tc::BM;
+  return halo::align256(tiles * halo::HMAX * 4) + halo::align256(tiles * 4) +
+         halo::align256(tiles * tc::BM * halo::KOFF * 2);
+}
+
+extern "C" int fpvs_kmap_halo_multi(const fpvs_halo_job* jobs, int njobs, void* stream) {
+  FPVS_CHECK_ARG(jobs && njobs >= 1 && njobs <= halo::kMaxHaloJobs, "1..4 halo jobs");
+  halo::HaloJobs J{};
+  J.count = njobs;
+  long long tiles = 0;
+  for (int i = 0; i < njobs; ++i) {
+    const fpvs_halo_job& q = jobs[i];
+    FPVS_CHECK_ARG(q.nbr && q.n_dev && q.halo_rows && q.halo_n && q.lnbr, "null pointer in halo job %d", i);
+    FPVS_CHECK_ARG(q.cap >= 0, "negative capacity");
+    J.j[i] = halo::HaloJob{q.nbr, q.n_dev, q.cap, q.halo_rows, q.halo_n, q.lnbr};
+    tiles += (q.cap + tc::BM - 1) / tc::BM;
+  }
+  if (tiles == 0) return FPVS_OK;
+  const int grid = (int)(tiles < 4 * kNumSMs ? tiles : 4 * kNumSMs);
+  halo::halo_build_kernel<<<grid, 256, 0, as_stream(stream)>>>(J);
+  FPVS_CHECK_LAUNCH("fpvs_kmap_halo");
+  return FPVS_OK;
+}
+
+extern "C" int fpvs_kmap_halo(const int32_t* nbr, const int32_t* n_dev, int cap, int32_t* halo_rows,
+                              int32_t* halo_n, int16_t* lnbr, void* stream) {
+  fpvs_halo_job j{nbr, n_dev, cap, halo_rows, halo_n, lnbr};
+  return fpvs_kmap_halo_multi(&j, 1, stream);
+}
+
+extern "C" size_t fpvs_spconv_halo_workspace_size(int cap, int cout, int bn, int split) {
+  if (cap < 1 || (bn != 64 && bn != 128) || cout % bn || split < 1) return 0;
+  const size_t tiles = (cap + tc::BM - 1) / tc::BM, nblk = cout / bn;
+  size_t b = halo::align256(tiles * nblk * 4);
+  if (split > 1) b += tiles * nblk * split * tc::BM * bn * 4;
+  return b;
+}
+
+extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
+                                const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
+                                const int32_t* n_dev, int cap, const void* w_packed, int bn, int split,
+                                const float* bias, int cin, int cout, int act, void* y, int ldy, int col_off,
+                                void* ws, size_t ws_bytes, void* stream) {
+  FPVS_CHECK_ARG(x && nbr && lnbr && halo_rows && halo_n && tile_masks && n_dev && w_packed && y,
+                 "null pointer");
+  if (bn == 0) bn = cout % 128 == 0 ? 128 : 64;
+  if (split == 0) split = 1;
+  FPVS_CHECK_ARG(bn == 64 || bn == 128, "halo conv tile width must be 64 or 128");
+  FPVS_CHECK_ARG(cin % 64 == 0 && cin >= 64, "halo conv needs Cin %% 64 == 0, got %d", cin);
+  FPVS_CHECK_ARG(cout % bn == 0 && cout <= 1024, "halo conv needs Cout %% %d == 0, got %d", bn, cout);
+  FPVS_CHECK_ARG(ldx % 8 == 0 && ldx >= cin, "bad input leading dimension");
+  FPVS_CHECK_ARG((long long)x_rows * ldx * 2 < (1LL << 31), "feature buffer too large for 32-bit row offsets");
+  FPVS_CHECK_ARG(ldy % 8 == 0 && col_off % 8 == 0 && ldy >= col_off + cout, "bad output leading dimension");
+  FPVS_CHECK_ARG(act == FPVS_ACT_NONE || act == FPVS_ACT_RELU, "halo conv epilogue supports none/relu");
+  FPVS_CHECK_ARG(split >= 1 && split <= 27 * (cin / 64), "split must lie in [1, 27 * Cin / 64]");
+  const size_t need = fpvs_spconv_halo_workspace_size(cap, cout, bn, split);
+  FPVS_CHECK_ARG(ws && ws_bytes >= need, "workspace too small: need %zu bytes", need);
+  if (cap <= 0) return FPVS_OK;
+  halo::Params p{};
+  p.x = (const __nv_bfloat16*)x;
+  p.ldx = ldx;
+  p.nbr = nbr;
+  p.lnbr = lnbr;
+  p.halo_rows = halo_rows;
+  p.halo_n = halo_n;
+  p.tile_masks = tile_masks;
+  p.n_dev = n_dev;
+  p.cap = cap;
+  p.wpk = (const uint8_t*)w_packed;
+  p.nchunks = 27 * cin / 64;
+  p.nblk = cout / bn;
+  p.split = split;
+  p.bias = bias;
+  p.cin = cin;
+  p.cout = cout;
+  p.act = act;
+  p.y = (__nv_bfloat16*)y;
+  p.ldy = ldy;
+  p.col_off = col_off;
+  const size_t tiles = (cap + tc::BM - 1) / tc::BM;
+  p.counters = (int*)ws;
+  p.part = (float*)((uint8_t*)ws + halo::align256(tiles * p.nblk * 4));
+  const char* dbg = getenv("FPVS_HALO_DEBUG");
+  p.dbg = dbg ? atoi(dbg) : 0;
+  return bn == 64 ? halo::launch<64>(p, as_stream(stream)) : halo::launch<128>(p, as_stream(stream));
+}

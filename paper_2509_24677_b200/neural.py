@@ -257,12 +257,20 @@ def pick_bn(cout: int, rows: int, sms: int = 148) -> int:
     return bn
 
 
+def halo_ok(K: int, cin: int, cout: int, dtype=None) -> bool:
+    """Shapes the halo-cached tensor-core conv (fpvs_spconv_halo) takes."""
+    return K == 27 and cin % 64 == 0 and cout % 64 == 0 and cout <= 1024
+
+
 def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int, col_off: int = 0,
-             precision: str = "fp32", act: str | None = None, stream=None, bn: int = 0, masks=None):
+             precision: str = "fp32", act: str | None = None, stream=None, bn: int = 0, masks=None,
+             halo=None, halo_tabs=None):
     """One sparse conv launch: y[:, col_off:col_off+Cout] = act(gather-GEMM(x, table) + b).
 
     ``masks`` are the table's per-tile offset masks (sparse.tile_masks); the
-    tensor-core path computes them here when not given.
+    tensor-core path computes them here when not given.  ``halo`` =
+    (bn, split, workspace) with ``halo_tabs`` (sparse.build_halo) selects the
+    halo-cached kernel for 27-tap layers with 64-multiple channels.
     """
     torch = _torch()
     spec = layer.spec
@@ -271,6 +279,13 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
     if precision == "bf16":
         if table is not None and masks is None:
             masks = sp.tile_masks(table, K, n, cap, stream=stream)
+        if halo is not None and halo_ok(K, spec.in_channels, spec.out_channels, x.dtype):
+            hbn, split, ws = halo
+            _lib.call("fpvs_spconv_halo", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), _lib.ptr(halo_tabs["lnbr"]),
+                      _lib.ptr(halo_tabs["rows"]), _lib.ptr(halo_tabs["n"]), _lib.ptr(masks), _lib.ptr(n), cap,
+                      _lib.ptr(layer.packed(hbn, stream)), hbn, split, _lib.ptr(layer.b), spec.in_channels,
+                      spec.out_channels, a, _lib.ptr(y), ldy, col_off, _lib.ptr(ws), ws.numel(), s)
+            return
         _lib.call("fpvs_spconv_tc", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), K, _lib.ptr(masks), _lib.ptr(n),
                   cap,
                   _lib.ptr(layer.packed(bn, stream)), bn, _lib.ptr(layer.b), spec.in_channels, spec.out_channels, a,

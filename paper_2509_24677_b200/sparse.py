@@ -95,6 +95,49 @@ def build_subm(lv: Level, stream=None):
     tile_masks(lv.nbr, 27, lv.n, lv.cap, lv.nbr_masks, stream)
 
 
+HALO_MAX = 512  # FPVS_HALO_MAX
+
+
+def _halo_tables(lv: Level) -> dict:
+    h = lv.extra.get("halo")
+    if h is None:
+        torch = _torch()
+        tiles = max(1, (lv.cap + 127) // 128)
+        dev = lv.nbr.device
+        h = {"rows": torch.empty((tiles, HALO_MAX), dtype=torch.int32, device=dev),
+             "n": torch.zeros(tiles, dtype=torch.int32, device=dev),
+             "lnbr": torch.empty((tiles, 128 * 27), dtype=torch.int16, device=dev)}
+        lv.extra["halo"] = h
+    return h
+
+
+def build_halo(lv: Level, stream=None) -> dict:
+    """Per 128-row tile: distinct neighbour rows of the level's K = 27 table and
+    the tile-local table (fpvs_kmap_halo) that the halo-cached conv reads."""
+    h = _halo_tables(lv)
+    _lib.call("fpvs_kmap_halo", _lib.ptr(lv.nbr), _lib.ptr(lv.n), lv.cap, _lib.ptr(h["rows"]), _lib.ptr(h["n"]),
+              _lib.ptr(h["lnbr"]), _lib.stream_ptr(stream))
+    return h
+
+
+class HaloBuilder:
+    """Halo tables of several levels in one launch (fpvs_kmap_halo_multi)."""
+
+    def __init__(self, levels):
+        import ctypes as C
+        self.levels = list(levels)
+        arr = (_lib.HaloJob * len(self.levels))()
+        for i, lv in enumerate(self.levels):
+            h = _halo_tables(lv)
+            arr[i].nbr, arr[i].n_dev, arr[i].cap = _lib.ptr(lv.nbr), _lib.ptr(lv.n), lv.cap
+            arr[i].halo_rows, arr[i].halo_n, arr[i].lnbr = _lib.ptr(h["rows"]), _lib.ptr(h["n"]), _lib.ptr(h["lnbr"])
+        self._arr = arr
+        self._ptr = C.addressof(arr)
+
+    def run(self, stream=None):
+        _lib.call("fpvs_kmap_halo_multi", self._ptr, len(self.levels), _lib.stream_ptr(stream))
+
+
 def build_subm_hash(lv: Level, hash_capacity: int | None = None, stream=None):
     """Same table through the open-addressing hash instead of the index volume."""
     torch = _torch()

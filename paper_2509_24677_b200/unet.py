@@ -23,11 +23,13 @@ allocation — and can be captured into a CUDA graph.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
 from . import sparse as sp
-from .neural import packed_cache, pick_bn, run_conv, run_head
+from .neural import halo_ok, packed_cache, pick_bn, run_conv, run_head
 
 
 def _torch():
@@ -128,6 +130,38 @@ class UNetPlan:
         self.bn = {}  # per-layer output-tile width (0 = auto from Cout); see tune()
         self.maps = sp.LevelMaps([self.L0, self.L1, self.L2], [self.down01, self.down12], [self.up10, self.up21],
                                  self.grid_dims, d) if d in (1, 2, 4, 8) else None
+        # 27-tap layers with 64-multiple channels run the halo-cached kernel
+        # (fpvs_spconv_halo); FPVS_HALO=0 keeps them on the plain gather-GEMM
+        self.use_halo = net.precision == "bf16" and os.environ.get("FPVS_HALO", "1") != "0"
+        self.level_of = {"enc0a": self.L0, "enc0b": self.L0, "dec0a": self.L0, "dec0b": self.L0,
+                         "enc1a": self.L1, "enc1b": self.L1, "dec1a": self.L1, "dec1b": self.L1,
+                         "enc2a": self.L2, "enc2b": self.L2}
+        self.halo_cfg = {}
+        self.halo_ws = None
+        self._halo_builder = None
+        if self.use_halo:
+            self.set_halo({k: lv.cap for k, lv in self.level_of.items()})
+
+    def set_halo(self, rows: dict, cfg: dict | None = None):
+        """(bn, split) per halo layer: bn = 128 when Cout allows, split so the
+        layer has about two waves of work units; ``cfg`` overrides."""
+        torch = _torch()
+        self.halo_cfg = {}
+        need = 256
+        for name, r in rows.items():
+            layer = self.net.layers[name]
+            cin, cout = layer.spec.in_channels, layer.spec.out_channels
+            if not halo_ok(27, cin, cout):
+                continue
+            bn = 128 if cout % 128 == 0 else 64
+            split = 1  # K splitting measured slower on config 2 (tools/halo_sweep.py)
+            if cfg and name in cfg:
+                bn, split = cfg[name]
+            self.halo_cfg[name] = (bn, split)
+            cap = self.level_of[name].cap
+            need = max(need, _lib.size("fpvs_spconv_halo_workspace_size", cap, cout, bn, split))
+        if self.halo_ws is None or self.halo_ws.numel() < need:
+            self.halo_ws = torch.zeros(need, dtype=torch.uint8, device=self.L0.coords.device)
 
     def tune(self, bits):
         """Pick per-layer tile widths from one frame's active counts (one host sync).
@@ -140,6 +174,8 @@ class UNetPlan:
         rows = {"enc0a": n0, "enc0b": n0, "down01": n1, "enc1a": n1, "enc1b": n1, "down12": n2, "enc2a": n2,
                 "enc2b": n2, "up21": n1, "dec1a": n1, "dec1b": n1, "up10": n0, "dec0a": n0, "dec0b": n0}
         self.bn = {k: pick_bn(self.net.layers[k].spec.out_channels, v) for k, v in rows.items()}
+        if self.use_halo:
+            self.set_halo({k: rows[k] for k in self.level_of})
         return self.bn
 
     def build_maps(self, bits, gather: bool = False, clear=None):
@@ -147,10 +183,14 @@ class UNetPlan:
         level-0 features, and ``clear`` (the output grid) is zeroed on the way."""
         if self.maps is not None:
             self.maps.run(bits, self.x0 if gather else None, 0, clear)
-            return
-        sp.fill_level_from_bits(self.L0, bits, self.grid_dims, self.net.d)
-        sp.fill_coarse(self.L0, self.L1, self.down01, self.up10)
-        sp.fill_coarse(self.L1, self.L2, self.down12, self.up21)
+        else:
+            sp.fill_level_from_bits(self.L0, bits, self.grid_dims, self.net.d)
+            sp.fill_coarse(self.L0, self.L1, self.down01, self.up10)
+            sp.fill_coarse(self.L1, self.L2, self.down12, self.up21)
+        if self.use_halo:
+            if self._halo_builder is None:
+                self._halo_builder = sp.HaloBuilder([self.L0, self.L1, self.L2])
+            self._halo_builder.run()
 
     def stages(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, maps: bool = True):
         """The frame as an ordered list of (stage name, launch function).
@@ -175,8 +215,12 @@ class UNetPlan:
                                                              out=self.x0)))
 
         def conv(name, x, ldx, table, K, lv, y, ldy, off=0, masks=None):
-            out.append((name, lambda: run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu",
-                                               bn=self.bn.get(name, 0), masks=masks)))
+            def launch():
+                hc = self.halo_cfg.get(name) if K == 27 else None
+                halo = (hc[0], hc[1], self.halo_ws) if hc else None
+                run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu", bn=self.bn.get(name, 0),
+                         masks=masks, halo=halo, halo_tabs=lv.extra.get("halo") if hc else None)
+            out.append((name, launch))
 
         m0, m1, m2 = L0.nbr_masks, L1.nbr_masks, L2.nbr_masks
         dm01, um10 = L1.extra["down_masks"], L1.extra["up_masks"]
