@@ -191,6 +191,41 @@ int fpvs_spconv_tc(const void* x, int ldx, int x_rows, const int32_t* nbr, int K
                    const float* bias, int cin, int cout, int act,
                    void* y, int ldy, int col_off, void* stream);
 
+/* k2s2 up-conv rows grouped by parity (upsort.cu).  In an up table every fine
+ * row has one valid tap (its parity); the rows are stably sorted by that
+ * class, each class padded to a multiple of 128 rows, so each 128-row tile of
+ * the up conv uses one weight slice instead of eight.  Outputs, for
+ * cap_pad = fpvs_up_sort_cap(cap_fine) rows: sorted_table int32 [cap_pad][8]
+ * (the up table in sorted order, -1 rows for padding), perm int32 [cap_pad]
+ * (sorted position -> fine row, -1 for padding), masks uint32 [cap_pad/128]
+ * (1 << class per tile), n_pad_dev (padded row count, device).  Pass them to
+ * fpvs_spconv_tc_scatter with K = 8. */
+typedef struct fpvs_up_sort_job {
+  const int32_t* up;
+  const int32_t* n_fine_dev;
+  int cap_fine;
+  int32_t* sorted_table;
+  int32_t* perm;
+  uint32_t* masks;
+  int32_t* n_pad_dev;
+  void* workspace;
+  size_t workspace_bytes;
+} fpvs_up_sort_job;
+int fpvs_up_sort_cap(int cap_fine);
+size_t fpvs_up_sort_workspace_size(int cap_fine);
+int fpvs_up_sort(const int32_t* up, const int32_t* n_fine_dev, int cap_fine, int32_t* sorted_table,
+                 int32_t* perm, uint32_t* masks, int32_t* n_pad_dev, void* workspace,
+                 size_t workspace_bytes, void* stream);
+int fpvs_up_sort_multi(const fpvs_up_sort_job* jobs, int njobs, void* stream);
+
+/* fpvs_spconv_tc with an output-row map: tile row i is written to row
+ * out_rows[i] of y (skipped when -1).  Used with the parity-sorted up conv. */
+int fpvs_spconv_tc_scatter(const void* x, int ldx, int x_rows, const int32_t* nbr, int K,
+                           const uint32_t* tile_masks, const int32_t* n_out_dev, int cap_out,
+                           const int32_t* out_rows, const void* w_packed, int bn,
+                           const float* bias, int cin, int cout, int act,
+                           void* y, int ldy, int col_off, void* stream);
+
 /* Halo-cached submanifold conv (spconv_halo.cu), same math as
  * fpvs_spconv_tc with K = 27 (neural.py:187-219 on the active set), for
  * Cin and Cout multiples of 64.  Each 128-row tile's distinct neighbour rows

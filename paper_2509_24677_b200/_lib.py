@@ -50,6 +50,11 @@ SIGNATURES = {
     "fpvs_spconv_halo_workspace_size": (_z, [_i, _i, _i, _i]),
     "fpvs_spconv_halo": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _i, _i, _p, _i, _i, _i, _p, _i, _i, _p,
                               _z, _p]),
+    "fpvs_up_sort_cap": (_i, [_i]),
+    "fpvs_up_sort_workspace_size": (_z, [_i]),
+    "fpvs_up_sort": (_i, [_p, _p, _i, _p, _p, _p, _p, _p, _z, _p]),
+    "fpvs_up_sort_multi": (_i, [_p, _i, _p]),
+    "fpvs_spconv_tc_scatter": (_i, [_p, _i, _i, _p, _i, _p, _p, _i, _p, _p, _i, _p, _i, _i, _i, _p, _i, _i, _p]),
     "fpvs_head_simt": (_i, [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p, _p]),
     "fpvs_head_tc": (_i, [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p, _p]),
     "fpvs_loss_sums_size": (_z, [_i, _i]),
@@ -76,6 +81,12 @@ class Level(C.Structure):
 class HaloJob(C.Structure):
     """struct fpvs_halo_job (include/fpvs.h)."""
     _fields_ = [("nbr", _p), ("n_dev", _p), ("cap", _i), ("halo_rows", _p), ("halo_n", _p), ("lnbr", _p)]
+
+
+class UpSortJob(C.Structure):
+    """struct fpvs_up_sort_job (include/fpvs.h)."""
+    _fields_ = [("up", _p), ("n_fine_dev", _p), ("cap_fine", _i), ("sorted_table", _p), ("perm", _p),
+                ("masks", _p), ("n_pad_dev", _p), ("workspace", _p), ("workspace_bytes", _z)]
 
 
 _LIB = None

@@ -51,6 +51,7 @@ struct Params {
   int cin, cout, act;
   __nv_bfloat16* y;
   int ldy, col_off;
+  const int* out_rows;  // tile row -> output row (-1 = skip); NULL = identity
   // head epilogue
   int head;
   const int4* coords;
@@ -413,18 +414,19 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
       const int row = mt * BM + r;
       const bool valid = row < n;
       const int col0 = nb * BN;
+      const long long orow = !valid ? -1 : p.out_rows ? (long long)__ldg(p.out_rows + row) : (long long)row;
       if (!p.head) {
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += 32) {
           float v[32];
           tmem_ld32(tmem_base + tlane + acc * BN + cb, v);
-          if (!valid || col0 + cb >= p.cout) continue;
+          if (!valid || col0 + cb >= p.cout || orow < 0) continue;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             float z = v[i] + s_bias[col0 + cb + i];
             v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
           }
-          uint4* dst = reinterpret_cast<uint4*>(p.y + (long long)row * p.ldy + p.col_off + col0 + cb);
+          uint4* dst = reinterpret_cast<uint4*>(p.y + orow * p.ldy + p.col_off + col0 + cb);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             dst[i] = make_uint4(pack_bf16x2(v[8 * i + 0], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
@@ -650,6 +652,29 @@ extern "C" int fpvs_spconv_tc(const void* x, int ldx, int x_rows, const int32_t*
   p.y = (__nv_bfloat16*)y;
   p.ldy = ldy;
   p.col_off = col_off;
+  return tc::dispatch(p, bn, as_stream(stream));
+}
+
+extern "C" int fpvs_spconv_tc_scatter(const void* x, int ldx, int x_rows, const int32_t* nbr, int K,
+                                      const uint32_t* tile_masks, const int32_t* n_out_dev, int cap_out,
+                                      const int32_t* out_rows, const void* w_packed, int bn, const float* bias,
+                                      int cin, int cout, int act, void* y, int ldy, int col_off, void* stream) {
+  tc::Params p;
+  bn = resolve_bn(bn, cout);
+  FPVS_CHECK_ARG(bn > 0, "tile width must be 0 (auto), 32, 64, 128 or 256");
+  FPVS_CHECK_ARG(out_rows, "null out_rows");
+  int rc = tc_common(p, x, ldx, x_rows, nbr, K, tile_masks, n_out_dev, cap_out, w_packed, bias, cin, cout, bn);
+  if (rc) return rc;
+  FPVS_CHECK_ARG(y, "null output");
+  FPVS_CHECK_ARG(cout % 32 == 0, "tcgen05 store epilogue needs Cout %% 32 == 0, got %d", cout);
+  FPVS_CHECK_ARG(ldy % 8 == 0 && col_off % 8 == 0 && ldy >= col_off + cout, "bad output leading dimension");
+  FPVS_CHECK_ARG(act == FPVS_ACT_NONE || act == FPVS_ACT_RELU, "tcgen05 store epilogue supports none/relu");
+  if (cap_out <= 0) return FPVS_OK;
+  p.act = act;
+  p.y = (__nv_bfloat16*)y;
+  p.ldy = ldy;
+  p.col_off = col_off;
+  p.out_rows = out_rows;
   return tc::dispatch(p, bn, as_stream(stream));
 }
 

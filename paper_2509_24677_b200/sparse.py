@@ -138,6 +138,45 @@ class HaloBuilder:
         _lib.call("fpvs_kmap_halo_multi", self._ptr, len(self.levels), _lib.stream_ptr(stream))
 
 
+def _up_sorted(fine: Level, up) -> dict:
+    u = fine.extra.get("upsort")
+    if u is None:
+        torch = _torch()
+        dev = up.device
+        cap_pad = _lib.size("fpvs_up_sort_cap", fine.cap)
+        u = {"cap": cap_pad,
+             "table": torch.empty((cap_pad, 8), dtype=torch.int32, device=dev),
+             "perm": torch.empty(cap_pad, dtype=torch.int32, device=dev),
+             "masks": torch.empty(max(1, cap_pad // 128), dtype=torch.int32, device=dev),
+             "n": torch.zeros(1, dtype=torch.int32, device=dev),
+             "ws": torch.empty(_lib.size("fpvs_up_sort_workspace_size", fine.cap), dtype=torch.uint8, device=dev),
+             "up": up}
+        fine.extra["upsort"] = u
+    return u
+
+
+class UpSorter:
+    """Parity-sorted up tables of several (fine level, up table) pairs
+    (fpvs_up_sort_multi): each 128-row tile of the sorted order has one class."""
+
+    def __init__(self, pairs):
+        import ctypes as C
+        self.pairs = list(pairs)
+        arr = (_lib.UpSortJob * len(self.pairs))()
+        for i, (fine, up) in enumerate(self.pairs):
+            u = _up_sorted(fine, up)
+            e = arr[i]
+            e.up, e.n_fine_dev, e.cap_fine = _lib.ptr(up), _lib.ptr(fine.n), fine.cap
+            e.sorted_table, e.perm, e.masks, e.n_pad_dev = (_lib.ptr(u["table"]), _lib.ptr(u["perm"]),
+                                                            _lib.ptr(u["masks"]), _lib.ptr(u["n"]))
+            e.workspace, e.workspace_bytes = _lib.ptr(u["ws"]), u["ws"].numel()
+        self._arr = arr
+        self._ptr = C.addressof(arr)
+
+    def run(self, stream=None):
+        _lib.call("fpvs_up_sort_multi", self._ptr, len(self.pairs), _lib.stream_ptr(stream))
+
+
 def build_subm_hash(lv: Level, hash_capacity: int | None = None, stream=None):
     """Same table through the open-addressing hash instead of the index volume."""
     torch = _torch()

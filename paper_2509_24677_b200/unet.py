@@ -139,6 +139,9 @@ class UNetPlan:
         self.halo_cfg = {}
         self.halo_ws = None
         self._halo_builder = None
+        # up convs run on parity-sorted rows (one weight slice per tile); FPVS_UPSORT=0 disables
+        self.use_upsort = net.precision == "bf16" and os.environ.get("FPVS_UPSORT", "1") != "0"
+        self._up_sorter = None
         if self.use_halo:
             self.set_halo({k: lv.cap for k, lv in self.level_of.items()})
 
@@ -187,6 +190,10 @@ class UNetPlan:
             sp.fill_level_from_bits(self.L0, bits, self.grid_dims, self.net.d)
             sp.fill_coarse(self.L0, self.L1, self.down01, self.up10)
             sp.fill_coarse(self.L1, self.L2, self.down12, self.up21)
+        if self.use_upsort:
+            if self._up_sorter is None:
+                self._up_sorter = sp.UpSorter([(self.L1, self.up21), (self.L0, self.up10)])
+            self._up_sorter.run()
         if self.use_halo:
             if self._halo_builder is None:
                 self._halo_builder = sp.HaloBuilder([self.L0, self.L1, self.L2])
@@ -218,6 +225,11 @@ class UNetPlan:
             def launch():
                 hc = self.halo_cfg.get(name) if K == 27 else None
                 halo = (hc[0], hc[1], self.halo_ws) if hc else None
+                us = lv.extra.get("upsort") if (self.use_upsort and name in ("up21", "up10")) else None
+                if us is not None:
+                    run_conv(L[name], x, ldx, us["table"], K, us["n"], us["cap"], y, ldy, off, P, act="relu",
+                             bn=self.bn.get(name, 0), masks=us["masks"], out_rows=us["perm"])
+                    return
                 run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu", bn=self.bn.get(name, 0),
                          masks=masks, halo=halo, halo_tabs=lv.extra.get("halo") if hc else None)
             out.append((name, launch))
