@@ -243,18 +243,27 @@ constexpr int W_EPI = 12;   // warps 12..15: epilogue
 constexpr int THREADS = 512;
 constexpr int LOADERS = 64;
 
+// Pipeline stage = G = 2 K-chunks: two TMEM A slots (one per builder group)
+// + two weight chunks in smem; one full/empty barrier pair and one commit per
+// stage (tcgen05 commits measured ~70-150 cycles each at N <= 128).
+// BN = 256 keeps a single accumulator (256 TMEM columns) and a single halo
+// buffer (its smem goes to the 32 KB weight chunks).
 template <int BN>
 struct Cfg {
-  static constexpr int NS = BN == 64 ? 8 : 4;  // stages: TMEM A slot + smem B chunk
+  static constexpr int G = BN == 64 ? 2 : 1;  // chunks per stage (BN >= 128: deeper weight prefetch instead)
+  static constexpr int NACC = BN == 256 ? 1 : 2;
+  static constexpr int NHB = BN == 256 ? 1 : 2;
+  static constexpr int NS = 4;
   static constexpr int B_SUB = BN * 128;
-  static constexpr int ACOL = 2 * BN;          // TMEM: [acc0 | acc1 | A slots]
-  static constexpr int B_OFF = 2 * HBUF;
-  static constexpr int BAR_OFF = B_OFF + NS * B_SUB;
-  static constexpr int NBARS = 2 * NS + 10;
+  static constexpr int STAGE_B = G * B_SUB;
+  static constexpr int ACOL = NACC * BN;  // TMEM: [accumulators | A slots]
+  static constexpr int B_OFF = NHB * HBUF;
+  static constexpr int BAR_OFF = B_OFF + NS * STAGE_B;
+  static constexpr int NBARS = 2 * NS + 2 * NACC + 3 * NHB;
   static constexpr int CTRL_OFF = BAR_OFF + 8 * NBARS;
   static constexpr int BIAS_OFF = CTRL_OFF + 64;
   static constexpr int SMEM = 1024 + BIAS_OFF + 4 * 1024;
-  static_assert(ACOL + NS * 32 <= 512, "TMEM columns");
+  static_assert(ACOL + NS * G * 32 <= 512, "TMEM columns");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -281,6 +290,25 @@ __device__ __forceinline__ void unit_of(const Params& p, int u, int cpo, Unit& U
 __device__ __forceinline__ int first_offset(uint32_t mask, int rank) { return (int)__fns(mask, 0, rank + 1); }
 __device__ __forceinline__ int next_offset(uint32_t mask, int j) { return __ffs(mask & ~((2u << j) - 1u)) - 1; }
 
+// chunk iterator over a unit's K range: q -> (channel chunk c, offset j)
+struct ChunkWalk {
+  uint32_t mask;
+  int npres, c, j;
+  __device__ __forceinline__ void start(const Unit& U) {
+    mask = U.mask;
+    npres = U.npres;
+    c = U.q0 / npres;
+    j = first_offset(mask, U.q0 - c * npres);
+  }
+  __device__ __forceinline__ void next() {
+    j = next_offset(mask, j);
+    if (j < 0) {
+      ++c;
+      j = __ffs(mask) - 1;
+    }
+  }
+};
+
 template <int BN>
 __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p) {
   using C = Cfg<BN>;
@@ -292,10 +320,10 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   uint64_t* full = bars;
   uint64_t* empty = bars + C::NS;
   uint64_t* tfull = bars + 2 * C::NS;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* hfull = tempty + 2;
-  uint64_t* hempty = hfull + 2;
-  uint64_t* hmeta = hempty + 2;  // the tile's local table + halo row list landed (bulk copy)
+  uint64_t* tempty = tfull + C::NACC;
+  uint64_t* hfull = tempty + C::NACC;
+  uint64_t* hempty = hfull + C::NHB;
+  uint64_t* hmeta = hempty + C::NHB;  // the tile's local table + halo row list landed (bulk copy)
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::CTRL_OFF);
   volatile int* s_last = reinterpret_cast<volatile int*>(smem + C::CTRL_OFF + 16);
   float* s_bias = reinterpret_cast<float*>(smem + C::BIAS_OFF);
@@ -309,12 +337,14 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
 
   if (tid == 0) {
     for (int s = 0; s < C::NS; ++s) {
-      mbar_init(smem_u32(full + s), 4 + 1);  // one builder group (4 warps) + the weight loader
+      mbar_init(smem_u32(full + s), 4 * C::G + 1);  // builder warps (4 per chunk) + the weight loader
       mbar_init(smem_u32(empty + s), 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < C::NACC; ++a) {
       mbar_init(smem_u32(tfull + a), 1);
       mbar_init(smem_u32(tempty + a), 4);
+    }
+    for (int a = 0; a < C::NHB; ++a) {
       mbar_init(smem_u32(hfull + a), LOADERS);
       mbar_init(smem_u32(hempty + a), 8);
       mbar_init(smem_u32(hmeta + a), 1);
@@ -335,26 +365,30 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
 
   if (warp < W_LOAD) {
     // ===================== A builders =====================
+    // group bg builds chunk slot bg of every stage (chunks i with i % 2 == bg)
     const int bg = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t t_a = tmem_base + ((uint32_t)(q4 * 32) << 16) + C::ACOL;
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u;
-    uint32_t kc = 0, gc = 0;
+    uint32_t sc0 = 0, gc = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
       unit_of(p, u, cpo, U);
-      for (int c = U.q0 / U.npres; U.q1 > U.q0 && c * U.npres < U.q1; ++c) {
+      const int nq = U.q1 - U.q0;
+      for (int c = U.q0 / U.npres; nq > 0 && c * U.npres < U.q1; ++c) {
         const int qs = max(U.q0, c * U.npres), qe = min(U.q1, (c + 1) * U.npres);
-        const int hb = gc & 1;
-        mbar_wait(smem_u32(hmeta + hb), (gc >> 1) & 1);
-        mbar_wait(smem_u32(hfull + hb), (gc >> 1) & 1);
+        const int hb = gc % C::NHB;
+        const uint32_t hph = (gc / C::NHB) & 1;
+        mbar_wait(smem_u32(hmeta + hb), hph);
+        mbar_wait(smem_u32(hfull + hb), hph);
         if (lane == 0 && q4 == 0) HTS(256 + 4 * gc + 2 * bg);
         const uint8_t* hbuf = smem + hb * HBUF;
         const int16_t* ln = reinterpret_cast<const int16_t*>(hbuf + HALO_BYTES) + r * KOFF;
         int j = first_offset(U.mask, qs - c * U.npres);
-        for (int q = qs; q < qe; ++q, ++kc, j = next_offset(U.mask, j)) {
-          if ((int)(kc & 1) != bg) continue;
-          const int stage = (int)(kc % C::NS);
-          const uint32_t ph = (kc / C::NS) & 1;
+        for (int q = qs; q < qe; ++q, j = next_offset(U.mask, j)) {
+          const int i = q - U.q0;
+          if ((i & 1) != bg) continue;
+          const uint32_t st = sc0 + i / C::G;
+          const int stage = (int)(st % C::NS);
           const int li = ln[j];
           uint32_t v[32];
           if (li >= 0) {
@@ -367,7 +401,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
             }
           } else if (li == -1) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0u;
+            for (int k = 0; k < 32; ++k) v[k] = 0u;
           } else {
             const int g = __ldg(p.nbr + ((long long)U.mt * BM + r) * KOFF + j);
             const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(p.x) +
@@ -378,22 +412,28 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
               v[4 * pc] = t4.x; v[4 * pc + 1] = t4.y; v[4 * pc + 2] = t4.z; v[4 * pc + 3] = t4.w;
             }
           }
-          if (lane == 0 && q4 == 0) HTS(1024 + 3 * kc);
-          mbar_wait(smem_u32(empty + stage), ph ^ 1);
-          if (lane == 0 && q4 == 0) HTS(1025 + 3 * kc);
+          mbar_wait(smem_u32(empty + stage), ((st / C::NS) & 1) ^ 1);
           tc_fence_after();
-          tmem_st32(t_a + stage * 32, v);
+          tmem_st32(t_a + (stage * C::G + i % C::G) * 32, v);
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(full + stage));
-          if (lane == 0 && q4 == 0) HTS(1026 + 3 * kc);
+          if (lane == 0 && q4 == 0 && st < 1400) HTS(1024 + 2 * st + bg);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(hempty + hb));
-        if (lane == 0 && q4 == 0) HTS(257 + 4 * gc + 2 * bg);
         ++gc;
       }
+      const uint32_t nst = (nq + C::G - 1) / C::G;
+      if (C::G == 2 && (nq & 1) && bg == 1) {
+        // odd chunk count: slot 1 of the unit's last stage stays empty
+        const uint32_t st = sc0 + nst - 1;
+        mbar_wait(smem_u32(empty + st % C::NS), ((st / C::NS) & 1) ^ 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(full + st % C::NS));
+      }
+      sc0 += nst;
     }
   } else if (warp < W_B) {
     // ===================== halo loaders =====================
@@ -405,8 +445,9 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       Unit U;
       unit_of(p, u, cpo, U);
       for (int c = U.q0 / U.npres; U.q1 > U.q0 && c * U.npres < U.q1; ++c) {
-        const int hb = gc & 1;
-        mbar_wait_sleep(smem_u32(hempty + hb), ((gc >> 1) & 1) ^ 1, 64);
+        const int hb = gc % C::NHB;
+        const uint32_t hph = (gc / C::NHB) & 1;
+        mbar_wait_sleep(smem_u32(hempty + hb), hph ^ 1, 64);
         if (tl == 0) HTS(16 + 3 * gc);
         uint8_t* hbuf = smem + hb * HBUF;
         const int H = __ldg(p.halo_n + U.mt);
@@ -418,7 +459,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
           bulk_g2s(smem_u32(hbuf + HALO_BYTES), p.lnbr + (long long)U.mt * BM * KOFF, LNBR_BYTES, mb);
           if (rb) bulk_g2s(smem_u32(hbuf + ROWS_OFF), p.halo_rows + (long long)U.mt * HMAX, rb, mb);
         }
-        mbar_wait(smem_u32(hmeta + hb), (gc >> 1) & 1);
+        mbar_wait(smem_u32(hmeta + hb), hph);
         if (tl == 0) HTS(17 + 3 * gc);
         const int* hr = reinterpret_cast<const int*>(hbuf + ROWS_OFF);
         const char* xb = reinterpret_cast<const char*>(p.x) + c * 128 + pc * 16;
@@ -436,21 +477,24 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   } else if (warp == W_B) {
     // ===================== weight loader =====================
     if (lane == 0) {
-      uint32_t kc = 0;
+      uint32_t st = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
         unit_of(p, u, cpo, U);
+        const int nq = U.q1 - U.q0;
         const uint8_t* wblk = p.wpk + (size_t)U.nb * p.nchunks * C::B_SUB;
-        for (int c = U.q0 / U.npres; c * U.npres < U.q1; ++c) {
-          const int qs = max(U.q0, c * U.npres), qe = min(U.q1, (c + 1) * U.npres);
-          int j = first_offset(U.mask, qs - c * U.npres);
-          for (int q = qs; q < qe; ++q, ++kc, j = next_offset(U.mask, j)) {
-            const int stage = (int)(kc % C::NS);
-            mbar_wait(smem_u32(empty + stage), ((kc / C::NS) & 1) ^ 1);
-            const uint32_t fb = smem_u32(full + stage);
-            mbar_arrive_expect_tx(fb, C::B_SUB);
-            bulk_g2s(smem_u32(sB + stage * C::B_SUB), wblk + (size_t)(j * cpo + c) * C::B_SUB, C::B_SUB, fb);
-          }
+        ChunkWalk w;
+        w.start(U);
+        for (int i = 0; i < nq; i += C::G, ++st) {
+          const int stage = (int)(st % C::NS);
+          const int nv = min(C::G, nq - i);
+          mbar_wait(smem_u32(empty + stage), ((st / C::NS) & 1) ^ 1);
+          if (st < 1000) HTS(5000 + st);
+          const uint32_t fb = smem_u32(full + stage);
+          mbar_arrive_expect_tx(fb, nv * C::B_SUB);
+          for (int g = 0; g < nv; ++g, w.next())
+            bulk_g2s(smem_u32(sB + stage * C::STAGE_B + g * C::B_SUB), wblk + (size_t)(w.j * cpo + w.c) * C::B_SUB,
+                     C::B_SUB, fb);
         }
       }
     }
@@ -458,29 +502,32 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     // ===================== MMA issuer =====================
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16<BN>();
-      uint32_t kc = 0;
+      uint32_t st = 0;
       int it = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
         Unit U;
         unit_of(p, u, cpo, U);
-        const int acc = it & 1;
-        mbar_wait(smem_u32(tempty + acc), ((it >> 1) & 1) ^ 1);
+        const int nq = U.q1 - U.q0;
+        const int acc = it % C::NACC;
+        mbar_wait(smem_u32(tempty + acc), ((it / C::NACC) & 1) ^ 1);
         HTS(7000 + 2 * it);
         tc_fence_after();
         const uint32_t dtm = tmem_base + acc * BN;
-        bool first = true;
-        for (int q = U.q0; q < U.q1; ++q, ++kc) {
-          const int stage = (int)(kc % C::NS);
-          mbar_wait(smem_u32(full + stage), (kc / C::NS) & 1);
-          HTS(4096 + 2 * kc);
+        for (int i = 0; i < nq; i += C::G, ++st) {
+          const int stage = (int)(st % C::NS);
+          const int nv = min(C::G, nq - i);
+          mbar_wait(smem_u32(full + stage), (st / C::NS) & 1);
+          if (st < 450) HTS(4096 + 2 * st);
           tc_fence_after();
-          const uint32_t ta = tmem_base + C::ACOL + stage * 32;
-          const uint64_t bd = sw128_desc(smem_u32(sB + stage * C::B_SUB));
+          for (int g = 0; g < nv; ++g) {
+            const uint32_t ta = tmem_base + C::ACOL + (stage * C::G + g) * 32;
+            const uint64_t bd = sw128_desc(smem_u32(sB + stage * C::STAGE_B + g * C::B_SUB));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) umma_bf16_ts(dtm, ta + 8 * k, bd + 2 * k, idesc, (first && k == 0) ? 0u : 1u);
-          first = false;
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_ts(dtm, ta + 8 * k, bd + 2 * k, idesc, (i == 0 && g == 0 && k == 0) ? 0u : 1u);
+          }
           umma_commit(smem_u32(empty + stage));
-          HTS(4097 + 2 * kc);
+          if (st < 450) HTS(4097 + 2 * st);
         }
         umma_commit(smem_u32(tfull + acc));
         HTS(7001 + 2 * it);
@@ -494,8 +541,8 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
       Unit U;
       unit_of(p, u, cpo, U);
-      const int acc = it & 1;
-      mbar_wait_sleep(smem_u32(tfull + acc), (it >> 1) & 1, 128);
+      const int acc = it % C::NACC;
+      mbar_wait_sleep(smem_u32(tfull + acc), (it / C::NACC) & 1, 128);
       if (q4 == 0 && lane == 0) HTS(7200 + 2 * it);
       tc_fence_after();
       const long long row = (long long)U.mt * BM + r;
@@ -522,57 +569,66 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
       } else {
+        // split K: fp32 partial per split, column-major [col][128 rows] so a
+        // warp's stores and loads are 128-byte coalesced; the last CTA of the
+        // tile to arrive sums the splits in a fixed order (deterministic),
+        // taking its own split from TMEM
         const long long slot = (long long)U.mt * p.nblk + U.nb;
-        float* mine = p.part + ((slot * p.split + U.s) * BM + r) * BN;
         const bool has = U.q1 > U.q0;
+        float* mine = p.part + (slot * p.split + U.s) * BM * BN + r;
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += 32) {
           float v[32];
           tmem_ld32(tmem_base + tlane + acc * BN + cb, v);
-          float4* dst = reinterpret_cast<float4*>(mine + cb);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dst[i] = has ? make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3])
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int i = 0; i < 32; ++i) __stcg(mine + (cb + i) * BM, has ? v[i] : 0.f);
+        }
+        named_bar(1, 128);
+        if (q4 == 0 && lane == 0) HTS(7400 + 4 * it);
+        if (warp == W_EPI && lane == 0) {
+          __threadfence();  // release the CTA's partial (ordered after the barrier) before the count
+          const int last = atomicAdd(p.counters + slot, 1) == p.split - 1;
+          if (last) __threadfence();  // acquire the other splits' partials
+          *s_last = last;
+        }
+        named_bar(1, 128);
+        if (q4 == 0 && lane == 0) HTS(7402 + 4 * it);
+        if (*s_last) {
+          const float* base = p.part + slot * p.split * BM * BN + r;
+#pragma unroll 1
+          for (int cb = 0; cb < BN; cb += 32) {
+            float own[32], v[32];
+            tmem_ld32(tmem_base + tlane + acc * BN + cb, own);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            for (int ss = 0; ss < p.split; ++ss) {
+              const float* src = base + (long long)ss * BM * BN + cb * BM;
+              if (ss == U.s) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] += has ? own[i] : 0.f;
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] += __ldcg(src + i * BM);
+              }
+            }
+            if (!valid) continue;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float z = v[i] + s_bias[col0 + cb + i];
+              v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
+            }
+            uint4* dst = reinterpret_cast<uint4*>(p.y + row * p.ldy + p.col_off + col0 + cb);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(pack_bf16x2(v[8 * i + 0], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                                  pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+          }
+          if (warp == W_EPI && lane == 0) p.counters[slot] = 0;
+          if (q4 == 0 && lane == 0) HTS(7403 + 4 * it);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
-        __threadfence();
-        named_bar(1, 128);
-        if (warp == W_EPI && lane == 0) *s_last = atomicAdd(p.counters + slot, 1) == p.split - 1;
-        named_bar(1, 128);
-        if (*s_last) {
-          __threadfence();
-          if (valid) {
-            const float* base = p.part + (slot * p.split * BM + r) * BN;
-#pragma unroll 1
-            for (int cb = 0; cb < BN; cb += 32) {
-              float v[32];
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = 0.f;
-              for (int ss = 0; ss < p.split; ++ss) {
-                const float4* src = reinterpret_cast<const float4*>(base + (long long)ss * BM * BN + cb);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const float4 t4 = __ldcg(src + i);
-                  v[4 * i] += t4.x; v[4 * i + 1] += t4.y; v[4 * i + 2] += t4.z; v[4 * i + 3] += t4.w;
-                }
-              }
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const float z = v[i] + s_bias[col0 + cb + i];
-                v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
-              }
-              uint4* dst = reinterpret_cast<uint4*>(p.y + row * p.ldy + p.col_off + col0 + cb);
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                dst[i] = make_uint4(pack_bf16x2(v[8 * i + 0], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
-                                    pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
-            }
-          }
-          if (warp == W_EPI && lane == 0) p.counters[slot] = 0;
-        }
       }
     }
   }
@@ -649,7 +705,7 @@ extern "C" int fpvs_kmap_halo(const int32_t* nbr, const int32_t* n_dev, int cap,
 }
 
 extern "C" size_t fpvs_spconv_halo_workspace_size(int cap, int cout, int bn, int split) {
-  if (cap < 1 || (bn != 64 && bn != 128) || cout % bn || split < 1) return 0;
+  if (cap < 1 || (bn != 64 && bn != 128 && bn != 256) || cout % bn || split < 1) return 0;
   const size_t tiles = (cap + tc::BM - 1) / tc::BM, nblk = cout / bn;
   size_t b = halo::align256(tiles * nblk * 4);
   if (split > 1) b += tiles * nblk * split * tc::BM * bn * 4;
@@ -663,9 +719,9 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
                                 void* ws, size_t ws_bytes, void* stream) {
   FPVS_CHECK_ARG(x && nbr && lnbr && halo_rows && halo_n && tile_masks && n_dev && w_packed && y,
                  "null pointer");
-  if (bn == 0) bn = cout % 128 == 0 ? 128 : 64;
+  if (bn == 0) bn = cout % 256 == 0 ? 256 : cout % 128 == 0 ? 128 : 64;
   if (split == 0) split = 1;
-  FPVS_CHECK_ARG(bn == 64 || bn == 128, "halo conv tile width must be 64 or 128");
+  FPVS_CHECK_ARG(bn == 64 || bn == 128 || bn == 256, "halo conv tile width must be 64, 128 or 256");
   FPVS_CHECK_ARG(cin % 64 == 0 && cin >= 64, "halo conv needs Cin %% 64 == 0, got %d", cin);
   FPVS_CHECK_ARG(cout % bn == 0 && cout <= 1024, "halo conv needs Cout %% %d == 0, got %d", bn, cout);
   FPVS_CHECK_ARG(ldx % 8 == 0 && ldx >= cin, "bad input leading dimension");
@@ -702,5 +758,7 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
   p.part = (float*)((uint8_t*)ws + halo::align256(tiles * p.nblk * 4));
   const char* dbg = getenv("FPVS_HALO_DEBUG");
   p.dbg = dbg ? atoi(dbg) : 0;
-  return bn == 64 ? halo::launch<64>(p, as_stream(stream)) : halo::launch<128>(p, as_stream(stream));
+  if (bn == 64) return halo::launch<64>(p, as_stream(stream));
+  if (bn == 128) return halo::launch<128>(p, as_stream(stream));
+  return halo::launch<256>(p, as_stream(stream));
 }

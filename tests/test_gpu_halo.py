@@ -143,7 +143,8 @@ def _rows(n, c, seed, cap):
 
 @pytest.mark.parametrize("cin,cout,bn,split", [(64, 64, 64, 1), (64, 64, 64, 2), (128, 64, 64, 1), (64, 128, 128, 1),
                                                (128, 128, 128, 3), (256, 128, 128, 1), (256, 256, 128, 5),
-                                               (256, 256, 64, 2), (128, 128, 64, 8)])
+                                               (256, 256, 64, 2), (128, 128, 64, 8), (256, 256, 256, 1),
+                                               (256, 256, 256, 3), (128, 256, 256, 2), (64, 64, 64, 3)])
 def test_halo_conv_vs_oracle(cin, cout, bn, split):
     import torch
     from paper_2509_24677_b200 import sparse as sp

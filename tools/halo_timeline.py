@@ -1,4 +1,6 @@
-"""Per-role timestamps of the halo conv for CTA 0 (FPVS_HALO_DEBUG=1)."""
+"""Per-role timestamps of the halo conv for CTA 0 (FPVS_HALO_DEBUG=1).
+
+LAYERS=enc0b,enc1a,enc2a  HALO_CFG="64,1;128,1;256,1" (bn,split per level)."""
 import ctypes
 import os
 import sys
@@ -16,6 +18,11 @@ occ = synth.config2_grid(1)
 bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
 plan = PvsUNet(seed=1).plan(1, occ.shape)
 plan.tune(bits)
+cfg = os.environ.get("HALO_CFG")
+if cfg:
+    per = [tuple(int(v) for v in c.split(",")) for c in cfg.split(";")]
+    rows = {k: lv.count() for k, lv in plan.level_of.items()}
+    plan.set_halo(rows, {k: per[int(k[-2])] for k in rows})
 out = torch.empty(occ.size // 8, dtype=torch.uint8, device="cuda")
 plan.run(bits, out, 0.5)
 stages = dict(plan.stages(bits, out, 0.5))
@@ -31,28 +38,30 @@ for name in os.environ.get("LAYERS", "enc0b,enc1a,enc2a").split(","):
     t = np.frombuffer(buf, dtype=np.uint64)[:8192].astype(np.int64)
     t0 = t[0]
     rel = lambda v: (v - t0) / 1000.0 if v else float("nan")  # noqa: E731
-    print(f"=== {name} cfg {plan.halo_cfg.get(name)}  start->setup {rel(t[1]):.2f}  main end {rel(t[2]):.2f}  "
+    print(f"=== {name} cfg {plan.halo_cfg.get(name)}  setup {rel(t[1]):.2f}  main end {rel(t[2]):.2f}  "
           f"exit {rel(t[3]):.2f} us")
-    for g in range(8):
+    for g in range(6):
         if not t[16 + 3 * g]:
             break
-        print(f"  group {g}: loader hempty {rel(t[16 + 3 * g]):7.2f} meta {rel(t[17 + 3 * g]):7.2f} "
-              f"issued {rel(t[18 + 3 * g]):7.2f} | builders ready g0 {rel(t[256 + 4 * g]):7.2f} "
-              f"g1 {rel(t[258 + 4 * g]):7.2f} done g0 {rel(t[257 + 4 * g]):7.2f} g1 {rel(t[259 + 4 * g]):7.2f}")
-    for it in range(8):
+        print(f"  halo group {g}: loader hempty {rel(t[16 + 3 * g]):7.2f} meta {rel(t[17 + 3 * g]):7.2f} "
+              f"issued {rel(t[18 + 3 * g]):7.2f} | builders ready g0 {rel(t[256 + 4 * g]):7.2f} g1 {rel(t[258 + 4 * g]):7.2f}")
+    for it in range(6):
         if not t[7000 + 2 * it]:
             break
         print(f"  unit {it}: mma tempty {rel(t[7000 + 2 * it]):7.2f} tfull {rel(t[7001 + 2 * it]):7.2f} "
-              f"epi got {rel(t[7200 + 2 * it]):7.2f}")
-    kc = 0
+              f"epi got {rel(t[7200 + 2 * it]):7.2f} | split: partial written {rel(t[7400 + 4 * it]):7.2f} "
+              f"counted {rel(t[7402 + 4 * it]):7.2f} "
+              f"reduced {rel(t[7403 + 4 * it]):7.2f}")
     rows = []
-    while t[4096 + 2 * kc] and kc < 1000:
-        rows.append((rel(t[1024 + 3 * kc]), rel(t[1025 + 3 * kc]), rel(t[1026 + 3 * kc]), rel(t[4096 + 2 * kc]),
-                     rel(t[4097 + 2 * kc])))
-        kc += 1
+    st = 0
+    while st < 450 and t[4096 + 2 * st]:
+        rows.append((rel(t[5000 + st]), rel(t[1024 + 2 * st]), rel(t[1025 + 2 * st]), rel(t[4096 + 2 * st]),
+                     rel(t[4097 + 2 * st])))
+        st += 1
     r = np.array(rows)
-    print(f"  chunks {kc}: mma full-wait-done interval mean {np.nanmean(np.diff(r[:, 3])):.3f} us; "
-          f"builder lds->arrive mean {np.nanmean(r[:, 2] - r[:, 0]):.3f}; empty wait mean "
-          f"{np.nanmean(r[:, 1] - r[:, 0]):.3f}; arrive->mma mean {np.nanmean(r[:, 3] - r[:, 2]):.3f}")
-    for i in list(range(0, min(kc, 12))) + list(range(26, min(kc, 34))):
-        print("   kc %3d  lds %7.2f empty %7.2f arrive %7.2f | mma full %7.2f commit %7.2f" % ((i,) + rows[i]))
+    bmax = np.fmax(r[:, 1], r[:, 2])
+    print(f"  stages {st}: mma start interval {np.nanmean(np.diff(r[:, 3])):.3f} us | mma start - last builder "
+          f"{np.nanmean(r[:, 3] - bmax):.3f} | mma start - B issue {np.nanmean(r[:, 3] - r[:, 0]):.3f} | "
+          f"issue->commit {np.nanmean(r[:, 4] - r[:, 3]):.3f}")
+    for i in list(range(0, min(st, 10))) + list(range(max(10, st - 4), st)):
+        print("   st %3d  B issued %7.2f | built g0 %7.2f g1 %7.2f | mma start %7.2f commit %7.2f" % ((i,) + rows[i]))
