@@ -226,13 +226,15 @@ struct Params {
 };
 
 // ---------------- profiling timestamps (FPVS_HALO_DEBUG) ----------------
-__device__ unsigned long long g_hts[2][8192];
+__device__ unsigned long long g_hts[2][8192];   // CTAs (dbg >> 8) and (dbg >> 8) + 1
+__device__ unsigned long long g_hcta[2][160];  // per-CTA start / end
+__device__ unsigned g_hsm[160];
 #define HTS(slot)                                                                        \
   do {                                                                                   \
-    if (p.dbg && blockIdx.x < 2 && (slot) < 8192) {                                     \
+    if (p.dbg && blockIdx.x - (unsigned)(p.dbg >> 8) < 2u && (slot) < 8192) {          \
       unsigned long long t_;                                                             \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
-      g_hts[blockIdx.x][(slot)] = t_;                                                    \
+      g_hts[blockIdx.x - (p.dbg >> 8)][(slot)] = t_;                                     \
     }                                                                                    \
   } while (0)
 
@@ -330,6 +332,14 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) HTS(0);
+  if (p.dbg && tid == 0 && blockIdx.x < 160) {
+    unsigned long long t_;
+    unsigned sm_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));
+    g_hcta[0][blockIdx.x] = t_;
+    g_hsm[blockIdx.x] = sm_;
+  }
   const int n = min(*p.n_dev, p.cap);
   const int mtiles = (n + BM - 1) / BM;
   const int nunits = mtiles * p.nblk * p.split;
@@ -637,6 +647,11 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   tc_fence_before();
   __syncthreads();
   if (tid == 0) HTS(3);
+  if (p.dbg && tid == 0 && blockIdx.x < 160) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    g_hcta[1][blockIdx.x] = t_;
+  }
   if (warp == W_MMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
@@ -670,6 +685,13 @@ using namespace fpvs;
 extern "C" int fpvs_debug_halo_timestamps(unsigned long long* host, int n) {
   if (n > 2 * 8192) n = 2 * 8192;
   return cudaMemcpyFromSymbol(host, halo::g_hts, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 3;
+}
+
+extern "C" int fpvs_debug_halo_cta_times(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, halo::g_hcta, sizeof(unsigned long long) * 320) == cudaSuccess ? 0 : 3;
+}
+extern "C" int fpvs_debug_halo_smid(unsigned* host) {
+  return cudaMemcpyFromSymbol(host, halo::g_hsm, sizeof(unsigned) * 160) == cudaSuccess ? 0 : 3;
 }
 
 extern "C" size_t fpvs_kmap_halo_size(int cap) {

@@ -5,7 +5,7 @@ import ctypes
 import os
 import sys
 
-os.environ["FPVS_HALO_DEBUG"] = "1"
+os.environ.setdefault("FPVS_HALO_DEBUG", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -35,6 +35,23 @@ for name in os.environ.get("LAYERS", "enc0b,enc1a,enc2a").split(","):
         stages[name]()
         torch.cuda.synchronize()
     lib.fpvs_debug_halo_timestamps(buf, 2 * 8192)
+    cta = (ctypes.c_ulonglong * 320)()
+    if hasattr(lib, "fpvs_debug_halo_cta_times"):
+        lib.fpvs_debug_halo_cta_times(cta)
+    ca = np.frombuffer(cta, dtype=np.uint64).astype(np.int64).reshape(2, 160)
+    ok = (ca[0] > 0) & (ca[1] > ca[0])
+    st_, en_ = ca[0][ok], ca[1][ok]
+    if len(st_):
+        t00 = st_.min()
+        d = (en_ - st_) / 1000.0
+        print(f"  CTAs {ok.sum()}: launch span {(en_.max() - t00) / 1000:.2f} us; start spread {(st_.max() - t00) / 1000:.2f} us; "
+              f"CTA duration min {d.min():.2f} median {np.median(d):.2f} max {d.max():.2f} us")
+        idx = np.nonzero(ok)[0]
+        print("   durations by CTA:", " ".join(f"{i}:{x:.1f}" for i, x in zip(idx[:40], d[:40])))
+        sm = (ctypes.c_uint * 160)()
+        if hasattr(lib, "fpvs_debug_halo_smid"):
+            lib.fpvs_debug_halo_smid(sm)
+            print("   smid:", " ".join(str(v) for v in list(sm)[:40]))
     t = np.frombuffer(buf, dtype=np.uint64)[:8192].astype(np.int64)
     t0 = t[0]
     rel = lambda v: (v - t0) / 1000.0 if v else float("nan")  # noqa: E731
@@ -65,3 +82,11 @@ for name in os.environ.get("LAYERS", "enc0b,enc1a,enc2a").split(","):
           f"issue->commit {np.nanmean(r[:, 4] - r[:, 3]):.3f}")
     for i in list(range(0, min(st, 10))) + list(range(max(10, st - 4), st)):
         print("   st %3d  B issued %7.2f | built g0 %7.2f g1 %7.2f | mma start %7.2f commit %7.2f" % ((i,) + rows[i]))
+    if os.environ.get("PEER"):
+        t1 = np.frombuffer(buf, dtype=np.uint64)[8192:].astype(np.int64)
+        rel1 = lambda v: (v - t0) / 1000.0 if v else float("nan")  # noqa: E731
+        print("  peer CTA (block 1), same clock:")
+        for i in range(0, 10):
+            print("   st %3d  B issued %7.2f | built g0 %7.2f g1 %7.2f | full seen %7.2f forwarded %7.2f" % (
+                i, rel1(t1[5000 + i]), rel1(t1[1024 + 2 * i]), rel1(t1[1025 + 2 * i]), rel1(t1[4096 + 2 * i]),
+                rel1(t1[4097 + 2 * i])))
