@@ -5,7 +5,8 @@ Workload (BASELINE config 2): one 256^3 froxel grid per step per GPU (4000
 seeded boxes, edges 1-12, seed 1), interleave d=4 -> 64^3 cells x 64 ch,
 3-level sparse U-Net (64/128/256 ch), bf16 activations/weights with fp32
 accumulation, fused sigmoid + threshold + deinterleave bit-pack.  A step is
-one whole frame: kernel maps (3 levels), sparse interleave, 14 convs, head.
+one whole frame: kernel maps (3 levels + parity-sorted up tables + per-tile
+halo tables), sparse interleave, 14 convs, head.
 
 * ``value``: frames with the packed input already in HBM, each step replayed
   from one CUDA graph; L2 is flushed (256 MiB memset, untimed) before every
@@ -13,9 +14,10 @@ one whole frame: kernel maps (3 levels), sparse interleave, 14 convs, head.
 * ``e2e``: the same frames through ``FramePipeline.infer`` — pinned host
   packed grid -> H2D -> frame -> D2H packed PVS — every copy inside the
   timed region.
-* ``roofline``: the dominant kernel (the tcgen05 gather-GEMM, spconv_tc, 14
-  launches per frame): algorithmic FLOPs (2 * present pairs * Cin * Cout;
-  zero-filled taps not counted) / its summed per-launch DEVICE time.  Each
+* ``roofline``: the dominant kernel, the tcgen05 sparse conv (14 launches per
+  frame: 10 halo-cached subm convs, spconv_halo, and 4 down/up gather-GEMMs,
+  spconv_tc): algorithmic FLOPs (2 * present pairs * Cin * Cout; zero-filled
+  taps not counted) / its summed per-launch DEVICE time.  Each
   stage of the frame is captured alone as a CUDA graph of 20 back-to-back
   launches and timed with CUDA events on its stream (host launch gaps
   excluded); peak = MEASURED_PEAKS.json bf16.  ``traffic`` = DRAM bytes per
@@ -157,7 +159,7 @@ def run_reference(args):
 
 
 # number of our kernels each C-ABI entry point launches
-KERNELS_PER_CALL = {"fpvs_kmap_compact": 1, "fpvs_hash_build": 1, "fpvs_levels_from_bits": 3}
+KERNELS_PER_CALL = {"fpvs_kmap_compact": 1, "fpvs_hash_build": 1, "fpvs_levels_from_bits": 3, "fpvs_up_sort_multi": 2}
 
 
 def count_launches(fn):
@@ -283,7 +285,7 @@ def run_ours(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh).get("spconv_tc_dram_bytes_per_launch")
+            traffic = json.load(fh).get("conv_dram_bytes_per_launch")
     except Exception:
         pass
 
@@ -305,7 +307,9 @@ def run_ours(args):
         "e2e": {"value": ws * args.steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes,
                 "d2h_bytes_per_step": nbytes, "ms_per_step": e2e_ms / args.steps,
                 "wall_ms_per_step": 1e3 * wall_e2e / args.steps},
-        "roofline": {"bound": "tensor", "kernel": "spconv_tc (tcgen05 gather-GEMM, 14 convs + head / frame)",
+        "roofline": {"bound": "tensor",
+                     "kernel": "tcgen05 sparse conv: spconv_halo (10 subm convs, halo-cached, A in TMEM) + spconv_tc "
+                               "(2 down + 2 parity-sorted up gather-GEMMs) per frame",
                      "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s", "frac": achieved / tf_peak,
                      "peak_kind": f"{peak_kind} bf16 burst", "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (mean over the 14 conv launches, ncu --set full)",

@@ -24,8 +24,15 @@ def launches(path):
     return [(i, per[i]["name"], float(per[i]["gpu__time_duration.sum"]) / 1e3) for i in sorted(per)]
 
 
+CONV = ("spconv_tc_kernel", "spconv_halo_kernel")
+
+
+def is_conv(name):
+    return any(c in name for c in CONV)
+
+
 def first_frame(ls):
-    """Kernels of the first full eager frame: from the first maps launch to the head (15th spconv_tc)."""
+    """Kernels of the first full eager frame: from the first maps launch to the head (15th conv kernel)."""
     out, started, nconv = [], False, 0
     for i, name, us in ls:
         if "l0_flags_kernel" in name:
@@ -35,7 +42,7 @@ def first_frame(ls):
         if not started or "pack_weights" in name:
             continue
         out.append((i, name, us))
-        if "spconv_tc_kernel" in name:
+        if is_conv(name):
             nconv += 1
             if nconv == 15:
                 break
@@ -43,11 +50,25 @@ def first_frame(ls):
 
 
 def raw(rep, metrics):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(metrics)],
-                         capture_output=True, text=True).stdout
+    """Metric values per launch; a metric may appear under a section prefix (e.g. TPC.TriageCompute.)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[0]
-    return [{m: r[h.index(m)] for m in metrics if m in h} | {"name": r[h.index("Kernel Name")]} for r in rows[2:]]
+    col = {}
+    for m in metrics:
+        exact = [i for i, name in enumerate(h) if name == m]
+        pref = [i for i, name in enumerate(h) if name.endswith("." + m)]
+        if exact or pref:
+            col[m] = (exact or pref)[0]
+    return [{m: r[i] for m, i in col.items()} | {"name": r[h.index("Kernel Name")]} for r in rows[2:]]
+
+
+def tensor_pct(r):
+    """tcgen05 (hmma subpipe) active cycles / elapsed SM cycles, per SM average."""
+    try:
+        return f"{100 * float(r['sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg']) / float(r['sm__cycles_elapsed.avg']):.1f}"
+    except (KeyError, ValueError, ZeroDivisionError):
+        return "n/a"
 
 
 def main(tag, launch_csv, conv_rep, maps_rep=None):
@@ -55,22 +76,23 @@ def main(tag, launch_csv, conv_rep, maps_rep=None):
     ls = launches(launch_csv)
     fr = first_frame(ls)
     tot = sum(u for _, _, u in fr)
-    conv = sum(u for _, n, u in fr if "spconv_tc_kernel" in n)
+    conv = sum(u for _, n, u in fr if is_conv(n))
     md += [f"Launch list: `{os.path.basename(launch_csv)}` (`ncu --metrics gpu__time_duration.sum "
            "--clock-control none`, cold-cache, serialised).", "",
-           f"First eager frame: {len(fr)} launches, {tot:.1f} us summed; spconv_tc (14 convs + head) "
+           f"First eager frame: {len(fr)} launches, {tot:.1f} us summed; sparse conv kernels (spconv_halo x10 + "
+           f"spconv_tc x4 + head) "
            f"{conv:.1f} us = {100 * conv / tot:.1f}% of the frame.", "",
            "| # | kernel | us |", "|---|---|---|"]
     md += [f"| {i} | `{n[:70]}` | {u:.2f} |" for i, n, u in fr]
     mets = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
             "launch__grid_size", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-            "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg", "sm__cycles_elapsed.avg",
             "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active"]
     rs = raw(conv_rep, mets)
-    md += ["", f"`--set full` capture `{os.path.basename(conv_rep)}` (first eager frame's 15 spconv_tc launches):", "",
-           "| launch | us | DRAM read MB | DRAM write MB | grid | SM % | L2 % |",
-           "|---|---|---|---|---|---|---|"]
+    md += ["", f"`--set full` capture `{os.path.basename(conv_rep)}` (first eager frame's 15 conv launches):", "",
+           "| launch | kernel | us | DRAM read MB | DRAM write MB | grid | SM % | L2 % | tensor pipe % |",
+           "|---|---|---|---|---|---|---|---|---|"]
     dram = []
     names = ["enc0a", "enc0b", "down01", "enc1a", "enc1b", "down12", "enc2a", "enc2b", "up21", "dec1a", "dec1b",
              "up10", "dec0a", "dec0b", "head"]
@@ -86,19 +108,21 @@ def main(tag, launch_csv, conv_rep, maps_rep=None):
         l2 = mb(r.get("lts__t_bytes.sum", "0"), 1.0)
         if k < 14:
             dram.append(rd + wr)
-        md.append(f"| {names[k] if k < len(names) else k} | {r.get('gpu__time_duration.sum')} | {rd:.2f} | {wr:.2f} | "
-                  f"{r.get('launch__grid_size')} | {r.get('sm__throughput.avg.pct_of_peak_sustained_elapsed')} | "
-                  f"{r.get('lts__throughput.avg.pct_of_peak_sustained_elapsed')} |")
+        kn = "halo" if "halo" in r["name"] else "tc"
+        md.append(f"| {names[k] if k < len(names) else k} | {kn} | {r.get('gpu__time_duration.sum')} | {rd:.2f} | "
+                  f"{wr:.2f} | {r.get('launch__grid_size')} | {r.get('sm__throughput.avg.pct_of_peak_sustained_elapsed')} | "
+                  f"{r.get('lts__throughput.avg.pct_of_peak_sustained_elapsed')} | "
+                  f"{tensor_pct(r)} |")
     if maps_rep:
         mr = raw(maps_rep, mets)
-        md += ["", f"`--set full` capture `{os.path.basename(maps_rep)}` (fused level build):", "",
+        md += ["", f"`--set full` capture `{os.path.basename(maps_rep)}` (map kernels: levels, up-sort, halo tables):", "",
                "| kernel | us | DRAM read MB | grid |", "|---|---|---|---|"]
         for r in mr:
             md.append(f"| `{r['name'][:40]}` | {r.get('gpu__time_duration.sum')} | {r.get('dram__bytes_read.sum')} | "
                       f"{r.get('launch__grid_size')} |")
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md"), "w") as fh:
         fh.write("\n".join(md) + "\n")
-    tr = {"spconv_tc_dram_bytes_per_launch": 1e6 * sum(dram) / max(1, len(dram)),
+    tr = {"conv_dram_bytes_per_launch": 1e6 * sum(dram) / max(1, len(dram)),
           "source": f"profiles/{tag}_ncu_summary.md (dram__bytes_read.sum + dram__bytes_write.sum, mean of 14 conv "
                     "launches, ncu --set full, caches flushed between replays)"}
     with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as fh:
