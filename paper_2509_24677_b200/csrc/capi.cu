@@ -1,4 +1,6 @@
 // Error reporting and version of the C ABI (include/fpvs.h).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace fpvs {
@@ -11,6 +13,14 @@ int set_error(int code, const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
   return code;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FPVS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 }  // namespace fpvs

@@ -30,6 +30,33 @@ int set_error(int code, const char* fmt, ...);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// -------- programmatic dependent launch (PDL) ------------------------------
+// Conv kernels are launched with cudaLaunchAttributeProgrammaticStreamSerialization:
+// a kernel may start while its predecessor drains, runs its prologue (barrier
+// init, TMEM alloc, weight prefetch: data produced two or more launches back),
+// and calls pdl_wait() before touching anything the predecessor writes or
+// reads.  Each kernel triggers its dependents only after its own wait, so a
+// kernel never overlaps anything older than its immediate predecessor.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();  // FPVS_PDL=0 disables (read once)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 inline int grid_for(long long work, int block, int per_sm = 8) {
   long long g = (work + block - 1) / block;
   long long cap = (long long)kNumSMs * per_sm;

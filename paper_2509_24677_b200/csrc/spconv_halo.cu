@@ -376,6 +376,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   if (warp < W_LOAD) {
     // ===================== A builders =====================
     // group bg builds chunk slot bg of every stage (chunks i with i % 2 == bg)
+    pdl_wait();  // the direct-read path reads x (the previous launch's output)
     const int bg = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t t_a = tmem_base + ((uint32_t)(q4 * 32) << 16) + C::ACOL;
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u;
@@ -447,6 +448,8 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     }
   } else if (warp < W_B) {
     // ===================== halo loaders =====================
+    pdl_wait();  // halo rows are the previous launch's output
+    if (tid == W_LOAD * 32) pdl_trigger();
     const int tl = tid - W_LOAD * 32;
     const int pc = tl & 7;
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u;
@@ -545,6 +548,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     }
   } else {
     // ===================== epilogue (4 warps) =====================
+    pdl_wait();  // y, partials and counters may be in use by the previous launch
     const int q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t tlane = (uint32_t)(q4 * 32) << 16;
     int it = 0;
@@ -669,7 +673,8 @@ int launch(const Params& p, cudaStream_t s) {
   }
   const long long units = (long long)((p.cap + BM - 1) / BM) * p.nblk * p.split;
   const int grid = (int)(units < kNumSMs ? (units < 1 ? 1 : units) : kNumSMs);
-  spconv_halo_kernel<BN><<<grid, THREADS, C::SMEM, s>>>(p);
+  cudaError_t e = launch_kernel(spconv_halo_kernel<BN>, dim3(grid), dim3(THREADS), C::SMEM, s, p);
+  if (e != cudaSuccess) return set_error(FPVS_ECUDA, "spconv_halo: %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("spconv_halo");
   return FPVS_OK;
 }

@@ -212,6 +212,8 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
 
   if (warp < C::P) {
     // ===================== A-gather warps =====================
+    pdl_wait();  // x is the previous launch's output
+    if (tid == 0) pdl_trigger();
     // All PROD threads gather every chunk: thread t owns column slot t%8 and
     // rows t/8 + RSTEP*i of the 128B-swizzled A chunk; a stage's full barrier
     // completes when every thread's cp.async pieces have landed (noinc arrival).
@@ -401,6 +403,7 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
     }
   } else {
     // ===================== epilogue (4 warps) =====================
+    pdl_wait();  // y may alias a buffer the previous launch reads
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int r = q * 32 + lane;
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
@@ -542,7 +545,8 @@ int launch_cfg(const Params& p, cudaStream_t s) {
   long long slots = (long long)kNumSMs * MINB;
   int grid = (int)(tiles < slots ? tiles : slots);
   if (grid < 1) grid = 1;
-  spconv_tc_kernel<BN, G, PW, MINB><<<grid, C::THREADS, C::SMEM, s>>>(p);
+  cudaError_t e = launch_kernel(spconv_tc_kernel<BN, G, PW, MINB>, dim3(grid), dim3(C::THREADS), C::SMEM, s, p);
+  if (e != cudaSuccess) return set_error(FPVS_ECUDA, "spconv_tc: %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("spconv_tc");
   return FPVS_OK;
 }
