@@ -237,9 +237,11 @@ int fpvs_spconv_tc_scatter(const void* x, int ldx, int x_rows, const int32_t* nb
  * cached: read directly; every row of a tile whose neighbours span more than
  * 16384 rows is read directly); tiles = ceil(cap / 128).  fpvs_kmap_halo_size is
  * the total bytes of the three arrays (each 256-byte aligned, in that order).
- * fpvs_spconv_halo: bn in {0 (auto), 64, 128}; split >= 1 cuts each tile's K
- * range across CTAs (fp32 partials in ws, reduced in a fixed order by the
- * last CTA: deterministic).  ws = fpvs_spconv_halo_workspace_size bytes,
+ * fpvs_spconv_halo: bn in {0 (auto), 64, 128, 256}; split >= 1 cuts each
+ * tile's K range across CTAs (fp32 partials in ws, reduced in a fixed order by
+ * the last CTA: deterministic); split = -S keeps whole waves of tiles whole
+ * and cuts only the last partial wave's tiles into up to S K ranges (load
+ * balance).  ws = fpvs_spconv_halo_workspace_size bytes,
  * ZEROED before its first use (the kernel leaves its counters at zero). */
 #define FPVS_HALO_MAX 512
 size_t fpvs_kmap_halo_size(int cap);

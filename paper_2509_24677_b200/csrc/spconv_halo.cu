@@ -215,7 +215,8 @@ struct Params {
   const int* n_dev;
   int cap;
   const uint8_t* wpk;
-  int nchunks, nblk, split;
+  int nchunks, nblk, split;  // split > 0: K ranges per item; < 0: tail balancing (see num_units)
+  int smax;                   // partial slots per item in the workspace (|split|)
   const float* bias;
   int cin, cout, act;
   __nv_bfloat16* y;
@@ -270,22 +271,52 @@ struct Cfg {
 };
 
 struct Unit {
-  int mt, nb, s, npres, q0, q1;
+  int mt, nb, s, ns, npres, q0, q1;  // ns: how many units share this (tile, column block)
   uint32_t mask;
 };
 
-__device__ __forceinline__ void unit_of(const Params& p, int u, int cpo, Unit& U) {
-  const int per = p.nblk * p.split;
-  U.mt = u / per;
-  const int rem = u - U.mt * per;
-  U.nb = rem / p.split;
-  U.s = rem - U.nb * p.split;
+// Work items are (tile, column block) pairs.  split > 0: every item is cut
+// into `split` K ranges.  split < 0 (tail balancing): the whole waves of items
+// (multiples of the grid) stay whole and only the items of the last partial
+// wave are cut, into up to -split K ranges, so no CTA carries a whole extra
+// item while others idle.
+__device__ __forceinline__ int num_units(const Params& p, int mtiles) {
+  const int items = mtiles * p.nblk;
+  if (p.split > 0) return items * p.split;
+  const int full = items / gridDim.x * gridDim.x, rem = items - full;
+  const int ts = rem ? max(1, min(-p.split, (int)gridDim.x / rem)) : 1;
+  return full + rem * ts;
+}
+
+__device__ __forceinline__ void unit_of(const Params& p, int u, int cpo, int mtiles, Unit& U) {
+  int item;
+  if (p.split > 0) {
+    item = u / p.split;
+    U.s = u - item * p.split;
+    U.ns = p.split;
+  } else {
+    const int items = mtiles * p.nblk;
+    const int full = items / gridDim.x * gridDim.x, rem = items - full;
+    const int ts = rem ? max(1, min(-p.split, (int)gridDim.x / rem)) : 1;
+    if (u < full) {
+      item = u;
+      U.s = 0;
+      U.ns = 1;
+    } else {
+      const int v = u - full;
+      item = full + v / ts;
+      U.s = v - (item - full) * ts;
+      U.ns = ts;
+    }
+  }
+  U.mt = item / p.nblk;
+  U.nb = item - U.mt * p.nblk;
   U.mask = __ldg(p.tile_masks + U.mt);
   if (!U.mask) U.mask = 1u << 13;
   U.npres = __popc(U.mask);
   const long long L = (long long)cpo * U.npres;
-  U.q0 = (int)(U.s * L / p.split);
-  U.q1 = (int)((U.s + 1) * L / p.split);
+  U.q0 = (int)(U.s * L / U.ns);
+  U.q1 = (int)((U.s + 1) * L / U.ns);
 }
 
 // offset of the q-th chunk inside channel chunk c: the (q - c*npres)-th set bit
@@ -342,7 +373,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   }
   const int n = min(*p.n_dev, p.cap);
   const int mtiles = (n + BM - 1) / BM;
-  const int nunits = mtiles * p.nblk * p.split;
+  const int nunits = num_units(p, mtiles);
   const int cpo = p.cin / BK;
 
   if (tid == 0) {
@@ -383,7 +414,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     uint32_t sc0 = 0, gc = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
-      unit_of(p, u, cpo, U);
+      unit_of(p, u, cpo, mtiles, U);
       const int nq = U.q1 - U.q0;
       for (int c = U.q0 / U.npres; nq > 0 && c * U.npres < U.q1; ++c) {
         const int qs = max(U.q0, c * U.npres), qe = min(U.q1, (c + 1) * U.npres);
@@ -456,7 +487,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     uint32_t gc = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
-      unit_of(p, u, cpo, U);
+      unit_of(p, u, cpo, mtiles, U);
       for (int c = U.q0 / U.npres; U.q1 > U.q0 && c * U.npres < U.q1; ++c) {
         const int hb = gc % C::NHB;
         const uint32_t hph = (gc / C::NHB) & 1;
@@ -493,7 +524,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       uint32_t st = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
-        unit_of(p, u, cpo, U);
+        unit_of(p, u, cpo, mtiles, U);
         const int nq = U.q1 - U.q0;
         const uint8_t* wblk = p.wpk + (size_t)U.nb * p.nchunks * C::B_SUB;
         ChunkWalk w;
@@ -519,7 +550,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       int it = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
         Unit U;
-        unit_of(p, u, cpo, U);
+        unit_of(p, u, cpo, mtiles, U);
         const int nq = U.q1 - U.q0;
         const int acc = it % C::NACC;
         mbar_wait(smem_u32(tempty + acc), ((it / C::NACC) & 1) ^ 1);
@@ -554,7 +585,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     int it = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
       Unit U;
-      unit_of(p, u, cpo, U);
+      unit_of(p, u, cpo, mtiles, U);
       const int acc = it % C::NACC;
       mbar_wait_sleep(smem_u32(tfull + acc), (it / C::NACC) & 1, 128);
       if (q4 == 0 && lane == 0) HTS(7200 + 2 * it);
@@ -562,7 +593,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       const long long row = (long long)U.mt * BM + r;
       const bool valid = row < n;
       const int col0 = U.nb * BN;
-      if (p.split == 1) {
+      if (U.ns == 1) {
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += 32) {
           float v[32];
@@ -589,7 +620,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         // taking its own split from TMEM
         const long long slot = (long long)U.mt * p.nblk + U.nb;
         const bool has = U.q1 > U.q0;
-        float* mine = p.part + (slot * p.split + U.s) * BM * BN + r;
+        float* mine = p.part + (slot * p.smax + U.s) * BM * BN + r;
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += 32) {
           float v[32];
@@ -601,21 +632,21 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         if (q4 == 0 && lane == 0) HTS(7400 + 4 * it);
         if (warp == W_EPI && lane == 0) {
           __threadfence();  // release the CTA's partial (ordered after the barrier) before the count
-          const int last = atomicAdd(p.counters + slot, 1) == p.split - 1;
+          const int last = atomicAdd(p.counters + slot, 1) == U.ns - 1;
           if (last) __threadfence();  // acquire the other splits' partials
           *s_last = last;
         }
         named_bar(1, 128);
         if (q4 == 0 && lane == 0) HTS(7402 + 4 * it);
         if (*s_last) {
-          const float* base = p.part + slot * p.split * BM * BN + r;
+          const float* base = p.part + slot * p.smax * BM * BN + r;
 #pragma unroll 1
           for (int cb = 0; cb < BN; cb += 32) {
             float own[32], v[32];
             tmem_ld32(tmem_base + tlane + acc * BN + cb, own);
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.f;
-            for (int ss = 0; ss < p.split; ++ss) {
+            for (int ss = 0; ss < U.ns; ++ss) {
               const float* src = base + (long long)ss * BM * BN + cb * BM;
               if (ss == U.s) {
 #pragma unroll
@@ -671,7 +702,7 @@ int launch(const Params& p, cudaStream_t s) {
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     configured = true;
   }
-  const long long units = (long long)((p.cap + BM - 1) / BM) * p.nblk * p.split;
+  const long long units = (long long)((p.cap + BM - 1) / BM) * p.nblk * p.smax;
   const int grid = (int)(units < kNumSMs ? (units < 1 ? 1 : units) : kNumSMs);
   cudaError_t e = launch_kernel(spconv_halo_kernel<BN>, dim3(grid), dim3(THREADS), C::SMEM, s, p);
   if (e != cudaSuccess) return set_error(FPVS_ECUDA, "spconv_halo: %s", cudaGetErrorString(e));
@@ -732,6 +763,7 @@ extern "C" int fpvs_kmap_halo(const int32_t* nbr, const int32_t* n_dev, int cap,
 }
 
 extern "C" size_t fpvs_spconv_halo_workspace_size(int cap, int cout, int bn, int split) {
+  if (split < 0) split = -split;
   if (cap < 1 || (bn != 64 && bn != 128 && bn != 256) || cout % bn || split < 1) return 0;
   const size_t tiles = (cap + tc::BM - 1) / tc::BM, nblk = cout / bn;
   size_t b = halo::align256(tiles * nblk * 4);
@@ -755,7 +787,8 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
   FPVS_CHECK_ARG((long long)x_rows * ldx * 2 < (1LL << 31), "feature buffer too large for 32-bit row offsets");
   FPVS_CHECK_ARG(ldy % 8 == 0 && col_off % 8 == 0 && ldy >= col_off + cout, "bad output leading dimension");
   FPVS_CHECK_ARG(act == FPVS_ACT_NONE || act == FPVS_ACT_RELU, "halo conv epilogue supports none/relu");
-  FPVS_CHECK_ARG(split >= 1 && split <= 27 * (cin / 64), "split must lie in [1, 27 * Cin / 64]");
+  FPVS_CHECK_ARG(split != 0 && (split < 0 ? -split : split) <= 27 * (cin / 64),
+                 "|split| must lie in [1, 27 * Cin / 64]");
   const size_t need = fpvs_spconv_halo_workspace_size(cap, cout, bn, split);
   FPVS_CHECK_ARG(ws && ws_bytes >= need, "workspace too small: need %zu bytes", need);
   if (cap <= 0) return FPVS_OK;
@@ -773,6 +806,7 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
   p.nchunks = 27 * cin / 64;
   p.nblk = cout / bn;
   p.split = split;
+  p.smax = split < 0 ? -split : split;
   p.bias = bias;
   p.cin = cin;
   p.cout = cout;

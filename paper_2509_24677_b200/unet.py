@@ -156,11 +156,13 @@ class UNetPlan:
             cin, cout = layer.spec.in_channels, layer.spec.out_channels
             if not halo_ok(27, cin, cout):
                 continue
-            # measured on config 2 (tools/halo_sweep.py): 128-wide tiles, and a
-            # 2-way K split only where the level has well under a wave of tiles
+            # measured on config 2 (tools/halo_sweep.py): 128-wide tiles; a
+            # 2-way K split where the level has well under a wave of tiles, and
+            # split = -2 (only the last partial wave's tiles cut in two) where it
+            # has more tiles than SMs
             bn = 128 if cout % 128 == 0 else 64
             tiles = max(1, (r + 127) // 128) * (cout // bn)
-            split = 2 if tiles * 2 <= 148 else 1
+            split = 2 if tiles * 2 <= 148 else -2 if tiles > 148 else 1
             if cfg and name in cfg:
                 bn, split = cfg[name]
             self.halo_cfg[name] = (bn, split)

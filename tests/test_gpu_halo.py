@@ -144,7 +144,8 @@ def _rows(n, c, seed, cap):
 @pytest.mark.parametrize("cin,cout,bn,split", [(64, 64, 64, 1), (64, 64, 64, 2), (128, 64, 64, 1), (64, 128, 128, 1),
                                                (128, 128, 128, 3), (256, 128, 128, 1), (256, 256, 128, 5),
                                                (256, 256, 64, 2), (128, 128, 64, 8), (256, 256, 256, 1),
-                                               (256, 256, 256, 3), (128, 256, 256, 2), (64, 64, 64, 3)])
+                                               (256, 256, 256, 3), (128, 256, 256, 2), (64, 64, 64, 3),
+                                               (64, 64, 64, -2), (128, 128, 128, -3)])
 def test_halo_conv_vs_oracle(cin, cout, bn, split):
     import torch
     from paper_2509_24677_b200 import sparse as sp
@@ -173,6 +174,30 @@ def test_halo_conv_vs_oracle(cin, cout, bn, split):
     _run_halo(layer, xt, cin, lv, lv.nbr, h, y3, 2 * cout, cout, bn, split)
     assert torch.equal(y3[:n, cout:], torch.relu(y[:n]))
     assert not y3[:n, :cout].any()
+
+
+def test_halo_conv_tail_balancing_more_tiles_than_sms():
+    """split = -2 with > 148 tiles: whole waves stay whole, only the tail tiles are cut."""
+    import torch
+    from paper_2509_24677_b200 import sparse as sp
+    lv = _level((40, 40, 40), 0.3, 77)
+    n = lv.count()
+    assert (n + 127) // 128 > 148
+    h = sp.build_halo(lv)
+    xv, xt = _rows(n, 64, 6, lv.cap)
+    layer = _layer(64, 64, 12)
+    w = osp.bf16_round(layer.w.cpu().numpy())
+    b = layer.b.cpu().numpy().astype(np.float64)
+    ya = torch.zeros((lv.cap, 64), dtype=torch.bfloat16, device="cuda")
+    yb = torch.zeros_like(ya)
+    _run_halo(layer, xt, 64, lv, lv.nbr, h, ya, 64, 0, 64, -2, act="none")
+    _run_halo(layer, xt, 64, lv, lv.nbr, h, yb, 64, 0, 64, 1, act="none")
+    z = osp.gather_conv(xv.astype(np.float64), lv.nbr[:n].cpu().numpy().astype(np.int64), w, b)
+    got = ya[:n].float().cpu().numpy()
+    assert np.all(np.abs(got - z) <= np.abs(z) * 2.0 ** -8 + 1e-4), np.abs(got - z).max()
+    # whole tiles are bit-identical to the unsplit run (same accumulation order)
+    full = 148 * 128
+    assert torch.equal(ya[:full], yb[:full])
 
 
 def test_halo_conv_direct_read_path():

@@ -64,12 +64,9 @@ print(f"halo build, 3 levels one launch: {e0.elapsed_time(e1) / 20 * 1000:.1f} u
 
 rows = {k: lv.count() for k, lv in plan.level_of.items()}
 variants = {
-    "L0 s2": {k: (64, 2) for k in L0},
-    "L1 s4": {k: (128, 4) for k in L1},
-    "L1 bn64 s2": {k: (64, 2) for k in L1},
-    "L2 s4": {k: (128, 4) for k in L2},
-    "L2 s5": {k: (128, 5) for k in L2},
-    "L2 bn256 s5": {k: (256, 5) for k in L2},
+    "L0 tail-split 2": {k: (64, -2) for k in L0},
+    "L0 tail-split 3": {k: (64, -3) for k in L0},
+    "L0 tail-split 4": {k: (64, -4) for k in L0},
 }
 for tag, cfg in (variants.items() if os.environ.get("SWEEP", "1") == "1" else []):
     plan.set_halo(rows, cfg)
