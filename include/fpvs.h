@@ -52,7 +52,7 @@ extern "C" {
 enum { FPVS_OK = 0, FPVS_EINVAL = 1, FPVS_ESHAPE = 2, FPVS_ECUDA = 3 };
 enum { FPVS_IN_PACKED = 0, FPVS_IN_U8 = 1, FPVS_IN_F32 = 2 };
 enum { FPVS_F32 = 0, FPVS_BF16 = 1 };
-enum { FPVS_ACT_NONE = 0, FPVS_ACT_RELU = 1, FPVS_ACT_SIGMOID = 2 };
+enum { FPVS_ACT_NONE = 0, FPVS_ACT_RELU = 1, FPVS_ACT_SIGMOID = 2, FPVS_ACT_MASK = 3 };
 
 const char* fpvs_last_error(void);
 int fpvs_abi_version(void);
@@ -308,6 +308,27 @@ int fpvs_spconv_wgrad_simt(const void* x, int ldx, int x_dtype, const float* dz,
                            const int32_t* nbr, int K, const int32_t* n_dev, int cap,
                            int cin, int cout, float* dw, float* db,
                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* Tensor-core backward (bf16 operands, fp32 accumulate), BASELINE config 5.
+ * dgrad: dx = conv over the same table with mirrored offsets and per-offset
+ * transposed weights (nbr[i][j] = k <=> nbr[k][K-1-j] = i for submanifold
+ * tables), packed by fpvs_pack_weights_tc_dgrad from the reference-layout
+ * W (K*Cin, Cout); the epilogue multiplies by relu'(z) = [mask > 0] taken from
+ * the kept bf16 output of the layer below (neural.py:227-228) and writes bf16.
+ * wgrad: dW[j*Cin + ci][co] = sum_i x[nbr[i][j]][ci] * dz[i][co] and
+ * db = sum_i dz[i] on tcgen05 with both operands MN-major (gathered x, dz),
+ * fixed-order reduction of per-CTA partials (deterministic). */
+int fpvs_pack_weights_tc_dgrad(const float* w, int K, int cin, int cout, int bn, void* packed, void* stream);
+int fpvs_spconv_tc_dgrad(const void* dz, int lddz, int dz_rows, const int32_t* nbr, int K,
+                         const uint32_t* tile_masks, const int32_t* n_dev, int cap,
+                         const void* w_packed_dgrad, int bn, int cin, int cout, const void* mask, int ldm,
+                         void* dx, int lddx, void* stream);
+size_t fpvs_wgrad_tc_workspace_size(int K, int cin, int cout, int cap);
+int fpvs_spconv_wgrad_tc(const void* x, int ldx, const void* dz, int lddz, const int32_t* nbr, int K,
+                         const int32_t* n_dev, int cap, int cin, int cout, float* dw, float* db,
+                         void* workspace, size_t workspace_bytes, void* stream);
+/* f32 -> bf16 (round to nearest even), n elements. */
+int fpvs_cast_bf16(const float* src, long long n, void* dst, void* stream);
 
 /* Optimizer steps over ONE flat fp32 parameter buffer (all layers' weights
  * and biases back to back; the data-parallel gradient is one all-reduce of

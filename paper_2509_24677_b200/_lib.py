@@ -50,6 +50,11 @@ SIGNATURES = {
     "fpvs_spconv_halo_workspace_size": (_z, [_i, _i, _i, _i]),
     "fpvs_spconv_halo": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _i, _i, _p, _i, _i, _i, _p, _i, _i, _p,
                               _z, _p]),
+    "fpvs_pack_weights_tc_dgrad": (_i, [_p, _i, _i, _i, _i, _p, _p]),
+    "fpvs_spconv_tc_dgrad": (_i, [_p, _i, _i, _p, _i, _p, _p, _i, _p, _i, _i, _i, _p, _i, _p, _i, _p]),
+    "fpvs_wgrad_tc_workspace_size": (_z, [_i, _i, _i, _i]),
+    "fpvs_spconv_wgrad_tc": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _p, _p, _p, _z, _p]),
+    "fpvs_cast_bf16": (_i, [_p, C.c_longlong, _p, _p]),
     "fpvs_up_sort_cap": (_i, [_i]),
     "fpvs_up_sort_workspace_size": (_z, [_i]),
     "fpvs_up_sort": (_i, [_p, _p, _i, _p, _p, _p, _p, _p, _z, _p]),

@@ -141,3 +141,18 @@ extern "C" int fpvs_bits_confusion(const uint8_t* pred_bits, const uint8_t* gt_b
   FPVS_CHECK_LAUNCH("fpvs_bits_confusion");
   return FPVS_OK;
 }
+
+namespace fpvs {
+__global__ void cast_bf16_kernel(const float* __restrict__ src, long long n, __nv_bfloat16* __restrict__ dst) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    dst[t] = __float2bfloat16_rn(src[t]);
+}
+}  // namespace fpvs
+
+extern "C" int fpvs_cast_bf16(const float* src, long long n, void* dst, void* stream) {
+  FPVS_CHECK_ARG(src && dst && n >= 0, "bad arguments");
+  if (n == 0) return FPVS_OK;
+  fpvs::cast_bf16_kernel<<<fpvs::grid_for(n, 256), 256, 0, fpvs::as_stream(stream)>>>(src, n, (__nv_bfloat16*)dst);
+  FPVS_CHECK_LAUNCH("fpvs_cast_bf16");
+  return FPVS_OK;
+}

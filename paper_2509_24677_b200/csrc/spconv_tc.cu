@@ -52,6 +52,8 @@ struct Params {
   __nv_bfloat16* y;
   int ldy, col_off;
   const int* out_rows;  // tile row -> output row (-1 = skip); NULL = identity
+  const __nv_bfloat16* mask;  // act == FPVS_ACT_MASK: out = z * (mask[row][col] > 0) (relu' of the layer below)
+  int ldm;
   // head epilogue
   int head;
   const int4* coords;
@@ -429,6 +431,19 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
             float z = v[i] + s_bias[col0 + cb + i];
             v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
           }
+          if (p.act == FPVS_ACT_MASK) {
+            const uint4* mk = reinterpret_cast<const uint4*>(p.mask + orow * p.ldm + col0 + cb);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint4 m4 = __ldg(mk + i);
+              const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const uint32_t h = (mw[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;  // bf16 bits; > 0 iff sign 0 and nonzero
+                if (!(h != 0u && h < 0x8000u)) v[8 * i + e] = 0.f;
+              }
+            }
+          }
           uint4* dst = reinterpret_cast<uint4*>(p.y + orow * p.ldy + p.col_off + col0 + cb);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -504,8 +519,11 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
 
 // packed[nb][c][n][128 B] for n < BN: element kk of chunk c at
 // n*128 + ((kk/8) ^ (n%8))*16 + (kk%8)*2 (Swizzle<3,4,3>), value W[c*64+kk][nb*BN + n]
+// dgrad (taps > 0): the packed matrix is W'[(j*cout_src + co)][ci] = W[((taps-1-j)*cin_src + ci)][co]
+// (mirrored offsets, transposed per offset), the forward weight of dx = conv(dz).
 __global__ void pack_weights_kernel(const float* __restrict__ w, int Ktot, int cout, int BN, int nchunks, int nblk,
-                                    __nv_bfloat16* __restrict__ out) {
+                                    __nv_bfloat16* __restrict__ out, int taps = 0, int cin_src = 0,
+                                    int cout_src = 0) {
   const long long total = (long long)nblk * nchunks * BN * BK;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
@@ -516,7 +534,15 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, int Ktot, int c
     int c = r % nchunks;
     int nb = (int)(r / nchunks);
     int k = c * BK + kk, col = nb * BN + nn;
-    float v = (k < Ktot && col < cout) ? w[(long long)k * cout + col] : 0.f;
+    float v = 0.f;
+    if (k < Ktot && col < cout) {
+      if (taps) {
+        const int j = k / cout_src, co = k - j * cout_src;
+        v = w[((long long)(taps - 1 - j) * cin_src + col) * cout_src + co];
+      } else {
+        v = w[(long long)k * cout + col];
+      }
+    }
     long long byte = (((long long)nb * nchunks + c) * BN + nn) * 128 + (((kk >> 3) ^ (nn & 7)) << 4) + (kk & 7) * 2;
     out[byte / 2] = __float2bfloat16_rn(v);
   }
@@ -679,6 +705,46 @@ extern "C" int fpvs_spconv_tc_scatter(const void* x, int ldx, int x_rows, const 
   p.ldy = ldy;
   p.col_off = col_off;
   p.out_rows = out_rows;
+  return tc::dispatch(p, bn, as_stream(stream));
+}
+
+extern "C" int fpvs_pack_weights_tc_dgrad(const float* w, int K, int cin, int cout, int bn, void* packed,
+                                          void* stream) {
+  FPVS_CHECK_ARG(w && packed, "null pointer");
+  // the dgrad conv maps cout -> cin channels
+  bn = resolve_bn(bn, cin);
+  FPVS_CHECK_ARG(bn > 0, "tile width must be 0 (auto), 32, 64, 128 or 256");
+  FPVS_CHECK_ARG(cout % 8 == 0, "tcgen05 dgrad needs Cout %% 8 == 0, got %d", cout);
+  const int nchunks = (K * cout + tc::BK - 1) / tc::BK;
+  const int nblk = (cin + bn - 1) / bn;
+  const long long total = (long long)nblk * nchunks * bn * tc::BK;
+  tc::pack_weights_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+      w, K * cout, cin, bn, nchunks, nblk, (__nv_bfloat16*)packed, K, cin, cout);
+  FPVS_CHECK_LAUNCH("fpvs_pack_weights_tc_dgrad");
+  return FPVS_OK;
+}
+
+extern "C" int fpvs_spconv_tc_dgrad(const void* dz, int lddz, int dz_rows, const int32_t* nbr, int K,
+                                    const uint32_t* tile_masks, const int32_t* n_dev, int cap,
+                                    const void* w_packed_dgrad, int bn, int cin, int cout, const void* mask, int ldm,
+                                    void* dx, int lddx, void* stream) {
+  tc::Params p;
+  bn = resolve_bn(bn, cin);
+  FPVS_CHECK_ARG(bn > 0, "tile width must be 0 (auto), 32, 64, 128 or 256");
+  // the forward kernel with Cin' = cout (dz channels), Cout' = cin
+  int rc = tc_common(p, dz, lddz, dz_rows, nbr, K, tile_masks, n_dev, cap, w_packed_dgrad, nullptr, cout, cin, bn);
+  if (rc) return rc;
+  FPVS_CHECK_ARG(dx, "null output");
+  FPVS_CHECK_ARG(cin % 32 == 0, "tcgen05 dgrad epilogue needs Cin %% 32 == 0, got %d", cin);
+  FPVS_CHECK_ARG(lddx % 8 == 0 && lddx >= cin, "bad dx leading dimension");
+  FPVS_CHECK_ARG(!mask || (ldm % 8 == 0 && ldm >= cin), "bad mask leading dimension");
+  if (cap <= 0) return FPVS_OK;
+  p.act = mask ? FPVS_ACT_MASK : FPVS_ACT_NONE;
+  p.mask = (const __nv_bfloat16*)mask;
+  p.ldm = ldm;
+  p.y = (__nv_bfloat16*)dx;
+  p.ldy = lddx;
+  p.col_off = 0;
   return tc::dispatch(p, bn, as_stream(stream));
 }
 

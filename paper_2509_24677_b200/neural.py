@@ -235,6 +235,24 @@ def packed_cache(layer, bn: int = 0, stream=None):
     return layer._packed[bn]
 
 
+def packed_dgrad_cache(layer, bn: int = 0, stream=None):
+    """The layer's dgrad weight image (mirrored offsets, per-offset Wᵀ), built once per update."""
+    if layer._packed is None:
+        layer._packed = {}
+    key = ("dgrad", bn)
+    if key not in layer._packed:
+        torch = _torch()
+        cin, cout = layer.spec.in_channels, layer.spec.out_channels
+        nbytes = _lib.size("fpvs_pack_weights_tc_size", layer.taps, cout, cin, bn)
+        if nbytes == 0:
+            raise ValueError(f"no tensor-core dgrad packing for taps={layer.taps}, Cin={cin}, Cout={cout}")
+        out = torch.empty(nbytes, dtype=torch.uint8, device=layer.w.device)
+        _lib.call("fpvs_pack_weights_tc_dgrad", _lib.ptr(layer.w.contiguous()), layer.taps, cin, cout, bn,
+                  _lib.ptr(out), _lib.stream_ptr(stream))
+        layer._packed[key] = out
+    return layer._packed[key]
+
+
 def pack_tc(w, taps: int, cin: int, cout: int, bn: int = 0, stream=None):
     torch = _torch()
     nbytes = _lib.size("fpvs_pack_weights_tc_size", taps, cin, cout, bn)

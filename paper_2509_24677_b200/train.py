@@ -44,7 +44,7 @@ import numpy as np
 from . import _lib
 from . import sparse as sp
 from .froxel import FroxelGrid
-from .neural import ModelConfig, PvsNet, TrainConfig, TrainingDiverged, run_conv, run_head
+from .neural import ModelConfig, PvsNet, TrainConfig, TrainingDiverged, packed_dgrad_cache, run_conv, run_head
 
 
 def _torch():
@@ -103,6 +103,14 @@ class TrainStep:
         self.dlogits = torch.empty((cap, d3), dtype=torch.float32, device=device)
         widest = max(L.spec.in_channels for L in net.layers)
         self.dx = [torch.empty((cap, widest), dtype=torch.float32, device=device) for _ in range(2)]
+        # bf16: the backward runs on tensor cores (tcgen05 dgrad / wgrad) with bf16 gradients
+        self.tc_backward = bf16 and self._tc_backward_ok()
+        if self.tc_backward:
+            self.dlog16 = torch.empty((cap, d3), dtype=torch.bfloat16, device=device)
+            self.dz16 = [torch.empty((cap, widest), dtype=torch.bfloat16, device=device) for _ in range(2)]
+            tws = max(_lib.size("fpvs_wgrad_tc_workspace_size", L.taps, L.spec.in_channels, L.spec.out_channels, cap)
+                      for L in net.layers)
+            self.wg_tc_ws = torch.empty(tws, dtype=torch.uint8, device=device)
         self.pred_bits = torch.zeros(B * self.grid_bytes, dtype=torch.uint8, device=device)
         # flat master parameters and gradient
         sizes = [(L.w.numel(), L.b.numel()) for L in net.layers]
@@ -157,7 +165,15 @@ class TrainStep:
                   _lib.ptr(self.counts), _lib.ptr(self.conf_ws), self.conf_ws.numel(), s)
         self.backward(stream)
 
+    def _tc_backward_ok(self) -> bool:
+        layers = self.net.layers
+        return (all(L.spec.in_channels % 8 == 0 and L.spec.out_channels % 8 == 0 and L.spec.out_channels <= 256
+                    for L in layers)
+                and all(L.spec.in_channels % 32 == 0 for L in layers[1:]))
+
     def backward(self, stream=None):
+        if self.tc_backward:
+            return self.backward_tc(stream)
         net, lv = self.net, self.lv
         s = _lib.stream_ptr(stream)
         ins = [self.x0] + self.acts
@@ -179,6 +195,34 @@ class TrainStep:
             _lib.call("fpvs_spconv_dgrad_simt", _lib.ptr(dz), lddz, _lib.ptr(table), K, _lib.ptr(lv.n), lv.cap,
                       _lib.ptr(layer.w), spec.in_channels, spec.out_channels, _lib.ptr(x), xdt, x.shape[1],
                       _lib.ptr(dx), dx.shape[1], s)
+            dz, lddz = dx, dx.shape[1]
+
+    def backward_tc(self, stream=None):
+        """Tensor-core backward: per layer tcgen05 wgrad (dW, db) and, below the
+        first layer, tcgen05 dgrad with the relu' mask fused (bf16 gradients)."""
+        net, lv = self.net, self.lv
+        s = _lib.stream_ptr(stream)
+        ins = [self.x0] + self.acts
+        cap = lv.cap
+        _lib.call("fpvs_cast_bf16", _lib.ptr(self.dlogits), cap * self.dlogits.shape[1], _lib.ptr(self.dlog16), s)
+        dz, lddz = self.dlog16, self.dlog16.shape[1]
+        for li in reversed(range(len(net.layers))):
+            layer = net.layers[li]
+            spec = layer.spec
+            x = ins[li]
+            table, K = (lv.nbr, 27) if spec.kernel == 3 else (None, 1)
+            dw, db = self.views[li]
+            _lib.call("fpvs_spconv_wgrad_tc", _lib.ptr(x), x.shape[1], _lib.ptr(dz), lddz, _lib.ptr(table), K,
+                      _lib.ptr(lv.n), cap, spec.in_channels, spec.out_channels, _lib.ptr(dw), _lib.ptr(db),
+                      _lib.ptr(self.wg_tc_ws), self.wg_tc_ws.numel(), s)
+            if li == 0:
+                break
+            dx = self.dz16[li % 2]
+            # dz of the layer below = (dz W'ᵀ on the mirrored map) * relu'(its kept output)
+            _lib.call("fpvs_spconv_tc_dgrad", _lib.ptr(dz), lddz, cap, _lib.ptr(table), K,
+                      _lib.ptr(lv.nbr_masks if table is not None else None), _lib.ptr(lv.n), cap,
+                      _lib.ptr(packed_dgrad_cache(layer, 0, stream)), 0, spec.in_channels, spec.out_channels,
+                      _lib.ptr(x), x.shape[1], _lib.ptr(dx), dx.shape[1], s)
             dz, lddz = dx, dx.shape[1]
 
     # -- exchange + update ---------------------------------------------------
