@@ -14,6 +14,8 @@
 // of 64-row K chunks; each unit accumulates in TMEM and writes an fp32
 // partial; a second kernel sums the partials of each block in a fixed order
 // (deterministic, no float atomics), and a third the bias gradient.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -25,8 +27,19 @@ using namespace tc;
 constexpr int KC = 64;          // rows of the reduction per pipeline stage
 constexpr int NS = 4;           // stages
 constexpr int A_STAGE = 16384;  // 128 (j, ci) x 64 rows x 2 B
-constexpr int THREADS = 256;    // warps 0-3 producers, warp 4 MMA, warps 4-7 epilogue
-constexpr int PROD = 128;
+constexpr int THREADS = 384;    // warps 0-7 producers, warp 8 MMA, warps 8-11 epilogue
+constexpr int PROD = 256;
+constexpr int W_MMA = PROD / 32;
+constexpr int APT = KC * 16 / PROD;  // A pieces per producer thread per chunk
+
+__device__ unsigned long long g_wts[4096];  // FPVS_WGRAD_DEBUG & 32: CTA 0 timestamps
+__device__ __forceinline__ void wts(const int dbg, int slot) {
+  if ((dbg & 32) && blockIdx.x == 0 && slot < 4096) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_wts[slot] = t;
+  }
+}
 
 struct Params {
   const __nv_bfloat16* x;
@@ -40,6 +53,7 @@ struct Params {
   int cin, cout, npad;  // npad: MMA N (cout rounded up to 16)
   int nmb, nsplit;      // (j, ci) blocks of 128, K-chunk ranges per block
   float* part;          // [nmb][nsplit][128][npad]
+  int dbg;              // FPVS_WGRAD_DEBUG (profiling only): 1 no A copies, 2 no MMA, 4 no nbr loads
 };
 
 __device__ __forceinline__ uint64_t desc_mn(uint32_t saddr) {
@@ -66,6 +80,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_tc_kernel(const Params p) {
   uint64_t* empty = bars + NS;
   uint64_t* tfull = bars + 2 * NS;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tfull + 1);
+  int* s_nb = reinterpret_cast<int*>(smem + NS * (A_STAGE + B_STAGE) + 1024);  // [64][32] chunk neighbour rows
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int mb = blockIdx.x / p.nsplit, rs = blockIdx.x - mb * p.nsplit;
@@ -82,7 +97,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_tc_kernel(const Params p) {
     mbar_init(smem_u32(tfull), 1);
     fence_mbar_init();
   }
-  if (warp == 4) {
+  if (warp == W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
                  "n"(TCOLS)
                  : "memory");
@@ -93,59 +108,132 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_tc_kernel(const Params p) {
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
-  if (warp < 4) {
+  if (warp < W_MMA) {
     // ===================== producers: gather A pieces, load B pieces =====================
+    // The chunk's neighbour indices of this block's offsets are first loaded
+    // (independent, coalesced) into smem, so the cp.async gather issues without
+    // dependent global latency; 8 consecutive lanes fill one 128-byte core
+    // matrix (8 rows of one 16-byte column), so the smem writes do not conflict.
     pdl_wait();
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u, lddz2 = (uint32_t)p.lddz * 2u;
+    const int jlo = (mb * 128) / p.cin;
+    const int jn = min(p.K, (mb * 128 + 127) / p.cin + 1) - jlo;  // offsets touched by this block
+    const int fones = (kcin % 128) ? kcin : -1;  // padding row used for db (sum of dz)
+    // Per-thread piece geometry is the same for every chunk: precomputed once.
+    // A: pieces q = tid + PROD t (t < APT): core row kk, 16-byte column mg.
+    int a_row[APT], a_nb[APT], a_cof[APT];
+    uint32_t a_dst[APT];
+#pragma unroll
+    for (int t = 0; t < APT; ++t) {
+      const int q = tid + PROD * t;
+      // 4 consecutive lanes read one row's 4 consecutive 16-byte pieces (64 B
+      // coalesced); a warp covers 8 rows; its smem writes are 4 x 128 B
+      const int mg = ((q >> 5) & 3) * 4 + (q & 3), kk = ((q >> 7) << 3) | ((q >> 2) & 7);
+      const int f = mb * 128 + mg * 8;
+      a_row[t] = kk;
+      a_dst[t] = mg * 1024 + (kk >> 3) * 128 + (kk & 7) * 16;
+      a_nb[t] = f == fones ? -2 : f < kcin ? kk * 32 + (f / p.cin - jlo) : -1;  // s_nb slot, -1 zero, -2 ones
+      a_cof[t] = (f % p.cin) * 2;
+    }
+    // B: pieces q = tid + PROD t
+    constexpr int NBP = (KC * (NPAD / 8) + PROD - 1) / PROD;
+    int b_row[NBP];
+    uint32_t b_dst[NBP], b_off[NBP];
+    bool b_ok[NBP];
+#pragma unroll
+    for (int t = 0; t < NBP; ++t) {
+      const int q = tid + PROD * t;
+      const int ng = q % (NPAD / 8), kk = q / (NPAD / 8);  // a row's pieces on consecutive lanes
+      b_row[t] = kk;
+      b_dst[t] = ng * 1024 + (kk >> 3) * 128 + (kk & 7) * 16;
+      b_off[t] = ng * 16;
+      b_ok[t] = q < KC * (NPAD / 8) && ng * 8 < p.cout;
+    }
+    // neighbour indices of the block's offsets, loaded one chunk ahead (jn <= 16)
+    constexpr int NPT = KC * 16 / PROD;
+    int n_slot[NPT], n_row[NPT], n_j[NPT];
+#pragma unroll
+    for (int t = 0; t < NPT; ++t) {
+      const int q = tid + PROD * t;
+      const int kk = q / jn, jj = q - kk * jn;
+      n_slot[t] = q < KC * jn ? kk * 32 + jj : -1;
+      n_row[t] = kk;
+      n_j[t] = jlo + jj;
+    }
+    int pre[NPT];
+    auto prefetch = [&](int c) {
+#pragma unroll
+      for (int t = 0; t < NPT; ++t) {
+        const int i = c * KC + n_row[t];
+        pre[t] = -1;
+        if (n_slot[t] >= 0 && i < n) pre[t] = (p.nbr && !(p.dbg & 4)) ? __ldg(p.nbr + (long long)i * p.K + n_j[t]) : i;
+      }
+    };
+    const char* xg = reinterpret_cast<const char*>(p.x);
+    const char* dg = reinterpret_cast<const char*>(p.dz);
+    if (c0 < c1) prefetch(c0);
     for (int c = c0; c < c1; ++c) {
       const int k = c - c0, stage = k % NS;
-      mbar_wait_sleep(smem_u32(empty + stage), ((k / NS) & 1) ^ 1, 32);
-      const uint32_t a_st = smem_u32(sA + stage * A_STAGE), b_st = smem_u32(sB + stage * B_STAGE);
       const int i0 = c * KC;
-      // A: 64 rows x 16 groups of 8 (j, ci) values
-#pragma unroll 2
-      for (int q = tid; q < KC * 16; q += PROD) {
-        const int kk = q >> 4, mg = q & 15;
-        const int f = mb * 128 + mg * 8;  // flattened (j, ci) of the piece
-        const int i = i0 + kk;
-        int src = -1;
-        if (i < n && f < kcin) {
-          const int j = f / p.cin;
-          src = p.nbr ? __ldg(p.nbr + (long long)i * p.K + j) : i;
+      if (tid == 0) wts(p.dbg, 8 * k);
+      named_bar(2, PROD);  // previous chunk's readers are done with s_nb
+#pragma unroll
+      for (int t = 0; t < NPT; ++t)
+        if (n_slot[t] >= 0) s_nb[n_slot[t]] = pre[t];
+      named_bar(2, PROD);
+      if (tid == 0) wts(p.dbg, 8 * k + 1);
+      if (c + 1 < c1) prefetch(c + 1);  // in flight while this chunk's copies issue
+      mbar_wait_sleep(smem_u32(empty + stage), ((k / NS) & 1) ^ 1, 32);
+      if (tid == 0) wts(p.dbg, 8 * k + 2);
+      const uint32_t a_st = smem_u32(sA + stage * A_STAGE), b_st = smem_u32(sB + stage * B_STAGE);
+#pragma unroll
+      for (int t = 0; t < APT; ++t) {
+        const uint32_t dst = a_st + a_dst[t];
+        if (a_nb[t] == -2) {
+          // db row: 1.0 in the first element for valid rows
+          const uint32_t one = (i0 + a_row[t] < n) ? 0x3F80u : 0u;
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(one), "r"(0u), "r"(0u), "r"(0u)
+                       : "memory");
+          continue;
         }
-        const char* g = reinterpret_cast<const char*>(p.x) + (src >= 0 ? (long long)src * ldx2 + (f % p.cin) * 2 : 0);
-        cp_async16(a_st + mg * 1024 + (kk >> 3) * 128 + (kk & 7) * 16, g, src >= 0 ? 16u : 0u);
+        const int src = a_nb[t] >= 0 ? s_nb[a_nb[t]] : -1;
+        const char* g = xg + (src >= 0 ? (long long)src * ldx2 + a_cof[t] : 0);
+        if (!(p.dbg & 1)) cp_async16(dst, g, src >= 0 ? 16u : 0u);
       }
-      // B: 64 rows x NPAD/8 groups of dz
-      for (int q = tid; q < KC * (NPAD / 8); q += PROD) {
-        const int kk = q / (NPAD / 8), ng = q - kk * (NPAD / 8);
-        const int i = i0 + kk;
-        const bool ok = i < n && ng * 8 < p.cout;
-        const char* g = reinterpret_cast<const char*>(p.dz) + (ok ? (long long)i * lddz2 + ng * 16 : 0);
-        cp_async16(b_st + ng * 1024 + (kk >> 3) * 128 + (kk & 7) * 16, g, ok ? 16u : 0u);
+#pragma unroll
+      for (int t = 0; t < NBP; ++t) {
+        const int i = i0 + b_row[t];
+        const bool ok = b_ok[t] && i < n;
+        const char* g = dg + (ok ? (long long)i * lddz2 + b_off[t] : 0);
+        if (tid + PROD * t < KC * (NPAD / 8)) cp_async16(b_st + b_dst[t], g, ok ? 16u : 0u);
       }
       cp_async_mbar_arrive_noinc(smem_u32(full + stage));
+      if (tid == 0) wts(p.dbg, 8 * k + 3);
     }
     if (tid == 0) pdl_trigger();
   } else {
-    // ===================== MMA issuer (warp 4, one lane) =====================
-    if (warp == 4 && lane == 0) {
+    // ===================== MMA issuer (one lane) =====================
+    if (warp == W_MMA && lane == 0) {
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
                              ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       for (int c = c0; c < c1; ++c) {
         const int k = c - c0, stage = k % NS;
         mbar_wait(smem_u32(full + stage), (k / NS) & 1);
+        wts(p.dbg, 8 * k + 4);
         tc_fence_after();
         fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor core (async proxy) reads
         const uint32_t a_st = smem_u32(sA + stage * A_STAGE), b_st = smem_u32(sB + stage * B_STAGE);
+        if (!(p.dbg & 2)) {
 #pragma unroll
-        for (int kk = 0; kk < KC / 16; ++kk)
-          umma_bf16(tmem, desc_mn(a_st + kk * 256), desc_mn(b_st + kk * 256), idesc, (k | kk) ? 1u : 0u);
+          for (int kk = 0; kk < KC / 16; ++kk)
+            umma_bf16(tmem, desc_mn(a_st + kk * 256), desc_mn(b_st + kk * 256), idesc, (k | kk) ? 1u : 0u);
+        }
         umma_commit(smem_u32(empty + stage));
+        wts(p.dbg, 8 * k + 5);
       }
       umma_commit(smem_u32(tfull));
     }
-    // ===================== epilogue (warps 4-7): TMEM -> fp32 partial =====================
+    // ===================== epilogue (warps 8-11): TMEM -> fp32 partial =====================
     pdl_wait();
     const int q4 = warp & 3, r = q4 * 32 + lane;
     mbar_wait_sleep(smem_u32(tfull), 0, 128);
@@ -163,16 +251,18 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_tc_kernel(const Params p) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == W_MMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS) : "memory");
   }
 }
 
-// dw[f][co] = sum over splits (fixed order) of part[f / 128][s][f % 128][co]
+// dw[f][co] = sum over splits (fixed order) of part[f / 128][s][f % 128][co];
+// row f = kcin (the all-ones A row, when kcin % 128 != 0) is db
 __global__ void wgrad_reduce_tc_kernel(const float* __restrict__ part, int nsplit, int npad, int kcin, int cout,
-                                       float* __restrict__ dw) {
-  const long long total = (long long)kcin * cout;
+                                       float* __restrict__ dw, float* __restrict__ db) {
+  const int rows = kcin + ((db && (kcin % 128)) ? 1 : 0);
+  const long long total = (long long)rows * cout;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const int f = (int)(t / cout), co = (int)(t - (long long)f * cout);
@@ -180,7 +270,8 @@ __global__ void wgrad_reduce_tc_kernel(const float* __restrict__ part, int nspli
     const float* src = part + ((long long)mb * nsplit * BM + m) * npad + co;
     float s = 0.f;
     for (int k = 0; k < nsplit; ++k) s += src[(long long)k * BM * npad];
-    dw[t] = s;
+    if (f < kcin) dw[t] = s;
+    else db[co] = s;
   }
 }
 
@@ -233,7 +324,7 @@ inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 template <int NPAD>
 int launch(const Params& p, cudaStream_t s) {
   constexpr int B_STAGE = (NPAD / 8) * 1024;
-  constexpr int SMEM = 1024 + NS * (A_STAGE + B_STAGE) + 8 * (2 * NS + 1) + 16;
+  constexpr int SMEM = 1024 + NS * (A_STAGE + B_STAGE) + 1024 + KC * 32 * 4;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(wgrad_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -250,8 +341,12 @@ int launch(const Params& p, cudaStream_t s) {
 
 using namespace fpvs;
 
+extern "C" int fpvs_debug_wgrad_timestamps(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, wg::g_wts, sizeof(unsigned long long) * 4096) == cudaSuccess ? 0 : 3;
+}
+
 extern "C" size_t fpvs_wgrad_tc_workspace_size(int K, int cin, int cout, int cap) {
-  if (K < 1 || cin < 8 || cout < 1 || cout > 256 || cap < 1) return 0;
+  if (K < 1 || cin < 8 || cin % 8 || cout < 1 || cout > 256 || cap < 1) return 0;
   const int nmb = (K * cin + 127) / 128;
   const int ns = wg::splits_for(nmb, cap);
   const size_t part = (size_t)nmb * ns * tc::BM * wg::npad_of(cout) * 4;
@@ -285,13 +380,15 @@ extern "C" int fpvs_spconv_wgrad_tc(const void* x, int ldx, const void* dz, int 
   p.nmb = (K * cin + 127) / 128;
   p.nsplit = wg::splits_for(p.nmb, cap);
   p.part = (float*)workspace;
+  const char* dbg = getenv("FPVS_WGRAD_DEBUG");
+  p.dbg = dbg ? atoi(dbg) : 0;
   cudaStream_t s = as_stream(stream);
   int rc = p.npad == 16 ? wg::launch<16>(p, s) : p.npad == 32 ? wg::launch<32>(p, s) : p.npad == 64 ? wg::launch<64>(p, s)
          : p.npad == 128 ? wg::launch<128>(p, s) : wg::launch<256>(p, s);
   if (rc) return rc;
-  const long long total = (long long)K * cin * cout;
-  wg::wgrad_reduce_tc_kernel<<<grid_for(total, 256), 256, 0, s>>>(p.part, p.nsplit, p.npad, K * cin, cout, dw);
-  if (db) {
+  const long long total = (long long)(K * cin + 1) * cout;
+  wg::wgrad_reduce_tc_kernel<<<grid_for(total, 256), 256, 0, s>>>(p.part, p.nsplit, p.npad, K * cin, cout, dw, db);
+  if (db && (K * cin) % 128 == 0) {
     float* bpart = (float*)((uint8_t*)workspace + wg::align256((size_t)p.nmb * p.nsplit * tc::BM * p.npad * 4));
     const int nb = (cap + wg::DB_ROWS - 1) / wg::DB_ROWS;
     wg::bias_partial_kernel<<<nb, 256, 0, s>>>((const __nv_bfloat16*)dz, lddz, n_dev, cap, cout, bpart);
