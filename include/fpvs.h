@@ -241,7 +241,8 @@ int fpvs_spconv_tc_scatter(const void* x, int ldx, int x_rows, const int32_t* nb
  * tile's K range across CTAs (fp32 partials in ws, reduced in a fixed order by
  * the last CTA: deterministic); split = -S keeps whole waves of tiles whole
  * and cuts only the last partial wave's tiles into up to S K ranges (load
- * balance).  ws = fpvs_spconv_halo_workspace_size bytes,
+ * balance; the workspace then covers one grid of items, not the capacity).
+ * Calls with different (cap, Cout, bn, split) must not share a workspace.  ws = fpvs_spconv_halo_workspace_size bytes,
  * ZEROED before its first use (the kernel leaves its counters at zero). */
 #define FPVS_HALO_MAX 512
 size_t fpvs_kmap_halo_size(int cap);

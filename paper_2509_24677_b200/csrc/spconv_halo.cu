@@ -272,6 +272,7 @@ struct Cfg {
 
 struct Unit {
   int mt, nb, s, ns, npres, q0, q1;  // ns: how many units share this (tile, column block)
+  int slot;                          // split items: partial / counter slot (tail-relative when split < 0)
   uint32_t mask;
 };
 
@@ -294,6 +295,7 @@ __device__ __forceinline__ void unit_of(const Params& p, int u, int cpo, int mti
     item = u / p.split;
     U.s = u - item * p.split;
     U.ns = p.split;
+    U.slot = item;
   } else {
     const int items = mtiles * p.nblk;
     const int full = items / gridDim.x * gridDim.x, rem = items - full;
@@ -302,11 +304,13 @@ __device__ __forceinline__ void unit_of(const Params& p, int u, int cpo, int mti
       item = u;
       U.s = 0;
       U.ns = 1;
+      U.slot = 0;
     } else {
       const int v = u - full;
       item = full + v / ts;
       U.s = v - (item - full) * ts;
       U.ns = ts;
+      U.slot = item - full;  // < grid: the workspace holds only the tail
     }
   }
   U.mt = item / p.nblk;
@@ -618,7 +622,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         // warp's stores and loads are 128-byte coalesced; the last CTA of the
         // tile to arrive sums the splits in a fixed order (deterministic),
         // taking its own split from TMEM
-        const long long slot = (long long)U.mt * p.nblk + U.nb;
+        const long long slot = U.slot;
         const bool has = U.q1 > U.q0;
         float* mine = p.part + (slot * p.smax + U.s) * BM * BN + r;
 #pragma unroll 1
@@ -763,11 +767,14 @@ extern "C" int fpvs_kmap_halo(const int32_t* nbr, const int32_t* n_dev, int cap,
 }
 
 extern "C" size_t fpvs_spconv_halo_workspace_size(int cap, int cout, int bn, int split) {
-  if (split < 0) split = -split;
-  if (cap < 1 || (bn != 64 && bn != 128 && bn != 256) || cout % bn || split < 1) return 0;
+  if (cap < 1 || (bn != 64 && bn != 128 && bn != 256) || split == 0) return 0;
+  if (cout % bn) return 0;
   const size_t tiles = (cap + tc::BM - 1) / tc::BM, nblk = cout / bn;
-  size_t b = halo::align256(tiles * nblk * 4);
-  if (split > 1) b += tiles * nblk * split * tc::BM * bn * 4;
+  // split < 0: only the last partial wave (< one grid of items) is split
+  const size_t items = split < 0 ? (size_t)kNumSMs : tiles * nblk;
+  const size_t sm = split < 0 ? (size_t)-split : (size_t)split;
+  size_t b = halo::align256(items * 4);
+  if (sm > 1) b += items * sm * tc::BM * bn * 4;
   return b;
 }
 
@@ -815,8 +822,9 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
   p.ldy = ldy;
   p.col_off = col_off;
   const size_t tiles = (cap + tc::BM - 1) / tc::BM;
+  const size_t items = split < 0 ? (size_t)kNumSMs : tiles * p.nblk;
   p.counters = (int*)ws;
-  p.part = (float*)((uint8_t*)ws + halo::align256(tiles * p.nblk * 4));
+  p.part = (float*)((uint8_t*)ws + halo::align256(items * 4));
   const char* dbg = getenv("FPVS_HALO_DEBUG");
   p.dbg = dbg ? atoi(dbg) : 0;
   if (bn == 64) return halo::launch<64>(p, as_stream(stream));

@@ -150,7 +150,7 @@ class UNetPlan:
         layer has about two waves of work units; ``cfg`` overrides."""
         torch = _torch()
         self.halo_cfg = {}
-        need = 256
+        need = {}  # one workspace per level: layers of a level share (cap, Cout, bn, split)
         for name, r in rows.items():
             layer = self.net.layers[name]
             cin, cout = layer.spec.in_channels, layer.spec.out_channels
@@ -166,10 +166,17 @@ class UNetPlan:
             if cfg and name in cfg:
                 bn, split = cfg[name]
             self.halo_cfg[name] = (bn, split)
-            cap = self.level_of[name].cap
-            need = max(need, _lib.size("fpvs_spconv_halo_workspace_size", cap, cout, bn, split))
-        if self.halo_ws is None or self.halo_ws.numel() < need:
-            self.halo_ws = torch.zeros(need, dtype=torch.uint8, device=self.L0.coords.device)
+            lv = self.level_of[name]
+            key = id(lv)
+            need[key] = max(need.get(key, 256),
+                            _lib.size("fpvs_spconv_halo_workspace_size", lv.cap, cout, bn, split))
+        if self.halo_ws is None:
+            self.halo_ws = {}
+        for key, nbytes in need.items():
+            if key not in self.halo_ws or self.halo_ws[key].numel() < nbytes:
+                self.halo_ws[key] = torch.zeros(nbytes, dtype=torch.uint8, device=self.L0.coords.device)
+            else:
+                self.halo_ws[key].zero_()  # the counter region moves with the split mode
 
     def tune(self, bits):
         """Pick per-layer tile widths from one frame's active counts (one host sync).
@@ -229,7 +236,7 @@ class UNetPlan:
         def conv(name, x, ldx, table, K, lv, y, ldy, off=0, masks=None):
             def launch():
                 hc = self.halo_cfg.get(name) if K == 27 else None
-                halo = (hc[0], hc[1], self.halo_ws) if hc else None
+                halo = (hc[0], hc[1], self.halo_ws[id(lv)]) if hc else None
                 us = lv.extra.get("upsort") if (self.use_upsort and name in ("up21", "up10")) else None
                 if us is not None:
                     run_conv(L[name], x, ldx, us["table"], K, us["n"], us["cap"], y, ldy, off, P, act="relu",
