@@ -24,6 +24,9 @@ halo tables), sparse interleave, 14 convs, head.
   launch from the committed ncu --set full capture (profiles/).
 * ``cpu_baseline``: the numpy sparse restatement (oracle/, fp64) of the same
   frame on this host's cores (rank 0, N=1).
+* ``train_config5`` (extra, rank 0): BASELINE config 5's training step on one
+  GPU (8 x 128^3 grids, bf16 + fp32 master weights, AdamW, tcgen05 backward),
+  10 steps timed with CUDA events; a reported side line, not the metric.
 
 Multi-GPU: one process per GPU (torchrun); frames are independent ("replicas
 only" per frame): each rank runs its own frames, no
@@ -179,6 +182,38 @@ def count_launches(fn):
     return n[0]
 
 
+def train_config5(steps: int = 10):
+    """BASELINE config 5 on this GPU: 8 grids of 128^3 per step, config-1 net, bf16
+    compute with fp32 master weights, AdamW; forward + fused loss + tcgen05
+    backward + update per step (the gradient all-reduce is the identity at N=1)."""
+    import torch
+    from paper_2509_24677_b200 import synth
+    from paper_2509_24677_b200.froxel import FroxelGrid
+    from paper_2509_24677_b200.neural import ModelConfig, PvsNet, TrainConfig
+    from paper_2509_24677_b200.train import TrainStep
+    B = 8
+    pairs = [synth.config5_pair(0, i) for i in range(B)]
+    bits = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(g).bits for g, _ in pairs])).cuda()
+    gt = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(lb).bits for _, lb in pairs])).cuda()
+    net = PvsNet(ModelConfig.config1(), np.random.Generator(np.random.PCG64(0)), precision="bf16")
+    step = TrainStep(net, B, (128, 128, 128), TrainConfig(optimizer="adamw", lr=1e-3))
+    for i in range(3):
+        step.forward_backward(bits, gt)
+        step.update(1e-3, i + 1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        step.forward_backward(bits, gt)
+        step.update(1e-3, 4 + i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return {"workload": "config5: 8 x 128^3 grids/step, config-1 net, bf16 + fp32 master, AdamW lr 1e-3",
+            "ms_per_step": ms, "grids_per_s": B / (ms * 1e-3), "active_rows": step.lv.count(),
+            "loss": float(step.loss), "backward": "tcgen05 dgrad + wgrad", "steps": steps}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -290,6 +325,9 @@ def run_ours(args):
         pass
 
     cpu = None
+    train = None
+    if not args.no_train:
+        train = train_config5()
     if ws == 1 and not args.no_cpu_baseline:
         t_cpu = cpu_frame_time(occ)
         cpu = {"value": 1.0 / t_cpu, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
@@ -322,6 +360,8 @@ def run_ours(args):
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if train is not None:
+        line["train_config5"] = train
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -335,6 +375,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train", action="store_true", help="skip the config-5 training-step line")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
