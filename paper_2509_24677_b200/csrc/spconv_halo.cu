@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       mbar_init(smem_u32(tempty + a), 4);
     }
     for (int a = 0; a < C::NHB; ++a) {
-      mbar_init(smem_u32(hfull + a), LOADERS);
+      mbar_init(smem_u32(hfull + a), LOADERS + 8 * 32);  // loaders + every builder thread (see below)
       mbar_init(smem_u32(hempty + a), 8);
       mbar_init(smem_u32(hmeta + a), 1);
     }
@@ -425,6 +425,21 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         const int hb = gc % C::NHB;
         const uint32_t hph = (gc / C::NHB) & 1;
         mbar_wait(smem_u32(hmeta + hb), hph);
+        if (gc == 0) {
+          // the CTA's first halo: nothing to overlap it with, so the 8 builder
+          // warps copy it together with the 2 loader warps (10 warps instead of 2)
+          const int H = __ldg(p.halo_n + U.mt);
+          const int pt = LOADERS + tid, pc = pt & 7;
+          const int* hr = reinterpret_cast<const int*>(smem + hb * HBUF + ROWS_OFF);
+          const char* xb = reinterpret_cast<const char*>(p.x) + c * 128 + pc * 16;
+          const uint32_t hs = smem_u32(smem + hb * HBUF);
+#pragma unroll 4
+          for (int i = pt >> 3; i < H; i += (LOADERS + 256) / 8)
+            cp_async16(hs + i * 128 + ((pc ^ (i & 7)) << 4), xb + (long long)hr[i] * ldx2, 16);
+          cp_async_mbar_arrive_noinc(smem_u32(hfull + hb));
+        } else {
+          mbar_arrive(smem_u32(hfull + hb));  // builders add no copies to later halos
+        }
         mbar_wait(smem_u32(hfull + hb), hph);
         if (lane == 0 && q4 == 0) HTS(256 + 4 * gc + 2 * bg);
         const uint8_t* hbuf = smem + hb * HBUF;
@@ -512,8 +527,11 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         const int* hr = reinterpret_cast<const int*>(hbuf + ROWS_OFF);
         const char* xb = reinterpret_cast<const char*>(p.x) + c * 128 + pc * 16;
         const uint32_t hs = smem_u32(hbuf);
+        // the first halo is shared with the builders: loader thread tl takes rows
+        // tl/8 + 40k of the 320-thread split; later halos rows tl/8 + 8k
+        const int rstep = gc == 0 ? (LOADERS + 256) / 8 : LOADERS / 8;
 #pragma unroll 4
-        for (int i = tl >> 3; i < H; i += LOADERS / 8) {
+        for (int i = tl >> 3; i < H; i += rstep) {
           const int g = hr[i];
           cp_async16(hs + i * 128 + ((pc ^ (i & 7)) << 4), xb + (long long)g * ldx2, 16);
         }
