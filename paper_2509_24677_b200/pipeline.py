@@ -111,6 +111,9 @@ def device_stage_times(plan, bits, out_bits, tau: float = 0.5, reps: int = 20, f
     excluded.  ``flush`` (a buffer > L2) is cleared before each replay."""
     torch = _torch()
     res = {}
+    saved = getattr(plan, "overlap", None)
+    if saved is not None:
+        plan.overlap = False  # each stage is captured alone: no cross-stage side stream
     for name, fn in plan.stages(bits, out_bits, tau):
         fn()
         torch.cuda.synchronize()
@@ -134,6 +137,8 @@ def device_stage_times(plan, bits, out_bits, tau: float = 0.5, reps: int = 20, f
             times.append(e0.elapsed_time(e1) / reps)
         res[name] = min(times)
         del g
+    if saved is not None:
+        plan.overlap = saved
     return res
 
 

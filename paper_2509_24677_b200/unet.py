@@ -142,6 +142,9 @@ class UNetPlan:
         # up convs run on parity-sorted rows (one weight slice per tile); FPVS_UPSORT=0 disables
         self.use_upsort = net.precision == "bf16" and os.environ.get("FPVS_UPSORT", "1") != "0"
         self._up_sorter = None
+        self.overlap = True  # side-stream map tables (see build_maps); device_stage_times turns it off
+        self._side = None
+        self._side_pending = False
         if self.use_halo:
             self.set_halo({k: lv.cap for k, lv in self.level_of.items()})
 
@@ -202,14 +205,41 @@ class UNetPlan:
             sp.fill_level_from_bits(self.L0, bits, self.grid_dims, self.net.d)
             sp.fill_coarse(self.L0, self.L1, self.down01, self.up10)
             sp.fill_coarse(self.L1, self.L2, self.down12, self.up21)
-        if self.use_upsort:
-            if self._up_sorter is None:
-                self._up_sorter = sp.UpSorter([(self.L1, self.up21), (self.L0, self.up10)])
-            self._up_sorter.run()
         if self.use_halo:
             if self._halo_builder is None:
-                self._halo_builder = sp.HaloBuilder([self.L0, self.L1, self.L2])
-            self._halo_builder.run()
+                self._halo_builder = sp.HaloBuilder([self.L0])
+                self._halo_builder_coarse = sp.HaloBuilder([self.L1, self.L2])
+            self._halo_builder.run()  # level 0: needed by the first conv
+        # the up-sort tables and the level-1/2 halo tables are first used by
+        # enc1a / up21: with ``overlap`` they run on a side stream, filling SMs
+        # the level-0 convs leave idle at their tails (joined before enc1a)
+        torch = _torch()
+        side = self.overlap and (self.use_upsort or self.use_halo)
+        if side:
+            if self._side is None:
+                self._side = torch.cuda.Stream()
+                self._ev_maps, self._ev_side = torch.cuda.Event(), torch.cuda.Event()
+            self._ev_maps.record()
+            self._side.wait_event(self._ev_maps)
+            ctx = torch.cuda.stream(self._side)
+        else:
+            import contextlib
+            ctx = contextlib.nullcontext()
+        with ctx:
+            if self.use_upsort:
+                if self._up_sorter is None:
+                    self._up_sorter = sp.UpSorter([(self.L1, self.up21), (self.L0, self.up10)])
+                self._up_sorter.run()
+            if self.use_halo:
+                self._halo_builder_coarse.run()
+        if side:
+            self._ev_side.record(self._side)
+            self._side_pending = True
+
+    def _join_side(self):
+        if self._side_pending:
+            _torch().cuda.current_stream().wait_event(self._ev_side)
+            self._side_pending = False
 
     def stages(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None, maps: bool = True):
         """The frame as an ordered list of (stage name, launch function).
@@ -235,6 +265,8 @@ class UNetPlan:
 
         def conv(name, x, ldx, table, K, lv, y, ldy, off=0, masks=None):
             def launch():
+                if name == "enc1a":
+                    self._join_side()
                 hc = self.halo_cfg.get(name) if K == 27 else None
                 halo = (hc[0], hc[1], self.halo_ws[id(lv)]) if hc else None
                 us = lv.extra.get("upsort") if (self.use_upsort and name in ("up21", "up10")) else None
