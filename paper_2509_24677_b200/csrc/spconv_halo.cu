@@ -239,6 +239,11 @@ __device__ unsigned g_hsm[160];
     }                                                                                    \
   } while (0)
 
+// Per-CTA unit table: the tile mask and halo size of this CTA's k-th unit,
+// loaded once in the prologue so no role pays a global-memory round trip at a
+// unit boundary (the MMA thread would stall ~1 us on it).
+constexpr int kUnitCache = 64;
+
 constexpr int W_LOAD = 8;   // warps 8, 9: halo loaders
 constexpr int W_B = 10;     // weight loader
 constexpr int W_MMA = 11;   // MMA issuer, TMEM owner
@@ -251,6 +256,12 @@ constexpr int LOADERS = 64;
 // stage (tcgen05 commits measured ~70-150 cycles each at N <= 128).
 // BN = 256 keeps a single accumulator (256 TMEM columns) and a single halo
 // buffer (its smem goes to the 32 KB weight chunks).
+struct Unit {
+  int mt, nb, s, ns, npres, q0, q1;  // ns: how many units share this (tile, column block)
+  int slot;                          // split items: partial / counter slot (tail-relative when split < 0)
+  uint32_t mask;
+};
+
 template <int BN>
 struct Cfg {
   static constexpr int G = BN == 64 ? 2 : 1;  // chunks per stage (BN >= 128: deeper weight prefetch instead)
@@ -265,16 +276,12 @@ struct Cfg {
   static constexpr int NBARS = 2 * NS + 2 * NACC + 3 * NHB;
   static constexpr int CTRL_OFF = BAR_OFF + 8 * NBARS;
   static constexpr int BIAS_OFF = CTRL_OFF + 64;
-  static constexpr int SMEM = 1024 + BIAS_OFF + 4 * 1024;
+  static constexpr int UC_OFF = BIAS_OFF + 4 * 1024;  // unit cache: Unit [64] + halo sizes [64]
+  static constexpr int SMEM = 1024 + UC_OFF + kUnitCache * (int)sizeof(Unit) + kUnitCache * 4;
   static_assert(ACOL + NS * G * 32 <= 512, "TMEM columns");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-struct Unit {
-  int mt, nb, s, ns, npres, q0, q1;  // ns: how many units share this (tile, column block)
-  int slot;                          // split items: partial / counter slot (tail-relative when split < 0)
-  uint32_t mask;
-};
 
 // Work items are (tile, column block) pairs.  split > 0: every item is cut
 // into `split` K ranges.  split < 0 (tail balancing): the whole waves of items
@@ -318,9 +325,22 @@ __device__ __forceinline__ void unit_of(const Params& p, int u, int cpo, int mti
   U.mask = __ldg(p.tile_masks + U.mt);
   if (!U.mask) U.mask = 1u << 13;
   U.npres = __popc(U.mask);
-  const long long L = (long long)cpo * U.npres;
-  U.q0 = (int)(U.s * L / U.ns);
-  U.q1 = (int)((U.s + 1) * L / U.ns);
+  // 32-bit: L <= 27 * Cin / 64 (a 64-bit divide is a long software sequence on
+  // the MMA thread's critical path at every unit boundary)
+  const int L = cpo * U.npres;
+  if (U.ns == 1) {
+    U.q0 = 0;
+    U.q1 = L;
+  } else {
+    U.q0 = U.s * L / U.ns;
+    U.q1 = (U.s + 1) * L / U.ns;
+  }
+}
+
+__device__ __forceinline__ void get_unit(const Params& p, int u, int cpo, int mtiles, Unit& U, const Unit* s_units) {
+  const int k = (u - (int)blockIdx.x) / (int)gridDim.x;
+  if (k < kUnitCache) U = s_units[k];
+  else unit_of(p, u, cpo, mtiles, U);
 }
 
 // offset of the q-th chunk inside channel chunk c: the (q - c*npres)-th set bit
@@ -364,6 +384,8 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::CTRL_OFF);
   volatile int* s_last = reinterpret_cast<volatile int*>(smem + C::CTRL_OFF + 16);
   float* s_bias = reinterpret_cast<float*>(smem + C::BIAS_OFF);
+  Unit* s_units = reinterpret_cast<Unit*>(smem + C::UC_OFF);
+  int* s_uhn = reinterpret_cast<int*>(smem + C::UC_OFF + kUnitCache * sizeof(Unit));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) HTS(0);
@@ -397,6 +419,19 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     fence_mbar_init();
   }
   for (int c = tid; c < p.cout; c += THREADS) s_bias[c] = p.bias ? p.bias[c] : 0.f;
+  if (tid < kUnitCache) {
+    // this CTA's units decoded in parallel (tile masks and halo sizes come
+    // from the map kernels, two or more launches back)
+    const int u = blockIdx.x + tid * gridDim.x;
+    Unit U{};
+    int hn = 0;
+    if (u < nunits) {
+      unit_of(p, u, cpo, mtiles, U);
+      hn = __ldg(p.halo_n + U.mt);
+    }
+    s_units[tid] = U;
+    s_uhn[tid] = hn;
+  }
   if (warp == W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem))
                  : "memory");
@@ -418,7 +453,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     uint32_t sc0 = 0, gc = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
-      unit_of(p, u, cpo, mtiles, U);
+      get_unit(p, u, cpo, mtiles, U, s_units);
       const int nq = U.q1 - U.q0;
       for (int c = U.q0 / U.npres; nq > 0 && c * U.npres < U.q1; ++c) {
         const int qs = max(U.q0, c * U.npres), qe = min(U.q1, (c + 1) * U.npres);
@@ -428,7 +463,8 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         if (gc == 0) {
           // the CTA's first halo: nothing to overlap it with, so the 8 builder
           // warps copy it together with the 2 loader warps (10 warps instead of 2)
-          const int H = __ldg(p.halo_n + U.mt);
+          const int ku = (u - (int)blockIdx.x) / (int)gridDim.x;
+          const int H = ku < kUnitCache ? s_uhn[ku] : __ldg(p.halo_n + U.mt);
           const int pt = LOADERS + tid, pc = pt & 7;
           const int* hr = reinterpret_cast<const int*>(smem + hb * HBUF + ROWS_OFF);
           const char* xb = reinterpret_cast<const char*>(p.x) + c * 128 + pc * 16;
@@ -506,14 +542,15 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     uint32_t gc = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
-      unit_of(p, u, cpo, mtiles, U);
+      get_unit(p, u, cpo, mtiles, U, s_units);
       for (int c = U.q0 / U.npres; U.q1 > U.q0 && c * U.npres < U.q1; ++c) {
         const int hb = gc % C::NHB;
         const uint32_t hph = (gc / C::NHB) & 1;
         mbar_wait_sleep(smem_u32(hempty + hb), hph ^ 1, 64);
         if (tl == 0) HTS(16 + 3 * gc);
         uint8_t* hbuf = smem + hb * HBUF;
-        const int H = __ldg(p.halo_n + U.mt);
+        const int ku = (u - (int)blockIdx.x) / (int)gridDim.x;
+        const int H = ku < kUnitCache ? s_uhn[ku] : __ldg(p.halo_n + U.mt);
         if (tl == 0) {
           // the tile's local table and its halo row list, one bulk copy each
           const uint32_t rb = (uint32_t)((H * 4 + 15) & ~15);
@@ -546,7 +583,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       uint32_t st = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         Unit U;
-        unit_of(p, u, cpo, mtiles, U);
+        get_unit(p, u, cpo, mtiles, U, s_units);
         const int nq = U.q1 - U.q0;
         const uint8_t* wblk = p.wpk + (size_t)U.nb * p.nchunks * C::B_SUB;
         ChunkWalk w;
@@ -571,10 +608,12 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       uint32_t st = 0;
       int it = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+        HTS(7600 + 2 * it);
         Unit U;
-        unit_of(p, u, cpo, mtiles, U);
+        get_unit(p, u, cpo, mtiles, U, s_units);
         const int nq = U.q1 - U.q0;
         const int acc = it % C::NACC;
+        HTS(7601 + 2 * it);
         mbar_wait(smem_u32(tempty + acc), ((it / C::NACC) & 1) ^ 1);
         HTS(7000 + 2 * it);
         tc_fence_after();
@@ -607,7 +646,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     int it = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
       Unit U;
-      unit_of(p, u, cpo, mtiles, U);
+      get_unit(p, u, cpo, mtiles, U, s_units);
       const int acc = it % C::NACC;
       mbar_wait_sleep(smem_u32(tfull + acc), (it / C::NACC) & 1, 128);
       if (q4 == 0 && lane == 0) HTS(7200 + 2 * it);

@@ -64,9 +64,12 @@ print(f"halo build, 3 levels one launch: {e0.elapsed_time(e1) / 20 * 1000:.1f} u
 
 rows = {k: lv.count() for k, lv in plan.level_of.items()}
 variants = {
-    "L0 tail-split 2": {k: (64, -2) for k in L0},
-    "L0 tail-split 3": {k: (64, -3) for k in L0},
-    "L0 tail-split 4": {k: (64, -4) for k in L0},
+    "L2 bn256 s2": {k: (256, 2) for k in L2},
+    "L2 bn256 s3": {k: (256, 3) for k in L2},
+    "L2 bn256 s4": {k: (256, 4) for k in L2},
+    "L2 bn128 s3": {k: (128, 3) for k in L2},
+    "L1 bn128 s2": {k: (128, 2) for k in L1},
+    "L0 s1": {k: (64, 1) for k in L0},
 }
 for tag, cfg in (variants.items() if os.environ.get("SWEEP", "1") == "1" else []):
     plan.set_halo(rows, cfg)

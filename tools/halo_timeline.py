@@ -66,7 +66,8 @@ for name in os.environ.get("LAYERS", "enc0b,enc1a,enc2a").split(","):
         if not t[7000 + 2 * it]:
             break
         print(f"  unit {it}: mma tempty {rel(t[7000 + 2 * it]):7.2f} tfull {rel(t[7001 + 2 * it]):7.2f} "
-              f"epi got {rel(t[7200 + 2 * it]):7.2f} | split: partial written {rel(t[7400 + 4 * it]):7.2f} "
+              f"epi got {rel(t[7200 + 2 * it]):7.2f} | loop top {rel(t[7600 + 2 * it]):7.2f} "
+              f"unit_of done {rel(t[7601 + 2 * it]):7.2f} | split: partial written {rel(t[7400 + 4 * it]):7.2f} "
               f"counted {rel(t[7402 + 4 * it]):7.2f} "
               f"reduced {rel(t[7403 + 4 * it]):7.2f}")
     rows = []
