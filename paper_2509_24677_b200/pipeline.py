@@ -171,15 +171,19 @@ class FramePipeline:
         torch.cuda.synchronize()
         if not self._use_graph:
             return
+        self.graph = self._capture(self.in_bits, self.out_bits)
+
+    def _capture(self, in_bits, out_bits):
+        torch = _torch()
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
-                self.plan.run(self.in_bits, self.out_bits, self.tau)
+                self.plan.run(in_bits, out_bits, self.tau)
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        self.graph = g
+        return g
 
     def run_device(self):
         if self.graph is not None:
@@ -198,3 +202,55 @@ class FramePipeline:
             host_out = torch.empty(self.out_bits.numel(), dtype=torch.uint8, pin_memory=True)
         host_out.copy_(self.out_bits, non_blocking=True)
         return host_out
+
+    # -- streaming: overlap frame i's compute with frame i+1's upload and
+    # frame i-1's download (double-buffered device grids, one graph each) ----
+    def _ensure_streaming(self):
+        if getattr(self, "_stream_bufs", None) is not None:
+            return
+        torch = _torch()
+        if self.graph is None:
+            self.capture(tune=False)
+        in2, out2 = torch.zeros_like(self.in_bits), torch.zeros_like(self.out_bits)
+        self.plan.run(in2, out2, self.tau)
+        torch.cuda.synchronize()
+        g2 = self._capture(in2, out2) if self._use_graph else None
+        self._stream_bufs = [(self.in_bits, self.out_bits, self.graph), (in2, out2, g2)]
+        self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        self._ev = {k: [torch.cuda.Event(), torch.cuda.Event()] for k in ("h2d", "comp", "d2h")}
+
+    def infer_stream(self, host_ins, host_outs):
+        """Frames ``host_ins[i]`` (pinned packed grids) -> ``host_outs[i]`` (pinned).
+
+        Every frame is uploaded, run and downloaded; the upload of frame i+1
+        and the download of frame i-1 run on copy streams while frame i
+        computes.  Enqueues on the current stream (which joins the copy
+        streams at the end); the caller synchronises."""
+        torch = _torch()
+        self._ensure_streaming()
+        comp = torch.cuda.current_stream()
+        ev = self._ev
+        for b in range(2):
+            ev["comp"][b].record(comp)
+            ev["d2h"][b].record(comp)
+        for i, (hin, hout) in enumerate(zip(host_ins, host_outs)):
+            b = i % 2
+            din, dout, g = self._stream_bufs[b]
+            self._h2d.wait_event(ev["comp"][b])  # frame i-2 no longer reads din
+            with torch.cuda.stream(self._h2d):
+                din.copy_(torch.as_tensor(hin), non_blocking=True)
+            ev["h2d"][b].record(self._h2d)
+            comp.wait_event(ev["h2d"][b])
+            comp.wait_event(ev["d2h"][b])  # frame i-2's result has left dout
+            if g is not None:
+                g.replay()
+            else:
+                self.plan.run(din, dout, self.tau)
+            ev["comp"][b].record(comp)
+            self._d2h.wait_event(ev["comp"][b])
+            with torch.cuda.stream(self._d2h):
+                hout.copy_(dout, non_blocking=True)
+            ev["d2h"][b].record(self._d2h)
+        comp.wait_stream(self._d2h)
+        comp.wait_stream(self._h2d)
+        return host_outs
