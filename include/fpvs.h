@@ -353,6 +353,36 @@ int fpvs_bits_confusion(const uint8_t* pred_bits, const uint8_t* gt_bits, int B,
 int fpvs_first_hit_labels(const uint8_t* bits, int B, int Nx, int Ny, int Nz, int radius,
                           uint8_t* out_bits, int32_t* zfirst_ws, void* stream);
 
+/* ---- (§8(f) #1) perspective froxelization ------------------------------ */
+/* Frustum of pkg/src/froxelpvs/core.py:297-325 as the rasterizer reads it:
+ * origin (_o), basis rows (right, up, forward) (_basis), half_extent =
+ * tan(fov/2), near, far. */
+typedef struct {
+  double origin[3];
+  double basis[9];
+  double half_extent, near_z, far_z;
+} fpvs_frustum;
+
+enum { FPVS_DEPTH_LINEAR = 0, FPVS_DEPTH_LOG = 1 };
+
+/* Rasterize a triangle scene into a packed geometry grid; replaces
+ * froxel.py:387-394 froxelize() in mode "perspective" (froxel.py:328-348,
+ * 292-325, 229-285, 203-219).  verts: float64 [nverts][3] world positions;
+ * tris: int64 [ntris][3] vertex indices (TriScene.triangles, after its
+ * degenerate-triangle drop); frustum: HOST pointer; dims (Nx % 8 == 0),
+ * supersample >= 1, depth_mode FPVS_DEPTH_*.  out_bits (Nz, Ny, Nx/8) is
+ * overwritten.  Triangle indices outside [0, nverts) are skipped.  Results
+ * equal the reference bit-for-bit in linear depth mode (the arithmetic is
+ * the reference's float64 expression sequence, unfused). */
+size_t fpvs_froxelize_workspace_size(long long ntris, int Nx, int Ny, int Nz);
+int fpvs_froxelize(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                   const fpvs_frustum* frustum, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                   uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream);
+/* Debug/measurement: number of candidate samples (sum of clipped bounding
+ * boxes) of the last fpvs_froxelize on this workspace, read back to host
+ * (synchronises the stream). */
+long long fpvs_froxelize_samples(const void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -73,6 +73,9 @@ SIGNATURES = {
     "fpvs_bits_confusion_workspace_size": (_z, [_i]),
     "fpvs_bits_confusion": (_i, [_p, _p, _i, C.c_longlong, _p, _p, _z, _p]),
     "fpvs_first_hit_labels": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p]),
+    "fpvs_froxelize_workspace_size": (_z, [C.c_longlong, _i, _i, _i]),
+    "fpvs_froxelize": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _i, _i, _i, _i, _i, _p, _p, _z, _p]),
+    "fpvs_froxelize_samples": (C.c_longlong, [_p, _p]),
 }
 
 
@@ -81,6 +84,12 @@ class Level(C.Structure):
     """struct fpvs_level (include/fpvs.h)."""
     _fields_ = [("coords", _p), ("index_vol", _p), ("n", _p), ("cap", _i), ("nbr", _p), ("nbr_masks", _p),
                 ("down", _p), ("down_masks", _p), ("up", _p), ("up_masks", _p)]
+
+
+class Frustum(C.Structure):
+    """fpvs_frustum (include/fpvs.h)."""
+    _fields_ = [("origin", C.c_double * 3), ("basis", C.c_double * 9), ("half_extent", C.c_double),
+                ("near_z", C.c_double), ("far_z", C.c_double)]
 
 
 class HaloJob(C.Structure):

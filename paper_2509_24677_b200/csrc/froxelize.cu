@@ -1,0 +1,415 @@
+// Perspective froxelization on sm_100a.
+//
+// Replaces froxel.py:387-394 froxelize() in "perspective" mode: every scene
+// triangle is moved to camera space, culled and clipped against the near
+// plane (froxel.py:292-325, Sutherland-Hodgman 203-219), projected to the
+// supersampled screen, rasterized at pixel centres with inclusive edge tests
+// (froxel.py:229-285), its perspective-correct depth quantized into a froxel
+// (froxel.py:28-42, 328-348) whose bit is OR-ed into the packed grid.
+//
+// Bit parity.  The reference computes in float64 with numpy, one rounding
+// per operation; every expression below uses the explicit-rounding
+// intrinsics (__dadd_rn, __dmul_rn, __ddiv_rn ...) in the reference's
+// evaluation order, so the compiler can neither contract nor reassociate.
+// The one place numpy fuses is the camera transform: (v - o) @ basis.T goes
+// through the BLAS dgemm kernel, which accumulates the k = 3 dot product as
+// fma(d2, b2, fma(d1, b1, d0 * b0)); cam_xyz() restates that order.
+//
+// Kernels (one stream, three launches after the output memset):
+//  1. setup: one thread per scene triangle -> up to two clipped screen
+//     triangles (slots 2t, 2t+1) with their edge/depth constants and pixel
+//     bounding box; each CTA also scans its 512 slots' sample counts
+//     (bbox area) into a block-local inclusive prefix + the block total.
+//  2. scan: one CTA turns the block totals into exclusive block offsets and
+//     the grand total of candidate samples.
+//  3. raster: persistent CTAs walk the flat sample space in 2048-sample
+//     chunks; each thread finds its slot by a two-level binary search
+//     (block offsets, then the block-local prefix), caches the slot's
+//     constants while consecutive samples stay inside it, evaluates the
+//     coverage/depth test and atomically ORs the froxel's bit into the
+//     32-bit word that holds it.  Work per chunk is uniform no matter how
+//     large or small the triangles are (a floor quad of 10^6 samples and
+//     10^4 slivers of one sample cost the same per sample).
+#include "common.cuh"
+
+namespace fpvs {
+namespace frox {
+
+constexpr int kSetupThreads = 256;
+constexpr int kSlotsPerBlock = 2 * kSetupThreads;
+constexpr int kRasterThreads = 256;
+constexpr int kPerThread = 8;
+constexpr int kChunk = kRasterThreads * kPerThread;
+constexpr double kDegenEps = 1e-12;  // froxel.py:23
+
+struct __align__(16) Slot {
+  double v0x, v0y, e1x, e1y, e2x, e2y, den;
+  double iz0, iz1, iz2;  // 1/z per vertex
+  double wv0, wv1, wv2;  // per-vertex depth coordinate
+  int x0, y0, w, h;
+  int pad[2];
+};
+static_assert(sizeof(Slot) == 128, "slot record is one 128-byte line");
+
+struct Params {
+  double o[3], b[9];
+  double h, nearz, farz;
+  double sx, sy;   // supersampled screen size (as float64, as the reference multiplies)
+  int isx, isy;
+  int nx, ny, nz;
+  int depth_log;
+};
+
+struct Work {
+  Slot* slots;
+  unsigned long long* lp;    // [2T] block-local inclusive prefix of slot sample counts
+  unsigned long long* bsum;  // [nb]
+  unsigned long long* bpre;  // [nb] exclusive block offsets
+  unsigned long long* total;
+  unsigned int* out_words;
+  long long ntris;
+  int nb;
+};
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+struct V3 {
+  double x, y, z;
+};
+
+// (v - o) @ basis.T, with dgemm's k = 3 accumulation order (froxel.py:288-289).
+__device__ __forceinline__ V3 cam_xyz(const Params& p, const double* v) {
+  const double d0 = dsub(v[0], p.o[0]), d1 = dsub(v[1], p.o[1]), d2 = dsub(v[2], p.o[2]);
+  V3 c;
+  c.x = __fma_rn(d2, p.b[2], __fma_rn(d1, p.b[1], dmul(d0, p.b[0])));
+  c.y = __fma_rn(d2, p.b[5], __fma_rn(d1, p.b[4], dmul(d0, p.b[3])));
+  c.z = __fma_rn(d2, p.b[8], __fma_rn(d1, p.b[7], dmul(d0, p.b[6])));
+  return c;
+}
+
+// p + t * (q - p) per component (froxel.py:218).
+__device__ __forceinline__ V3 lerp(const V3& p, const V3& q, double t) {
+  return V3{dadd(p.x, dmul(t, dsub(q.x, p.x))), dadd(p.y, dmul(t, dsub(q.y, p.y))),
+            dadd(p.z, dmul(t, dsub(q.z, p.z)))};
+}
+
+// Screen triangle (a, b, c) in camera space -> slot constants; returns the
+// sample count (0 when culled as degenerate or off-screen).
+__device__ unsigned long long make_slot(const Params& p, const V3& a, const V3& b, const V3& c, Slot& s) {
+  const V3 v[3] = {a, b, c};
+  double u[3], vv[3], iz[3], wv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    // u = (0.5 + 0.5 * x / (z * h)) * W   (froxel.py:322-323)
+    const double zh = dmul(v[k].z, p.h);
+    u[k] = dmul(dadd(0.5, ddiv(dmul(0.5, v[k].x), zh)), p.sx);
+    vv[k] = dmul(dadd(0.5, ddiv(dmul(0.5, v[k].y), zh)), p.sy);
+    iz[k] = ddiv(1.0, v[k].z);
+    // froxel.py:335-338
+    if (p.depth_log)
+      wv[k] = ddiv(log(ddiv(1.0, dmul(iz[k], p.nearz))), log(ddiv(p.farz, p.nearz)));
+    else
+      wv[k] = ddiv(dsub(ddiv(1.0, iz[k]), p.nearz), dsub(p.farz, p.nearz));
+  }
+  // froxel.py:243-259
+  s.v0x = u[0];
+  s.v0y = vv[0];
+  s.e1x = dsub(u[1], u[0]);
+  s.e1y = dsub(vv[1], vv[0]);
+  s.e2x = dsub(u[2], u[0]);
+  s.e2y = dsub(vv[2], vv[0]);
+  s.den = dsub(dmul(s.e1x, s.e2y), dmul(s.e2x, s.e1y));
+  s.iz0 = iz[0];
+  s.iz1 = iz[1];
+  s.iz2 = iz[2];
+  s.wv0 = wv[0];
+  s.wv1 = wv[1];
+  s.wv2 = wv[2];
+  const double minx = fmin(fmin(u[0], u[1]), u[2]), maxx = fmax(fmax(u[0], u[1]), u[2]);
+  const double miny = fmin(fmin(vv[0], vv[1]), vv[2]), maxy = fmax(fmax(vv[0], vv[1]), vv[2]);
+  const double x0 = fmin(fmax(ceil(dsub(minx, 0.5)), 0.0), p.sx);
+  const double x1 = fmin(fmax(dadd(floor(dsub(maxx, 0.5)), 1.0), 0.0), p.sx);
+  const double y0 = fmin(fmax(ceil(dsub(miny, 0.5)), 0.0), p.sy);
+  const double y1 = fmin(fmax(dadd(floor(dsub(maxy, 0.5)), 1.0), 0.0), p.sy);
+  const int ix0 = (int)x0, ix1 = (int)x1, iy0 = (int)y0, iy1 = (int)y1;
+  s.x0 = ix0;
+  s.y0 = iy0;
+  s.w = max(ix1 - ix0, 0);
+  s.h = max(iy1 - iy0, 0);
+  const bool live = fabs(s.den) > kDegenEps && s.w > 0 && s.h > 0;
+  if (!live) s.w = s.h = 0;
+  return (unsigned long long)s.w * (unsigned long long)s.h;
+}
+
+__global__ void __launch_bounds__(kSetupThreads) setup_kernel(Params p, const double* __restrict__ verts,
+                                                              long long nverts, const int64_t* __restrict__ tris,
+                                                              Work wk) {
+  const long long t = (long long)blockIdx.x * kSetupThreads + threadIdx.x;
+  Slot s0, s1;
+  unsigned long long c0 = 0, c1 = 0;
+  if (t < wk.ntris) {
+    long long id[3];
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      id[k] = tris[t * 3 + k];
+      ok &= id[k] >= 0 && id[k] < nverts;
+    }
+    if (ok) {
+      V3 c[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) c[k] = cam_xyz(p, verts + id[k] * 3);
+      const double zmin = fmin(fmin(c[0].z, c[1].z), c[2].z);
+      const double zmax = fmax(fmax(c[0].z, c[1].z), c[2].z);
+      if (zmax > p.nearz && zmin < p.farz) {  // froxel.py:307
+        if (zmin >= p.nearz) {
+          c0 = make_slot(p, c[0], c[1], c[2], s0);
+        } else {
+          // Sutherland-Hodgman against z - near >= 0 (froxel.py:203-219), fan (p0, pk, pk+1)
+          V3 poly[4];
+          int n = 0;
+          double d[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) d[k] = dsub(c[k].z, p.nearz);
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const int j = (i + 1) % 3;
+            if (d[i] >= 0) poly[n++] = c[i];
+            if ((d[i] >= 0) != (d[j] >= 0)) poly[n++] = lerp(c[i], c[j], ddiv(d[i], dsub(d[i], d[j])));
+          }
+          if (n >= 3) c0 = make_slot(p, poly[0], poly[1], poly[2], s0);
+          if (n >= 4) c1 = make_slot(p, poly[0], poly[2], poly[3], s1);
+        }
+      }
+    }
+  }
+  if (t < wk.ntris) {
+    if (c0) wk.slots[2 * t] = s0;
+    if (c1) wk.slots[2 * t + 1] = s1;
+  }
+  // block scan of (c0 + c1)
+  __shared__ unsigned long long warp_tot[kSetupThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long incl = c0 + c1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  unsigned long long base = 0, btot = 0;
+#pragma unroll
+  for (int i = 0; i < kSetupThreads / 32; ++i) {
+    if (i < wid) base += warp_tot[i];
+    btot += warp_tot[i];
+  }
+  const unsigned long long excl = base + incl - (c0 + c1);
+  if (t < wk.ntris) {
+    wk.lp[2 * t] = excl + c0;
+    wk.lp[2 * t + 1] = excl + c0 + c1;
+  }
+  if (threadIdx.x == 0) wk.bsum[blockIdx.x] = btot;
+}
+
+__global__ void __launch_bounds__(1024) scan_kernel(Work wk) {
+  __shared__ unsigned long long warp_tot[32];
+  __shared__ unsigned long long carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < wk.nb; b0 += 1024) {
+    const int b = b0 + threadIdx.x;
+    const unsigned long long v = b < wk.nb ? wk.bsum[b] : 0;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    unsigned long long base = carry, tot = 0;
+    for (int i = 0; i < 32; ++i) {
+      if (i < wid) base += warp_tot[i];
+      tot += warp_tot[i];
+    }
+    if (b < wk.nb) wk.bpre[b] = base + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *wk.total = carry;
+}
+
+// Slot holding flat sample g (g < total): largest block b with bpre[b] <= g,
+// then the first slot of that block whose inclusive local prefix exceeds
+// g - bpre[b].  Returns the slot and its exclusive global start.
+__device__ __forceinline__ long long find_slot(const Work& wk, unsigned long long g, unsigned long long& start) {
+  int lo = 0, hi = wk.nb - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(wk.bpre + mid) <= g) lo = mid;
+    else hi = mid - 1;
+  }
+  const unsigned long long bp = __ldg(wk.bpre + lo);
+  const unsigned long long local = g - bp;
+  long long a = (long long)lo * kSlotsPerBlock;
+  long long z = min(a + kSlotsPerBlock, 2 * wk.ntris) - 1;
+  const long long first = a;
+  while (a < z) {
+    const long long mid = (a + z) >> 1;
+    if (__ldg(wk.lp + mid) > local) z = mid;
+    else a = mid + 1;
+  }
+  start = bp + (a > first ? __ldg(wk.lp + a - 1) : 0ull);
+  return a;
+}
+
+__global__ void __launch_bounds__(kRasterThreads) raster_kernel(Params p, Work wk) {
+  const unsigned long long total = *wk.total;
+  long long cur = -1;
+  unsigned long long cs = 0, ce = 0;  // current slot's [start, end) in flat sample space
+  Slot s;
+  const unsigned int row = (unsigned int)(p.nx >> 3);
+  const double dnx = (double)p.nx, dny = (double)p.ny, dnz = (double)p.nz;
+  for (unsigned long long c0 = (unsigned long long)blockIdx.x * kChunk; c0 < total;
+       c0 += (unsigned long long)gridDim.x * kChunk) {
+#pragma unroll 1
+    for (int k = 0; k < kPerThread; ++k) {
+      const unsigned long long g = c0 + (unsigned long long)k * kRasterThreads + threadIdx.x;
+      if (g >= total) break;
+      if (g < cs || g >= ce) {
+        cur = find_slot(wk, g, cs);
+        s = wk.slots[cur];
+        ce = cs + (unsigned long long)s.w * (unsigned long long)s.h;
+      }
+      const unsigned int r = (unsigned int)(g - cs);
+      const unsigned int ry = r / (unsigned int)s.w;
+      const int px = s.x0 + (int)(r - ry * (unsigned int)s.w);
+      const int py = s.y0 + (int)ry;
+      // froxel.py:272-279
+      const double cx = dadd((double)px, 0.5), cy = dadd((double)py, 0.5);
+      const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
+      const double b1 = ddiv(dsub(dmul(dx, s.e2y), dmul(s.e2x, dy)), s.den);
+      const double b2 = ddiv(dsub(dmul(s.e1x, dy), dmul(dx, s.e1y)), s.den);
+      const double b0 = dsub(dsub(1.0, b1), b2);
+      if (!(b0 >= 0 && b1 >= 0 && b2 >= 0)) continue;
+      // froxel.py:340-344 perspective-correct depth
+      const double inv = dadd(dadd(s.iz0, dmul(b1, dsub(s.iz1, s.iz0))), dmul(b2, dsub(s.iz2, s.iz0)));
+      const double w1 = ddiv(dmul(b1, s.iz1), inv), w2 = ddiv(dmul(b2, s.iz2), inv);
+      const double w = dadd(dadd(s.wv0, dmul(w1, dsub(s.wv1, s.wv0))), dmul(w2, dsub(s.wv2, s.wv0)));
+      if (!(w >= 0 && w <= 1)) continue;
+      // quantize (froxel.py:28-42) of ((px+0.5)/sx, (py+0.5)/sy, w)
+      const int ix = min(max((int)floor(dmul(ddiv(cx, p.sx), dnx)), 0), p.nx - 1);
+      const int iy = min(max((int)floor(dmul(ddiv(cy, p.sy), dny)), 0), p.ny - 1);
+      const int iz = min(max((int)floor(dmul(w, dnz)), 0), p.nz - 1);
+      const unsigned long long byte =
+          (unsigned long long)(ix >> 3) + (unsigned long long)row * ((unsigned long long)iy + (unsigned long long)p.ny * iz);
+      atomicOr(wk.out_words + (byte >> 2), 1u << ((((unsigned int)byte & 3u) << 3) | ((unsigned int)ix & 7u)));
+    }
+  }
+}
+
+struct Layout {
+  size_t slots, lp, bsum, bpre, total, words, bytes;
+};
+
+inline size_t up256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+inline Layout layout(long long ntris, long long grid_bytes) {
+  Layout L;
+  const long long nslot = 2 * (ntris > 0 ? ntris : 1);
+  const long long nb = (nslot + kSlotsPerBlock - 1) / kSlotsPerBlock;
+  size_t o = 0;
+  L.total = o; o = up256(o + 8);  // first, so fpvs_froxelize_samples finds it without the sizes
+  L.slots = o; o = up256(o + (size_t)nslot * sizeof(Slot));
+  L.lp = o;    o = up256(o + (size_t)nslot * 8);
+  L.bsum = o;  o = up256(o + (size_t)nb * 8);
+  L.bpre = o;  o = up256(o + (size_t)nb * 8);
+  L.words = o; o = up256(o + (size_t)((grid_bytes + 3) & ~3LL));  // used only for unaligned outputs
+  L.bytes = o;
+  return L;
+}
+
+}  // namespace frox
+}  // namespace fpvs
+
+using namespace fpvs;
+using namespace fpvs::frox;
+
+extern "C" size_t fpvs_froxelize_workspace_size(long long ntris, int Nx, int Ny, int Nz) {
+  if (ntris < 0 || Nx <= 0 || Ny <= 0 || Nz <= 0) return 0;
+  return layout(ntris, (long long)Nx * Ny * Nz / 8).bytes;
+}
+
+extern "C" int fpvs_froxelize(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                              const fpvs_frustum* fr, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                              uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream) {
+  FPVS_CHECK_ARG(fr != nullptr && out_bits != nullptr, "froxelize: null frustum or output");
+  FPVS_CHECK_ARG(Nx > 0 && Ny > 0 && Nz > 0 && Nx % 8 == 0, "N_x must be divisible by 8, got %d", Nx);
+  FPVS_CHECK_ARG(supersample >= 1, "supersample factor must be >= 1");
+  FPVS_CHECK_ARG(depth_mode == FPVS_DEPTH_LINEAR || depth_mode == FPVS_DEPTH_LOG, "bad depth mode %d", depth_mode);
+  FPVS_CHECK_ARG(ntris >= 0 && nverts >= 0 && (ntris == 0 || (verts && tris)), "froxelize: bad scene arrays");
+  FPVS_CHECK_ARG(fr->near_z > 0 && fr->near_z < fr->far_z && fr->half_extent > 0, "need 0 < near < far");
+  const long long sx = (long long)supersample * Nx, sy = (long long)supersample * Ny;
+  FPVS_CHECK_ARG(sx * sy < (1LL << 32) && sx < (1LL << 30) && sy < (1LL << 30),
+                 "froxelize: supersampled screen %lld x %lld too large", sx, sy);
+  const long long grid_bytes = (long long)Nx * Ny * Nz / 8;
+  const Layout L = layout(ntris, grid_bytes);
+  FPVS_CHECK_ARG(workspace != nullptr && workspace_bytes >= L.bytes, "froxelize: workspace too small (%zu < %zu)",
+                 workspace_bytes, L.bytes);
+  cudaStream_t s = as_stream(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const bool direct = ((uintptr_t)out_bits & 3) == 0 && grid_bytes % 4 == 0;
+  unsigned int* words = direct ? reinterpret_cast<unsigned int*>(out_bits) : reinterpret_cast<unsigned int*>(ws + L.words);
+  if (cudaMemsetAsync(words, 0, (size_t)((grid_bytes + 3) & ~3LL), s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  Work wk;
+  wk.slots = reinterpret_cast<Slot*>(ws + L.slots);
+  wk.lp = reinterpret_cast<unsigned long long*>(ws + L.lp);
+  wk.bsum = reinterpret_cast<unsigned long long*>(ws + L.bsum);
+  wk.bpre = reinterpret_cast<unsigned long long*>(ws + L.bpre);
+  wk.total = reinterpret_cast<unsigned long long*>(ws + L.total);
+  wk.out_words = words;
+  wk.ntris = ntris;
+  wk.nb = (int)((2 * (ntris > 0 ? ntris : 1) + kSlotsPerBlock - 1) / kSlotsPerBlock);
+  Params p;
+  for (int i = 0; i < 3; ++i) p.o[i] = fr->origin[i];
+  for (int i = 0; i < 9; ++i) p.b[i] = fr->basis[i];
+  p.h = fr->half_extent;
+  p.nearz = fr->near_z;
+  p.farz = fr->far_z;
+  p.isx = (int)sx;
+  p.isy = (int)sy;
+  p.sx = (double)sx;
+  p.sy = (double)sy;
+  p.nx = Nx;
+  p.ny = Ny;
+  p.nz = Nz;
+  p.depth_log = depth_mode == FPVS_DEPTH_LOG;
+  if (ntris == 0) {
+    if (cudaMemsetAsync(wk.total, 0, 8, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  } else {
+    setup_kernel<<<wk.nb, kSetupThreads, 0, s>>>(p, verts, nverts, tris, wk);
+    FPVS_CHECK_LAUNCH("froxelize setup");
+    scan_kernel<<<1, 1024, 0, s>>>(wk);
+    FPVS_CHECK_LAUNCH("froxelize scan");
+    raster_kernel<<<kNumSMs * 8, kRasterThreads, 0, s>>>(p, wk);
+    FPVS_CHECK_LAUNCH("froxelize raster");
+  }
+  if (!direct && cudaMemcpyAsync(out_bits, words, (size_t)grid_bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    FPVS_CHECK_LAUNCH("froxelize copy");
+  return FPVS_OK;
+}
+
+extern "C" long long fpvs_froxelize_samples(const void* workspace, void* stream) {
+  if (workspace == nullptr) return -1;
+  unsigned long long v = 0;
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemcpyAsync(&v, workspace, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return -1;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+  return (long long)v;
+}

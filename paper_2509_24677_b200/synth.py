@@ -112,3 +112,89 @@ def config5_pair(rank: int, i: int):
     seed = 5000 + 64 * rank + i
     occ, _ = box_grid_density((128, 128, 128), 0.04, 1, 8, seed)
     return occ, first_hit_labels(occ)
+
+
+# --------------------------------------------------------------- triangle scenes
+def _uv_sphere(nu: int, nv: int):
+    """Closed lat-long sphere mesh of radius 1: (verts, tris)."""
+    th = np.linspace(0, np.pi, nv + 1)[1:-1]
+    ph = np.linspace(0, 2 * np.pi, nu, endpoint=False)
+    ring = np.stack([np.sin(th)[:, None] * np.cos(ph)[None], np.cos(th)[:, None] + 0 * ph[None],
+                     np.sin(th)[:, None] * np.sin(ph)[None]], axis=-1).reshape(-1, 3)
+    verts = np.concatenate([[[0, 1, 0]], ring, [[0, -1, 0]]])
+    tris = []
+    for j in range(nu):
+        tris.append([0, 1 + (j + 1) % nu, 1 + j])
+    for i in range(nv - 2):
+        a, b = 1 + i * nu, 1 + (i + 1) * nu
+        for j in range(nu):
+            k = (j + 1) % nu
+            tris += [[a + j, a + k, b + j], [a + k, b + k, b + j]]
+    last, pole = 1 + (nv - 2) * nu, len(verts) - 1
+    for j in range(nu):
+        tris.append([last + j, last + (j + 1) % nu, pole])
+    return verts.astype(np.float64), np.asarray(tris, dtype=np.int64)
+
+
+def _grid_quad(n: int):
+    """Unit quad [-1,1]^2 in the xz plane tessellated into 2 n^2 triangles."""
+    t = np.linspace(-1, 1, n + 1)
+    x, z = np.meshgrid(t, t, indexing="ij")
+    verts = np.stack([x.ravel(), 0 * x.ravel(), z.ravel()], axis=1)
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    a = (i * (n + 1) + j).ravel()
+    tris = np.concatenate([np.stack([a, a + 1, a + n + 2], 1), np.stack([a, a + n + 2, a + n + 1], 1)])
+    return verts, tris.astype(np.int64)
+
+
+def _rot(rng):
+    q = rng.normal(size=4)
+    q /= np.linalg.norm(q)
+    w, x, y, z = q
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                     [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                     [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+
+
+def froxel_scene(seed: int = 0, n_objects: int = 12, detail: int = 12, extent: float = 12.0):
+    """Seeded triangle scene of the reference generator's kind (scenegen.py:312-372):
+    a floor and a back wall spanning the view plus ``n_objects`` rotated,
+    anisotropically scaled closed meshes around a viewcell at the origin.
+    Returns (vertices float64 (V,3), triangles int64 (T,3), frustum args) where
+    the frustum args are (origin, forward, up, right, fov_deg, near, far) of a
+    viewcell frustum (core.py:361-373) looking along a random yaw."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    vs, ts, n = [], [], 0
+
+    def add(v, t):
+        nonlocal n
+        vs.append(v)
+        ts.append(t + n)
+        n += len(v)
+
+    sv, st = _uv_sphere(detail, max(3, detail // 2))
+    cv = np.array([[x, y, z] for x in (-1, 1) for y in (-1, 1) for z in (-1, 1)], dtype=np.float64)
+    ct = np.array([[0, 1, 3], [0, 3, 2], [4, 6, 7], [4, 7, 5], [0, 4, 5], [0, 5, 1],
+                   [2, 3, 7], [2, 7, 6], [0, 2, 6], [0, 6, 4], [1, 5, 7], [1, 7, 3]], dtype=np.int64)
+    for _ in range(n_objects):
+        v, t = (sv, st) if rng.random() < 0.5 else (cv, ct)
+        scale = np.exp(rng.uniform(np.log(0.5), np.log(4.0), size=3))
+        pos = np.array([rng.uniform(-extent, extent), rng.uniform(0.2, 4.0), rng.uniform(-extent, extent)])
+        add((v * scale) @ _rot(rng).T + pos, t)
+    gq, gt = _grid_quad(max(1, detail // 2))
+    span = 2.5 * extent
+    add(gq * span, gt)                                                  # floor (y = 0)
+    yaw = rng.uniform(0, 2 * np.pi)
+    fwd = np.array([np.sin(yaw), 0.0, np.cos(yaw)])
+    right = np.array([fwd[2], 0.0, -fwd[0]])
+    wall = gq[:, [0, 2, 1]] * span                                      # xy plane
+    wall = wall[:, 0:1] * right + wall[:, 1:2] * np.array([0.0, 1.0, 0.0]) + 1.5 * extent * fwd
+    add(wall, gt)
+    verts, tris = np.concatenate(vs), np.concatenate(ts)
+    height = rng.uniform(0.8, 2.2)
+    radius, fov, beta, near, far = 0.3, 60.0, 15.0, 0.3, 20.0
+    h = np.tan(np.radians(fov) / 2)
+    disp = radius / h
+    origin = np.array([0.0, height, 0.0]) - disp * fwd
+    up = np.array([0.0, 1.0, 0.0])
+    return verts, tris, (origin, fwd, up, -right, fov + 2 * beta, disp, disp + far)

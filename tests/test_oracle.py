@@ -257,3 +257,44 @@ def test_oracle_against_live_reference(rng):
     coords = np.argwhere(mask).astype(np.int64)
     z = osp.gather_conv(x[tuple(coords.T)], osp.kmap_subm(coords, (5, 5, 5)), layer.w, layer.b)
     np.testing.assert_allclose(np.maximum(z, 0), y[tuple(coords.T)], atol=1e-12)
+
+
+# ---------------------------------------------------------------- froxelize
+
+
+def test_froxelize_oracle_matches_reference_golden(golden):
+    """oracle/froxelize.py vs the reference's froxelize output (froxel.py:387-394)."""
+    from oracle import froxelize as ofz
+    g = golden("froxelize.npz")
+    for i in range(int(g["ncases"])):
+        h, n, f = g[f"c{i}_lens"]
+        bits = ofz.froxelize(g[f"c{i}_verts"], g[f"c{i}_tris"], g[f"c{i}_origin"], g[f"c{i}_basis"], h, n, f,
+                             g[f"c{i}_dims"], int(g[f"c{i}_ss"]),
+                             "linear" if int(g[f"c{i}_depth"]) == 0 else "log")
+        assert np.array_equal(bits, g[f"c{i}_bits"]), str(g[f"c{i}_name"])
+
+
+def test_froxelize_full_span_quad_is_one_layer(golden):
+    """test_froxel.py:148-159: a full-cross-section quad at w = 0.5 fills layer 8 of 16 only."""
+    g = golden("froxelize.npz")
+    i = next(i for i in range(int(g["ncases"])) if str(g[f"c{i}_name"]) == "full_span_quad")
+    dense = FroxelGrid((16, 16, 16), bits=g[f"c{i}_bits"]).to_dense()
+    assert dense[:, :, 8].all()
+    dense[:, :, 8] = False
+    assert not dense.any()
+
+
+@pytest.mark.skipif(ref is None, reason="reference not mounted (GPU box)")
+def test_froxelize_oracle_against_live_reference():
+    import sys
+    from oracle import froxelize as ofz
+    sys.path.insert(0, refbridge.REF_SRC)
+    from froxelpvs import core, froxel, scenegen
+    for seed in (11, 12):
+        scene, cell = scenegen.generate_scene(scenegen.SceneGenConfig(seed=seed, count_range=(3, 6)))
+        fr = core.build_viewcell_frustum(cell)
+        for ss in (1, 2):
+            want = froxel.froxelize(scene, fr, (32, 16, 24), froxel.FroxelizeConfig(supersample=ss)).bits
+            got = ofz.froxelize(scene.vertices, scene.triangles, fr._o, fr._basis, fr.half_extent, fr.near,
+                                fr.far, (32, 16, 24), ss)
+            assert np.array_equal(got, want)
