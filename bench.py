@@ -27,6 +27,9 @@ halo tables), sparse interleave, 14 convs, head.
   launch from the committed ncu --set full capture (profiles/).
 * ``cpu_baseline``: the numpy sparse restatement (oracle/, fp64) of the same
   frame on this host's cores (rank 0, N=1).
+* ``froxelize`` (extra, N=1): SURVEY §8(f) #1, the device froxelizer on two
+  seeded triangle scenes into the 256^3 grid, device us per call and the
+  numpy oracle's CPU time on the same scene; a side line, not the metric.
 * ``train_config5`` (extra, rank 0): BASELINE config 5's training step on one
   GPU (8 x 128^3 grids, bf16 + fp32 master weights, AdamW, tcgen05 backward),
   10 steps timed with CUDA events; a reported side line, not the metric.
@@ -218,6 +221,53 @@ def train_config5(steps: int = 10):
             "loss": float(step.loss), "backward": "tcgen05 dgrad + wgrad", "steps": steps}
 
 
+def froxelize_side(reps: int = 20):
+    """fpvs_froxelize of a seeded triangle scene into the 256^3
+    grid (supersample 4, linear depth) — device time per call from a CUDA graph
+    of ``reps`` calls; the oracle port (oracle/froxelize.py, numpy) on the same
+    scene as its CPU baseline.  A reported side line, not the metric."""
+    import torch
+    from paper_2509_24677_b200 import synth
+    from paper_2509_24677_b200.froxelize import FroxelizeConfig, Froxelizer, Frustum
+    from oracle import froxelize as ofz
+    dims, cfg = (256, 256, 256), FroxelizeConfig(supersample=4)
+    out = {}
+    for name, args in (("scene0", (0, 12, 12)), ("scene1", (1, 40, 24))):
+        v, t, fa = synth.froxel_scene(*args)
+        fr = Frustum.from_vectors(*fa)
+        fz = Froxelizer(v, t)
+        bits = torch.empty(256 ** 3 // 8, dtype=torch.uint8, device="cuda")
+        fz.run(fr, dims, cfg, out=bits)
+        torch.cuda.synchronize()
+        samples = fz.samples()
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(g, stream=st):
+                for _ in range(reps):
+                    fz.run(fr, dims, cfg, out=bits)
+        torch.cuda.current_stream().wait_stream(st)
+        best = float("inf")
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / reps)
+        t0 = time.perf_counter()
+        ref = ofz.froxelize(v, t, fr._o, fr._basis, fr.half_extent, fr.near, fr.far, dims, 4)
+        cpu_s = time.perf_counter() - t0
+        got = bits.cpu().numpy()
+        out[name] = {"triangles": int(len(t)), "samples": int(samples), "device_us": round(best * 1e3, 2),
+                     "gsamples_per_s": round(samples / (best * 1e-3) / 1e9, 2),
+                     "oracle_cpu_s": round(cpu_s, 4), "speedup_vs_oracle": round(cpu_s / (best * 1e-3), 1),
+                     "bit_exact_vs_oracle": bool(np.array_equal(got, ref))}
+    return {"workload": "synth.froxel_scene -> 256^3 geometry grid, supersample 4, linear depth, viewcell frustum",
+            "kernels": "setup + scan + raster (3 launches + memset)", **out}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -341,8 +391,11 @@ def run_ours(args):
 
     cpu = None
     train = None
+    frox = None
     if not args.no_train:
         train = train_config5()
+    if ws == 1 and not args.no_froxelize:
+        frox = froxelize_side()
     if ws == 1 and not args.no_cpu_baseline:
         t_cpu = cpu_frame_time(occ)
         cpu = {"value": 1.0 / t_cpu, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
@@ -378,6 +431,8 @@ def run_ours(args):
         line["cpu_baseline"] = cpu
     if train is not None:
         line["train_config5"] = train
+    if frox is not None:
+        line["froxelize"] = frox
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -392,6 +447,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the config-5 training-step line")
+    ap.add_argument("--no-froxelize", action="store_true", help="skip the froxelization side line")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

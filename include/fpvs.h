@@ -374,7 +374,7 @@ enum { FPVS_DEPTH_LINEAR = 0, FPVS_DEPTH_LOG = 1 };
  * overwritten.  Triangle indices outside [0, nverts) are skipped.  Results
  * equal the reference bit-for-bit in linear depth mode (the arithmetic is
  * the reference's float64 expression sequence, unfused). */
-size_t fpvs_froxelize_workspace_size(long long ntris, int Nx, int Ny, int Nz);
+size_t fpvs_froxelize_workspace_size(long long ntris, int Nx, int Ny, int Nz, int supersample);
 int fpvs_froxelize(const double* verts, long long nverts, const int64_t* tris, long long ntris,
                    const fpvs_frustum* frustum, int Nx, int Ny, int Nz, int supersample, int depth_mode,
                    uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream);

@@ -73,7 +73,7 @@ SIGNATURES = {
     "fpvs_bits_confusion_workspace_size": (_z, [_i]),
     "fpvs_bits_confusion": (_i, [_p, _p, _i, C.c_longlong, _p, _p, _z, _p]),
     "fpvs_first_hit_labels": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p]),
-    "fpvs_froxelize_workspace_size": (_z, [C.c_longlong, _i, _i, _i]),
+    "fpvs_froxelize_workspace_size": (_z, [C.c_longlong, _i, _i, _i, _i]),
     "fpvs_froxelize": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _i, _i, _i, _i, _i, _p, _p, _z, _p]),
     "fpvs_froxelize_samples": (C.c_longlong, [_p, _p]),
 }

@@ -46,10 +46,13 @@ struct __align__(16) Slot {
   double v0x, v0y, e1x, e1y, e2x, e2y, den;
   double iz0, iz1, iz2;  // 1/z per vertex
   double wv0, wv1, wv2;  // per-vertex depth coordinate
+  double rden;           // 1/den, for the filtered fast path only
+  double wtol;           // relative depth tolerance of the fast path (scales with zmax/zmin)
   int x0, y0, w, h;
-  int pad[2];
+  unsigned int wmagic;  // ceil(2^32 / w): row = umulhi(r, wmagic) +-1
+  int pad;
 };
-static_assert(sizeof(Slot) == 128, "slot record is one 128-byte line");
+static_assert(sizeof(Slot) == 144, "slot record");
 
 struct Params {
   double o[3], b[9];
@@ -67,6 +70,8 @@ struct Work {
   unsigned long long* bpre;  // [nb] exclusive block offsets
   unsigned long long* total;
   unsigned int* out_words;
+  int* tabx;  // froxel column of supersampled pixel column px (quantize of (px+0.5)/sx)
+  int* taby;
   long long ntris;
   int nb;
 };
@@ -128,6 +133,11 @@ __device__ unsigned long long make_slot(const Params& p, const V3& a, const V3& 
   s.wv0 = wv[0];
   s.wv1 = wv[1];
   s.wv2 = wv[2];
+  s.rden = 1.0 / s.den;
+  {
+    const double izmax = fmax(fmax(iz[0], iz[1]), iz[2]), izmin = fmin(fmin(iz[0], iz[1]), iz[2]);
+    s.wtol = 1e-12 * (izmax / izmin);
+  }
   const double minx = fmin(fmin(u[0], u[1]), u[2]), maxx = fmax(fmax(u[0], u[1]), u[2]);
   const double miny = fmin(fmin(vv[0], vv[1]), vv[2]), maxy = fmax(fmax(vv[0], vv[1]), vv[2]);
   const double x0 = fmin(fmax(ceil(dsub(minx, 0.5)), 0.0), p.sx);
@@ -141,6 +151,9 @@ __device__ unsigned long long make_slot(const Params& p, const V3& a, const V3& 
   s.h = max(iy1 - iy0, 0);
   const bool live = fabs(s.den) > kDegenEps && s.w > 0 && s.h > 0;
   if (!live) s.w = s.h = 0;
+  s.wmagic = s.w > 1 ? (unsigned int)((0x100000000ull + (unsigned long long)s.w - 1) / (unsigned long long)s.w)
+                     : 0xffffffffu;
+  s.pad = 0;
   return (unsigned long long)s.w * (unsigned long long)s.h;
 }
 
@@ -215,7 +228,12 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(Params p, const do
   if (threadIdx.x == 0) wk.bsum[blockIdx.x] = btot;
 }
 
-__global__ void __launch_bounds__(1024) scan_kernel(Work wk) {
+__global__ void __launch_bounds__(1024) scan_kernel(Params p, Work wk) {
+  // pixel column/row -> froxel index, exactly quantize((px + 0.5) / sx) (froxel.py:28-42, 345-346)
+  for (int i = threadIdx.x; i < p.isx; i += 1024)
+    wk.tabx[i] = min(max((int)floor(dmul(ddiv(dadd((double)i, 0.5), p.sx), (double)p.nx)), 0), p.nx - 1);
+  for (int i = threadIdx.x; i < p.isy; i += 1024)
+    wk.taby[i] = min(max((int)floor(dmul(ddiv(dadd((double)i, 0.5), p.sy), (double)p.ny)), 0), p.ny - 1);
   __shared__ unsigned long long warp_tot[32];
   __shared__ unsigned long long carry;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -269,58 +287,172 @@ __device__ __forceinline__ long long find_slot(const Work& wk, unsigned long lon
   return a;
 }
 
-__global__ void __launch_bounds__(kRasterThreads) raster_kernel(Params p, Work wk) {
+// The reference's own expression sequence for one sample (froxel.py:272-279,
+// 340-344; quantize 28-42).  Returns the depth layer, or -1 when the sample
+// is outside the triangle or the depth range.
+__device__ __forceinline__ int sample_exact(const Slot& s, double cx, double cy, int nz) {
+  const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
+  const double b1 = ddiv(dsub(dmul(dx, s.e2y), dmul(s.e2x, dy)), s.den);
+  const double b2 = ddiv(dsub(dmul(s.e1x, dy), dmul(dx, s.e1y)), s.den);
+  const double b0 = dsub(dsub(1.0, b1), b2);
+  if (!(b0 >= 0 && b1 >= 0 && b2 >= 0)) return -1;
+  const double inv = dadd(dadd(s.iz0, dmul(b1, dsub(s.iz1, s.iz0))), dmul(b2, dsub(s.iz2, s.iz0)));
+  const double w1 = ddiv(dmul(b1, s.iz1), inv), w2 = ddiv(dmul(b2, s.iz2), inv);
+  const double w = dadd(dadd(s.wv0, dmul(w1, dsub(s.wv1, s.wv0))), dmul(w2, dsub(s.wv2, s.wv0)));
+  if (!(w >= 0 && w <= 1)) return -1;
+  return min(max((int)floor(dmul(w, (double)nz)), 0), nz - 1);
+}
+
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = __fma_rn(-x, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
+// Filtered evaluation: decides with no division whenever the decision is
+// provably the one sample_exact makes, else defers to it.  Returns the depth
+// layer, -1 for a dropped sample.
+//  * b1 >= 0 / b2 >= 0: the sign of the rounded numerator (computed exactly
+//    as the reference does) is the sign of the rounded quotient, barring
+//    underflow (|n| tiny -> exact path);
+//  * b0 and the depth w from q = n * (1/den) and an approximate 1/inv: their
+//    error is ~1e-15 relative (w: times zmax/zmin, folded into s.wtol), so a
+//    decision more than 1e-13 / wtol away from its boundary (b0 = 0, w = 0,
+//    w = 1, w * nz integral) cannot flip; closer samples take the exact path.
+__device__ __forceinline__ int sample_fast(const Slot& s, double cx, double cy, int nz) {
+  const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
+  const double n1 = dsub(dmul(dx, s.e2y), dmul(s.e2x, dy));
+  const double n2 = dsub(dmul(s.e1x, dy), dmul(dx, s.e1y));
+  const bool dneg = s.den < 0;
+  const double a1 = fabs(n1), a2 = fabs(n2);
+  constexpr double kTiny = 1e-250;
+  if ((a1 != 0 && a1 < kTiny) || (a2 != 0 && a2 < kTiny)) return sample_exact(s, cx, cy, nz);
+  if ((n1 != 0 && ((n1 < 0) != dneg)) || (n2 != 0 && ((n2 < 0) != dneg))) return -1;
+  const double q1 = n1 * s.rden, q2 = n2 * s.rden;  // >= 0 here
+  const double a0 = (1.0 - q1) - q2;
+  const double m0 = 1e-13 * (1.0 + q1 + q2);
+  if (a0 < -m0) return -1;
+  if (a0 <= m0) return sample_exact(s, cx, cy, nz);
+  const double inv = __fma_rn(q2, s.iz2 - s.iz0, __fma_rn(q1, s.iz1 - s.iz0, s.iz0));
+  const double r = rcp_nr(inv);
+  const double w1 = q1 * s.iz1 * r, w2 = q2 * s.iz2 * r;
+  const double d1 = s.wv1 - s.wv0, d2 = s.wv2 - s.wv0;
+  const double w = __fma_rn(w2, d2, __fma_rn(w1, d1, s.wv0));
+  const double mw = s.wtol * (1.0 + fabs(s.wv0) + w1 * fabs(d1) + w2 * fabs(d2));
+  if (w < -mw || w > 1.0 + mw) return -1;
+  const double t = w * (double)nz, f = floor(t);
+  const double mt = mw * (double)nz + 1e-15 * t;
+  if (w <= mw || w >= 1.0 - mw || t - f <= mt || f + 1.0 - t <= mt) return sample_exact(s, cx, cy, nz);
+  return min(max((int)f, 0), nz - 1);
+}
+
+// (double)px + 0.5 without the int->fp64 converter: 2^52 + px from the bit
+// pattern, minus (2^52 - 0.5); both steps are exact for 0 <= px < 2^31.
+__device__ __forceinline__ double centre(int px) {
+  return __dsub_rn(__hiloint2double(0x43300000, px), 4503599627370495.5);
+}
+
+// Global inclusive end of slot sl's sample range.
+__device__ __forceinline__ unsigned long long slot_end(const Work& wk, long long sl) {
+  return __ldg(wk.bpre + sl / kSlotsPerBlock) + __ldg(wk.lp + sl);
+}
+
+// Each warp rasterizes 32 * kPerThread consecutive samples, 32 at a time
+// (lane = sample), so the lanes of one step share a slot or walk forward to
+// the next few; only the warp's first sample needs the binary search.
+template <bool kFilter>
+__global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(Params p, Work wk) {
+  constexpr int kWarpSpan = 32 * kPerThread;
   const unsigned long long total = *wk.total;
-  long long cur = -1;
-  unsigned long long cs = 0, ce = 0;  // current slot's [start, end) in flat sample space
-  Slot s;
   const unsigned int row = (unsigned int)(p.nx >> 3);
-  const double dnx = (double)p.nx, dny = (double)p.ny, dnz = (double)p.nz;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long have = -1;  // slot whose constants are in s
+  Slot s;
   for (unsigned long long c0 = (unsigned long long)blockIdx.x * kChunk; c0 < total;
        c0 += (unsigned long long)gridDim.x * kChunk) {
+    const unsigned long long wbase = c0 + (unsigned long long)warp * kWarpSpan;
+    if (wbase >= total) break;  // warp-uniform
+    unsigned long long cs = 0;
+    long long cur = 0;
+    if (lane == 0) cur = find_slot(wk, wbase, cs);
+    cur = __shfl_sync(0xffffffffu, cur, 0);
+    cs = __shfl_sync(0xffffffffu, cs, 0);
+    unsigned long long ce = slot_end(wk, cur);
 #pragma unroll 1
     for (int k = 0; k < kPerThread; ++k) {
-      const unsigned long long g = c0 + (unsigned long long)k * kRasterThreads + threadIdx.x;
-      if (g >= total) break;
-      if (g < cs || g >= ce) {
-        cur = find_slot(wk, g, cs);
-        s = wk.slots[cur];
-        ce = cs + (unsigned long long)s.w * (unsigned long long)s.h;
+      const unsigned long long g = wbase + (unsigned long long)(k * 32 + lane);
+      bool valid = g < total;
+      unsigned int word = 0, bit = 0;
+      long long mine = cur;
+      if (valid) {
+        unsigned long long ms = cs, me = ce;
+        // walk a few slots forward (odd slots of unclipped triangles are
+        // empty), then fall back to the search (long zero-count runs)
+        int steps = 0;
+        while (g >= me && steps < 4) {
+          ms = me;
+          me = slot_end(wk, ++mine);
+          ++steps;
+        }
+        if (g >= me) {
+          mine = find_slot(wk, g, ms);
+          me = slot_end(wk, mine);
+        }
+        if (mine != have) {
+          s = wk.slots[mine];
+          have = mine;
+        }
+        const unsigned int r = (unsigned int)(g - ms);
+        unsigned int ry = __umulhi(r, s.wmagic);
+        const int rem = (int)(r - ry * (unsigned int)s.w);
+        if (rem < 0) --ry;
+        else if (rem >= s.w) ++ry;
+        const int px = s.x0 + (int)(r - ry * (unsigned int)s.w);
+        const int py = s.y0 + (int)ry;
+        const double cx = centre(px), cy = centre(py);
+        const int iz = kFilter ? sample_fast(s, cx, cy, p.nz) : sample_exact(s, cx, cy, p.nz);
+        valid = iz >= 0;
+        if (valid) {
+          const int ix = __ldg(wk.tabx + px), iy = __ldg(wk.taby + py);
+          const unsigned long long byte = (unsigned long long)(ix >> 3) +
+                                          (unsigned long long)row * ((unsigned long long)iy + (unsigned long long)p.ny * iz);
+          word = (unsigned int)(byte >> 2);
+          bit = 1u << ((((unsigned int)byte & 3u) << 3) | ((unsigned int)ix & 7u));
+        }
       }
-      const unsigned int r = (unsigned int)(g - cs);
-      const unsigned int ry = r / (unsigned int)s.w;
-      const int px = s.x0 + (int)(r - ry * (unsigned int)s.w);
-      const int py = s.y0 + (int)ry;
-      // froxel.py:272-279
-      const double cx = dadd((double)px, 0.5), cy = dadd((double)py, 0.5);
-      const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
-      const double b1 = ddiv(dsub(dmul(dx, s.e2y), dmul(s.e2x, dy)), s.den);
-      const double b2 = ddiv(dsub(dmul(s.e1x, dy), dmul(dx, s.e1y)), s.den);
-      const double b0 = dsub(dsub(1.0, b1), b2);
-      if (!(b0 >= 0 && b1 >= 0 && b2 >= 0)) continue;
-      // froxel.py:340-344 perspective-correct depth
-      const double inv = dadd(dadd(s.iz0, dmul(b1, dsub(s.iz1, s.iz0))), dmul(b2, dsub(s.iz2, s.iz0)));
-      const double w1 = ddiv(dmul(b1, s.iz1), inv), w2 = ddiv(dmul(b2, s.iz2), inv);
-      const double w = dadd(dadd(s.wv0, dmul(w1, dsub(s.wv1, s.wv0))), dmul(w2, dsub(s.wv2, s.wv0)));
-      if (!(w >= 0 && w <= 1)) continue;
-      // quantize (froxel.py:28-42) of ((px+0.5)/sx, (py+0.5)/sy, w)
-      const int ix = min(max((int)floor(dmul(ddiv(cx, p.sx), dnx)), 0), p.nx - 1);
-      const int iy = min(max((int)floor(dmul(ddiv(cy, p.sy), dny)), 0), p.ny - 1);
-      const int iz = min(max((int)floor(dmul(w, dnz)), 0), p.nz - 1);
-      const unsigned long long byte =
-          (unsigned long long)(ix >> 3) + (unsigned long long)row * ((unsigned long long)iy + (unsigned long long)p.ny * iz);
-      atomicOr(wk.out_words + (byte >> 2), 1u << ((((unsigned int)byte & 3u) << 3) | ((unsigned int)ix & 7u)));
+      // the warp's next step starts from the last lane's slot
+      const long long nxt = __shfl_sync(0xffffffffu, mine, 31);
+      if (nxt != cur) {
+        cur = nxt;
+        cs = (cur % kSlotsPerBlock ? slot_end(wk, cur - 1) : __ldg(wk.bpre + cur / kSlotsPerBlock));
+        ce = slot_end(wk, cur);
+      }
+      // warp-combined OR: one atomic when every covered lane hits the same word
+      const unsigned int vm = __ballot_sync(0xffffffffu, valid);
+      if (vm) {
+        const int leader = __ffs(vm) - 1;
+        const unsigned int w0 = __shfl_sync(0xffffffffu, word, leader);
+        if (__all_sync(0xffffffffu, !valid || word == w0)) {
+          const unsigned int bits = __reduce_or_sync(0xffffffffu, valid ? bit : 0u);
+          if (lane == leader) atomicOr(wk.out_words + w0, bits);
+        } else if (valid) {
+          atomicOr(wk.out_words + word, bit);
+        }
+      }
     }
   }
 }
 
 struct Layout {
-  size_t slots, lp, bsum, bpre, total, words, bytes;
+  size_t slots, lp, bsum, bpre, total, tabx, taby, words, bytes;
 };
 
 inline size_t up256(size_t v) { return (v + 255) & ~(size_t)255; }
 
-inline Layout layout(long long ntris, long long grid_bytes) {
+inline Layout layout(long long ntris, long long grid_bytes, long long sx, long long sy) {
   Layout L;
   const long long nslot = 2 * (ntris > 0 ? ntris : 1);
   const long long nb = (nslot + kSlotsPerBlock - 1) / kSlotsPerBlock;
@@ -330,9 +462,20 @@ inline Layout layout(long long ntris, long long grid_bytes) {
   L.lp = o;    o = up256(o + (size_t)nslot * 8);
   L.bsum = o;  o = up256(o + (size_t)nb * 8);
   L.bpre = o;  o = up256(o + (size_t)nb * 8);
+  L.tabx = o;  o = up256(o + (size_t)sx * 4);
+  L.taby = o;  o = up256(o + (size_t)sy * 4);
   L.words = o; o = up256(o + (size_t)((grid_bytes + 3) & ~3LL));  // used only for unaligned outputs
   L.bytes = o;
   return L;
+}
+
+// FPVS_FROX_EXACT=1 evaluates every sample with the reference sequence (A/B check)
+inline bool filtered() {
+  static const bool f = [] {
+    const char* e = getenv("FPVS_FROX_EXACT");
+    return !(e && e[0] == '1');
+  }();
+  return f;
 }
 
 }  // namespace frox
@@ -341,9 +484,9 @@ inline Layout layout(long long ntris, long long grid_bytes) {
 using namespace fpvs;
 using namespace fpvs::frox;
 
-extern "C" size_t fpvs_froxelize_workspace_size(long long ntris, int Nx, int Ny, int Nz) {
-  if (ntris < 0 || Nx <= 0 || Ny <= 0 || Nz <= 0) return 0;
-  return layout(ntris, (long long)Nx * Ny * Nz / 8).bytes;
+extern "C" size_t fpvs_froxelize_workspace_size(long long ntris, int Nx, int Ny, int Nz, int supersample) {
+  if (ntris < 0 || Nx <= 0 || Ny <= 0 || Nz <= 0 || supersample < 1) return 0;
+  return layout(ntris, (long long)Nx * Ny * Nz / 8, (long long)supersample * Nx, (long long)supersample * Ny).bytes;
 }
 
 extern "C" int fpvs_froxelize(const double* verts, long long nverts, const int64_t* tris, long long ntris,
@@ -359,7 +502,7 @@ extern "C" int fpvs_froxelize(const double* verts, long long nverts, const int64
   FPVS_CHECK_ARG(sx * sy < (1LL << 32) && sx < (1LL << 30) && sy < (1LL << 30),
                  "froxelize: supersampled screen %lld x %lld too large", sx, sy);
   const long long grid_bytes = (long long)Nx * Ny * Nz / 8;
-  const Layout L = layout(ntris, grid_bytes);
+  const Layout L = layout(ntris, grid_bytes, sx, sy);
   FPVS_CHECK_ARG(workspace != nullptr && workspace_bytes >= L.bytes, "froxelize: workspace too small (%zu < %zu)",
                  workspace_bytes, L.bytes);
   cudaStream_t s = as_stream(stream);
@@ -374,6 +517,8 @@ extern "C" int fpvs_froxelize(const double* verts, long long nverts, const int64
   wk.bpre = reinterpret_cast<unsigned long long*>(ws + L.bpre);
   wk.total = reinterpret_cast<unsigned long long*>(ws + L.total);
   wk.out_words = words;
+  wk.tabx = reinterpret_cast<int*>(ws + L.tabx);
+  wk.taby = reinterpret_cast<int*>(ws + L.taby);
   wk.ntris = ntris;
   wk.nb = (int)((2 * (ntris > 0 ? ntris : 1) + kSlotsPerBlock - 1) / kSlotsPerBlock);
   Params p;
@@ -395,9 +540,21 @@ extern "C" int fpvs_froxelize(const double* verts, long long nverts, const int64
   } else {
     setup_kernel<<<wk.nb, kSetupThreads, 0, s>>>(p, verts, nverts, tris, wk);
     FPVS_CHECK_LAUNCH("froxelize setup");
-    scan_kernel<<<1, 1024, 0, s>>>(wk);
+    scan_kernel<<<1, 1024, 0, s>>>(p, wk);
     FPVS_CHECK_LAUNCH("froxelize scan");
-    raster_kernel<<<kNumSMs * 8, kRasterThreads, 0, s>>>(p, wk);
+    static const int per_sm[2] = {[] {
+      int n = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, raster_kernel<false>, kRasterThreads, 0);
+      return n > 0 ? n : 1;
+    }(), [] {
+      int n = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, raster_kernel<true>, kRasterThreads, 0);
+      return n > 0 ? n : 1;
+    }()};
+    if (filtered())
+      raster_kernel<true><<<kNumSMs * per_sm[1], kRasterThreads, 0, s>>>(p, wk);
+    else
+      raster_kernel<false><<<kNumSMs * per_sm[0], kRasterThreads, 0, s>>>(p, wk);
     FPVS_CHECK_LAUNCH("froxelize raster");
   }
   if (!direct && cudaMemcpyAsync(out_bits, words, (size_t)grid_bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)

@@ -127,10 +127,10 @@ class Froxelizer:
     def ntris(self) -> int:
         return int(self.tris.shape[0])
 
-    def workspace(self, dims):
+    def workspace(self, dims, supersample: int):
         torch = _torch()
         nx, ny, nz = dims
-        need = _lib.size("fpvs_froxelize_workspace_size", self.ntris, nx, ny, nz)
+        need = _lib.size("fpvs_froxelize_workspace_size", self.ntris, nx, ny, nz, int(supersample))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         return self._ws
@@ -148,7 +148,7 @@ class Froxelizer:
             out = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         elif out.numel() != nbytes or out.dtype != torch.uint8:
             raise ValueError("output buffer does not match dims")
-        ws = self.workspace((nx, ny, nz))
+        ws = self.workspace((nx, ny, nz), cfg.supersample)
         c = fr.c_struct()
         import ctypes
         _lib.call("fpvs_froxelize", _lib.ptr(self.verts), self.verts.shape[0], _lib.ptr(self.tris), self.ntris,

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--ss", type=int, default=4)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--cpu", action="store_true", help="also time the oracle port")
+    ap.add_argument("--scenes", default="0,1,2,3")
     a = ap.parse_args()
     import torch
     from paper_2509_24677_b200 import synth
@@ -28,7 +29,8 @@ def main():
     from oracle import froxelize as ofz
     dims = (a.dims,) * 3
     cfg = FroxelizeConfig(supersample=a.ss)
-    for seed, nobj, detail in [(0, 12, 12), (1, 40, 24), (2, 200, 48), (3, 2000, 24)]:
+    scenes = [(0, 12, 12), (1, 40, 24), (2, 200, 48), (3, 2000, 24)]
+    for seed, nobj, detail in [scenes[int(i)] for i in a.scenes.split(",")]:
         v, t, fa = synth.froxel_scene(seed, nobj, detail)
         fr = Frustum.from_vectors(*fa)
         fz = Froxelizer(v, t)
