@@ -378,8 +378,28 @@ size_t fpvs_froxelize_workspace_size(long long ntris, int Nx, int Ny, int Nz, in
 int fpvs_froxelize(const double* verts, long long nverts, const int64_t* tris, long long ntris,
                    const fpvs_frustum* frustum, int Nx, int Ny, int Nz, int supersample, int depth_mode,
                    uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream);
+/* Ground-truth PVS by dense viewpoint sampling; replaces oracle.py:141-172
+ * compute_gt_pvs() (render_depth oracle.py:107-138 per camera, then
+ * reprojection core.py:380-452 into the viewcell frustum).  cams: DEVICE
+ * array of ncams cameras in fpvs_frustum form (origin = camera position,
+ * basis rows right/up/forward, half_extent, near, far); frustum: HOST
+ * pointer (build_viewcell_frustum).  res_w x res_h is the depth-buffer
+ * resolution (OracleConfig.resolution_for: default 4 Nx x 4 Ny).  prim_ids
+ * (int64 per triangle) is only needed when some id is negative: exact depth
+ * ties then resolve to the smallest id and pixels won by a negative id are
+ * not fragments; NULL means ids 0..T-1.  gt_bits is cleared unless
+ * accumulate != 0 (several camera batches into one grid); geometry_bits
+ * (nullable) gets every GT bit OR-ed in too.  Grids must be 4-byte aligned
+ * with Nx*Ny*Nz/8 % 4 == 0.  Linear depth is bit-exact with the reference. */
+size_t fpvs_gt_pvs_workspace_size(long long ntris, int ncams, int res_w, int res_h, int with_prim_ids);
+int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                const int64_t* prim_ids, const fpvs_frustum* cams, int ncams, int res_w, int res_h,
+                const fpvs_frustum* frustum, int Nx, int Ny, int Nz, int depth_mode, int accumulate,
+                uint8_t* gt_bits, uint8_t* geometry_bits, void* workspace, size_t workspace_bytes,
+                void* stream);
+
 /* Debug/measurement: number of candidate samples (sum of clipped bounding
- * boxes) of the last fpvs_froxelize on this workspace, read back to host
+ * boxes) of the last fpvs_froxelize / fpvs_gt_pvs on this workspace, read back to host
  * (synchronises the stream). */
 long long fpvs_froxelize_samples(const void* workspace, void* stream);
 

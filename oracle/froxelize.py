@@ -47,22 +47,26 @@ def _clip_near(poly, near):
     return np.asarray(out, dtype=np.float64).reshape(-1, 3)
 
 
-def camera_triangles(verts, tris, origin, basis, near, far):
-    """Camera-space triangles after cull + near clip: (T', 3, 3) float64."""
+def camera_triangles(verts, tris, origin, basis, near, far, with_src=False):
+    """Camera-space triangles after cull + near clip: (T', 3, 3) float64
+    (and the source triangle of each when ``with_src``)."""
     verts = np.asarray(verts, dtype=np.float64).reshape(-1, 3)
     tris = np.asarray(tris, dtype=np.int64).reshape(-1, 3)
     if len(tris) == 0:
-        return np.zeros((0, 3, 3))
+        return (np.zeros((0, 3, 3)), np.zeros(0, np.int64)) if with_src else np.zeros((0, 3, 3))
     cam = (verts - np.asarray(origin, dtype=np.float64)) @ np.asarray(basis, dtype=np.float64).T
     ct = cam[tris]
     z = ct[:, :, 2]
     cand = (z.max(axis=1) > near) & (z.min(axis=1) < far)
-    keep = [ct[cand & (z.min(axis=1) >= near)]]
+    clean = np.nonzero(cand & (z.min(axis=1) >= near))[0]
+    keep, src = [ct[clean]], [clean]
     for t in np.nonzero(cand & (z.min(axis=1) < near))[0]:
         poly = _clip_near(ct[t], near)
         for k in range(1, len(poly) - 1):
             keep.append(poly[[0, k, k + 1]][None])
-    return np.concatenate(keep, axis=0)
+            src.append(np.array([t]))
+    out = np.concatenate(keep, axis=0)
+    return (out, np.concatenate(src)) if with_src else out
 
 
 def froxelize(verts, tris, origin, basis, half_extent, near, far, dims, supersample=4, depth_mode="linear"):

@@ -153,22 +153,39 @@ __device__ unsigned long long make_slot(const Params& p, const V3& a, const V3& 
   if (!live) s.w = s.h = 0;
   s.wmagic = s.w > 1 ? (unsigned int)((0x100000000ull + (unsigned long long)s.w - 1) / (unsigned long long)s.w)
                      : 0xffffffffu;
-  s.pad = 0;
   return (unsigned long long)s.w * (unsigned long long)s.h;
 }
 
-__global__ void __launch_bounds__(kSetupThreads) setup_kernel(Params p, const double* __restrict__ verts,
-                                                              long long nverts, const int64_t* __restrict__ tris,
-                                                              Work wk) {
+// One thread per (view, scene triangle); flat index f = view * T + tri, slots
+// 2f and 2f+1.  kMulti: the view's frustum comes from views[f / T] (GT-PVS
+// cameras); else from p (froxelize).  Slot.pad records the view.
+template <bool kMulti>
+__global__ void __launch_bounds__(kSetupThreads) setup_kernel(Params p, const fpvs_frustum* __restrict__ views,
+                                                              const double* __restrict__ verts, long long nverts,
+                                                              const int64_t* __restrict__ tris, long long T, Work wk) {
   const long long t = (long long)blockIdx.x * kSetupThreads + threadIdx.x;
   Slot s0, s1;
   unsigned long long c0 = 0, c1 = 0;
+  int view = 0;
   if (t < wk.ntris) {
+    long long tri = t;
+    if (kMulti) {
+      view = (int)(t / T);
+      tri = t - (long long)view * T;
+      const fpvs_frustum& f = views[view];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) p.o[i] = f.origin[i];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) p.b[i] = f.basis[i];
+      p.h = f.half_extent;
+      p.nearz = f.near_z;
+      p.farz = f.far_z;
+    }
     long long id[3];
     bool ok = true;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      id[k] = tris[t * 3 + k];
+      id[k] = tris[tri * 3 + k];
       ok &= id[k] >= 0 && id[k] < nverts;
     }
     if (ok) {
@@ -198,6 +215,7 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(Params p, const do
         }
       }
     }
+    s0.pad = s1.pad = view;
   }
   if (t < wk.ntris) {
     if (c0) wk.slots[2 * t] = s0;
@@ -276,7 +294,7 @@ __device__ __forceinline__ long long find_slot(const Work& wk, unsigned long lon
   const unsigned long long bp = __ldg(wk.bpre + lo);
   const unsigned long long local = g - bp;
   long long a = (long long)lo * kSlotsPerBlock;
-  long long z = min(a + kSlotsPerBlock, 2 * wk.ntris) - 1;
+  long long z = min(a + kSlotsPerBlock, 2 * wk.ntris) - 1;  // ntris = views x scene triangles
   const long long first = a;
   while (a < z) {
     const long long mid = (a + z) >> 1;
@@ -538,7 +556,7 @@ extern "C" int fpvs_froxelize(const double* verts, long long nverts, const int64
   if (ntris == 0) {
     if (cudaMemsetAsync(wk.total, 0, 8, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
   } else {
-    setup_kernel<<<wk.nb, kSetupThreads, 0, s>>>(p, verts, nverts, tris, wk);
+    setup_kernel<false><<<wk.nb, kSetupThreads, 0, s>>>(p, nullptr, verts, nverts, tris, ntris, wk);
     FPVS_CHECK_LAUNCH("froxelize setup");
     scan_kernel<<<1, 1024, 0, s>>>(p, wk);
     FPVS_CHECK_LAUNCH("froxelize scan");
@@ -569,4 +587,319 @@ extern "C" long long fpvs_froxelize_samples(const void* workspace, void* stream)
   if (cudaMemcpyAsync(&v, workspace, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return -1;
   if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
   return (long long)v;
+}
+
+// ===========================================================================
+// GT PVS: oracle.py:107-172 on the device.
+//
+// All cameras at once: setup<true> builds slots for every (camera, scene
+// triangle) against that camera's frustum at the depth-buffer resolution;
+// depth_kernel<0> rasterizes every candidate sample, computes the reference's
+// depth 1 / interp(1/z) exactly and keeps the minimum per pixel with a 64-bit
+// atomicMin on the (positive) double's bits; with primitive ids,
+// depth_kernel<1> re-rasterizes and keeps the smallest id among the samples
+// whose depth equals the pixel's minimum (oracle.py:130-136); resolve_kernel
+// unprojects every covered pixel from its camera (core.py:431-446), projects
+// it into the viewcell frustum (core.py:380-405), quantizes and ORs its bit
+// into the GT grid and optionally the geometry grid.
+// ===========================================================================
+namespace fpvs {
+namespace frox {
+
+struct GtParams {
+  double fo[3], fb[9];
+  double fh, fnear, ffar, flogr;  // flogr = log(far / near), computed like math.log on the host
+  double W, H;
+  int iw, ih;
+  int nx, ny, nz, depth_log;
+  long long T;     // scene triangles (per camera)
+  long long npix;  // W * H
+};
+
+// Reference depth of one sample (froxel.py:272-279 coverage; oracle.py:127
+// depth = 1 / interp_affine(invz, b1, b2)); < 0 when not covered.
+__device__ __forceinline__ double depth_exact(const Slot& s, double cx, double cy) {
+  const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
+  const double b1 = ddiv(dsub(dmul(dx, s.e2y), dmul(s.e2x, dy)), s.den);
+  const double b2 = ddiv(dsub(dmul(s.e1x, dy), dmul(dx, s.e1y)), s.den);
+  const double b0 = dsub(dsub(1.0, b1), b2);
+  if (!(b0 >= 0 && b1 >= 0 && b2 >= 0)) return -1.0;
+  return ddiv(1.0, dadd(dadd(s.iz0, dmul(b1, dsub(s.iz1, s.iz0))), dmul(b2, dsub(s.iz2, s.iz0))));
+}
+
+// Coverage filter before the exact evaluation: samples provably outside
+// (exact numerator signs, or b0 < 0 by more than the approximation error)
+// skip the three divisions.
+__device__ __forceinline__ double depth_filtered(const Slot& s, double cx, double cy) {
+  const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
+  const double n1 = dsub(dmul(dx, s.e2y), dmul(s.e2x, dy));
+  const double n2 = dsub(dmul(s.e1x, dy), dmul(dx, s.e1y));
+  const bool dneg = s.den < 0;
+  const double a1 = fabs(n1), a2 = fabs(n2);
+  constexpr double kTiny = 1e-250;
+  if (!((a1 != 0 && a1 < kTiny) || (a2 != 0 && a2 < kTiny))) {
+    if ((n1 != 0 && ((n1 < 0) != dneg)) || (n2 != 0 && ((n2 < 0) != dneg))) return -1.0;
+    const double q1 = n1 * s.rden, q2 = n2 * s.rden;
+    if ((1.0 - q1) - q2 < -1e-13 * (1.0 + q1 + q2)) return -1.0;
+  }
+  return depth_exact(s, cx, cy);
+}
+
+template <int kPass>
+__global__ void __launch_bounds__(kRasterThreads, 4)
+    depth_kernel(GtParams g, const fpvs_frustum* __restrict__ views, const int64_t* __restrict__ prim_ids, Work wk,
+                 unsigned long long* __restrict__ zbuf, long long* __restrict__ pidbuf) {
+  constexpr int kWarpSpan = 32 * kPerThread;
+  const unsigned long long total = *wk.total;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long have = -1;
+  Slot s;
+  double farz = 0;
+  long long zoff = 0, pid = 0;
+  for (unsigned long long c0 = (unsigned long long)blockIdx.x * kChunk; c0 < total;
+       c0 += (unsigned long long)gridDim.x * kChunk) {
+    const unsigned long long wbase = c0 + (unsigned long long)warp * kWarpSpan;
+    if (wbase >= total) break;
+    unsigned long long cs = 0;
+    long long cur = 0;
+    if (lane == 0) cur = find_slot(wk, wbase, cs);
+    cur = __shfl_sync(0xffffffffu, cur, 0);
+    cs = __shfl_sync(0xffffffffu, cs, 0);
+    unsigned long long ce = slot_end(wk, cur);
+#pragma unroll 1
+    for (int k = 0; k < kPerThread; ++k) {
+      const unsigned long long gi = wbase + (unsigned long long)(k * 32 + lane);
+      long long mine = cur;
+      if (gi < total) {
+        unsigned long long ms = cs, me = ce;
+        int steps = 0;
+        while (gi >= me && steps < 4) {
+          ms = me;
+          me = slot_end(wk, ++mine);
+          ++steps;
+        }
+        if (gi >= me) {
+          mine = find_slot(wk, gi, ms);
+          me = slot_end(wk, mine);
+        }
+        if (mine != have) {
+          s = wk.slots[mine];
+          have = mine;
+          farz = views[s.pad].far_z;
+          zoff = (long long)s.pad * g.npix;
+          if (kPass == 1) pid = prim_ids[(mine >> 1) - (long long)s.pad * g.T];
+        }
+        const unsigned int r = (unsigned int)(gi - ms);
+        unsigned int ry = __umulhi(r, s.wmagic);
+        const int rem = (int)(r - ry * (unsigned int)s.w);
+        if (rem < 0) --ry;
+        else if (rem >= s.w) ++ry;
+        const int px = s.x0 + (int)(r - ry * (unsigned int)s.w);
+        const int py = s.y0 + (int)ry;
+        const double depth = depth_filtered(s, centre(px), centre(py));
+        if (depth >= 0 && depth <= farz) {  // oracle.py:128
+          const long long pix = zoff + (long long)py * g.iw + px;
+          const unsigned long long bits = (unsigned long long)__double_as_longlong(depth);
+          if (kPass == 0) {
+            atomicMin(zbuf + pix, bits);
+          } else if (bits == zbuf[pix]) {
+            atomicMin(pidbuf + pix, pid);
+          }
+        }
+      }
+      const long long nxt = __shfl_sync(0xffffffffu, mine, 31);
+      if (nxt != cur) {
+        cur = nxt;
+        cs = (cur % kSlotsPerBlock ? slot_end(wk, cur - 1) : __ldg(wk.bpre + cur / kSlotsPerBlock));
+        ce = slot_end(wk, cur);
+      }
+    }
+  }
+}
+
+// Covered pixel -> world -> viewcell frustum -> froxel bit (core.py:380-452).
+__global__ void __launch_bounds__(256) resolve_kernel(GtParams g, const fpvs_frustum* __restrict__ views,
+                                                      int nviews, const unsigned long long* __restrict__ zbuf,
+                                                      const long long* __restrict__ pidbuf,
+                                                      unsigned int* __restrict__ gt_words,
+                                                      unsigned int* __restrict__ geo_words) {
+  const long long n = (long long)nviews * g.npix;
+  const unsigned int row = (unsigned int)(g.nx >> 3);
+  const int lane = threadIdx.x & 31;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += (long long)gridDim.x * blockDim.x) {
+    const long long i = base + threadIdx.x;
+    bool valid = false;
+    unsigned int word = 0, bit = 0;
+    if (i < n) {
+      const unsigned long long zb = zbuf[i];
+      valid = zb != ~0ull && (pidbuf == nullptr || pidbuf[i] >= 0);
+      if (valid) {
+        const int v = (int)(i / g.npix);
+        const long long p = i - (long long)v * g.npix;
+        const int py = (int)(p / g.iw), px = (int)(p - (long long)py * g.iw);
+        const fpvs_frustum& c = views[v];
+        const double z = __longlong_as_double((long long)zb);
+        // x = (2 (px + 0.5) / W - 1) h z   (core.py:441-442)
+        const double x = dmul(dmul(dsub(ddiv(dmul(2.0, centre(px)), g.W), 1.0), c.half_extent), z);
+        const double y = dmul(dmul(dsub(ddiv(dmul(2.0, centre(py)), g.H), 1.0), c.half_extent), z);
+        // world = position + [x y z] @ basis (dgemm k = 3 order), core.py:443-446
+        double wv[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          wv[k] = dadd(c.origin[k], __fma_rn(z, c.basis[6 + k], __fma_rn(y, c.basis[3 + k], dmul(x, c.basis[k]))));
+        const double d0 = dsub(wv[0], g.fo[0]), d1 = dsub(wv[1], g.fo[1]), d2 = dsub(wv[2], g.fo[2]);
+        const double lx = __fma_rn(d2, g.fb[2], __fma_rn(d1, g.fb[1], dmul(d0, g.fb[0])));
+        const double ly = __fma_rn(d2, g.fb[5], __fma_rn(d1, g.fb[4], dmul(d0, g.fb[3])));
+        const double lz = __fma_rn(d2, g.fb[8], __fma_rn(d1, g.fb[7], dmul(d0, g.fb[6])));
+        valid = lz > 0;
+        if (valid) {
+          const double zh = dmul(lz, g.fh);
+          const double u = dadd(0.5, ddiv(dmul(0.5, lx), zh));
+          const double vv = dadd(0.5, ddiv(dmul(0.5, ly), zh));
+          const double w = g.depth_log ? ddiv(log(ddiv(lz, g.fnear)), g.flogr)
+                                       : ddiv(dsub(lz, g.fnear), dsub(g.ffar, g.fnear));
+          valid = u >= 0 && u <= 1 && vv >= 0 && vv <= 1 && w >= 0 && w <= 1;
+          if (valid) {
+            const int ix = min(max((int)floor(dmul(u, (double)g.nx)), 0), g.nx - 1);
+            const int iy = min(max((int)floor(dmul(vv, (double)g.ny)), 0), g.ny - 1);
+            const int iz = min(max((int)floor(dmul(w, (double)g.nz)), 0), g.nz - 1);
+            const unsigned long long byte = (unsigned long long)(ix >> 3) +
+                                            (unsigned long long)row * ((unsigned long long)iy + (unsigned long long)g.ny * iz);
+            word = (unsigned int)(byte >> 2);
+            bit = 1u << ((((unsigned int)byte & 3u) << 3) | ((unsigned int)ix & 7u));
+          }
+        }
+      }
+    }
+    const unsigned int vm = __ballot_sync(0xffffffffu, valid);
+    if (vm) {
+      const int leader = __ffs(vm) - 1;
+      const unsigned int w0 = __shfl_sync(0xffffffffu, word, leader);
+      if (__all_sync(0xffffffffu, !valid || word == w0)) {
+        const unsigned int bits = __reduce_or_sync(0xffffffffu, valid ? bit : 0u);
+        if (lane == leader) {
+          atomicOr(gt_words + w0, bits);
+          if (geo_words) atomicOr(geo_words + w0, bits);
+        }
+      } else if (valid) {
+        atomicOr(gt_words + word, bit);
+        if (geo_words) atomicOr(geo_words + word, bit);
+      }
+    }
+  }
+}
+
+struct GtLayout {
+  size_t total, slots, lp, bsum, bpre, zbuf, pid, bytes;
+};
+
+inline GtLayout gt_layout(long long ntris, int nviews, long long npix, bool with_pids) {
+  GtLayout L;
+  const long long flat = (ntris > 0 ? ntris : 1) * (long long)(nviews > 0 ? nviews : 1);
+  const long long nslot = 2 * flat;
+  const long long nb = (nslot + kSlotsPerBlock - 1) / kSlotsPerBlock;
+  size_t o = 0;
+  L.total = o; o = up256(o + 8);
+  L.slots = o; o = up256(o + (size_t)nslot * sizeof(Slot));
+  L.lp = o;    o = up256(o + (size_t)nslot * 8);
+  L.bsum = o;  o = up256(o + (size_t)nb * 8);
+  L.bpre = o;  o = up256(o + (size_t)nb * 8);
+  L.zbuf = o;  o = up256(o + (size_t)nviews * (size_t)npix * 8);
+  L.pid = o;   o = up256(o + (with_pids ? (size_t)nviews * (size_t)npix * 8 : 0));
+  L.bytes = o;
+  return L;
+}
+
+}  // namespace frox
+}  // namespace fpvs
+
+extern "C" size_t fpvs_gt_pvs_workspace_size(long long ntris, int ncams, int res_w, int res_h, int with_prim_ids) {
+  if (ntris < 0 || ncams < 0 || res_w <= 0 || res_h <= 0) return 0;
+  return gt_layout(ntris, ncams, (long long)res_w * res_h, with_prim_ids != 0).bytes;
+}
+
+extern "C" int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                           const int64_t* prim_ids, const fpvs_frustum* cams, int ncams, int res_w, int res_h,
+                           const fpvs_frustum* fr, int Nx, int Ny, int Nz, int depth_mode, int accumulate,
+                           uint8_t* gt_bits, uint8_t* geometry_bits, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+  FPVS_CHECK_ARG(fr != nullptr && gt_bits != nullptr, "gt_pvs: null frustum or output");
+  FPVS_CHECK_ARG(Nx > 0 && Ny > 0 && Nz > 0 && Nx % 8 == 0, "N_x must be divisible by 8, got %d", Nx);
+  FPVS_CHECK_ARG(res_w >= Nx && res_h >= Ny, "depth buffer must be at least the grid cross-section");
+  FPVS_CHECK_ARG((long long)res_w * res_h < (1LL << 32) && res_w < (1 << 30) && res_h < (1 << 30),
+                 "gt_pvs: depth buffer %d x %d too large", res_w, res_h);
+  FPVS_CHECK_ARG(depth_mode == FPVS_DEPTH_LINEAR || depth_mode == FPVS_DEPTH_LOG, "bad depth mode %d", depth_mode);
+  FPVS_CHECK_ARG(ncams >= 0 && (ncams == 0 || cams != nullptr), "gt_pvs: bad camera array");
+  FPVS_CHECK_ARG(ntris >= 0 && nverts >= 0 && (ntris == 0 || (verts && tris)), "gt_pvs: bad scene arrays");
+  FPVS_CHECK_ARG(fr->near_z > 0 && fr->near_z < fr->far_z && fr->half_extent > 0, "need 0 < near < far");
+  const long long grid_bytes = (long long)Nx * Ny * Nz / 8;
+  FPVS_CHECK_ARG(grid_bytes % 4 == 0 && ((uintptr_t)gt_bits & 3) == 0 && ((uintptr_t)geometry_bits & 3) == 0,
+                 "gt_pvs: grids must be 4-byte aligned with Nx*Ny*Nz/8 a multiple of 4");
+  const long long npix = (long long)res_w * res_h;
+  const GtLayout L = gt_layout(ntris, ncams, npix, prim_ids != nullptr);
+  FPVS_CHECK_ARG(workspace != nullptr && workspace_bytes >= L.bytes, "gt_pvs: workspace too small (%zu < %zu)",
+                 workspace_bytes, L.bytes);
+  cudaStream_t s = as_stream(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  if (!accumulate && cudaMemsetAsync(gt_bits, 0, (size_t)grid_bytes, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  if (ntris == 0 || ncams == 0) return FPVS_OK;
+  Work wk;
+  wk.slots = reinterpret_cast<Slot*>(ws + L.slots);
+  wk.lp = reinterpret_cast<unsigned long long*>(ws + L.lp);
+  wk.bsum = reinterpret_cast<unsigned long long*>(ws + L.bsum);
+  wk.bpre = reinterpret_cast<unsigned long long*>(ws + L.bpre);
+  wk.total = reinterpret_cast<unsigned long long*>(ws + L.total);
+  wk.out_words = nullptr;
+  wk.tabx = wk.taby = nullptr;
+  wk.ntris = ntris * ncams;
+  wk.nb = (int)((2 * wk.ntris + kSlotsPerBlock - 1) / kSlotsPerBlock);
+  unsigned long long* zbuf = reinterpret_cast<unsigned long long*>(ws + L.zbuf);
+  long long* pidbuf = prim_ids ? reinterpret_cast<long long*>(ws + L.pid) : nullptr;
+  if (cudaMemsetAsync(zbuf, 0xff, (size_t)ncams * npix * 8, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  if (pidbuf && cudaMemsetAsync(pidbuf, 0x7f, (size_t)ncams * npix * 8, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  Params p = {};
+  p.sx = (double)res_w;
+  p.sy = (double)res_h;
+  p.isx = 0;  // no pixel->froxel tables in this mode
+  p.isy = 0;
+  p.nx = Nx;
+  p.ny = Ny;
+  p.nz = Nz;
+  p.depth_log = 0;
+  GtParams g;
+  for (int i = 0; i < 3; ++i) g.fo[i] = fr->origin[i];
+  for (int i = 0; i < 9; ++i) g.fb[i] = fr->basis[i];
+  g.fh = fr->half_extent;
+  g.fnear = fr->near_z;
+  g.ffar = fr->far_z;
+  g.flogr = log(fr->far_z / fr->near_z);
+  g.W = (double)res_w;
+  g.H = (double)res_h;
+  g.iw = res_w;
+  g.ih = res_h;
+  g.nx = Nx;
+  g.ny = Ny;
+  g.nz = Nz;
+  g.depth_log = depth_mode == FPVS_DEPTH_LOG;
+  g.T = ntris;
+  g.npix = npix;
+  setup_kernel<true><<<wk.nb, kSetupThreads, 0, s>>>(p, cams, verts, nverts, tris, ntris, wk);
+  FPVS_CHECK_LAUNCH("gt_pvs setup");
+  scan_kernel<<<1, 1024, 0, s>>>(p, wk);
+  FPVS_CHECK_LAUNCH("gt_pvs scan");
+  static const int per_sm = [] {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, depth_kernel<0>, kRasterThreads, 0);
+    return n > 0 ? n : 1;
+  }();
+  depth_kernel<0><<<kNumSMs * per_sm, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
+  FPVS_CHECK_LAUNCH("gt_pvs depth");
+  if (pidbuf) {
+    depth_kernel<1><<<kNumSMs * per_sm, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
+    FPVS_CHECK_LAUNCH("gt_pvs prim ids");
+  }
+  resolve_kernel<<<kNumSMs * 8, 256, 0, s>>>(g, cams, ncams, zbuf, pidbuf, reinterpret_cast<unsigned int*>(gt_bits),
+                                             reinterpret_cast<unsigned int*>(geometry_bits));
+  FPVS_CHECK_LAUNCH("gt_pvs resolve");
+  return FPVS_OK;
 }

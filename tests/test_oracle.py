@@ -298,3 +298,46 @@ def test_froxelize_oracle_against_live_reference():
             got = ofz.froxelize(scene.vertices, scene.triangles, fr._o, fr._basis, fr.half_extent, fr.near,
                                 fr.far, (32, 16, 24), ss)
             assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------- GT PVS
+
+
+def _gt_case(g, i):
+    return {k[len(f"c{i}_"):]: g[k] for k in g.files if k.startswith(f"c{i}_")}
+
+
+def test_gtpvs_oracle_and_viewpoints_match_reference_golden(golden):
+    """oracle/gtpvs.py and views.sample_viewpoints vs compute_gt_pvs / sample_viewpoints output."""
+    from oracle import gtpvs as ogt
+    from paper_2509_24677_b200 import views
+    g = golden("gtpvs.npz")
+    for i in range(int(g["ncases"])):
+        c = _gt_case(g, i)
+        cams = [(r[0:3], r[3:12].reshape(3, 3), r[12], r[13], r[14]) for r in c["cams"]]
+        f = c["frustum"]
+        geo = c["geo_in"].copy() if "geo_in" in c else None
+        bits = ogt.gt_pvs(c["verts"], c["tris"], cams, (f[0:3], f[3:12].reshape(3, 3), f[12], f[13], f[14]),
+                          c["dims"], c["res"], "linear" if int(c["depth"]) == 0 else "log", c["prim_ids"], geo)
+        assert np.array_equal(bits, c["bits"]), str(c["name"])
+        if geo is not None:
+            assert np.array_equal(geo, c["geo_out"])
+        cl = c["cell"]
+        cell = views.ViewCell(tuple(cl[0:3]), cl[3], cl[4], cl[5], tuple(cl[6:9]), tuple(cl[9:12]),
+                              tuple(cl[12:15]), cl[15], cl[16])
+        vp, mode, seed, sub = (int(x) for x in c["sampling"])
+        vs = views.sample_viewpoints(cell, vp, "uniform-grid" if mode == 0 else "uniform-random", seed)
+        vs = vs[:sub] if sub >= 0 else vs
+        rows = np.array([np.concatenate([v.position, v.right, v.up, v.forward, [v.half_extent, v.near, v.far]])
+                         for v in vs]).reshape(-1, 15)
+        assert np.array_equal(rows, c["cams"]), str(c["name"])
+        fv = views.build_viewcell_frustum(cell)
+        assert np.array_equal(np.concatenate([fv._o, fv._basis.ravel(), [fv.half_extent, fv.near, fv.far]]), f)
+
+
+def test_gtpvs_occluder_hides_everything_behind(golden):
+    """test_oracle.py:113-137: no GT froxel strictly behind a full-cross-section occluder."""
+    g = golden("gtpvs.npz")
+    i = next(i for i in range(int(g["ncases"])) if str(g[f"c{i}_name"]) == "occluder")
+    dense = FroxelGrid((16, 16, 16), bits=g[f"c{i}_bits"]).to_dense()
+    assert dense[:, :, :9].sum() > 0 and dense[:, :, 9:].sum() == 0
