@@ -398,6 +398,38 @@ int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t* tris, long
                 uint8_t* gt_bits, uint8_t* geometry_bits, void* workspace, size_t workspace_bytes,
                 void* stream);
 
+/* Culling from a froxel PVS: kept[t] = 1 iff scene
+ * triangle t has a perspective fragment (the froxelize() stream with the
+ * same frustum / dims / supersample / depth mode) in a froxel whose pvs bit
+ * is set — i.e. evalrt.py:62-68 cull() over froxel_id_map() (froxel.py:
+ * 397-417) without materialising the map.  kept: uint8 [ntris], zeroed by
+ * the call; pvs_bits 4-byte aligned, Nx*Ny*Nz/8 % 4 == 0.  Workspace:
+ * fpvs_froxelize_workspace_size. */
+int fpvs_froxel_cull(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                     const fpvs_frustum* frustum, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                     const uint8_t* pvs_bits, uint8_t* kept, void* workspace, size_t workspace_bytes, void* stream);
+
+/* The fragment pairs behind froxel_id_map() (froxel.py:397-417): one int64
+ * key = (x + Nx*(y + Ny*z)) * ntris + triangle per fragment, duplicates
+ * within a warp dropped (callers unique the keys).  At most cap keys are
+ * written; *npairs_dev (device) receives the number produced, which may
+ * exceed cap (then call again with a larger buffer; cap = the candidate
+ * sample count from fpvs_froxelize_samples always suffices). */
+int fpvs_froxel_pairs(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                      const fpvs_frustum* frustum, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                      long long* pairs, long long cap, unsigned long long* npairs_dev, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* Depth + primitive-id buffers of oracle.py:107-138 render_depth() for
+ * ncams cameras (DEVICE array, fpvs_frustum form) at res_w x res_h:
+ * depth_out float64 [ncams][res_h][res_w] (+inf where empty, nullable),
+ * prim_out int64 (-1 where empty; exact depth ties -> smallest id).
+ * prim_ids NULL = triangle index.  Workspace:
+ * fpvs_gt_pvs_workspace_size(ntris, ncams, res_w, res_h, 1). */
+int fpvs_render_depth(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                      const int64_t* prim_ids, const fpvs_frustum* cams, int ncams, int res_w, int res_h,
+                      double* depth_out, int64_t* prim_out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Debug/measurement: number of candidate samples (sum of clipped bounding
  * boxes) of the last fpvs_froxelize / fpvs_gt_pvs on this workspace, read back to host
  * (synchronises the stream). */

@@ -72,6 +72,11 @@ struct Work {
   unsigned int* out_words;
   int* tabx;  // froxel column of supersampled pixel column px (quantize of (px+0.5)/sx)
   int* taby;
+  const unsigned int* pvs_words;  // kMode 1: the PVS grid whose froxels keep their primitives
+  uint8_t* kept;                  // kMode 1: per scene triangle, 1 = touches a PVS froxel
+  long long* pairs;               // kMode 2: (froxel * T + triangle) per fragment
+  unsigned long long* npairs;
+  long long pair_cap;
   long long ntris;
   int nb;
 };
@@ -381,7 +386,10 @@ __device__ __forceinline__ unsigned long long slot_end(const Work& wk, long long
 // Each warp rasterizes 32 * kPerThread consecutive samples, 32 at a time
 // (lane = sample), so the lanes of one step share a slot or walk forward to
 // the next few; only the warp's first sample needs the binary search.
-template <bool kFilter>
+// kMode 0: OR fragment bits into the grid (froxelize); 1: mark the triangles
+// with a fragment in a PVS froxel (cull, evalrt.py:62-68); 2: emit (froxel,
+// triangle) fragment pairs (froxel_id_map, froxel.py:397-417).
+template <bool kFilter, int kMode>
 __global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(Params p, Work wk) {
   constexpr int kWarpSpan = 32 * kPerThread;
   const unsigned long long total = *wk.total;
@@ -404,7 +412,7 @@ __global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(Params p, Wor
       const unsigned long long g = wbase + (unsigned long long)(k * 32 + lane);
       bool valid = g < total;
       unsigned int word = 0, bit = 0;
-      long long mine = cur;
+      long long mine = cur, flat = 0;
       if (valid) {
         unsigned long long ms = cs, me = ce;
         // walk a few slots forward (odd slots of unclipped triangles are
@@ -439,6 +447,7 @@ __global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(Params p, Wor
                                           (unsigned long long)row * ((unsigned long long)iy + (unsigned long long)p.ny * iz);
           word = (unsigned int)(byte >> 2);
           bit = 1u << ((((unsigned int)byte & 3u) << 3) | ((unsigned int)ix & 7u));
+          if (kMode == 2) flat = ix + (long long)p.nx * (iy + (long long)p.ny * iz);  // froxel.py:411
         }
       }
       // the warp's next step starts from the last lane's slot
@@ -448,16 +457,28 @@ __global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(Params p, Wor
         cs = (cur % kSlotsPerBlock ? slot_end(wk, cur - 1) : __ldg(wk.bpre + cur / kSlotsPerBlock));
         ce = slot_end(wk, cur);
       }
-      // warp-combined OR: one atomic when every covered lane hits the same word
-      const unsigned int vm = __ballot_sync(0xffffffffu, valid);
-      if (vm) {
-        const int leader = __ffs(vm) - 1;
-        const unsigned int w0 = __shfl_sync(0xffffffffu, word, leader);
-        if (__all_sync(0xffffffffu, !valid || word == w0)) {
-          const unsigned int bits = __reduce_or_sync(0xffffffffu, valid ? bit : 0u);
-          if (lane == leader) atomicOr(wk.out_words + w0, bits);
-        } else if (valid) {
-          atomicOr(wk.out_words + word, bit);
+      if (kMode == 0) {
+        // warp-combined OR: one atomic when every covered lane hits the same word
+        const unsigned int vm = __ballot_sync(0xffffffffu, valid);
+        if (vm) {
+          const int leader = __ffs(vm) - 1;
+          const unsigned int w0 = __shfl_sync(0xffffffffu, word, leader);
+          if (__all_sync(0xffffffffu, !valid || word == w0)) {
+            const unsigned int bits = __reduce_or_sync(0xffffffffu, valid ? bit : 0u);
+            if (lane == leader) atomicOr(wk.out_words + w0, bits);
+          } else if (valid) {
+            atomicOr(wk.out_words + word, bit);
+          }
+        }
+      } else if (kMode == 1) {
+        if (valid && (__ldg(wk.pvs_words + word) & bit)) wk.kept[mine >> 1] = 1;
+      } else {
+        // one pair per distinct (froxel, triangle) among the warp's lanes
+        const long long key = valid ? flat * wk.ntris + (mine >> 1) : -1 - lane;
+        const unsigned int peers = __match_any_sync(0xffffffffu, key);
+        if (valid && (__ffs(peers) - 1) == lane) {
+          const unsigned long long slot = atomicAdd(wk.npairs, 1ull);
+          if ((long long)slot < wk.pair_cap) wk.pairs[slot] = key;
         }
       }
     }
@@ -507,10 +528,35 @@ extern "C" size_t fpvs_froxelize_workspace_size(long long ntris, int Nx, int Ny,
   return layout(ntris, (long long)Nx * Ny * Nz / 8, (long long)supersample * Nx, (long long)supersample * Ny).bytes;
 }
 
-extern "C" int fpvs_froxelize(const double* verts, long long nverts, const int64_t* tris, long long ntris,
-                              const fpvs_frustum* fr, int Nx, int Ny, int Nz, int supersample, int depth_mode,
-                              uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream) {
-  FPVS_CHECK_ARG(fr != nullptr && out_bits != nullptr, "froxelize: null frustum or output");
+namespace fpvs {
+namespace frox {
+
+template <int kMode>
+int launch_raster(const Params& p, const Work& wk, cudaStream_t s) {
+  static const int per_sm[2] = {[] {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, raster_kernel<false, kMode>, kRasterThreads, 0);
+    return n > 0 ? n : 1;
+  }(), [] {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, raster_kernel<true, kMode>, kRasterThreads, 0);
+    return n > 0 ? n : 1;
+  }()};
+  if (filtered())
+    raster_kernel<true, kMode><<<kNumSMs * per_sm[1], kRasterThreads, 0, s>>>(p, wk);
+  else
+    raster_kernel<false, kMode><<<kNumSMs * per_sm[0], kRasterThreads, 0, s>>>(p, wk);
+  FPVS_CHECK_LAUNCH("froxelize raster");
+  return FPVS_OK;
+}
+
+// Argument checks, workspace carve-up, setup + scan, then the raster of the
+// requested mode.  out_words: the (aligned) grid for mode 0.
+template <int kMode>
+int froxel_pass(const double* verts, long long nverts, const int64_t* tris, long long ntris, const fpvs_frustum* fr,
+                int Nx, int Ny, int Nz, int supersample, int depth_mode, void* workspace, size_t workspace_bytes,
+                cudaStream_t s, Work& wk, Layout& L) {
+  FPVS_CHECK_ARG(fr != nullptr, "froxelize: null frustum");
   FPVS_CHECK_ARG(Nx > 0 && Ny > 0 && Nz > 0 && Nx % 8 == 0, "N_x must be divisible by 8, got %d", Nx);
   FPVS_CHECK_ARG(supersample >= 1, "supersample factor must be >= 1");
   FPVS_CHECK_ARG(depth_mode == FPVS_DEPTH_LINEAR || depth_mode == FPVS_DEPTH_LOG, "bad depth mode %d", depth_mode);
@@ -520,21 +566,15 @@ extern "C" int fpvs_froxelize(const double* verts, long long nverts, const int64
   FPVS_CHECK_ARG(sx * sy < (1LL << 32) && sx < (1LL << 30) && sy < (1LL << 30),
                  "froxelize: supersampled screen %lld x %lld too large", sx, sy);
   const long long grid_bytes = (long long)Nx * Ny * Nz / 8;
-  const Layout L = layout(ntris, grid_bytes, sx, sy);
+  L = layout(ntris, grid_bytes, sx, sy);
   FPVS_CHECK_ARG(workspace != nullptr && workspace_bytes >= L.bytes, "froxelize: workspace too small (%zu < %zu)",
                  workspace_bytes, L.bytes);
-  cudaStream_t s = as_stream(stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  const bool direct = ((uintptr_t)out_bits & 3) == 0 && grid_bytes % 4 == 0;
-  unsigned int* words = direct ? reinterpret_cast<unsigned int*>(out_bits) : reinterpret_cast<unsigned int*>(ws + L.words);
-  if (cudaMemsetAsync(words, 0, (size_t)((grid_bytes + 3) & ~3LL), s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
-  Work wk;
   wk.slots = reinterpret_cast<Slot*>(ws + L.slots);
   wk.lp = reinterpret_cast<unsigned long long*>(ws + L.lp);
   wk.bsum = reinterpret_cast<unsigned long long*>(ws + L.bsum);
   wk.bpre = reinterpret_cast<unsigned long long*>(ws + L.bpre);
   wk.total = reinterpret_cast<unsigned long long*>(ws + L.total);
-  wk.out_words = words;
   wk.tabx = reinterpret_cast<int*>(ws + L.tabx);
   wk.taby = reinterpret_cast<int*>(ws + L.taby);
   wk.ntris = ntris;
@@ -555,29 +595,79 @@ extern "C" int fpvs_froxelize(const double* verts, long long nverts, const int64
   p.depth_log = depth_mode == FPVS_DEPTH_LOG;
   if (ntris == 0) {
     if (cudaMemsetAsync(wk.total, 0, 8, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
-  } else {
-    setup_kernel<false><<<wk.nb, kSetupThreads, 0, s>>>(p, nullptr, verts, nverts, tris, ntris, wk);
-    FPVS_CHECK_LAUNCH("froxelize setup");
-    scan_kernel<<<1, 1024, 0, s>>>(p, wk);
-    FPVS_CHECK_LAUNCH("froxelize scan");
-    static const int per_sm[2] = {[] {
-      int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, raster_kernel<false>, kRasterThreads, 0);
-      return n > 0 ? n : 1;
-    }(), [] {
-      int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, raster_kernel<true>, kRasterThreads, 0);
-      return n > 0 ? n : 1;
-    }()};
-    if (filtered())
-      raster_kernel<true><<<kNumSMs * per_sm[1], kRasterThreads, 0, s>>>(p, wk);
-    else
-      raster_kernel<false><<<kNumSMs * per_sm[0], kRasterThreads, 0, s>>>(p, wk);
-    FPVS_CHECK_LAUNCH("froxelize raster");
+    return FPVS_OK;
   }
+  setup_kernel<false><<<wk.nb, kSetupThreads, 0, s>>>(p, nullptr, verts, nverts, tris, ntris, wk);
+  FPVS_CHECK_LAUNCH("froxelize setup");
+  scan_kernel<<<1, 1024, 0, s>>>(p, wk);
+  FPVS_CHECK_LAUNCH("froxelize scan");
+  return launch_raster<kMode>(p, wk, s);
+}
+
+}  // namespace frox
+}  // namespace fpvs
+
+extern "C" int fpvs_froxelize(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                              const fpvs_frustum* fr, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                              uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream) {
+  FPVS_CHECK_ARG(out_bits != nullptr, "froxelize: null output");
+  FPVS_CHECK_ARG(Nx > 0 && Ny > 0 && Nz > 0, "froxelize: bad dims");
+  cudaStream_t s = as_stream(stream);
+  const long long grid_bytes = (long long)Nx * Ny * Nz / 8;
+  const bool direct = ((uintptr_t)out_bits & 3) == 0 && grid_bytes % 4 == 0;
+  Work wk = {};
+  Layout L = {};
+  // the scratch grid offset is needed before the pass: compute the layout first
+  {
+    const long long sx = (long long)supersample * Nx, sy = (long long)supersample * Ny;
+    L = layout(ntris, grid_bytes, sx, sy);
+  }
+  unsigned int* words = direct ? reinterpret_cast<unsigned int*>(out_bits)
+                               : reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(workspace) + L.words);
+  if (workspace == nullptr || workspace_bytes < L.bytes)
+    return set_error(FPVS_EINVAL, "froxelize: workspace too small (%zu < %zu)", workspace_bytes, L.bytes);
+  if (cudaMemsetAsync(words, 0, (size_t)((grid_bytes + 3) & ~3LL), s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  wk.out_words = words;
+  const int rc = froxel_pass<0>(verts, nverts, tris, ntris, fr, Nx, Ny, Nz, supersample, depth_mode, workspace,
+                                workspace_bytes, s, wk, L);
+  if (rc) return rc;
   if (!direct && cudaMemcpyAsync(out_bits, words, (size_t)grid_bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
     FPVS_CHECK_LAUNCH("froxelize copy");
   return FPVS_OK;
+}
+
+extern "C" int fpvs_froxel_cull(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                                const fpvs_frustum* fr, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                                const uint8_t* pvs_bits, uint8_t* kept, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  const long long grid_bytes = (long long)Nx * Ny * Nz / 8;
+  FPVS_CHECK_ARG(pvs_bits != nullptr && (ntris == 0 || kept != nullptr), "froxel_cull: null pvs or output");
+  FPVS_CHECK_ARG(((uintptr_t)pvs_bits & 3) == 0 && grid_bytes % 4 == 0,
+                 "froxel_cull: pvs grid must be 4-byte aligned with Nx*Ny*Nz/8 a multiple of 4");
+  cudaStream_t s = as_stream(stream);
+  if (ntris > 0 && cudaMemsetAsync(kept, 0, (size_t)ntris, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  Work wk = {};
+  Layout L = {};
+  wk.pvs_words = reinterpret_cast<const unsigned int*>(pvs_bits);
+  wk.kept = kept;
+  return froxel_pass<1>(verts, nverts, tris, ntris, fr, Nx, Ny, Nz, supersample, depth_mode, workspace,
+                        workspace_bytes, s, wk, L);
+}
+
+extern "C" int fpvs_froxel_pairs(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                                 const fpvs_frustum* fr, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                                 long long* pairs, long long cap, unsigned long long* npairs_dev, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  FPVS_CHECK_ARG(npairs_dev != nullptr && cap >= 0 && (cap == 0 || pairs != nullptr), "froxel_pairs: bad output");
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(npairs_dev, 0, 8, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  Work wk = {};
+  Layout L = {};
+  wk.pairs = pairs;
+  wk.npairs = npairs_dev;
+  wk.pair_cap = cap;
+  return froxel_pass<2>(verts, nverts, tris, ntris, fr, Nx, Ny, Nz, supersample, depth_mode, workspace,
+                        workspace_bytes, s, wk, L);
 }
 
 extern "C" long long fpvs_froxelize_samples(const void* workspace, void* stream) {
@@ -687,7 +777,10 @@ __global__ void __launch_bounds__(kRasterThreads, 4)
           have = mine;
           farz = views[s.pad].far_z;
           zoff = (long long)s.pad * g.npix;
-          if (kPass == 1) pid = prim_ids[(mine >> 1) - (long long)s.pad * g.T];
+          if (kPass == 1) {
+            const long long tri = (mine >> 1) - (long long)s.pad * g.T;
+            pid = prim_ids ? prim_ids[tri] : tri;
+          }
         }
         const unsigned int r = (unsigned int)(gi - ms);
         unsigned int ry = __umulhi(r, s.wmagic);
@@ -786,6 +879,18 @@ __global__ void __launch_bounds__(256) resolve_kernel(GtParams g, const fpvs_fru
         if (geo_words) atomicOr(geo_words + word, bit);
       }
     }
+  }
+}
+
+// DepthBuffer of oracle.py:48-62: depth (+inf where empty), prim (-1 where empty).
+__global__ void depth_out_kernel(long long n, const unsigned long long* __restrict__ zbuf,
+                                 const long long* __restrict__ pidbuf, double* __restrict__ depth,
+                                 long long* __restrict__ prim) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long zb = zbuf[i];
+    const bool hit = zb != ~0ull;
+    if (depth) depth[i] = hit ? __longlong_as_double((long long)zb) : __longlong_as_double(0x7ff0000000000000LL);
+    if (prim) prim[i] = hit ? pidbuf[i] : -1;
   }
 }
 
@@ -901,5 +1006,59 @@ extern "C" int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t*
   resolve_kernel<<<kNumSMs * 8, 256, 0, s>>>(g, cams, ncams, zbuf, pidbuf, reinterpret_cast<unsigned int*>(gt_bits),
                                              reinterpret_cast<unsigned int*>(geometry_bits));
   FPVS_CHECK_LAUNCH("gt_pvs resolve");
+  return FPVS_OK;
+}
+
+extern "C" int fpvs_render_depth(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                                 const int64_t* prim_ids, const fpvs_frustum* cams, int ncams, int res_w, int res_h,
+                                 double* depth_out, int64_t* prim_out, void* workspace, size_t workspace_bytes,
+                                 void* stream) {
+  FPVS_CHECK_ARG(res_w > 0 && res_h > 0 && (long long)res_w * res_h < (1LL << 32), "render_depth: bad resolution");
+  FPVS_CHECK_ARG(ncams >= 0 && (ncams == 0 || cams != nullptr), "render_depth: bad camera array");
+  FPVS_CHECK_ARG(ntris >= 0 && nverts >= 0 && (ntris == 0 || (verts && tris)), "render_depth: bad scene arrays");
+  const long long npix = (long long)res_w * res_h;
+  const GtLayout L = gt_layout(ntris, ncams, npix, true);
+  FPVS_CHECK_ARG(workspace != nullptr && workspace_bytes >= L.bytes, "render_depth: workspace too small (%zu < %zu)",
+                 workspace_bytes, L.bytes);
+  if (ncams == 0) return FPVS_OK;
+  cudaStream_t s = as_stream(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  unsigned long long* zbuf = reinterpret_cast<unsigned long long*>(ws + L.zbuf);
+  long long* pidbuf = reinterpret_cast<long long*>(ws + L.pid);
+  if (cudaMemsetAsync(zbuf, 0xff, (size_t)ncams * npix * 8, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  if (cudaMemsetAsync(pidbuf, 0x7f, (size_t)ncams * npix * 8, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  if (ntris > 0) {
+    Work wk = {};
+    wk.slots = reinterpret_cast<Slot*>(ws + L.slots);
+    wk.lp = reinterpret_cast<unsigned long long*>(ws + L.lp);
+    wk.bsum = reinterpret_cast<unsigned long long*>(ws + L.bsum);
+    wk.bpre = reinterpret_cast<unsigned long long*>(ws + L.bpre);
+    wk.total = reinterpret_cast<unsigned long long*>(ws + L.total);
+    wk.ntris = ntris * ncams;
+    wk.nb = (int)((2 * wk.ntris + kSlotsPerBlock - 1) / kSlotsPerBlock);
+    Params p = {};
+    p.sx = (double)res_w;
+    p.sy = (double)res_h;
+    GtParams g = {};
+    g.iw = res_w;
+    g.ih = res_h;
+    g.W = (double)res_w;
+    g.H = (double)res_h;
+    g.T = ntris;
+    g.npix = npix;
+    setup_kernel<true><<<wk.nb, kSetupThreads, 0, s>>>(p, cams, verts, nverts, tris, ntris, wk);
+    FPVS_CHECK_LAUNCH("render_depth setup");
+    scan_kernel<<<1, 1024, 0, s>>>(p, wk);
+    FPVS_CHECK_LAUNCH("render_depth scan");
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, depth_kernel<0>, kRasterThreads, 0);
+    per_sm = per_sm > 0 ? per_sm : 1;
+    depth_kernel<0><<<kNumSMs * per_sm, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
+    FPVS_CHECK_LAUNCH("render_depth depth");
+    depth_kernel<1><<<kNumSMs * per_sm, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
+    FPVS_CHECK_LAUNCH("render_depth ids");
+  }
+  depth_out_kernel<<<kNumSMs * 8, 256, 0, s>>>((long long)ncams * npix, zbuf, pidbuf, depth_out, reinterpret_cast<long long*>(prim_out));
+  FPVS_CHECK_LAUNCH("render_depth out");
   return FPVS_OK;
 }
