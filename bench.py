@@ -30,6 +30,9 @@ halo tables), sparse interleave, 14 convs, head.
 * ``froxelize`` (extra, N=1): SURVEY §8(f) #1, the device froxelizer on two
   seeded triangle scenes into the 256^3 grid, device us per call and the
   numpy oracle's CPU time on the same scene; a side line, not the metric.
+* ``gt_pvs`` (extra, N=1): SURVEY §8(f) #3, the device GT-PVS generator for
+  one viewcell (128 viewpoints, 1024^2 depth buffers, 256^3 grid) against the
+  numpy oracle's time per viewpoint; a side line, not the metric.
 * ``train_config5`` (extra, rank 0): BASELINE config 5's training step on one
   GPU (8 x 128^3 grids, bf16 + fp32 master weights, AdamW, tcgen05 backward),
   10 steps timed with CUDA events; a reported side line, not the metric.
@@ -268,6 +271,45 @@ def froxelize_side(reps: int = 20):
             "kernels": "setup + scan + raster (3 launches + memset)", **out}
 
 
+def gt_pvs_side(views_n: int = 128):
+    """fpvs_gt_pvs of a seeded scene for one viewcell — 128
+    viewpoints (OracleConfig default), 1024^2 depth buffers, 256^3 grid — device
+    time per viewcell (CUDA events, best of 3); the numpy oracle on ONE of the
+    same viewpoints as its CPU baseline (per view).  A side line."""
+    import torch
+    from paper_2509_24677_b200 import gtpvs, synth, views
+    from oracle import gtpvs as ogt
+    dims = (256, 256, 256)
+    v, t, fa = synth.froxel_scene(0, 12, 12)
+    cell = views.ViewCell.from_forward(tuple(fa[0] + fa[5] * fa[1]), 0.3, 60.0, 15.0, tuple(fa[1]), 0.3, 20.0)
+    ocfg = gtpvs.OracleConfig(viewpoints=views_n)
+    g = gtpvs.GtPvs(v, t)
+    out = torch.zeros(256 ** 3 // 8, dtype=torch.uint8, device="cuda")
+    g.for_cell(cell, dims, ocfg, out=out)
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.for_cell(cell, dims, ocfg, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    cams = views.sample_viewpoints(cell, views_n)[:1]
+    fr = views.build_viewcell_frustum(cell)
+    t0 = time.perf_counter()
+    ogt.gt_pvs(v, t, [c.params() for c in cams], (fr._o, fr._basis, fr.half_extent, fr.near, fr.far), dims,
+               ocfg.resolution_for(dims))
+    cpu_view_s = time.perf_counter() - t0
+    return {"workload": f"synth.froxel_scene(0): {len(t)} triangles, {views_n} viewpoints, 1024x1024 depth buffers, "
+                        "256^3 GT grid, linear depth",
+            "kernels": "setup + scan + depth (64-bit atomicMin z-test) + resolve (4 launches + 2 memsets)",
+            "device_ms_per_viewcell": round(best, 3), "device_us_per_view": round(best * 1e3 / views_n, 2),
+            "gt_froxels": int(np.unpackbits(out.cpu().numpy()).sum()),
+            "oracle_cpu_s_per_view": round(cpu_view_s, 4),
+            "speedup_vs_oracle": round(cpu_view_s * views_n / (best * 1e-3), 1)}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -394,8 +436,10 @@ def run_ours(args):
     frox = None
     if not args.no_train:
         train = train_config5()
+    gtp = None
     if ws == 1 and not args.no_froxelize:
         frox = froxelize_side()
+        gtp = gt_pvs_side()
     if ws == 1 and not args.no_cpu_baseline:
         t_cpu = cpu_frame_time(occ)
         cpu = {"value": 1.0 / t_cpu, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
@@ -433,6 +477,8 @@ def run_ours(args):
         line["train_config5"] = train
     if frox is not None:
         line["froxelize"] = frox
+    if gtp is not None:
+        line["gt_pvs"] = gtp
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -447,7 +493,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the config-5 training-step line")
-    ap.add_argument("--no-froxelize", action="store_true", help="skip the froxelization side line")
+    ap.add_argument("--no-froxelize", action="store_true", help="skip the froxelization / GT-PVS side lines")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
