@@ -77,6 +77,8 @@ struct Work {
   long long* pairs;               // kMode 2: (froxel * T + triangle) per fragment
   unsigned long long* npairs;
   long long pair_cap;
+  double* ufx;  // GT mode: 2 (px + 0.5) / W - 1 per pixel column (core.py:441), nullptr otherwise
+  double* ufy;
   long long ntris;
   int nb;
 };
@@ -253,6 +255,12 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(Params p, const fp
 
 __global__ void __launch_bounds__(1024) scan_kernel(Params p, Work wk) {
   // pixel column/row -> froxel index, exactly quantize((px + 0.5) / sx) (froxel.py:28-42, 345-346)
+  if (wk.ufx) {
+    for (int i = threadIdx.x; i < (int)p.sx; i += 1024)
+      wk.ufx[i] = dsub(ddiv(dmul(2.0, dadd((double)i, 0.5)), p.sx), 1.0);
+    for (int i = threadIdx.x; i < (int)p.sy; i += 1024)
+      wk.ufy[i] = dsub(ddiv(dmul(2.0, dadd((double)i, 0.5)), p.sy), 1.0);
+  }
   for (int i = threadIdx.x; i < p.isx; i += 1024)
     wk.tabx[i] = min(max((int)floor(dmul(ddiv(dadd((double)i, 0.5), p.sx), (double)p.nx)), 0), p.nx - 1);
   for (int i = threadIdx.x; i < p.isy; i += 1024)
@@ -370,6 +378,15 @@ __device__ __forceinline__ int sample_fast(const Slot& s, double cx, double cy, 
   const double mt = mw * (double)nz + 1e-15 * t;
   if (w <= mw || w >= 1.0 - mw || t - f <= mt || f + 1.0 - t <= mt) return sample_exact(s, cx, cy, nz);
   return min(max((int)f, 0), nz - 1);
+}
+
+// OR bits into a grid word, skipping the atomic when a (possibly stale, L1)
+// read already shows them: bits are only ever set during a pass, so a set
+// bit in any copy is set in memory, and a miss just costs the atomic.  Most
+// fragments hit froxels other fragments already marked; the contended
+// same-address atomics at L2 were the cost.
+__device__ __forceinline__ void or_bits(unsigned int* w, unsigned int bits) {
+  if ((*reinterpret_cast<volatile unsigned int*>(w) & bits) != bits) atomicOr(w, bits);
 }
 
 // (double)px + 0.5 without the int->fp64 converter: 2^52 + px from the bit
@@ -810,31 +827,63 @@ __global__ void __launch_bounds__(kRasterThreads, 4)
   }
 }
 
+// quantize (froxel.py:28-42) of an in-range test on an approximate NDC value
+// a whose error is far below m: -1 = certainly outside [0, 1], index = certain
+// froxel, -2 = within m of a decision boundary (0, 1, k/n): evaluate exactly.
+__device__ __forceinline__ int quant_fast(double a, int n, double m) {
+  if (!(a >= -m && a <= 1.0 + m)) return -1;
+  if (a <= m || a >= 1.0 - m) return -2;
+  const double t = a * (double)n, f = floor(t);
+  const double mt = m * (double)n;
+  if (t - f <= mt || f + 1.0 - t <= mt) return -2;
+  return min(max((int)f, 0), n - 1);
+}
+
+__device__ __forceinline__ int quant_exact(double a, int n) {
+  if (!(a >= 0 && a <= 1)) return -1;
+  return min(max((int)floor(dmul(a, (double)n)), 0), n - 1);
+}
+
 // Covered pixel -> world -> viewcell frustum -> froxel bit (core.py:380-452).
+// The world point is the reference's exact float64 sequence; the three NDC
+// divisions go through one approximate reciprocal and are redone exactly
+// only for points within 1e-12 of an inside/outside or froxel boundary.
 __global__ void __launch_bounds__(256) resolve_kernel(GtParams g, const fpvs_frustum* __restrict__ views,
                                                       int nviews, const unsigned long long* __restrict__ zbuf,
                                                       const long long* __restrict__ pidbuf,
+                                                      const double* __restrict__ ufx, const double* __restrict__ ufy,
                                                       unsigned int* __restrict__ gt_words,
                                                       unsigned int* __restrict__ geo_words) {
-  const long long n = (long long)nviews * g.npix;
+  const unsigned int npix = (unsigned int)g.npix, iw = (unsigned int)g.iw;
+  const unsigned int wmag = iw > 1 ? (unsigned int)((0x100000000ull + iw - 1) / iw) : 0xffffffffu;
   const unsigned int row = (unsigned int)(g.nx >> 3);
   const int lane = threadIdx.x & 31;
-  for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += (long long)gridDim.x * blockDim.x) {
-    const long long i = base + threadIdx.x;
+  const double rfn = 1.0 / dsub(g.ffar, g.fnear);
+  constexpr double kM = 1e-12;
+  // (view, pixel) walk in 32-bit pixel arithmetic; the warp-uniform bound keeps
+  // every lane in the ballot below
+  const unsigned int per_view_steps = (npix + blockDim.x - 1) / blockDim.x;
+  const unsigned int nsteps = (unsigned int)nviews * per_view_steps;  // < 2^32 (checked by the entry)
+  for (unsigned int stp = blockIdx.x; stp < nsteps; stp += gridDim.x) {
+    const int v = (int)(stp / per_view_steps);
+    const unsigned int p = (stp - (unsigned int)v * per_view_steps) * blockDim.x + threadIdx.x;
+    const long long i = (long long)v * g.npix + p;
     bool valid = false;
     unsigned int word = 0, bit = 0;
-    if (i < n) {
+    if (p < npix) {
       const unsigned long long zb = zbuf[i];
       valid = zb != ~0ull && (pidbuf == nullptr || pidbuf[i] >= 0);
       if (valid) {
-        const int v = (int)(i / g.npix);
-        const long long p = i - (long long)v * g.npix;
-        const int py = (int)(p / g.iw), px = (int)(p - (long long)py * g.iw);
+        unsigned int py = __umulhi(p, wmag);
+        const int rem = (int)(p - py * iw);
+        if (rem < 0) --py;
+        else if (rem >= (int)iw) ++py;
+        const int px = (int)(p - py * iw);
         const fpvs_frustum& c = views[v];
         const double z = __longlong_as_double((long long)zb);
         // x = (2 (px + 0.5) / W - 1) h z   (core.py:441-442)
-        const double x = dmul(dmul(dsub(ddiv(dmul(2.0, centre(px)), g.W), 1.0), c.half_extent), z);
-        const double y = dmul(dmul(dsub(ddiv(dmul(2.0, centre(py)), g.H), 1.0), c.half_extent), z);
+        const double x = dmul(dmul(__ldg(ufx + px), c.half_extent), z);
+        const double y = dmul(dmul(__ldg(ufy + py), c.half_extent), z);
         // world = position + [x y z] @ basis (dgemm k = 3 order), core.py:443-446
         double wv[3];
 #pragma unroll
@@ -847,15 +896,17 @@ __global__ void __launch_bounds__(256) resolve_kernel(GtParams g, const fpvs_fru
         valid = lz > 0;
         if (valid) {
           const double zh = dmul(lz, g.fh);
-          const double u = dadd(0.5, ddiv(dmul(0.5, lx), zh));
-          const double vv = dadd(0.5, ddiv(dmul(0.5, ly), zh));
-          const double w = g.depth_log ? ddiv(log(ddiv(lz, g.fnear)), g.flogr)
-                                       : ddiv(dsub(lz, g.fnear), dsub(g.ffar, g.fnear));
-          valid = u >= 0 && u <= 1 && vv >= 0 && vv <= 1 && w >= 0 && w <= 1;
+          const double r = rcp_nr(zh);
+          int ix = quant_fast(0.5 + (0.5 * lx) * r, g.nx, kM);
+          int iy = ix == -1 ? -1 : quant_fast(0.5 + (0.5 * ly) * r, g.ny, kM);
+          int iz = (ix == -1 || iy == -1 || g.depth_log) ? -2 : quant_fast((lz - g.fnear) * rfn, g.nz, kM);
+          if (ix == -2) ix = quant_exact(dadd(0.5, ddiv(dmul(0.5, lx), zh)), g.nx);
+          if (iy == -2) iy = quant_exact(dadd(0.5, ddiv(dmul(0.5, ly), zh)), g.ny);
+          if (iz == -2 && ix >= 0 && iy >= 0)
+            iz = quant_exact(g.depth_log ? ddiv(log(ddiv(lz, g.fnear)), g.flogr)
+                                         : ddiv(dsub(lz, g.fnear), dsub(g.ffar, g.fnear)), g.nz);
+          valid = ix >= 0 && iy >= 0 && iz >= 0;
           if (valid) {
-            const int ix = min(max((int)floor(dmul(u, (double)g.nx)), 0), g.nx - 1);
-            const int iy = min(max((int)floor(dmul(vv, (double)g.ny)), 0), g.ny - 1);
-            const int iz = min(max((int)floor(dmul(w, (double)g.nz)), 0), g.nz - 1);
             const unsigned long long byte = (unsigned long long)(ix >> 3) +
                                             (unsigned long long)row * ((unsigned long long)iy + (unsigned long long)g.ny * iz);
             word = (unsigned int)(byte >> 2);
@@ -871,12 +922,12 @@ __global__ void __launch_bounds__(256) resolve_kernel(GtParams g, const fpvs_fru
       if (__all_sync(0xffffffffu, !valid || word == w0)) {
         const unsigned int bits = __reduce_or_sync(0xffffffffu, valid ? bit : 0u);
         if (lane == leader) {
-          atomicOr(gt_words + w0, bits);
-          if (geo_words) atomicOr(geo_words + w0, bits);
+          or_bits(gt_words + w0, bits);
+          if (geo_words) or_bits(geo_words + w0, bits);
         }
       } else if (valid) {
-        atomicOr(gt_words + word, bit);
-        if (geo_words) atomicOr(geo_words + word, bit);
+        or_bits(gt_words + word, bit);
+        if (geo_words) or_bits(geo_words + word, bit);
       }
     }
   }
@@ -895,8 +946,10 @@ __global__ void depth_out_kernel(long long n, const unsigned long long* __restri
 }
 
 struct GtLayout {
-  size_t total, slots, lp, bsum, bpre, zbuf, pid, bytes;
+  size_t total, slots, lp, bsum, bpre, zbuf, pid, ufx, ufy, bytes;
 };
+
+constexpr int kMaxRes = 1 << 15;  // depth-buffer width / height bound of the pixel tables
 
 inline GtLayout gt_layout(long long ntris, int nviews, long long npix, bool with_pids) {
   GtLayout L;
@@ -911,6 +964,8 @@ inline GtLayout gt_layout(long long ntris, int nviews, long long npix, bool with
   L.bpre = o;  o = up256(o + (size_t)nb * 8);
   L.zbuf = o;  o = up256(o + (size_t)nviews * (size_t)npix * 8);
   L.pid = o;   o = up256(o + (with_pids ? (size_t)nviews * (size_t)npix * 8 : 0));
+  L.ufx = o;   o = up256(o + (size_t)npix * 0 + 8 * (size_t)kMaxRes);
+  L.ufy = o;   o = up256(o + 8 * (size_t)kMaxRes);
   L.bytes = o;
   return L;
 }
@@ -931,10 +986,12 @@ extern "C" int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t*
   FPVS_CHECK_ARG(fr != nullptr && gt_bits != nullptr, "gt_pvs: null frustum or output");
   FPVS_CHECK_ARG(Nx > 0 && Ny > 0 && Nz > 0 && Nx % 8 == 0, "N_x must be divisible by 8, got %d", Nx);
   FPVS_CHECK_ARG(res_w >= Nx && res_h >= Ny, "depth buffer must be at least the grid cross-section");
-  FPVS_CHECK_ARG((long long)res_w * res_h < (1LL << 32) && res_w < (1 << 30) && res_h < (1 << 30),
+  FPVS_CHECK_ARG((long long)res_w * res_h < (1LL << 32) && res_w <= kMaxRes && res_h <= kMaxRes,
                  "gt_pvs: depth buffer %d x %d too large", res_w, res_h);
   FPVS_CHECK_ARG(depth_mode == FPVS_DEPTH_LINEAR || depth_mode == FPVS_DEPTH_LOG, "bad depth mode %d", depth_mode);
   FPVS_CHECK_ARG(ncams >= 0 && (ncams == 0 || cams != nullptr), "gt_pvs: bad camera array");
+  FPVS_CHECK_ARG((long long)ncams * (((long long)res_w * res_h + 255) / 256) < (1LL << 32),
+                 "gt_pvs: too many cameras for one call (%d)", ncams);
   FPVS_CHECK_ARG(ntris >= 0 && nverts >= 0 && (ntris == 0 || (verts && tris)), "gt_pvs: bad scene arrays");
   FPVS_CHECK_ARG(fr->near_z > 0 && fr->near_z < fr->far_z && fr->half_extent > 0, "need 0 < near < far");
   const long long grid_bytes = (long long)Nx * Ny * Nz / 8;
@@ -956,6 +1013,8 @@ extern "C" int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t*
   wk.total = reinterpret_cast<unsigned long long*>(ws + L.total);
   wk.out_words = nullptr;
   wk.tabx = wk.taby = nullptr;
+  wk.ufx = reinterpret_cast<double*>(ws + L.ufx);
+  wk.ufy = reinterpret_cast<double*>(ws + L.ufy);
   wk.ntris = ntris * ncams;
   wk.nb = (int)((2 * wk.ntris + kSlotsPerBlock - 1) / kSlotsPerBlock);
   unsigned long long* zbuf = reinterpret_cast<unsigned long long*>(ws + L.zbuf);
@@ -1003,7 +1062,8 @@ extern "C" int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t*
     depth_kernel<1><<<kNumSMs * per_sm, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
     FPVS_CHECK_LAUNCH("gt_pvs prim ids");
   }
-  resolve_kernel<<<kNumSMs * 8, 256, 0, s>>>(g, cams, ncams, zbuf, pidbuf, reinterpret_cast<unsigned int*>(gt_bits),
+  resolve_kernel<<<kNumSMs * 8, 256, 0, s>>>(g, cams, ncams, zbuf, pidbuf, wk.ufx, wk.ufy,
+                                             reinterpret_cast<unsigned int*>(gt_bits),
                                              reinterpret_cast<unsigned int*>(geometry_bits));
   FPVS_CHECK_LAUNCH("gt_pvs resolve");
   return FPVS_OK;

@@ -270,7 +270,7 @@ def pick_bn(cout: int, rows: int, sms: int = 148) -> int:
     mtiles = max(1, (rows + 127) // 128)
     # splitting N re-gathers A once per column block; measured on B200 it only
     # pays when the layer has well under half a wave of row tiles
-    while bn > 64 and mtiles * ((cout + bn - 1) // bn) < sms // 4:
+    while bn > 64 and mtiles * ((cout + bn - 1) // bn) < sms // 2:
         bn //= 2
     return bn
 

@@ -203,54 +203,67 @@ class FramePipeline:
         host_out.copy_(self.out_bits, non_blocking=True)
         return host_out
 
-    # -- streaming: overlap frame i's compute with frame i+1's upload and
-    # frame i-1's download (double-buffered device grids, one graph each) ----
-    def _ensure_streaming(self):
-        if getattr(self, "_stream_bufs", None) is not None:
+    # -- streaming: frames in flight on separate compute streams ------------
+    # Lane k (k < inflight) is a FramePipeline with its own buffers, CUDA graph
+    # and compute stream (lane 0 is this one); frame i runs on lane i % inflight.
+    # Uploads and downloads go through two shared copy streams, so frame i's
+    # compute overlaps frame i+1's upload, frame i-1's download and, with
+    # inflight >= 2, the other lanes' compute: the level-1/2 convs leave SMs
+    # idle (111 and 29 row tiles for 148 SMs) that the next frame fills.
+    def _ensure_streaming(self, inflight: int):
+        lanes = getattr(self, "_lanes", None)
+        if lanes is not None and len(lanes) == inflight:
             return
         torch = _torch()
         if self.graph is None:
             self.capture(tune=False)
-        in2, out2 = torch.zeros_like(self.in_bits), torch.zeros_like(self.out_bits)
-        self.plan.run(in2, out2, self.tau)
-        torch.cuda.synchronize()
-        g2 = self._capture(in2, out2) if self._use_graph else None
-        self._stream_bufs = [(self.in_bits, self.out_bits, self.graph), (in2, out2, g2)]
+        pipes = [self]
+        for _ in range(1, inflight):
+            p = FramePipeline(self.net, self.B, self.grid_dims, self.tau, graph=self._use_graph)
+            p.in_bits.copy_(self.in_bits)
+            p.capture()
+            pipes.append(p)
+        self._lanes = [{"pipe": p, "comp": torch.cuda.Stream(), "h2d": torch.cuda.Event(),
+                        "done": torch.cuda.Event(), "d2h": torch.cuda.Event()} for p in pipes]
         self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
-        self._ev = {k: [torch.cuda.Event(), torch.cuda.Event()] for k in ("h2d", "comp", "d2h")}
 
-    def infer_stream(self, host_ins, host_outs):
+    def infer_stream(self, host_ins, host_outs, inflight: int = 2):
         """Frames ``host_ins[i]`` (pinned packed grids) -> ``host_outs[i]`` (pinned).
 
-        Every frame is uploaded, run and downloaded; the upload of frame i+1
-        and the download of frame i-1 run on copy streams while frame i
-        computes.  Enqueues on the current stream (which joins the copy
-        streams at the end); the caller synchronises."""
+        Every frame is uploaded, run and downloaded; up to ``inflight`` frames
+        compute concurrently (separate buffers), copies overlap compute.
+        Enqueues relative to the current stream (which joins every stream used
+        at the end); the caller synchronises."""
         torch = _torch()
-        self._ensure_streaming()
-        comp = torch.cuda.current_stream()
-        ev = self._ev
-        for b in range(2):
-            ev["comp"][b].record(comp)
-            ev["d2h"][b].record(comp)
+        self._ensure_streaming(max(1, int(inflight)))
+        cur = torch.cuda.current_stream()
+        lanes = self._lanes
+        for ln in lanes:
+            ln["done"].record(cur)
+            ln["d2h"].record(cur)
+        self._h2d.wait_stream(cur)
+        self._d2h.wait_stream(cur)
         for i, (hin, hout) in enumerate(zip(host_ins, host_outs)):
-            b = i % 2
-            din, dout, g = self._stream_bufs[b]
-            self._h2d.wait_event(ev["comp"][b])  # frame i-2 no longer reads din
+            ln = lanes[i % len(lanes)]
+            p, comp = ln["pipe"], ln["comp"]
+            self._h2d.wait_event(ln["done"])  # the lane's previous frame no longer reads in_bits
             with torch.cuda.stream(self._h2d):
-                din.copy_(torch.as_tensor(hin), non_blocking=True)
-            ev["h2d"][b].record(self._h2d)
-            comp.wait_event(ev["h2d"][b])
-            comp.wait_event(ev["d2h"][b])  # frame i-2's result has left dout
-            if g is not None:
-                g.replay()
-            else:
-                self.plan.run(din, dout, self.tau)
-            ev["comp"][b].record(comp)
-            self._d2h.wait_event(ev["comp"][b])
+                p.in_bits.copy_(torch.as_tensor(hin), non_blocking=True)
+            ln["h2d"].record(self._h2d)
+            comp.wait_event(ln["h2d"])
+            comp.wait_event(ln["d2h"])  # the lane's previous result has left out_bits
+            with torch.cuda.stream(comp):
+                if p.graph is not None:
+                    p.graph.replay()
+                else:
+                    p.plan.run(p.in_bits, p.out_bits, p.tau)
+            ln["done"].record(comp)
+            self._d2h.wait_event(ln["done"])
             with torch.cuda.stream(self._d2h):
-                hout.copy_(dout, non_blocking=True)
-            ev["d2h"][b].record(self._d2h)
-        comp.wait_stream(self._d2h)
-        comp.wait_stream(self._h2d)
+                hout.copy_(p.out_bits, non_blocking=True)
+            ln["d2h"].record(self._d2h)
+        for ln in lanes:
+            cur.wait_stream(ln["comp"])
+        cur.wait_stream(self._d2h)
+        cur.wait_stream(self._h2d)
         return host_outs

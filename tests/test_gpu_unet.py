@@ -86,3 +86,30 @@ def test_unet_config2_full_size():
     print(f"cfg2: logits max-abs {err:.3g}, mask diffs {soft} (outside band {hard}), visible {vis}")
     assert err <= BF16_LOGIT_TOL, err
     assert hard == 0, (hard, soft)
+
+
+@pytest.mark.parametrize("inflight", [1, 2, 3])
+def test_streamed_frames_match_eager(inflight):
+    """FramePipeline.infer_stream: every streamed frame (distinct inputs, up to
+    ``inflight`` computing concurrently on separate buffers) equals the eager frame."""
+    import torch
+    from paper_2509_24677_b200 import synth
+    from paper_2509_24677_b200.froxel import FroxelGrid
+    from paper_2509_24677_b200.pipeline import FramePipeline
+    from paper_2509_24677_b200.unet import PvsUNet
+    dims = (64, 64, 64)
+    frames = [FroxelGrid.from_dense(synth.box_grid(dims, 40 + 7 * k, 1, 8, 10 + k)).bits for k in range(5)]
+    ins = [torch.from_numpy(b).pin_memory() for b in frames]
+    outs = [torch.empty(len(frames[0]), dtype=torch.uint8, pin_memory=True) for _ in range(7)]
+    net = PvsUNet(seed=1, precision="bf16")
+    pipe = FramePipeline(net, 1, dims, graph=True)
+    pipe.load(ins[0].cuda())
+    pipe.capture()
+    seq = [ins[i % len(ins)] for i in range(7)]
+    pipe.infer_stream(seq, outs, inflight=inflight)
+    torch.cuda.synchronize()
+    ref = FramePipeline(net, 1, dims, graph=False)
+    for i, x in enumerate(seq):
+        ref.plan.run(x.cuda(), ref.out_bits, 0.5)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[i], ref.out_bits.cpu()), i

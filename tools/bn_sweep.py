@@ -1,4 +1,4 @@
-"""Per-layer output-tile width sweep on the cfg2 frame (device stage times)."""
+"""Device time of the down/up convs of the config-2 frame over tile widths bn."""
 import os
 import sys
 
@@ -13,17 +13,24 @@ from paper_2509_24677_b200.unet import PvsUNet  # noqa: E402
 occ = synth.config2_grid(1)
 bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
 net = PvsUNet(seed=1, precision="bf16")
-plan = net.plan(1, occ.shape)
 out = torch.empty(occ.size // 8, dtype=torch.uint8, device="cuda")
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+plan = net.plan(1, occ.shape)
 plan.tune(bits)
+print("auto bn", {k: v for k, v in plan.bn.items() if k.startswith(("down", "up"))}, flush=True)
 base = dict(plan.bn)
-print("tuned", base, plan.counts())
-res = {}
-for bn in (32, 64, 128, 256):
-    plan.bn = {k: bn for k in base}
-    plan.run(bits, out, 0.5)
-    t = device_stage_times(plan, bits, out)
-    res[bn] = t
-    print(bn, {k: round(v * 1000, 1) for k, v in t.items() if k in base})
-best = {k: min((res[b][k], b) for b in res) for k in base}
-print("best", {k: (b, round(v * 1000, 1)) for k, (v, b) in best.items()})
+for name in ("down01", "down12", "up21", "up10"):
+    for bn in (32, 64, 128, 256):
+        cout = plan.net.layers[name].spec.out_channels
+        if bn > 256 or bn > max(cout, 32) * 2:
+            continue
+        plan.bn = dict(base)
+        plan.bn[name] = bn
+        try:
+            plan.run(bits, out, 0.5)
+            torch.cuda.synchronize()
+            t = device_stage_times(plan, bits, out, flush=flush)
+            print(f"{name} bn={bn}: {t[name] * 1000:.2f} us", flush=True)
+        except Exception as e:  # noqa: BLE001
+            print(f"{name} bn={bn}: {type(e).__name__} {e}", flush=True)
+plan.bn = base
