@@ -15,14 +15,21 @@
 // through the BLAS dgemm kernel, which accumulates the k = 3 dot product as
 // fma(d2, b2, fma(d1, b1, d0 * b0)); cam_xyz() restates that order.
 //
-// Kernels (one stream, three launches after the output memset):
+// Kernels (one stream, three launches after the output memset; the span
+// raster below replaced the whole-bounding-box raster as the default, which
+// stays selectable with FPVS_FROX_SPANS=0 for A/B checks):
 //  1. setup: one thread per scene triangle -> up to two clipped screen
 //     triangles (slots 2t, 2t+1) with their edge/depth constants and pixel
 //     bounding box; each CTA also scans its 512 slots' sample counts
 //     (bbox area) into a block-local inclusive prefix + the block total.
 //  2. scan: one CTA turns the block totals into exclusive block offsets and
 //     the grand total of candidate samples.
-//  3. raster: persistent CTAs walk the flat sample space in 2048-sample
+//  3. span raster (span_kernel): work items are bounding-box rows cut into
+//     16-column segments (64 for the GT z-buffer); a warp bounds its 32
+//     items' candidate columns by the three edge functions (row_span,
+//     conservative) and expands them into samples 32 at a time, so samples
+//     outside the triangle are never evaluated.
+//     Whole-box raster (raster_kernel): persistent CTAs walk the flat sample space in 2048-sample
 //     chunks; each thread finds its slot by a two-level binary search
 //     (block offsets, then the block-local prefix), caches the slot's
 //     constants while consecutive samples stay inside it, evaluates the
@@ -61,6 +68,8 @@ struct Params {
   int isx, isy;
   int nx, ny, nz;
   int depth_log;
+  int rows_mode;  // 1: the flat work space counts bounding-box row segments (span raster), 0: samples
+  int seg;        // span raster: columns per work item
 };
 
 struct Work {
@@ -69,6 +78,7 @@ struct Work {
   unsigned long long* bsum;  // [nb]
   unsigned long long* bpre;  // [nb] exclusive block offsets
   unsigned long long* total;
+  unsigned long long* nsamples;  // candidate samples (bbox areas), next to total
   unsigned int* out_words;
   int* tabx;  // froxel column of supersampled pixel column px (quantize of (px+0.5)/sx)
   int* taby;
@@ -227,6 +237,30 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(Params p, const fp
   if (t < wk.ntris) {
     if (c0) wk.slots[2 * t] = s0;
     if (c1) wk.slots[2 * t + 1] = s1;
+  }
+  {
+    // candidate samples (bbox areas) for the statistics counter
+    unsigned long long smp = c0 + c1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) smp += __shfl_xor_sync(0xffffffffu, smp, o);
+    if ((threadIdx.x & 31) == 0 && smp) atomicAdd(wk.nsamples, smp);
+  }
+  if (p.rows_mode) {
+    // the span raster's work items: bounding-box rows cut into p.seg-column
+    // segments (h * ceil(w / seg) per slot); wmagic becomes the segment
+    // count's reciprocal for the item -> (row, segment) split
+    if (c0) {
+      const unsigned int ns = (unsigned int)(s0.w + p.seg - 1) / (unsigned int)p.seg;
+      c0 = (unsigned long long)s0.h * ns;
+      s0.wmagic = ns > 1 ? (unsigned int)((0x100000000ull + ns - 1) / ns) : 0xffffffffu;
+      if (t < wk.ntris) wk.slots[2 * t].wmagic = s0.wmagic;
+    }
+    if (c1) {
+      const unsigned int ns = (unsigned int)(s1.w + p.seg - 1) / (unsigned int)p.seg;
+      c1 = (unsigned long long)s1.h * ns;
+      s1.wmagic = ns > 1 ? (unsigned int)((0x100000000ull + ns - 1) / ns) : 0xffffffffu;
+      if (t < wk.ntris) wk.slots[2 * t + 1].wmagic = s1.wmagic;
+    }
   }
   // block scan of (c0 + c1)
   __shared__ unsigned long long warp_tot[kSetupThreads / 32];
@@ -502,6 +536,252 @@ __global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(Params p, Wor
   }
 }
 
+struct GtParams {
+  double fo[3], fb[9];
+  double fh, fnear, ffar, flogr;  // flogr = log(far / near), computed like math.log on the host
+  double W, H;
+  int iw, ih;
+  int nx, ny, nz, depth_log;
+  long long T;     // scene triangles (per camera)
+  long long npix;  // W * H
+};
+
+// Reference depth of one sample (froxel.py:272-279 coverage; oracle.py:127
+// depth = 1 / interp_affine(invz, b1, b2)); < 0 when not covered.
+__device__ __forceinline__ double depth_exact(const Slot& s, double cx, double cy) {
+  const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
+  const double b1 = ddiv(dsub(dmul(dx, s.e2y), dmul(s.e2x, dy)), s.den);
+  const double b2 = ddiv(dsub(dmul(s.e1x, dy), dmul(dx, s.e1y)), s.den);
+  const double b0 = dsub(dsub(1.0, b1), b2);
+  if (!(b0 >= 0 && b1 >= 0 && b2 >= 0)) return -1.0;
+  return ddiv(1.0, dadd(dadd(s.iz0, dmul(b1, dsub(s.iz1, s.iz0))), dmul(b2, dsub(s.iz2, s.iz0))));
+}
+
+// Coverage filter before the exact evaluation: samples provably outside
+// (exact numerator signs, or b0 < 0 by more than the approximation error)
+// skip the three divisions.
+__device__ __forceinline__ double depth_filtered(const Slot& s, double cx, double cy) {
+  const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
+  const double n1 = dsub(dmul(dx, s.e2y), dmul(s.e2x, dy));
+  const double n2 = dsub(dmul(s.e1x, dy), dmul(dx, s.e1y));
+  const bool dneg = s.den < 0;
+  const double a1 = fabs(n1), a2 = fabs(n2);
+  constexpr double kTiny = 1e-250;
+  if (!((a1 != 0 && a1 < kTiny) || (a2 != 0 && a2 < kTiny))) {
+    if ((n1 != 0 && ((n1 < 0) != dneg)) || (n2 != 0 && ((n2 < 0) != dneg))) return -1.0;
+    const double q1 = n1 * s.rden, q2 = n2 * s.rden;
+    if ((1.0 - q1) - q2 < -1e-13 * (1.0 + q1 + q2)) return -1.0;
+  }
+  return depth_exact(s, cx, cy);
+}
+
+// ---------------------------------------------------------------------------
+// Span raster.  The flat work space counts bounding-box ROWS; a warp takes
+// 32 rows at a time (lane = row), bounds each row's candidate columns with
+// row_span, and expands the rows' spans into samples 32 at a time (lane =
+// sample, its row found by a 5-step search over the warp's span prefix).
+// Only samples inside the spans are evaluated (by the same exact / filtered
+// per-sample code), so the outside half of every bounding box costs nothing.
+// ---------------------------------------------------------------------------
+
+// Conservative candidate columns [xa, xb) of bounding-box row py: each edge's
+// sign condition is linear in the pixel centre cx (f = a cx + b >= 0, sign-
+// normalised by den); columns are dropped only where an edge value is below
+// -tol, with tol ~1e-9 of the magnitudes (its rounding error is ~1e-16 of
+// them), and one pixel of margin is kept on either side.
+__device__ __forceinline__ void row_span(const Slot& s, int py, int& xa, int& xb) {
+  const double dy = centre(py) - s.v0y;
+  const double sg = s.den < 0 ? -1.0 : 1.0;
+  double lo = s.x0 + 0.5, hi = s.x0 + s.w - 0.5;
+  const double M = fmax(fabs(lo), fabs(hi)) + 1.0;
+  const double a1 = sg * s.e2y, b1 = -sg * (s.e2y * s.v0x + s.e2x * dy);
+  const double a2 = -sg * s.e1y, b2 = sg * (s.e1x * dy + s.e1y * s.v0x);
+  const double a0 = -(a1 + a2), b0 = fabs(s.den) - b1 - b2;
+  const double t1 = 1e-9 * (fabs(a1) * M + fabs(b1)), t2 = 1e-9 * (fabs(a2) * M + fabs(b2));
+  const double t0 = t1 + t2 + 1e-9 * fabs(s.den);
+  const double a[3] = {a0, a1, a2}, b[3] = {b0, b1, b2}, tl[3] = {t0, t1, t2};
+  bool empty = false;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (a[k] > 0) lo = fmax(lo, (-tl[k] - b[k]) / a[k]);
+    else if (a[k] < 0) hi = fmin(hi, (-tl[k] - b[k]) / a[k]);
+    else empty |= b[k] < -tl[k];
+  }
+  xa = s.x0;
+  xb = s.x0 + s.w;
+  if (empty || lo > hi + 2.0) {
+    xb = xa;
+    return;
+  }
+  if (isfinite(lo)) xa = max(xa, (int)fmax(ceil(lo - 1.5), (double)s.x0));
+  if (isfinite(hi)) xb = min(xb, (int)fmin(floor(hi + 0.5) + 1.0, (double)(s.x0 + s.w)));
+  if (xb < xa) xb = xa;
+}
+
+constexpr int kSpanRowsPerThread = 2;
+constexpr int kSpanChunk = kRasterThreads * kSpanRowsPerThread;
+
+// kKind 0: OR bits (froxelize), 1: cull marks, 2: (froxel, triangle) pairs,
+// 3: z-buffer min (GT), 4: smallest primitive id among z-ties (GT).
+template <bool kFilter, int kKind>
+__global__ void __launch_bounds__(kRasterThreads, 3)
+    span_kernel(Params p, GtParams g, const fpvs_frustum* __restrict__ views, const int64_t* __restrict__ prim_ids,
+                Work wk, unsigned long long* __restrict__ zbuf, long long* __restrict__ pidbuf) {
+  constexpr int kWarpRows = 32 * kSpanRowsPerThread;
+  constexpr bool kDepth = kKind >= 3;
+  const unsigned long long total = *wk.total;  // rows
+  const unsigned int row = (unsigned int)(p.nx >> 3);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long have = -1;  // slot whose constants are in s
+  Slot s;
+  double farz = 0;
+  long long zoff = 0;
+  for (unsigned long long c0 = (unsigned long long)blockIdx.x * kSpanChunk; c0 < total;
+       c0 += (unsigned long long)gridDim.x * kSpanChunk) {
+    const unsigned long long wbase = c0 + (unsigned long long)warp * kWarpRows;
+    if (wbase >= total) break;  // warp-uniform
+    unsigned long long cs = 0;
+    long long cur = 0;
+    if (lane == 0) cur = find_slot(wk, wbase, cs);
+    cur = __shfl_sync(0xffffffffu, cur, 0);
+    cs = __shfl_sync(0xffffffffu, cs, 0);
+    unsigned long long ce = slot_end(wk, cur);
+#pragma unroll 1
+    for (int k = 0; k < kSpanRowsPerThread; ++k) {
+      // ---- lane = row: its slot, pixel row and candidate span
+      const unsigned long long r = wbase + (unsigned long long)(k * 32 + lane);
+      long long mine = cur;
+      int py = 0, xa = 0, len = 0;
+      if (r < total) {
+        unsigned long long ms = cs, me = ce;
+        int steps = 0;
+        while (r >= me && steps < 4) {
+          ms = me;
+          me = slot_end(wk, ++mine);
+          ++steps;
+        }
+        if (r >= me) {
+          mine = find_slot(wk, r, ms);
+          me = slot_end(wk, mine);
+        }
+        if (mine != have) {
+          s = wk.slots[mine];
+          have = mine;
+          if (kDepth) {
+            farz = views[s.pad].far_z;
+            zoff = (long long)s.pad * g.npix;
+          }
+        }
+        // item -> (bounding-box row, p.seg-column segment)
+        const unsigned int it = (unsigned int)(r - ms);
+        const unsigned int ns = (unsigned int)(s.w + p.seg - 1) / (unsigned int)p.seg;
+        unsigned int ry = __umulhi(it, s.wmagic);
+        const int rem = (int)(it - ry * ns);
+        if (rem < 0) --ry;
+        else if (rem >= (int)ns) ++ry;
+        const int seg = (int)(it - ry * ns);
+        py = s.y0 + (int)ry;
+        int xb;
+        row_span(s, py, xa, xb);
+        xa = max(xa, s.x0 + seg * p.seg);
+        xb = min(xb, s.x0 + seg * p.seg + p.seg);
+        len = max(xb - xa, 0);
+      }
+      const long long nxt = __shfl_sync(0xffffffffu, mine, 31);
+      // ---- warp prefix of span lengths
+      int incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      // ---- lane = sample
+      for (int t0 = 0; t0 < tot; t0 += 32) {
+        const int t = t0 + lane;
+        int kr = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int v = __shfl_sync(0xffffffffu, incl, kr + step - 1);
+          if (v <= t) kr += step;
+        }
+        const long long sl = __shfl_sync(0xffffffffu, mine, kr);
+        const int spy = __shfl_sync(0xffffffffu, py, kr);
+        const int sxa = __shfl_sync(0xffffffffu, xa, kr);
+        const int sex = __shfl_sync(0xffffffffu, incl, kr) - __shfl_sync(0xffffffffu, len, kr);
+        bool valid = t < tot;
+        unsigned int word = 0, bit = 0;
+        long long flat = 0;
+        if (valid) {
+          if (sl != have) {
+            s = wk.slots[sl];
+            have = sl;
+            if (kDepth) {
+              farz = views[s.pad].far_z;
+              zoff = (long long)s.pad * g.npix;
+            }
+          }
+          const int px = sxa + (t - sex);
+          const double cx = centre(px), cy = centre(spy);
+          if (kDepth) {
+            const double depth = depth_filtered(s, cx, cy);
+            valid = false;
+            if (depth >= 0 && depth <= farz) {  // oracle.py:128
+              const long long pix = zoff + (long long)spy * g.iw + px;
+              const unsigned long long bits = (unsigned long long)__double_as_longlong(depth);
+              if (kKind == 3) {
+                atomicMin(zbuf + pix, bits);
+              } else if (bits == zbuf[pix]) {
+                const long long tri = (sl >> 1) - (long long)s.pad * g.T;
+                atomicMin(pidbuf + pix, prim_ids ? prim_ids[tri] : tri);
+              }
+            }
+          } else {
+            const int iz = kFilter ? sample_fast(s, cx, cy, p.nz) : sample_exact(s, cx, cy, p.nz);
+            valid = iz >= 0;
+            if (valid) {
+              const int ix = __ldg(wk.tabx + px), iy = __ldg(wk.taby + spy);
+              const unsigned long long byte = (unsigned long long)(ix >> 3) +
+                                              (unsigned long long)row * ((unsigned long long)iy + (unsigned long long)p.ny * iz);
+              word = (unsigned int)(byte >> 2);
+              bit = 1u << ((((unsigned int)byte & 3u) << 3) | ((unsigned int)ix & 7u));
+              if (kKind == 2) flat = ix + (long long)p.nx * (iy + (long long)p.ny * iz);  // froxel.py:411
+            }
+          }
+        }
+        if (kKind == 0) {
+          const unsigned int vm = __ballot_sync(0xffffffffu, valid);
+          if (vm) {
+            const int leader = __ffs(vm) - 1;
+            const unsigned int w0 = __shfl_sync(0xffffffffu, word, leader);
+            if (__all_sync(0xffffffffu, !valid || word == w0)) {
+              const unsigned int bits = __reduce_or_sync(0xffffffffu, valid ? bit : 0u);
+              if (lane == leader) atomicOr(wk.out_words + w0, bits);
+            } else if (valid) {
+              atomicOr(wk.out_words + word, bit);
+            }
+          }
+        } else if (kKind == 1) {
+          if (valid && (__ldg(wk.pvs_words + word) & bit)) wk.kept[sl >> 1] = 1;
+        } else if (kKind == 2) {
+          const long long key = valid ? flat * wk.ntris + (sl >> 1) : -1 - lane;
+          const unsigned int peers = __match_any_sync(0xffffffffu, key);
+          if (valid && (__ffs(peers) - 1) == lane) {
+            const unsigned long long slot = atomicAdd(wk.npairs, 1ull);
+            if ((long long)slot < wk.pair_cap) wk.pairs[slot] = key;
+          }
+        }
+      }
+      // the warp's next rows start from the last lane's slot
+      if (nxt != cur) {
+        cur = nxt;
+        cs = (cur % kSlotsPerBlock ? slot_end(wk, cur - 1) : __ldg(wk.bpre + cur / kSlotsPerBlock));
+        ce = slot_end(wk, cur);
+      }
+    }
+  }
+}
+
 struct Layout {
   size_t slots, lp, bsum, bpre, total, tabx, taby, words, bytes;
 };
@@ -523,6 +803,21 @@ inline Layout layout(long long ntris, long long grid_bytes, long long sx, long l
   L.words = o; o = up256(o + (size_t)((grid_bytes + 3) & ~3LL));  // used only for unaligned outputs
   L.bytes = o;
   return L;
+}
+
+inline int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : dflt;
+  return v >= 8 && v <= 1024 ? v : dflt;
+}
+
+// FPVS_FROX_SPANS=0 rasterizes whole bounding boxes instead of row spans (A/B check)
+inline bool spans() {
+  static const bool f = [] {
+    const char* e = getenv("FPVS_FROX_SPANS");
+    return !(e && e[0] == '0');
+  }();
+  return f;
 }
 
 // FPVS_FROX_EXACT=1 evaluates every sample with the reference sequence (A/B check)
@@ -548,21 +843,29 @@ extern "C" size_t fpvs_froxelize_workspace_size(long long ntris, int Nx, int Ny,
 namespace fpvs {
 namespace frox {
 
+template <typename K>
+int occupancy_grid(K kernel) {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kRasterThreads, 0);
+  return kNumSMs * (n > 0 ? n : 1);
+}
+
 template <int kMode>
 int launch_raster(const Params& p, const Work& wk, cudaStream_t s) {
-  static const int per_sm[2] = {[] {
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, raster_kernel<false, kMode>, kRasterThreads, 0);
-    return n > 0 ? n : 1;
-  }(), [] {
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, raster_kernel<true, kMode>, kRasterThreads, 0);
-    return n > 0 ? n : 1;
-  }()};
-  if (filtered())
-    raster_kernel<true, kMode><<<kNumSMs * per_sm[1], kRasterThreads, 0, s>>>(p, wk);
-  else
-    raster_kernel<false, kMode><<<kNumSMs * per_sm[0], kRasterThreads, 0, s>>>(p, wk);
+  const GtParams g = {};
+  if (spans()) {
+    static const int grid[2] = {occupancy_grid(span_kernel<false, kMode>), occupancy_grid(span_kernel<true, kMode>)};
+    if (filtered())
+      span_kernel<true, kMode><<<grid[1], kRasterThreads, 0, s>>>(p, g, nullptr, nullptr, wk, nullptr, nullptr);
+    else
+      span_kernel<false, kMode><<<grid[0], kRasterThreads, 0, s>>>(p, g, nullptr, nullptr, wk, nullptr, nullptr);
+  } else {
+    static const int grid[2] = {occupancy_grid(raster_kernel<false, kMode>), occupancy_grid(raster_kernel<true, kMode>)};
+    if (filtered())
+      raster_kernel<true, kMode><<<grid[1], kRasterThreads, 0, s>>>(p, wk);
+    else
+      raster_kernel<false, kMode><<<grid[0], kRasterThreads, 0, s>>>(p, wk);
+  }
   FPVS_CHECK_LAUNCH("froxelize raster");
   return FPVS_OK;
 }
@@ -592,6 +895,7 @@ int froxel_pass(const double* verts, long long nverts, const int64_t* tris, long
   wk.bsum = reinterpret_cast<unsigned long long*>(ws + L.bsum);
   wk.bpre = reinterpret_cast<unsigned long long*>(ws + L.bpre);
   wk.total = reinterpret_cast<unsigned long long*>(ws + L.total);
+  wk.nsamples = wk.total + 1;
   wk.tabx = reinterpret_cast<int*>(ws + L.tabx);
   wk.taby = reinterpret_cast<int*>(ws + L.taby);
   wk.ntris = ntris;
@@ -610,10 +914,10 @@ int froxel_pass(const double* verts, long long nverts, const int64_t* tris, long
   p.ny = Ny;
   p.nz = Nz;
   p.depth_log = depth_mode == FPVS_DEPTH_LOG;
-  if (ntris == 0) {
-    if (cudaMemsetAsync(wk.total, 0, 8, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
-    return FPVS_OK;
-  }
+  p.rows_mode = spans() ? 1 : 0;
+  p.seg = env_int("FPVS_FROX_SEG", 16);
+  if (cudaMemsetAsync(wk.total, 0, 16, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");  // total + nsamples
+  if (ntris == 0) return FPVS_OK;
   setup_kernel<false><<<wk.nb, kSetupThreads, 0, s>>>(p, nullptr, verts, nverts, tris, ntris, wk);
   FPVS_CHECK_LAUNCH("froxelize setup");
   scan_kernel<<<1, 1024, 0, s>>>(p, wk);
@@ -691,7 +995,8 @@ extern "C" long long fpvs_froxelize_samples(const void* workspace, void* stream)
   if (workspace == nullptr) return -1;
   unsigned long long v = 0;
   cudaStream_t s = as_stream(stream);
-  if (cudaMemcpyAsync(&v, workspace, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return -1;
+  if (cudaMemcpyAsync(&v, static_cast<const uint8_t*>(workspace) + 8, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return -1;
   if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
   return (long long)v;
 }
@@ -712,45 +1017,6 @@ extern "C" long long fpvs_froxelize_samples(const void* workspace, void* stream)
 // ===========================================================================
 namespace fpvs {
 namespace frox {
-
-struct GtParams {
-  double fo[3], fb[9];
-  double fh, fnear, ffar, flogr;  // flogr = log(far / near), computed like math.log on the host
-  double W, H;
-  int iw, ih;
-  int nx, ny, nz, depth_log;
-  long long T;     // scene triangles (per camera)
-  long long npix;  // W * H
-};
-
-// Reference depth of one sample (froxel.py:272-279 coverage; oracle.py:127
-// depth = 1 / interp_affine(invz, b1, b2)); < 0 when not covered.
-__device__ __forceinline__ double depth_exact(const Slot& s, double cx, double cy) {
-  const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
-  const double b1 = ddiv(dsub(dmul(dx, s.e2y), dmul(s.e2x, dy)), s.den);
-  const double b2 = ddiv(dsub(dmul(s.e1x, dy), dmul(dx, s.e1y)), s.den);
-  const double b0 = dsub(dsub(1.0, b1), b2);
-  if (!(b0 >= 0 && b1 >= 0 && b2 >= 0)) return -1.0;
-  return ddiv(1.0, dadd(dadd(s.iz0, dmul(b1, dsub(s.iz1, s.iz0))), dmul(b2, dsub(s.iz2, s.iz0))));
-}
-
-// Coverage filter before the exact evaluation: samples provably outside
-// (exact numerator signs, or b0 < 0 by more than the approximation error)
-// skip the three divisions.
-__device__ __forceinline__ double depth_filtered(const Slot& s, double cx, double cy) {
-  const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
-  const double n1 = dsub(dmul(dx, s.e2y), dmul(s.e2x, dy));
-  const double n2 = dsub(dmul(s.e1x, dy), dmul(dx, s.e1y));
-  const bool dneg = s.den < 0;
-  const double a1 = fabs(n1), a2 = fabs(n2);
-  constexpr double kTiny = 1e-250;
-  if (!((a1 != 0 && a1 < kTiny) || (a2 != 0 && a2 < kTiny))) {
-    if ((n1 != 0 && ((n1 < 0) != dneg)) || (n2 != 0 && ((n2 < 0) != dneg))) return -1.0;
-    const double q1 = n1 * s.rden, q2 = n2 * s.rden;
-    if ((1.0 - q1) - q2 < -1e-13 * (1.0 + q1 + q2)) return -1.0;
-  }
-  return depth_exact(s, cx, cy);
-}
 
 template <int kPass>
 __global__ void __launch_bounds__(kRasterThreads, 4)
@@ -945,6 +1211,29 @@ __global__ void depth_out_kernel(long long n, const unsigned long long* __restri
   }
 }
 
+// z pass (+ the primitive-id tie pass) over every camera's candidate samples
+inline int launch_depth(const Params& p, const GtParams& g, const fpvs_frustum* cams, const int64_t* prim_ids,
+                        const Work& wk, unsigned long long* zbuf, long long* pidbuf, bool id_pass, cudaStream_t s) {
+  if (spans()) {
+    static const int grid[2] = {occupancy_grid(span_kernel<true, 3>), occupancy_grid(span_kernel<true, 4>)};
+    span_kernel<true, 3><<<grid[0], kRasterThreads, 0, s>>>(p, g, cams, prim_ids, wk, zbuf, pidbuf);
+    FPVS_CHECK_LAUNCH("depth (spans)");
+    if (id_pass) {
+      span_kernel<true, 4><<<grid[1], kRasterThreads, 0, s>>>(p, g, cams, prim_ids, wk, zbuf, pidbuf);
+      FPVS_CHECK_LAUNCH("primitive ids (spans)");
+    }
+  } else {
+    static const int grid = occupancy_grid(depth_kernel<0>);
+    depth_kernel<0><<<grid, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
+    FPVS_CHECK_LAUNCH("depth");
+    if (id_pass) {
+      depth_kernel<1><<<grid, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
+      FPVS_CHECK_LAUNCH("primitive ids");
+    }
+  }
+  return FPVS_OK;
+}
+
 struct GtLayout {
   size_t total, slots, lp, bsum, bpre, zbuf, pid, ufx, ufy, bytes;
 };
@@ -1005,12 +1294,14 @@ extern "C" int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t*
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   if (!accumulate && cudaMemsetAsync(gt_bits, 0, (size_t)grid_bytes, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
   if (ntris == 0 || ncams == 0) return FPVS_OK;
-  Work wk;
+  Work wk = {};
   wk.slots = reinterpret_cast<Slot*>(ws + L.slots);
   wk.lp = reinterpret_cast<unsigned long long*>(ws + L.lp);
   wk.bsum = reinterpret_cast<unsigned long long*>(ws + L.bsum);
   wk.bpre = reinterpret_cast<unsigned long long*>(ws + L.bpre);
   wk.total = reinterpret_cast<unsigned long long*>(ws + L.total);
+  wk.nsamples = wk.total + 1;
+  if (cudaMemsetAsync(wk.total, 0, 16, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
   wk.out_words = nullptr;
   wk.tabx = wk.taby = nullptr;
   wk.ufx = reinterpret_cast<double*>(ws + L.ufx);
@@ -1030,6 +1321,8 @@ extern "C" int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t*
   p.ny = Ny;
   p.nz = Nz;
   p.depth_log = 0;
+  p.rows_mode = spans() ? 1 : 0;
+  p.seg = env_int("FPVS_GT_SEG", 64);
   GtParams g;
   for (int i = 0; i < 3; ++i) g.fo[i] = fr->origin[i];
   for (int i = 0; i < 9; ++i) g.fb[i] = fr->basis[i];
@@ -1051,16 +1344,9 @@ extern "C" int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t*
   FPVS_CHECK_LAUNCH("gt_pvs setup");
   scan_kernel<<<1, 1024, 0, s>>>(p, wk);
   FPVS_CHECK_LAUNCH("gt_pvs scan");
-  static const int per_sm = [] {
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, depth_kernel<0>, kRasterThreads, 0);
-    return n > 0 ? n : 1;
-  }();
-  depth_kernel<0><<<kNumSMs * per_sm, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
-  FPVS_CHECK_LAUNCH("gt_pvs depth");
-  if (pidbuf) {
-    depth_kernel<1><<<kNumSMs * per_sm, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
-    FPVS_CHECK_LAUNCH("gt_pvs prim ids");
+  {
+    const int rc = launch_depth(p, g, cams, prim_ids, wk, zbuf, pidbuf, pidbuf != nullptr, s);
+    if (rc) return rc;
   }
   resolve_kernel<<<kNumSMs * 8, 256, 0, s>>>(g, cams, ncams, zbuf, pidbuf, wk.ufx, wk.ufy,
                                              reinterpret_cast<unsigned int*>(gt_bits),
@@ -1094,11 +1380,15 @@ extern "C" int fpvs_render_depth(const double* verts, long long nverts, const in
     wk.bsum = reinterpret_cast<unsigned long long*>(ws + L.bsum);
     wk.bpre = reinterpret_cast<unsigned long long*>(ws + L.bpre);
     wk.total = reinterpret_cast<unsigned long long*>(ws + L.total);
+    wk.nsamples = wk.total + 1;
+    if (cudaMemsetAsync(wk.total, 0, 16, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
     wk.ntris = ntris * ncams;
     wk.nb = (int)((2 * wk.ntris + kSlotsPerBlock - 1) / kSlotsPerBlock);
     Params p = {};
     p.sx = (double)res_w;
     p.sy = (double)res_h;
+    p.rows_mode = spans() ? 1 : 0;
+    p.seg = env_int("FPVS_GT_SEG", 64);
     GtParams g = {};
     g.iw = res_w;
     g.ih = res_h;
@@ -1110,13 +1400,8 @@ extern "C" int fpvs_render_depth(const double* verts, long long nverts, const in
     FPVS_CHECK_LAUNCH("render_depth setup");
     scan_kernel<<<1, 1024, 0, s>>>(p, wk);
     FPVS_CHECK_LAUNCH("render_depth scan");
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, depth_kernel<0>, kRasterThreads, 0);
-    per_sm = per_sm > 0 ? per_sm : 1;
-    depth_kernel<0><<<kNumSMs * per_sm, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
-    FPVS_CHECK_LAUNCH("render_depth depth");
-    depth_kernel<1><<<kNumSMs * per_sm, kRasterThreads, 0, s>>>(g, cams, prim_ids, wk, zbuf, pidbuf);
-    FPVS_CHECK_LAUNCH("render_depth ids");
+    const int rc = launch_depth(p, g, cams, prim_ids, wk, zbuf, pidbuf, true, s);
+    if (rc) return rc;
   }
   depth_out_kernel<<<kNumSMs * 8, 256, 0, s>>>((long long)ncams * npix, zbuf, pidbuf, depth_out, reinterpret_cast<long long*>(prim_out));
   FPVS_CHECK_LAUNCH("render_depth out");

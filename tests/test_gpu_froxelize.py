@@ -176,3 +176,35 @@ def test_feeds_the_pvs_pipeline():
     out = pipe.run_device()
     torch.cuda.synchronize()
     assert out.numel() == ref.size
+
+
+_ALT_CHECK = r"""
+import os, sys, numpy as np
+sys.path.insert(0, os.getcwd())
+from paper_2509_24677_b200.froxelize import FroxelizeConfig, Froxelizer, Frustum
+g = np.load("tests/golden/froxelize.npz")
+bad = 0
+for i in range(int(g["ncases"])):
+    c = {k[len(f"c{i}_"):]: g[k] for k in g.files if k.startswith(f"c{i}_")}
+    if int(c["depth"]) != 0:
+        continue
+    h, n, f = (float(v) for v in c["lens"])
+    got = Froxelizer(c["verts"], c["tris"]).run(Frustum(c["origin"], c["basis"], h, n, f),
+        tuple(int(v) for v in c["dims"]), FroxelizeConfig(supersample=int(c["ss"]))).cpu().numpy()
+    bad += int(np.unpackbits(got ^ c["bits"]).sum())
+print("BAD", bad)
+"""
+
+
+@pytest.mark.parametrize("env", [{"FPVS_FROX_SPANS": "0"}, {"FPVS_FROX_EXACT": "1"}, {"FPVS_FROX_SEG": "8"},
+                                 {"FPVS_FROX_SEG": "256"}])
+def test_alternative_raster_paths_match_golden(env):
+    """The whole-box raster, the exact-only evaluation and other span segment
+    widths (env switches read once per process, hence the subprocess)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _ALT_CHECK], cwd=root, env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "BAD 0" in r.stdout, r.stdout
