@@ -42,7 +42,7 @@
 namespace fpvs {
 namespace frox {
 
-constexpr int kSetupThreads = 256;
+constexpr int kSetupThreads = 64;
 constexpr int kSlotsPerBlock = 2 * kSetupThreads;
 constexpr int kRasterThreads = 256;
 constexpr int kPerThread = 8;
