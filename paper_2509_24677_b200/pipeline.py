@@ -41,13 +41,23 @@ class ChainPlan:
         self.x0 = torch.empty((k, d ** 3), dtype=dt, device=device)
         self.ping = torch.empty((k, widest), dtype=dt, device=device)
         self.pong = torch.empty((k, widest), dtype=dt, device=device)
+        # the fused level build (levels.cu: three launches for flags, compaction,
+        # tables + features + output clear) where the grid shape allows it
+        try:
+            self.maps = sp.LevelMaps([self.L0], [], [], self.grid_dims, d)
+        except ValueError:
+            self.maps = None
 
     def stages(self, bits, out_bits, tau: float = 0.5, probs=None, logits=None):
         """Ordered (name, idempotent launch function) list of one frame."""
         net, lv = self.net, self.L0
         d = net.cfg.d
-        out = [("maps", lambda: sp.fill_level_from_bits(lv, bits, self.grid_dims, d)),
-               ("gather", lambda: sp.gather_features(bits, lv, self.grid_dims, d, self.x0.dtype, out=self.x0))]
+        if self.maps is not None:
+            # maps + sparse interleave + clearing the output grid in one fused build
+            out = [("maps", lambda: self.maps.run(bits, self.x0, d ** 3, out_bits))]
+        else:
+            out = [("maps", lambda: sp.fill_level_from_bits(lv, bits, self.grid_dims, d)),
+                   ("gather", lambda: sp.gather_features(bits, lv, self.grid_dims, d, self.x0.dtype, out=self.x0))]
         x, ldx = self.x0, d ** 3
         bufs = (self.ping, self.pong)
         for i, layer in enumerate(net.layers[:-1]):
@@ -59,7 +69,8 @@ class ChainPlan:
             x, ldx = y, y.shape[1]
 
         def head(x=x, ldx=ldx):
-            out_bits.zero_()
+            if self.maps is None:
+                out_bits.zero_()  # else cleared by the fused map build
             run_head(net.layers[-1], x, ldx, lv, d, self.grid_dims, tau, out_bits, probs, logits, net.precision)
         out.append(("head", head))
         return out
