@@ -353,6 +353,17 @@ int fpvs_bits_confusion(const uint8_t* pred_bits, const uint8_t* gt_bits, int B,
 int fpvs_first_hit_labels(const uint8_t* bits, int B, int Nx, int Ny, int Nz, int radius,
                           uint8_t* out_bits, int32_t* zfirst_ws, void* stream);
 
+/* Halo-cached weight gradient of a 27-tap conv with Cin = 32 (wgrad_halo.cu):
+ * the same dW / db as fpvs_spconv_wgrad_tc (K = 27), reading each 128-row
+ * tile's neighbour rows once from the halo tables of fpvs_kmap_halo
+ * (halo_rows, halo_n, lnbr) instead of gathering 27 pieces per row.
+ * Cout in {8, 16, 24, 32}; workspace fpvs_wgrad_halo_workspace_size(cap). */
+size_t fpvs_wgrad_halo_workspace_size(int cap);
+int fpvs_spconv_wgrad_halo(const void* x, int ldx, const void* dz, int lddz, const int32_t* nbr,
+                           const int32_t* n_dev, int cap, const int32_t* halo_rows, const int32_t* halo_n,
+                           const int16_t* lnbr, int cin, int cout, float* dw, float* db, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* ---- (§8(f) #1) perspective froxelization ------------------------------ */
 /* Frustum of pkg/src/froxelpvs/core.py:297-325 as the rasterizer reads it:
  * origin (_o), basis rows (right, up, forward) (_basis), half_extent =

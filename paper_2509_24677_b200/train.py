@@ -76,6 +76,12 @@ def allreduce_weighted(flat, weight: float):
     return flat
 
 
+def use_halo_wgrad() -> bool:
+    """FPVS_HALO_WGRAD=0 keeps every layer on the gathering wgrad (A/B checks)."""
+    import os
+    return os.environ.get("FPVS_HALO_WGRAD", "1") != "0"
+
+
 class TrainStep:
     """All device buffers of one (B, grid) training step; ``run`` only launches kernels.
 
@@ -111,6 +117,13 @@ class TrainStep:
             tws = max(_lib.size("fpvs_wgrad_tc_workspace_size", L.taps, L.spec.in_channels, L.spec.out_channels, cap)
                       for L in net.layers)
             self.wg_tc_ws = torch.empty(tws, dtype=torch.uint8, device=device)
+            # 27-tap layers with Cin = 32 take the halo-cached wgrad (wgrad_halo.cu):
+            # the level's halo tables are rebuilt with the maps every step
+            self.halo_wgrad = use_halo_wgrad() and any(self._halo_wgrad_ok(L) for L in net.layers)
+            if self.halo_wgrad:
+                self.halo_builder = sp.HaloBuilder([self.lv])
+                self.wg_halo_ws = torch.empty(_lib.size("fpvs_wgrad_halo_workspace_size", cap), dtype=torch.uint8,
+                                              device=device)
         self.pred_bits = torch.zeros(B * self.grid_bytes, dtype=torch.uint8, device=device)
         # flat master parameters and gradient
         sizes = [(L.w.numel(), L.b.numel()) for L in net.layers]
@@ -165,6 +178,11 @@ class TrainStep:
                   _lib.ptr(self.counts), _lib.ptr(self.conf_ws), self.conf_ws.numel(), s)
         self.backward(stream)
 
+    @staticmethod
+    def _halo_wgrad_ok(L) -> bool:
+        s = L.spec
+        return s.kernel == 3 and s.in_channels == 32 and s.out_channels % 8 == 0 and s.out_channels <= 32
+
     def _tc_backward_ok(self) -> bool:
         layers = self.net.layers
         return (all(L.spec.in_channels % 8 == 0 and L.spec.out_channels % 8 == 0 and L.spec.out_channels <= 256
@@ -204,6 +222,10 @@ class TrainStep:
         s = _lib.stream_ptr(stream)
         ins = [self.x0] + self.acts
         cap = lv.cap
+        halo = None
+        if self.halo_wgrad:
+            self.halo_builder.run(stream)
+            halo = sp._halo_tables(lv)
         _lib.call("fpvs_cast_bf16", _lib.ptr(self.dlogits), cap * self.dlogits.shape[1], _lib.ptr(self.dlog16), s)
         dz, lddz = self.dlog16, self.dlog16.shape[1]
         for li in reversed(range(len(net.layers))):
@@ -212,9 +234,15 @@ class TrainStep:
             x = ins[li]
             table, K = (lv.nbr, 27) if spec.kernel == 3 else (None, 1)
             dw, db = self.views[li]
-            _lib.call("fpvs_spconv_wgrad_tc", _lib.ptr(x), x.shape[1], _lib.ptr(dz), lddz, _lib.ptr(table), K,
-                      _lib.ptr(lv.n), cap, spec.in_channels, spec.out_channels, _lib.ptr(dw), _lib.ptr(db),
-                      _lib.ptr(self.wg_tc_ws), self.wg_tc_ws.numel(), s)
+            if halo is not None and self._halo_wgrad_ok(layer):
+                _lib.call("fpvs_spconv_wgrad_halo", _lib.ptr(x), x.shape[1], _lib.ptr(dz), lddz, _lib.ptr(table),
+                          _lib.ptr(lv.n), cap, _lib.ptr(halo["rows"]), _lib.ptr(halo["n"]), _lib.ptr(halo["lnbr"]),
+                          spec.in_channels, spec.out_channels, _lib.ptr(dw), _lib.ptr(db), _lib.ptr(self.wg_halo_ws),
+                          self.wg_halo_ws.numel(), s)
+            else:
+                _lib.call("fpvs_spconv_wgrad_tc", _lib.ptr(x), x.shape[1], _lib.ptr(dz), lddz, _lib.ptr(table), K,
+                          _lib.ptr(lv.n), cap, spec.in_channels, spec.out_channels, _lib.ptr(dw), _lib.ptr(db),
+                          _lib.ptr(self.wg_tc_ws), self.wg_tc_ws.numel(), s)
             if li == 0:
                 break
             dx = self.dz16[li % 2]

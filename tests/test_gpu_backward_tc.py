@@ -127,3 +127,38 @@ def test_train_step_tc_backward_matches_simt():
             rel = float((a - b).norm() / (b.norm() + 1e-30))
             assert rel < 0.02, (layer.spec, t.shape, rel)
             o += t.numel()
+
+
+@pytest.mark.parametrize("cout,dims,density", [(32, (20, 18, 16), 0.3), (8, (20, 18, 16), 0.3),
+                                               (16, (40, 36, 30), 0.25), (32, (64, 64, 32), 0.08)])
+def test_wgrad_halo_vs_float64(cout, dims, density):
+    """fpvs_spconv_wgrad_halo (27 taps, Cin 32): dW / db vs float64, and vs the gathering wgrad."""
+    import torch
+    from paper_2509_24677_b200 import _lib, sparse as sp
+    lv = _level(dims, density, cout + 7)
+    n = lv.count()
+    cin = 32
+    h = sp.build_halo(lv)
+    xv, xt = _bf16(n, cin, lv.cap, 5, relu=True)
+    dv, dt = _bf16(n, cout, lv.cap, 6)
+    dw = torch.full((27 * cin, cout), 7.0, device="cuda")
+    db = torch.full((cout,), 7.0, device="cuda")
+    ws = torch.empty(_lib.size("fpvs_wgrad_halo_workspace_size", lv.cap), dtype=torch.uint8, device="cuda")
+    _lib.call("fpvs_spconv_wgrad_halo", _lib.ptr(xt), cin, _lib.ptr(dt), cout, _lib.ptr(lv.nbr), _lib.ptr(lv.n),
+              lv.cap, _lib.ptr(h["rows"]), _lib.ptr(h["n"]), _lib.ptr(h["lnbr"]), cin, cout, _lib.ptr(dw), _lib.ptr(db),
+              _lib.ptr(ws), ws.numel(), 0)
+    tab = lv.nbr[:n].cpu().numpy().astype(np.int64)
+    ref = np.zeros((27, cin, cout))
+    for j in range(27):
+        v = tab[:, j] >= 0
+        ref[j] = xv[tab[v, j]].T @ dv[v]
+    ref = ref.reshape(27 * cin, cout)
+    got = dw.cpu().numpy()
+    scale = np.abs(ref).max()
+    assert np.abs(got - ref).max() <= 2e-5 * scale + 1e-4, (np.abs(got - ref).max(), scale)
+    assert np.allclose(db.cpu().numpy(), dv.sum(0), rtol=1e-4, atol=1e-3)
+    dw2 = torch.zeros_like(dw)
+    _lib.call("fpvs_spconv_wgrad_halo", _lib.ptr(xt), cin, _lib.ptr(dt), cout, _lib.ptr(lv.nbr), _lib.ptr(lv.n),
+              lv.cap, _lib.ptr(h["rows"]), _lib.ptr(h["n"]), _lib.ptr(h["lnbr"]), cin, cout, _lib.ptr(dw2), None,
+              _lib.ptr(ws), ws.numel(), 0)
+    assert torch.equal(dw, dw2)  # deterministic
