@@ -15,7 +15,7 @@
 //
 //   warps 0-7  A producers: per stage (64 rows x one (j, ci) block) 1024
 //              16-byte pieces, halo -> no-swizzle MN-major A layout
-//   warp 8     loader: per tile the local table + halo row list (bulk
+//   warps 8,10,11 loaders: per tile the local table + halo row list (bulk
 //              copies), the halo rows and the tile's dz rows (cp.async)
 //   warp 9     MMA issuer (one lane): 4 x kind::f16 M=128 N=32 K=16 per stage
 //   warps 8-11 epilogue after the loop: TMEM -> fp32 partial per CTA
@@ -53,7 +53,8 @@ constexpr int HBUF = (HB_B + B_CHUNK + 1023) & ~1023;
 constexpr int NHB = 2;
 constexpr int THREADS = 384;
 constexpr int PROD = 256;
-constexpr int W_LOAD = 8, W_MMA = 9;
+constexpr int W_LOAD = 8, W_MMA = 9;  // loaders: warps 8, 10, 11
+constexpr int LOADERS = 96;
 constexpr int SMEM = 1024 + NS * A_STAGE + NHB * HBUF + 256;
 static_assert(SMEM <= 232448, "shared memory budget");
 
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_halo_kernel(const Params p) 
     }
     for (int b = 0; b < NHB; ++b) {
       mbar_init(smem_u32(hmeta + b), 1);
-      mbar_init(smem_u32(hfull + b), 32);
+      mbar_init(smem_u32(hfull + b), LOADERS);
       mbar_init(smem_u32(hempty + b), PROD / 32 + 1);
     }
     mbar_init(smem_u32(tfull), 1);
@@ -230,9 +231,10 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_halo_kernel(const Params p) 
       if (lane == 0) mbar_arrive(hempty_a + 8 * hb);
     }
     if (tid == 0) pdl_trigger();
-  } else if (warp == W_LOAD) {
-    // ===================== loader =====================
+  } else if (warp != W_MMA) {
+    // ===================== loaders (warps 8, 10, 11) =====================
     pdl_wait();
+    const int lt = (warp == W_LOAD ? 0 : warp - W_MMA) * 32 + lane;  // 0..95
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u, lddz2 = (uint32_t)p.lddz * 2u;
     const char* xg = reinterpret_cast<const char*>(p.x);
     const char* dg = reinterpret_cast<const char*>(p.dz);
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_halo_kernel(const Params p) 
       mbar_wait_sleep(smem_u32(hempty + hb), hph ^ 1, 32);
       uint8_t* hbuf = sH + hb * HBUF;
       const int H = min(__ldg(p.halo_n + tile), HMAX);
-      if (lane == 0) {
+      if (lt == 0) {
         const uint32_t rb = (uint32_t)((H * 4 + 15) & ~15);
         const uint32_t mb = smem_u32(hmeta + hb);
         mbar_arrive_expect_tx(mb, LNBR_BYTES + rb);
@@ -253,14 +255,14 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_halo_kernel(const Params p) 
       mbar_wait(smem_u32(hmeta + hb), hph);
       const int* hr = reinterpret_cast<const int*>(hbuf + HB_ROWS);
       const uint32_t hs = smem_u32(hbuf);
-      for (int q = lane; q < ((p.dbg & 8) ? 0 : H * 4); q += 32) {
+      for (int q = lt; q < ((p.dbg & 8) ? 0 : H * 4); q += LOADERS) {
         const int i = q >> 2, pc = q & 3;
         cp_async16(hs + i * 64 + ((pc ^ (i & 3)) << 4), xg + (long long)hr[i] * ldx2 + pc * 16, 16);
       }
       // the tile's dz rows: two 64-row chunks, MN-major (rows past n and
       // channels past Cout are zero-filled)
       const uint32_t bs = smem_u32(hbuf + HB_B);
-      for (int q = lane; q < RT * (NPAD / 8); q += 32) {
+      for (int q = lt; q < RT * (NPAD / 8); q += LOADERS) {
         const int kk = q / (NPAD / 8), ng = q - kk * (NPAD / 8);
         const int row = tile * RT + kk;
         const bool ok = row < n && ng * 8 < p.cout;
