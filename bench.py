@@ -250,7 +250,8 @@ def froxelize_side(reps: int = 20):
         g = torch.cuda.CUDAGraph()
         st = torch.cuda.Stream()
         st.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(st):
+        from paper_2509_24677_b200.pipeline import no_gc
+        with torch.cuda.stream(st), no_gc():
             with torch.cuda.graph(g, stream=st):
                 for _ in range(reps):
                     fz.run(fr, dims, cfg, out=bits)

@@ -24,6 +24,27 @@ def _torch():
     return torch
 
 
+class _NoGC:
+    """Garbage collection off while a CUDA graph is captured: a collected
+    CUDAGraph from earlier work would be destroyed mid-capture, which CUDA
+    forbids (cudaErrorStreamCaptureUnsupported)."""
+
+    def __enter__(self):
+        import gc
+        self._was = gc.isenabled()
+        gc.collect()
+        gc.disable()
+
+    def __exit__(self, *exc):
+        import gc
+        if self._was:
+            gc.enable()
+        return False
+
+
+no_gc = _NoGC
+
+
 class ChainPlan:
     """Buffers for a linear PvsNet (configs 1, 3, 4, 5) over B packed grids."""
 
@@ -131,7 +152,7 @@ def device_stage_times(plan, bits, out_bits, tau: float = 0.5, reps: int = 20, f
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
+        with torch.cuda.stream(s), no_gc():
             with torch.cuda.graph(g, stream=s):
                 for _ in range(reps):
                     fn()
@@ -189,7 +210,7 @@ class FramePipeline:
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
+        with torch.cuda.stream(s), no_gc():
             with torch.cuda.graph(g, stream=s):
                 self.plan.run(in_bits, out_bits, self.tau)
         torch.cuda.current_stream().wait_stream(s)

@@ -146,7 +146,8 @@ def test_unaligned_output_and_graph_replay():
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
+    from paper_2509_24677_b200.pipeline import no_gc
+    with torch.cuda.stream(s), no_gc():
         fz.run(fr, dims, FroxelizeConfig(supersample=2), out=out)
         with torch.cuda.graph(g, stream=s):
             fz.run(fr, dims, FroxelizeConfig(supersample=2), out=out)
