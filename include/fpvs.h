@@ -107,6 +107,17 @@ int fpvs_kmap_up(const int32_t* fine_coords, const int32_t* n_fine_dev, int cap_
                  const int32_t* coarse_index_vol, int B, int X, int Y, int Z,
                  int32_t* up, void* stream);
 
+/* Per-offset pair lists of a neighbour table (SURVEY.md §8(a) row KM): for
+ * offset j the pairs (in = table[i][j], out = i) with in >= 0, sorted by
+ * out, stored at [pair_off[j], pair_off[j+1]) of pair_in / pair_out;
+ * pair_off: int64 [K+1] (device), exclusive prefix of the list lengths.
+ * At most cap_pairs pairs are stored (pair_off[K] is the full count).
+ * Deterministic; workspace fpvs_kmap_pairs_workspace_size(K, cap). */
+size_t fpvs_kmap_pairs_workspace_size(int K, int cap);
+int fpvs_kmap_pairs(const int32_t* table, int K, const int32_t* n_dev, int cap, int32_t* pair_in,
+                    int32_t* pair_out, int64_t* pair_off, long long cap_pairs, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* Per 128-row tile of a neighbour table: bit j set iff some live row of the
  * tile has table[row][j] >= 0.  masks: uint32 [ceil(cap/128)].  The
  * tensor-core conv skips K-chunks of offsets absent from a whole tile. */

@@ -16,7 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfpvs.so")
-SOURCES = ["capi.cu", "interleave.cu", "kmap.cu", "levels.cu", "spconv_simt.cu", "spconv_tc.cu", "spconv_halo.cu", "upsort.cu", "wgrad_tc.cu", "wgrad_halo.cu", "optim.cu", "froxelize.cu"]
+SOURCES = ["capi.cu", "interleave.cu", "kmap.cu", "kmap_pairs.cu", "levels.cu", "spconv_simt.cu", "spconv_tc.cu", "spconv_halo.cu", "upsort.cu", "wgrad_tc.cu", "wgrad_halo.cu", "optim.cu", "froxelize.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-diag-suppress", "177"]

@@ -98,6 +98,26 @@ def build_subm(lv: Level, stream=None):
 HALO_MAX = 512  # FPVS_HALO_MAX
 
 
+def pair_lists(table, K: int, n, cap: int, stream=None):
+    """Per-offset (in_row, out_row) pair lists of a neighbour table, sorted by
+    out_row within each offset, and their int64 offsets [K+1] (row KM).
+    Returns device tensors (pair_in, pair_out, pair_off); one host sync sizes
+    the outputs (the pair count is data-dependent)."""
+    torch = _torch()
+    dev = table.device
+    ws = torch.empty(_lib.size("fpvs_kmap_pairs_workspace_size", K, cap), dtype=torch.uint8, device=dev)
+    off = torch.empty(K + 1, dtype=torch.int64, device=dev)
+    s = _lib.stream_ptr(stream)
+    _lib.call("fpvs_kmap_pairs", _lib.ptr(table), K, _lib.ptr(n), cap, None, None, _lib.ptr(off), 0, _lib.ptr(ws),
+              ws.numel(), s)
+    total = int(off[K].item())
+    pin = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    pout = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    _lib.call("fpvs_kmap_pairs", _lib.ptr(table), K, _lib.ptr(n), cap, _lib.ptr(pin), _lib.ptr(pout), _lib.ptr(off),
+              total, _lib.ptr(ws), ws.numel(), s)
+    return pin[:total], pout[:total], off
+
+
 def _halo_tables(lv: Level) -> dict:
     h = lv.extra.get("halo")
     if h is None:

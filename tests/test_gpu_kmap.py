@@ -168,3 +168,22 @@ def test_fused_levels_match_granular(case):
         assert torch.equal(feat[:n0, :d ** 3], want[:n0])
         assert bool((feat[:n0, d ** 3:] == 7).all())  # columns past d^3 untouched
         assert int(clear.sum()) == 0
+
+
+@pytest.mark.parametrize("dims,density", [((20, 18, 16), 0.3), ((64, 64, 32), 0.06), ((3, 4, 5), 0.9)])
+def test_pair_lists_match_oracle(dims, density):
+    """fpvs_kmap_pairs: per-offset (in, out) lists sorted by out and their offsets (row KM) == oracle."""
+    import torch
+    from oracle import sparse as osp
+    from paper_2509_24677_b200 import sparse as sp
+    rng = np.random.default_rng(int(density * 1000))
+    mask = rng.random((1,) + dims) < density
+    lv = sp.new_level(1, dims)
+    lv.active.copy_(torch.from_numpy(mask.reshape(-1).astype(np.uint8)).cuda())
+    sp.compact(lv)
+    sp.build_subm(lv)
+    n = lv.count()
+    pin, pout, off = sp.pair_lists(lv.nbr, 27, lv.n, lv.cap)
+    ins, outs, ref_off = osp.pair_lists(lv.nbr[:n].cpu().numpy())
+    assert np.array_equal(off.cpu().numpy(), ref_off)
+    assert np.array_equal(pin.cpu().numpy(), ins) and np.array_equal(pout.cpu().numpy(), outs)
