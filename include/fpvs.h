@@ -341,6 +341,9 @@ int fpvs_spconv_wgrad_tc(const void* x, int ldx, const void* dz, int lddz, const
                          void* workspace, size_t workspace_bytes, void* stream);
 /* f32 -> bf16 (round to nearest even), n elements. */
 int fpvs_cast_bf16(const float* src, long long n, void* dst, void* stream);
+/* The first min(*n_dev, cap) rows of an fp32 [cap][cols] matrix to bf16
+ * (rows past the device count are left untouched). */
+int fpvs_cast_bf16_rows(const float* src, int cols, const int32_t* n_dev, int cap, void* dst, void* stream);
 
 /* Optimizer steps over ONE flat fp32 parameter buffer (all layers' weights
  * and biases back to back; the data-parallel gradient is one all-reduce of

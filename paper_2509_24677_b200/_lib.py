@@ -77,6 +77,7 @@ SIGNATURES = {
     "fpvs_froxelize": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _i, _i, _i, _i, _i, _p, _p, _z, _p]),
     "fpvs_froxelize_samples": (C.c_longlong, [_p, _p]),
     "fpvs_gt_pvs_workspace_size": (_z, [C.c_longlong, _i, _i, _i, _i]),
+    "fpvs_cast_bf16_rows": (_i, [_p, _i, _p, _i, _p, _p]),
     "fpvs_kmap_pairs_workspace_size": (_z, [_i, _i]),
     "fpvs_kmap_pairs": (_i, [_p, _i, _p, _i, _p, _p, _p, C.c_longlong, _p, _z, _p]),
     "fpvs_wgrad_halo_workspace_size": (_z, [_i]),

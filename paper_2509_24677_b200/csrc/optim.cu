@@ -147,7 +147,23 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, long long n, __n
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
     dst[t] = __float2bfloat16_rn(src[t]);
 }
+__global__ void cast_bf16_rows_kernel(const float* __restrict__ src, int cols, const int* n_dev, int cap,
+                                      __nv_bfloat16* __restrict__ dst) {
+  const long long n = (long long)min(*n_dev, cap) * cols;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    dst[t] = __float2bfloat16_rn(src[t]);
+}
 }  // namespace fpvs
+
+extern "C" int fpvs_cast_bf16_rows(const float* src, int cols, const int32_t* n_dev, int cap, void* dst,
+                                   void* stream) {
+  FPVS_CHECK_ARG(src && dst && n_dev && cols > 0 && cap >= 0, "bad arguments");
+  if (cap == 0) return FPVS_OK;
+  fpvs::cast_bf16_rows_kernel<<<fpvs::grid_for((long long)cap * cols, 256, 4), 256, 0, fpvs::as_stream(stream)>>>(
+      src, cols, n_dev, cap, (__nv_bfloat16*)dst);
+  FPVS_CHECK_LAUNCH("fpvs_cast_bf16_rows");
+  return FPVS_OK;
+}
 
 extern "C" int fpvs_cast_bf16(const float* src, long long n, void* dst, void* stream) {
   FPVS_CHECK_ARG(src && dst && n >= 0, "bad arguments");

@@ -257,21 +257,33 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_tc_kernel(const Params p) {
   }
 }
 
-// dw[f][co] = sum over splits (fixed order) of part[f / 128][s][f % 128][co];
-// row f = kcin (the all-ones A row, when kcin % 128 != 0) is db
-__global__ void wgrad_reduce_tc_kernel(const float* __restrict__ part, int nsplit, int npad, int kcin, int cout,
-                                       float* __restrict__ dw, float* __restrict__ db) {
-  const int rows = kcin + ((db && (kcin % 128)) ? 1 : 0);
-  const long long total = (long long)rows * cout;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int f = (int)(t / cout), co = (int)(t - (long long)f * cout);
-    const int mb = f >> 7, m = f & 127;
-    const float* src = part + ((long long)mb * nsplit * BM + m) * npad + co;
+// dw[f][co] = sum over splits of part[f / 128][s][f % 128][co] in a fixed order
+// (eight interleaved partial sums, then those in order); row f = kcin (the
+// all-ones A row, when kcin % 128 != 0) is db.  One block per row f:
+// 32 channels x 8 split lanes, looping over channel groups of 32.
+__global__ void __launch_bounds__(256) wgrad_reduce_tc_kernel(const float* __restrict__ part, int nsplit, int npad,
+                                                              int kcin, int cout, float* __restrict__ dw,
+                                                              float* __restrict__ db) {
+  __shared__ float acc[8][32];
+  const int f = blockIdx.x, cl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mb = f >> 7, m = f & 127;
+  for (int co0 = 0; co0 < cout; co0 += 32) {
+    const int co = co0 + lane;
     float s = 0.f;
-    for (int k = 0; k < nsplit; ++k) s += src[(long long)k * BM * npad];
-    if (f < kcin) dw[t] = s;
-    else db[co] = s;
+    if (co < cout) {
+      const float* src = part + ((long long)mb * nsplit * BM + m) * npad + co;
+      for (int k = cl; k < nsplit; k += 8) s += __ldg(src + (long long)k * BM * npad);
+    }
+    acc[cl][lane] = s;
+    __syncthreads();
+    if (cl == 0 && co < cout) {
+      float t = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += acc[k][lane];
+      if (f < kcin) dw[(long long)f * cout + co] = t;
+      else if (db) db[co] = t;
+    }
+    __syncthreads();
   }
 }
 
@@ -386,8 +398,8 @@ extern "C" int fpvs_spconv_wgrad_tc(const void* x, int ldx, const void* dz, int 
   int rc = p.npad == 16 ? wg::launch<16>(p, s) : p.npad == 32 ? wg::launch<32>(p, s) : p.npad == 64 ? wg::launch<64>(p, s)
          : p.npad == 128 ? wg::launch<128>(p, s) : wg::launch<256>(p, s);
   if (rc) return rc;
-  const long long total = (long long)(K * cin + 1) * cout;
-  wg::wgrad_reduce_tc_kernel<<<grid_for(total, 256), 256, 0, s>>>(p.part, p.nsplit, p.npad, K * cin, cout, dw, db);
+  const int rows = K * cin + ((db && (K * cin) % 128) ? 1 : 0);
+  wg::wgrad_reduce_tc_kernel<<<rows, 256, 0, s>>>(p.part, p.nsplit, p.npad, K * cin, cout, dw, db);
   if (db && (K * cin) % 128 == 0) {
     float* bpart = (float*)((uint8_t*)workspace + wg::align256((size_t)p.nmb * p.nsplit * tc::BM * p.npad * 4));
     const int nb = (cap + wg::DB_ROWS - 1) / wg::DB_ROWS;

@@ -226,7 +226,8 @@ class TrainStep:
         if self.halo_wgrad:
             self.halo_builder.run(stream)
             halo = sp._halo_tables(lv)
-        _lib.call("fpvs_cast_bf16", _lib.ptr(self.dlogits), cap * self.dlogits.shape[1], _lib.ptr(self.dlog16), s)
+        _lib.call("fpvs_cast_bf16_rows", _lib.ptr(self.dlogits), self.dlogits.shape[1], _lib.ptr(lv.n), cap,
+                  _lib.ptr(self.dlog16), s)
         dz, lddz = self.dlog16, self.dlog16.shape[1]
         for li in reversed(range(len(net.layers))):
             layer = net.layers[li]
