@@ -251,19 +251,45 @@ __device__ __forceinline__ int first_row_of(const int4* coords, int n, int b) {
   return lo;
 }
 
-// one block per sample: sums[b] = (TP, sum p, GTP); fixed-order tree reduction
-__global__ void loss_sums_kernel(const double2* __restrict__ rows, const int4* __restrict__ coords,
-                                 const int* __restrict__ n_dev, int cap, const uint8_t* __restrict__ gt,
-                                 long long grid_bytes, double* __restrict__ sums) {
+// sums[b] = (TP, sum p, GTP): LOSS_G blocks per sample each reduce a slice of
+// the sample's rows and of its packed labels (16-byte popcounts) with a
+// fixed-order tree, then one warp adds the slices in order (deterministic)
+constexpr int LOSS_G = 16;
+__global__ void __launch_bounds__(256) loss_sums_part_kernel(const double2* __restrict__ rows,
+                                                             const int4* __restrict__ coords,
+                                                             const int* __restrict__ n_dev, int cap,
+                                                             const uint8_t* __restrict__ gt, long long grid_bytes,
+                                                             double* __restrict__ part) {
   __shared__ double r0[256], r1[256], r2[256];
   const int n = min(*n_dev, cap);
-  const int b = blockIdx.x;
+  const int g = blockIdx.x, b = blockIdx.y;
   const int i0 = first_row_of(coords, n, b), i1 = first_row_of(coords, n, b + 1);
-  double a = 0.0, s = 0.0, g = 0.0;
-  for (int i = i0 + threadIdx.x; i < i1; i += 256) { a += rows[i].x; s += rows[i].y; }
+  const int a0 = i0 + (int)((long long)(i1 - i0) * g / LOSS_G), a1 = i0 + (int)((long long)(i1 - i0) * (g + 1) / LOSS_G);
+  double a = 0.0, s = 0.0, c = 0.0;
+  for (int i = a0 + threadIdx.x; i < a1; i += 256) {
+    const double2 v = rows[i];
+    a += v.x;
+    s += v.y;
+  }
   const uint8_t* gb = gt + (long long)b * grid_bytes;
-  for (long long e = threadIdx.x; e < grid_bytes; e += 256) g += __popc((unsigned)gb[e]);
-  r0[threadIdx.x] = a; r1[threadIdx.x] = s; r2[threadIdx.x] = g;
+  const long long nv = grid_bytes / 16;  // whole 16-byte vectors, the tail bytes by block 0
+  const long long v0 = nv * g / LOSS_G, v1 = nv * (g + 1) / LOSS_G;
+  const bool aligned = (((uintptr_t)gb) & 15) == 0;
+  unsigned cnt = 0;
+  if (aligned) {
+    const uint4* gv = reinterpret_cast<const uint4*>(gb);
+    for (long long e = v0 + threadIdx.x; e < v1; e += 256) {
+      const uint4 w = __ldg(gv + e);
+      cnt += __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
+    }
+    if (g == 0)
+      for (long long e = nv * 16 + threadIdx.x; e < grid_bytes; e += 256) cnt += __popc((unsigned)gb[e]);
+  } else {
+    const long long e0 = grid_bytes * g / LOSS_G, e1 = grid_bytes * (g + 1) / LOSS_G;
+    for (long long e = e0 + threadIdx.x; e < e1; e += 256) cnt += __popc((unsigned)gb[e]);
+  }
+  c = (double)cnt;
+  r0[threadIdx.x] = a; r1[threadIdx.x] = s; r2[threadIdx.x] = c;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
     if (threadIdx.x < o) {
@@ -273,7 +299,21 @@ __global__ void loss_sums_kernel(const double2* __restrict__ rows, const int4* _
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) { sums[3 * b] = r0[0]; sums[3 * b + 1] = r1[0]; sums[3 * b + 2] = r2[0]; }
+  if (threadIdx.x == 0) {
+    double* o = part + ((long long)b * LOSS_G + g) * 3;
+    o[0] = r0[0]; o[1] = r1[0]; o[2] = r2[0];
+  }
+}
+
+__global__ void loss_sums_final_kernel(const double* __restrict__ part, int B, double* __restrict__ sums) {
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    for (int g = 0; g < LOSS_G; ++g) {
+      const double* o = part + ((long long)b * LOSS_G + g) * 3;
+      t0 += o[0]; t1 += o[1]; t2 += o[2];
+    }
+    sums[3 * b] = t0; sums[3 * b + 1] = t1; sums[3 * b + 2] = t2;
+  }
 }
 
 struct LossCoef { double g1, g0, loss; };
@@ -301,15 +341,35 @@ __global__ void loss_grad_kernel(const float* __restrict__ probs, int C, const i
                                  const int* __restrict__ n_dev, int cap, const uint8_t* __restrict__ gt, int d, int Nx,
                                  int Ny, int Nz, const double* __restrict__ sums, int B, double alpha, double lam,
                                  float* __restrict__ dlogits) {
+  // per-sample coefficients once per block (B <= kMaxB), else per element
+  constexpr int kMaxB = 256;
+  __shared__ double s_g1[kMaxB], s_g0[kMaxB];
+  const bool cached = B <= kMaxB;
+  if (cached)
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+      const LossCoef lc = loss_coef(sums, b, alpha, lam);
+      s_g1[b] = lc.g1;
+      s_g0[b] = lc.g0;
+    }
+  __syncthreads();
   const int n = min(*n_dev, cap);
   const long long total = (long long)n * C;
+  const int lc2 = (C & (C - 1)) == 0 ? __ffs(C) - 1 : -1;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    long long i = t / C;
-    int k = t % C;
+    const long long i = lc2 >= 0 ? (t >> lc2) : t / C;
+    const int k = (int)(t - i * C);
     int4 c = coords[i];
-    LossCoef lc = loss_coef(sums, c.x, alpha, lam);
-    double gp = label_bit(gt, c, k, d, Nx, Ny, Nz) ? lc.g1 : lc.g0;
+    double g1, g0;
+    if (cached) {
+      g1 = s_g1[c.x];
+      g0 = s_g0[c.x];
+    } else {
+      const LossCoef lc = loss_coef(sums, c.x, alpha, lam);
+      g1 = lc.g1;
+      g0 = lc.g0;
+    }
+    double gp = label_bit(gt, c, k, d, Nx, Ny, Nz) ? g1 : g0;
     double p = probs[t];
     dlogits[t] = (float)(gp * p * (1.0 - p) / B);  // sigmoid' = y(1-y) (neural.py:229-230)
   }
@@ -471,7 +531,8 @@ extern "C" int fpvs_spconv_wgrad_simt(const void* x, int ldx, int x_dtype, const
 }
 
 extern "C" size_t fpvs_loss_sums_size(int B, int cap) {
-  return sizeof(double) * (3 * (size_t)B + ((3 * (size_t)B) & 1) + 2 * (size_t)cap);
+  // [B][3] results, cap double2 row partials, [B][LOSS_G][3] slice partials
+  return sizeof(double) * (3 * (size_t)B + ((3 * (size_t)B) & 1) + 2 * (size_t)cap + 3 * (size_t)B * fpvs::LOSS_G);
 }
 
 extern "C" int fpvs_loss_counts(const float* probs, int C, const int32_t* coords, const int32_t* n_dev, int cap,
@@ -485,8 +546,10 @@ extern "C" int fpvs_loss_counts(const float* probs, int C, const int32_t* coords
   double2* rows = reinterpret_cast<double2*>(sums + 3 * (size_t)B + ((3 * (size_t)B) & 1));
   loss_rows_kernel<<<grid_for(cap, 256), 256, 0, s>>>(probs, C, (const int4*)coords, n_dev, cap, gt_bits, d, Nx, Ny,
                                                       Nz, rows);
-  loss_sums_kernel<<<B, 256, 0, s>>>(rows, (const int4*)coords, n_dev, cap, gt_bits,
-                                     (long long)(Nx / 8) * Ny * Nz, sums);
+  double* part = reinterpret_cast<double*>(rows + cap);
+  loss_sums_part_kernel<<<dim3(LOSS_G, B), 256, 0, s>>>(rows, (const int4*)coords, n_dev, cap, gt_bits,
+                                                        (long long)(Nx / 8) * Ny * Nz, part);
+  loss_sums_final_kernel<<<1, 32, 0, s>>>(part, B, sums);
   FPVS_CHECK_LAUNCH("fpvs_loss_counts");
   return FPVS_OK;
 }
