@@ -480,6 +480,41 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
               uint32_t* word = reinterpret_cast<uint32_t*>(p.out_bits + (byte & ~3LL));
               atomicOr(word, rb << ((int)(byte & 3) * 8 + (fx & 7)));
             }
+          } else if (d <= 8 && (d & (d - 1)) == 0 && cb + 8 <= p.cout && (p.cout & 7) == 0) {
+            // probabilities / logits requested (training): vector stores, and the
+            // [p >= tau] bits one RED.OR per (ly, lz) row of the cell as above
+            const int dl2 = __ffs(d) - 1;
+            float z8[8], p8[8];
+            uint32_t bits8 = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              z8[i] = v[i] + s_bias[cb + i];
+              p8[i] = sigmoidf_stable(z8[i]);
+              bits8 |= (p8[i] >= p.tau ? 1u : 0u) << i;
+            }
+            if (p.logits) {
+              float4* lg = reinterpret_cast<float4*>(p.logits + (long long)row * p.cout + cb);
+              lg[0] = make_float4(z8[0], z8[1], z8[2], z8[3]);
+              lg[1] = make_float4(z8[4], z8[5], z8[6], z8[7]);
+            }
+            if (p.probs) {
+              float4* pp = reinterpret_cast<float4*>(p.probs + (long long)row * p.cout + cb);
+              pp[0] = make_float4(p8[0], p8[1], p8[2], p8[3]);
+              pp[1] = make_float4(p8[4], p8[5], p8[6], p8[7]);
+            }
+            if (bits8 && p.out_bits) {
+              const uint32_t dm = (1u << d) - 1u;
+              for (int q = 0; q < (8 >> dl2); ++q) {
+                const uint32_t rb = (bits8 >> (q * d)) & dm;
+                if (!rb) continue;
+                const int rr = (cb >> dl2) + q;  // rr = ly + d*lz
+                const int ly = rr & (d - 1), lz = rr >> dl2;
+                const int fx = cc.y * d;
+                const long long byte = bit_byte(cc.x, fx, cc.z * d + ly, cc.w * d + lz, p.Nx, p.Ny, p.Nz);
+                uint32_t* word = reinterpret_cast<uint32_t*>(p.out_bits + (byte & ~3LL));
+                atomicOr(word, rb << ((int)(byte & 3) * 8 + (fx & 7)));
+              }
+            }
           } else {
 #pragma unroll 1
             for (int i = 0; i < 8; ++i) {
