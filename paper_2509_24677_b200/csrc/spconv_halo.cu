@@ -264,7 +264,7 @@ struct Unit {
 
 template <int BN>
 struct Cfg {
-  static constexpr int G = BN == 64 ? 2 : 1;  // chunks per stage (BN >= 128: deeper weight prefetch instead)
+  static constexpr int G = BN <= 64 ? 2 : 1;  // chunks per stage (BN >= 128: deeper weight prefetch instead)
   static constexpr int NACC = BN == 256 ? 1 : 2;
   static constexpr int NHB = BN == 256 ? 1 : 2;
   static constexpr int NS = 4;
@@ -323,7 +323,16 @@ __device__ __forceinline__ void unit_of(const Params& p, int u, int cpo, int mti
   U.mt = item / p.nblk;
   U.nb = item - U.mt * p.nblk;
   U.mask = __ldg(p.tile_masks + U.mt);
-  if (!U.mask) U.mask = 1u << 13;
+  if (p.cin == 32) {
+    // Cin = 32: a 64-wide K chunk is an offset PAIR (2t, 2t + 1) x 32 channels,
+    // the chunk order of the flattened (j, ci) weights; the walk runs over pairs
+    uint32_t pm = 0;
+#pragma unroll
+    for (int t = 0; t < 14; ++t) pm |= ((U.mask >> (2 * t)) & 3u) ? (1u << t) : 0u;
+    U.mask = pm ? pm : 1u << 6;
+  } else if (!U.mask) {
+    U.mask = 1u << 13;
+  }
   U.npres = __popc(U.mask);
   // 32-bit: L <= 27 * Cin / 64 (a 64-bit divide is a long software sequence on
   // the MMA thread's critical path at every unit boundary)
@@ -400,7 +409,8 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   const int n = min(*p.n_dev, p.cap);
   const int mtiles = (n + BM - 1) / BM;
   const int nunits = num_units(p, mtiles);
-  const int cpo = p.cin / BK;
+  const int cpo = p.cin == 32 ? 1 : p.cin / BK;  // chunks per offset (per offset pair at Cin 32)
+  const bool pair = p.cin == 32;
 
   if (tid == 0) {
     for (int s = 0; s < C::NS; ++s) {
@@ -469,9 +479,11 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
           const int* hr = reinterpret_cast<const int*>(smem + hb * HBUF + ROWS_OFF);
           const char* xb = reinterpret_cast<const char*>(p.x) + c * 128 + pc * 16;
           const uint32_t hs = smem_u32(smem + hb * HBUF);
+          if (!pair || pc < 4) {
 #pragma unroll 4
-          for (int i = pt >> 3; i < H; i += (LOADERS + 256) / 8)
-            cp_async16(hs + i * 128 + ((pc ^ (i & 7)) << 4), xb + (long long)hr[i] * ldx2, 16);
+            for (int i = pt >> 3; i < H; i += (LOADERS + 256) / 8)
+              cp_async16(hs + i * 128 + ((pc ^ (i & 7)) << 4), xb + (long long)hr[i] * ldx2, 16);
+          }
           cp_async_mbar_arrive_noinc(smem_u32(hfull + hb));
         } else {
           mbar_arrive(smem_u32(hfull + hb));  // builders add no copies to later halos
@@ -486,8 +498,36 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
           if ((i & 1) != bg) continue;
           const uint32_t st = sc0 + i / C::G;
           const int stage = (int)(st % C::NS);
-          const int li = ln[j];
           uint32_t v[32];
+          if (pair) {
+            // columns 0-31: offset 2j's neighbour (32 channels), 32-63: offset 2j+1's
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int jj = 2 * j + h;
+              const int li = jj < KOFF ? ln[jj] : -1;
+              if (li >= 0) {
+                const uint8_t* src = hbuf + li * 128;
+                const int sw = li & 7;
+#pragma unroll
+                for (int pc = 0; pc < 4; ++pc) {
+                  const uint4 t4 = *reinterpret_cast<const uint4*>(src + ((pc ^ sw) << 4));
+                  v[16 * h + 4 * pc] = t4.x; v[16 * h + 4 * pc + 1] = t4.y;
+                  v[16 * h + 4 * pc + 2] = t4.z; v[16 * h + 4 * pc + 3] = t4.w;
+                }
+              } else {
+                const int g = li == -2 ? __ldg(p.nbr + ((long long)U.mt * BM + r) * KOFF + jj) : -1;
+                const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(p.x) +
+                                                                  (long long)(g >= 0 ? g : 0) * ldx2);
+#pragma unroll
+                for (int pc = 0; pc < 4; ++pc) {
+                  const uint4 t4 = g >= 0 ? __ldg(src + pc) : make_uint4(0u, 0u, 0u, 0u);
+                  v[16 * h + 4 * pc] = t4.x; v[16 * h + 4 * pc + 1] = t4.y;
+                  v[16 * h + 4 * pc + 2] = t4.z; v[16 * h + 4 * pc + 3] = t4.w;
+                }
+              }
+            }
+          } else {
+          const int li = ln[j];
           if (li >= 0) {
             const uint8_t* src = hbuf + li * 128;
             const int sw = li & 7;
@@ -508,6 +548,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
               const uint4 t4 = __ldg(src + pc);
               v[4 * pc] = t4.x; v[4 * pc + 1] = t4.y; v[4 * pc + 2] = t4.z; v[4 * pc + 3] = t4.w;
             }
+          }
           }
           mbar_wait(smem_u32(empty + stage), ((st / C::NS) & 1) ^ 1);
           tc_fence_after();
@@ -567,10 +608,12 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         // the first halo is shared with the builders: loader thread tl takes rows
         // tl/8 + 40k of the 320-thread split; later halos rows tl/8 + 8k
         const int rstep = gc == 0 ? (LOADERS + 256) / 8 : LOADERS / 8;
+        if (!pair || pc < 4) {  // 32-channel rows: four 16-byte pieces
 #pragma unroll 4
-        for (int i = tl >> 3; i < H; i += rstep) {
-          const int g = hr[i];
-          cp_async16(hs + i * 128 + ((pc ^ (i & 7)) << 4), xb + (long long)g * ldx2, 16);
+          for (int i = tl >> 3; i < H; i += rstep) {
+            const int g = hr[i];
+            cp_async16(hs + i * 128 + ((pc ^ (i & 7)) << 4), xb + (long long)g * ldx2, 16);
+          }
         }
         cp_async_mbar_arrive_noinc(smem_u32(hfull + hb));
         if (tl == 0) HTS(18 + 3 * gc);
@@ -824,7 +867,7 @@ extern "C" int fpvs_kmap_halo(const int32_t* nbr, const int32_t* n_dev, int cap,
 }
 
 extern "C" size_t fpvs_spconv_halo_workspace_size(int cap, int cout, int bn, int split) {
-  if (cap < 1 || (bn != 64 && bn != 128 && bn != 256) || split == 0) return 0;
+  if (cap < 1 || (bn != 32 && bn != 64 && bn != 128 && bn != 256) || split == 0) return 0;
   if (cout % bn) return 0;
   const size_t tiles = (cap + tc::BM - 1) / tc::BM, nblk = cout / bn;
   // split < 0: only the last partial wave (< one grid of items) is split
@@ -842,17 +885,18 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
                                 void* ws, size_t ws_bytes, void* stream) {
   FPVS_CHECK_ARG(x && nbr && lnbr && halo_rows && halo_n && tile_masks && n_dev && w_packed && y,
                  "null pointer");
-  if (bn == 0) bn = cout % 256 == 0 ? 256 : cout % 128 == 0 ? 128 : 64;
+  if (bn == 0) bn = cout % 256 == 0 ? 256 : cout % 128 == 0 ? 128 : cout % 64 == 0 ? 64 : 32;
   if (split == 0) split = 1;
-  FPVS_CHECK_ARG(bn == 64 || bn == 128 || bn == 256, "halo conv tile width must be 64, 128 or 256");
-  FPVS_CHECK_ARG(cin % 64 == 0 && cin >= 64, "halo conv needs Cin %% 64 == 0, got %d", cin);
+  FPVS_CHECK_ARG(bn == 32 || bn == 64 || bn == 128 || bn == 256, "halo conv tile width must be 32, 64, 128 or 256");
+  FPVS_CHECK_ARG((cin % 64 == 0 && cin >= 64) || cin == 32, "halo conv needs Cin %% 64 == 0 or Cin = 32, got %d",
+                 cin);
   FPVS_CHECK_ARG(cout % bn == 0 && cout <= 1024, "halo conv needs Cout %% %d == 0, got %d", bn, cout);
   FPVS_CHECK_ARG(ldx % 8 == 0 && ldx >= cin, "bad input leading dimension");
   FPVS_CHECK_ARG((long long)x_rows * ldx * 2 < (1LL << 31), "feature buffer too large for 32-bit row offsets");
   FPVS_CHECK_ARG(ldy % 8 == 0 && col_off % 8 == 0 && ldy >= col_off + cout, "bad output leading dimension");
   FPVS_CHECK_ARG(act == FPVS_ACT_NONE || act == FPVS_ACT_RELU, "halo conv epilogue supports none/relu");
-  FPVS_CHECK_ARG(split != 0 && (split < 0 ? -split : split) <= 27 * (cin / 64),
-                 "|split| must lie in [1, 27 * Cin / 64]");
+  FPVS_CHECK_ARG(split != 0 && (split < 0 ? -split : split) <= (27 * cin + 63) / 64,
+                 "|split| must lie in [1, ceil(27 * Cin / 64)]");
   const size_t need = fpvs_spconv_halo_workspace_size(cap, cout, bn, split);
   FPVS_CHECK_ARG(ws && ws_bytes >= need, "workspace too small: need %zu bytes", need);
   if (cap <= 0) return FPVS_OK;
@@ -867,7 +911,7 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
   p.n_dev = n_dev;
   p.cap = cap;
   p.wpk = (const uint8_t*)w_packed;
-  p.nchunks = 27 * cin / 64;
+  p.nchunks = (27 * cin + 63) / 64;
   p.nblk = cout / bn;
   p.split = split;
   p.smax = split < 0 ? -split : split;
@@ -884,6 +928,7 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
   p.part = (float*)((uint8_t*)ws + halo::align256(items * 4));
   const char* dbg = getenv("FPVS_HALO_DEBUG");
   p.dbg = dbg ? atoi(dbg) : 0;
+  if (bn == 32) return halo::launch<32>(p, as_stream(stream));
   if (bn == 64) return halo::launch<64>(p, as_stream(stream));
   if (bn == 128) return halo::launch<128>(p, as_stream(stream));
   return halo::launch<256>(p, as_stream(stream));

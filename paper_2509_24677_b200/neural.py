@@ -277,7 +277,7 @@ def pick_bn(cout: int, rows: int, sms: int = 148) -> int:
 
 def halo_ok(K: int, cin: int, cout: int, dtype=None) -> bool:
     """Shapes the halo-cached tensor-core conv (fpvs_spconv_halo) takes."""
-    return K == 27 and cin % 64 == 0 and cout % 64 == 0 and cout <= 1024
+    return K == 27 and (cin % 64 == 0 or cin == 32) and cout % 32 == 0 and cout <= 1024
 
 
 def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int, col_off: int = 0,

@@ -145,7 +145,10 @@ def _rows(n, c, seed, cap):
                                                (128, 128, 128, 3), (256, 128, 128, 1), (256, 256, 128, 5),
                                                (256, 256, 64, 2), (128, 128, 64, 8), (256, 256, 256, 1),
                                                (256, 256, 256, 3), (128, 256, 256, 2), (64, 64, 64, 3),
-                                               (64, 64, 64, -2), (128, 128, 128, -3)])
+                                               (64, 64, 64, -2), (128, 128, 128, -3),
+                                               # Cin = 32: 64-wide K chunks are offset pairs
+                                               (32, 32, 32, 1), (32, 32, 32, 2), (32, 32, 32, -2), (32, 64, 64, 1),
+                                               (32, 64, 32, 3), (32, 128, 128, 1)])
 def test_halo_conv_vs_oracle(cin, cout, bn, split):
     import torch
     from paper_2509_24677_b200 import sparse as sp
@@ -200,12 +203,13 @@ def test_halo_conv_tail_balancing_more_tiles_than_sms():
     assert torch.equal(ya[:full], yb[:full])
 
 
-def test_halo_conv_direct_read_path():
+@pytest.mark.parametrize("cin,bn", [(64, 64), (32, 32)])
+def test_halo_conv_direct_read_path(cin, bn):
     """Tiles whose halo overflows the cache read uncached rows straight from HBM."""
     import torch
     from paper_2509_24677_b200 import sparse as sp
     rng = np.random.default_rng(11)
-    n, cap, cin, cout = 600, 640, 64, 64
+    n, cap, cout = 600, 640, 64
     nbr = rng.integers(0, n, size=(n, 27))
     nbr[rng.random((n, 27)) < 0.4] = -1
     nbr[:, 13] = np.arange(n)
@@ -222,7 +226,7 @@ def test_halo_conv_direct_read_path():
     w = osp.bf16_round(layer.w.cpu().numpy())
     b = layer.b.cpu().numpy().astype(np.float64)
     y = torch.zeros((cap, cout), dtype=torch.bfloat16, device="cuda")
-    _run_halo(layer, xt, cin, lv, lv.nbr, h, y, cout, 0, 64, 1, act="none")
+    _run_halo(layer, xt, cin, lv, lv.nbr, h, y, cout, 0, bn, 1, act="none")
     z = osp.gather_conv(xv.astype(np.float64), nbr.astype(np.int64), w, b)
     got = y[:n].float().cpu().numpy()
     assert np.all(np.abs(got - z) <= np.abs(z) * 2.0 ** -8 + 1e-4), np.abs(got - z).max()
