@@ -375,7 +375,7 @@ struct ChunkWalk {
   }
 };
 
-template <int BN>
+template <int BN, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -409,8 +409,10 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   const int n = min(*p.n_dev, p.cap);
   const int mtiles = (n + BM - 1) / BM;
   const int nunits = num_units(p, mtiles);
-  const int cpo = p.cin == 32 ? 1 : p.cin / BK;  // chunks per offset (per offset pair at Cin 32)
-  const bool pair = p.cin == 32;
+  // Cin 32 (PAIR): one 64-wide chunk per offset pair; the 64k-channel kernels
+  // are compiled without the pair paths
+  const int cpo = PAIR ? 1 : p.cin / BK;
+  constexpr bool pair = PAIR;
 
   if (tid == 0) {
     for (int s = 0; s < C::NS; ++s) {
@@ -797,18 +799,19 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   }
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 int launch(const Params& p, cudaStream_t s) {
   using C = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(spconv_halo_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(spconv_halo_kernel<BN, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     configured = true;
   }
   const long long units = (long long)((p.cap + BM - 1) / BM) * p.nblk * p.smax;
   const int grid = (int)(units < kNumSMs ? (units < 1 ? 1 : units) : kNumSMs);
-  cudaError_t e = launch_kernel(spconv_halo_kernel<BN>, dim3(grid), dim3(THREADS), C::SMEM, s, p);
+  cudaError_t e = launch_kernel(spconv_halo_kernel<BN, PAIR>, dim3(grid), dim3(THREADS), C::SMEM, s, p);
   if (e != cudaSuccess) return set_error(FPVS_ECUDA, "spconv_halo: %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("spconv_halo");
   return FPVS_OK;
@@ -928,8 +931,15 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
   p.part = (float*)((uint8_t*)ws + halo::align256(items * 4));
   const char* dbg = getenv("FPVS_HALO_DEBUG");
   p.dbg = dbg ? atoi(dbg) : 0;
-  if (bn == 32) return halo::launch<32>(p, as_stream(stream));
-  if (bn == 64) return halo::launch<64>(p, as_stream(stream));
-  if (bn == 128) return halo::launch<128>(p, as_stream(stream));
-  return halo::launch<256>(p, as_stream(stream));
+  const cudaStream_t st = as_stream(stream);
+  if (cin == 32) {
+    if (bn == 32) return halo::launch<32, true>(p, st);
+    if (bn == 64) return halo::launch<64, true>(p, st);
+    if (bn == 128) return halo::launch<128, true>(p, st);
+    return halo::launch<256, true>(p, st);
+  }
+  if (bn == 32) return halo::launch<32, false>(p, st);
+  if (bn == 64) return halo::launch<64, false>(p, st);
+  if (bn == 128) return halo::launch<128, false>(p, st);
+  return halo::launch<256, false>(p, st);
 }
