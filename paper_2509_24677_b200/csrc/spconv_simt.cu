@@ -11,6 +11,7 @@
 // The fp32 mode must not use TF32 tensor cores: its
 // logits are checked to 1e-4 against the float64 oracle.
 #include "common.cuh"
+#include <stdlib.h>
 
 namespace fpvs {
 
@@ -99,6 +100,140 @@ __global__ void __launch_bounds__(256) spconv_simt_kernel(
         y[(long long)row * ldy + col_off + co] = from_f32<Tout>(z);
       }
     }
+  }
+}
+
+// fp32 forward for the chain nets (config 1's precision): a 64-row x Cout
+// tile per CTA (Cout 32 or 64, Cin <= 64 and a multiple of 4).  The tile's
+// neighbour rows are staged in shared memory first and give the offsets
+// present anywhere in the tile; only those offsets are gathered (float4 rows)
+// and multiplied, two offsets in flight (the next offset's gather is issued
+// into registers before the current one's FMAs).  4 x 4 outputs per thread,
+// fp32 FMA in offset order (deterministic).
+constexpr int kT2M = 64;
+constexpr int kT2CinMax = 64;
+
+template <int TN>
+__global__ void __launch_bounds__(kT2M * TN / 16) spconv_simt_tap_kernel(
+    const float* __restrict__ x, int ldx, const int* __restrict__ nbr, int K, const int* __restrict__ n_dev, int cap,
+    const float* __restrict__ w, const float* __restrict__ bias, int cin, int cout, int act, float* __restrict__ y,
+    int ldy, int col_off) {
+  constexpr int NT = kT2M * TN / 16;
+  extern __shared__ __align__(16) float sm2[];
+  float* As = sm2;                                   // [2][cin][kT2M + 4]
+  float* Bs = As + 2 * kT2CinMax * (kT2M + 4);       // [2][cin][TN]
+  int* snb = reinterpret_cast<int*>(Bs + 2 * kT2CinMax * TN);  // [kT2M][K]
+  __shared__ unsigned s_mask;
+  const int n = min(*n_dev, cap);
+  const int tx = threadIdx.x % (TN / 4), ty = threadIdx.x / (TN / 4);
+  const int c4n = cin / 4;
+  const int mt = (n + kT2M - 1) / kT2M;
+  for (int tile = blockIdx.x; tile < mt; tile += gridDim.x) {
+    const int m0 = tile * kT2M;
+    if (threadIdx.x == 0) s_mask = 0u;
+    __syncthreads();
+    unsigned mloc = 0u;
+    for (int e = threadIdx.x; e < kT2M * K; e += NT) {
+      const int r = e / K, j = e - r * K;
+      const int row = m0 + r;
+      int v = -1;
+      if (row < n) v = nbr ? __ldg(nbr + (long long)row * K + j) : row;
+      snb[e] = v;
+      if (v >= 0) mloc |= 1u << j;
+    }
+    atomicOr(&s_mask, mloc);
+    __syncthreads();
+    unsigned mask = s_mask;
+    float acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+    // register staging of one offset: A pieces (row, 4 channels) and B pieces
+    constexpr int AMAX = kT2M * kT2CinMax / 4 / NT + 1;
+    constexpr int BMAX = kT2CinMax * TN / 4 / NT + 1;
+    float4 ra[AMAX], rb[BMAX];
+    auto fetch = [&](int j) {
+#pragma unroll
+      for (int i = 0; i < AMAX; ++i) {
+        const int e = threadIdx.x + i * NT;
+        ra[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e < kT2M * c4n) {
+          const int r = e % kT2M, c4 = e / kT2M;
+          const int src = snb[r * K + j];
+          if (src >= 0) ra[i] = __ldg(reinterpret_cast<const float4*>(x + (long long)src * ldx) + c4);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < BMAX; ++i) {
+        const int e = threadIdx.x + i * NT;
+        rb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e < cin * (TN / 4)) {
+          const int k = e / (TN / 4), c4 = e - k * (TN / 4);
+          if (c4 * 4 < cout) rb[i] = __ldg(reinterpret_cast<const float4*>(w + ((long long)j * cin + k) * cout) + c4);
+        }
+      }
+    };
+    auto stash = [&](int buf) {
+      float* a = As + buf * kT2CinMax * (kT2M + 4);
+      float* b = Bs + buf * kT2CinMax * TN;
+#pragma unroll
+      for (int i = 0; i < AMAX; ++i) {
+        const int e = threadIdx.x + i * NT;
+        if (e < kT2M * c4n) {
+          const int r = e % kT2M, c4 = e / kT2M;
+          a[(c4 * 4 + 0) * (kT2M + 4) + r] = ra[i].x;
+          a[(c4 * 4 + 1) * (kT2M + 4) + r] = ra[i].y;
+          a[(c4 * 4 + 2) * (kT2M + 4) + r] = ra[i].z;
+          a[(c4 * 4 + 3) * (kT2M + 4) + r] = ra[i].w;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < BMAX; ++i) {
+        const int e = threadIdx.x + i * NT;
+        if (e < cin * (TN / 4)) reinterpret_cast<float4*>(b)[e] = rb[i];
+      }
+    };
+    int j = mask ? __ffs(mask) - 1 : -1;
+    if (j >= 0) {
+      fetch(j);
+      stash(0);
+    }
+    __syncthreads();
+    int buf = 0;
+    while (j >= 0) {
+      const int jn = __ffs(mask & ~((2u << j) - 1u)) - 1;
+      if (jn >= 0) fetch(jn);  // in flight during the FMAs below
+      const float* a = As + buf * kT2CinMax * (kT2M + 4);
+      const float* b = Bs + buf * kT2CinMax * TN;
+#pragma unroll 4
+      for (int k = 0; k < cin; ++k) {
+        const float4 av = *reinterpret_cast<const float4*>(a + k * (kT2M + 4) + ty * 4);
+        const float4 bv = *reinterpret_cast<const float4*>(b + k * TN + tx * 4);
+        const float aa[4] = {av.x, av.y, av.z, av.w}, bb[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[p][q] = fmaf(aa[p], bb[q], acc[p][q]);
+      }
+      if (jn >= 0) stash(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+      j = jn;
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int row = m0 + ty * 4 + p;
+      if (row >= n) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int co = tx * 4 + q;
+        if (co >= cout) continue;
+        float z = acc[p][q] + (bias ? __ldg(bias + co) : 0.f);
+        y[(long long)row * ldy + col_off + co] = apply_act(z, act);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -436,9 +571,42 @@ __global__ void first_hit_kernel(const uint8_t* __restrict__ bits, int B, int Nx
 
 using namespace fpvs;
 
+// FPVS_SIMT_TAP=0 keeps the fp32 forward on the dense-K tile kernel (A/B checks)
+static bool simt_tap_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FPVS_SIMT_TAP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static int launch_simt(const void* x, int ldx, int in_dtype, const int32_t* nbr, int K, const int32_t* n_dev, int cap,
                        const float* w, int wmode, const float* bias, int cin, int cout, int act, const void* ymask,
                        int mask_bf16, int ldm, void* y, int ldy, int col_off, int out_dtype, cudaStream_t s) {
+  if (in_dtype == FPVS_F32 && out_dtype == FPVS_F32 && wmode == 0 && !ymask && (cout == 32 || cout == 64) &&
+      cin % 4 == 0 && cin <= kT2CinMax && K <= 32 && ldx % 4 == 0 && simt_tap_enabled()) {
+    const int g2 = grid_for((cap + kT2M - 1) / kT2M, 1, 8);
+    const size_t sh = sizeof(float) * (2 * kT2CinMax * (kT2M + 4) + 2 * kT2CinMax * cout) + sizeof(int) * kT2M * K;
+    if (cout == 32) {
+      static bool cfg32 = false;
+      if (!cfg32) {
+        cudaFuncSetAttribute(spconv_simt_tap_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cfg32 = true;
+      }
+      spconv_simt_tap_kernel<32><<<g2, kT2M * 32 / 16, sh, s>>>((const float*)x, ldx, nbr, K, n_dev, cap, w, bias, cin,
+                                                              cout, act, (float*)y, ldy, col_off);
+    } else {
+      static bool cfg64 = false;
+      if (!cfg64) {
+        cudaFuncSetAttribute(spconv_simt_tap_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cfg64 = true;
+      }
+      spconv_simt_tap_kernel<64><<<g2, kT2M * 64 / 16, sh, s>>>((const float*)x, ldx, nbr, K, n_dev, cap, w, bias, cin,
+                                                              cout, act, (float*)y, ldy, col_off);
+    }
+    FPVS_CHECK_LAUNCH("spconv_simt_tap");
+    return FPVS_OK;
+  }
   const long long tiles = (long long)((cap + kTM - 1) / kTM) * ((cout + kTN - 1) / kTN);
   const int g = grid_for(tiles, 1, 4);
 #define FPVS_SIMT(TI, TO)                                                                                  \
