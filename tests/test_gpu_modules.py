@@ -94,3 +94,29 @@ def test_sparse_conv_function_vs_float64():
     assert np.allclose(b.grad.cpu().numpy(), dz.sum(0), atol=1e-3, rtol=1e-4)
     assert np.allclose(x.grad[:n].cpu().numpy(), dx, atol=1e-3, rtol=1e-4)
     assert not x.grad[n:].any()
+
+
+def test_module_bf16_grads_close_to_fp32():
+    """bf16 tensor-core autograd path: loss and per-parameter gradients within bf16 noise of fp32."""
+    import torch
+    from paper_2509_24677_b200 import synth
+    from paper_2509_24677_b200.froxel import FroxelGrid
+    from paper_2509_24677_b200.modules import PvsNetModule
+    from paper_2509_24677_b200.neural import ModelConfig, TrainConfig
+    B, dims = 2, (64, 64, 64)
+    pairs = [synth.config5_pair(2, i) for i in range(B)]
+    pairs = [(g[:64, :64, :64], lb[:64, :64, :64]) for g, lb in pairs]
+    bits = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(g).bits for g, _ in pairs])).cuda()
+    gt = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(lb).bits for _, lb in pairs])).cuda()
+    cfg = ModelConfig.config1()
+    mods = {p: PvsNetModule(cfg, np.random.Generator(np.random.PCG64(5)), precision=p) for p in ("fp32", "bf16")}
+    losses = {}
+    for p, m in mods.items():
+        loss = m.loss(bits, gt, B, dims, TrainConfig())
+        loss.backward()
+        losses[p] = float(loss.detach())
+    torch.cuda.synchronize()
+    assert abs(losses["bf16"] - losses["fp32"]) <= 0.02 * abs(losses["fp32"]) + 1e-4
+    for a, b in zip(mods["bf16"].parameters(), mods["fp32"].parameters()):
+        rel = float((a.grad - b.grad).norm() / (b.grad.norm() + 1e-30))
+        assert rel < 0.05, (a.shape, rel)
