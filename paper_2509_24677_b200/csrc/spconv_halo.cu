@@ -264,10 +264,12 @@ struct Unit {
 
 template <int BN>
 struct Cfg {
-  static constexpr int G = BN <= 64 ? 2 : 1;  // chunks per stage (BN >= 128: deeper weight prefetch instead)
+  // chunks per stage: BN 64 runs 4 chunks (16 MMAs) per stage and commit, two
+  // stages deep; BN >= 128: one chunk per stage, deeper weight prefetch
+  static constexpr int G = BN == 64 ? 4 : BN < 64 ? 2 : 1;
   static constexpr int NACC = BN == 256 ? 1 : 2;
   static constexpr int NHB = BN == 256 ? 1 : 2;
-  static constexpr int NS = 4;
+  static constexpr int NS = BN == 64 ? 2 : 4;
   static constexpr int B_SUB = BN * 128;
   static constexpr int STAGE_B = G * B_SUB;
   static constexpr int ACOL = NACC * BN;  // TMEM: [accumulators | A slots]
@@ -566,12 +568,20 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         ++gc;
       }
       const uint32_t nst = (nq + C::G - 1) / C::G;
-      if (C::G == 2 && (nq & 1) && bg == 1) {
-        // odd chunk count: slot 1 of the unit's last stage stays empty
+      if (C::G > 1 && nq % C::G) {
+        // the unit's last stage is short: its missing slots (built by group
+        // slot & 1, as chunk i goes to group i & 1 and slot i % G) still arrive
         const uint32_t st = sc0 + nst - 1;
-        mbar_wait(smem_u32(empty + st % C::NS), ((st / C::NS) & 1) ^ 1);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(full + st % C::NS));
+        bool waited = false;
+        for (int sl = nq % C::G; sl < C::G; ++sl) {
+          if ((sl & 1) != bg) continue;
+          if (!waited) {
+            mbar_wait(smem_u32(empty + st % C::NS), ((st / C::NS) & 1) ^ 1);
+            waited = true;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(full + st % C::NS));
+        }
       }
       sc0 += nst;
     }
