@@ -403,6 +403,17 @@ size_t fpvs_froxelize_workspace_size(long long ntris, int Nx, int Ny, int Nz, in
 int fpvs_froxelize(const double* verts, long long nverts, const int64_t* tris, long long ntris,
                    const fpvs_frustum* frustum, int Nx, int Ny, int Nz, int supersample, int depth_mode,
                    uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream);
+/* Orthographic three-view froxelization; replaces froxel.py:351-376
+ * froxelize_orthographic() (FroxelizeConfig(mode="ortho"), the dataset
+ * generator's default).  Three axis-aligned passes over the frustum's world
+ * AABB at spacing max(extent) / (supersample * max(N)); every covered sample
+ * point is reconstructed in world space, projected into the frustum and its
+ * froxel bit set.  Same arguments and output as fpvs_froxelize; bit-exact
+ * with the reference in both depth modes. */
+size_t fpvs_froxelize_ortho_workspace_size(long long ntris, int Nx, int Ny, int Nz, int supersample);
+int fpvs_froxelize_ortho(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                         const fpvs_frustum* frustum, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                         uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream);
 /* Ground-truth PVS by dense viewpoint sampling; replaces oracle.py:141-172
  * compute_gt_pvs() (render_depth oracle.py:107-138 per camera, then
  * reprojection core.py:380-452 into the viewcell frustum).  cams: DEVICE

@@ -124,3 +124,90 @@ def froxelize(verts, tris, origin, basis, half_extent, near, far, dims, supersam
         byte = (idx[:, 0] >> 3) + row * (idx[:, 1] + ny * idx[:, 2])
         np.bitwise_or.at(bits, byte, (np.uint8(1) << (idx[:, 0] & 7).astype(np.uint8)).astype(np.uint8))
     return bits
+
+
+# ---------------------------------------------------------------------------
+# orthographic three-view mode (froxel.py:351-376)
+# ---------------------------------------------------------------------------
+
+
+def world_aabb(origin, basis, half_extent, near, far):
+    """core.py:349-354 (unproject_ndc of the 8 NDC corners, linear depth)."""
+    uvw = np.array([[u, v, w] for u in (0, 1) for v in (0, 1) for w in (0, 1)], dtype=np.float64)
+    z = near + uvw[:, 2] * (far - near)
+    x = (2.0 * uvw[:, 0] - 1.0) * half_extent * z
+    y = (2.0 * uvw[:, 1] - 1.0) * half_extent * z
+    corners = np.asarray(origin, dtype=np.float64) + np.column_stack([x, y, z]) @ np.asarray(basis, dtype=np.float64)
+    return corners.min(axis=0), corners.max(axis=0)
+
+
+def project_points(origin, basis, half_extent, near, far, pts, depth_mode="linear"):
+    """core.py:380-405: (uvw, inside)."""
+    local = (pts - np.asarray(origin, dtype=np.float64)) @ np.asarray(basis, dtype=np.float64).T
+    x, y, z = local[:, 0], local[:, 1], local[:, 2]
+    ahead = z > 0
+    zs = np.where(ahead, z, 1.0)
+    u = 0.5 + 0.5 * x / (zs * half_extent)
+    v = 0.5 + 0.5 * y / (zs * half_extent)
+    if depth_mode == "linear":
+        w = (z - near) / (far - near)
+    else:
+        import math
+        w = np.log(np.where(ahead, z, near) / near) / math.log(far / near)
+    inside = ahead & (u >= 0) & (u <= 1) & (v >= 0) & (v <= 1) & (w >= 0) & (w <= 1)
+    return np.column_stack([u, v, w]), inside
+
+
+def froxelize_ortho(verts, tris, origin, basis, half_extent, near, far, dims, supersample=4, depth_mode="linear"):
+    """Three axis-aligned orthographic passes over the frustum's world AABB, every
+    covered sample point reprojected into the frustum (froxel.py:351-376)."""
+    nx, ny, nz = (int(v) for v in dims)
+    bits = np.zeros(nx * ny * nz // 8, dtype=np.uint8)
+    verts = np.asarray(verts, dtype=np.float64).reshape(-1, 3)
+    tris = np.asarray(tris, dtype=np.int64).reshape(-1, 3)
+    if len(tris) == 0:
+        return bits
+    lo, hi = world_aabb(origin, basis, half_extent, near, far)
+    extent = hi - lo
+    spacing = extent.max() / (supersample * max(nx, ny, nz))
+    counts = np.maximum(np.ceil(extent / spacing).astype(np.int64), 1)
+    tv = verts[tris]
+    live = np.nonzero(((tv.max(axis=1) >= lo) & (tv.min(axis=1) <= hi)).all(axis=1))[0]
+    d = np.array([nx, ny, nz], dtype=np.int64)
+    for a0, a1, ar in ((1, 2, 0), (2, 0, 1), (0, 1, 2)):
+        t2 = (tv[live][:, :, [a0, a1]] - lo[[a0, a1]]) / spacing
+        attrs = tv[live][:, :, ar]
+        W, H = int(counts[a0]), int(counts[a1])
+        for t in range(len(live)):
+            u, v = t2[t, :, 0], t2[t, :, 1]
+            e1x, e1y = u[1] - u[0], v[1] - v[0]
+            e2x, e2y = u[2] - u[0], v[2] - v[0]
+            den = e1x * e2y - e2x * e1y
+            x0 = int(np.clip(np.ceil(u.min() - 0.5), 0, W))
+            x1 = int(np.clip(np.floor(u.max() - 0.5) + 1, 0, W))
+            y0 = int(np.clip(np.ceil(v.min() - 0.5), 0, H))
+            y1 = int(np.clip(np.floor(v.max() - 0.5) + 1, 0, H))
+            if not (abs(den) > DEGEN_EPS) or x1 <= x0 or y1 <= y0:
+                continue
+            sv, su = np.mgrid[y0:y1, x0:x1]
+            su, sv = su.ravel(), sv.ravel()
+            dx = (su + 0.5) - u[0]
+            dy = (sv + 0.5) - v[0]
+            b1 = (dx * e2y - e2x * dy) / den
+            b2 = (e1x * dy - dx * e1y) / den
+            b0 = 1.0 - b1 - b2
+            m = (b0 >= 0) & (b1 >= 0) & (b2 >= 0)
+            if not m.any():
+                continue
+            a = attrs[t]
+            world = np.empty((int(m.sum()), 3))
+            world[:, a0] = lo[a0] + (su[m] + 0.5) * spacing
+            world[:, a1] = lo[a1] + (sv[m] + 0.5) * spacing
+            world[:, ar] = a[0] + b1[m] * (a[1] - a[0]) + b2[m] * (a[2] - a[0])
+            uvw, inside = project_points(origin, basis, half_extent, near, far, world, depth_mode)
+            if not inside.any():
+                continue
+            idx = np.clip(np.floor(uvw[inside] * d).astype(np.int64), 0, d - 1)
+            byte = (idx[:, 0] >> 3) + (nx // 8) * (idx[:, 1] + ny * idx[:, 2])
+            np.bitwise_or.at(bits, byte, (np.uint8(1) << (idx[:, 0] & 7).astype(np.uint8)).astype(np.uint8))
+    return bits

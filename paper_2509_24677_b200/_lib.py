@@ -76,6 +76,8 @@ SIGNATURES = {
     "fpvs_froxelize_workspace_size": (_z, [C.c_longlong, _i, _i, _i, _i]),
     "fpvs_froxelize": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _i, _i, _i, _i, _i, _p, _p, _z, _p]),
     "fpvs_froxelize_samples": (C.c_longlong, [_p, _p]),
+    "fpvs_froxelize_ortho_workspace_size": (_z, [C.c_longlong, _i, _i, _i, _i]),
+    "fpvs_froxelize_ortho": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _i, _i, _i, _i, _i, _p, _p, _z, _p]),
     "fpvs_gt_pvs_workspace_size": (_z, [C.c_longlong, _i, _i, _i, _i]),
     "fpvs_cast_bf16_rows": (_i, [_p, _i, _p, _i, _p, _p]),
     "fpvs_kmap_pairs_workspace_size": (_z, [_i, _i]),

@@ -87,6 +87,7 @@ struct Work {
   long long* pairs;               // kMode 2: (froxel * T + triangle) per fragment
   unsigned long long* npairs;
   long long pair_cap;
+  double* oframe;  // ortho mode: lo[3], spacing of the frustum's world AABB (written by the setup)
   double* ufx;  // GT mode: 2 (px + 0.5) / W - 1 per pixel column (core.py:441), nullptr otherwise
   double* ufy;
   long long ntris;
@@ -173,6 +174,63 @@ __device__ unsigned long long make_slot(const Params& p, const V3& a, const V3& 
   return (unsigned long long)s.w * (unsigned long long)s.h;
 }
 
+// Store a thread's two slots, count its work items and scan the block's
+// counts into the block-local prefix (shared by every setup kernel).
+__device__ __forceinline__ void finish_setup(const Params& p, const Work& wk, long long t, unsigned long long c0,
+                                             unsigned long long c1, Slot& s0, Slot& s1) {
+  if (t < wk.ntris) {
+    if (c0) wk.slots[2 * t] = s0;
+    if (c1) wk.slots[2 * t + 1] = s1;
+  }
+  {
+    // candidate samples (bbox areas) for the statistics counter
+    unsigned long long smp = c0 + c1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) smp += __shfl_xor_sync(0xffffffffu, smp, o);
+    if ((threadIdx.x & 31) == 0 && smp) atomicAdd(wk.nsamples, smp);
+  }
+  if (p.rows_mode) {
+    // the span raster's work items: bounding-box rows cut into p.seg-column
+    // segments (h * ceil(w / seg) per slot); wmagic becomes the segment
+    // count's reciprocal for the item -> (row, segment) split
+    if (c0) {
+      const unsigned int ns = (unsigned int)(s0.w + p.seg - 1) / (unsigned int)p.seg;
+      c0 = (unsigned long long)s0.h * ns;
+      s0.wmagic = ns > 1 ? (unsigned int)((0x100000000ull + ns - 1) / ns) : 0xffffffffu;
+      if (t < wk.ntris) wk.slots[2 * t].wmagic = s0.wmagic;
+    }
+    if (c1) {
+      const unsigned int ns = (unsigned int)(s1.w + p.seg - 1) / (unsigned int)p.seg;
+      c1 = (unsigned long long)s1.h * ns;
+      s1.wmagic = ns > 1 ? (unsigned int)((0x100000000ull + ns - 1) / ns) : 0xffffffffu;
+      if (t < wk.ntris) wk.slots[2 * t + 1].wmagic = s1.wmagic;
+    }
+  }
+  // block scan of (c0 + c1)
+  __shared__ unsigned long long warp_tot[kSetupThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long incl = c0 + c1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  unsigned long long base = 0, btot = 0;
+#pragma unroll
+  for (int i = 0; i < kSetupThreads / 32; ++i) {
+    if (i < wid) base += warp_tot[i];
+    btot += warp_tot[i];
+  }
+  const unsigned long long excl = base + incl - (c0 + c1);
+  if (t < wk.ntris) {
+    wk.lp[2 * t] = excl + c0;
+    wk.lp[2 * t + 1] = excl + c0 + c1;
+  }
+  if (threadIdx.x == 0) wk.bsum[blockIdx.x] = btot;
+}
+
 // One thread per (view, scene triangle); flat index f = view * T + tri, slots
 // 2f and 2f+1.  kMulti: the view's frustum comes from views[f / T] (GT-PVS
 // cameras); else from p (froxelize).  Slot.pad records the view.
@@ -234,57 +292,7 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(Params p, const fp
     }
     s0.pad = s1.pad = view;
   }
-  if (t < wk.ntris) {
-    if (c0) wk.slots[2 * t] = s0;
-    if (c1) wk.slots[2 * t + 1] = s1;
-  }
-  {
-    // candidate samples (bbox areas) for the statistics counter
-    unsigned long long smp = c0 + c1;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) smp += __shfl_xor_sync(0xffffffffu, smp, o);
-    if ((threadIdx.x & 31) == 0 && smp) atomicAdd(wk.nsamples, smp);
-  }
-  if (p.rows_mode) {
-    // the span raster's work items: bounding-box rows cut into p.seg-column
-    // segments (h * ceil(w / seg) per slot); wmagic becomes the segment
-    // count's reciprocal for the item -> (row, segment) split
-    if (c0) {
-      const unsigned int ns = (unsigned int)(s0.w + p.seg - 1) / (unsigned int)p.seg;
-      c0 = (unsigned long long)s0.h * ns;
-      s0.wmagic = ns > 1 ? (unsigned int)((0x100000000ull + ns - 1) / ns) : 0xffffffffu;
-      if (t < wk.ntris) wk.slots[2 * t].wmagic = s0.wmagic;
-    }
-    if (c1) {
-      const unsigned int ns = (unsigned int)(s1.w + p.seg - 1) / (unsigned int)p.seg;
-      c1 = (unsigned long long)s1.h * ns;
-      s1.wmagic = ns > 1 ? (unsigned int)((0x100000000ull + ns - 1) / ns) : 0xffffffffu;
-      if (t < wk.ntris) wk.slots[2 * t + 1].wmagic = s1.wmagic;
-    }
-  }
-  // block scan of (c0 + c1)
-  __shared__ unsigned long long warp_tot[kSetupThreads / 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  unsigned long long incl = c0 + c1;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) warp_tot[wid] = incl;
-  __syncthreads();
-  unsigned long long base = 0, btot = 0;
-#pragma unroll
-  for (int i = 0; i < kSetupThreads / 32; ++i) {
-    if (i < wid) base += warp_tot[i];
-    btot += warp_tot[i];
-  }
-  const unsigned long long excl = base + incl - (c0 + c1);
-  if (t < wk.ntris) {
-    wk.lp[2 * t] = excl + c0;
-    wk.lp[2 * t + 1] = excl + c0 + c1;
-  }
-  if (threadIdx.x == 0) wk.bsum[blockIdx.x] = btot;
+  finish_setup(p, wk, t, c0, c1, s0, s1);
 }
 
 __global__ void __launch_bounds__(1024) scan_kernel(Params p, Work wk) {
@@ -546,6 +554,170 @@ struct GtParams {
   long long npix;  // W * H
 };
 
+// Coverage and the reference barycentrics (froxel.py:272-279): false when
+// the sample is outside; samples provably outside skip the divisions.
+__device__ __forceinline__ bool bary_filtered(const Slot& s, double cx, double cy, double& b1, double& b2) {
+  const double dx = dsub(cx, s.v0x), dy = dsub(cy, s.v0y);
+  const double n1 = dsub(dmul(dx, s.e2y), dmul(s.e2x, dy));
+  const double n2 = dsub(dmul(s.e1x, dy), dmul(dx, s.e1y));
+  const bool dneg = s.den < 0;
+  const double a1 = fabs(n1), a2 = fabs(n2);
+  constexpr double kTiny = 1e-250;
+  if (!((a1 != 0 && a1 < kTiny) || (a2 != 0 && a2 < kTiny))) {
+    if ((n1 != 0 && ((n1 < 0) != dneg)) || (n2 != 0 && ((n2 < 0) != dneg))) return false;
+    const double q1 = n1 * s.rden, q2 = n2 * s.rden;
+    if ((1.0 - q1) - q2 < -1e-13 * (1.0 + q1 + q2)) return false;
+  }
+  b1 = ddiv(n1, s.den);
+  b2 = ddiv(n2, s.den);
+  const double b0 = dsub(dsub(1.0, b1), b2);
+  return b0 >= 0 && b1 >= 0 && b2 >= 0;
+}
+
+// The orthographic frame of froxel.py:355-358: the frustum's world AABB
+// (core.py:349-354, unproject_ndc of the 8 NDC corners in linear depth, the
+// corner product in dgemm k = 3 order), the sample spacing and the per-axis
+// sample counts.
+__device__ __forceinline__ void ortho_frame(const GtParams& g, int supersample, double lo[3], double hi[3],
+                                            double& spacing, int counts[3]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = __longlong_as_double(0x7ff0000000000000LL);
+    hi[k] = -lo[k];
+  }
+  for (int c = 0; c < 8; ++c) {
+    const double u = (double)((c >> 2) & 1), v = (double)((c >> 1) & 1), w = (double)(c & 1);
+    const double z = dadd(g.fnear, dmul(w, dsub(g.ffar, g.fnear)));
+    const double x = dmul(dmul(dsub(dmul(2.0, u), 1.0), g.fh), z);
+    const double y = dmul(dmul(dsub(dmul(2.0, v), 1.0), g.fh), z);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double wk = dadd(g.fo[k], __fma_rn(z, g.fb[6 + k], __fma_rn(y, g.fb[3 + k], dmul(x, g.fb[k]))));
+      lo[k] = fmin(lo[k], wk);
+      hi[k] = fmax(hi[k], wk);
+    }
+  }
+  const double e0 = dsub(hi[0], lo[0]), e1 = dsub(hi[1], lo[1]), e2 = dsub(hi[2], lo[2]);
+  const int dmax = max(g.nx, max(g.ny, g.nz));
+  spacing = ddiv(fmax(e0, fmax(e1, e2)), (double)(supersample * dmax));
+  const double e[3] = {e0, e1, e2};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) counts[k] = max((int)ceil(ddiv(e[k], spacing)), 1);
+}
+
+__device__ __forceinline__ int quant_fast(double a, int n, double m);
+__device__ __forceinline__ int quant_exact(double a, int n);
+
+// project_points (core.py:380-405) of a world point into the frustum, then
+// quantize (froxel.py:28-42): froxel (ix, iy, iz) or false when outside.
+// Same filtered divisions as resolve_kernel.
+__device__ __forceinline__ bool project_quantize(const GtParams& g, double wx, double wy, double wz, int& ix,
+                                                 int& iy, int& iz) {
+  constexpr double kM = 1e-12;
+  const double d0 = dsub(wx, g.fo[0]), d1 = dsub(wy, g.fo[1]), d2 = dsub(wz, g.fo[2]);
+  const double lx = __fma_rn(d2, g.fb[2], __fma_rn(d1, g.fb[1], dmul(d0, g.fb[0])));
+  const double ly = __fma_rn(d2, g.fb[5], __fma_rn(d1, g.fb[4], dmul(d0, g.fb[3])));
+  const double lz = __fma_rn(d2, g.fb[8], __fma_rn(d1, g.fb[7], dmul(d0, g.fb[6])));
+  if (!(lz > 0)) return false;
+  const double zh = dmul(lz, g.fh);
+  const double r = rcp_nr(zh);
+  const double rfn = 1.0 / dsub(g.ffar, g.fnear);
+  ix = quant_fast(0.5 + (0.5 * lx) * r, g.nx, kM);
+  iy = ix == -1 ? -1 : quant_fast(0.5 + (0.5 * ly) * r, g.ny, kM);
+  iz = (ix == -1 || iy == -1 || g.depth_log) ? -2 : quant_fast((lz - g.fnear) * rfn, g.nz, kM);
+  if (ix == -2) ix = quant_exact(dadd(0.5, ddiv(dmul(0.5, lx), zh)), g.nx);
+  if (iy == -2) iy = quant_exact(dadd(0.5, ddiv(dmul(0.5, ly), zh)), g.ny);
+  if (iz == -2 && ix >= 0 && iy >= 0)
+    iz = quant_exact(g.depth_log ? ddiv(log(ddiv(lz, g.fnear)), g.flogr)
+                                 : ddiv(dsub(lz, g.fnear), dsub(g.ffar, g.fnear)), g.nz);
+  return ix >= 0 && iy >= 0 && iz >= 0;
+}
+
+// Orthographic passes (froxel.py:351-376): one thread per (pass, scene
+// triangle), flat index f = pass * T + tri, slot 2f (2f + 1 stays empty).
+// Pass 0/1/2 rasterizes axes (1,2)/(2,0)/(0,1) of the world AABB at the
+// sample spacing and interpolates axis 0/1/2; triangles whose AABB misses the
+// frustum's are skipped (froxel.py:363-364).  Block 0 publishes the frame.
+__global__ void __launch_bounds__(kSetupThreads) ortho_setup_kernel(Params p, GtParams g, int supersample,
+                                                                    const double* __restrict__ verts,
+                                                                    long long nverts,
+                                                                    const int64_t* __restrict__ tris, long long T,
+                                                                    Work wk) {
+  double lo[3], hi[3], spacing;
+  int counts[3];
+  ortho_frame(g, supersample, lo, hi, spacing, counts);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    wk.oframe[0] = lo[0];
+    wk.oframe[1] = lo[1];
+    wk.oframe[2] = lo[2];
+    wk.oframe[3] = spacing;
+  }
+  const long long t = (long long)blockIdx.x * kSetupThreads + threadIdx.x;
+  Slot s0, s1;
+  unsigned long long c0 = 0, c1 = 0;
+  if (t < wk.ntris) {
+    const int pass = (int)(t / T);
+    const long long tri = t - (long long)pass * T;
+    const int a0 = pass == 0 ? 1 : pass == 1 ? 2 : 0, a1 = pass == 0 ? 2 : pass == 1 ? 0 : 1;
+    const int ar = 3 - a0 - a1;
+    long long id[3];
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      id[k] = tris[tri * 3 + k];
+      ok &= id[k] >= 0 && id[k] < nverts;
+    }
+    if (ok) {
+      const double* v[3] = {verts + id[0] * 3, verts + id[1] * 3, verts + id[2] * 3};
+      bool live = true;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double mn = fmin(fmin(v[0][k], v[1][k]), v[2][k]), mx = fmax(fmax(v[0][k], v[1][k]), v[2][k]);
+        live &= mx >= lo[k] && mn <= hi[k];
+      }
+      if (live) {
+        double u[3], w[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          u[k] = ddiv(dsub(v[k][a0], lo[a0]), spacing);
+          w[k] = ddiv(dsub(v[k][a1], lo[a1]), spacing);
+        }
+        Slot& sl = s0;
+        sl.v0x = u[0];
+        sl.v0y = w[0];
+        sl.e1x = dsub(u[1], u[0]);
+        sl.e1y = dsub(w[1], w[0]);
+        sl.e2x = dsub(u[2], u[0]);
+        sl.e2y = dsub(w[2], w[0]);
+        sl.den = dsub(dmul(sl.e1x, sl.e2y), dmul(sl.e2x, sl.e1y));
+        sl.iz0 = v[0][ar];  // the interpolated world coordinate
+        sl.iz1 = v[1][ar];
+        sl.iz2 = v[2][ar];
+        sl.wv0 = sl.wv1 = sl.wv2 = 0.0;
+        sl.rden = 1.0 / sl.den;
+        sl.wtol = 0.0;
+        const double W = (double)counts[a0], H = (double)counts[a1];
+        const double minx = fmin(fmin(u[0], u[1]), u[2]), maxx = fmax(fmax(u[0], u[1]), u[2]);
+        const double miny = fmin(fmin(w[0], w[1]), w[2]), maxy = fmax(fmax(w[0], w[1]), w[2]);
+        const int ix0 = (int)fmin(fmax(ceil(dsub(minx, 0.5)), 0.0), W);
+        const int ix1 = (int)fmin(fmax(dadd(floor(dsub(maxx, 0.5)), 1.0), 0.0), W);
+        const int iy0 = (int)fmin(fmax(ceil(dsub(miny, 0.5)), 0.0), H);
+        const int iy1 = (int)fmin(fmax(dadd(floor(dsub(maxy, 0.5)), 1.0), 0.0), H);
+        sl.x0 = ix0;
+        sl.y0 = iy0;
+        sl.w = max(ix1 - ix0, 0);
+        sl.h = max(iy1 - iy0, 0);
+        if (!(fabs(sl.den) > kDegenEps && sl.w > 0 && sl.h > 0)) sl.w = sl.h = 0;
+        sl.wmagic = sl.w > 1 ? (unsigned int)((0x100000000ull + (unsigned long long)sl.w - 1) / (unsigned long long)sl.w)
+                             : 0xffffffffu;
+        c0 = (unsigned long long)sl.w * (unsigned long long)sl.h;
+      }
+    }
+    s0.pad = s1.pad = pass;
+  }
+  finish_setup(p, wk, t, c0, c1, s0, s1);
+}
+
 // Reference depth of one sample (froxel.py:272-279 coverage; oracle.py:127
 // depth = 1 / interp_affine(invz, b1, b2)); < 0 when not covered.
 __device__ __forceinline__ double depth_exact(const Slot& s, double cx, double cy) {
@@ -628,7 +800,13 @@ __global__ void __launch_bounds__(kRasterThreads, 3)
     span_kernel(Params p, GtParams g, const fpvs_frustum* __restrict__ views, const int64_t* __restrict__ prim_ids,
                 Work wk, unsigned long long* __restrict__ zbuf, long long* __restrict__ pidbuf) {
   constexpr int kWarpRows = 32 * kSpanRowsPerThread;
-  constexpr bool kDepth = kKind >= 3;
+  constexpr bool kDepth = kKind == 3 || kKind == 4;
+  __shared__ double s_lo[3], s_spacing;
+  if (kKind == 5) {
+    if (threadIdx.x < 3) s_lo[threadIdx.x] = wk.oframe[threadIdx.x];
+    if (threadIdx.x == 3) s_spacing = wk.oframe[3];
+    __syncthreads();
+  }
   const unsigned long long total = *wk.total;  // rows
   const unsigned int row = (unsigned int)(p.nx >> 3);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -723,7 +901,28 @@ __global__ void __launch_bounds__(kRasterThreads, 3)
           }
           const int px = sxa + (t - sex);
           const double cx = centre(px), cy = centre(spy);
-          if (kDepth) {
+          if (kKind == 5) {
+            // orthographic pass s.pad: axes (a0, a1) on screen, ar interpolated
+            // (froxel.py:366-374)
+            double b1, b2;
+            valid = false;
+            if (bary_filtered(s, cx, cy, b1, b2)) {
+              const int pass = s.pad;
+              const int a0 = pass == 0 ? 1 : pass == 1 ? 2 : 0, a1 = pass == 0 ? 2 : pass == 1 ? 0 : 1;
+              double wv[3];
+              wv[a0] = dadd(s_lo[a0], dmul(cx, s_spacing));
+              wv[a1] = dadd(s_lo[a1], dmul(cy, s_spacing));
+              wv[3 - a0 - a1] = dadd(dadd(s.iz0, dmul(b1, dsub(s.iz1, s.iz0))), dmul(b2, dsub(s.iz2, s.iz0)));
+              int ix, iy, iz;
+              if (project_quantize(g, wv[0], wv[1], wv[2], ix, iy, iz)) {
+                const unsigned long long byte = (unsigned long long)(ix >> 3) +
+                                                (unsigned long long)row * ((unsigned long long)iy + (unsigned long long)p.ny * iz);
+                word = (unsigned int)(byte >> 2);
+                bit = 1u << ((((unsigned int)byte & 3u) << 3) | ((unsigned int)ix & 7u));
+                valid = true;
+              }
+            }
+          } else if (kDepth) {
             const double depth = depth_filtered(s, cx, cy);
             valid = false;
             if (depth >= 0 && depth <= farz) {  // oracle.py:128
@@ -749,7 +948,7 @@ __global__ void __launch_bounds__(kRasterThreads, 3)
             }
           }
         }
-        if (kKind == 0) {
+        if (kKind == 0 || kKind == 5) {
           const unsigned int vm = __ballot_sync(0xffffffffu, valid);
           if (vm) {
             const int leader = __ffs(vm) - 1;
@@ -999,6 +1198,83 @@ extern "C" long long fpvs_froxelize_samples(const void* workspace, void* stream)
     return -1;
   if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
   return (long long)v;
+}
+
+// Orthographic three-view froxelization (froxel.py:351-376, the dataset
+// generator's default mode): one setup over (pass, triangle), the shared
+// scan, then span_kernel<5> rasterizes each pass's triangles on the world
+// AABB's sample lattice, reconstructs the world point of every covered sample
+// and ORs its froxel (project_points + quantize) into the grid.  The 32-byte
+// AABB frame (lo, spacing) lives where the perspective path keeps its
+// pixel->froxel table.
+extern "C" size_t fpvs_froxelize_ortho_workspace_size(long long ntris, int Nx, int Ny, int Nz, int supersample) {
+  if (ntris < 0 || Nx <= 0 || Ny <= 0 || Nz <= 0 || supersample < 1) return 0;
+  return frox::layout(3 * ntris, (long long)Nx * Ny * Nz / 8, 8, 0).bytes;
+}
+
+extern "C" int fpvs_froxelize_ortho(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                                    const fpvs_frustum* fr, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                                    uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace frox;
+  FPVS_CHECK_ARG(out_bits != nullptr && fr != nullptr, "froxelize_ortho: null output or frustum");
+  FPVS_CHECK_ARG(Nx > 0 && Ny > 0 && Nz > 0 && Nx % 8 == 0, "N_x must be divisible by 8, got %d", Nx);
+  FPVS_CHECK_ARG(supersample >= 1, "supersample factor must be >= 1");
+  FPVS_CHECK_ARG(depth_mode == FPVS_DEPTH_LINEAR || depth_mode == FPVS_DEPTH_LOG, "bad depth mode %d", depth_mode);
+  FPVS_CHECK_ARG(ntris >= 0 && nverts >= 0 && (ntris == 0 || (verts && tris)), "froxelize_ortho: bad scene arrays");
+  FPVS_CHECK_ARG(fr->near_z > 0 && fr->near_z < fr->far_z && fr->half_extent > 0, "need 0 < near < far");
+  const long long dmax = Nx > Ny ? (Nx > Nz ? Nx : Nz) : (Ny > Nz ? Ny : Nz);
+  FPVS_CHECK_ARG((long long)supersample * dmax < (1LL << 20), "froxelize_ortho: sample lattice too large");
+  cudaStream_t s = as_stream(stream);
+  const long long grid_bytes = (long long)Nx * Ny * Nz / 8;
+  const Layout L = layout(3 * ntris, grid_bytes, 8, 0);
+  FPVS_CHECK_ARG(workspace != nullptr && workspace_bytes >= L.bytes, "froxelize_ortho: workspace too small (%zu < %zu)",
+                 workspace_bytes, L.bytes);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const bool direct = ((uintptr_t)out_bits & 3) == 0 && grid_bytes % 4 == 0;
+  unsigned int* words = direct ? reinterpret_cast<unsigned int*>(out_bits) : reinterpret_cast<unsigned int*>(ws + L.words);
+  if (cudaMemsetAsync(words, 0, (size_t)((grid_bytes + 3) & ~3LL), s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  if (cudaMemsetAsync(ws + L.total, 0, 16, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  if (ntris > 0) {
+    Work wk = {};
+    wk.slots = reinterpret_cast<Slot*>(ws + L.slots);
+    wk.lp = reinterpret_cast<unsigned long long*>(ws + L.lp);
+    wk.bsum = reinterpret_cast<unsigned long long*>(ws + L.bsum);
+    wk.bpre = reinterpret_cast<unsigned long long*>(ws + L.bpre);
+    wk.total = reinterpret_cast<unsigned long long*>(ws + L.total);
+    wk.nsamples = wk.total + 1;
+    wk.oframe = reinterpret_cast<double*>(ws + L.tabx);
+    wk.out_words = words;
+    wk.ntris = 3 * ntris;
+    wk.nb = (int)((2 * wk.ntris + kSlotsPerBlock - 1) / kSlotsPerBlock);
+    Params p = {};
+    p.nx = Nx;
+    p.ny = Ny;
+    p.nz = Nz;
+    p.depth_log = depth_mode == FPVS_DEPTH_LOG;
+    p.rows_mode = 1;
+    p.seg = env_int("FPVS_FROX_SEG", 16);
+    GtParams g = {};
+    for (int i = 0; i < 3; ++i) g.fo[i] = fr->origin[i];
+    for (int i = 0; i < 9; ++i) g.fb[i] = fr->basis[i];
+    g.fh = fr->half_extent;
+    g.fnear = fr->near_z;
+    g.ffar = fr->far_z;
+    g.flogr = log(fr->far_z / fr->near_z);
+    g.nx = Nx;
+    g.ny = Ny;
+    g.nz = Nz;
+    g.depth_log = p.depth_log;
+    ortho_setup_kernel<<<wk.nb, kSetupThreads, 0, s>>>(p, g, supersample, verts, nverts, tris, ntris, wk);
+    FPVS_CHECK_LAUNCH("froxelize_ortho setup");
+    scan_kernel<<<1, 1024, 0, s>>>(p, wk);
+    FPVS_CHECK_LAUNCH("froxelize_ortho scan");
+    static const int grid = occupancy_grid(span_kernel<true, 5>);
+    span_kernel<true, 5><<<grid, kRasterThreads, 0, s>>>(p, g, nullptr, nullptr, wk, nullptr, nullptr);
+    FPVS_CHECK_LAUNCH("froxelize_ortho raster");
+  }
+  if (!direct && cudaMemcpyAsync(out_bits, words, (size_t)grid_bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    FPVS_CHECK_LAUNCH("froxelize_ortho copy");
+  return FPVS_OK;
 }
 
 // ===========================================================================

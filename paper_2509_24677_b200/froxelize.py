@@ -1,10 +1,11 @@
 """Device froxelization: triangle scene -> packed geometry grid.
 
 Drop-in for ``froxelpvs.froxel.froxelize`` (pkg/src/froxelpvs/froxel.py:387-394)
-in ``mode="perspective"``: same arguments (a scene with ``vertices`` /
+in both modes (``"perspective"``, froxel.py:328-348, and the three-view
+``"ortho"``, froxel.py:351-376, via ``fpvs_froxelize_ortho``): same arguments (a scene with ``vertices`` /
 ``triangles``, a frustum with ``_o`` / ``_basis`` / ``half_extent`` / ``near`` /
 ``far``, dims, a ``FroxelizeConfig``), same ``FroxelGrid`` result, bit-for-bit
-in linear depth mode.  The work runs in ``fpvs_froxelize`` (csrc/froxelize.cu);
+in both depth modes.  The work runs in ``fpvs_froxelize`` (csrc/froxelize.cu);
 there is no CPU path — without the CUDA library the call raises.
 
 ``Froxelizer`` keeps the scene and workspace resident on the device for
@@ -127,10 +128,11 @@ class Froxelizer:
     def ntris(self) -> int:
         return int(self.tris.shape[0])
 
-    def workspace(self, dims, supersample: int):
+    def workspace(self, dims, supersample: int, mode: str = "perspective"):
         torch = _torch()
         nx, ny, nz = dims
-        need = _lib.size("fpvs_froxelize_workspace_size", self.ntris, nx, ny, nz, int(supersample))
+        fn = "fpvs_froxelize_ortho_workspace_size" if mode == "ortho" else "fpvs_froxelize_workspace_size"
+        need = _lib.size(fn, self.ntris, nx, ny, nz, int(supersample))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         return self._ws
@@ -139,8 +141,6 @@ class Froxelizer:
         """Packed grid (uint8 CUDA tensor, Nx*Ny*Nz/8) of this scene in ``frustum``."""
         torch = _torch()
         cfg = cfg or FroxelizeConfig()
-        if cfg.mode != "perspective":
-            raise NotImplementedError("the device froxelizer implements mode='perspective' only")
         nx, ny, nz = _check_dims(dims)
         fr = Frustum.of(frustum)
         nbytes = nx * ny * nz // 8
@@ -148,10 +148,10 @@ class Froxelizer:
             out = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         elif out.numel() != nbytes or out.dtype != torch.uint8:
             raise ValueError("output buffer does not match dims")
-        ws = self.workspace((nx, ny, nz), cfg.supersample)
+        ws = self.workspace((nx, ny, nz), cfg.supersample, cfg.mode)
         c = fr.c_struct()
         import ctypes
-        _lib.call("fpvs_froxelize", _lib.ptr(self.verts), self.verts.shape[0], _lib.ptr(self.tris), self.ntris,
+        _lib.call("fpvs_froxelize_ortho" if cfg.mode == "ortho" else "fpvs_froxelize", _lib.ptr(self.verts), self.verts.shape[0], _lib.ptr(self.tris), self.ntris,
                   ctypes.byref(c), nx, ny, nz, int(cfg.supersample), 0 if cfg.depth_mode == "linear" else 1,
                   _lib.ptr(out), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
         return out

@@ -46,15 +46,15 @@ def cases(m):
     Vec3, Frustum, TriScene = core.Vec3, core.Frustum, core.TriScene
     out = []
 
-    def add(name, scene, frustum, dims, ss=4, depth="linear"):
-        cfg = froxel.FroxelizeConfig(supersample=ss, mode="perspective", depth_mode=depth)
+    def add(name, scene, frustum, dims, ss=4, depth="linear", mode="perspective"):
+        cfg = froxel.FroxelizeConfig(supersample=ss, mode=mode, depth_mode=depth)
         grid = froxel.froxelize(scene, frustum, dims, cfg)
         out.append(dict(name=name, verts=scene.vertices.copy(), tris=scene.triangles.astype(np.int64),
                         origin=frustum._o.copy(), basis=frustum._basis.copy(),
                         lens=np.array([frustum.half_extent, frustum.near, frustum.far]),
                         dims=np.array(dims), ss=np.array(ss), depth=np.array(0 if depth == "linear" else 1),
-                        bits=grid.bits.copy()))
-        print(f"{name:28s} dims={dims} s={ss} {depth:6s} tris={len(scene.triangles):6d} "
+                        mode=np.array(0 if mode == "perspective" else 1), bits=grid.bits.copy()))
+        print(f"{name:28s} {mode:11s} dims={dims} s={ss} {depth:6s} tris={len(scene.triangles):6d} "
               f"occupied={grid.occupied_count()}")
 
     # reference scene generator, viewcell frusta (SURVEY §8(f) #1 input)
@@ -102,6 +102,17 @@ def cases(m):
 
     # empty scene
     add("empty", TriScene(np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64)), fr, (16, 16, 16))
+
+    # orthographic three-view mode (froxel.py:351-376), the dataset generator's default
+    for seed, dims, ss, depth in [(0, (16, 16, 16), 4, "linear"), (1, (64, 64, 64), 2, "linear"),
+                                  (2, (32, 16, 24), 3, "linear"), (3, (32, 32, 32), 1, "log")]:
+        scene, cell = sg.generate_scene(sg.SceneGenConfig(seed=seed))
+        add(f"ortho_scene{seed}", scene, core.build_viewcell_frustum(cell), dims, ss, depth, mode="ortho")
+    v, t = _quad(z, 1.2 * z * fr.half_extent, 1.2 * z * fr.half_extent)
+    add("ortho_full_span_quad", TriScene(fr._o + v @ fr._basis, t), fr, (16, 16, 16), mode="ortho")
+    add("ortho_soup", TriScene(soup.reshape(-1, 3), np.arange(1200).reshape(-1, 3)), fr2, (64, 48, 40), 2,
+        mode="ortho")
+    add("ortho_empty", TriScene(np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64)), fr, (16, 16, 16), mode="ortho")
     return out
 
 

@@ -43,11 +43,16 @@ def _frustum(c):
     return Frustum(c["origin"], c["basis"], h, n, f)
 
 
+def _mode(c):
+    return "ortho" if int(c.get("mode", 0)) == 1 else "perspective"
+
+
 @pytest.mark.parametrize("idx", range(len(CASES)), ids=[str(c["name"]) for c in CASES])
 def test_golden(idx):
     from paper_2509_24677_b200.froxelize import FroxelizeConfig, Froxelizer
     c = CASES[idx]
-    cfg = FroxelizeConfig(supersample=int(c["ss"]), depth_mode="linear" if int(c["depth"]) == 0 else "log")
+    cfg = FroxelizeConfig(supersample=int(c["ss"]), depth_mode="linear" if int(c["depth"]) == 0 else "log",
+                          mode=_mode(c))
     fz = Froxelizer(c["verts"], c["tris"])
     got = fz.run(_frustum(c), tuple(int(v) for v in c["dims"]), cfg).cpu().numpy()
     ref = c["bits"]
@@ -179,6 +184,51 @@ def test_feeds_the_pvs_pipeline():
     assert out.numel() == ref.size
 
 
+@pytest.mark.parametrize("seed,dims,ss,depth", [(0, (32, 32, 32), 2, "linear"), (1, (24, 40, 16), 3, "linear"),
+                                                (2, (64, 32, 48), 1, "linear"), (3, (16, 16, 16), 4, "log")])
+def test_ortho_random_scenes_vs_oracle(seed, dims, ss, depth):
+    """mode="ortho" (froxel.py:351-376) on random soups and frusta vs the oracle."""
+    from paper_2509_24677_b200.froxelize import FroxelizeConfig, Froxelizer
+    fr = _random_frustum(100 + seed)
+    v, t = _soup(seed, 300, fr)
+    got = Froxelizer(v, t).run(fr, dims, FroxelizeConfig(supersample=ss, mode="ortho", depth_mode=depth)).cpu().numpy()
+    ref = ofz.froxelize_ortho(v, t, fr._o, fr._basis, fr.half_extent, fr.near, fr.far, dims, ss, depth)
+    diff = int(np.unpackbits(got ^ ref).sum())
+    assert np.unpackbits(ref).sum() > 0
+    if depth == "linear":
+        assert diff == 0, diff
+    else:
+        assert diff <= 4, diff
+
+
+def test_ortho_drop_in_and_graph_replay():
+    """froxelize(..., FroxelizeConfig(mode="ortho")) and a captured replay give the golden grid."""
+    import torch
+    from types import SimpleNamespace
+    from paper_2509_24677_b200.froxelize import FroxelizeConfig, Froxelizer, froxelize
+    c = next(c for c in CASES if str(c["name"]) == "ortho_scene1")
+    scene = SimpleNamespace(vertices=c["verts"], triangles=c["tris"])
+    ref_frustum = SimpleNamespace(_o=c["origin"], _basis=c["basis"], half_extent=float(c["lens"][0]),
+                                  near=float(c["lens"][1]), far=float(c["lens"][2]))
+    dims = tuple(int(v) for v in c["dims"])
+    cfg = FroxelizeConfig(supersample=int(c["ss"]), mode="ortho")
+    grid = froxelize(scene, ref_frustum, dims, cfg)
+    assert np.array_equal(grid.bits, c["bits"])
+    fz = Froxelizer(c["verts"], c["tris"])
+    out = torch.zeros(int(np.prod(dims)) // 8, dtype=torch.uint8, device="cuda")
+    fz.run(_frustum(c), dims, cfg, out=out)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            fz.run(_frustum(c), dims, cfg, out=out)
+    out.fill_(0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), c["bits"])
+
+
 _ALT_CHECK = r"""
 import os, sys, numpy as np
 sys.path.insert(0, os.getcwd())
@@ -191,7 +241,8 @@ for i in range(int(g["ncases"])):
         continue
     h, n, f = (float(v) for v in c["lens"])
     got = Froxelizer(c["verts"], c["tris"]).run(Frustum(c["origin"], c["basis"], h, n, f),
-        tuple(int(v) for v in c["dims"]), FroxelizeConfig(supersample=int(c["ss"]))).cpu().numpy()
+        tuple(int(v) for v in c["dims"]), FroxelizeConfig(supersample=int(c["ss"]),
+        mode="ortho" if int(c.get("mode", 0)) == 1 else "perspective")).cpu().numpy()
     bad += int(np.unpackbits(got ^ c["bits"]).sum())
 print("BAD", bad)
 """

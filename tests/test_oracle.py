@@ -268,20 +268,21 @@ def test_froxelize_oracle_matches_reference_golden(golden):
     g = golden("froxelize.npz")
     for i in range(int(g["ncases"])):
         h, n, f = g[f"c{i}_lens"]
-        bits = ofz.froxelize(g[f"c{i}_verts"], g[f"c{i}_tris"], g[f"c{i}_origin"], g[f"c{i}_basis"], h, n, f,
-                             g[f"c{i}_dims"], int(g[f"c{i}_ss"]),
-                             "linear" if int(g[f"c{i}_depth"]) == 0 else "log")
+        fn = ofz.froxelize_ortho if int(g[f"c{i}_mode"]) == 1 else ofz.froxelize
+        bits = fn(g[f"c{i}_verts"], g[f"c{i}_tris"], g[f"c{i}_origin"], g[f"c{i}_basis"], h, n, f,
+                  g[f"c{i}_dims"], int(g[f"c{i}_ss"]), "linear" if int(g[f"c{i}_depth"]) == 0 else "log")
         assert np.array_equal(bits, g[f"c{i}_bits"]), str(g[f"c{i}_name"])
 
 
 def test_froxelize_full_span_quad_is_one_layer(golden):
-    """test_froxel.py:148-159: a full-cross-section quad at w = 0.5 fills layer 8 of 16 only."""
+    """test_froxel.py:148-159: a full-cross-section quad at w = 0.5 fills layer 8 of 16 only (both modes)."""
     g = golden("froxelize.npz")
-    i = next(i for i in range(int(g["ncases"])) if str(g[f"c{i}_name"]) == "full_span_quad")
-    dense = FroxelGrid((16, 16, 16), bits=g[f"c{i}_bits"]).to_dense()
-    assert dense[:, :, 8].all()
-    dense[:, :, 8] = False
-    assert not dense.any()
+    for name in ("full_span_quad", "ortho_full_span_quad"):
+        i = next(i for i in range(int(g["ncases"])) if str(g[f"c{i}_name"]) == name)
+        dense = FroxelGrid((16, 16, 16), bits=g[f"c{i}_bits"]).to_dense()
+        assert dense[:, :, 8].all()
+        dense[:, :, 8] = False
+        assert not dense.any()
 
 
 @pytest.mark.skipif(ref is None, reason="reference not mounted (GPU box)")
