@@ -1,6 +1,6 @@
 """Time fpvs_froxelize on synthetic scenes (device time, CUDA graph of R calls).
 
-    python tools/froxelize_bench.py [--dims 256] [--ss 4]
+    python tools/froxelize_bench.py [--dims 256] [--ss 4] [--mode ortho]
 """
 
 from __future__ import annotations
@@ -22,13 +22,14 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--cpu", action="store_true", help="also time the oracle port")
     ap.add_argument("--scenes", default="0,1,2,3")
+    ap.add_argument("--mode", default="perspective", choices=["perspective", "ortho"])
     a = ap.parse_args()
     import torch
     from paper_2509_24677_b200 import synth
     from paper_2509_24677_b200.froxelize import FroxelizeConfig, Froxelizer, Frustum
     from oracle import froxelize as ofz
     dims = (a.dims,) * 3
-    cfg = FroxelizeConfig(supersample=a.ss)
+    cfg = FroxelizeConfig(supersample=a.ss, mode=a.mode)
     scenes = [(0, 12, 12), (1, 40, 24), (2, 200, 48), (3, 2000, 24)]
     for seed, nobj, detail in [scenes[int(i)] for i in a.scenes.split(",")]:
         v, t, fa = synth.froxel_scene(seed, nobj, detail)
@@ -59,7 +60,8 @@ def main():
                 f"device {best * 1e3:8.1f} us  {ns / best / 1e6:7.2f} Gsample/s")
         if a.cpu and len(t) < 50000:
             t0 = time.perf_counter()
-            ref = ofz.froxelize(v, t, fr._o, fr._basis, fr.half_extent, fr.near, fr.far, dims, a.ss)
+            fn = ofz.froxelize_ortho if a.mode == "ortho" else ofz.froxelize
+            ref = fn(v, t, fr._o, fr._basis, fr.half_extent, fr.near, fr.far, dims, a.ss)
             line += f"  oracle {time.perf_counter() - t0:6.2f} s  match {np.array_equal(ref, got)}"
         print(line, flush=True)
 
