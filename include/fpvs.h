@@ -456,6 +456,20 @@ int fpvs_froxel_pairs(const double* verts, long long nverts, const int64_t* tris
                       long long* pairs, long long cap, unsigned long long* npairs_dev, void* workspace,
                       size_t workspace_bytes, void* stream);
 
+/* The same two consumers over the orthographic fragment stream
+ * (froxel.py:351-376, 397-417 with FroxelizeConfig(mode="ortho"), as the
+ * reference's CLI infer/metrics path uses it, cli.py:297-300).  Arguments as
+ * above; workspace: fpvs_froxelize_ortho_workspace_size; cap = the candidate
+ * sample count from fpvs_froxelize_samples after fpvs_froxelize_ortho. */
+int fpvs_froxel_cull_ortho(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                           const fpvs_frustum* frustum, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                           const uint8_t* pvs_bits, uint8_t* kept, void* workspace, size_t workspace_bytes,
+                           void* stream);
+int fpvs_froxel_pairs_ortho(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                            const fpvs_frustum* frustum, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                            long long* pairs, long long cap, unsigned long long* npairs_dev, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
 /* Depth + primitive-id buffers of oracle.py:107-138 render_depth() for
  * ncams cameras (DEVICE array, fpvs_frustum form) at res_w x res_h:
  * depth_out float64 [ncams][res_h][res_w] (+inf where empty, nullable),

@@ -87,6 +87,9 @@ SIGNATURES = {
     "fpvs_froxel_cull": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _i, _i, _i, _i, _i, _p, _p, _p, _z, _p]),
     "fpvs_froxel_pairs": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _i, _i, _i, _i, _i, _p, C.c_longlong, _p, _p,
                                _z, _p]),
+    "fpvs_froxel_cull_ortho": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _i, _i, _i, _i, _i, _p, _p, _p, _z, _p]),
+    "fpvs_froxel_pairs_ortho": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _i, _i, _i, _i, _i, _p, C.c_longlong, _p,
+                                     _p, _z, _p]),
     "fpvs_render_depth": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _p, _i, _i, _i, _p, _p, _p, _z, _p]),
     "fpvs_gt_pvs": (_i, [_p, C.c_longlong, _p, C.c_longlong, _p, _p, _i, _i, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p,
                          _z, _p]),

@@ -801,8 +801,10 @@ __global__ void __launch_bounds__(kRasterThreads, 3)
                 Work wk, unsigned long long* __restrict__ zbuf, long long* __restrict__ pidbuf) {
   constexpr int kWarpRows = 32 * kSpanRowsPerThread;
   constexpr bool kDepth = kKind == 3 || kKind == 4;
+  constexpr bool kOrtho = kKind >= 5;                // kinds 5/6/7: orthographic bits / cull / pairs
+  constexpr int kAct = kOrtho ? kKind - 5 : kKind;  // 0 bits, 1 cull, 2 pairs, 3/4 depth
   __shared__ double s_lo[3], s_spacing;
-  if (kKind == 5) {
+  if (kOrtho) {
     if (threadIdx.x < 3) s_lo[threadIdx.x] = wk.oframe[threadIdx.x];
     if (threadIdx.x == 3) s_spacing = wk.oframe[3];
     __syncthreads();
@@ -901,7 +903,7 @@ __global__ void __launch_bounds__(kRasterThreads, 3)
           }
           const int px = sxa + (t - sex);
           const double cx = centre(px), cy = centre(spy);
-          if (kKind == 5) {
+          if (kOrtho) {
             // orthographic pass s.pad: axes (a0, a1) on screen, ar interpolated
             // (froxel.py:366-374)
             double b1, b2;
@@ -919,6 +921,7 @@ __global__ void __launch_bounds__(kRasterThreads, 3)
                                                 (unsigned long long)row * ((unsigned long long)iy + (unsigned long long)p.ny * iz);
                 word = (unsigned int)(byte >> 2);
                 bit = 1u << ((((unsigned int)byte & 3u) << 3) | ((unsigned int)ix & 7u));
+                if (kAct == 2) flat = ix + (long long)p.nx * (iy + (long long)p.ny * iz);
                 valid = true;
               }
             }
@@ -948,7 +951,9 @@ __global__ void __launch_bounds__(kRasterThreads, 3)
             }
           }
         }
-        if (kKind == 0 || kKind == 5) {
+        // scene triangle of the sample (ortho slots are numbered pass * T + tri)
+        const long long tri = kOrtho ? (sl >> 1) - (long long)s.pad * g.T : (sl >> 1);
+        if (kAct == 0) {
           const unsigned int vm = __ballot_sync(0xffffffffu, valid);
           if (vm) {
             const int leader = __ffs(vm) - 1;
@@ -960,10 +965,10 @@ __global__ void __launch_bounds__(kRasterThreads, 3)
               atomicOr(wk.out_words + word, bit);
             }
           }
-        } else if (kKind == 1) {
-          if (valid && (__ldg(wk.pvs_words + word) & bit)) wk.kept[sl >> 1] = 1;
-        } else if (kKind == 2) {
-          const long long key = valid ? flat * wk.ntris + (sl >> 1) : -1 - lane;
+        } else if (kAct == 1) {
+          if (valid && (__ldg(wk.pvs_words + word) & bit)) wk.kept[tri] = 1;
+        } else if (kAct == 2) {
+          const long long key = valid ? flat * (kOrtho ? g.T : wk.ntris) + tri : -1 - lane;
           const unsigned int peers = __match_any_sync(0xffffffffu, key);
           if (valid && (__ffs(peers) - 1) == lane) {
             const unsigned long long slot = atomicAdd(wk.npairs, 1ull);
@@ -1212,11 +1217,16 @@ extern "C" size_t fpvs_froxelize_ortho_workspace_size(long long ntris, int Nx, i
   return frox::layout(3 * ntris, (long long)Nx * Ny * Nz / 8, 8, 0).bytes;
 }
 
-extern "C" int fpvs_froxelize_ortho(const double* verts, long long nverts, const int64_t* tris, long long ntris,
-                                    const fpvs_frustum* fr, int Nx, int Ny, int Nz, int supersample, int depth_mode,
-                                    uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream) {
-  using namespace frox;
-  FPVS_CHECK_ARG(out_bits != nullptr && fr != nullptr, "froxelize_ortho: null output or frustum");
+namespace fpvs {
+namespace frox {
+
+// kKind 5: grid bits into out_bits; 6: cull flags (wk.pvs_words / wk.kept);
+// 7: fragment pairs (wk.pairs / npairs / pair_cap).  out_bits only for 5.
+template <int kKind>
+int ortho_pass(const double* verts, long long nverts, const int64_t* tris, long long ntris, const fpvs_frustum* fr,
+               int Nx, int Ny, int Nz, int supersample, int depth_mode, uint8_t* out_bits, void* workspace,
+               size_t workspace_bytes, cudaStream_t s, Work wk) {
+  FPVS_CHECK_ARG(fr != nullptr && (kKind != 5 || out_bits != nullptr), "froxelize_ortho: null output or frustum");
   FPVS_CHECK_ARG(Nx > 0 && Ny > 0 && Nz > 0 && Nx % 8 == 0, "N_x must be divisible by 8, got %d", Nx);
   FPVS_CHECK_ARG(supersample >= 1, "supersample factor must be >= 1");
   FPVS_CHECK_ARG(depth_mode == FPVS_DEPTH_LINEAR || depth_mode == FPVS_DEPTH_LOG, "bad depth mode %d", depth_mode);
@@ -1224,18 +1234,19 @@ extern "C" int fpvs_froxelize_ortho(const double* verts, long long nverts, const
   FPVS_CHECK_ARG(fr->near_z > 0 && fr->near_z < fr->far_z && fr->half_extent > 0, "need 0 < near < far");
   const long long dmax = Nx > Ny ? (Nx > Nz ? Nx : Nz) : (Ny > Nz ? Ny : Nz);
   FPVS_CHECK_ARG((long long)supersample * dmax < (1LL << 20), "froxelize_ortho: sample lattice too large");
-  cudaStream_t s = as_stream(stream);
   const long long grid_bytes = (long long)Nx * Ny * Nz / 8;
   const Layout L = layout(3 * ntris, grid_bytes, 8, 0);
   FPVS_CHECK_ARG(workspace != nullptr && workspace_bytes >= L.bytes, "froxelize_ortho: workspace too small (%zu < %zu)",
                  workspace_bytes, L.bytes);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  const bool direct = ((uintptr_t)out_bits & 3) == 0 && grid_bytes % 4 == 0;
-  unsigned int* words = direct ? reinterpret_cast<unsigned int*>(out_bits) : reinterpret_cast<unsigned int*>(ws + L.words);
-  if (cudaMemsetAsync(words, 0, (size_t)((grid_bytes + 3) & ~3LL), s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  const bool direct = kKind != 5 || (((uintptr_t)out_bits & 3) == 0 && grid_bytes % 4 == 0);
+  unsigned int* words = kKind != 5 ? nullptr
+                        : direct   ? reinterpret_cast<unsigned int*>(out_bits)
+                                   : reinterpret_cast<unsigned int*>(ws + L.words);
+  if (kKind == 5 && cudaMemsetAsync(words, 0, (size_t)((grid_bytes + 3) & ~3LL), s) != cudaSuccess)
+    FPVS_CHECK_LAUNCH("memset");
   if (cudaMemsetAsync(ws + L.total, 0, 16, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
   if (ntris > 0) {
-    Work wk = {};
     wk.slots = reinterpret_cast<Slot*>(ws + L.slots);
     wk.lp = reinterpret_cast<unsigned long long*>(ws + L.lp);
     wk.bsum = reinterpret_cast<unsigned long long*>(ws + L.bsum);
@@ -1264,17 +1275,60 @@ extern "C" int fpvs_froxelize_ortho(const double* verts, long long nverts, const
     g.ny = Ny;
     g.nz = Nz;
     g.depth_log = p.depth_log;
+    g.T = ntris;
     ortho_setup_kernel<<<wk.nb, kSetupThreads, 0, s>>>(p, g, supersample, verts, nverts, tris, ntris, wk);
     FPVS_CHECK_LAUNCH("froxelize_ortho setup");
     scan_kernel<<<1, 1024, 0, s>>>(p, wk);
     FPVS_CHECK_LAUNCH("froxelize_ortho scan");
-    static const int grid = occupancy_grid(span_kernel<true, 5>);
-    span_kernel<true, 5><<<grid, kRasterThreads, 0, s>>>(p, g, nullptr, nullptr, wk, nullptr, nullptr);
+    static const int grid = occupancy_grid(span_kernel<true, kKind>);
+    span_kernel<true, kKind><<<grid, kRasterThreads, 0, s>>>(p, g, nullptr, nullptr, wk, nullptr, nullptr);
     FPVS_CHECK_LAUNCH("froxelize_ortho raster");
   }
   if (!direct && cudaMemcpyAsync(out_bits, words, (size_t)grid_bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
     FPVS_CHECK_LAUNCH("froxelize_ortho copy");
   return FPVS_OK;
+}
+
+}  // namespace frox
+}  // namespace fpvs
+
+extern "C" int fpvs_froxelize_ortho(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                                    const fpvs_frustum* fr, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                                    uint8_t* out_bits, void* workspace, size_t workspace_bytes, void* stream) {
+  return frox::ortho_pass<5>(verts, nverts, tris, ntris, fr, Nx, Ny, Nz, supersample, depth_mode, out_bits, workspace,
+                             workspace_bytes, as_stream(stream), frox::Work{});
+}
+
+extern "C" int fpvs_froxel_cull_ortho(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                                      const fpvs_frustum* fr, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                                      const uint8_t* pvs_bits, uint8_t* kept, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  const long long grid_bytes = (long long)Nx * Ny * Nz / 8;
+  FPVS_CHECK_ARG(pvs_bits != nullptr && (ntris == 0 || kept != nullptr), "froxel_cull_ortho: null pvs or output");
+  FPVS_CHECK_ARG(((uintptr_t)pvs_bits & 3) == 0 && grid_bytes % 4 == 0,
+                 "froxel_cull_ortho: pvs grid must be 4-byte aligned with Nx*Ny*Nz/8 a multiple of 4");
+  cudaStream_t s = as_stream(stream);
+  if (ntris > 0 && cudaMemsetAsync(kept, 0, (size_t)ntris, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  frox::Work wk = {};
+  wk.pvs_words = reinterpret_cast<const unsigned int*>(pvs_bits);
+  wk.kept = kept;
+  return frox::ortho_pass<6>(verts, nverts, tris, ntris, fr, Nx, Ny, Nz, supersample, depth_mode, nullptr, workspace,
+                             workspace_bytes, s, wk);
+}
+
+extern "C" int fpvs_froxel_pairs_ortho(const double* verts, long long nverts, const int64_t* tris, long long ntris,
+                                       const fpvs_frustum* fr, int Nx, int Ny, int Nz, int supersample, int depth_mode,
+                                       long long* pairs, long long cap, unsigned long long* npairs_dev, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
+  FPVS_CHECK_ARG(npairs_dev != nullptr && cap >= 0 && (cap == 0 || pairs != nullptr), "froxel_pairs_ortho: bad output");
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(npairs_dev, 0, 8, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");
+  frox::Work wk = {};
+  wk.pairs = pairs;
+  wk.npairs = npairs_dev;
+  wk.pair_cap = cap;
+  return frox::ortho_pass<7>(verts, nverts, tris, ntris, fr, Nx, Ny, Nz, supersample, depth_mode, nullptr, workspace,
+                             workspace_bytes, s, wk);
 }
 
 // ===========================================================================

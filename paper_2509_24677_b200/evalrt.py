@@ -7,7 +7,7 @@ Drop-ins for pkg/src/froxelpvs/evalrt.py and froxel.py:397-417:
 * ``froxel_id_map(scene, frustum, dims, cfg)`` — returns an ``IdMap``: the
   froxel -> primitive-id map of froxel.py:397-417 held as its scene +
   frustum on the device.  ``cull`` consumes it with ONE fused raster pass
-  (``fpvs_froxel_cull``: every perspective fragment reads the PVS bit of its
+  (``fpvs_froxel_cull``: every fragment reads the PVS bit of its
   froxel and marks its triangle) instead of iterating a dict; reading it as
   a mapping materialises the reference's dict from ``fpvs_froxel_pairs``;
 * ``cull(scene, pvs, id_map)`` (evalrt.py:62-68);
@@ -93,8 +93,6 @@ class IdMap(Mapping):
 
     def __init__(self, scene, frustum, dims, cfg: FroxelizeConfig | None = None):
         self.cfg = cfg or FroxelizeConfig()
-        if self.cfg.mode != "perspective":
-            raise NotImplementedError("the device id map implements mode='perspective' only")
         nx, ny, nz = (int(d) for d in dims)
         if nx % 8 != 0:
             raise ValueError(f"N_x must be divisible by 8, got {nx}")
@@ -106,8 +104,10 @@ class IdMap(Mapping):
 
     def _call(self, name, *args):
         nx, ny, nz = self.dims
-        ws = self.fz.workspace(self.dims, self.cfg.supersample)
+        ws = self.fz.workspace(self.dims, self.cfg.supersample, self.cfg.mode)
         c = self.frustum.c_struct()
+        if self.cfg.mode == "ortho":
+            name += "_ortho"
         _lib.call(name, _lib.ptr(self.fz.verts), self.fz.verts.shape[0], _lib.ptr(self.fz.tris), self.fz.ntris,
                   ctypes.byref(c), nx, ny, nz, int(self.cfg.supersample),
                   0 if self.cfg.depth_mode == "linear" else 1, *args, _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
@@ -151,7 +151,7 @@ class IdMap(Mapping):
 
 
 def froxel_id_map(scene, frustum, dims, cfg: FroxelizeConfig | None = None) -> IdMap:
-    """froxel.py:397-417 (perspective mode) -> device-backed ``IdMap``."""
+    """froxel.py:397-417 (perspective or ortho fragment stream) -> device-backed ``IdMap``."""
     return IdMap(scene, frustum, dims, cfg)
 
 

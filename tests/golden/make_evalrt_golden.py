@@ -45,11 +45,16 @@ def cases(m):
     core, froxel, oracle, sg, ev = m["core"], m["froxel"], m["oracle"], m["scenegen"], m["evalrt"]
     rng = np.random.default_rng(31)
     out = []
-    for seed, dims, ss, count in [(0, (16, 16, 16), 4, (6, 14)), (1, (32, 16, 24), 2, (3, 6)),
-                                  (2, (32, 32, 32), 4, (6, 14))]:
+    # the last two use the orthographic fragment stream, as the reference's
+    # CLI infer / metrics path does (cli.py:297-300)
+    for seed, dims, ss, count, mode in [(0, (16, 16, 16), 4, (6, 14), "perspective"),
+                                        (1, (32, 16, 24), 2, (3, 6), "perspective"),
+                                        (2, (32, 32, 32), 4, (6, 14), "perspective"),
+                                        (3, (16, 16, 16), 4, (6, 14), "ortho"),
+                                        (4, (32, 24, 16), 2, (3, 6), "ortho")]:
         scene, cell = sg.generate_scene(sg.SceneGenConfig(seed=seed, count_range=count))
         fr = core.build_viewcell_frustum(cell)
-        cfg = froxel.FroxelizeConfig(supersample=ss)
+        cfg = froxel.FroxelizeConfig(supersample=ss, mode=mode)
         idm = froxel.froxel_id_map(scene, fr, dims, cfg)
         rows = np.array(sorted((x, y, z, p) for (x, y, z), ids in idm.items() for p in ids), dtype=np.int64)
         geo = froxel.froxelize(scene, fr, dims, cfg)
@@ -67,7 +72,8 @@ def cases(m):
         thr = 0.5 * (cell.near + cell.far)
         ff = np.array(sorted(ev.far_field_merge(scene, cell, gt, idm, thr, resolution=res)), dtype=np.int64)
         met = ev.froxel_metrics(froxel.FroxelGrid(dims, bits=pvs_list[1]), gt)
-        c = dict(name=np.array(f"scene{seed}"), verts=scene.vertices.copy(), tris=scene.triangles.astype(np.int64),
+        c = dict(name=np.array(f"scene{seed}" + ("_ortho" if mode == "ortho" else "")),
+                 mode=np.array(0 if mode == "perspective" else 1), verts=scene.vertices.copy(), tris=scene.triangles.astype(np.int64),
                  prim_ids=scene.primitive_ids.astype(np.int64), cell=_cell_row(cell),
                  frustum=np.concatenate([fr._o, fr._basis.reshape(-1), [fr.half_extent, fr.near, fr.far]]),
                  dims=np.array(dims), ss=np.array(ss), idmap=rows, geo=geo.bits.copy(), gt=gt.bits.copy(),

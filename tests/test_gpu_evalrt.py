@@ -4,7 +4,8 @@ Pinned on tests/golden/evalrt.npz (tests/golden/make_evalrt_golden.py): the
 reference's own froxel_id_map (froxel.py:397-417), cull (evalrt.py:62-68),
 render_depth (oracle.py:107-138), pixel_error_rate (evalrt.py:71-84),
 far_field_merge (evalrt.py:87-106) and froxel_metrics (evalrt.py:38-59)
-outputs.  All comparisons are exact (sets, ids, float64 depths, the PER
+outputs, over both fragment streams (perspective and the CLI's ortho).  All
+comparisons are exact (sets, ids, float64 depths, the PER
 fraction).
 """
 
@@ -45,7 +46,9 @@ def _objs(c):
                           cl[15], cl[16])
     cams = [views.Camera(tuple(r[0:3]), tuple(r[9:12]), tuple(r[6:9]), tuple(r[3:6]), r[15], r[13], r[14])
             for r in c["cams"]]
-    return scene, fr, cell, cams, tuple(int(x) for x in c["dims"]), FroxelizeConfig(supersample=int(c["ss"]))
+    mode = "ortho" if int(c.get("mode", 0)) == 1 else "perspective"
+    return scene, fr, cell, cams, tuple(int(x) for x in c["dims"]), FroxelizeConfig(supersample=int(c["ss"]),
+                                                                                    mode=mode)
 
 
 @pytest.mark.parametrize("idx", range(len(CASES)), ids=IDS)
