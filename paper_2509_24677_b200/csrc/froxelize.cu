@@ -796,7 +796,7 @@ constexpr int kSpanChunk = kRasterThreads * kSpanRowsPerThread;
 // kKind 0: OR bits (froxelize), 1: cull marks, 2: (froxel, triangle) pairs,
 // 3: z-buffer min (GT), 4: smallest primitive id among z-ties (GT).
 template <bool kFilter, int kKind>
-__global__ void __launch_bounds__(kRasterThreads, 3)
+__global__ void __launch_bounds__(kRasterThreads, kKind >= 5 ? 4 : 3)
     span_kernel(Params p, GtParams g, const fpvs_frustum* __restrict__ views, const int64_t* __restrict__ prim_ids,
                 Work wk, unsigned long long* __restrict__ zbuf, long long* __restrict__ pidbuf) {
   constexpr int kWarpRows = 32 * kSpanRowsPerThread;
