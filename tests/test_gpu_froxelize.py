@@ -201,6 +201,35 @@ def test_ortho_random_scenes_vs_oracle(seed, dims, ss, depth):
         assert diff <= 4, diff
 
 
+def _boxes(seed, n, frustum):
+    """Axis-aligned boxes (12 triangles each): faces edge-on in two of the
+    three ortho passes (zero-area, dropped by the degeneracy test) and
+    edges on lattice lines."""
+    rng = np.random.default_rng(seed)
+    corners = np.array([[x, y, z] for z in (0, 1) for y in (0, 1) for x in (0, 1)], dtype=np.float64)
+    faces = np.array([[0, 1, 3], [0, 3, 2], [4, 6, 7], [4, 7, 5], [0, 4, 5], [0, 5, 1],
+                      [2, 3, 7], [2, 7, 6], [0, 2, 6], [0, 6, 4], [1, 5, 7], [1, 7, 3]])
+    vs, ts = [], []
+    for k in range(n):
+        lo = frustum._o + 8.0 * frustum._basis[2] + rng.uniform(-5, 5, size=3)
+        vs.append(lo + corners * rng.uniform(0.2, 3.0, size=3))
+        ts.append(faces + 8 * k)
+    return np.concatenate(vs), np.concatenate(ts)
+
+
+@pytest.mark.parametrize("seed,dims,ss", [(0, (8, 8, 8), 1), (1, (32, 32, 32), 2), (2, (16, 40, 24), 3)])
+def test_axis_aligned_boxes_vs_oracle(seed, dims, ss):
+    from paper_2509_24677_b200.froxelize import FroxelizeConfig, Froxelizer
+    fr = _random_frustum(200 + seed)
+    v, t = _boxes(seed, 60, fr)
+    fz = Froxelizer(v, t)
+    for mode, fn in (("ortho", ofz.froxelize_ortho), ("perspective", ofz.froxelize)):
+        got = fz.run(fr, dims, FroxelizeConfig(supersample=ss, mode=mode)).cpu().numpy()
+        ref = fn(v, t, fr._o, fr._basis, fr.half_extent, fr.near, fr.far, dims, ss)
+        assert np.unpackbits(ref).sum() > 0, mode
+        assert np.array_equal(got, ref), (mode, int(np.unpackbits(got ^ ref).sum()))
+
+
 def test_ortho_drop_in_and_graph_replay():
     """froxelize(..., FroxelizeConfig(mode="ortho")) and a captured replay give the golden grid."""
     import torch
