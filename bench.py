@@ -155,7 +155,7 @@ def run_reference(args):
     from paper_2509_24677_b200 import synth
     occ = synth.config2_grid(1)
     cores = os.cpu_count()
-    warm = min(args.warmup, 1)
+    warm = min(args.warmup, 3)  # CPU frames take seconds; 3 covers the warm-up rule without stretching the run
     for _ in range(warm):
         cpu_frame_time(occ)
     times = [cpu_frame_time(occ) for _ in range(args.steps)]
