@@ -47,6 +47,12 @@ for name in os.environ.get("LAYERS", "enc0b,enc1a,enc2a").split(","):
         print(f"  CTAs {ok.sum()}: launch span {(en_.max() - t00) / 1000:.2f} us; start spread {(st_.max() - t00) / 1000:.2f} us; "
               f"CTA duration min {d.min():.2f} median {np.median(d):.2f} max {d.max():.2f} us")
         idx = np.nonzero(ok)[0]
+        if hasattr(lib, "fpvs_debug_halo_clk"):
+            ck = (ctypes.c_longlong * 320)()
+            lib.fpvs_debug_halo_clk(ck)
+            ck = np.frombuffer(ck, dtype=np.int64).reshape(2, 160)
+            f = (ck[1][ok] - ck[0][ok]) / np.maximum(en_ - st_, 1)
+            print(f"   SM clock over the CTA: median {np.median(f) * 1e3:.0f} MHz (min {f.min() * 1e3:.0f}, max {f.max() * 1e3:.0f})")
         print("   durations by CTA:", " ".join(f"{i}:{x:.1f}" for i, x in zip(idx[:40], d[:40])))
         sm = (ctypes.c_uint * 160)()
         if hasattr(lib, "fpvs_debug_halo_smid"):
@@ -81,6 +87,17 @@ for name in os.environ.get("LAYERS", "enc0b,enc1a,enc2a").split(","):
     print(f"  stages {st}: mma start interval {np.nanmean(np.diff(r[:, 3])):.3f} us | mma start - last builder "
           f"{np.nanmean(r[:, 3] - bmax):.3f} | mma start - B issue {np.nanmean(r[:, 3] - r[:, 0]):.3f} | "
           f"issue->commit {np.nanmean(r[:, 4] - r[:, 3]):.3f}")
+    ch = []
+    for i in range(min(st, 200)):
+        prev = t[4096 + 2 * i]
+        for g in range(4):
+            v = t[6000 + 4 * i + g]
+            if v and prev:
+                ch.append((v - prev) / 1000.0)
+                prev = v
+    if ch:
+        ch = np.array(ch)
+        print(f"  per-chunk (4 MMA) issue time: mean {ch.mean():.3f} us, median {np.median(ch):.3f}, p10 {np.percentile(ch, 10):.3f}, p90 {np.percentile(ch, 90):.3f}")
     for i in list(range(0, min(st, 10))) + list(range(max(10, st - 4), st)):
         print("   st %3d  B issued %7.2f | built g0 %7.2f g1 %7.2f | mma start %7.2f commit %7.2f" % ((i,) + rows[i]))
     if os.environ.get("PEER"):

@@ -94,8 +94,8 @@ void run(long long* d) {
 int main() {
   long long* d;
   cudaMalloc(&d, 8);
-  run<64, 1, 0>(d); run<64, 1, 1>(d); run<64, 0, 1>(d);
-  run<128, 1, 0>(d); run<128, 1, 1>(d); run<128, 0, 1>(d);
-  run<256, 1, 1>(d); run<256, 0, 1>(d);
+  run<64, 1, 1>(d); run<64, 1, 2>(d); run<64, 1, 4>(d); run<64, 1, 8>(d); run<64, 1, 16>(d);
+  run<64, 0, 1>(d); run<64, 0, 4>(d); run<64, 0, 0>(d);
+  run<128, 1, 2>(d); run<128, 1, 4>(d); run<128, 0, 4>(d);
   return 0;
 }
