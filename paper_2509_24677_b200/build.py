@@ -16,6 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfpvs.so")
+PROFILE_LIB = os.path.join(HERE, "libfpvs_prof.so")  # -DFPVS_PROFILE: timestamps + ablation knobs (tools/ only)
 SOURCES = ["capi.cu", "interleave.cu", "kmap.cu", "kmap_pairs.cu", "levels.cu", "spconv_simt.cu", "spconv_tc.cu", "spconv_halo.cu", "upsort.cu", "wgrad_tc.cu", "wgrad_halo.cu", "optim.cu", "froxelize.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
@@ -29,19 +30,25 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale(objs_src) -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "fpvs.h")]
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    """Compile every .cu under csrc/ into libfpvs.so (parallel per-file objects)."""
-    if not force and not _stale(SOURCES):
-        return LIB
-    objdir = os.path.join(HERE, "_build")
+def build(force: bool = False, verbose: bool = True, profile: bool = False) -> str:
+    """Compile every .cu under csrc/ into libfpvs.so (parallel per-file objects).
+
+    ``profile`` builds libfpvs_prof.so instead, with -DFPVS_PROFILE: per-role
+    timestamp buffers, the FPVS_*_DEBUG / FPVS_HALO_ABL knobs and the
+    fpvs_debug_* read-out entry points (tools/halo_timeline.py, halo_ablate.py
+    load it through FPVS_LIB).  The product library never contains them."""
+    lib = PROFILE_LIB if profile else LIB
+    if not force and not _stale(lib):
+        return lib
+    objdir = os.path.join(HERE, "_build_prof" if profile else "_build")
     os.makedirs(objdir, exist_ok=True)
     cc = nvcc()
     procs = []
@@ -49,7 +56,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [cc, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [cc, *ARCH, *FLAGS, *(["-DFPVS_PROFILE"] if profile else []), "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     for src, p in procs:
         out = p.communicate()[0].decode()
@@ -57,13 +64,13 @@ def build(force: bool = False, verbose: bool = True) -> str:
             raise RuntimeError(f"nvcc failed on {src}:\n{out}")
         if verbose and out.strip():
             print(out, file=sys.stderr)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.check_call([cc, *ARCH, "-shared", "-o", tmp, *objs])
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
-        print(f"built {LIB}", file=sys.stderr)
-    return LIB
+        print(f"built {lib}", file=sys.stderr)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    build(force="--force" in sys.argv, profile="--profile" in sys.argv)

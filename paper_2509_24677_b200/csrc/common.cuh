@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdarg.h>
+#include <stdlib.h>
 
 #include "../../include/fpvs.h"
 
@@ -56,6 +57,23 @@ cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
+
+// -------- profiling builds ----------------------------------------------
+// Per-role timestamp buffers and ablation switches exist only in a profiling
+// build (-DFPVS_PROFILE; `python -m paper_2509_24677_b200.build --profile`
+// writes libfpvs_prof.so).  In the production library a kernel's knob is the
+// constant 0, so every debug branch folds away, no launcher reads the
+// environment and no __device__ scratch is shared between concurrent launches.
+#ifdef FPVS_PROFILE
+#define FPVS_KNOB(p) ((p).dbg)
+inline int debug_knob(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : 0;
+}
+#else
+#define FPVS_KNOB(p) 0
+inline int debug_knob(const char*) { return 0; }
+#endif
 
 inline int grid_for(long long work, int block, int per_sm = 8) {
   long long g = (work + block - 1) / block;

@@ -1009,10 +1009,19 @@ inline Layout layout(long long ntris, long long grid_bytes, long long sx, long l
   return L;
 }
 
-inline int env_int(const char* name, int dflt) {
+// raster segment widths: FPVS_FROX_SEG / FPVS_GT_SEG (tuning knobs, read once per process)
+inline int env_seg(const char* name, int dflt) {
   const char* e = getenv(name);
   const int v = e ? atoi(e) : dflt;
   return v >= 8 && v <= 1024 ? v : dflt;
+}
+inline int frox_seg() {
+  static const int v = env_seg("FPVS_FROX_SEG", 16);
+  return v;
+}
+inline int gt_seg() {
+  static const int v = env_seg("FPVS_GT_SEG", 64);
+  return v;
 }
 
 // FPVS_FROX_SPANS=0 rasterizes whole bounding boxes instead of row spans (A/B check)
@@ -1119,7 +1128,7 @@ int froxel_pass(const double* verts, long long nverts, const int64_t* tris, long
   p.nz = Nz;
   p.depth_log = depth_mode == FPVS_DEPTH_LOG;
   p.rows_mode = spans() ? 1 : 0;
-  p.seg = env_int("FPVS_FROX_SEG", 16);
+  p.seg = frox_seg();
   if (cudaMemsetAsync(wk.total, 0, 16, s) != cudaSuccess) FPVS_CHECK_LAUNCH("memset");  // total + nsamples
   if (ntris == 0) return FPVS_OK;
   setup_kernel<false><<<wk.nb, kSetupThreads, 0, s>>>(p, nullptr, verts, nverts, tris, ntris, wk);
@@ -1263,7 +1272,7 @@ int ortho_pass(const double* verts, long long nverts, const int64_t* tris, long 
     p.nz = Nz;
     p.depth_log = depth_mode == FPVS_DEPTH_LOG;
     p.rows_mode = 1;
-    p.seg = env_int("FPVS_FROX_SEG", 16);
+    p.seg = frox_seg();
     GtParams g = {};
     for (int i = 0; i < 3; ++i) g.fo[i] = fr->origin[i];
     for (int i = 0; i < 9; ++i) g.fb[i] = fr->basis[i];
@@ -1652,7 +1661,7 @@ extern "C" int fpvs_gt_pvs(const double* verts, long long nverts, const int64_t*
   p.nz = Nz;
   p.depth_log = 0;
   p.rows_mode = spans() ? 1 : 0;
-  p.seg = env_int("FPVS_GT_SEG", 64);
+  p.seg = gt_seg();
   GtParams g;
   for (int i = 0; i < 3; ++i) g.fo[i] = fr->origin[i];
   for (int i = 0; i < 9; ++i) g.fb[i] = fr->basis[i];
@@ -1718,7 +1727,7 @@ extern "C" int fpvs_render_depth(const double* verts, long long nverts, const in
     p.sx = (double)res_w;
     p.sy = (double)res_h;
     p.rows_mode = spans() ? 1 : 0;
-    p.seg = env_int("FPVS_GT_SEG", 64);
+    p.seg = gt_seg();
     GtParams g = {};
     g.iw = res_w;
     g.ih = res_h;

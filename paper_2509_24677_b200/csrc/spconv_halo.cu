@@ -223,13 +223,21 @@ struct Params {
   int ldy, col_off;
   float* part;    // [tiles][nblk][split][128][BN] fp32 partials (split > 1)
   int* counters;  // [tiles][nblk] arrival counters, zero between launches
-  int dbg;        // FPVS_HALO_DEBUG=1: per-role timestamps of CTAs 0/1 (profiling only)
+  int dbg;        // profiling builds: FPVS_HALO_DEBUG (timestamps)
+  int abl;        // profiling builds: FPVS_HALO_ABL (ablations)
 };
 
-// ---------------- profiling timestamps (FPVS_HALO_DEBUG) ----------------
+// ---------------- profiling (profiling builds only) ----------------
+// FPVS_HALO_DEBUG = 1 + 256 k: per-role timestamps of CTAs k, k + 1;
+// FPVS_HALO_ABL: ablation switches for bound analysis (tools/halo_ablate.py;
+// results are wrong by construction): bit 16 weight chunks only for the first
+// NS stages, 17 builders skip the smem halo reads, 18 builders skip
+// tcgen05.st, 19 loaders skip the halo row copies, 20 no MMAs.
+#ifdef FPVS_PROFILE
 __device__ unsigned long long g_hts[2][8192];   // CTAs (dbg >> 8) and (dbg >> 8) + 1
 __device__ unsigned long long g_hcta[2][160];  // per-CTA start / end
 __device__ unsigned g_hsm[160];
+__device__ long long g_hclk[2][160];
 #define HTS(slot)                                                                        \
   do {                                                                                   \
     if (p.dbg && blockIdx.x - (unsigned)(p.dbg >> 8) < 2u && (slot) < 8192) {          \
@@ -238,6 +246,13 @@ __device__ unsigned g_hsm[160];
       g_hts[blockIdx.x - (p.dbg >> 8)][(slot)] = t_;                                     \
     }                                                                                    \
   } while (0)
+#define ABL(bit) (p.abl & (1 << (bit)))
+#else
+#define HTS(slot) \
+  do {            \
+  } while (0)
+#define ABL(bit) 0
+#endif
 
 // Per-CTA unit table: the tile mask and halo size of this CTA's k-th unit,
 // loaded once in the prologue so no role pays a global-memory round trip at a
@@ -400,6 +415,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) HTS(0);
+#ifdef FPVS_PROFILE
   if (p.dbg && tid == 0 && blockIdx.x < 160) {
     unsigned long long t_;
     unsigned sm_;
@@ -407,7 +423,9 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));
     g_hcta[0][blockIdx.x] = t_;
     g_hsm[blockIdx.x] = sm_;
+    g_hclk[0][blockIdx.x] = clock64();
   }
+#endif
   const int n = min(*p.n_dev, p.cap);
   const int mtiles = (n + BM - 1) / BM;
   const int nunits = num_units(p, mtiles);
@@ -434,17 +452,13 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   }
   for (int c = tid; c < p.cout; c += THREADS) s_bias[c] = p.bias ? p.bias[c] : 0.f;
   if (tid < kUnitCache) {
-    // this CTA's units decoded in parallel (tile masks and halo sizes come
-    // from the map kernels, two or more launches back)
+    // this CTA's units decoded in parallel (the tile masks come from the map
+    // kernels, two or more launches back; the halo sizes may be the previous
+    // launch's output, so the loader warps read them after their PDL wait)
     const int u = blockIdx.x + tid * gridDim.x;
     Unit U{};
-    int hn = 0;
-    if (u < nunits) {
-      unit_of(p, u, cpo, mtiles, U);
-      hn = __ldg(p.halo_n + U.mt);
-    }
+    if (u < nunits) unit_of(p, u, cpo, mtiles, U);
     s_units[tid] = U;
-    s_uhn[tid] = hn;
   }
   if (warp == W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem))
@@ -531,7 +545,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
               }
             }
           } else {
-          const int li = ln[j];
+          const int li = ABL(17) ? -1 : ln[j];
           if (li >= 0) {
             const uint8_t* src = hbuf + li * 128;
             const int sw = li & 7;
@@ -556,8 +570,10 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
           }
           mbar_wait(smem_u32(empty + stage), ((st / C::NS) & 1) ^ 1);
           tc_fence_after();
-          tmem_st32(t_a + (stage * C::G + i % C::G) * 32, v);
-          tmem_st_wait();
+          if (!ABL(18)) {
+            tmem_st32(t_a + (stage * C::G + i % C::G) * 32, v);
+            tmem_st_wait();
+          }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(full + stage));
@@ -587,9 +603,16 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     }
   } else if (warp < W_B) {
     // ===================== halo loaders =====================
-    pdl_wait();  // halo rows are the previous launch's output
+    pdl_wait();  // halo rows, sizes and local tables may be the previous launch's output
     if (tid == W_LOAD * 32) pdl_trigger();
     const int tl = tid - W_LOAD * 32;
+    // the unit cache's halo sizes; the builders read them only after the first
+    // hmeta barrier, which loader thread 0 arrives on after this named barrier
+    for (int k = tl; k < kUnitCache; k += LOADERS) {
+      const int u = blockIdx.x + k * gridDim.x;
+      s_uhn[k] = u < nunits ? __ldg(p.halo_n + s_units[k].mt) : 0;
+    }
+    named_bar(2, LOADERS);
     const int pc = tl & 7;
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u;
     uint32_t gc = 0;
@@ -620,7 +643,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         // the first halo is shared with the builders: loader thread tl takes rows
         // tl/8 + 40k of the 320-thread split; later halos rows tl/8 + 8k
         const int rstep = gc == 0 ? (LOADERS + 256) / 8 : LOADERS / 8;
-        if (!pair || pc < 4) {  // 32-channel rows: four 16-byte pieces
+        if ((!pair || pc < 4) && !ABL(19)) {  // 32-channel rows: four 16-byte pieces
 #pragma unroll 4
           for (int i = tl >> 3; i < H; i += rstep) {
             const int g = hr[i];
@@ -634,6 +657,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     }
   } else if (warp == W_B) {
     // ===================== weight loader =====================
+    pdl_wait();  // the packed weights may be the previous launch's output (lazy / per-step re-pack)
     if (lane == 0) {
       uint32_t st = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -649,6 +673,10 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
           mbar_wait(smem_u32(empty + stage), ((st / C::NS) & 1) ^ 1);
           if (st < 1000) HTS(5000 + st);
           const uint32_t fb = smem_u32(full + stage);
+          if (ABL(16) && st >= (uint32_t)C::NS) {
+            mbar_arrive(fb);
+            continue;
+          }
           mbar_arrive_expect_tx(fb, nv * C::B_SUB);
           for (int g = 0; g < nv; ++g, w.next())
             bulk_g2s(smem_u32(sB + stage * C::STAGE_B + g * C::B_SUB), wblk + (size_t)(w.j * cpo + w.c) * C::B_SUB,
@@ -682,9 +710,12 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
           for (int g = 0; g < nv; ++g) {
             const uint32_t ta = tmem_base + C::ACOL + (stage * C::G + g) * 32;
             const uint64_t bd = sw128_desc(smem_u32(sB + stage * C::STAGE_B + g * C::B_SUB));
+            if (!ABL(20)) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              umma_bf16_ts(dtm, ta + 8 * k, bd + 2 * k, idesc, (i == 0 && g == 0 && k == 0) ? 0u : 1u);
+              for (int k = 0; k < BK / 16; ++k)
+                umma_bf16_ts(dtm, ta + 8 * k, bd + 2 * k, idesc, (i == 0 && g == 0 && k == 0) ? 0u : 1u);
+            }
+            if (st < 200) HTS(6000 + 4 * st + g);
           }
           umma_commit(smem_u32(empty + stage));
           if (st < 450) HTS(4097 + 2 * st);
@@ -798,11 +829,14 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   tc_fence_before();
   __syncthreads();
   if (tid == 0) HTS(3);
+#ifdef FPVS_PROFILE
   if (p.dbg && tid == 0 && blockIdx.x < 160) {
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
     g_hcta[1][blockIdx.x] = t_;
+    g_hclk[1][blockIdx.x] = clock64();
   }
+#endif
   if (warp == W_MMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
@@ -834,18 +868,22 @@ inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 using namespace fpvs;
 
-// internal profiling hook (not part of the ABI): CTA 0/1 timestamps
+#ifdef FPVS_PROFILE
+// profiling builds only (not part of the ABI): CTA timestamps, SM ids, clocks
 extern "C" int fpvs_debug_halo_timestamps(unsigned long long* host, int n) {
   if (n > 2 * 8192) n = 2 * 8192;
   return cudaMemcpyFromSymbol(host, halo::g_hts, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 3;
 }
-
 extern "C" int fpvs_debug_halo_cta_times(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, halo::g_hcta, sizeof(unsigned long long) * 320) == cudaSuccess ? 0 : 3;
+}
+extern "C" int fpvs_debug_halo_clk(long long* host) {
+  return cudaMemcpyFromSymbol(host, halo::g_hclk, sizeof(long long) * 320) == cudaSuccess ? 0 : 3;
 }
 extern "C" int fpvs_debug_halo_smid(unsigned* host) {
   return cudaMemcpyFromSymbol(host, halo::g_hsm, sizeof(unsigned) * 160) == cudaSuccess ? 0 : 3;
 }
+#endif
 
 extern "C" size_t fpvs_kmap_halo_size(int cap) {
   if (cap < 1) return 0;
@@ -939,8 +977,8 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
   const size_t items = split < 0 ? (size_t)kNumSMs : tiles * p.nblk;
   p.counters = (int*)ws;
   p.part = (float*)((uint8_t*)ws + halo::align256(items * 4));
-  const char* dbg = getenv("FPVS_HALO_DEBUG");
-  p.dbg = dbg ? atoi(dbg) : 0;
+  p.dbg = debug_knob("FPVS_HALO_DEBUG");
+  p.abl = debug_knob("FPVS_HALO_ABL");
   const cudaStream_t st = as_stream(stream);
   if (cin == 32) {
     if (bn == 32) return halo::launch<32, true>(p, st);

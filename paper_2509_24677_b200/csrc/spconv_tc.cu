@@ -91,7 +91,8 @@ struct Cfg {
   static_assert(SMEM * MINB <= 232448, "shared memory budget");
 };
 
-// ---------------- profiling timestamps (FPVS_TC_DEBUG & 16) ----------------
+// ---------------- profiling timestamps (profiling builds, FPVS_TC_DEBUG & 16) ----------------
+#ifdef FPVS_PROFILE
 __device__ unsigned long long g_dbg_ts[2][4096];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -100,8 +101,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define TS(slot)                                                              \
   do {                                                                        \
-    if ((p.dbg & 16) && blockIdx.x < 2 && (slot) < 4096) g_dbg_ts[blockIdx.x][(slot)] = gtimer(); \
+    if ((FPVS_KNOB(p) & 16) && blockIdx.x < 2 && (slot) < 4096) g_dbg_ts[blockIdx.x][(slot)] = gtimer(); \
   } while (0)
+#else
+#define TS(slot) \
+  do {           \
+  } while (0)
+#endif
 
 // Walks the K-chunks a tile needs, in order, from its offset mask: for
 // Cin >= 64 every ci-chunk (cpo per offset) of each present offset j; for
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
             skip[i] = v < 0;
             off[i] = skip[i] ? 0u : (uint32_t)v * ldx2;
           }
-          if (!(p.dbg & 2)) {
+          if (!(FPVS_KNOB(p) & 2)) {
 #pragma unroll
             for (int i = 0; i < NPT; ++i) cp_async16_zfill(a_sub + dsto[i], base + off[i], skip[i]);
           }
@@ -293,7 +299,10 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
   } else if (warp == C::BW_WARP) {
     // ===================== B loader (one elected lane) =====================
     // Streams each stage's weight chunks with bulk copies (TMA engine) and
-    // writes the stage flags the MMA issuer reads.
+    // writes the stage flags the MMA issuer reads.  Waits for the previous
+    // launch first: the packed weights may be its output (a lazy or per-step
+    // re-pack enqueued right before this conv).
+    pdl_wait();
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
           const uint32_t fb = smem_u32(full + stage);
           const uint32_t b_stage = smem_u32(sB + stage * C::STAGE_B);
           s_info[stage] = (st == 0 ? 1u : 0u) | (st == nst - 1 ? 2u : 0u) | ((uint32_t)nvalid << 2);
-          if (p.dbg & 4) {
+          if (FPVS_KNOB(p) & 4) {
             mbar_arrive(fb);
           } else {
             mbar_arrive_expect_tx(fb, nvalid * C::B_SUB);
@@ -380,9 +389,9 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
           if (firstc) TS(11 + 8 * it);
           firstc = false;
           tc_fence_after();
-          if (!(p.dbg & 128)) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 (async proxy) reads
+          if (!(FPVS_KNOB(p) & 128)) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 (async proxy) reads
           const uint32_t info = s_info[stage];
-          if (!(p.dbg & 1)) {
+          if (!(FPVS_KNOB(p) & 1)) {
             const uint32_t a_stage = smem_u32(sA + stage * C::STAGE_A);
             const uint32_t b_stage = smem_u32(sB + stage * C::STAGE_B);
             const int nvalid = (int)(info >> 2);
@@ -639,12 +648,14 @@ static int resolve_bn(int bn, int cout) {
   return tc::valid_bn(bn) ? bn : -1;
 }
 
-// internal profiling hook (not part of the ABI): copy CTA 0/1 timestamps out
+#ifdef FPVS_PROFILE
+// profiling builds only (not part of the ABI): copy CTA 0/1 timestamps out
 extern "C" int fpvs_debug_tc_timestamps(unsigned long long* host, int n) {
   if (n > 2 * 4096) n = 2 * 4096;
   cudaError_t e = cudaMemcpyFromSymbol(host, tc::g_dbg_ts, sizeof(unsigned long long) * n);
   return e == cudaSuccess ? 0 : 3;
 }
+#endif
 
 extern "C" size_t fpvs_pack_weights_tc_size(int K, int cin, int cout, int bn) {
   bn = resolve_bn(bn, cout);
@@ -694,8 +705,7 @@ static int tc_common(tc::Params& p, const void* x, int ldx, int x_rows, const in
   p.bias = bias;
   p.cin = cin;
   p.cout = cout;
-  const char* dbg = getenv("FPVS_TC_DEBUG");
-  p.dbg = dbg ? atoi(dbg) : 0;
+  p.dbg = debug_knob("FPVS_TC_DEBUG");
   return FPVS_OK;
 }
 

@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_halo_kernel(const Params p) 
                           : make_uint4(0u, 0u, 0u, 0u);
           }
         }
-        if (p.dbg & 1) {
+        if (FPVS_KNOB(p) & 1) {
 #pragma unroll
           for (int t = 0; t < PPT; ++t) v[t] = make_uint4(0u, 0u, 0u, 0u);
         }
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_halo_kernel(const Params p) 
       mbar_wait(smem_u32(hmeta + hb), hph);
       const int* hr = reinterpret_cast<const int*>(hbuf + HB_ROWS);
       const uint32_t hs = smem_u32(hbuf);
-      for (int q = lt; q < ((p.dbg & 8) ? 0 : H * 4); q += LOADERS) {
+      for (int q = lt; q < ((FPVS_KNOB(p) & 8) ? 0 : H * 4); q += LOADERS) {
         const int i = q >> 2, pc = q & 3;
         cp_async16(hs + i * 64 + ((pc ^ (i & 3)) << 4), xg + (long long)hr[i] * ldx2 + pc * 16, 16);
       }
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_halo_kernel(const Params p) 
 #pragma unroll
           for (int kk = 0; kk < KC / 16; ++kk) {
             const uint32_t accumulate = ((started >> mb) & 1u) | (kk ? 1u : 0u);
-            if (!(p.dbg & 2)) umma_bf16(acc, desc_mn(a_st + kk * 256), desc_mn(bs + kk * 256), idesc, accumulate);
+            if (!(FPVS_KNOB(p) & 2)) umma_bf16(acc, desc_mn(a_st + kk * 256), desc_mn(bs + kk * 256), idesc, accumulate);
           }
           started |= 1u << mb;
           umma_commit(smem_u32(empty + stage));
@@ -392,8 +392,7 @@ extern "C" int fpvs_spconv_wgrad_halo(const void* x, int ldx, const void* dz, in
   p.lnbr = lnbr;
   p.cout = cout;
   p.part = (float*)workspace;
-  const char* dbg = getenv("FPVS_WGRAD_DEBUG");
-  p.dbg = dbg ? atoi(dbg) : 0;
+  p.dbg = debug_knob("FPVS_WGRAD_DEBUG");
   cudaStream_t s = as_stream(stream);
   const int grid = kNumSMs;
   cudaError_t e = launch_kernel(wgh::wgrad_halo_kernel, dim3(grid), dim3(wgh::THREADS), wgh::SMEM, s, p);

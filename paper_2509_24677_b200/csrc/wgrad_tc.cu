@@ -32,6 +32,7 @@ constexpr int PROD = 256;
 constexpr int W_MMA = PROD / 32;
 constexpr int APT = KC * 16 / PROD;  // A pieces per producer thread per chunk
 
+#ifdef FPVS_PROFILE
 __device__ unsigned long long g_wts[4096];  // FPVS_WGRAD_DEBUG & 32: CTA 0 timestamps
 __device__ __forceinline__ void wts(const int dbg, int slot) {
   if ((dbg & 32) && blockIdx.x == 0 && slot < 4096) {
@@ -40,6 +41,9 @@ __device__ __forceinline__ void wts(const int dbg, int slot) {
     g_wts[slot] = t;
   }
 }
+#else
+__device__ __forceinline__ void wts(const int, int) {}
+#endif
 
 struct Params {
   const __nv_bfloat16* x;
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_tc_kernel(const Params p) {
       for (int t = 0; t < NPT; ++t) {
         const int i = c * KC + n_row[t];
         pre[t] = -1;
-        if (n_slot[t] >= 0 && i < n) pre[t] = (p.nbr && !(p.dbg & 4)) ? __ldg(p.nbr + (long long)i * p.K + n_j[t]) : i;
+        if (n_slot[t] >= 0 && i < n) pre[t] = (p.nbr && !(FPVS_KNOB(p) & 4)) ? __ldg(p.nbr + (long long)i * p.K + n_j[t]) : i;
       }
     };
     const char* xg = reinterpret_cast<const char*>(p.x);
@@ -175,16 +179,16 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_tc_kernel(const Params p) {
     for (int c = c0; c < c1; ++c) {
       const int k = c - c0, stage = k % NS;
       const int i0 = c * KC;
-      if (tid == 0) wts(p.dbg, 8 * k);
+      if (tid == 0) wts(FPVS_KNOB(p), 8 * k);
       named_bar(2, PROD);  // previous chunk's readers are done with s_nb
 #pragma unroll
       for (int t = 0; t < NPT; ++t)
         if (n_slot[t] >= 0) s_nb[n_slot[t]] = pre[t];
       named_bar(2, PROD);
-      if (tid == 0) wts(p.dbg, 8 * k + 1);
+      if (tid == 0) wts(FPVS_KNOB(p), 8 * k + 1);
       if (c + 1 < c1) prefetch(c + 1);  // in flight while this chunk's copies issue
       mbar_wait_sleep(smem_u32(empty + stage), ((k / NS) & 1) ^ 1, 32);
-      if (tid == 0) wts(p.dbg, 8 * k + 2);
+      if (tid == 0) wts(FPVS_KNOB(p), 8 * k + 2);
       const uint32_t a_st = smem_u32(sA + stage * A_STAGE), b_st = smem_u32(sB + stage * B_STAGE);
 #pragma unroll
       for (int t = 0; t < APT; ++t) {
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_tc_kernel(const Params p) {
         }
         const int src = a_nb[t] >= 0 ? s_nb[a_nb[t]] : -1;
         const char* g = xg + (src >= 0 ? (long long)src * ldx2 + a_cof[t] : 0);
-        if (!(p.dbg & 1)) cp_async16(dst, g, src >= 0 ? 16u : 0u);
+        if (!(FPVS_KNOB(p) & 1)) cp_async16(dst, g, src >= 0 ? 16u : 0u);
       }
 #pragma unroll
       for (int t = 0; t < NBP; ++t) {
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_tc_kernel(const Params p) {
         if (tid + PROD * t < KC * (NPAD / 8)) cp_async16(b_st + b_dst[t], g, ok ? 16u : 0u);
       }
       cp_async_mbar_arrive_noinc(smem_u32(full + stage));
-      if (tid == 0) wts(p.dbg, 8 * k + 3);
+      if (tid == 0) wts(FPVS_KNOB(p), 8 * k + 3);
     }
     if (tid == 0) pdl_trigger();
   } else {
@@ -219,17 +223,17 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_tc_kernel(const Params p) {
       for (int c = c0; c < c1; ++c) {
         const int k = c - c0, stage = k % NS;
         mbar_wait(smem_u32(full + stage), (k / NS) & 1);
-        wts(p.dbg, 8 * k + 4);
+        wts(FPVS_KNOB(p), 8 * k + 4);
         tc_fence_after();
         fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor core (async proxy) reads
         const uint32_t a_st = smem_u32(sA + stage * A_STAGE), b_st = smem_u32(sB + stage * B_STAGE);
-        if (!(p.dbg & 2)) {
+        if (!(FPVS_KNOB(p) & 2)) {
 #pragma unroll
           for (int kk = 0; kk < KC / 16; ++kk)
             umma_bf16(tmem, desc_mn(a_st + kk * 256), desc_mn(b_st + kk * 256), idesc, (k | kk) ? 1u : 0u);
         }
         umma_commit(smem_u32(empty + stage));
-        wts(p.dbg, 8 * k + 5);
+        wts(FPVS_KNOB(p), 8 * k + 5);
       }
       umma_commit(smem_u32(tfull));
     }
@@ -353,9 +357,11 @@ int launch(const Params& p, cudaStream_t s) {
 
 using namespace fpvs;
 
+#ifdef FPVS_PROFILE
 extern "C" int fpvs_debug_wgrad_timestamps(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, wg::g_wts, sizeof(unsigned long long) * 4096) == cudaSuccess ? 0 : 3;
 }
+#endif
 
 extern "C" size_t fpvs_wgrad_tc_workspace_size(int K, int cin, int cout, int cap) {
   if (K < 1 || cin < 8 || cin % 8 || cout < 1 || cout > 256 || cap < 1) return 0;
@@ -392,8 +398,7 @@ extern "C" int fpvs_spconv_wgrad_tc(const void* x, int ldx, const void* dz, int 
   p.nmb = (K * cin + 127) / 128;
   p.nsplit = wg::splits_for(p.nmb, cap);
   p.part = (float*)workspace;
-  const char* dbg = getenv("FPVS_WGRAD_DEBUG");
-  p.dbg = dbg ? atoi(dbg) : 0;
+  p.dbg = debug_knob("FPVS_WGRAD_DEBUG");
   cudaStream_t s = as_stream(stream);
   int rc = p.npad == 16 ? wg::launch<16>(p, s) : p.npad == 32 ? wg::launch<32>(p, s) : p.npad == 64 ? wg::launch<64>(p, s)
          : p.npad == 128 ? wg::launch<128>(p, s) : wg::launch<256>(p, s);

@@ -10,6 +10,9 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# timestamps / ablations exist only in the profiling build (python -m paper_2509_24677_b200.build --profile)
+os.environ.setdefault("FPVS_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                               "paper_2509_24677_b200", "libfpvs_prof.so"))
 import torch  # noqa: E402
 
 from paper_2509_24677_b200 import synth  # noqa: E402
