@@ -92,6 +92,14 @@ int fpvs_kmap_subm(const int32_t* coords, const int32_t* n_active_dev, int cap,
                    const int32_t* index_vol, int B, int X, int Y, int Z,
                    int32_t* nbr, void* stream);
 
+/* Submanifold map for any odd kernel size k (K = k^3 taps; k = 3 gives the
+ * fpvs_kmap_subm table): nbr[i][(a*k + b)*k + c] = row of
+ * coords[i] + (a - k/2, b - k/2, c - k/2) or -1 (neural.py:187-199 im2col
+ * order; ModelConfig accepts any odd kernel, neural.py:49-51). */
+int fpvs_kmap_subm_k(const int32_t* coords, const int32_t* n_active_dev, int cap,
+                     const int32_t* index_vol, int B, int X, int Y, int Z, int k,
+                     int32_t* nbr, void* stream);
+
 /* Parent flags of a k2s2 down-conv: coarse_active[b, x>>1, y>>1, z>>1] = 1.
  * coarse_active must be zeroed first (fine dims X, Y, Z must be even). */
 int fpvs_kmap_coarsen(const int32_t* coords, const int32_t* n_active_dev, int cap,
@@ -306,6 +314,17 @@ int fpvs_loss_grad(const float* probs, int C, const int32_t* coords, const int32
                    int cap, const uint8_t* gt_bits, int d, int B, int Nx, int Ny, int Nz,
                    const double* sums, double alpha, double lam, float* dlogits,
                    double* loss_out, void* stream);
+
+/* Head epilogue over logits rows f32 [cap][ld] (a head layer with kernel
+ * k > 1, run first as a conv with no activation): sigmoid, [p >= tau],
+ * packed-bit scatter into out_bits (nullable), probs f32 [cap][d^3] (nullable). */
+int fpvs_head_rows(const float* logits, int ld, const int32_t* coords, const int32_t* n_dev, int cap,
+                   int d, int B, int Nx, int Ny, int Nz, float tau, uint8_t* out_bits, float* probs,
+                   void* stream);
+/* dz = dy * act'(y) on active rows from the layer's kept output y
+ * (relu: y > 0 <=> z > 0, neural.py:227-228; sigmoid: y (1 - y), :229-230). */
+int fpvs_act_backward(const float* dy, int lddy, const void* y, int y_dtype, int ldy,
+                      const int32_t* n_dev, int cap, int C, int act, float* dz, int lddz, void* stream);
 
 /* dgrad: dx[n] += dz[i] . W_j^T over pairs n = nbr[i][j] (mirrored gather:
  * dx[n] = sum_j dz[nbr[n][K-1-j]] . W_j^T for the symmetric subm map), then

@@ -109,11 +109,19 @@ def lookup(coords_q, coords_set, dims) -> np.ndarray:
     return np.where(hit, pos_c, -1).astype(np.int64)
 
 
-def kmap_subm(coords: np.ndarray, dims) -> np.ndarray:
-    """nbr[i, j] = row of coords[i] + o_j, or -1 (o_j z-fastest, j = 9a+3b+c)."""
+def subm_offsets(k: int) -> np.ndarray:
+    """Tap offsets of an odd k^3 kernel, j = (a*k + b)*k + c -> (a-p, b-p, c-p), p = k//2
+    (the im2col order of neural.py:187-199)."""
+    p = k // 2
+    return np.array([(a - p, b - p, c - p) for a in range(k) for b in range(k) for c in range(k)], np.int64)
+
+
+def kmap_subm(coords: np.ndarray, dims, k: int = 3) -> np.ndarray:
+    """nbr[i, j] = row of coords[i] + o_j, or -1 (o_j z-fastest, j = 9a+3b+c for k = 3)."""
     a = len(coords)
-    nbr = np.empty((a, 27), np.int64)
-    for j, o in enumerate(SUBM_OFFSETS):
+    offs = SUBM_OFFSETS if k == 3 else subm_offsets(k)
+    nbr = np.empty((a, len(offs)), np.int64)
+    for j, o in enumerate(offs):
         q = coords.copy()
         q[:, 1:] += o
         nbr[:, j] = lookup(q, coords, dims)
@@ -227,13 +235,12 @@ def chain_forward(cells: np.ndarray, layers, bf16: bool = False, return_logits: 
     dims = cells.shape[1:4]
     coords = active_coords(cells)
     x = cells[tuple(coords.T)].astype(np.float64)
-    nbr = kmap_subm(coords, dims)
-    centre = np.arange(len(coords))[:, None]
+    tabs = {k: kmap_subm(coords, dims, k) for k in {layer[0] for layer in layers}}
     rnd = bf16_round if bf16 else (lambda v: v)
     x = rnd(x)
     for li, (k, w, b, act) in enumerate(layers):
         w = rnd(w)
-        z = gather_conv(x, nbr if k == 3 else centre, w, b)
+        z = gather_conv(x, tabs[k], w, b)
         if li == len(layers) - 1:
             return coords, (z if return_logits else _act(z, act))
         x = rnd(_act(z, act))
@@ -353,11 +360,12 @@ def combined_loss(pred, gt, alpha=0.1, lam=0.99):
 # ---------------------------------------------------------------------------
 
 
-def chain_forward_cached(x0, nbr, layers):
+def chain_forward_cached(x0, nbr, layers, tables=None):
+    """``nbr`` is the k = 3 table; ``tables`` maps other kernel sizes to their k^3 tables."""
     centre = np.arange(len(x0))[:, None]
     caches, x = [], x0
     for k, w, b, act in layers:
-        tab = nbr if k == 3 else centre
+        tab = nbr if k == 3 else centre if k == 1 else tables[k]
         z = gather_conv(x, tab, w, b)
         y = _act(z, act)
         caches.append((x, tab, z, y))

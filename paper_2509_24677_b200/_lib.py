@@ -31,6 +31,7 @@ SIGNATURES = {
     "fpvs_cell_active_from_bits": (_i, [_p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_kmap_compact": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _i, _p, _z, _p]),
     "fpvs_kmap_subm": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _p, _p]),
+    "fpvs_kmap_subm_k": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_kmap_coarsen": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_kmap_down": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _p, _p]),
     "fpvs_kmap_up": (_i, [_p, _p, _i, _p, _i, _i, _i, _i, _p, _p]),
@@ -65,6 +66,8 @@ SIGNATURES = {
     "fpvs_loss_sums_size": (_z, [_i, _i]),
     "fpvs_loss_counts": (_i, [_p, _i, _p, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_loss_grad": (_i, [_p, _i, _p, _p, _i, _p, _i, _i, _i, _i, _i, _p, _d, _d, _p, _p, _p]),
+    "fpvs_head_rows": (_i, [_p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p]),
+    "fpvs_act_backward": (_i, [_p, _i, _p, _i, _i, _p, _i, _i, _i, _p, _i, _p]),
     "fpvs_spconv_dgrad_simt": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _p, _i, _i, _p, _i, _p]),
     "fpvs_wgrad_workspace_size": (_z, [_i, _i, _i, _i]),
     "fpvs_spconv_wgrad_simt": (_i, [_p, _i, _i, _p, _i, _p, _i, _p, _i, _i, _i, _p, _p, _p, _z, _p]),

@@ -142,6 +142,25 @@ __global__ void kmap_subm_kernel(const int4* __restrict__ coords, const int* __r
   }
 }
 
+// general odd kernel size k (neural.py:187-199 with k^3 taps): offset
+// j = (a*k + b)*k + c reads (x + a - p, y + b - p, z + c - p), p = k/2
+__global__ void kmap_subm_k_kernel(const int4* __restrict__ coords, const int* __restrict__ n_dev, int cap,
+                                   const int* __restrict__ index_vol, int X, int Y, int Z, int k,
+                                   int* __restrict__ nbr) {
+  const int n = min(*n_dev, cap);
+  const int K = k * k * k, pad = k / 2;
+  const long long total = (long long)n * K;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(t % K);
+    const int4 c = coords[t / K];
+    const int x = c.y + j / (k * k) - pad, y = c.z + (j / k) % k - pad, z = c.w + j % k - pad;
+    int r = -1;
+    if (x >= 0 && x < X && y >= 0 && y < Y && z >= 0 && z < Z) r = __ldg(index_vol + lin4(c.x, x, y, z, X, Y, Z));
+    nbr[t] = r;
+  }
+}
+
 __global__ void kmap_coarsen_kernel(const int4* __restrict__ coords, const int* __restrict__ n_dev, int cap,
                                     int X, int Y, int Z, uint8_t* __restrict__ coarse) {
   const int n = min(*n_dev, cap);
@@ -320,6 +339,19 @@ extern "C" int fpvs_kmap_subm(const int32_t* coords, const int32_t* n_active_dev
   kmap_subm_kernel<<<grid_for((long long)cap * 27, 256), 256, 0, as_stream(stream)>>>(
       (const int4*)coords, n_active_dev, cap, index_vol, X, Y, Z, nbr);
   FPVS_CHECK_LAUNCH("fpvs_kmap_subm");
+  return FPVS_OK;
+}
+
+extern "C" int fpvs_kmap_subm_k(const int32_t* coords, const int32_t* n_active_dev, int cap, const int32_t* index_vol,
+                                int B, int X, int Y, int Z, int k, int32_t* nbr, void* stream) {
+  FPVS_CHECK_ARG(coords && n_active_dev && index_vol && nbr, "null pointer");
+  FPVS_CHECK_ARG(k >= 1 && k % 2 == 1 && k <= 15, "kernel size must be odd (1..15), got %d", k);
+  (void)B;
+  if (cap <= 0) return FPVS_OK;
+  const long long K = (long long)k * k * k;
+  kmap_subm_k_kernel<<<grid_for((long long)cap * K, 256), 256, 0, as_stream(stream)>>>(
+      (const int4*)coords, n_active_dev, cap, index_vol, X, Y, Z, k, nbr);
+  FPVS_CHECK_LAUNCH("fpvs_kmap_subm_k");
   return FPVS_OK;
 }
 

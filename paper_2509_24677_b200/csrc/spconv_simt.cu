@@ -270,6 +270,48 @@ __global__ void head_simt_kernel(const Tin* __restrict__ x, int ldx, const int4*
   }
 }
 
+// Head epilogue over precomputed logits rows (a head layer with k > 1 runs as
+// an ordinary conv with no activation first): sigmoid + [p >= tau] +
+// packed-bit scatter, probabilities optional (neural.py:513-526, 151-157).
+__global__ void head_rows_kernel(const float* __restrict__ logits, int ld, const int4* __restrict__ coords,
+                                 const int* __restrict__ n_dev, int cap, int d, int Nx, int Ny, int Nz, float tau,
+                                 uint8_t* __restrict__ out_bits, float* __restrict__ probs) {
+  const int d3 = d * d * d;
+  const int n = min(*n_dev, cap);
+  const long long total = (long long)n * d3;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(t % d3);
+    const long long i = t / d3;
+    const float p = sigmoidf_stable(logits[i * ld + k]);
+    if (probs) probs[t] = p;
+    if (p >= tau && out_bits) {
+      const int4 c = coords[i];
+      const int lx = k % d, ly = (k / d) % d, lz = k / (d * d);
+      const int fx = c.y * d + lx;
+      atomic_or_bit(out_bits, bit_byte(c.x, fx, c.z * d + ly, c.w * d + lz, Nx, Ny, Nz), fx & 7);
+    }
+  }
+}
+
+// dz = dy * act'(.) from the layer's kept output y (neural.py:225-232):
+// relu z > 0 <=> y > 0, sigmoid y (1 - y), none 1
+template <typename Ty>
+__global__ void act_backward_kernel(const float* __restrict__ dy, int lddy, const Ty* __restrict__ y, int ldy,
+                                    const int* __restrict__ n_dev, int cap, int C, int act, float* __restrict__ dz,
+                                    int lddz) {
+  const int n = min(*n_dev, cap);
+  const long long total = (long long)n * C;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / C;
+    const int c = (int)(t % C);
+    const float g = dy[i * lddy + c];
+    const float v = to_f32<Ty>(y[i * ldy + c]);
+    dz[i * lddz + c] = act == FPVS_ACT_RELU ? (v > 0.f ? g : 0.f) : act == FPVS_ACT_SIGMOID ? g * v * (1.f - v) : g;
+  }
+}
+
 // ---- wgrad: deterministic split over rows, fixed-order reduction ---------
 constexpr int kWgSplits = 64;
 constexpr int kWgRows = 32;
@@ -660,7 +702,10 @@ extern "C" int fpvs_spconv_dgrad_simt(const float* dz, int lddz, const int32_t* 
                                       int cap, const float* w, int cin, int cout, const void* ymask, int mask_dtype,
                                       int ldm, float* dx, int lddx, void* stream) {
   FPVS_CHECK_ARG(dz && w && dx && n_dev, "null pointer");
-  FPVS_CHECK_ARG(K == 27 || K == 1, "dgrad supports the symmetric subm map (K=27) and 1x1x1 (K=1)");
+  // the mirrored gather needs a symmetric map: K = k^3 submanifold taps, k odd
+  int kk = 1;
+  while (kk * kk * kk < K) kk += 2;
+  FPVS_CHECK_ARG(kk * kk * kk == K, "dgrad supports symmetric subm maps (K = k^3, k odd), got K = %d", K);
   FPVS_CHECK_ARG(nbr || K == 1, "nbr may be NULL only for K == 1");
   if (cap <= 0) return FPVS_OK;
   // effective conv: input dz (Cin_eff = cout), output dx (Cout_eff = cin)
@@ -745,5 +790,38 @@ extern "C" int fpvs_first_hit_labels(const uint8_t* bits, int B, int Nx, int Ny,
   first_hit_kernel<<<grid_for((long long)B * Nz * Ny * (Nx / 8), 256), 256, 0, s>>>(bits, B, Nx, Ny, Nz, radius,
                                                                                      zfirst_ws, out_bits);
   FPVS_CHECK_LAUNCH("fpvs_first_hit_labels");
+  return FPVS_OK;
+}
+
+extern "C" int fpvs_head_rows(const float* logits, int ld, const int32_t* coords, const int32_t* n_dev, int cap, int d,
+                              int B, int Nx, int Ny, int Nz, float tau, uint8_t* out_bits, float* probs,
+                              void* stream) {
+  FPVS_CHECK_ARG(logits && coords && n_dev, "null pointer");
+  FPVS_CHECK_ARG(Nx % 8 == 0, "N_x must be divisible by 8");
+  FPVS_CHECK_ARG(d >= 1 && ld >= d * d * d, "bad logits leading dimension");
+  (void)B;
+  if (cap <= 0) return FPVS_OK;
+  const int d3 = d * d * d;
+  head_rows_kernel<<<grid_for((long long)cap * d3, 256), 256, 0, as_stream(stream)>>>(
+      logits, ld, (const int4*)coords, n_dev, cap, d, Nx, Ny, Nz, tau, out_bits, probs);
+  FPVS_CHECK_LAUNCH("fpvs_head_rows");
+  return FPVS_OK;
+}
+
+extern "C" int fpvs_act_backward(const float* dy, int lddy, const void* y, int y_dtype, int ldy, const int32_t* n_dev,
+                                 int cap, int C, int act, float* dz, int lddz, void* stream) {
+  FPVS_CHECK_ARG(dy && y && dz && n_dev, "null pointer");
+  FPVS_CHECK_ARG(C >= 1 && lddy >= C && ldy >= C && lddz >= C, "bad leading dimension");
+  FPVS_CHECK_ARG(act == FPVS_ACT_NONE || act == FPVS_ACT_RELU || act == FPVS_ACT_SIGMOID, "bad activation");
+  FPVS_CHECK_ARG(y_dtype == FPVS_F32 || y_dtype == FPVS_BF16, "bad y dtype");
+  if (cap <= 0) return FPVS_OK;
+  const int g = grid_for((long long)cap * C, 256);
+  cudaStream_t s = as_stream(stream);
+  if (y_dtype == FPVS_F32)
+    act_backward_kernel<float><<<g, 256, 0, s>>>(dy, lddy, (const float*)y, ldy, n_dev, cap, C, act, dz, lddz);
+  else
+    act_backward_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(dy, lddy, (const __nv_bfloat16*)y, ldy, n_dev, cap, C, act,
+                                                         dz, lddz);
+  FPVS_CHECK_LAUNCH("fpvs_act_backward");
   return FPVS_OK;
 }

@@ -94,17 +94,18 @@ class ModelConfig:
             for spec in self.layers:
                 if spec.out_channels < want and spec is not self.layers[-1]:
                     raise ValueError("identity init needs >= d^3 channels per hidden layer")
-        for spec in self.layers:
-            if spec.kernel not in (1, 3):
-                raise ValueError("the sparse kernels support kernel sizes 1 and 3")
-        if last.kernel != 1:
-            raise ValueError("the fused head needs a 1x1x1 final layer")
+        # any odd kernel (ConvSpec) and any head kernel run on the device: k = 3
+        # on the tensor-core / halo kernels, other k on the SIMT gather-GEMM over
+        # a k^3-tap map (fpvs_kmap_subm_k); a 1x1x1 head is fused with the
+        # threshold and bit-pack, a wider head runs as a conv + fpvs_head_rows
 
     @classmethod
     def default(cls, d: int = 4, hidden: int = 32, init: str = "he") -> "ModelConfig":
+        """The reference's default estimator (neural.py:94-99): two 3^3 ReLU
+        convs and a 3^3 sigmoid head."""
         c = d ** 3
         return cls(d, [ConvSpec(3, c, hidden, "relu"), ConvSpec(3, hidden, hidden, "relu"),
-                       ConvSpec(1, hidden, c, "sigmoid")], init)
+                       ConvSpec(3, hidden, c, "sigmoid")], init)
 
     @classmethod
     def config1(cls, init: str = "kaiming_uniform") -> "ModelConfig":
@@ -225,6 +226,150 @@ class Conv3d:
     def packed(self, bn: int = 0, stream=None):
         return packed_cache(self, bn, stream)
 
+    # -- reference-shaped dense API (neural.py:201-249) ----------------------
+    def forward(self, x, keep_cache: bool = False, level: sp.Level | None = None):
+        """(B, D, H, W, Cin) -> activation output (B, D, H, W, Cout); with
+        ``keep_cache`` also the backward cache (neural.py:201-219).
+
+        Submanifold: outputs exist on the active cells — those with any nonzero
+        input channel, or the cells of ``level`` when a network passes its
+        level-0 set along — and read 0 elsewhere.  fp32 on the device (SIMT
+        FFMA); numpy in -> float64 numpy out, CUDA tensors stay on the device.
+        """
+        torch = _torch()
+        host = not isinstance(x, torch.Tensor)
+        xt = _dense_in(x, self.spec.in_channels)
+        lv = level if level is not None else dense_level(xt)
+        x_rows = dense_to_rows(xt, lv)
+        y_rows = self.forward_rows_f32(x_rows, lv)
+        y = rows_to_dense(y_rows, lv, self.spec.out_channels)
+        out = y.cpu().numpy().astype(np.float64) if host else y
+        if not keep_cache:
+            return out
+        return out, Conv3dCache(lv, x_rows, y_rows, tuple(xt.shape), host)
+
+    def forward_rows_f32(self, x_rows, lv: sp.Level, stream=None):
+        """fp32 rows in -> fp32 activation rows out on level ``lv``."""
+        torch = _torch()
+        build_layer_tables(lv, [self.spec.kernel], stream)
+        table, K, _ = layer_table(lv, self.spec.kernel)
+        y_rows = torch.zeros((lv.cap, self.spec.out_channels), dtype=torch.float32, device=x_rows.device)
+        run_conv(self, x_rows, x_rows.shape[1], table, K, lv.n, lv.cap, y_rows, y_rows.shape[1], 0, "fp32",
+                 stream=stream)
+        return y_rows
+
+    def backward(self, dy, cache):
+        """Gradients (dx, dw, db) of the scalar loss (neural.py:221-249) on the
+        cached active set: relu' = z > 0, sigmoid' = y (1 - y); dw in the
+        reference's (k^3 Cin, Cout) row order."""
+        if cache is None:
+            raise ValueError("backward requires the forward cache")
+        torch = _torch()
+        host = not isinstance(dy, torch.Tensor)
+        dyt = _dense_in(dy, self.spec.out_channels)
+        if tuple(dyt.shape[:4]) != tuple(cache.shape[:4]):
+            raise ValueError(f"gradient shape {tuple(dyt.shape)} does not match the cached output")
+        dx_rows, dw, db = self.backward_rows(dense_to_rows(dyt, cache.level), cache)
+        dx = rows_to_dense(dx_rows, cache.level, self.spec.in_channels)
+        if host:
+            return (dx.cpu().numpy().astype(np.float64), dw.cpu().numpy().astype(np.float64),
+                    db.cpu().numpy().astype(np.float64))
+        return dx, dw, db
+
+    def backward_rows(self, dy_rows, cache, need_dx: bool = True, stream=None):
+        """Rows form of :meth:`backward`: fpvs_act_backward, fpvs_spconv_wgrad_simt
+        (deterministic) and fpvs_spconv_dgrad_simt (mirrored offsets)."""
+        torch = _torch()
+        lv, spec = cache.level, self.spec
+        s = _lib.stream_ptr(stream)
+        table, K, _ = layer_table(lv, spec.kernel)
+        cin, cout = spec.in_channels, spec.out_channels
+        dev = dy_rows.device
+        dz = torch.zeros((lv.cap, cout), dtype=torch.float32, device=dev)
+        _lib.call("fpvs_act_backward", _lib.ptr(dy_rows.contiguous()), dy_rows.shape[1], _lib.ptr(cache.y_rows),
+                  _lib.F32, cache.y_rows.shape[1], _lib.ptr(lv.n), lv.cap, cout, _lib.ACT[spec.activation], _lib.ptr(dz),
+                  cout, s)
+        dw = torch.zeros((K * cin, cout), dtype=torch.float32, device=dev)
+        db = torch.zeros(cout, dtype=torch.float32, device=dev)
+        ws = torch.empty(_lib.size("fpvs_wgrad_workspace_size", K, cin, cout, lv.cap), dtype=torch.uint8, device=dev)
+        _lib.call("fpvs_spconv_wgrad_simt", _lib.ptr(cache.x_rows), cache.x_rows.shape[1], _lib.F32, _lib.ptr(dz), cout,
+                  _lib.ptr(table), K, _lib.ptr(lv.n), lv.cap, cin, cout, _lib.ptr(dw), _lib.ptr(db), _lib.ptr(ws),
+                  ws.numel(), s)
+        dx = None
+        if need_dx:
+            dx = torch.zeros((lv.cap, cin), dtype=torch.float32, device=dev)
+            _lib.call("fpvs_spconv_dgrad_simt", _lib.ptr(dz), cout, _lib.ptr(table), K, _lib.ptr(lv.n), lv.cap,
+                      _lib.ptr(self.w.contiguous()), cin, cout, None, _lib.F32, 0, _lib.ptr(dx), cin, s)
+        return dx, dw, db
+
+
+@dataclass
+class Conv3dCache:
+    """What Conv3d.backward needs (the reference keeps (cols, z, y, shape),
+    neural.py:219): the active set, the input rows and the output rows."""
+    level: object
+    x_rows: object
+    y_rows: object
+    shape: tuple
+    host: bool
+
+
+def conv3d_forward(x, layer: Conv3d):
+    """neural.py:252-253."""
+    return layer.forward(x)
+
+
+def conv3d_backward(layer: Conv3d, dy, cache):
+    """neural.py:256-257."""
+    return layer.backward(dy, cache)
+
+
+def _dense_in(x, channels: int):
+    """(B, X, Y, Z, C) numpy / tensor -> contiguous f32 CUDA tensor, shape-checked as neural.py:203-205."""
+    torch = _torch()
+    xt = x.to("cuda", torch.float32) if isinstance(x, torch.Tensor) else \
+        torch.as_tensor(np.asarray(x, dtype=np.float32)).cuda()
+    if xt.dim() != 5 or xt.shape[4] != channels:
+        raise ValueError(f"expected (B, D, H, W, {channels}) input, got {tuple(xt.shape)}")
+    return xt.contiguous()
+
+
+def dense_level(xt) -> sp.Level:
+    """Level of a dense (B, X, Y, Z, C) tensor: active = any nonzero channel, C-order rows, 3^3 map."""
+    torch = _torch()
+    B, X, Y, Z, _ = xt.shape
+    lv = sp.new_level(B, (X, Y, Z))
+    lv.active.copy_((xt != 0).any(-1).reshape(-1).to(torch.uint8))
+    sp.compact(lv)
+    sp.build_subm(lv)
+    return lv
+
+
+def _row_index(lv: sp.Level):
+    c = lv.coords[:lv.count()].long()
+    X, Y, Z = lv.dims
+    return ((c[:, 0] * X + c[:, 1]) * Y + c[:, 2]) * Z + c[:, 3]
+
+
+def dense_to_rows(xt, lv: sp.Level):
+    """Active rows (cap, C) f32 of a dense (B, X, Y, Z, C) tensor (zero past the count)."""
+    torch = _torch()
+    C = xt.shape[-1]
+    rows = torch.zeros((lv.cap, C), dtype=torch.float32, device=xt.device)
+    idx = _row_index(lv)
+    rows[:len(idx)] = xt.reshape(-1, C)[idx].to(torch.float32)
+    return rows
+
+
+def rows_to_dense(rows, lv: sp.Level, C: int):
+    """Scatter active rows back to a dense (B, X, Y, Z, C) f32 tensor (0 at inactive cells)."""
+    torch = _torch()
+    X, Y, Z = lv.dims
+    out = torch.zeros((lv.B * X * Y * Z, C), dtype=torch.float32, device=rows.device)
+    idx = _row_index(lv)
+    out[idx] = rows[:len(idx), :C].to(torch.float32)
+    return out.reshape(lv.B, X, Y, Z, C)
+
 
 def packed_cache(layer, bn: int = 0, stream=None):
     """The layer's bf16 weight image for tile width ``bn`` (built once per bn)."""
@@ -275,6 +420,43 @@ def pick_bn(cout: int, rows: int, sms: int = 148) -> int:
     return bn
 
 
+def layer_table(lv: sp.Level, k: int):
+    """(table, K, tile masks) a kernel-k submanifold conv reads on level ``lv``.
+
+    k = 3 is the level's own table; other odd k get a k^3-tap table in
+    ``lv.extra`` that :func:`build_layer_tables` (re)fills after every map build.
+    """
+    if k == 1:
+        return None, 1, None
+    if k == 3:
+        return lv.nbr, 27, lv.nbr_masks
+    key = ("nbr", k)
+    t = lv.extra.get(key)
+    if t is None:
+        torch = _torch()
+        t = torch.empty((lv.cap, k ** 3), dtype=torch.int32, device=lv.coords.device)
+        lv.extra[key] = t
+    return t, k ** 3, None
+
+
+def build_layer_tables(lv: sp.Level, kernels, stream=None):
+    """Fill the k^3-tap tables (k not in {1, 3}) of ``kernels`` from the level's
+    coordinates and index volume (one fpvs_kmap_subm_k launch per distinct k)."""
+    X, Y, Z = lv.dims
+    for k in sorted(set(kernels)):
+        if k in (1, 3):
+            continue
+        t, _, _ = layer_table(lv, k)
+        _lib.call("fpvs_kmap_subm_k", _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap, _lib.ptr(lv.index_vol), lv.B, X, Y,
+                  Z, k, _lib.ptr(t), _lib.stream_ptr(stream))
+
+
+def tc_ok(K: int, cin: int, cout: int, act: str = "relu") -> bool:
+    """Shapes the tcgen05 gather-GEMM (fpvs_spconv_tc) takes; others run on the
+    SIMT kernel with bf16 operands."""
+    return K <= 27 and cin % 8 == 0 and cout % 32 == 0 and cout <= 1024 and act in ("relu", "none")
+
+
 def halo_ok(K: int, cin: int, cout: int, dtype=None) -> bool:
     """Shapes the halo-cached tensor-core conv (fpvs_spconv_halo) takes."""
     return K == 27 and (cin % 64 == 0 or cin == 32) and cout % 32 == 0 and cout <= 1024
@@ -296,6 +478,9 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
     spec = layer.spec
     a = _lib.ACT[act or spec.activation]
     s = _lib.stream_ptr(stream)
+    if precision == "bf16" and out_rows is None and not tc_ok(K, spec.in_channels, spec.out_channels,
+                                                              act or spec.activation):
+        precision = "simt"  # e.g. k = 5 (125 taps): SIMT FFMA on the bf16 rows
     if precision == "bf16":
         if table is not None and masks is None:
             masks = sp.tile_masks(table, K, n, cap, stream=stream)
@@ -325,11 +510,31 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
 
 def run_head(layer: Conv3d, x, ldx: int, lv: sp.Level, d: int, grid_dims, tau: float, out_bits=None,
              probs=None, logits=None, precision: str = "fp32", stream=None):
-    """Fused 1x1x1 conv + sigmoid + [p >= tau] + deinterleave bit-pack (neural.py:513-526)."""
+    """Head + sigmoid + [p >= tau] + deinterleave bit-pack (neural.py:513-526).
+
+    A 1x1x1 head is one fused kernel; a k^3 head (the reference default,
+    neural.py:94-99) runs as a conv with no activation into f32 logits rows
+    (SIMT, exact fp32 accumulation) followed by fpvs_head_rows."""
     torch = _torch()
     nx, ny, nz = grid_dims
     s = _lib.stream_ptr(stream)
     spec = layer.spec
+    if spec.kernel != 1:
+        d3 = d ** 3
+        table, K, _ = layer_table(lv, spec.kernel)
+        lg = logits
+        if lg is None:
+            lg = lv.extra.get("head_logits")
+            if lg is None or lg.shape[1] != d3:
+                lg = torch.empty((lv.cap, d3), dtype=torch.float32, device=x.device)
+                lv.extra["head_logits"] = lg
+        idt = _lib.BF16 if x.dtype == torch.bfloat16 else _lib.F32
+        _lib.call("fpvs_spconv_simt", _lib.ptr(x), ldx, idt, _lib.ptr(table), K, _lib.ptr(lv.n), lv.cap,
+                  _lib.ptr(layer.w), _lib.ptr(layer.b), spec.in_channels, d3, _lib.ACT["none"], _lib.ptr(lg),
+                  lg.shape[1], 0, _lib.F32, s)
+        _lib.call("fpvs_head_rows", _lib.ptr(lg), lg.shape[1], _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap, d, lv.B,
+                  nx, ny, nz, float(tau), _lib.ptr(out_bits), _lib.ptr(probs), s)
+        return
     if precision == "bf16":
         _lib.call("fpvs_head_tc", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(lv.coords), _lib.ptr(lv.n), lv.cap,
                   _lib.ptr(layer.packed(0, stream)), _lib.ptr(layer.b), spec.in_channels, d, lv.B, nx, ny, nz,
@@ -365,6 +570,9 @@ class PvsNet:
             self.layers[-1].b.fill_(-self.OUTPUT_GAIN / 2.0)
 
     # -- device path ---------------------------------------------------------
+    def kernels(self):
+        return [L.spec.kernel for L in self.layers]
+
     def forward_rows(self, feats, lv: sp.Level, grid_dims, tau: float = 0.5, out_bits=None, probs=None,
                      logits=None, keep: bool = False, stream=None):
         """Run the chain on active-cell rows; the head writes bits / probs / logits.
@@ -375,13 +583,14 @@ class PvsNet:
         d = self.cfg.d
         bf16 = self.precision == "bf16"
         dt = torch.bfloat16 if bf16 else torch.float32
+        build_layer_tables(lv, self.kernels(), stream)
         x = feats
         acts = [x]
         for layer in self.layers[:-1]:
             y = torch.empty((lv.cap, layer.spec.out_channels), dtype=dt, device=x.device)
-            table, K = (lv.nbr, 27) if layer.spec.kernel == 3 else (None, 1)
+            table, K, masks = layer_table(lv, layer.spec.kernel)
             run_conv(layer, x, x.shape[1], table, K, lv.n, lv.cap, y, y.shape[1], 0, self.precision, stream=stream,
-                     masks=lv.nbr_masks if table is not None else None)
+                     masks=masks)
             x = y
             acts.append(x)
         run_head(self.layers[-1], x, x.shape[1], lv, d, grid_dims, tau, out_bits, probs, logits,
@@ -400,35 +609,69 @@ class PvsNet:
         self.forward_rows(feats, lv, grid_dims, tau, out_bits=out, stream=stream)
         return out
 
-    # -- reference-shaped dense API ------------------------------------------
+    # -- reference-shaped dense API (neural.py:260-297) ------------------------
+    def _dense_level(self, x):
+        xt = _dense_in(x, self.cfg.layers[0].in_channels)
+        return xt, dense_level(xt)
+
     def forward(self, x):
         """(B, X, Y, Z, d^3) -> probabilities of the same shape; inactive cells -> 0."""
         torch = _torch()
         host = not isinstance(x, torch.Tensor)
-        xt = torch.as_tensor(np.asarray(x), dtype=torch.float32).cuda() if host else x.to("cuda", torch.float32)
-        if xt.dim() != 5 or xt.shape[4] != self.cfg.layers[0].in_channels:
-            raise ValueError(f"expected (B, D, H, W, {self.cfg.layers[0].in_channels}) input, got {tuple(xt.shape)}")
+        xt, lv = self._dense_level(x)
         B, X, Y, Z, C = xt.shape
-        lv = sp.new_level(B, (X, Y, Z))
-        lv.active.copy_((xt != 0).any(-1).reshape(-1).to(torch.uint8))
-        sp.compact(lv)
-        sp.build_subm(lv)
-        n = lv.count()
-        rows = xt.reshape(-1, C)[lv.coords[:n, 0].long() * (X * Y * Z) + (lv.coords[:n, 1].long() * Y
-                                 + lv.coords[:n, 2].long()) * Z + lv.coords[:n, 3].long()]
-        feats = torch.zeros((lv.cap, C), dtype=torch.bfloat16 if self.precision == "bf16" else torch.float32,
-                            device="cuda")
-        feats[:n] = rows.to(feats.dtype)
+        feats = dense_to_rows(xt, lv)
+        if self.precision == "bf16":
+            feats = feats.to(torch.bfloat16)
         d3 = self.cfg.layers[-1].out_channels
         probs = torch.zeros((lv.cap, d3), dtype=torch.float32, device="cuda")
         grid_dims = (X * self.cfg.d, Y * self.cfg.d, Z * self.cfg.d)
         self.forward_rows(feats, lv, grid_dims, 0.5, probs=probs)
-        out = torch.zeros((B * X * Y * Z, d3), dtype=torch.float32, device="cuda")
-        lin = ((lv.coords[:n, 0].long() * X + lv.coords[:n, 1].long()) * Y + lv.coords[:n, 2].long()) * Z \
-            + lv.coords[:n, 3].long()
-        out[lin] = probs[:n]
-        out = out.reshape(B, X, Y, Z, d3)
+        out = rows_to_dense(probs, lv, d3)
         return out.cpu().numpy().astype(np.float64) if host else out
+
+    def forward_cached(self, x):
+        """(probabilities, per-layer caches) as neural.py:263-268; fp32 on the device."""
+        torch = _torch()
+        host = not isinstance(x, torch.Tensor)
+        xt, lv = self._dense_level(x)
+        rows = dense_to_rows(xt, lv)
+        caches = []
+        for layer in self.layers:
+            y_rows = layer.forward_rows_f32(rows, lv)
+            caches.append(Conv3dCache(lv, rows, y_rows, tuple(xt.shape[:4]) + (layer.spec.out_channels,), host))
+            rows = y_rows
+        out = rows_to_dense(rows, lv, self.layers[-1].spec.out_channels)
+        return (out.cpu().numpy().astype(np.float64) if host else out), caches
+
+    def backward(self, dy, caches):
+        """Per-layer (dw, db) gradients plus the input gradient (neural.py:270-276)."""
+        torch = _torch()
+        if not caches:
+            raise ValueError("backward requires the forward caches")
+        host = not isinstance(dy, torch.Tensor)
+        lv = caches[-1].level
+        g = dense_to_rows(_dense_in(dy, self.layers[-1].spec.out_channels), lv)
+        grads = [None] * len(self.layers)
+        for i in reversed(range(len(self.layers))):
+            g, dw, db = self.layers[i].backward_rows(g, caches[i])
+            grads[i] = (dw, db)
+        dx = rows_to_dense(g, lv, self.layers[0].spec.in_channels)
+        if host:
+            grads = [(dw.cpu().numpy().astype(np.float64), db.cpu().numpy().astype(np.float64)) for dw, db in grads]
+            dx = dx.cpu().numpy().astype(np.float64)
+        return grads, dx
+
+    def sgd_step(self, grads, lr: float):
+        """w -= lr dw, b -= lr db per layer (neural.py:278-281), fpvs_sgd_step on the device."""
+        torch = _torch()
+        for layer, (dw, db) in zip(self.layers, grads):
+            for param, grad in ((layer.w, dw), (layer.b, db)):
+                gt = torch.as_tensor(grad if isinstance(grad, torch.Tensor) else np.asarray(grad, dtype=np.float32),
+                                     dtype=torch.float32).to(param.device).reshape(param.shape).contiguous()
+                _lib.call("fpvs_sgd_step", _lib.ptr(param), _lib.ptr(gt), param.numel(), float(lr),
+                          _lib.stream_ptr())
+            layer.invalidate()
 
     def parameters(self):
         out = []
@@ -571,9 +814,44 @@ def train(pairs, mcfg: ModelConfig, tcfg: TrainConfig, eval_pairs=None, target_f
                   precision)
 
 
-def evaluate_pairs(net: PvsNet, pairs, tau: float):
-    """Hard FNR/FPR over (geometry, gt) pairs (neural.py:423-434)."""
-    from .train import evaluate_pairs as _ev
+def _tensor_pairs(pairs, d: int):
+    """Stacked interleaved (geometry, gt) tensors of FroxelGrid pairs (neural.py:415-420), float64 numpy."""
+    from .interleave import interleave
+    xs, ys = [], []
+    for geo, gt in pairs:
+        xs.append(interleave(geo, d).values)
+        ys.append(interleave(gt, d).values)
+    return np.stack(xs), np.stack(ys)
+
+
+def _epoch_rates(tp, fp, fn, gtp):
+    """(FNR, FPR) = (FN / GTP, FP / GTP), (0, 0) without positives (neural.py:423-426)."""
+    if gtp == 0:
+        return 0.0, 0.0
+    return fn / gtp, fp / gtp
+
+
+def evaluate_pairs(net: PvsNet, x, y, tau: float, batch: int = 8):
+    """Hard FNR/FPR of thresholded predictions over a stacked pair set
+    (neural.py:429-439): pred = p >= tau over every cell (inactive cells have
+    p = 0), gt = y > 0.5; counted on the device, ``batch`` samples per pass."""
+    torch = _torch()
+    n = len(x)
+    tot = torch.zeros(4, dtype=torch.int64, device="cuda")
+    for i in range(0, n, batch):
+        xs = x[i:i + batch]
+        probs = net.forward(xs if isinstance(xs, torch.Tensor) else torch.as_tensor(np.asarray(xs, np.float32)).cuda())
+        ys = y[i:i + batch]
+        gt = (ys.cuda() if isinstance(ys, torch.Tensor) else torch.as_tensor(np.asarray(ys, np.float32)).cuda()) > 0.5
+        pred = probs >= tau
+        tot += torch.stack([(pred & gt).sum(), (pred & ~gt).sum(), (~pred & gt).sum(), gt.sum()])
+    tp, fp, fn, gtp = (int(v) for v in tot.cpu())
+    return _epoch_rates(tp, fp, fn, gtp)
+
+
+def evaluate_grid_pairs(net: PvsNet, pairs, tau: float):
+    """Hard FNR/FPR over (geometry, gt) FroxelGrid pairs on packed bits (fpvs_bits_confusion)."""
+    from .train import evaluate_grid_pairs as _ev
     return _ev(net, pairs, tau)
 
 

@@ -16,7 +16,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import sparse as sp
-from .neural import PvsNet, run_conv, run_head
+from .neural import PvsNet, build_layer_tables, layer_table, run_conv, run_head
 
 
 def _torch():
@@ -73,20 +73,24 @@ class ChainPlan:
         """Ordered (name, idempotent launch function) list of one frame."""
         net, lv = self.net, self.L0
         d = net.cfg.d
+        kernels = net.kernels()
+
+        def tables():
+            build_layer_tables(lv, kernels)  # k^3 maps of k not in {1, 3} (none for configs 1-5)
         if self.maps is not None:
             # maps + sparse interleave + clearing the output grid in one fused build
-            out = [("maps", lambda: self.maps.run(bits, self.x0, d ** 3, out_bits))]
+            out = [("maps", lambda: (self.maps.run(bits, self.x0, d ** 3, out_bits), tables()))]
         else:
-            out = [("maps", lambda: sp.fill_level_from_bits(lv, bits, self.grid_dims, d)),
+            out = [("maps", lambda: (sp.fill_level_from_bits(lv, bits, self.grid_dims, d), tables())),
                    ("gather", lambda: sp.gather_features(bits, lv, self.grid_dims, d, self.x0.dtype, out=self.x0))]
         x, ldx = self.x0, d ** 3
         bufs = (self.ping, self.pong)
         for i, layer in enumerate(net.layers[:-1]):
             y = bufs[i % 2]
-            table, K = (lv.nbr, 27) if layer.spec.kernel == 3 else (None, 1)
-            out.append((f"conv{i}", lambda layer=layer, x=x, ldx=ldx, table=table, K=K, y=y:
+            table, K, masks = layer_table(lv, layer.spec.kernel)
+            out.append((f"conv{i}", lambda layer=layer, x=x, ldx=ldx, table=table, K=K, y=y, masks=masks:
                         run_conv(layer, x, ldx, table, K, lv.n, lv.cap, y, y.shape[1], 0, net.precision,
-                                 masks=lv.nbr_masks if table is not None else None)))
+                                 masks=masks)))
             x, ldx = y, y.shape[1]
 
         def head(x=x, ldx=ldx):

@@ -44,7 +44,8 @@ import numpy as np
 from . import _lib
 from . import sparse as sp
 from .froxel import FroxelGrid
-from .neural import ModelConfig, PvsNet, TrainConfig, TrainingDiverged, packed_dgrad_cache, run_conv, run_head
+from .neural import (ModelConfig, PvsNet, TrainConfig, TrainingDiverged, build_layer_tables, layer_table,
+                     packed_dgrad_cache, run_conv, run_head)
 
 
 def _torch():
@@ -160,11 +161,12 @@ class TrainStep:
         nx, ny, nz = self.grid_dims
         s = _lib.stream_ptr(stream)
         self.maps.run(bits, feat=self.x0, clear=self.pred_bits, stream=stream)
+        build_layer_tables(lv, net.kernels(), stream)
         x = self.x0
         for layer, y in zip(net.layers[:-1], self.acts):
-            table, K = (lv.nbr, 27) if layer.spec.kernel == 3 else (None, 1)
+            table, K, masks = layer_table(lv, layer.spec.kernel)
             run_conv(layer, x, x.shape[1], table, K, lv.n, lv.cap, y, y.shape[1], 0, net.precision, stream=stream,
-                     masks=lv.nbr_masks if table is not None else None)
+                     masks=masks)
             x = y
         run_head(net.layers[-1], x, x.shape[1], lv, d, self.grid_dims, tc.tau, self.pred_bits, self.probs, None,
                  net.precision, stream)
@@ -184,9 +186,12 @@ class TrainStep:
         return s.kernel == 3 and s.in_channels == 32 and s.out_channels % 8 == 0 and s.out_channels <= 32
 
     def _tc_backward_ok(self) -> bool:
+        # tcgen05 dgrad / wgrad cover 1^3 and 3^3 layers and the fused 1^3 head;
+        # other kernel sizes (and a k^3 head) keep the SIMT backward
         layers = self.net.layers
         return (all(L.spec.in_channels % 8 == 0 and L.spec.out_channels % 8 == 0 and L.spec.out_channels <= 256
-                    for L in layers)
+                    and L.spec.kernel in (1, 3) for L in layers)
+                and layers[-1].spec.kernel == 1
                 and all(L.spec.in_channels % 32 == 0 for L in layers[1:]))
 
     def backward(self, stream=None):
@@ -200,7 +205,7 @@ class TrainStep:
             layer = net.layers[li]
             spec = layer.spec
             x = ins[li]
-            table, K = (lv.nbr, 27) if spec.kernel == 3 else (None, 1)
+            table, K, _ = layer_table(lv, spec.kernel)
             dw, db = self.views[li]
             xdt = _lib.F32 if x.dtype == self.dx[0].dtype else _lib.BF16
             _lib.call("fpvs_spconv_wgrad_simt", _lib.ptr(x), x.shape[1], xdt, _lib.ptr(dz), lddz, _lib.ptr(table), K,
@@ -331,8 +336,9 @@ def _rates(tp, fp, fn, gtp):
     return fn / gtp, fp / gtp
 
 
-def evaluate_pairs(net: PvsNet, pairs, tau: float, batch: int = 8):
-    """Hard FNR/FPR of thresholded predictions over (geometry, gt) pairs (neural.py:423-434)."""
+def evaluate_grid_pairs(net: PvsNet, pairs, tau: float, batch: int = 8):
+    """Hard FNR/FPR of thresholded predictions over (geometry, gt) FroxelGrid
+    pairs (the rates of neural.py:423-439), predicted and counted on packed bits."""
     torch = _torch()
     if not pairs:
         return 0.0, 0.0
@@ -418,7 +424,7 @@ def train(pairs, mcfg: ModelConfig, tcfg: TrainConfig, eval_pairs=None, target_f
         fnr, fpr = _rates(*[int(v) for v in tot])
         entry = {"epoch": epoch, "loss": epoch_loss / max(n, 1), "fnr": fnr, "fpr": fpr}
         if eval_pairs:
-            entry["val_fnr"], entry["val_fpr"] = evaluate_pairs(net, eval_pairs, tcfg.tau)
+            entry["val_fnr"], entry["val_fpr"] = evaluate_grid_pairs(net, eval_pairs, tcfg.tau)
         history.append(entry)
         if verbose and rank == 0:
             print("  ".join(f"{k}={v:.5g}" if isinstance(v, float) else f"{k}={v}" for k, v in entry.items()))

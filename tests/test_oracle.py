@@ -342,3 +342,49 @@ def test_gtpvs_occluder_hides_everything_behind(golden):
     i = next(i for i in range(int(g["ncases"])) if str(g[f"c{i}_name"]) == "occluder")
     dense = FroxelGrid((16, 16, 16), bits=g[f"c{i}_bits"]).to_dense()
     assert dense[:, :, :9].sum() > 0 and dense[:, :, 9:].sum() == 0
+
+
+# ------------------------------------------- any odd kernel, 3^3 head (api.npz)
+
+def _api_layers(g, tag, specs):
+    return [(k, g[f"{tag}_w{i}"], g[f"{tag}_b{i}"], act) for i, (k, act) in enumerate(specs)]
+
+
+API_SPECS = {"def": [(3, "relu"), (3, "relu"), (3, "sigmoid")], "k5": [(5, "relu"), (3, "sigmoid")]}
+
+
+@pytest.mark.parametrize("tag", ["def", "k5"])
+def test_oracle_general_kernels_match_masked_reference(golden, tag):
+    """The oracle's k^3 maps and chain (forward, backward) against the reference's
+    own Conv3d on the reference default net (3^3 head) and a 5^3 layer."""
+    g = golden("api.npz")
+    x, mask = g["x"], g["mask"]
+    coords, rows = _sparse_from_dense(x, mask)
+    layers = _api_layers(g, tag, API_SPECS[tag])
+    c, prob = osp.chain_forward(x, layers)
+    assert np.array_equal(c, coords)
+    np.testing.assert_allclose(prob, g[f"{tag}_y{len(layers) - 1}"][tuple(coords.T)], rtol=0, atol=1e-12)
+    dims = mask.shape[1:]
+    tables = {k: osp.kmap_subm(coords, dims, k) for k in (3, 5)}
+    _, caches = osp.chain_forward_cached(rows, tables[3], layers, tables)
+    grads, dx = osp.chain_backward(g[f"{tag}_dy"][tuple(coords.T)], layers, caches)
+    for i, (dw, db) in enumerate(grads):
+        np.testing.assert_allclose(dw, g[f"{tag}_dw{i}"], rtol=1e-10, atol=1e-10)
+        np.testing.assert_allclose(db, g[f"{tag}_db{i}"], rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(dx, g[f"{tag}_dx"][tuple(coords.T)], rtol=1e-10, atol=1e-10)
+
+
+def test_kmap_subm_general_k_offsets(rng):
+    """k^3 maps: centre tap is the identity, k = 3 equals the default table,
+    mirror symmetry nbr[nbr[i][j]][K-1-j] == i for k = 5."""
+    dims = (6, 7, 5)
+    occ = rng.random((1,) + dims) < 0.3
+    coords = np.argwhere(occ)
+    n3 = osp.kmap_subm(coords, dims)
+    assert np.array_equal(osp.kmap_subm(coords, dims, 3), n3)
+    assert np.array_equal(osp.kmap_subm(coords, dims, 1)[:, 0], np.arange(len(coords)))
+    n5 = osp.kmap_subm(coords, dims, 5)
+    assert np.array_equal(n5[:, 62], np.arange(len(coords)))
+    for j in range(125):
+        m = n5[:, j] >= 0
+        assert np.array_equal(n5[n5[m, j], 124 - j], np.nonzero(m)[0])
