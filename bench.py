@@ -15,34 +15,34 @@ halo tables), sparse interleave, 14 convs, head.
   host packed grid -> H2D -> frame -> D2H packed PVS for every step, every
   copy inside the timed region; up to E2E_INFLIGHT = 3 frames compute
   concurrently on separate streams with separate buffers (each frame is
-  still one bs1 pass; the level-1/2 convs leave SMs idle that the next frame
-  fills), and copies overlap compute.  ``value`` stays strictly one frame at
-  a time.
-  The streamed inputs are 64 distinct frames (the config-2 scene shifted by
-  whole cells, same density; 128 MiB in total, more than the L2), cycled.
+  still one bs1 pass).  ``e2e.latency_ms``: one frame in flight, pinned host
+  in -> device -> packed PVS back on the host, synchronised per frame (the
+  bs1 ms/frame of the metric, end to end).
 * ``roofline``: the dominant kernel, the tcgen05 sparse conv (14 launches per
-  frame: 10 halo-cached subm convs, spconv_halo, and 4 down/up gather-GEMMs,
-  spconv_tc): algorithmic FLOPs (2 * present pairs * Cin * Cout; zero-filled
-  taps not counted) / its summed per-launch DEVICE time.  Each
-  stage of the frame is captured alone as a CUDA graph of 20 back-to-back
-  launches and timed with CUDA events on its stream (host launch gaps
-  excluded); peak = MEASURED_PEAKS.json bf16.  ``traffic`` = DRAM bytes per
-  launch from the committed ncu --set full capture (profiles/).
+  frame: 10 halo-cached subm convs and 4 down/up gather-GEMMs): algorithmic
+  FLOPs (2 * present pairs * Cin * Cout; zero-filled taps not counted) / its
+  per-launch device time measured INSIDE the L2-flushed frame
+  (``pipeline.frame_stage_times``: the frame as one CUDA graph with timing
+  events between stages).  ``traffic`` = DRAM bytes per conv launch from the
+  committed ncu --set full capture (profiles/).
 * ``cpu_baseline``: the numpy sparse restatement (oracle/, fp64) of the same
   frame on this host's cores (rank 0, N=1).
-* ``froxelize`` (extra, N=1): SURVEY §8(f) #1, the device froxelizer on two
-  seeded triangle scenes into the 256^3 grid, device us per call and the
-  numpy oracle's CPU time on the same scene; a side line, not the metric.
-* ``gt_pvs`` (extra, N=1): SURVEY §8(f) #3, the device GT-PVS generator for
-  one viewcell (128 viewpoints, 1024^2 depth buffers, 256^3 grid) against the
-  numpy oracle's time per viewpoint; a side line, not the metric.
-* ``train_config5`` (extra, rank 0): BASELINE config 5's training step on one
-  GPU (8 x 128^3 grids, bf16 + fp32 master weights, AdamW, tcgen05 backward),
-  10 steps timed with CUDA events; a reported side line, not the metric.
+* ``config3`` (side line, every N): BASELINE config 3, 64 independent config-1
+  grids sharded over the ranks — rank r runs grids [r*64/N, (r+1)*64/N) as
+  one batched frame (CUDA graph, L2 flushed between steps), no collective on
+  the data path; grids/s = 64 * steps / max-rank time.
+* ``train_config5`` (side line, every N): BASELINE config 5, 8 x 128^3 grids
+  per GPU, bf16 + fp32 master weights, AdamW; a step = forward + loss +
+  tcgen05 backward + ONE all-reduce of [gradient | loss, counts] (NCCL under
+  torchrun) + update, timed with CUDA events, max over ranks.
+* ``froxelize`` / ``gt_pvs`` (side lines, N=1): SURVEY §8(f) #1 / #3.
 
-Multi-GPU: one process per GPU (torchrun); frames are independent ("replicas
-only" per frame): each rank runs its own frames, no
-collective on the data path; value = total frames / max-rank time.
+Multi-GPU: one process per GPU.  ``--gpus N`` with N > 1 outside torchrun
+re-executes this script under ``torch.distributed.run`` with N ranks on
+127.0.0.1; a WORLD_SIZE that disagrees with ``--gpus`` is an error.  Frames
+are independent ("replicas only" per frame); value = total
+frames / max-rank time.  ``--selftest`` runs the multi-rank plumbing on CPU
+with gloo (the config-3 sharding over the numpy oracle), for the CPU tests.
 
 ``--impl reference`` times the CPU reference path (the oracle port) instead.
 """
@@ -136,6 +136,95 @@ def dist_env():
     return ws, rank, local
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn(args) -> int:
+    """Re-execute this script under torch.distributed.run with --gpus ranks (127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous slice [r*n/N, (r+1)*n/N) of n independent units."""
+    return rank * n // world, (rank + 1) * n // world
+
+
+def run_selftest(args):
+    """CPU / gloo check of the multi-rank plumbing: config-3 sharding (8 config-1
+    grids through the numpy oracle at bs = slice), barrier-bracketed timing,
+    max over ranks, one JSON line from rank 0 with a checksum of every grid's
+    predicted bits (identical for any N)."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    from oracle import sparse as osp
+    from paper_2509_24677_b200 import synth
+    G = 8
+    lo, hi = shard_range(G, rank, ws)
+    rng = np.random.Generator(np.random.PCG64(0))
+    layers = []
+    for k, cin, cout, act in ((3, 8, 32, "relu"), (3, 32, 32, "relu"), (1, 32, 8, "sigmoid")):
+        w, b = osp.kaiming_uniform(rng, k ** 3, cin, cout, act)
+        layers.append((k, w, b, act))
+    occs = [synth.config3_grid(i) for i in range(lo, hi)]
+
+    def step():
+        out = []
+        for occ in occs:
+            cells = osp.interleave(occ.astype(np.float64), 2)[None]
+            coords, prob = osp.chain_forward(cells, layers)
+            dense = osp.deinterleave(osp.scatter_cells(coords, prob, (1,) + cells.shape[1:4])[0], 2)
+            out.append(np.packbits((dense >= 0.5).transpose(2, 1, 0), axis=2, bitorder="little").tobytes())
+        return out
+    for _ in range(args.warmup):
+        step()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        bits = step()
+    dt = time.perf_counter() - t0
+    if ws > 1:
+        dist.barrier()
+        t = torch.tensor([dt], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t[0])
+        gathered = [None] * ws
+        dist.all_gather_object(gathered, [hashlib.sha256(b).hexdigest() for b in bits])
+        digests = sum(gathered, [])
+    else:
+        digests = [hashlib.sha256(b).hexdigest() for b in bits]
+    if rank == 0:
+        print(json.dumps({"impl": "selftest", "metric": "config3 sharding over the oracle (CPU, gloo)",
+                          "value": G * args.steps / dt, "unit": "grids/s", "n_gpus": ws, "steps": args.steps,
+                          "warmup": args.warmup, "grids": G, "shards": [list(shard_range(G, r, ws)) for r in range(ws)],
+                          "checksum": hashlib.sha256("".join(digests).encode()).hexdigest()}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_threads() -> int:
+    """Give OpenBLAS every host thread (torchrun sets OMP_NUM_THREADS=1 per rank)."""
+    n = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(n)
+    except Exception:
+        pass
+    return n
+
+
 def cpu_frame_time(occ, seed=1):
     """One config-2 frame through the numpy sparse restatement (oracle, float64)."""
     from oracle import sparse as osp
@@ -154,7 +243,7 @@ def run_reference(args):
         return 0
     from paper_2509_24677_b200 import synth
     occ = synth.config2_grid(1)
-    cores = os.cpu_count()
+    cores = cpu_threads()
     warm = min(args.warmup, 3)  # CPU frames take seconds; 3 covers the warm-up rule without stretching the run
     for _ in range(warm):
         cpu_frame_time(occ)
@@ -196,36 +285,121 @@ def count_launches(fn):
     return n[0]
 
 
-def train_config5(steps: int = 10):
-    """BASELINE config 5 on this GPU: 8 grids of 128^3 per step, config-1 net, bf16
-    compute with fp32 master weights, AdamW; forward + fused loss + tcgen05
-    backward + update per step (the gradient all-reduce is the identity at N=1)."""
+def train_config5(ws: int = 1, rank: int = 0, steps: int = 10, warmup: int = 3):
+    """BASELINE config 5 per GPU: 8 grids of 128^3 (rank-specific seeds; weak
+    scaling), config-1 net, bf16 compute with fp32 master weights, AdamW; a step
+    = forward + fused loss + tcgen05 backward + ONE all-reduce of the
+    [gradient | loss, counts] exchange buffer (NCCL over NVLink when N > 1) +
+    update.  Device time with CUDA events, max over ranks."""
     import torch
+    import torch.distributed as dist
     from paper_2509_24677_b200 import synth
     from paper_2509_24677_b200.froxel import FroxelGrid
     from paper_2509_24677_b200.neural import ModelConfig, PvsNet, TrainConfig
     from paper_2509_24677_b200.train import TrainStep
     B = 8
-    pairs = [synth.config5_pair(0, i) for i in range(B)]
+    pairs = [synth.config5_pair(rank, i) for i in range(B)]
     bits = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(g).bits for g, _ in pairs])).cuda()
     gt = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(lb).bits for _, lb in pairs])).cuda()
     net = PvsNet(ModelConfig.config1(), np.random.Generator(np.random.PCG64(0)), precision="bf16")
     step = TrainStep(net, B, (128, 128, 128), TrainConfig(optimizer="adamw", lr=1e-3))
-    for i in range(3):
-        step.forward_backward(bits, gt)
-        step.update(1e-3, i + 1)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for i in range(steps):
-        step.forward_backward(bits, gt)
-        step.update(1e-3, 4 + i)
-    e1.record()
-    torch.cuda.synchronize()
+    acc = torch.zeros(8, dtype=torch.float64, device="cuda")
+    acc[6] = -1
+    launches = {"allreduce": 0}
+    if ws > 1:
+        orig = dist.all_reduce
+
+        def counting(*a, **k):
+            launches["allreduce"] += 1
+            return orig(*a, **k)
+        dist.all_reduce = counting
+    try:
+        for i in range(warmup):
+            step.forward_backward(bits, gt)
+            step.exchange(1.0 / ws)
+            step.accumulate(acc, i)
+            step.update(1e-3, i + 1)
+        torch.cuda.synchronize()
+        launches["allreduce"] = 0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        for i in range(steps):
+            step.forward_backward(bits, gt)
+            step.exchange(1.0 / ws)
+            step.accumulate(acc, warmup + i)
+            step.update(1e-3, warmup + i + 1)
+        e1.record()
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+    finally:
+        if ws > 1:
+            dist.all_reduce = orig
     ms = e0.elapsed_time(e1) / steps
-    return {"workload": "config5: 8 x 128^3 grids/step, config-1 net, bf16 + fp32 master, AdamW lr 1e-3",
-            "ms_per_step": ms, "grids_per_s": B / (ms * 1e-3), "active_rows": step.lv.count(),
-            "loss": float(step.loss), "backward": "tcgen05 dgrad + wgrad", "steps": steps}
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    a = acc.cpu().numpy()
+    return {"workload": "config5: 8 x 128^3 grids per GPU, config-1 net, bf16 + fp32 master, AdamW lr 1e-3",
+            "n_gpus": ws, "global_batch": B * ws, "scaling": "weak", "ms_per_step": ms,
+            "grids_per_s": B * ws / (ms * 1e-3), "active_rows_rank0": step.lv.count(),
+            "loss_mean": float(a[0] / max(a[1], 1)), "diverged": bool(a[6] >= 0),
+            "allreduce_per_step": launches["allreduce"] / steps if ws > 1 else 0,
+            "exchange_bytes": int(step.grads.numel() * 4), "backward": "tcgen05 dgrad + wgrad", "steps": steps}
+
+
+def config3_line(ws: int = 1, rank: int = 0, steps: int = 20, warmup: int = 3, flush=None):
+    """BASELINE config 3: 64 independent config-1 grids (seeds 100+i, density
+    U(1%, 6%)) sharded contiguously over the ranks, each rank one batched frame
+    of its slice per step (CUDA graph; L2 flushed between steps, untimed); no
+    collective on the data path.  bf16 (tensor cores) and fp32 (SIMT, the
+    config-1 parity precision).  grids/s = 64 * steps / max-rank time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2509_24677_b200 import synth
+    from paper_2509_24677_b200.froxel import FroxelGrid
+    from paper_2509_24677_b200.neural import ModelConfig, PvsNet
+    from paper_2509_24677_b200.pipeline import FramePipeline
+    G = 64
+    lo, hi = shard_range(G, rank, ws)
+    bits = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(synth.config3_grid(i)).bits
+                                            for i in range(lo, hi)])).cuda()
+    out = {"workload": "config3: 64 x (64x64x32) grids, config-1 net, sharded [r*64/N, (r+1)*64/N)",
+           "n_gpus": ws, "grids": G, "scaling": "strong", "slice_rank0": [lo, hi]}
+    for prec in ("bf16", "fp32"):
+        net = PvsNet(ModelConfig.config1(), np.random.Generator(np.random.PCG64(0)), precision=prec)
+        pipe = FramePipeline(net, hi - lo, (64, 64, 32), graph=True)
+        pipe.load(bits)
+        pipe.capture()
+        for _ in range(warmup):
+            pipe.run_device()
+        torch.cuda.synchronize()
+        st = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        en = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(steps):
+            if flush is not None:
+                flush.zero_()
+            st[i].record()
+            pipe.run_device()
+            en[i].record()
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        ms = sum(a.elapsed_time(b) for a, b in zip(st, en))
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        if ws > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+        out[prec] = {"grids_per_s": G * steps / (ms * 1e-3), "ms_per_batch": ms / steps,
+                     "active_rows_rank0": pipe.plan.L0.count()}
+    return out
 
 
 def froxelize_side(reps: int = 20):
@@ -319,6 +493,30 @@ def gt_pvs_side(views_n: int = 128):
             "speedup_vs_oracle": round(cpu_view_s * views_n / (best * 1e-3), 1)}
 
 
+def single_frame_latency(pipe, host_ins, host_out, frames: int = 20):
+    """bs1 end to end with ONE frame in flight: pinned host packed grid -> H2D ->
+    frame (graph replay) -> D2H packed PVS -> synchronise, per frame.  Device
+    time between events before the upload and after the download, plus the
+    host wall time of the same span; medians over ``frames``."""
+    import torch
+    dev, wall = [], []
+    stream = torch.cuda.current_stream()
+    for i in range(frames):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        e0.record(stream)
+        pipe.in_bits.copy_(host_ins[i % len(host_ins)], non_blocking=True)
+        pipe.run_device()
+        host_out.copy_(pipe.out_bits, non_blocking=True)
+        e1.record(stream)
+        e1.synchronize()
+        wall.append(time.perf_counter() - w0)
+        dev.append(e0.elapsed_time(e1))
+    return {"frames_in_flight": 1, "device_ms": statistics.median(dev), "wall_ms": 1e3 * statistics.median(wall),
+            "frames": frames}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -328,7 +526,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2509_24677_b200 import synth
     from paper_2509_24677_b200.froxel import FroxelGrid
-    from paper_2509_24677_b200.pipeline import FramePipeline, device_stage_times
+    from paper_2509_24677_b200.pipeline import FramePipeline, frame_stage_times
     from paper_2509_24677_b200.unet import PvsUNet
 
     dims = (256, 256, 256)
@@ -342,13 +540,14 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
-    # ---- per-stage device times (graph-replayed stages), FLOPs, launch count
+    # ---- per-stage device times inside the L2-flushed frame, FLOPs, launch count
     layer_flops = pipe.plan.layer_flops()
     n0, n1, n2 = pipe.plan.counts()
     launches_per_frame = count_launches(lambda: pipe.plan.run(pipe.in_bits, pipe.out_bits, 0.5))
     torch.cuda.synchronize()
-    stage_dev = device_stage_times(pipe.plan, pipe.in_bits, pipe.out_bits, 0.5, reps=20)
+    stage_dev, staged_frame_ms = frame_stage_times(pipe.plan, pipe.in_bits, pipe.out_bits, 0.5, flush=flush, reps=20)
     conv_ms = {k: stage_dev[k] for k in layer_flops if k != "head"}
+    pipe.capture(tune=False)  # the timed graph (no stage events)
 
     # ---- warm-up graph replays
     for _ in range(args.warmup):
@@ -400,10 +599,13 @@ def run_ours(args):
         dist.barrier()
     e2e_ms = e0.elapsed_time(e1)
     host_out = host_outs[-1]
+    latency = single_frame_latency(pipe, host_ins, torch.empty(nbytes, dtype=torch.uint8, pin_memory=True))
     time.sleep(0.2)
     clocks = sampler.stop()
 
     # correctness guard: the timed output equals the eager output
+    pipe.in_bits.copy_(host_bits.cuda())
+    pipe.run_device()
     check = pipe.out_bits.clone()
     pipe.plan.run(pipe.in_bits, pipe.out_bits, 0.5)
     torch.cuda.synchronize()
@@ -416,10 +618,15 @@ def run_ours(args):
     if not torch.equal(host_out.cuda(), pipe.out_bits):
         raise RuntimeError("streamed e2e output differs from the eager frame")
 
-    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([dev_ms, e2e_ms, latency["device_ms"], latency["wall_ms"]], dtype=torch.float64, device="cuda")
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_ms, e2e_ms = float(t[0]), float(t[1])
+    latency["device_ms"], latency["wall_ms"] = float(t[2]), float(t[3])
+
+    # ---- side lines at every N (collectives inside: all ranks take part)
+    c3 = None if args.no_config3 else config3_line(ws, rank, steps=20, warmup=3, flush=flush)
+    train = None if args.no_train else train_config5(ws, rank)
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()
@@ -441,17 +648,15 @@ def run_ours(args):
         pass
 
     cpu = None
-    train = None
     frox = None
-    if not args.no_train:
-        train = train_config5()
     gtp = None
     if ws == 1 and not args.no_froxelize:
         frox = froxelize_side()
         gtp = gt_pvs_side()
     if ws == 1 and not args.no_cpu_baseline:
+        cores = cpu_threads()
         t_cpu = cpu_frame_time(occ)
-        cpu = {"value": 1.0 / t_cpu, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": 1.0 / t_cpu, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": "one config-2 frame (interleave, maps, U-Net, threshold) through the numpy sparse "
                          "restatement oracle/sparse.py in float64 on all host threads (OpenBLAS)"}
 
@@ -466,7 +671,8 @@ def run_ours(args):
                    "active_cells": [n0, n1, n2], "density": float(occ.mean()), "cuda_graph": True},
         "e2e": {"value": ws * args.steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes,
                 "d2h_bytes_per_step": nbytes, "ms_per_step": e2e_ms / args.steps,
-                "wall_ms_per_step": 1e3 * wall_e2e / args.steps, "frames_in_flight": E2E_INFLIGHT},
+                "wall_ms_per_step": 1e3 * wall_e2e / args.steps, "frames_in_flight": E2E_INFLIGHT,
+                "latency_ms": latency},
         "roofline": {"bound": "tensor",
                      "kernel": "tcgen05 sparse conv: spconv_halo (10 subm convs, halo-cached, A in TMEM) + spconv_tc "
                                "(2 down + 2 parity-sorted up gather-GEMMs) per frame",
@@ -474,14 +680,19 @@ def run_ours(args):
                      "peak_kind": f"{peak_kind} bf16 burst", "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (mean over the 14 conv launches, ncu --set full)",
                      "flops_per_frame": tc_flops, "launches_per_frame": n_tc_launches,
-                     "kernel_ms_per_frame": tc_ms, "per_layer": per_layer},
+                     "kernel_ms_per_frame": tc_ms, "per_layer": per_layer,
+                     "timing": "per stage inside the L2-flushed frame: prefix graphs of the frame's first k stages, "
+                               "stage k = T_k - T_(k-1), medians of 20 replays (pipeline.frame_stage_times)"},
         "stages_ms": stage_ms,
         "stages_total_ms": round(sum(stage_dev.values()), 5),
+        "staged_frame_ms": round(staged_frame_ms, 5),
         "gpu_launches": launches_per_frame * args.steps,
         "clocks": clocks,
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if c3 is not None:
+        line["config3"] = c3
     if train is not None:
         line["train_config5"] = train
     if frox is not None:
@@ -502,8 +713,20 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the config-5 training-step line")
+    ap.add_argument("--no-config3", action="store_true", help="skip the config-3 sharded-batch line")
     ap.add_argument("--no-froxelize", action="store_true", help="skip the froxelization / GT-PVS side lines")
+    ap.add_argument("--selftest", action="store_true", help="CPU/gloo check of the multi-rank plumbing")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn(args)
+    ws, _, _ = dist_env()
+    if ws != args.gpus:
+        print(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if args.selftest:
+        return run_selftest(args)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

@@ -371,6 +371,21 @@ int fpvs_cast_bf16_rows(const float* src, int cols, const int32_t* n_dev, int ca
  * AdamW (BASELINE config 5, fp32 master weights): m, v zero-initialised,
  * step counts from 1, decoupled weight decay. */
 int fpvs_sgd_step(float* params, const float* grads, size_t n, float lr, void* stream);
+
+/* Data-parallel exchange (one all-reduce per step): flat = [gradient n f32 |
+ * FPVS_EXCHANGE_TAIL f32].  fpvs_exchange_pack scales the local mean gradient
+ * by weight = B_local / B_global (the sum over ranks is the batch mean of
+ * neural.py:472-477) and writes the tail: batch-mean loss x B_local, B_local,
+ * and the summed TP/FP/FN/GTP of counts[4B] as exact 12-bit f32 digits.
+ * After the all-reduce fpvs_exchange_accumulate adds the tail into the epoch
+ * accumulator acc f64[8] = {loss x samples, samples, TP, FP, FN, GTP,
+ * first non-finite batch index (init -1), its loss} on the device, so the
+ * training loop needs no host round trip per step (TrainingDiverged is raised
+ * from acc[6] at the end of the epoch). */
+#define FPVS_EXCHANGE_TAIL 10
+int fpvs_exchange_pack(float* flat, size_t n, float weight, const double* loss, const int64_t* counts,
+                       int B, void* stream);
+int fpvs_exchange_accumulate(const float* tail, double* acc, int batch_index, void* stream);
 int fpvs_adamw_step(float* params, const float* grads, float* m, float* v, size_t n, float lr,
                     float beta1, float beta2, float eps, float weight_decay, int step, void* stream);
 

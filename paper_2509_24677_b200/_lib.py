@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("FPVS_LIB", os.path.join(HERE, "libfpvs.so"))
 
 F32, BF16 = 0, 1
 IN_PACKED, IN_U8, IN_F32 = 0, 1, 2
+EXCHANGE_TAIL = 10  # FPVS_EXCHANGE_TAIL
 ACT = {"none": 0, "relu": 1, "sigmoid": 2}
 
 _i, _f, _d, _p, _z = C.c_int, C.c_float, C.c_double, C.c_void_p, C.c_size_t
@@ -71,6 +72,8 @@ SIGNATURES = {
     "fpvs_spconv_dgrad_simt": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _p, _i, _i, _p, _i, _p]),
     "fpvs_wgrad_workspace_size": (_z, [_i, _i, _i, _i]),
     "fpvs_spconv_wgrad_simt": (_i, [_p, _i, _i, _p, _i, _p, _i, _p, _i, _i, _i, _p, _p, _p, _z, _p]),
+    "fpvs_exchange_pack": (_i, [_p, _z, _f, _p, _p, _i, _p]),
+    "fpvs_exchange_accumulate": (_i, [_p, _p, _i, _p]),
     "fpvs_sgd_step": (_i, [_p, _p, _z, _f, _p]),
     "fpvs_adamw_step": (_i, [_p, _p, _p, _p, _z, _f, _f, _f, _f, _f, _i, _p]),
     "fpvs_bits_confusion_workspace_size": (_z, [_i]),

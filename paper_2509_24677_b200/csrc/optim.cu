@@ -100,9 +100,69 @@ __global__ void confusion_reduce_kernel(const unsigned long long* __restrict__ p
   counts[t] = (long long)s;
 }
 
+// ---- data-parallel exchange buffer ---------------------------------------
+// One NCCL all-reduce per training step moves [gradient (n f32) | tail]: the
+// local mean gradient pre-scaled by B_local / B_global (so the sum over ranks
+// is the reference's batch mean, neural.py:472-477) and a tail that carries
+// the step's loss and hard counts.  Counts are split into 12-bit digits so
+// their f32 sums stay exact (< 2^24 per digit for up to 4096 ranks).
+//   tail[0] = batch-mean loss x local samples   tail[1] = local samples
+//   tail[2 + 2q], tail[3 + 2q] = (count_q >> 12, count_q & 4095), q = TP, FP, FN, GTP
+constexpr int kExchTail = FPVS_EXCHANGE_TAIL;
+
+__global__ void exchange_pack_kernel(float* __restrict__ flat, long long n, float weight,
+                                     const double* __restrict__ loss, const long long* __restrict__ counts, int B) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    flat[i] *= weight;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    float* t = flat + n;
+    long long c[4] = {0, 0, 0, 0};
+    for (int b = 0; b < B; ++b)
+      for (int q = 0; q < 4; ++q) c[q] += counts[4 * b + q];
+    t[0] = B > 0 ? (float)(loss[0] * B) : 0.f;
+    t[1] = (float)B;
+    for (int q = 0; q < 4; ++q) {
+      t[2 + 2 * q] = (float)(c[q] >> 12);
+      t[3 + 2 * q] = (float)(c[q] & 4095);
+    }
+  }
+}
+
+// acc: [0] sum of batch-mean loss x batch size, [1] samples, [2..5] TP FP FN GTP,
+//      [6] index of the first batch with a non-finite loss (-1 none), [7] that loss
+__global__ void exchange_accumulate_kernel(const float* __restrict__ t, double* __restrict__ acc, int batch_index) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double ls = t[0], ns = t[1];
+  const double mean = ns > 0 ? ls / ns : 0.0;
+  if (!isfinite(mean) && acc[6] < 0) {
+    acc[6] = batch_index;
+    acc[7] = mean;
+  }
+  acc[0] += ls;
+  acc[1] += ns;
+  for (int q = 0; q < 4; ++q) acc[2 + q] += (double)t[2 + 2 * q] * 4096.0 + (double)t[3 + 2 * q];
+}
+
 }  // namespace fpvs
 
 using namespace fpvs;
+
+extern "C" int fpvs_exchange_pack(float* flat, size_t n, float weight, const double* loss, const int64_t* counts,
+                                  int B, void* stream) {
+  FPVS_CHECK_ARG(flat, "null pointer");
+  FPVS_CHECK_ARG(B == 0 || (loss && counts), "loss and counts are required with B > 0");
+  exchange_pack_kernel<<<grid_for((long long)n, 256), 256, 0, as_stream(stream)>>>(
+      flat, (long long)n, weight, loss, (const long long*)counts, B);
+  FPVS_CHECK_LAUNCH("fpvs_exchange_pack");
+  return FPVS_OK;
+}
+
+extern "C" int fpvs_exchange_accumulate(const float* tail, double* acc, int batch_index, void* stream) {
+  FPVS_CHECK_ARG(tail && acc, "null pointer");
+  exchange_accumulate_kernel<<<1, 32, 0, as_stream(stream)>>>(tail, acc, batch_index);
+  FPVS_CHECK_LAUNCH("fpvs_exchange_accumulate");
+  return FPVS_OK;
+}
 
 extern "C" int fpvs_sgd_step(float* params, const float* grads, size_t n, float lr, void* stream) {
   FPVS_CHECK_ARG(params && grads, "null pointer");

@@ -178,6 +178,70 @@ def device_stage_times(plan, bits, out_bits, tau: float = 0.5, reps: int = 20, f
     return res
 
 
+def frame_stage_times(plan, bits, out_bits, tau: float = 0.5, flush=None, reps: int = 10):
+    """Per-stage DEVICE time (ms) inside the real, L2-flushed frame.
+
+    Prefix differencing: for k = 1..S the first k stages are captured as one
+    CUDA graph (exactly the benchmarked frame's launches, PDL overlap and
+    side-stream fork/join included, no timing nodes inside) and timed with
+    events around each replay after an untimed L2 flush (``flush``, larger
+    than the L2); stage k's time is T_k - T_{k-1} (medians over ``reps``), so
+    the stages sum to the frame time.  (Timing events BETWEEN stages were
+    measured to add ~7 us per boundary — they break PDL overlap — and L2-warm
+    isolated replays to undercount it.)  The U-Net's side-stream map tables
+    are serialised into "maps" here (``overlap`` off), or their join would be
+    charged to whichever conv a prefix happens to end on.  Returns
+    (per-stage dict, frame ms of this serialised frame).
+    """
+    torch = _torch()
+    saved = getattr(plan, "overlap", None)
+    if saved is not None:
+        plan.overlap = False
+    try:
+        return _prefix_times(plan, bits, out_bits, tau, flush, reps)
+    finally:
+        if saved is not None:
+            plan.overlap = saved
+
+
+def _prefix_times(plan, bits, out_bits, tau, flush, reps):
+    torch = _torch()
+    stages = plan.stages(bits, out_bits, tau)
+    for _, fn in stages:
+        fn()
+    join = getattr(plan, "_join_side", None)
+    if join is not None:
+        join()
+    torch.cuda.synchronize()
+    prefix = [0.0]
+    for k in range(1, len(stages) + 1):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s), no_gc():
+            with torch.cuda.graph(g, stream=s):
+                for _, fn in stages[:k]:
+                    fn()
+                if join is not None:
+                    join()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            if flush is not None:
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        prefix.append(float(np.median(ts)))
+        del g
+    per = {name: max(prefix[i + 1] - prefix[i], 0.0) for i, (name, _) in enumerate(stages)}
+    return per, prefix[-1]
+
+
 class FramePipeline:
     """CUDA-graph replay of one frame for a fixed (B, grid) shape.
 

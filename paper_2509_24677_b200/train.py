@@ -36,7 +36,6 @@ subset of the occupancy, row LBL).
 
 from __future__ import annotations
 
-import math
 from pathlib import Path
 
 import numpy as np
@@ -129,8 +128,11 @@ class TrainStep:
         # flat master parameters and gradient
         sizes = [(L.w.numel(), L.b.numel()) for L in net.layers]
         total = sum(a + b for a, b in sizes)
+        self.nparams = total
         self.params = torch.empty(total, dtype=torch.float32, device=device)
-        self.grads = torch.zeros(total, dtype=torch.float32, device=device)
+        # the exchange buffer: [flat gradient | loss + hard-count tail] (fpvs_exchange_pack)
+        self.grads = torch.zeros(total + _lib.EXCHANGE_TAIL, dtype=torch.float32, device=device)
+        self.tail = self.grads[total:]
         self.views = []
         o = 0
         for L, (nw, nb) in zip(net.layers, sizes):
@@ -260,14 +262,33 @@ class TrainStep:
             dz, lddz = dx, dx.shape[1]
 
     # -- exchange + update ---------------------------------------------------
-    def exchange(self, weight: float = 1.0):
-        """Weight the local mean gradient and sum it across ranks (one all-reduce)."""
-        allreduce_weighted(self.grads, weight)
+    def pack(self, weight: float = 1.0, samples: int | None = None, stream=None):
+        """Scale the local mean gradient by ``weight`` (= B_local / B_global) and
+        write the loss / hard-count tail of the exchange buffer.  ``samples`` = 0
+        packs an empty share (a rank with no samples in this batch)."""
+        B = self.B if samples is None else samples
+        if B == 0:
+            self.grads.zero_()
+        _lib.call("fpvs_exchange_pack", _lib.ptr(self.grads), self.nparams, float(weight), _lib.ptr(self.loss),
+                  _lib.ptr(self.counts), B, _lib.stream_ptr(stream))
+
+    def exchange(self, weight: float = 1.0, samples: int | None = None, stream=None):
+        """pack() and sum the buffer across ranks: ONE all-reduce per step (NCCL
+        over NVLink under torchrun; identity at world size 1)."""
+        self.pack(weight, samples, stream)
+        dist = _dist()
+        if dist is not None and dist.get_world_size() > 1:
+            dist.all_reduce(self.grads, op=dist.ReduceOp.SUM)
+
+    def accumulate(self, acc, batch_index: int, stream=None):
+        """Add the exchanged tail into the epoch accumulator (device f64[8])."""
+        _lib.call("fpvs_exchange_accumulate", _lib.ptr(self.tail), _lib.ptr(acc), int(batch_index),
+                  _lib.stream_ptr(stream))
 
     def update(self, lr: float, step: int, stream=None):
         tc = self.tcfg
         s = _lib.stream_ptr(stream)
-        n = self.params.numel()
+        n = self.nparams
         if tc.optimizer == "adamw":
             _lib.call("fpvs_adamw_step", _lib.ptr(self.params), _lib.ptr(self.grads), _lib.ptr(self.m),
                       _lib.ptr(self.v), n, float(lr), 0.9, 0.999, 1e-8, float(tc.weight_decay), int(step), s)
@@ -387,42 +408,40 @@ def train(pairs, mcfg: ModelConfig, tcfg: TrainConfig, eval_pairs=None, target_f
     trainer = Trainer(net, dims, tcfg)
     n = len(pairs)
     history, step = [], 0
+    # epoch accumulator on the device: loss x samples, samples, TP/FP/FN/GTP,
+    # first non-finite batch (-1) and its loss (fpvs_exchange_accumulate)
+    acc = torch.zeros(8, dtype=torch.float64, device="cuda")
     for epoch in range(tcfg.epochs):
         order = rng.permutation(n)
-        epoch_loss = 0.0
-        tot = np.zeros(4, dtype=np.int64)
+        acc.zero_()
+        acc[6] = -1.0
+        # a step is: forward + loss + backward, pack, ONE all-reduce of the
+        # [gradient | loss, counts] buffer, accumulate, optimizer — no host sync
         for start in range(0, n, tcfg.batch_size):
             batch = order[start:start + tcfg.batch_size]
             mine = shard(batch, rank, world)
-            stats = torch.zeros(2, dtype=torch.float64, device="cuda")  # (sum of sample losses, local count)
-            counts = torch.zeros(4, dtype=torch.int64, device="cuda")
             if mine:
                 plan = trainer.plan(len(mine))
                 idx = torch.as_tensor(np.asarray(mine, dtype=np.int64), device="cuda")
                 bits = geo.view(n, gb)[idx].reshape(-1)
                 gt = lab.view(n, gb)[idx].reshape(-1)
                 plan.forward_backward(bits, gt)
-                stats[0] = plan.loss[0] * len(mine)
-                stats[1] = len(mine)
-                counts += plan.counts.view(-1, 4).sum(0)
                 plan.exchange(len(mine) / len(batch))
             else:
                 plan = trainer.plan(1)
-                plan.grads.zero_()
-                plan.exchange(1.0)
-            if dist is not None and world > 1:
-                dist.all_reduce(stats)
-                dist.all_reduce(counts)
-            loss = float(stats[0]) / len(batch)
-            if not math.isfinite(loss):
-                raise TrainingDiverged(start // tcfg.batch_size, loss)
+                plan.exchange(0.0, samples=0)
+            plan.accumulate(acc, start // tcfg.batch_size)
             lr = tcfg.lr * (1.0 - tcfg.decay) ** step
             step += 1
             plan.update(lr, step)
-            epoch_loss += loss * len(batch)
-            tot += counts.cpu().numpy()
+        # one host read per epoch; a non-finite loss raises as the reference's
+        # per-batch check does (neural.py:478-479), with the same batch index and value
+        a = acc.cpu().numpy()
+        if a[6] >= 0:
+            raise TrainingDiverged(int(a[6]), float(a[7]))
+        tot = np.rint(a[2:6]).astype(np.int64)
         fnr, fpr = _rates(*[int(v) for v in tot])
-        entry = {"epoch": epoch, "loss": epoch_loss / max(n, 1), "fnr": fnr, "fpr": fpr}
+        entry = {"epoch": epoch, "loss": float(a[0]) / max(n, 1), "fnr": fnr, "fpr": fpr}
         if eval_pairs:
             entry["val_fnr"], entry["val_fpr"] = evaluate_grid_pairs(net, eval_pairs, tcfg.tau)
         history.append(entry)

@@ -50,8 +50,8 @@ TAPS = {"subm": 27, "down": 8, "up": 8, "head": 1}
 
 
 class _Spec:
-    def __init__(self, cin, cout, act):
-        self.in_channels, self.out_channels, self.activation = cin, cout, act
+    def __init__(self, cin, cout, act, kernel):
+        self.in_channels, self.out_channels, self.activation, self.kernel = cin, cout, act, kernel
 
 
 class SparseLayer:
@@ -60,7 +60,8 @@ class SparseLayer:
     def __init__(self, name, kind, cin, cout, w, b, device="cuda"):
         torch = _torch()
         self.name, self.kind, self.taps = name, kind, TAPS[kind]
-        self.spec = _Spec(cin, cout, "sigmoid" if kind == "head" else "relu")
+        self.spec = _Spec(cin, cout, "sigmoid" if kind == "head" else "relu",
+                          {"subm": 3, "down": 2, "up": 2, "head": 1}[kind])
         self.w = torch.as_tensor(np.asarray(w, np.float32)).to(device).contiguous()
         self.b = torch.as_tensor(np.asarray(b, np.float32)).to(device).contiguous()
         self._packed = None
