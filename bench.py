@@ -300,7 +300,11 @@ def train_config5(ws: int = 1, rank: int = 0, steps: int = 10, warmup: int = 3):
     B = 8
     pairs = [synth.config5_pair(rank, i) for i in range(B)]
     bits = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(g).bits for g, _ in pairs])).cuda()
-    gt = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(lb).bits for _, lb in pairs])).cuda()
+    # row LBL labels made on the device from the packed geometry (fpvs_first_hit_labels)
+    gt = synth.first_hit_labels_bits(bits, B, (128, 128, 128), 2)
+    want = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(lb).bits for _, lb in pairs])).cuda()
+    if not torch.equal(gt, want):
+        raise RuntimeError("device labels differ from synth.first_hit_labels")
     net = PvsNet(ModelConfig.config1(), np.random.Generator(np.random.PCG64(0)), precision="bf16")
     step = TrainStep(net, B, (128, 128, 128), TrainConfig(optimizer="adamw", lr=1e-3))
     acc = torch.zeros(8, dtype=torch.float64, device="cuda")

@@ -401,3 +401,56 @@ def chain_backward(dy, layers, caches):
         grads[li] = (dw, dz.sum(0))
         dy = dx
     return grads, dy
+
+
+def chain_train_step_bf16(cells, gts, layers, alpha=0.1, lam=0.99):
+    """bf16-emulating restatement of the device's bf16 training step
+    (TrainStep with the tcgen05 backward, BASELINE config 5).
+
+    Rounding points follow the device: weights and every stored activation are
+    RNE-rounded to bf16; products accumulate exactly here (float64; the device
+    accumulates in fp32 in TMEM); the head's logits and probabilities stay
+    unrounded; dL/dlogit (the per-sample combined loss of neural.py:353-399
+    times sigmoid', over the batch size) is rounded to bf16 before the
+    backward; each lower layer's dz is rounded to bf16 after the relu' mask
+    (the dgrad epilogue, z > 0 <=> the kept bf16 output > 0, neural.py:227-228);
+    dW and db accumulate exactly from those bf16 operands.
+    Returns (batch-mean loss, [(dw, db)] per layer, coords, probs)."""
+    dims = cells.shape[1:4]
+    B = cells.shape[0]
+    coords = active_coords(cells)
+    x = cells[tuple(coords.T)].astype(np.float64)
+    tabs = {k: (np.arange(len(coords))[:, None] if k == 1 else kmap_subm(coords, dims, k))
+            for k in {layer[0] for layer in layers}}
+    wb = [bf16_round(w) for _, w, _, _ in layers]
+    acts = [bf16_round(x)]
+    for (k, _, b, act), w in zip(layers[:-1], wb[:-1]):
+        acts.append(bf16_round(_act(gather_conv(acts[-1], tabs[k], w, b), act)))
+    kh, _, bh, _ = layers[-1]
+    probs = sigmoid(gather_conv(acts[-1], tabs[kh], wb[-1], bh))
+    loss, dp = 0.0, np.zeros_like(probs)
+    for bi in range(B):
+        rows = coords[:, 0] == bi
+        pd = np.zeros(dims + (probs.shape[1],))
+        pd[tuple(coords[rows, 1:].T)] = probs[rows]
+        lv, lg = combined_loss(pd, gts[bi], alpha, lam)
+        loss += lv
+        dp[rows] = lg[tuple(coords[rows, 1:].T)] / B
+    dz = bf16_round(dp * probs * (1.0 - probs))
+    grads = [None] * len(layers)
+    for li in reversed(range(len(layers))):
+        k = layers[li][0]
+        tab, xin = tabs[k], acts[li]
+        cin = xin.shape[1]
+        dw = np.zeros_like(wb[li])
+        dx = np.zeros_like(xin)
+        for j in range(tab.shape[1]):
+            m = tab[:, j] >= 0
+            src = tab[m, j]
+            dw[j * cin:(j + 1) * cin] += xin[src].T @ dz[m]
+            if li > 0:
+                np.add.at(dx, src, dz[m] @ wb[li][j * cin:(j + 1) * cin].T)
+        grads[li] = (dw, dz.sum(0))
+        if li > 0:
+            dz = bf16_round(dx * (xin > 0))
+    return loss / B, grads, coords, probs

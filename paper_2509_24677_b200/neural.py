@@ -775,9 +775,11 @@ def combined_loss(pred, gt, cfg: TrainConfig):
 
 
 def _like(ref, val):
+    """Gradient in the caller's form: a tensor on the caller's device for tensor
+    input, a float64 numpy array for numpy input (neural.py returns np arrays)."""
     torch = _torch()
     if isinstance(ref, torch.Tensor):
-        return val if isinstance(val, torch.Tensor) else torch.as_tensor(val)
+        return (val if isinstance(val, torch.Tensor) else torch.as_tensor(val)).to(ref.device)
     return val.cpu().numpy() if isinstance(val, torch.Tensor) else np.asarray(val)
 
 

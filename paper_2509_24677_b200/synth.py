@@ -84,6 +84,21 @@ def first_hit_labels(occ: np.ndarray, radius: int = 2) -> np.ndarray:
     return vis & occ
 
 
+def first_hit_labels_bits(bits, B: int, grid_dims, radius: int = 2, out=None, stream=None):
+    """The same labels on the device from packed geometry bits (fpvs_first_hit_labels):
+    B packed (Nx, Ny, Nz) grids in, B packed label grids out (CUDA uint8)."""
+    import torch
+
+    from . import _lib
+    nx, ny, nz = grid_dims
+    if out is None:
+        out = torch.empty(B * nx * ny * nz // 8, dtype=torch.uint8, device=bits.device)
+    ws = torch.empty(B * nx * ny, dtype=torch.int32, device=bits.device)
+    _lib.call("fpvs_first_hit_labels", _lib.ptr(bits), B, nx, ny, nz, int(radius), _lib.ptr(out), _lib.ptr(ws),
+              _lib.stream_ptr(stream))
+    return out
+
+
 # BASELINE.json config shapes ------------------------------------------------
 
 def config1_grid(seed: int = 0) -> np.ndarray:

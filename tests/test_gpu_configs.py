@@ -88,7 +88,7 @@ def test_config3_batch_equals_single_grids():
         assert np.array_equal(out_b[b * per:(b + 1) * per], out_1), b
 
 
-@pytest.mark.parametrize("density", [0.005, 0.08])
+@pytest.mark.parametrize("density", [0.005, 0.02, 0.08, pytest.param(0.25, marks=pytest.mark.slow)])
 def test_config4_density_sweep_full_size(density):
     occ = synth.config4_grid(density)
     assert abs(float(occ.mean()) - density) < 0.25 * density

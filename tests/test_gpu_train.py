@@ -189,3 +189,74 @@ def test_train_adamw_bf16_runs_and_learns():
     losses = [h["loss"] for h in hist]
     assert all(np.isfinite(losses)) and losses[-1] < losses[0]
     assert "val_fnr" in hist[-1]
+
+
+@pytest.mark.slow
+def test_config5_full_size_bf16_step_vs_bf16_oracle():
+    """BASELINE config 5 at its stated size: 8 x 128^3 grids (~4 % density), the
+    config-1 net in bf16, one forward + fused loss + tcgen05 backward, against
+    the oracle's bf16 emulation of the same rounding points
+    (osp.chain_train_step_bf16).  Tolerance: loss within 1e-4 relative;
+    each gradient tensor within 1e-2 relative (Frobenius) — the device sums in
+    fp32 in a different order, which flips occasional bf16 roundings of dz."""
+    import torch
+    from paper_2509_24677_b200.neural import ModelConfig, PvsNet, TrainConfig
+    from paper_2509_24677_b200.train import TrainStep
+    pairs = [synth.config5_pair(0, i) for i in range(8)]
+    occs, labs = [g for g, _ in pairs], [lb for _, lb in pairs]
+    net = PvsNet(ModelConfig.config1(), np.random.Generator(np.random.PCG64(0)), precision="bf16")
+    layers = _layers(net)
+    step = TrainStep(net, 8, (128, 128, 128), TrainConfig(optimizer="adamw"))
+    assert step.tc_backward
+    step.forward_backward(_bits(occs), _bits(labs))
+    torch.cuda.synchronize()
+    cells = np.stack([osp.interleave(o.astype(np.float64), 2) for o in occs])
+    gts = np.stack([osp.interleave(g.astype(np.float64), 2) for g in labs])
+    loss, grads, coords, _ = osp.chain_train_step_bf16(cells, gts, layers)
+    assert step.lv.count() == len(coords)
+    got_loss = float(step.loss[0])
+    assert abs(got_loss - loss) <= 1e-4 * abs(loss), (got_loss, loss)
+    for li, (L, (gw, gb)) in enumerate(zip(net.layers, grads)):
+        dw, db = (t.double().cpu().numpy() for t in step.views[li])
+        for name, a, b in (("dw", dw.reshape(gw.shape), gw), ("db", db, gb)):
+            rel = float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
+            assert rel <= 1e-2, (li, name, rel)
+
+
+@pytest.mark.parametrize("radius", [0, 1, 2, 3])
+def test_first_hit_labels_kernel_matches_host_rule(radius):
+    """Row LBL on the device (fpvs_first_hit_labels) == synth.first_hit_labels:
+    config-5 grids, a grid with occupancy against every border, an empty grid."""
+    from paper_2509_24677_b200.synth import first_hit_labels_bits
+    dims = (128, 128, 128)
+    grids = [synth.config5_pair(0, i)[0] for i in range(2)]
+    edge = np.zeros(dims, bool)
+    edge[0, :, 5] = edge[-1, :, 7] = edge[:, 0, 0] = edge[:, -1, -1] = True
+    edge[60:70, 60:70, 30:40] = True
+    grids += [edge, np.zeros(dims, bool)]
+    got = first_hit_labels_bits(_bits(grids), len(grids), dims, radius).cpu().numpy()
+    per = dims[0] * dims[1] * dims[2] // 8
+    for b, g in enumerate(grids):
+        want = FroxelGrid.from_dense(synth.first_hit_labels(g, radius)).bits
+        assert np.array_equal(got[b * per:(b + 1) * per], want), b
+
+
+def test_dropin_losses_match_reference_golden(golden):
+    """dice_loss / rvl_loss / combined_loss (neural.py:353-399) on the device vs
+    the reference's own values and gradients (tests/golden/loss.npz), numpy in
+    -> numpy out and CUDA tensors in -> tensors out; shape mismatch -> ValueError."""
+    import torch
+    from paper_2509_24677_b200.neural import TrainConfig, combined_loss, dice_loss, rvl_loss
+    g = golden("loss.npz")
+    cfg = TrainConfig()
+    for i in range(int(g["n"])):
+        pred, gt = g[f"l{i}_pred"], g[f"l{i}_gt"]
+        for fn, key, args in ((dice_loss, "dice", (cfg.alpha,)), (rvl_loss, "rvl", ()), (combined_loss, "comb", (cfg,))):
+            v, gr = fn(pred, gt, *args)
+            assert abs(float(v) - float(g[f"l{i}_{key}"])) <= 1e-12, (i, key)
+            assert isinstance(gr, np.ndarray) and np.abs(gr - g[f"l{i}_{key}_g"]).max() <= 1e-12, (i, key)
+            vt, gt_ = fn(torch.as_tensor(pred).cuda(), torch.as_tensor(gt).cuda(), *args)
+            assert abs(float(vt) - float(g[f"l{i}_{key}"])) <= 1e-12
+            assert isinstance(gt_, torch.Tensor) and float((gt_.cpu() - torch.as_tensor(g[f"l{i}_{key}_g"])).abs().max()) <= 1e-12
+    with pytest.raises(ValueError):
+        dice_loss(np.zeros(3), np.zeros(4), 0.1)
