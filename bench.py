@@ -406,6 +406,72 @@ def config3_line(ws: int = 1, rank: int = 0, steps: int = 20, warmup: int = 3, f
     return out
 
 
+def interleave_side(reps: int = 20):
+    """North_star (1): the standalone interleave / deinterleave kernels at the
+    config-2 size (256^3, d = 4) — algorithmic bytes (input + output, once) per
+    call / device time, against the HBM peak.  Each timed call follows an
+    untimed L2 flush; the call is replayed from a CUDA graph so the events
+    bracket device work only."""
+    import torch
+    from paper_2509_24677_b200 import synth
+    from paper_2509_24677_b200.froxel import FroxelGrid
+    from paper_2509_24677_b200.interleave import deinterleave_device, interleave_device
+    hbm, _, kind = peaks()
+    occ = synth.config2_grid(1)
+    dense = torch.from_numpy(occ.astype(np.float32)).cuda()[None]
+    bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    dims = (1,) + occ.shape
+    cells16 = interleave_device(dense, 4, torch.bfloat16)
+    cells32 = interleave_device(dense, 4, torch.float32)
+    cases = {
+        "dense_f32_to_bf16": (lambda: interleave_device(dense, 4, torch.bfloat16), 4 * occ.size + 2 * occ.size),
+        "packed_to_bf16": (lambda: interleave_device(bits, 4, torch.bfloat16, packed_dims=dims),
+                           occ.size // 8 + 2 * occ.size),
+        "deinterleave_f32_to_f32": (lambda: deinterleave_device(cells32, 4), 8 * occ.size),
+        "deinterleave_bf16_threshold_bits": (lambda: deinterleave_device(cells16, 4, 0.5), 2 * occ.size + occ.size // 8),
+    }
+    out = {"workload": "256^3 froxels, d = 4 (config 2): 64^3 cells x 64 channels", "peak_gbs": hbm,
+           "peak_kind": kind}
+    from paper_2509_24677_b200.pipeline import no_gc
+
+    def graph_of(body, k=8):
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st), no_gc():
+            with torch.cuda.graph(g, stream=st):
+                for _ in range(k):
+                    body()
+        torch.cuda.current_stream().wait_stream(st)
+        return g
+
+    def timed(g):
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+    # per call: graphs of 8 x (L2 flush, call) and of 8 x (L2 flush) alone;
+    # the difference / 8 is the call's device time with a cold L2 and no host
+    # or graph-launch overhead inside
+    k = 8
+    t_flush = timed(graph_of(lambda: flush.zero_(), k))
+    for name, (fn, nbytes) in cases.items():
+        fn()
+        torch.cuda.synchronize()
+        g = graph_of(lambda fn=fn: (flush.zero_(), fn()), k)
+        ms = max(timed(g) - t_flush, 1e-6) / k
+        del g
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[name] = {"us": round(ms * 1e3, 2), "bytes": int(nbytes), "gbs": round(gbs, 1), "frac": round(gbs / hbm, 3)}
+    return out
+
+
 def froxelize_side(reps: int = 20):
     """fpvs_froxelize of a seeded triangle scene into the 256^3
     grid (supersample 4, linear depth) — device time per call from a CUDA graph
@@ -654,9 +720,12 @@ def run_ours(args):
     cpu = None
     frox = None
     gtp = None
+    il = None
     if ws == 1 and not args.no_froxelize:
         frox = froxelize_side()
         gtp = gt_pvs_side()
+    if ws == 1:
+        il = interleave_side()
     if ws == 1 and not args.no_cpu_baseline:
         cores = cpu_threads()
         t_cpu = cpu_frame_time(occ)
@@ -699,6 +768,8 @@ def run_ours(args):
         line["config3"] = c3
     if train is not None:
         line["train_config5"] = train
+    if il is not None:
+        line["interleave"] = il
     if frox is not None:
         line["froxelize"] = frox
     if gtp is not None:

@@ -50,8 +50,8 @@ extern "C" {
 #endif
 
 enum { FPVS_OK = 0, FPVS_EINVAL = 1, FPVS_ESHAPE = 2, FPVS_ECUDA = 3 };
-enum { FPVS_IN_PACKED = 0, FPVS_IN_U8 = 1, FPVS_IN_F32 = 2 };
-enum { FPVS_F32 = 0, FPVS_BF16 = 1 };
+enum { FPVS_IN_PACKED = 0, FPVS_IN_U8 = 1, FPVS_IN_F32 = 2, FPVS_IN_F64 = 3 };
+enum { FPVS_F32 = 0, FPVS_BF16 = 1, FPVS_F64 = 2 };
 enum { FPVS_ACT_NONE = 0, FPVS_ACT_RELU = 1, FPVS_ACT_SIGMOID = 2, FPVS_ACT_MASK = 3 };
 
 const char* fpvs_last_error(void);
@@ -60,16 +60,22 @@ int fpvs_abi_version(void);
 /* ---- (1) interleave / deinterleave ------------------------------------ */
 
 /* Replaces interleave(grid, d) (interleave.py:54-65) for B grids at once.
- * in: packed bits, u8 or f32 dense; out: (B, Nx/d, Ny/d, Nz/d, d^3) f32/bf16;
- * cell_active (nullable): u8 (B, X, Y, Z), 1 iff the block holds a nonzero. */
+ * in: packed bits, u8, f32 or f64 dense; out: (B, Nx/d, Ny/d, Nz/d, d^3)
+ * f32/bf16 (the cast fused), or f64 for f64 input (an exact permutation, as
+ * the reference keeps an ndarray's dtype, interleave.py:45-51);
+ * cell_active (nullable): u8 (B, X, Y, Z), 1 iff the block holds a nonzero.
+ * d in {1, 2, 4, 8}: shared-memory tiled transpose with 16-byte loads and
+ * stores (HBM-bound); other d: a generic kernel. */
 int fpvs_interleave(const void* in, int in_fmt, int B, int Nx, int Ny, int Nz, int d,
                     void* out, int out_dtype, uint8_t* cell_active, void* stream);
 
 /* Replaces deinterleave(t, d, threshold) (interleave.py:68-85).
- * in: (B, X, Y, Z, d^3) f32/bf16.  If tau is NaN, out is f32 dense
- * (B, X*d, Y*d, Z*d); else out is packed bits of [value >= tau]. */
+ * in: (B, X, Y, Z, d^3) f32/bf16/f64.  If tau is NaN, out is dense
+ * (B, X*d, Y*d, Z*d): f64 for f64 cells (exact inverse), else f32; otherwise
+ * out is packed bits of [value >= tau], compared in the cells' precision
+ * (float64 for f64, float32 otherwise: numpy's comparison under NEP 50). */
 int fpvs_deinterleave(const void* in, int in_dtype, int B, int X, int Y, int Z, int d,
-                      float tau, void* out, void* stream);
+                      double tau, void* out, void* stream);
 
 /* ---- (2) kernel maps --------------------------------------------------- */
 

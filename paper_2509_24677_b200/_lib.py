@@ -15,8 +15,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FPVS_LIB", os.path.join(HERE, "libfpvs.so"))
 
-F32, BF16 = 0, 1
-IN_PACKED, IN_U8, IN_F32 = 0, 1, 2
+F32, BF16, F64 = 0, 1, 2
+IN_PACKED, IN_U8, IN_F32, IN_F64 = 0, 1, 2, 3
 EXCHANGE_TAIL = 10  # FPVS_EXCHANGE_TAIL
 ACT = {"none": 0, "relu": 1, "sigmoid": 2}
 
@@ -27,7 +27,7 @@ SIGNATURES = {
     "fpvs_last_error": (C.c_char_p, []),
     "fpvs_abi_version": (_i, []),
     "fpvs_interleave": (_i, [_p, _i, _i, _i, _i, _i, _i, _p, _i, _p, _p]),
-    "fpvs_deinterleave": (_i, [_p, _i, _i, _i, _i, _i, _i, _f, _p, _p]),
+    "fpvs_deinterleave": (_i, [_p, _i, _i, _i, _i, _i, _i, _d, _p, _p]),
     "fpvs_kmap_workspace_size": (_z, [_i, _i, _i, _i]),
     "fpvs_cell_active_from_bits": (_i, [_p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_kmap_compact": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _i, _p, _z, _p]),

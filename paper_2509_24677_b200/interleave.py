@@ -10,6 +10,10 @@ Mirrors pkg/src/froxelpvs/interleave.py:18-85:
   a threshold applies ``>= tau`` and returns a packed FroxelGrid
   (interleave.py:68-85).
 
+Values move exactly: float64 (and integer) arrays are permuted as 8-byte
+elements on the device, float32 and u8 as themselves, and a threshold is
+compared in the cells' own precision (float64 cells in float64).
+
 The arithmetic runs on the GPU (``fpvs_interleave`` / ``fpvs_deinterleave``).
 numpy/FroxelGrid inputs are copied to the device and the result copied back,
 so reference-style callers get numpy out; CUDA tensors stay on the device and
@@ -75,12 +79,16 @@ def interleave_device(grid, d: int, out_dtype=None, packed_dims=None, want_activ
         B, nx, ny, nz = grid.shape
         if grid.dtype in (torch.bool, torch.uint8):
             fmt, src = _lib.IN_U8, grid.to(torch.uint8).contiguous()
+        elif grid.dtype == torch.float64:
+            fmt, src = _lib.IN_F64, grid.contiguous()
         else:
             fmt, src = _lib.IN_F32, grid.to(torch.float32).contiguous()
     if d < 1 or nx % d or ny % d or nz % d:
         raise ValueError(f"interleave factor {d} must divide grid dims {(nx, ny, nz)}")
+    if fmt == _lib.IN_F64:
+        out_dtype = torch.float64  # exact permutation of the float64 values
     out_dtype = out_dtype or torch.float32
-    od = _lib.BF16 if out_dtype == torch.bfloat16 else _lib.F32
+    od = {torch.bfloat16: _lib.BF16, torch.float64: _lib.F64}.get(out_dtype, _lib.F32)
     out = torch.empty((B, nx // d, ny // d, nz // d, d ** 3), dtype=out_dtype, device=src.device)
     act = torch.empty((B, nx // d, ny // d, nz // d), dtype=torch.uint8, device=src.device) if want_active else None
     _lib.call("fpvs_interleave", _lib.ptr(src), fmt, B, nx, ny, nz, d, _lib.ptr(out), od, _lib.ptr(act),
@@ -103,7 +111,8 @@ def interleave(grid, d: int) -> ChannelTensor:
         if grid.dim() != 3:
             raise ValueError("expected a FroxelGrid or a dense 3D array")
         dt = grid.dtype
-        out = interleave_device(grid[None].cuda(), d, torch.float32)[0]
+        src = grid if dt in (torch.bool, torch.uint8, torch.float32, torch.float64) else grid.to(torch.float64)
+        out = interleave_device(src[None].cuda(), d, torch.float32)[0]
         return ChannelTensor(out.to(dt if dt.is_floating_point else torch.float32), d)
     arr = np.asarray(grid)
     if arr.ndim != 3:
@@ -111,12 +120,17 @@ def interleave(grid, d: int) -> ChannelTensor:
     nx, ny, nz = arr.shape
     if d < 1 or nx % d or ny % d or nz % d:
         raise ValueError(f"interleave factor {d} must divide grid dims {(nx, ny, nz)}")
+    # the reference keeps the input dtype (interleave.py:45-51), so the values
+    # must move unchanged: u8/bool and float32 travel as themselves, float64
+    # (and every other dtype, through float64: exact for integers < 2^53) as
+    # float64 — the device permutes the 8-byte elements exactly
     if arr.dtype in (np.bool_, np.uint8):
         src = torch.from_numpy(np.ascontiguousarray(arr.astype(np.uint8)))[None].cuda()
+    elif arr.dtype == np.float32:
+        src = torch.from_numpy(np.ascontiguousarray(arr))[None].cuda()
     else:
-        src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32))[None].cuda()
+        src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64))[None].cuda()
     out = interleave_device(src, d, torch.float32)[0].cpu().numpy()
-    # the reference keeps the input dtype (interleave.py:45-51); values are an exact permutation
     return ChannelTensor(out.astype(arr.dtype, copy=False), d)
 
 
@@ -127,11 +141,12 @@ def deinterleave_device(cells, d: int, threshold: float | None = None):
         raise ValueError(f"channel count {cells.shape[-1]} does not match d^3 = {d ** 3}")
     B, X, Y, Z, _ = cells.shape
     src = cells.contiguous()
-    if src.dtype not in (torch.float32, torch.bfloat16):
-        src = src.to(torch.float32)
-    dt = _lib.BF16 if src.dtype == torch.bfloat16 else _lib.F32
+    if src.dtype not in (torch.float32, torch.bfloat16, torch.float64):
+        src = src.to(torch.float64)
+    dt = {torch.bfloat16: _lib.BF16, torch.float64: _lib.F64}.get(src.dtype, _lib.F32)
     if threshold is None:
-        out = torch.empty((B, X * d, Y * d, Z * d), dtype=torch.float32, device=src.device)
+        odt = torch.float64 if src.dtype == torch.float64 else torch.float32
+        out = torch.empty((B, X * d, Y * d, Z * d), dtype=odt, device=src.device)
         tau = float("nan")
     else:
         if (X * d) % 8:
@@ -155,7 +170,10 @@ def deinterleave(tensor: ChannelTensor, d: int | None = None, threshold: float |
     on_host = not isinstance(vals, torch.Tensor)
     if on_host:
         arr = np.asarray(vals)
-        src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).cuda()
+        # float32 cells compare in float32 and float64 in float64, as the
+        # reference's numpy `values >= threshold` does (NEP 50)
+        keep = arr.dtype if arr.dtype in (np.float32, np.float64) else np.float64
+        src = torch.from_numpy(np.ascontiguousarray(arr, dtype=keep)).cuda()
     else:
         src = vals.cuda()
     if threshold is None:

@@ -81,3 +81,94 @@ def test_interleave_config_sizes_bit_exact():
         cells2, act2 = interleave_device(dense, d, torch.float32, want_active=True)
         assert np.array_equal(cells2[0].cpu().numpy(), ref)
         assert torch.equal(act2, act)
+
+
+def _np_interleave(a, d):
+    nx, ny, nz = a.shape[-3:]
+    lead = a.shape[:-3]
+    t = a.reshape(lead + (nx // d, d, ny // d, d, nz // d, d))
+    n = len(lead)
+    t = t.transpose(tuple(range(n)) + (n, n + 2, n + 4, n + 5, n + 3, n + 1))  # (X, Y, Z, lz, ly, lx)
+    return t.reshape(lead + (nx // d, ny // d, nz // d, d ** 3))
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("kind", ["u8", "f32", "f64"])
+def test_tiled_and_generic_paths_exact(d, kind):
+    """Every dtype x d on the tiled kernels (d in {1,2,4,8}, aligned) and the
+    generic ones (d = 3, odd N_z, misaligned views): exact permutations, exact
+    casts, the active mask, and the inverse."""
+    import torch
+    from paper_2509_24677_b200.interleave import deinterleave_device, interleave_device
+    rng = np.random.default_rng(40 + d)
+    for dims in ((2, 8 * d, 4 * d, 16 * d), (1, 8 * d, 2 * d, 3 * d)):
+        if kind == "u8":
+            host = (rng.random(dims) < 0.2).astype(np.uint8)
+            tdt = torch.uint8
+        elif kind == "f32":
+            host = (rng.random(dims) * (rng.random(dims) < 0.3)).astype(np.float32)
+            tdt = torch.float32
+        else:
+            host = rng.standard_normal(dims) * (rng.random(dims) < 0.3)
+            tdt = torch.float64
+        want = _np_interleave(host, d)
+        base = torch.from_numpy(host).cuda()
+        flat = torch.empty(base.numel() + 1, dtype=tdt, device="cuda")
+        views = [base, flat[1:].view(dims)]  # aligned and 1-element-misaligned (generic kernels)
+        views[1].copy_(base)
+        for src in views:
+            for odt in ((torch.float64,) if kind == "f64" else (torch.float32, torch.bfloat16)):
+                cells, act = interleave_device(src, d, odt, want_active=True)
+                got = cells.double().cpu().numpy()
+                assert np.array_equal(got, torch.from_numpy(want.astype(np.float64)).to(odt).double().numpy())
+                assert np.array_equal(act.cpu().numpy().astype(bool), want.any(-1))
+            back = deinterleave_device(interleave_device(src, d, torch.float64 if kind == "f64" else torch.float32),
+                                       d)
+            assert np.array_equal(back.cpu().numpy(), host.astype(back.cpu().numpy().dtype))
+
+
+def test_float64_threshold_exact_near_tau():
+    """float64 cells within 1e-8 of tau keep the reference's float64
+    comparison (values just below tau stay clear), and float64 arrays
+    interleave to float64 exactly."""
+    from paper_2509_24677_b200.interleave import ChannelTensor, deinterleave, interleave
+    rng = np.random.default_rng(3)
+    vals = 0.5 + rng.choice([-1e-9, -1e-12, 0.0, 1e-12, 5e-9], size=(8, 4, 4, 8))
+    for d, shape in ((2, (8, 4, 4, 8)),):
+        t = ChannelTensor(vals.reshape(shape), d)
+        got = deinterleave(t, d, threshold=0.5).to_dense()
+        want = _np_inverse(vals, d) >= 0.5
+        assert np.array_equal(got, want) and got.sum() > 0 and (~got).sum() > 0
+    dense = rng.standard_normal((16, 8, 24))
+    t = interleave(dense, 4)
+    assert t.values.dtype == np.float64 and np.array_equal(t.values, _np_interleave(dense, 4))
+    assert np.array_equal(deinterleave(t, 4), dense)
+    ints = rng.integers(-2 ** 40, 2 ** 40, (8, 8, 8))
+    ti = interleave(ints, 2)
+    assert ti.values.dtype == ints.dtype and np.array_equal(ti.values, _np_interleave(ints, 2))
+
+
+def _np_inverse(cells, d):
+    X, Y, Z, _ = cells.shape
+    t = cells.reshape(X, Y, Z, d, d, d).transpose(0, 5, 1, 4, 2, 3)  # (X, lx, Y, ly, Z, lz)
+    return t.reshape(X * d, Y * d, Z * d)
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 8])
+def test_deinterleave_threshold_word_and_byte_paths(d):
+    """Packed [p >= tau] via the 32-bit word kernel (N_x % 32 == 0) and the byte
+    kernel (N_x % 32 != 0), bf16 / f32 / f64 cells."""
+    import torch
+    from paper_2509_24677_b200.interleave import deinterleave_device
+    rng = np.random.default_rng(d)
+    for nx in (32 * d, 8 * d if d < 4 else 8 * d + 8 * (d == 4)):
+        if nx % d:
+            continue
+        cells = rng.random((2, nx // d, 3, 2, d ** 3))
+        dense = np.stack([_np_inverse(c, d) for c in cells])
+        for dt in (torch.float32, torch.bfloat16, torch.float64):
+            ct = torch.from_numpy(cells).to(dt).cuda()
+            bits = deinterleave_device(ct, d, 0.5).cpu().numpy()
+            ref_dense = torch.from_numpy(dense).to(dt).double().numpy() >= 0.5
+            want = np.concatenate([FroxelGrid.from_dense(g).bits for g in ref_dense])
+            assert np.array_equal(bits, want), (nx, dt)
