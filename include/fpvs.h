@@ -165,6 +165,11 @@ typedef struct fpvs_level {
   uint32_t* down_masks;
   int32_t* up;
   uint32_t* up_masks;
+  /* nullable: the halo-cached conv's per-tile tables of this level's 3^3 map
+   * (as fpvs_kmap_halo writes them), built in the same launch as the map */
+  int32_t* halo_rows;
+  int32_t* halo_n;
+  int16_t* halo_lnbr;
 } fpvs_level;
 
 size_t fpvs_levels_workspace_size(int B, int Nx, int Ny, int Nz, int d, int nlev);

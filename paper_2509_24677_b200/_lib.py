@@ -106,7 +106,8 @@ SIGNATURES = {
 class Level(C.Structure):
     """struct fpvs_level (include/fpvs.h)."""
     _fields_ = [("coords", _p), ("index_vol", _p), ("n", _p), ("cap", _i), ("nbr", _p), ("nbr_masks", _p),
-                ("down", _p), ("down_masks", _p), ("up", _p), ("up_masks", _p)]
+                ("down", _p), ("down_masks", _p), ("up", _p), ("up_masks", _p), ("halo_rows", _p), ("halo_n", _p),
+                ("halo_lnbr", _p)]
 
 
 class Frustum(C.Structure):

@@ -24,6 +24,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "halo_build.cuh"
 
 namespace fpvs {
 namespace lv {
@@ -46,6 +47,9 @@ struct LevelDev {
   uint32_t* down_masks;
   int* up;
   uint32_t* up_masks;
+  int* halo_rows;     // nullable: per-tile halo tables (halo_build.cuh) of the 3^3 map
+  int* halo_n;
+  int16_t* halo_lnbr;
   int X, Y, Z;
   int ntiles;         // K2 scan tiles
   unsigned* status;   // [ntiles] look-back flags, then 1 tile counter
@@ -281,7 +285,7 @@ __device__ __forceinline__ uint32_t subm_row(const LevelDev& L, const int4 c, in
 
 // 128 rows x 27: thread t handles row t%128, offsets [0,14) or [14,27); the
 // tile is staged in shared memory and leaves as coalesced 16-byte stores
-__device__ void subm_unit(const LevelDev& L, int n, int tile, int* s_tab, uint32_t* s_red) {
+__device__ void subm_unit(const LevelDev& L, int n, int tile, int* s_tab, uint32_t* s_red, halob::Smem* s_halo) {
   const int r0 = tile * kRows;
   const int rows = min(kRows, n - r0);
   const int row = threadIdx.x & (kRows - 1);
@@ -301,6 +305,12 @@ __device__ void subm_unit(const LevelDev& L, int n, int tile, int* s_tab, uint32
   }
   if (L.nbr_masks) block_or_store(m, s_red, L.nbr_masks + tile);
   else __syncthreads();  // s_tab is reused by the next unit
+  if (L.halo_rows) {
+    // the tile's halo list and local table straight from the staged rows
+    halob::build_tile([&](int e) { return e / 27 < rows ? s_tab[e] : -1; }, *s_halo,
+                      L.halo_rows + (long long)tile * halob::kHmax, L.halo_n + tile,
+                      L.halo_lnbr + (long long)tile * kRows * 27);
+  }
 }
 
 // down table of level l (rows of l) into level l-1
@@ -419,6 +429,7 @@ constexpr int kClearChunk = kThreads * 64;  // bytes per clear unit
 __global__ void __launch_bounds__(kThreads) tables_kernel(const Args a) {
   __shared__ uint32_t s_red[kThreads / 32];
   __shared__ __align__(16) int s_tab[kRows * 27];
+  __shared__ __align__(16) halob::Smem s_halo;
   __shared__ int s_pre[T_COUNT * kMaxLev + 1];  // unit prefix per (task, level)
   __shared__ int s_nl[kMaxLev];
   if (threadIdx.x < kMaxLev) s_nl[threadIdx.x] = (int)threadIdx.x < a.nlev ? nrows(a.L[threadIdx.x]) : 0;
@@ -455,7 +466,7 @@ __global__ void __launch_bounds__(kThreads) tables_kernel(const Args a) {
     const int idx = __popc(__ballot_sync(0xffffffffu, le)) - 1;
     const int t = idx / kMaxLev, l = idx % kMaxLev, k = u - s_pre[idx];
     switch (t) {
-      case T_SUBM: subm_unit(a.L[l], nl[l], k, s_tab, s_red); break;
+      case T_SUBM: subm_unit(a.L[l], nl[l], k, s_tab, s_red, &s_halo); break;
       case T_DOWN: down_unit(a.L[l], a.L[l - 1], nl[l], k, s_red); break;
       case T_UP: up_unit(a.L[l], a.L[l - 1], nl[l - 1], k, s_red); break;
       case T_GATHER: gather_unit(a, nl[0], k); break;
@@ -561,6 +572,10 @@ extern "C" int fpvs_levels_from_bits(const uint8_t* bits, int B, int Nx, int Ny,
     L.down_masks = h.down_masks;
     L.up = h.up;
     L.up_masks = h.up_masks;
+    FPVS_CHECK_ARG(!h.halo_rows || (h.halo_n && h.halo_lnbr && h.nbr), "level %d: halo tables need nbr, n, lnbr", l);
+    L.halo_rows = h.halo_rows;
+    L.halo_n = h.halo_n;
+    L.halo_lnbr = h.halo_lnbr;
     L.X = X >> l; L.Y = Y >> l; L.Z = Z >> l;
     const long long nc = (long long)B * L.X * L.Y * L.Z;
     L.ntiles = (int)((nc + lv::kTileCells - 1) / lv::kTileCells);

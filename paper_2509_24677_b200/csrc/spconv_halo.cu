@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
+#include "halo_build.cuh"
 
 namespace fpvs {
 namespace halo {
@@ -43,7 +44,6 @@ constexpr int LNBR_BYTES = BM * KOFF * 2;   // int16 [128][27]
 constexpr int HALO_BYTES = HMAX * 128;      // one 64-channel chunk of every halo row
 constexpr int ROWS_OFF = HALO_BYTES + LNBR_BYTES;   // the tile's halo row list (int32 [HMAX])
 constexpr int HBUF = (ROWS_OFF + HMAX * 4 + 1023) / 1024 * 1024;
-constexpr int WIN_WORDS = 512;              // 16384-row window of the build (wider tiles read directly)
 
 // ------------------------------------------------------------------------
 // Halo build: per 128-row tile, the sorted distinct neighbour rows and the
@@ -67,14 +67,10 @@ struct HaloJobs {
 // One launch for every level's table: CTA b takes active tiles b, b + grid, ...
 // of the concatenated (level, tile) space (counts read on the device).
 __global__ void __launch_bounds__(256) halo_build_kernel(const HaloJobs J) {
-  __shared__ __align__(16) uint8_t s_flag[WIN_WORDS * 32];
-  __shared__ uint32_t s_bits[WIN_WORDS];
-  __shared__ int s_pre[WIN_WORDS];
-  __shared__ int s_red[2][8];
-  __shared__ int s_wsum[8];
+  __shared__ __align__(16) halob::Smem s;
   __shared__ int s_base[kMaxHaloJobs + 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
+  pdl_wait();  // the neighbour tables are the previous launch's output
+  if (threadIdx.x == 0) {
     int acc = 0;
     for (int l = 0; l < J.count; ++l) {
       s_base[l] = acc;
@@ -90,114 +86,9 @@ __global__ void __launch_bounds__(256) halo_build_kernel(const HaloJobs J) {
     const int t = tt - s_base[l];
     const int* __restrict__ nbr = J.j[l].nbr;
     const int n = min(*J.j[l].n, J.j[l].cap);
-    int* __restrict__ halo_rows = J.j[l].rows;
-    int16_t* __restrict__ lnbr = J.j[l].lnbr;
     const long long row0 = (long long)t * BM;
-    constexpr int PER = (BM * KOFF + 255) / 256;
-    int vals[PER];
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int e = tid + 256 * k;
-      vals[k] = (e < BM * KOFF && row0 + e / KOFF < n) ? __ldg(nbr + row0 * KOFF + e) : -1;
-    }
-    int lo = INT_MAX, hi = -1;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      if (vals[k] >= 0) {
-        lo = min(lo, vals[k]);
-        hi = max(hi, vals[k]);
-      }
-    }
-    for (int o = 16; o; o >>= 1) {
-      lo = min(lo, __shfl_xor_sync(~0u, lo, o));
-      hi = max(hi, __shfl_xor_sync(~0u, hi, o));
-    }
-    if (lane == 0) {
-      s_red[0][warp] = lo;
-      s_red[1][warp] = hi;
-    }
-    __syncthreads();
-    lo = INT_MAX;
-    hi = -1;
-    for (int w = 0; w < 8; ++w) {
-      lo = min(lo, s_red[0][w]);
-      hi = max(hi, s_red[1][w]);
-    }
-    const bool win = hi >= 0 && hi - lo < WIN_WORDS * 32;
-    const int nw = win ? ((hi - lo) >> 5) + 1 : 0;
-    // mark the window rows with plain byte stores (no atomics: equal values),
-    // then fold 32 flags into one bitmap word per thread
-    for (int i = tid; i < nw * 2; i += 256) reinterpret_cast<uint4*>(s_flag)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    if (win) {
-#pragma unroll
-      for (int k = 0; k < PER; ++k)
-        if (vals[k] >= 0) s_flag[vals[k] - lo] = 1;
-    }
-    __syncthreads();
-    for (int w = tid; w < nw; w += 256) {
-      const uint4 a = reinterpret_cast<const uint4*>(s_flag)[2 * w];
-      const uint4 b = reinterpret_cast<const uint4*>(s_flag)[2 * w + 1];
-      const uint32_t q[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      uint32_t m = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        // bytes are 0/1: gather bit 0 of each byte
-        const uint32_t v = q[i];
-        m |= ((v & 1u) | ((v >> 7) & 2u) | ((v >> 14) & 4u) | ((v >> 21) & 8u)) << (4 * i);
-      }
-      s_bits[w] = m;
-    }
-    __syncthreads();
-    // exclusive scan of the word popcounts (one word per thread per round) and
-    // the sorted halo list: word w's set bits are rows lo + 32 w + b
-    int* hr = halo_rows + (long long)t * HMAX;
-    int H = 0;
-    for (int base = 0; base < nw; base += 256) {
-      const int w = base + tid;
-      const uint32_t bw = w < nw ? s_bits[w] : 0u;
-      const int c = __popc(bw);
-      int incl = c;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(~0u, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (lane == 31) s_wsum[warp] = incl;
-      __syncthreads();
-      int woff = 0, rtot = 0;
-      for (int i = 0; i < 8; ++i) {
-        if (i < warp) woff += s_wsum[i];
-        rtot += s_wsum[i];
-      }
-      int rk = H + woff + incl - c;
-      if (w < nw) s_pre[w] = rk;
-      uint32_t bits = bw;
-      while (bits && rk < HMAX) {
-        hr[rk++] = lo + w * 32 + (__ffs(bits) - 1);
-        bits &= bits - 1;
-      }
-      H += rtot;
-      __syncthreads();
-    }
-    if (tid == 0) J.j[l].hn[t] = win ? min(H, HMAX) : 0;
-    int16_t* ln = lnbr + (long long)t * BM * KOFF;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int e = tid + 256 * k;
-      if (e >= BM * KOFF) break;
-      const int v = vals[k];
-      int o = -1;
-      if (v >= 0) {
-        o = -2;
-        if (win) {
-          const int dd = v - lo;
-          const int rk = s_pre[dd >> 5] + __popc(s_bits[dd >> 5] & ((1u << (dd & 31)) - 1u));
-          if (rk < HMAX) o = rk;
-        }
-      }
-      ln[e] = (int16_t)o;
-    }
-    __syncthreads();
+    halob::build_tile([&](int e) { return row0 + e / KOFF < n ? __ldg(nbr + row0 * KOFF + e) : -1; }, s,
+                      J.j[l].rows + (long long)t * HMAX, J.j[l].hn + t, J.j[l].lnbr + (long long)t * BM * KOFF);
   }
 }
 
@@ -242,7 +133,8 @@ __device__ long long g_hclk[2][160];
   do {                                                                                   \
     if (p.dbg && blockIdx.x - (unsigned)(p.dbg >> 8) < 2u && (slot) < 8192) {          \
       unsigned long long t_;                                                             \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+      if (p.dbg & 128) t_ = clock64();                                                   \
+      else asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
       g_hts[blockIdx.x - (p.dbg >> 8)][(slot)] = t_;                                     \
     }                                                                                    \
   } while (0)
@@ -473,9 +365,15 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
 
   if (warp < W_LOAD) {
     // ===================== A builders =====================
-    // group bg builds chunk slot bg of every stage (chunks i with i % 2 == bg)
+    // group bg builds half of every stage's chunk slots: with G >= 2 the
+    // group owns slots [bg G/2, (bg + 1) G/2) and builds its (up to) two
+    // chunks of a stage together — both chunks' halo reads in flight at once,
+    // one empty-wait, two TMEM stores, one store-wait and one counted arrival
+    // (measured: a builder's per-chunk sync, not its shared-memory traffic,
+    // paced the N = 64 layers); with G = 1 the groups alternate stages.
     pdl_wait();  // the direct-read path reads x (the previous launch's output)
     const int bg = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
+    auto grp = [](int i) { return C::G >= 2 ? ((i % C::G) >= C::G / 2 ? 1 : 0) : (i & 1); };
     const uint32_t t_a = tmem_base + ((uint32_t)(q4 * 32) << 16) + C::ACOL;
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u;
     uint32_t sc0 = 0, gc = 0;
@@ -513,7 +411,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         int j = first_offset(U.mask, qs - c * U.npres);
         for (int q = qs; q < qe; ++q, j = next_offset(U.mask, j)) {
           const int i = q - U.q0;
-          if ((i & 1) != bg) continue;
+          if (grp(i) != bg) continue;
           const uint32_t st = sc0 + i / C::G;
           const int stage = (int)(st % C::NS);
           uint32_t v[32];
@@ -545,30 +443,60 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
               }
             }
           } else {
-          const int li = ABL(17) ? -1 : ln[j];
-          if (li >= 0) {
-            const uint8_t* src = hbuf + li * 128;
-            const int sw = li & 7;
+            if (lane == 0 && q4 == 0 && st < 300) HTS(5400 + 2 * st + bg);
+            auto load = [&](int jj, uint32_t (&vv)[32]) {
+              const int li = ABL(17) ? -1 : ln[jj];
+              if (li >= 0) {
+                const uint8_t* src = hbuf + li * 128;
+                const int sw = li & 7;
 #pragma unroll
-            for (int pc = 0; pc < 8; ++pc) {
-              const uint4 t4 = *reinterpret_cast<const uint4*>(src + ((pc ^ sw) << 4));
-              v[4 * pc] = t4.x; v[4 * pc + 1] = t4.y; v[4 * pc + 2] = t4.z; v[4 * pc + 3] = t4.w;
+                for (int pc = 0; pc < 8; ++pc) {
+                  const uint4 t4 = *reinterpret_cast<const uint4*>(src + ((pc ^ sw) << 4));
+                  vv[4 * pc] = t4.x; vv[4 * pc + 1] = t4.y; vv[4 * pc + 2] = t4.z; vv[4 * pc + 3] = t4.w;
+                }
+              } else if (li == -1) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) vv[k] = 0u;
+              } else {
+                const int g = __ldg(p.nbr + ((long long)U.mt * BM + r) * KOFF + jj);
+                const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(p.x) +
+                                                                  (long long)g * ldx2 + c * 128);
+#pragma unroll
+                for (int pc = 0; pc < 8; ++pc) {
+                  const uint4 t4 = __ldg(src + pc);
+                  vv[4 * pc] = t4.x; vv[4 * pc + 1] = t4.y; vv[4 * pc + 2] = t4.z; vv[4 * pc + 3] = t4.w;
+                }
+              }
+            };
+            const int slot = i % C::G;
+            // the group's second chunk of this stage, when it is in this range
+            const bool two = C::G >= 2 && q + 1 < qe && slot + 1 < C::G && grp(i + 1) == bg;
+            uint32_t w[32];
+            const int j2 = two ? next_offset(U.mask, j) : j;
+            load(j, v);
+            if (two) load(j2, w);
+            if (lane == 0 && q4 == 0 && st < 400) HTS(2000 + 2 * st + bg);
+            mbar_wait(smem_u32(empty + stage), ((st / C::NS) & 1) ^ 1);
+            if (lane == 0 && q4 == 0 && st < 400) HTS(2800 + 2 * st + bg);
+            tc_fence_after();
+            if (!ABL(18)) {
+              tmem_st32(t_a + (stage * C::G + slot) * 32, v);
+              if (two) tmem_st32(t_a + (stage * C::G + slot + 1) * 32, w);
+              tmem_st_wait();
             }
-          } else if (li == -1) {
-#pragma unroll
-            for (int k = 0; k < 32; ++k) v[k] = 0u;
-          } else {
-            const int g = __ldg(p.nbr + ((long long)U.mt * BM + r) * KOFF + j);
-            const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(p.x) +
-                                                              (long long)g * ldx2 + c * 128);
-#pragma unroll
-            for (int pc = 0; pc < 8; ++pc) {
-              const uint4 t4 = __ldg(src + pc);
-              v[4 * pc] = t4.x; v[4 * pc + 1] = t4.y; v[4 * pc + 2] = t4.z; v[4 * pc + 3] = t4.w;
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cnt(smem_u32(full + stage), two ? 2u : 1u);
+            if (lane == 0 && q4 == 0 && st < 1400) HTS(1024 + 2 * st + bg);
+            if (two) {
+              ++q;  // the partner chunk is done; the loop increment moves past it
+              j = j2;
             }
+            continue;
           }
-          }
+          if (lane == 0 && q4 == 0 && st < 400) HTS(2000 + 2 * st + bg);
           mbar_wait(smem_u32(empty + stage), ((st / C::NS) & 1) ^ 1);
+          if (lane == 0 && q4 == 0 && st < 400) HTS(2800 + 2 * st + bg);
           tc_fence_after();
           if (!ABL(18)) {
             tmem_st32(t_a + (stage * C::G + i % C::G) * 32, v);
@@ -585,12 +513,12 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       }
       const uint32_t nst = (nq + C::G - 1) / C::G;
       if (C::G > 1 && nq % C::G) {
-        // the unit's last stage is short: its missing slots (built by group
-        // slot & 1, as chunk i goes to group i & 1 and slot i % G) still arrive
+        // the unit's last stage is short: its missing slots (owned by group
+        // grp(slot)) still arrive
         const uint32_t st = sc0 + nst - 1;
         bool waited = false;
         for (int sl = nq % C::G; sl < C::G; ++sl) {
-          if ((sl & 1) != bg) continue;
+          if (grp(sl) != bg) continue;
           if (!waited) {
             mbar_wait(smem_u32(empty + st % C::NS), ((st / C::NS) & 1) ^ 1);
             waited = true;
@@ -688,6 +616,8 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     // ===================== MMA issuer =====================
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16<BN>();
+      const uint32_t a_base = tmem_base + C::ACOL;
+      const uint64_t b_desc0 = sw128_desc(smem_u32(sB));
       uint32_t st = 0;
       int it = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
@@ -701,21 +631,38 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         HTS(7000 + 2 * it);
         tc_fence_after();
         const uint32_t dtm = tmem_base + acc * BN;
+        // The issue loop is on the critical path of every MMA (tcgen05.mma
+        // issue is effectively synchronous at N <= 128): any dependent scalar
+        // work between two MMAs adds straight to their cost (measured
+        // tools/micro_commit2.cu: 47 -> 89 cycles per N = 64 MMA with one
+        // division in the loop).  So a stage's A / B addresses are affine in
+        // the stage index (bases hoisted out of all loops) and a full stage is
+        // one fully unrolled run of G x 4 MMAs with immediate offsets; only the
+        // unit's first MMA clears the accumulator.
         for (int i = 0; i < nq; i += C::G, ++st) {
           const int stage = (int)(st % C::NS);
           const int nv = min(C::G, nq - i);
+          if (st < 400) HTS(3600 + st);
           mbar_wait(smem_u32(full + stage), (st / C::NS) & 1);
           if (st < 450) HTS(4096 + 2 * st);
           tc_fence_after();
-          for (int g = 0; g < nv; ++g) {
-            const uint32_t ta = tmem_base + C::ACOL + (stage * C::G + g) * 32;
-            const uint64_t bd = sw128_desc(smem_u32(sB + stage * C::STAGE_B + g * C::B_SUB));
-            if (!ABL(20)) {
+          const uint32_t ta0 = a_base + (uint32_t)stage * (C::G * 32);
+          const uint64_t bd0 = b_desc0 + (uint64_t)((uint32_t)stage * (C::STAGE_B >> 4));
+          if (!ABL(20)) {
+            if (nv == C::G) {
 #pragma unroll
-              for (int k = 0; k < BK / 16; ++k)
-                umma_bf16_ts(dtm, ta + 8 * k, bd + 2 * k, idesc, (i == 0 && g == 0 && k == 0) ? 0u : 1u);
+              for (int g = 0; g < C::G; ++g)
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  umma_bf16_ts(dtm, ta0 + g * 32 + 8 * k, bd0 + (uint64_t)(g * (C::B_SUB >> 4) + 2 * k), idesc,
+                               (g == 0 && k == 0) ? (i != 0 ? 1u : 0u) : 1u);
+            } else {
+              for (int g = 0; g < nv; ++g)
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  umma_bf16_ts(dtm, ta0 + g * 32 + 8 * k, bd0 + (uint64_t)(g * (C::B_SUB >> 4) + 2 * k), idesc,
+                               (i == 0 && g == 0 && k == 0) ? 0u : 1u);
             }
-            if (st < 200) HTS(6000 + 4 * st + g);
           }
           umma_commit(smem_u32(empty + stage));
           if (st < 450) HTS(4097 + 2 * st);
@@ -906,7 +853,8 @@ extern "C" int fpvs_kmap_halo_multi(const fpvs_halo_job* jobs, int njobs, void* 
   }
   if (tiles == 0) return FPVS_OK;
   const int grid = (int)(tiles < 4 * kNumSMs ? tiles : 4 * kNumSMs);
-  halo::halo_build_kernel<<<grid, 256, 0, as_stream(stream)>>>(J);
+  cudaError_t e = launch_kernel(halo::halo_build_kernel, dim3(grid), dim3(256), 0, as_stream(stream), J);
+  if (e != cudaSuccess) return set_error(FPVS_ECUDA, "fpvs_kmap_halo: %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("fpvs_kmap_halo");
   return FPVS_OK;
 }

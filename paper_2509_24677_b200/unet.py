@@ -129,11 +129,14 @@ class UNetPlan:
         self.t1a, self.t1b, self.buf1 = e(k1, c1), e(k1, c1), e(k1, 2 * c1)
         self.t2a, self.t2b = e(k2, c2), e(k2, c2)
         self.bn = {}  # per-layer output-tile width (0 = auto from Cout); see tune()
-        self.maps = sp.LevelMaps([self.L0, self.L1, self.L2], [self.down01, self.down12], [self.up10, self.up21],
-                                 self.grid_dims, d) if d in (1, 2, 4, 8) else None
         # 27-tap layers with 64-multiple channels run the halo-cached kernel
         # (fpvs_spconv_halo); FPVS_HALO=0 keeps them on the plain gather-GEMM
         self.use_halo = net.precision == "bf16" and os.environ.get("FPVS_HALO", "1") != "0"
+        # the level-0 halo tables (needed by the first conv) come out of the
+        # fused map build itself; levels 1 and 2 get theirs on the side stream
+        self.maps = sp.LevelMaps([self.L0, self.L1, self.L2], [self.down01, self.down12], [self.up10, self.up21],
+                                 self.grid_dims, d, halo_levels=(0,) if self.use_halo else ()) \
+            if d in (1, 2, 4, 8) else None
         self.level_of = {"enc0a": self.L0, "enc0b": self.L0, "dec0a": self.L0, "dec0b": self.L0,
                          "enc1a": self.L1, "enc1b": self.L1, "dec1a": self.L1, "dec1b": self.L1,
                          "enc2a": self.L2, "enc2b": self.L2}
@@ -212,7 +215,8 @@ class UNetPlan:
             if self._halo_builder is None:
                 self._halo_builder = sp.HaloBuilder([self.L0])
                 self._halo_builder_coarse = sp.HaloBuilder([self.L1, self.L2])
-            self._halo_builder.run()  # level 0: needed by the first conv
+            if self.maps is None:
+                self._halo_builder.run()  # level 0: needed by the first conv (else built by the fused maps)
         # the up-sort tables and the level-1/2 halo tables are first used by
         # enc1a / up21: with ``overlap`` they run on a side stream, filling SMs
         # the level-0 convs leave idle at their tails (joined before enc1a)
