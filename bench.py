@@ -35,6 +35,9 @@ halo tables), sparse interleave, 14 convs, head.
   per GPU, bf16 + fp32 master weights, AdamW; a step = forward + loss +
   tcgen05 backward + ONE all-reduce of [gradient | loss, counts] (NCCL under
   torchrun) + update, timed with CUDA events, max over ranks.
+* ``config4`` (side line, N=1): BASELINE config 4's density sweep with the
+  cuDNN dense-conv crossover comparator.
+* ``interleave`` (side line, N=1): north_star (1)'s standalone kernels, GB/s.
 * ``froxelize`` / ``gt_pvs`` (side lines, N=1): SURVEY §8(f) #1 / #3.
 
 Multi-GPU: one process per GPU.  ``--gpus N`` with N > 1 outside torchrun
@@ -472,6 +475,115 @@ def interleave_side(reps: int = 20):
     return out
 
 
+def config4_line(flush, densities=(0.005, 0.02, 0.08, 0.25), reps: int = 10):
+    """BASELINE config 4: the config-1 net (bf16) on 256^3 grids at swept
+    occupancy — per-stage device time inside the L2-flushed frame
+    (pipeline.frame_stage_times), HBM GB/s of the map stage and TFLOP/s of the
+    convs — beside a DENSE comparator: the same network as cuDNN bf16 conv3d
+    over the whole 128^3 x 8 interleaved grid (channels-last, the reference's
+    dense semantics, torch.nn.functional.conv3d; used only as the crossover
+    comparator, never on the product path).  ``crossover_density``: where the
+    sparse frame time reaches the dense one (log-linear interpolation)."""
+    import torch
+    import torch.nn.functional as F
+    from paper_2509_24677_b200 import synth
+    from paper_2509_24677_b200.froxel import FroxelGrid
+    from paper_2509_24677_b200.interleave import interleave_device
+    from paper_2509_24677_b200.neural import ModelConfig, PvsNet
+    from paper_2509_24677_b200.pipeline import FramePipeline, frame_stage_times, no_gc
+    hbm, tf_peak, _ = peaks()
+    net = PvsNet(ModelConfig.config1(), np.random.Generator(np.random.PCG64(0)), precision="bf16")
+    torch.backends.cudnn.benchmark = True
+    wts = []
+    for L in net.layers:
+        k, cin, cout = L.spec.kernel, L.spec.in_channels, L.spec.out_channels
+        w = L.w.reshape(k, k, k, cin, cout).permute(4, 3, 0, 1, 2).contiguous().to(torch.bfloat16)
+        wts.append((w.to(memory_format=torch.channels_last_3d), L.b.to(torch.bfloat16), k // 2, L.spec.activation))
+
+    def dense_net(x):
+        for w, b, pad, act in wts:
+            x = F.conv3d(x, w, b, padding=pad)
+            x = torch.relu_(x) if act == "relu" else torch.sigmoid(x)
+        return x
+
+    def timed_graph(body, captured=False):
+        body()
+        torch.cuda.synchronize()
+        g = None
+        if not captured:
+            g = torch.cuda.CUDAGraph()
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st), no_gc():
+                with torch.cuda.graph(g, stream=st):
+                    body()
+            torch.cuda.current_stream().wait_stream(st)
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay() if g is not None else body()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        del g
+        return statistics.median(ts)
+
+    rows = []
+    dense_ms = None
+    for dens in densities:
+        occ = synth.config4_grid(dens)
+        bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+        pipe = FramePipeline(net, 1, occ.shape, graph=True)
+        pipe.load(bits)
+        pipe.capture()
+        frame = timed_graph(pipe.run_device, captured=True)
+        stages, _ = frame_stage_times(pipe.plan, pipe.in_bits, pipe.out_bits, 0.5, flush=flush, reps=reps)
+        n = pipe.plan.L0.count()
+        lf = pipe.plan.layer_flops()
+        conv_ms = sum(stages[k] for k in lf if k != "head")
+        conv_fl = sum(v for k, v in lf.items() if k != "head")
+        cells = pipe.plan.L0.ncells
+        map_bytes = occ.size // 8 + 7 * cells + 124 * n + n * 8 * 2
+        if dense_ms is None:
+            x = interleave_device(bits, 2, torch.bfloat16, packed_dims=(1,) + occ.shape)  # (1, X, Y, Z, 8)
+            xd = x.permute(0, 4, 1, 2, 3).contiguous(memory_format=torch.channels_last_3d)
+            dense_ms = timed_graph(lambda: dense_net(xd))
+            dense_flops = 2 * cells * sum(L.spec.kernel ** 3 * L.spec.in_channels * L.spec.out_channels
+                                          for L in net.layers)
+        rows.append({"density": float(occ.mean()), "target": dens, "active_cells": n, "cells": cells,
+                     "frame_us": round(frame * 1e3, 1),
+                     "maps_us": round(stages["maps"] * 1e3, 1),
+                     "maps_gbs": round(map_bytes / (stages["maps"] * 1e-3) / 1e9, 1),
+                     "maps_hbm_frac": round(map_bytes / (stages["maps"] * 1e-3) / 1e9 / hbm, 3),
+                     "conv_us": round(conv_ms * 1e3, 1),
+                     "conv_tflops": round(conv_fl / (conv_ms * 1e-3) / 1e12, 1),
+                     "conv_tensor_frac": round(conv_fl / (conv_ms * 1e-3) / 1e12 / tf_peak, 3),
+                     "head_us": round(stages["head"] * 1e3, 1),
+                     "sparse_over_dense": round(frame / dense_ms, 3)})
+    cross = None
+    for a, b in zip(rows, rows[1:]):
+        ra, rb = a["frame_us"] / (dense_ms * 1e3), b["frame_us"] / (dense_ms * 1e3)
+        if ra < 1.0 <= rb:
+            la, lb = np.log(a["density"]), np.log(b["density"])
+            cross = float(np.exp(la + (np.log(1.0) - np.log(ra)) / (np.log(rb) - np.log(ra)) * (lb - la)))
+    # sparse frame time is close to affine in the active-cell count: extrapolate
+    # where it would reach the dense frame (as a fraction of all cells active)
+    na = np.array([r["active_cells"] for r in rows], np.float64)
+    fu = np.array([r["frame_us"] for r in rows], np.float64)
+    slope, icpt = np.polyfit(na, fu, 1)
+    n_star = (dense_ms * 1e3 - icpt) / slope if slope > 0 else float("inf")
+    return {"workload": "config4: config-1 net (bf16) on 256^3 grids, d = 2 -> 128^3 cells",
+            "crossover_active_fraction_extrapolated": round(float(n_star / rows[0]["cells"]), 3)
+            if "cells" in rows[0] else None,
+            "dense_comparator": "cuDNN bf16 conv3d (torch.nn.functional.conv3d, channels-last) over all 128^3 cells",
+            "dense_frame_us": round(dense_ms * 1e3, 1),
+            "dense_tflops": round(dense_flops / (dense_ms * 1e-3) / 1e12, 1), "sweep": rows,
+            "crossover_density": cross if cross is not None else
+            ("sparse faster at every swept density" if rows[-1]["sparse_over_dense"] < 1 else "dense faster at every swept density")}
+
+
 def froxelize_side(reps: int = 20):
     """fpvs_froxelize of a seeded triangle scene into the 256^3
     grid (supersample 4, linear depth) — device time per call from a CUDA graph
@@ -724,8 +836,11 @@ def run_ours(args):
     if ws == 1 and not args.no_froxelize:
         frox = froxelize_side()
         gtp = gt_pvs_side()
+    c4 = None
     if ws == 1:
         il = interleave_side()
+        if not args.no_config4:
+            c4 = config4_line(flush)
     if ws == 1 and not args.no_cpu_baseline:
         cores = cpu_threads()
         t_cpu = cpu_frame_time(occ)
@@ -770,6 +885,8 @@ def run_ours(args):
         line["train_config5"] = train
     if il is not None:
         line["interleave"] = il
+    if c4 is not None:
+        line["config4"] = c4
     if frox is not None:
         line["froxelize"] = frox
     if gtp is not None:
@@ -789,6 +906,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the config-5 training-step line")
     ap.add_argument("--no-config3", action="store_true", help="skip the config-3 sharded-batch line")
+    ap.add_argument("--no-config4", action="store_true", help="skip the config-4 density sweep / dense crossover line")
     ap.add_argument("--no-froxelize", action="store_true", help="skip the froxelization / GT-PVS side lines")
     ap.add_argument("--selftest", action="store_true", help="CPU/gloo check of the multi-rank plumbing")
     args = ap.parse_args()

@@ -374,6 +374,8 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
     // the final barrier.
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16<BN>();
+      const uint64_t a_desc0 = sw128_desc(smem_u32(sA));
+      const uint64_t b_desc0 = sw128_desc(smem_u32(sB));
       int stage = 0;
       uint32_t phase = 0;
       int it = 0, kst = 0;
@@ -392,15 +394,26 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
           if (!(FPVS_KNOB(p) & 128)) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 (async proxy) reads
           const uint32_t info = s_info[stage];
           if (!(FPVS_KNOB(p) & 1)) {
-            const uint32_t a_stage = smem_u32(sA + stage * C::STAGE_A);
-            const uint32_t b_stage = smem_u32(sB + stage * C::STAGE_B);
+            // descriptors affine in the stage index, hoisted; a full stage is one
+            // unrolled run of MMAs with immediate offsets (no dependent scalar
+            // work between MMAs: it adds straight to their issue cost)
+            const uint64_t ad0 = a_desc0 + (uint64_t)((uint32_t)stage * (C::STAGE_A >> 4));
+            const uint64_t bd0 = b_desc0 + (uint64_t)((uint32_t)stage * (C::STAGE_B >> 4));
             const int nvalid = (int)(info >> 2);
-            for (int g = 0; g < nvalid; ++g) {
-              const uint64_t ad = sw128_desc(a_stage + g * A_BYTES);
-              const uint64_t bd = sw128_desc(b_stage + g * C::B_SUB);
+            const uint32_t acc0 = (info & 1u) ? 0u : 1u;
+            if (nvalid == G) {
 #pragma unroll
-              for (int k = 0; k < BK / 16; ++k)
-                umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, ((info & 1u) && g == 0 && k == 0) ? 0u : 1u);
+              for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  umma_bf16(dtm, ad0 + (uint64_t)(g * (A_BYTES >> 4) + 2 * k), bd0 + (uint64_t)(g * (C::B_SUB >> 4) + 2 * k),
+                            idesc, (g == 0 && k == 0) ? acc0 : 1u);
+            } else {
+              for (int g = 0; g < nvalid; ++g)
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  umma_bf16(dtm, ad0 + (uint64_t)(g * (A_BYTES >> 4) + 2 * k),
+                            bd0 + (uint64_t)(g * (C::B_SUB >> 4) + 2 * k), idesc, (g == 0 && k == 0) ? acc0 : 1u);
             }
           }
           umma_commit(smem_u32(empty + stage));
