@@ -295,6 +295,19 @@ int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_t* nbr, con
                      const float* bias, int cin, int cout, int act, void* y, int ldy, int col_off,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* The U-Net's last level-0 conv (Cout = 64, relu) with the 1x1x1 head fused
+ * into its epilogue (d = 4): each tile's bf16 activations become the A
+ * operand of the head's tcgen05 MMAs in tensor memory and [p >= tau] is
+ * bit-packed into out_bits (zeroed first); the conv's own output never goes
+ * to HBM.  Same conv arguments as fpvs_spconv_halo with bn = 64, split = 1;
+ * head_w_packed: the head's fpvs_pack_weights_tc image (K = 1, bn = 64). */
+int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
+                          const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
+                          const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin,
+                          void* ws, size_t ws_bytes, const void* head_w_packed, const float* head_bias,
+                          const int32_t* coords, int d, int B, int Nx, int Ny, int Nz, float tau,
+                          uint8_t* out_bits, void* stream);
+
 /* Fused head (replaces the final Conv3d + sigmoid + deinterleave(tau),
  * neural.py:513-526): 1x1x1 conv Cin -> d^3, sigmoid, [p >= tau], packed-bit
  * scatter into out_bits (zeroed first; u32-aligned).  probs (nullable):

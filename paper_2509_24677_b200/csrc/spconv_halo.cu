@@ -116,6 +116,16 @@ struct Params {
   int* counters;  // [tiles][nblk] arrival counters, zero between launches
   int dbg;        // profiling builds: FPVS_HALO_DEBUG (timestamps)
   int abl;        // profiling builds: FPVS_HALO_ABL (ablations)
+  // fused 1x1x1 head (dec0b of the U-Net, BN = Cout = d^3 = 64, no split):
+  // the tile's bf16 activations become the A operand of 4 TS MMAs against the
+  // head weights, then [z >= logit(tau)] is bit-packed into out_bits
+  int head;
+  const uint8_t* head_wpk;   // packed head weights, 64 x 64 bf16 (one SW128 chunk)
+  const float* head_bias;
+  const int4* coords;
+  int d, dlog, Nx, Ny, Nz;
+  float zt;
+  uint8_t* out_bits;
 };
 
 // ---------------- profiling (profiling builds only) ----------------
@@ -182,12 +192,19 @@ struct Cfg {
   static constexpr int ACOL = NACC * BN;  // TMEM: [accumulators | A slots]
   static constexpr int B_OFF = NHB * HBUF;
   static constexpr int BAR_OFF = B_OFF + NS * STAGE_B;
-  static constexpr int NBARS = 2 * NS + 2 * NACC + 3 * NHB;
+  static constexpr int NBARS = 2 * NS + 2 * NACC + 3 * NHB + 2;  // + fused head: weights landed, head MMA done
   static constexpr int CTRL_OFF = BAR_OFF + 8 * NBARS;
   static constexpr int BIAS_OFF = CTRL_OFF + 64;
   static constexpr int UC_OFF = BIAS_OFF + 4 * 1024;  // unit cache: Unit [64] + halo sizes [64]
-  static constexpr int SMEM = 1024 + UC_OFF + kUnitCache * (int)sizeof(Unit) + kUnitCache * 4;
+  static constexpr int UC_END = UC_OFF + kUnitCache * (int)sizeof(Unit) + kUnitCache * 4;
+  // fused head (BN = 64 only): 8 KB of packed head weights, 1024-aligned
+  static constexpr bool HEAD = BN == 64;
+  static constexpr int HW_OFF = (UC_END + 1023) / 1024 * 1024;
+  static constexpr int SMEM = 1024 + (HEAD ? HW_OFF + 64 * 128 : UC_END);
+  static constexpr int HEAD_A = ACOL + NS * G * 32;  // TMEM: head A operand (32 cols), head accumulator (64 cols)
+  static constexpr int HEAD_D = HEAD_A + 32;
   static_assert(ACOL + NS * G * 32 <= 512, "TMEM columns");
+  static_assert(!HEAD || HEAD_D + 64 <= 512, "TMEM columns (fused head)");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -299,6 +316,8 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   uint64_t* hfull = tempty + C::NACC;
   uint64_t* hempty = hfull + C::NHB;
   uint64_t* hmeta = hempty + C::NHB;  // the tile's local table + halo row list landed (bulk copy)
+  uint64_t* hwbar = hmeta + C::NHB;   // fused head: weights landed
+  uint64_t* hdbar = hwbar + 1;        // fused head: the tile's head MMAs done
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::CTRL_OFF);
   volatile int* s_last = reinterpret_cast<volatile int*>(smem + C::CTRL_OFF + 16);
   float* s_bias = reinterpret_cast<float*>(smem + C::BIAS_OFF);
@@ -340,9 +359,13 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       mbar_init(smem_u32(hempty + a), 8);
       mbar_init(smem_u32(hmeta + a), 1);
     }
+    mbar_init(smem_u32(hwbar), 1);
+    mbar_init(smem_u32(hdbar), 1);
     fence_mbar_init();
   }
   for (int c = tid; c < p.cout; c += THREADS) s_bias[c] = p.bias ? p.bias[c] : 0.f;
+  if (C::HEAD && p.head)
+    for (int c = tid; c < 64; c += THREADS) s_bias[512 + c] = p.head_bias ? p.head_bias[c] : 0.f;
   if (tid < kUnitCache) {
     // this CTA's units decoded in parallel (the tile masks come from the map
     // kernels, two or more launches back; the halo sizes may be the previous
@@ -676,6 +699,13 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     pdl_wait();  // y, partials and counters may be in use by the previous launch
     const int q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t tlane = (uint32_t)(q4 * 32) << 16;
+    const bool fuse_head = C::HEAD && p.head;
+    uint32_t head_phase = 0;
+    if (fuse_head && warp == W_EPI && lane == 0) {
+      // the packed head weights (one 64 x 64 bf16 SW128 chunk), once per CTA
+      mbar_arrive_expect_tx(smem_u32(hwbar), 64 * 128);
+      bulk_g2s(smem_u32(smem + C::HW_OFF), p.head_wpk, 64 * 128, smem_u32(hwbar));
+    }
     int it = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
       Unit U;
@@ -688,16 +718,24 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       const bool valid = row < n;
       const int col0 = U.nb * BN;
       if (U.ns == 1) {
-#pragma unroll 1
+        uint32_t ha[32];  // fused head: this row's bf16 activations as the head's A operand
+#pragma unroll(BN == 64 ? 2 : 1)
         for (int cb = 0; cb < BN; cb += 32) {
           float v[32];
           tmem_ld32(tmem_base + tlane + acc * BN + cb, v);
-          if (!valid) continue;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float z = v[i] + s_bias[col0 + cb + i];
             v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
           }
+          if (fuse_head) {
+            if constexpr (BN == 64) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) ha[cb / 2 + i] = valid ? pack_bf16x2(v[2 * i], v[2 * i + 1]) : 0u;
+            }
+            continue;
+          }
+          if (!valid) continue;
           uint4* dst = reinterpret_cast<uint4*>(p.y + row * p.ldy + p.col_off + col0 + cb);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -707,6 +745,58 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+        if constexpr (C::HEAD) {
+          if (fuse_head) {
+            // head = 1x1x1 conv of the bf16 activations (exactly what the
+            // stand-alone head reads back from HBM): A rows into tensor memory,
+            // 4 TS MMAs (K = 64) by one epilogue thread, then the threshold
+            // bit-pack of head_tc's fast path ([z >= logit(tau)], one RED.OR
+            // per (ly, lz) voxel row of the cell)
+            tmem_st32(tmem_base + tlane + C::HEAD_A, ha);
+            tmem_st_wait();
+            tc_fence_before();
+            named_bar(3, 128);
+            if (warp == W_EPI && lane == 0) {
+              if (it == 0) mbar_wait(smem_u32(hwbar), 0);
+              tc_fence_after();
+              const uint64_t hb = sw128_desc(smem_u32(smem + C::HW_OFF));
+              const uint32_t hidesc = idesc_bf16<64>();
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                umma_bf16_ts(tmem_base + C::HEAD_D, tmem_base + C::HEAD_A + 8 * k, hb + 2 * k, hidesc, k ? 1u : 0u);
+              umma_commit(smem_u32(hdbar));
+            }
+            mbar_wait(smem_u32(hdbar), head_phase);
+            head_phase ^= 1;
+            tc_fence_after();
+            int4 cc = make_int4(0, 0, 0, 0);
+            if (valid) cc = p.coords[row];
+            const int d = p.d, dl = p.dlog;
+#pragma unroll 1
+            for (int cb = 0; cb < 64; cb += 8) {
+              float v[8];
+              tmem_ld8(tmem_base + tlane + C::HEAD_D + cb, v);
+              if (!valid) continue;
+              uint32_t bits8 = 0;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) bits8 |= (v[i] + s_bias[512 + cb + i] >= p.zt ? 1u : 0u) << i;
+              if (!bits8) continue;
+              const uint32_t dm = (1u << d) - 1u;
+              for (int q = 0; q < (8 >> dl); ++q) {
+                const uint32_t rb = (bits8 >> (q * d)) & dm;
+                if (!rb) continue;
+                const int rr = (cb >> dl) + q;  // rr = ly + d * lz
+                const int ly = rr & (d - 1), lz = rr >> dl;
+                const int fx = cc.y * d;
+                const long long byte = bit_byte(cc.x, fx, cc.z * d + ly, cc.w * d + lz, p.Nx, p.Ny, p.Nz);
+                uint32_t* word = reinterpret_cast<uint32_t*>(p.out_bits + (byte & ~3LL));
+                atomicOr(word, rb << ((int)(byte & 3) * 8 + (fx & 7)));
+              }
+            }
+            tc_fence_before();  // the next tile's head A store / MMA come after these reads
+            named_bar(3, 128);
+          }
+        }
       } else {
         // split K: fp32 partial per split, column-major [col][128 rows] so a
         // warp's stores and loads are 128-byte coalesced; the last CTA of the
@@ -877,11 +967,19 @@ extern "C" size_t fpvs_spconv_halo_workspace_size(int cap, int cout, int bn, int
   return b;
 }
 
-extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
-                                const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
-                                const int32_t* n_dev, int cap, const void* w_packed, int bn, int split,
-                                const float* bias, int cin, int cout, int act, void* y, int ldy, int col_off,
-                                void* ws, size_t ws_bytes, void* stream) {
+struct HeadArgs {
+  const void* wpk;
+  const float* bias;
+  const int32_t* coords;
+  int d, Nx, Ny, Nz;
+  float tau;
+  uint8_t* out_bits;
+};
+
+static int halo_conv(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
+                     const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks, const int32_t* n_dev,
+                     int cap, const void* w_packed, int bn, int split, const float* bias, int cin, int cout, int act,
+                     void* y, int ldy, int col_off, void* ws, size_t ws_bytes, void* stream, const HeadArgs* head) {
   FPVS_CHECK_ARG(x && nbr && lnbr && halo_rows && halo_n && tile_masks && n_dev && w_packed && y,
                  "null pointer");
   if (bn == 0) bn = cout % 256 == 0 ? 256 : cout % 128 == 0 ? 128 : cout % 64 == 0 ? 64 : 32;
@@ -927,6 +1025,25 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
   p.part = (float*)((uint8_t*)ws + halo::align256(items * 4));
   p.dbg = debug_knob("FPVS_HALO_DEBUG");
   p.abl = debug_knob("FPVS_HALO_ABL");
+  if (head) {
+    FPVS_CHECK_ARG(bn == 64 && cout == 64 && split == 1 && cin % 64 == 0,
+                   "fused head needs a Cout = 64 layer with 64-wide tiles, no K split and Cin %% 64 == 0");
+    FPVS_CHECK_ARG(head->wpk && head->coords && head->out_bits, "fused head: null pointer");
+    FPVS_CHECK_ARG(head->d == 4 && head->Nx % 8 == 0, "fused head needs d = 4 (d^3 = 64) and N_x %% 8 == 0");
+    p.head = 1;
+    p.head_wpk = (const uint8_t*)head->wpk;
+    p.head_bias = head->bias;
+    p.coords = (const int4*)head->coords;
+    p.d = head->d;
+    p.dlog = __builtin_ctz(head->d);
+    p.Nx = head->Nx;
+    p.Ny = head->Ny;
+    p.Nz = head->Nz;
+    // [sigmoid(z) >= tau] as [z >= logit(tau)] (head_tc's fast path)
+    p.zt = head->tau <= 0.f ? -INFINITY : head->tau >= 1.f ? INFINITY
+                                        : (float)log((double)head->tau / (1.0 - (double)head->tau));
+    p.out_bits = head->out_bits;
+  }
   const cudaStream_t st = as_stream(stream);
   if (cin == 32) {
     if (bn == 32) return halo::launch<32, true>(p, st);
@@ -938,4 +1055,26 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
   if (bn == 64) return halo::launch<64, false>(p, st);
   if (bn == 128) return halo::launch<128, false>(p, st);
   return halo::launch<256, false>(p, st);
+}
+
+extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
+                                const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
+                                const int32_t* n_dev, int cap, const void* w_packed, int bn, int split,
+                                const float* bias, int cin, int cout, int act, void* y, int ldy, int col_off,
+                                void* ws, size_t ws_bytes, void* stream) {
+  return halo_conv(x, ldx, x_rows, nbr, lnbr, halo_rows, halo_n, tile_masks, n_dev, cap, w_packed, bn, split, bias, cin,
+                   cout, act, y, ldy, col_off, ws, ws_bytes, stream, nullptr);
+}
+
+extern "C" int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
+                                     const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
+                                     const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin,
+                                     void* ws, size_t ws_bytes, const void* head_w_packed, const float* head_bias,
+                                     const int32_t* coords, int d, int B, int Nx, int Ny, int Nz, float tau,
+                                     uint8_t* out_bits, void* stream) {
+  (void)B;
+  const HeadArgs h{head_w_packed, head_bias, coords, d, Nx, Ny, Nz, tau, out_bits};
+  // the conv's own output is consumed in the epilogue: y is never written
+  return halo_conv(x, ldx, x_rows, nbr, lnbr, halo_rows, halo_n, tile_masks, n_dev, cap, w_packed, 64, 1, bias, cin, 64,
+                   FPVS_ACT_RELU, out_bits, 64, 0, ws, ws_bytes, stream, &h);
 }

@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
         int4 cc = make_int4(0, 0, 0, 0);
         if (valid) cc = p.coords[row];
         const int d = p.d, dl = p.dlog;
-        const bool fast = dl >= 0 && d <= 8 && !p.probs && !p.logits && p.out_bits;
+        const bool fast = dl >= 0 && d <= 8 && !p.probs && !p.logits && p.out_bits && p.zt < INFINITY;
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += 8) {
           float v[8];
@@ -824,7 +824,9 @@ extern "C" int fpvs_head_tc(const void* x, int ldx, int x_rows, const int32_t* c
   p.d = d;
   p.dlog = (d & (d - 1)) == 0 ? __builtin_ctz(d) : -1;
   // logit(tau) for the fast threshold; tau outside (0, 1) takes the sigmoid path
-  p.zt = (tau > 0.f && tau < 1.f) ? (float)log((double)tau / (1.0 - (double)tau)) : 0.f;
+  // tau <= 0: every p >= tau; tau >= 1: the fast path is not taken for a
+  // saturating sigmoid (see below), so only the p >= tau form decides there
+  p.zt = tau <= 0.f ? -INFINITY : tau >= 1.f ? INFINITY : (float)log((double)tau / (1.0 - (double)tau));
   if (!(tau > 0.f && tau < 1.f)) p.dlog = -1;
   p.Nx = Nx;
   p.Ny = Ny;

@@ -147,6 +147,8 @@ class UNetPlan:
         self.use_upsort = net.precision == "bf16" and os.environ.get("FPVS_UPSORT", "1") != "0"
         self._up_sorter = None
         self.overlap = True  # side-stream map tables (see build_maps); device_stage_times turns it off
+        # the 1x1x1 head fused into dec0b (FPVS_FUSE_HEAD=0 keeps the stand-alone head launch)
+        self.fuse_head = net.precision == "bf16" and os.environ.get("FPVS_FUSE_HEAD", "1") != "0"
         self._side = None
         self._side_pending = False
         if self.use_halo:
@@ -301,6 +303,25 @@ class UNetPlan:
         conv("dec1b", self.t1a, c1, L1.nbr, 27, L1, self.t1b, c1, masks=m1)
         conv("up10", self.t1b, c1, self.up10, 8, L0, self.buf0, 2 * c0, c0, um10)       # U0 -> buf0[:, c0:]
         conv("dec0a", self.buf0, 2 * c0, L0.nbr, 27, L0, self.t0a, c0, masks=m0)
+        hc0 = self.halo_cfg.get("dec0b")
+        # the head fused into dec0b's epilogue (fpvs_spconv_halo_head): the
+        # activations never leave the SM; taken for thresholded bits only
+        # (probabilities / logits keep the stand-alone head)
+        fuse_head = (self.fuse_head and fused and hc0 is not None and hc0 == (64, 1) and c0 == 64 and net.d == 4
+                     and probs is None and logits is None and 0.0 < float(tau) < 1.0)
+        if fuse_head:
+            def dec0b_head():
+                hl = L["head"]
+                ht = L0.extra["halo"]
+                ws = self.halo_ws[id(L0)]
+                nx, ny, nz = self.grid_dims
+                _lib.call("fpvs_spconv_halo_head", _lib.ptr(self.t0a), c0, self.t0a.shape[0], _lib.ptr(L0.nbr),
+                          _lib.ptr(ht["lnbr"]), _lib.ptr(ht["rows"]), _lib.ptr(ht["n"]), _lib.ptr(m0), _lib.ptr(L0.n),
+                          L0.cap, _lib.ptr(L["dec0b"].packed(64)), _lib.ptr(L["dec0b"].b), c0, _lib.ptr(ws), ws.numel(),
+                          _lib.ptr(hl.packed(64)), _lib.ptr(hl.b), _lib.ptr(L0.coords), net.d, self.B, nx, ny, nz,
+                          float(tau), _lib.ptr(out_bits), _lib.stream_ptr())
+            out.append(("dec0b", dec0b_head))
+            return out
         conv("dec0b", self.t0a, c0, L0.nbr, 27, L0, self.t0b, c0, masks=m0)
 
         def head():

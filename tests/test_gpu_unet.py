@@ -113,3 +113,31 @@ def test_streamed_frames_match_eager(inflight):
         ref.plan.run(x.cuda(), ref.out_bits, 0.5)
         torch.cuda.synchronize()
         assert torch.equal(outs[i], ref.out_bits.cpu()), i
+
+
+def test_fused_head_equals_standalone_head():
+    """dec0b with the head fused into its epilogue (fpvs_spconv_halo_head)
+    writes exactly the bits of dec0b + the stand-alone head (same bf16
+    activations, same MMA products and K order)."""
+    import torch
+    from paper_2509_24677_b200 import synth
+    from paper_2509_24677_b200.froxel import FroxelGrid
+    from paper_2509_24677_b200.unet import PvsUNet
+    for seed, dims in ((1, (128, 128, 128)), (3, (256, 256, 256))):
+        occ = synth.box_grid(dims, 4000 if dims[0] == 256 else 600, 1, 12, seed)
+        bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+        net = PvsUNet(seed=1, precision="bf16")
+        plan = net.plan(1, occ.shape)
+        plan.tune(bits)
+        outs = []
+        for fuse in (True, False):
+            plan.fuse_head = fuse
+            out = torch.empty(occ.size // 8, dtype=torch.uint8, device="cuda")
+            names = [n for n, _ in plan.stages(bits, out, 0.5)]
+            # fused only where dec0b runs unsplit 64-wide tiles (the 256^3 frame)
+            assert ("head" in names) != (fuse and dims[0] == 256)
+            plan.run(bits, out, 0.5)
+            torch.cuda.synchronize()
+            outs.append(out.cpu().numpy())
+        assert np.array_equal(outs[0], outs[1]), (seed, int(np.unpackbits(outs[0] ^ outs[1]).sum()))
+        assert np.unpackbits(outs[0]).sum() > 0

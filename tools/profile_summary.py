@@ -64,10 +64,14 @@ def raw(rep, metrics):
 
 
 def tensor_pct(r):
-    """tcgen05 (hmma subpipe) active cycles / elapsed SM cycles, per SM average."""
+    """tcgen05 (hmma subpipe) busy cycles as a fraction of the SM's ACTIVE cycles,
+    both in the SM clock domain (ncu's own pct_of_peak_sustained_active ratio;
+    round 1 divided a realtime-clock count by SM-clock cycles, which could
+    exceed 100 %)."""
+    v = r.get("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active")
     try:
-        return f"{100 * float(r['sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg']) / float(r['sm__cycles_elapsed.avg']):.1f}"
-    except (KeyError, ValueError, ZeroDivisionError):
+        return f"{float(v):.1f}"
+    except (TypeError, ValueError):
         return "n/a"
 
 
@@ -87,11 +91,11 @@ def main(tag, launch_csv, conv_rep, maps_rep=None):
     mets = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
             "launch__grid_size", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-            "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg", "sm__cycles_elapsed.avg",
+            "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active"]
     rs = raw(conv_rep, mets)
     md += ["", f"`--set full` capture `{os.path.basename(conv_rep)}` (first eager frame's 15 conv launches):", "",
-           "| launch | kernel | us | DRAM read MB | DRAM write MB | grid | SM % | L2 % | tensor pipe % |",
+           "| launch | kernel | us | DRAM read MB | DRAM write MB | grid | SM % | L2 % | tensor pipe % (of active SM cycles) |",
            "|---|---|---|---|---|---|---|---|---|"]
     dram = []
     names = ["enc0a", "enc0b", "down01", "enc1a", "enc1b", "down12", "enc2a", "enc2b", "up21", "dec1a", "dec1b",
