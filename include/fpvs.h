@@ -297,16 +297,25 @@ int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_t* nbr, con
 
 /* The U-Net's last level-0 conv (Cout = 64, relu) with the 1x1x1 head fused
  * into its epilogue (d = 4): each tile's bf16 activations become the A
- * operand of the head's tcgen05 MMAs in tensor memory and [p >= tau] is
- * bit-packed into out_bits (zeroed first); the conv's own output never goes
- * to HBM.  Same conv arguments as fpvs_spconv_halo with bn = 64, split = 1;
- * head_w_packed: the head's fpvs_pack_weights_tc image (K = 1, bn = 64). */
+ * operand of the head's tcgen05 MMAs in tensor memory, and active row r's
+ * 64 thresholded outputs [sigmoid(z) >= tau] go to row_bits[r] (bit k =
+ * channel k = lx + 4 ly + 16 lz); the conv's own output never goes to HBM.
+ * Same conv arguments as fpvs_spconv_halo with bn = 64, split = 1;
+ * head_w_packed: the head's fpvs_pack_weights_tc image (K = 1, bn = 64).
+ * With fpvs_rowbits_to_grid this replaces the final Conv3d + sigmoid +
+ * deinterleave(tau) of the reference (neural.py:513-526, interleave.py:68-80). */
 int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
                           const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
                           const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin,
                           void* ws, size_t ws_bytes, const void* head_w_packed, const float* head_bias,
-                          const int32_t* coords, int d, int B, int Nx, int Ny, int Nz, float tau,
-                          uint8_t* out_bits, void* stream);
+                          float tau, uint64_t* row_bits, void* stream);
+
+/* Per-row 64-bit cell masks (fpvs_spconv_halo_head) -> the packed froxel grid
+ * B x Nx x Ny x Nz (FPVS bit order, d = 4, N_x % 32 == 0): every 32-bit word
+ * of out_bits is written exactly once (no clear needed); cells whose
+ * level-0 index_vol entry is -1 are 0. */
+int fpvs_rowbits_to_grid(const uint64_t* row_bits, const int32_t* index_vol, int B, int Nx, int Ny, int Nz, int d,
+                         uint8_t* out_bits, void* stream);
 
 /* Fused head (replaces the final Conv3d + sigmoid + deinterleave(tau),
  * neural.py:513-526): 1x1x1 conv Cin -> d^3, sigmoid, [p >= tau], packed-bit

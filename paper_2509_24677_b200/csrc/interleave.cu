@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kTileThreads) il_tile_kernel(const Tin* __rest
   constexpr int R = D * D, M = D * D;
   constexpr int VI = 16 / sizeof(Tin);                  // input elements per 16-byte load
   constexpr int VO = cmin(M, (int)(16 / sizeof(Tout)));  // output elements per store
-  extern __shared__ __align__(16) unsigned char il_smem[];
+  extern __shared__ __align__(128) unsigned char il_smem[];
   Tin* tile = reinterpret_cast<Tin*>(il_smem);
   const int X = Nx / D, Y = Ny / D, Z = Nz / D;
   const int ld = zt + VI;  // padded row (keeps 16-byte alignment, shifts banks)
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kTileThreads) deil_tile_kernel(const Tin* __re
   constexpr int R = D * D, M = D * D;
   constexpr int VI = cmin(M, (int)(16 / sizeof(Tin)));
   constexpr int VO = 16 / sizeof(Tout);
-  extern __shared__ __align__(16) unsigned char il_smem[];
+  extern __shared__ __align__(128) unsigned char il_smem[];
   Tout* tile = reinterpret_cast<Tout*>(il_smem);
   const int Nx = X * D, Ny = Y * D, Nz = Z * D;
   const int ld = zt + VO;
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(kTileThreads) il_bits_tile_kernel(const uint8_
   constexpr int M = D * D;
   constexpr int VO = cmin(M, (int)(16 / sizeof(Tout)));
   constexpr int MV = M / VO;
-  extern __shared__ __align__(16) unsigned char il_smem[];
+  extern __shared__ __align__(128) unsigned char il_smem[];
   const int X = Nx / D, Y = Ny / D, Z = Nz / D;
   const int rowb = Nx >> 3;
   const int nzc = (Nz + zt - 1) / zt;

@@ -118,14 +118,12 @@ struct Params {
   int abl;        // profiling builds: FPVS_HALO_ABL (ablations)
   // fused 1x1x1 head (dec0b of the U-Net, BN = Cout = d^3 = 64, no split):
   // the tile's bf16 activations become the A operand of 4 TS MMAs against the
-  // head weights, then [z >= logit(tau)] is bit-packed into out_bits
+  // head weights, then the row's 64 [z >= logit(tau)] bits go to row_bits
   int head;
   const uint8_t* head_wpk;   // packed head weights, 64 x 64 bf16 (one SW128 chunk)
   const float* head_bias;
-  const int4* coords;
-  int d, dlog, Nx, Ny, Nz;
   float zt;
-  uint8_t* out_bits;
+  unsigned long long* row_bits;
 };
 
 // ---------------- profiling (profiling builds only) ----------------
@@ -161,12 +159,21 @@ __device__ long long g_hclk[2][160];
 // unit boundary (the MMA thread would stall ~1 us on it).
 constexpr int kUnitCache = 64;
 
-constexpr int W_LOAD = 8;   // warps 8, 9: halo loaders
-constexpr int W_B = 10;     // weight loader
-constexpr int W_MMA = 11;   // MMA issuer, TMEM owner
-constexpr int W_EPI = 12;   // warps 12..15: epilogue
-constexpr int THREADS = 512;
 constexpr int LOADERS = 64;
+
+// Warp roles for NBG builder groups of 4 warps (one warp per TMEM lane
+// quadrant): warps [0, 4 NBG) build A, then 2 halo loaders, the weight loader,
+// the MMA issuer (TMEM owner) and 4 epilogue warps (first one quadrant-aligned).
+template <int NBG>
+struct Roles {
+  static constexpr int W_LOAD = 4 * NBG;   // two loader warps
+  static constexpr int W_B = W_LOAD + 2;   // weight loader
+  static constexpr int W_MMA = W_B + 1;    // MMA issuer, TMEM owner
+  static constexpr int W_EPI = W_MMA + 1;  // epilogue warps W_EPI .. W_EPI + 3
+  static constexpr int THREADS = (W_EPI + 4) * 32;
+  static constexpr int NBT = 128 * NBG;  // builder threads
+  static_assert(W_EPI % 4 == 0, "epilogue warps must cover the four lane quadrants in order");
+};
 
 // Pipeline stage = G = 2 K-chunks: two TMEM A slots (one per builder group)
 // + two weight chunks in smem; one full/empty barrier pair and one commit per
@@ -301,9 +308,12 @@ struct ChunkWalk {
   }
 };
 
-template <int BN, bool PAIR>
-__global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p) {
+template <int BN, bool PAIR, int NBG>
+__global__ void __launch_bounds__(Roles<NBG>::THREADS, 1) spconv_halo_kernel(const Params p) {
   using C = Cfg<BN>;
+  using R = Roles<NBG>;
+  constexpr int W_LOAD = R::W_LOAD, W_B = R::W_B, W_MMA = R::W_MMA, W_EPI = R::W_EPI, THREADS = R::THREADS;
+  static_assert(C::G == 1 || C::G % NBG == 0, "a stage's chunk slots split evenly over the builder groups");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
@@ -355,8 +365,8 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       mbar_init(smem_u32(tempty + a), 4);
     }
     for (int a = 0; a < C::NHB; ++a) {
-      mbar_init(smem_u32(hfull + a), LOADERS + 8 * 32);  // loaders + every builder thread (see below)
-      mbar_init(smem_u32(hempty + a), 8);
+      mbar_init(smem_u32(hfull + a), LOADERS + R::NBT);  // loaders + every builder thread (see below)
+      mbar_init(smem_u32(hempty + a), 4 * NBG);
       mbar_init(smem_u32(hmeta + a), 1);
     }
     mbar_init(smem_u32(hwbar), 1);
@@ -396,7 +406,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     // paced the N = 64 layers); with G = 1 the groups alternate stages.
     pdl_wait();  // the direct-read path reads x (the previous launch's output)
     const int bg = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
-    auto grp = [](int i) { return C::G >= 2 ? ((i % C::G) >= C::G / 2 ? 1 : 0) : (i & 1); };
+    auto grp = [](int i) { return C::G >= NBG ? (i % C::G) / (C::G / NBG) : i % NBG; };
     const uint32_t t_a = tmem_base + ((uint32_t)(q4 * 32) << 16) + C::ACOL;
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u;
     uint32_t sc0 = 0, gc = 0;
@@ -420,7 +430,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
           const uint32_t hs = smem_u32(smem + hb * HBUF);
           if (!pair || pc < 4) {
 #pragma unroll 4
-            for (int i = pt >> 3; i < H; i += (LOADERS + 256) / 8)
+            for (int i = pt >> 3; i < H; i += (LOADERS + R::NBT) / 8)
               cp_async16(hs + i * 128 + ((pc ^ (i & 7)) << 4), xb + (long long)hr[i] * ldx2, 16);
           }
           cp_async_mbar_arrive_noinc(smem_u32(hfull + hb));
@@ -428,7 +438,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
           mbar_arrive(smem_u32(hfull + hb));  // builders add no copies to later halos
         }
         mbar_wait(smem_u32(hfull + hb), hph);
-        if (lane == 0 && q4 == 0) HTS(256 + 4 * gc + 2 * bg);
+        if (lane == 0 && q4 == 0 && bg < 2) HTS(256 + 4 * gc + 2 * bg);
         const uint8_t* hbuf = smem + hb * HBUF;
         const int16_t* ln = reinterpret_cast<const int16_t*>(hbuf + HALO_BYTES) + r * KOFF;
         int j = first_offset(U.mask, qs - c * U.npres);
@@ -466,7 +476,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
               }
             }
           } else {
-            if (lane == 0 && q4 == 0 && st < 300) HTS(5400 + 2 * st + bg);
+            if (lane == 0 && q4 == 0 && bg < 2 && st < 300) HTS(5400 + 2 * st + bg);
             auto load = [&](int jj, uint32_t (&vv)[32]) {
               const int li = ABL(17) ? -1 : ln[jj];
               if (li >= 0) {
@@ -493,33 +503,36 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
             };
             const int slot = i % C::G;
             // the group's second chunk of this stage, when it is in this range
-            const bool two = C::G >= 2 && q + 1 < qe && slot + 1 < C::G && grp(i + 1) == bg;
-            uint32_t w[32];
+            constexpr bool kTwo = C::G / NBG >= 2;  // a group owns two slots of a stage
+            const bool two = kTwo && q + 1 < qe && slot + 1 < C::G && grp(i + 1) == bg;
+            uint32_t w[kTwo ? 32 : 1];
             const int j2 = two ? next_offset(U.mask, j) : j;
             load(j, v);
-            if (two) load(j2, w);
-            if (lane == 0 && q4 == 0 && st < 400) HTS(2000 + 2 * st + bg);
+            if constexpr (kTwo)
+              if (two) load(j2, w);
+            if (lane == 0 && q4 == 0 && bg < 2 && st < 400) HTS(2000 + 2 * st + bg);
             mbar_wait(smem_u32(empty + stage), ((st / C::NS) & 1) ^ 1);
-            if (lane == 0 && q4 == 0 && st < 400) HTS(2800 + 2 * st + bg);
+            if (lane == 0 && q4 == 0 && bg < 2 && st < 400) HTS(2800 + 2 * st + bg);
             tc_fence_after();
             if (!ABL(18)) {
               tmem_st32(t_a + (stage * C::G + slot) * 32, v);
-              if (two) tmem_st32(t_a + (stage * C::G + slot + 1) * 32, w);
+              if constexpr (kTwo)
+                if (two) tmem_st32(t_a + (stage * C::G + slot + 1) * 32, w);
               tmem_st_wait();
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cnt(smem_u32(full + stage), two ? 2u : 1u);
-            if (lane == 0 && q4 == 0 && st < 1400) HTS(1024 + 2 * st + bg);
+            if (lane == 0 && q4 == 0 && bg < 2 && st < 1400) HTS(1024 + 2 * st + bg);
             if (two) {
               ++q;  // the partner chunk is done; the loop increment moves past it
               j = j2;
             }
             continue;
           }
-          if (lane == 0 && q4 == 0 && st < 400) HTS(2000 + 2 * st + bg);
+          if (lane == 0 && q4 == 0 && bg < 2 && st < 400) HTS(2000 + 2 * st + bg);
           mbar_wait(smem_u32(empty + stage), ((st / C::NS) & 1) ^ 1);
-          if (lane == 0 && q4 == 0 && st < 400) HTS(2800 + 2 * st + bg);
+          if (lane == 0 && q4 == 0 && bg < 2 && st < 400) HTS(2800 + 2 * st + bg);
           tc_fence_after();
           if (!ABL(18)) {
             tmem_st32(t_a + (stage * C::G + i % C::G) * 32, v);
@@ -528,7 +541,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(full + stage));
-          if (lane == 0 && q4 == 0 && st < 1400) HTS(1024 + 2 * st + bg);
+          if (lane == 0 && q4 == 0 && bg < 2 && st < 1400) HTS(1024 + 2 * st + bg);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(hempty + hb));
@@ -541,7 +554,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         const uint32_t st = sc0 + nst - 1;
         bool waited = false;
         for (int sl = nq % C::G; sl < C::G; ++sl) {
-          if (grp(sl) != bg) continue;
+          if (grp((int)(nst - 1) * C::G + sl) != bg) continue;
           if (!waited) {
             mbar_wait(smem_u32(empty + st % C::NS), ((st / C::NS) & 1) ^ 1);
             waited = true;
@@ -593,7 +606,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         const uint32_t hs = smem_u32(hbuf);
         // the first halo is shared with the builders: loader thread tl takes rows
         // tl/8 + 40k of the 320-thread split; later halos rows tl/8 + 8k
-        const int rstep = gc == 0 ? (LOADERS + 256) / 8 : LOADERS / 8;
+        const int rstep = gc == 0 ? (LOADERS + R::NBT) / 8 : LOADERS / 8;
         if ((!pair || pc < 4) && !ABL(19)) {  // 32-channel rows: four 16-byte pieces
 #pragma unroll 4
           for (int i = tl >> 3; i < H; i += rstep) {
@@ -700,6 +713,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
     const int q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t tlane = (uint32_t)(q4 * 32) << 16;
     const bool fuse_head = C::HEAD && p.head;
+    constexpr int EC = NBG == 4 ? 16 : 32;
     uint32_t head_phase = 0;
     if (fuse_head && warp == W_EPI && lane == 0) {
       // the packed head weights (one 64 x 64 bf16 SW128 chunk), once per CTA
@@ -719,26 +733,27 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
       const int col0 = U.nb * BN;
       if (U.ns == 1) {
         uint32_t ha[32];  // fused head: this row's bf16 activations as the head's A operand
-#pragma unroll(BN == 64 ? 2 : 1)
-        for (int cb = 0; cb < BN; cb += 32) {
-          float v[32];
-          tmem_ld32(tmem_base + tlane + acc * BN + cb, v);
+        // EC columns per TMEM load (16 in the 768-thread variant: 80 registers)
+#pragma unroll(BN == 64 ? 64 / EC : 1)
+        for (int cb = 0; cb < BN; cb += EC) {
+          float v[EC];
+          tmem_ldn<EC>(tmem_base + tlane + acc * BN + cb, v);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < EC; ++i) {
             const float z = v[i] + s_bias[col0 + cb + i];
             v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
           }
           if (fuse_head) {
             if constexpr (BN == 64) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) ha[cb / 2 + i] = valid ? pack_bf16x2(v[2 * i], v[2 * i + 1]) : 0u;
+              for (int i = 0; i < EC / 2; ++i) ha[cb / 2 + i] = valid ? pack_bf16x2(v[2 * i], v[2 * i + 1]) : 0u;
             }
             continue;
           }
           if (!valid) continue;
           uint4* dst = reinterpret_cast<uint4*>(p.y + row * p.ldy + p.col_off + col0 + cb);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < EC / 8; ++i)
             dst[i] = make_uint4(pack_bf16x2(v[8 * i + 0], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
                                 pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
         }
@@ -756,7 +771,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
             tmem_st_wait();
             tc_fence_before();
             named_bar(3, 128);
-            if (warp == W_EPI && lane == 0) {
+            if (warp == W_EPI && lane == 0 && !ABL(22)) {
               if (it == 0) mbar_wait(smem_u32(hwbar), 0);
               tc_fence_after();
               const uint64_t hb = sw128_desc(smem_u32(smem + C::HW_OFF));
@@ -766,33 +781,21 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
                 umma_bf16_ts(tmem_base + C::HEAD_D, tmem_base + C::HEAD_A + 8 * k, hb + 2 * k, hidesc, k ? 1u : 0u);
               umma_commit(smem_u32(hdbar));
             }
-            mbar_wait(smem_u32(hdbar), head_phase);
+            if (!ABL(22)) mbar_wait(smem_u32(hdbar), head_phase);
             head_phase ^= 1;
             tc_fence_after();
-            int4 cc = make_int4(0, 0, 0, 0);
-            if (valid) cc = p.coords[row];
-            const int d = p.d, dl = p.dlog;
-#pragma unroll 1
+            // the row's 64 head outputs as one word (bit k = channel k =
+            // lx + 4 ly + 16 lz); rowbits_grid_kernel writes the froxel grid
+            unsigned long long rb = 0;
+#pragma unroll
             for (int cb = 0; cb < 64; cb += 8) {
               float v[8];
               tmem_ld8(tmem_base + tlane + C::HEAD_D + cb, v);
-              if (!valid) continue;
-              uint32_t bits8 = 0;
 #pragma unroll
-              for (int i = 0; i < 8; ++i) bits8 |= (v[i] + s_bias[512 + cb + i] >= p.zt ? 1u : 0u) << i;
-              if (!bits8) continue;
-              const uint32_t dm = (1u << d) - 1u;
-              for (int q = 0; q < (8 >> dl); ++q) {
-                const uint32_t rb = (bits8 >> (q * d)) & dm;
-                if (!rb) continue;
-                const int rr = (cb >> dl) + q;  // rr = ly + d * lz
-                const int ly = rr & (d - 1), lz = rr >> dl;
-                const int fx = cc.y * d;
-                const long long byte = bit_byte(cc.x, fx, cc.z * d + ly, cc.w * d + lz, p.Nx, p.Ny, p.Nz);
-                uint32_t* word = reinterpret_cast<uint32_t*>(p.out_bits + (byte & ~3LL));
-                atomicOr(word, rb << ((int)(byte & 3) * 8 + (fx & 7)));
-              }
+              for (int i = 0; i < 8; ++i)
+                rb |= (unsigned long long)(v[i] + s_bias[512 + cb + i] >= p.zt ? 1u : 0u) << (cb + i);
             }
+            if (valid && !ABL(21)) p.row_bits[row] = rb;
             tc_fence_before();  // the next tile's head A store / MMA come after these reads
             named_bar(3, 128);
           }
@@ -806,11 +809,11 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         const bool has = U.q1 > U.q0;
         float* mine = p.part + (slot * p.smax + U.s) * BM * BN + r;
 #pragma unroll 1
-        for (int cb = 0; cb < BN; cb += 32) {
-          float v[32];
-          tmem_ld32(tmem_base + tlane + acc * BN + cb, v);
+        for (int cb = 0; cb < BN; cb += EC) {
+          float v[EC];
+          tmem_ldn<EC>(tmem_base + tlane + acc * BN + cb, v);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) __stcg(mine + (cb + i) * BM, has ? v[i] : 0.f);
+          for (int i = 0; i < EC; ++i) __stcg(mine + (cb + i) * BM, has ? v[i] : 0.f);
         }
         named_bar(1, 128);
         if (q4 == 0 && lane == 0) HTS(7400 + 4 * it);
@@ -825,30 +828,30 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
         if (*s_last) {
           const float* base = p.part + slot * p.smax * BM * BN + r;
 #pragma unroll 1
-          for (int cb = 0; cb < BN; cb += 32) {
-            float own[32], v[32];
-            tmem_ld32(tmem_base + tlane + acc * BN + cb, own);
+          for (int cb = 0; cb < BN; cb += EC) {
+            float own[EC], v[EC];
+            tmem_ldn<EC>(tmem_base + tlane + acc * BN + cb, own);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            for (int i = 0; i < EC; ++i) v[i] = 0.f;
             for (int ss = 0; ss < U.ns; ++ss) {
               const float* src = base + (long long)ss * BM * BN + cb * BM;
               if (ss == U.s) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] += has ? own[i] : 0.f;
+                for (int i = 0; i < EC; ++i) v[i] += has ? own[i] : 0.f;
               } else {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] += __ldcg(src + i * BM);
+                for (int i = 0; i < EC; ++i) v[i] += __ldcg(src + i * BM);
               }
             }
             if (!valid) continue;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < EC; ++i) {
               const float z = v[i] + s_bias[col0 + cb + i];
               v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
             }
             uint4* dst = reinterpret_cast<uint4*>(p.y + row * p.ldy + p.col_off + col0 + cb);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < EC / 8; ++i)
               dst[i] = make_uint4(pack_bf16x2(v[8 * i + 0], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
                                   pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
           }
@@ -880,23 +883,27 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_halo_kernel(const Params p)
   }
 }
 
-template <int BN, bool PAIR>
+template <int BN, bool PAIR, int NBG>
 int launch(const Params& p, cudaStream_t s) {
   using C = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(spconv_halo_kernel<BN, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(spconv_halo_kernel<BN, PAIR, NBG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     configured = true;
   }
   const long long units = (long long)((p.cap + BM - 1) / BM) * p.nblk * p.smax;
   const int grid = (int)(units < kNumSMs ? (units < 1 ? 1 : units) : kNumSMs);
-  cudaError_t e = launch_kernel(spconv_halo_kernel<BN, PAIR>, dim3(grid), dim3(THREADS), C::SMEM, s, p);
+  cudaError_t e = launch_kernel(spconv_halo_kernel<BN, PAIR, NBG>, dim3(grid), dim3(Roles<NBG>::THREADS), C::SMEM, s, p);
   if (e != cudaSuccess) return set_error(FPVS_ECUDA, "spconv_halo: %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("spconv_halo");
   return FPVS_OK;
 }
+
+// 4 builder groups at N = 64 (level 0: the A build paces the MMA issue; at
+// N >= 128 measured no faster, tools/halo_variant.py)
+inline bool default_nbg4(int bn) { return bn == 64; }
 
 inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
@@ -970,10 +977,8 @@ extern "C" size_t fpvs_spconv_halo_workspace_size(int cap, int cout, int bn, int
 struct HeadArgs {
   const void* wpk;
   const float* bias;
-  const int32_t* coords;
-  int d, Nx, Ny, Nz;
   float tau;
-  uint8_t* out_bits;
+  unsigned long long* row_bits;
 };
 
 static int halo_conv(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
@@ -1028,33 +1033,31 @@ static int halo_conv(const void* x, int ldx, int x_rows, const int32_t* nbr, con
   if (head) {
     FPVS_CHECK_ARG(bn == 64 && cout == 64 && split == 1 && cin % 64 == 0,
                    "fused head needs a Cout = 64 layer with 64-wide tiles, no K split and Cin %% 64 == 0");
-    FPVS_CHECK_ARG(head->wpk && head->coords && head->out_bits, "fused head: null pointer");
-    FPVS_CHECK_ARG(head->d == 4 && head->Nx % 8 == 0, "fused head needs d = 4 (d^3 = 64) and N_x %% 8 == 0");
+    FPVS_CHECK_ARG(head->wpk && head->row_bits, "fused head: null pointer");
     p.head = 1;
     p.head_wpk = (const uint8_t*)head->wpk;
     p.head_bias = head->bias;
-    p.coords = (const int4*)head->coords;
-    p.d = head->d;
-    p.dlog = __builtin_ctz(head->d);
-    p.Nx = head->Nx;
-    p.Ny = head->Ny;
-    p.Nz = head->Nz;
     // [sigmoid(z) >= tau] as [z >= logit(tau)] (head_tc's fast path)
     p.zt = head->tau <= 0.f ? -INFINITY : head->tau >= 1.f ? INFINITY
                                         : (float)log((double)head->tau / (1.0 - (double)head->tau));
-    p.out_bits = head->out_bits;
+    p.row_bits = head->row_bits;
   }
   const cudaStream_t st = as_stream(stream);
   if (cin == 32) {
-    if (bn == 32) return halo::launch<32, true>(p, st);
-    if (bn == 64) return halo::launch<64, true>(p, st);
-    if (bn == 128) return halo::launch<128, true>(p, st);
-    return halo::launch<256, true>(p, st);
+    if (bn == 32) return halo::launch<32, true, 2>(p, st);
+    if (bn == 64) return halo::launch<64, true, 2>(p, st);
+    if (bn == 128) return halo::launch<128, true, 2>(p, st);
+    return halo::launch<256, true, 2>(p, st);
   }
-  if (bn == 32) return halo::launch<32, false>(p, st);
-  if (bn == 64) return halo::launch<64, false>(p, st);
-  if (bn == 128) return halo::launch<128, false>(p, st);
-  return halo::launch<256, false>(p, st);
+  // builder groups: 4 (16 builder warps) where the A build paces the MMA
+  const int nbg_knob = debug_knob("FPVS_HALO_NBG");
+  // (profiling knob: 2 / 4 for every width, 8 + m: bit 0/1/2 of m = 4 groups at BN 64/128/256)
+  const int bnbit = bn == 64 ? 1 : bn == 128 ? 2 : 4;
+  const bool nbg4 = nbg_knob >= 8 ? ((nbg_knob - 8) & bnbit) != 0 : nbg_knob ? nbg_knob == 4 : halo::default_nbg4(bn);
+  if (bn == 32) return halo::launch<32, false, 2>(p, st);
+  if (bn == 64) return nbg4 ? halo::launch<64, false, 4>(p, st) : halo::launch<64, false, 2>(p, st);
+  if (bn == 128) return nbg4 ? halo::launch<128, false, 4>(p, st) : halo::launch<128, false, 2>(p, st);
+  return nbg4 ? halo::launch<256, false, 4>(p, st) : halo::launch<256, false, 2>(p, st);
 }
 
 extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
@@ -1070,11 +1073,111 @@ extern "C" int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const i
                                      const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
                                      const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin,
                                      void* ws, size_t ws_bytes, const void* head_w_packed, const float* head_bias,
-                                     const int32_t* coords, int d, int B, int Nx, int Ny, int Nz, float tau,
-                                     uint8_t* out_bits, void* stream) {
-  (void)B;
-  const HeadArgs h{head_w_packed, head_bias, coords, d, Nx, Ny, Nz, tau, out_bits};
+                                     float tau, uint64_t* row_bits, void* stream) {
+  const HeadArgs h{head_w_packed, head_bias, tau, reinterpret_cast<unsigned long long*>(row_bits)};
   // the conv's own output is consumed in the epilogue: y is never written
   return halo_conv(x, ldx, x_rows, nbr, lnbr, halo_rows, halo_n, tile_masks, n_dev, cap, w_packed, 64, 1, bias, cin, 64,
-                   FPVS_ACT_RELU, out_bits, 64, 0, ws, ws_bytes, stream, &h);
+                   FPVS_ACT_RELU, row_bits, 64, 0, ws, ws_bytes, stream, &h);
+}
+
+namespace fpvs {
+namespace halo {
+// Per-row head bits -> the packed froxel grid (d = 4).  Block = (b, cell row
+// cy, RZ cells of z); its cells' 64-bit masks are staged in shared memory
+// (level-0 index volume, coalesced along z, read before the PDL wait: it is
+// the map kernels' output), then thread (z cell, 32-froxel word w) assembles
+// the 16 words of its 8 cells' (ly, lz) voxel rows: every word of the grid is
+// written exactly once, no atomics and no clear.
+constexpr int RZ = 16;
+__device__ __forceinline__ unsigned long long ld_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+struct RowBitsArgs {
+  const unsigned long long* row_bits;
+  const int* index_vol;
+  int B, X, Y, Z, Nx, Ny, Nz;
+  uint32_t* out;
+};
+
+__global__ void __launch_bounds__(128) rowbits_grid_kernel(const RowBitsArgs a) {
+  extern __shared__ unsigned long long s_rb[];  // [RZ][X + 1]
+  const int nzc = (a.Z + RZ - 1) / RZ;
+  int blk = blockIdx.x;
+  const int zc = blk % nzc;
+  blk /= nzc;
+  const int cy = blk % a.Y, b = blk / a.Y;
+  const int cz0 = zc * RZ, nz = min(RZ, a.Z - cz0);
+  const int ld = a.X + 1;
+  const int cells = a.X * RZ;
+  constexpr int kPre = 8;
+  int idx[kPre];
+#pragma unroll
+  for (int k = 0; k < kPre; ++k) {
+    const int c = threadIdx.x + k * 128, cx = c / RZ, czl = c % RZ;
+    idx[k] = (c < cells && czl < nz) ? __ldg(a.index_vol + (((long long)b * a.X + cx) * a.Y + cy) * a.Z + cz0 + czl) : -1;
+  }
+  pdl_wait();  // row_bits: the previous launch's output
+  if (threadIdx.x == 0) pdl_trigger();
+  for (int c0 = 0; c0 < cells; c0 += kPre * 128) {
+    if (c0) {
+#pragma unroll
+      for (int k = 0; k < kPre; ++k) {
+        const int c = c0 + threadIdx.x + k * 128, cx = c / RZ, czl = c % RZ;
+        idx[k] = (c < cells && czl < nz)
+                     ? __ldg(a.index_vol + (((long long)b * a.X + cx) * a.Y + cy) * a.Z + cz0 + czl) : -1;
+      }
+    }
+    // all gathers in flight before the first shared-memory store
+    unsigned long long m[kPre];
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) m[k] = idx[k] >= 0 ? ld_u64(a.row_bits + idx[k]) : 0ull;
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) {
+      const int c = c0 + threadIdx.x + k * 128;
+      if (c < cells) s_rb[(c % RZ) * ld + c / RZ] = m[k];
+    }
+  }
+  __syncthreads();
+  const int wpr = a.Nx >> 5;  // 32-froxel words per voxel row
+  const long long plane = (long long)wpr * a.Ny * a.Nz;
+  for (int t = threadIdx.x; t < nz * wpr; t += 128) {
+    const int w = t % wpr, czl = t / wpr;
+    unsigned long long m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = s_rb[czl * ld + 8 * w + i];
+    uint32_t* dst = a.out + b * plane + w + (long long)wpr * (4 * cy + (long long)a.Ny * 4 * (cz0 + czl));
+#pragma unroll
+    for (int lz = 0; lz < 4; ++lz)
+#pragma unroll
+      for (int ly = 0; ly < 4; ++ly) {
+        const int sh = 4 * (ly + 4 * lz);
+        uint32_t word = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) word |= (uint32_t)((m[i] >> sh) & 0xFull) << (4 * i);
+        dst[(long long)wpr * (ly + (long long)a.Ny * lz)] = word;
+      }
+  }
+}
+}  // namespace halo
+}  // namespace fpvs
+
+extern "C" int fpvs_rowbits_to_grid(const uint64_t* row_bits, const int32_t* index_vol, int B, int Nx, int Ny, int Nz,
+                                    int d, uint8_t* out_bits, void* stream) {
+  FPVS_CHECK_ARG(row_bits && index_vol && out_bits, "null pointer");
+  FPVS_CHECK_ARG(d == 4, "fpvs_rowbits_to_grid: d = 4 (64 bits per cell), got %d", d);
+  FPVS_CHECK_ARG(B >= 1 && Nx > 0 && Ny > 0 && Nz > 0 && Nx % 32 == 0 && Ny % 4 == 0 && Nz % 4 == 0,
+                 "grid must be B x Nx x Ny x Nz with N_x %% 32 == 0 and N_y, N_z %% 4 == 0");
+  FPVS_CHECK_ARG(((uintptr_t)out_bits & 3) == 0, "out_bits must be 4-byte aligned");
+  halo::RowBitsArgs a{reinterpret_cast<const unsigned long long*>(row_bits), index_vol, B, Nx / 4, Ny / 4, Nz / 4,
+                      Nx, Ny, Nz, reinterpret_cast<uint32_t*>(out_bits)};
+  const int nzc = (a.Z + halo::RZ - 1) / halo::RZ;
+  const long long blocks = (long long)B * a.Y * nzc;
+  const size_t smem = (size_t)halo::RZ * (a.X + 1) * 8;
+  FPVS_CHECK_ARG(blocks < (1LL << 31) && smem <= 48 * 1024, "grid too large (N_x <= 1024)");
+  cudaError_t e = launch_kernel(halo::rowbits_grid_kernel, dim3((unsigned)blocks), dim3(128), smem, as_stream(stream), a);
+  if (e != cudaSuccess) return set_error(FPVS_ECUDA, "fpvs_rowbits_to_grid: %s", cudaGetErrorString(e));
+  FPVS_CHECK_LAUNCH("fpvs_rowbits_to_grid");
+  return FPVS_OK;
 }

@@ -132,10 +132,12 @@ class UNetPlan:
         # 27-tap layers with 64-multiple channels run the halo-cached kernel
         # (fpvs_spconv_halo); FPVS_HALO=0 keeps them on the plain gather-GEMM
         self.use_halo = net.precision == "bf16" and os.environ.get("FPVS_HALO", "1") != "0"
-        # the level-0 halo tables (needed by the first conv) come out of the
-        # fused map build itself; levels 1 and 2 get theirs on the side stream
+        # the halo tables come out of the fused map build's K3 for the levels in
+        # FPVS_MAPS_HALO (default all three: 4 us per frame better than building
+        # levels 1 and 2 on the side stream, tools/frame_variant.py)
+        self.maps_halo = tuple(int(c) for c in os.environ.get("FPVS_MAPS_HALO", "012")) if self.use_halo else ()
         self.maps = sp.LevelMaps([self.L0, self.L1, self.L2], [self.down01, self.down12], [self.up10, self.up21],
-                                 self.grid_dims, d, halo_levels=(0,) if self.use_halo else ()) \
+                                 self.grid_dims, d, halo_levels=self.maps_halo) \
             if d in (1, 2, 4, 8) else None
         self.level_of = {"enc0a": self.L0, "enc0b": self.L0, "dec0a": self.L0, "dec0b": self.L0,
                          "enc1a": self.L1, "enc1b": self.L1, "dec1a": self.L1, "dec1b": self.L1,
@@ -149,6 +151,8 @@ class UNetPlan:
         self.overlap = True  # side-stream map tables (see build_maps); device_stage_times turns it off
         # the 1x1x1 head fused into dec0b (FPVS_FUSE_HEAD=0 keeps the stand-alone head launch)
         self.fuse_head = net.precision == "bf16" and os.environ.get("FPVS_FUSE_HEAD", "1") != "0"
+        # the fused head's per-row 64-bit cell masks (fpvs_rowbits_to_grid writes the grid from them)
+        self.row_bits = torch.empty(k0, dtype=torch.int64, device=device) if self.fuse_head else None
         self._side = None
         self._side_pending = False
         if self.use_halo:
@@ -216,14 +220,15 @@ class UNetPlan:
         if self.use_halo:
             if self._halo_builder is None:
                 self._halo_builder = sp.HaloBuilder([self.L0])
-                self._halo_builder_coarse = sp.HaloBuilder([self.L1, self.L2])
+                side = [lv for i, lv in ((1, self.L1), (2, self.L2)) if self.maps is None or i not in self.maps_halo]
+                self._halo_builder_coarse = sp.HaloBuilder(side) if side else None
             if self.maps is None:
                 self._halo_builder.run()  # level 0: needed by the first conv (else built by the fused maps)
         # the up-sort tables and the level-1/2 halo tables are first used by
         # enc1a / up21: with ``overlap`` they run on a side stream, filling SMs
         # the level-0 convs leave idle at their tails (joined before enc1a)
         torch = _torch()
-        side = self.overlap and (self.use_upsort or self.use_halo)
+        side = self.overlap and (self.use_upsort or (self.use_halo and self._halo_builder_coarse is not None))
         if side:
             if self._side is None:
                 self._side = torch.cuda.Stream()
@@ -239,7 +244,7 @@ class UNetPlan:
                 if self._up_sorter is None:
                     self._up_sorter = sp.UpSorter([(self.L1, self.up21), (self.L0, self.up10)])
                 self._up_sorter.run()
-            if self.use_halo:
+            if self.use_halo and self._halo_builder_coarse is not None:
                 self._halo_builder_coarse.run()
         if side:
             self._ev_side.record(self._side)
@@ -263,9 +268,20 @@ class UNetPlan:
         d3 = net.d ** 3
         out = []
         fused = maps and self.maps is not None
+        # the head fused into dec0b's epilogue (fpvs_spconv_halo_head): the
+        # activations never leave the SM and each active cell's 64 threshold
+        # bits go out as one word, which fpvs_rowbits_to_grid turns into every
+        # word of the output grid (no clear); taken for thresholded bits only
+        # (probabilities / logits keep the stand-alone head)
+        hc0 = self.halo_cfg.get("dec0b")
+        nx, ny, nz = self.grid_dims
+        fuse_head = (self.fuse_head and fused and hc0 is not None and hc0 == (64, 1) and c0 == 64 and net.d == 4
+                     and nx % 32 == 0 and probs is None and logits is None and 0.0 < float(tau) < 1.0)
         if fused:
-            # maps + level-0 features + clearing the output grid: three launches
-            out.append(("maps", lambda: self.build_maps(bits, gather=True, clear=out_bits)))
+            # maps + level-0 features (+ clearing the output grid for the
+            # stand-alone head's scatter): three launches
+            clear = None if fuse_head else out_bits
+            out.append(("maps", lambda: self.build_maps(bits, gather=True, clear=clear)))
         else:
             if maps:
                 out.append(("maps", lambda: self.build_maps(bits)))
@@ -303,23 +319,18 @@ class UNetPlan:
         conv("dec1b", self.t1a, c1, L1.nbr, 27, L1, self.t1b, c1, masks=m1)
         conv("up10", self.t1b, c1, self.up10, 8, L0, self.buf0, 2 * c0, c0, um10)       # U0 -> buf0[:, c0:]
         conv("dec0a", self.buf0, 2 * c0, L0.nbr, 27, L0, self.t0a, c0, masks=m0)
-        hc0 = self.halo_cfg.get("dec0b")
-        # the head fused into dec0b's epilogue (fpvs_spconv_halo_head): the
-        # activations never leave the SM; taken for thresholded bits only
-        # (probabilities / logits keep the stand-alone head)
-        fuse_head = (self.fuse_head and fused and hc0 is not None and hc0 == (64, 1) and c0 == 64 and net.d == 4
-                     and probs is None and logits is None and 0.0 < float(tau) < 1.0)
         if fuse_head:
             def dec0b_head():
                 hl = L["head"]
                 ht = L0.extra["halo"]
                 ws = self.halo_ws[id(L0)]
-                nx, ny, nz = self.grid_dims
                 _lib.call("fpvs_spconv_halo_head", _lib.ptr(self.t0a), c0, self.t0a.shape[0], _lib.ptr(L0.nbr),
                           _lib.ptr(ht["lnbr"]), _lib.ptr(ht["rows"]), _lib.ptr(ht["n"]), _lib.ptr(m0), _lib.ptr(L0.n),
                           L0.cap, _lib.ptr(L["dec0b"].packed(64)), _lib.ptr(L["dec0b"].b), c0, _lib.ptr(ws), ws.numel(),
-                          _lib.ptr(hl.packed(64)), _lib.ptr(hl.b), _lib.ptr(L0.coords), net.d, self.B, nx, ny, nz,
-                          float(tau), _lib.ptr(out_bits), _lib.stream_ptr())
+                          _lib.ptr(hl.packed(64)), _lib.ptr(hl.b), float(tau), _lib.ptr(self.row_bits),
+                          _lib.stream_ptr())
+                _lib.call("fpvs_rowbits_to_grid", _lib.ptr(self.row_bits), _lib.ptr(L0.index_vol), self.B, nx, ny, nz,
+                          net.d, _lib.ptr(out_bits), _lib.stream_ptr())
             out.append(("dec0b", dec0b_head))
             return out
         conv("dec0b", self.t0a, c0, L0.nbr, 27, L0, self.t0b, c0, masks=m0)

@@ -132,7 +132,8 @@ def test_fused_head_equals_standalone_head():
         outs = []
         for fuse in (True, False):
             plan.fuse_head = fuse
-            out = torch.empty(occ.size // 8, dtype=torch.uint8, device="cuda")
+            # garbage in the output grid: the fused path writes every word (no clear)
+            out = torch.full((occ.size // 8,), 0xA5, dtype=torch.uint8, device="cuda")
             names = [n for n, _ in plan.stages(bits, out, 0.5)]
             # fused only where dec0b runs unsplit 64-wide tiles (the 256^3 frame)
             assert ("head" in names) != (fuse and dims[0] == 256)
@@ -141,3 +142,39 @@ def test_fused_head_equals_standalone_head():
             outs.append(out.cpu().numpy())
         assert np.array_equal(outs[0], outs[1]), (seed, int(np.unpackbits(outs[0] ^ outs[1]).sum()))
         assert np.unpackbits(outs[0]).sum() > 0
+
+
+def test_rowbits_to_grid_matches_dense_scatter():
+    """fpvs_rowbits_to_grid: per-row 64-bit cell masks (bit lx + 4 ly + 16 lz)
+    scattered through the level-0 index volume into the packed froxel grid,
+    every word written (inactive cells and garbage in the buffer -> 0)."""
+    import torch
+    from paper_2509_24677_b200 import _lib
+    rng = np.random.default_rng(5)
+    B, dims = 2, (64, 32, 48)
+    X, Y, Z = (n // 4 for n in dims)
+    active = rng.random((B, X, Y, Z)) < 0.3
+    index_vol = np.full((B, X, Y, Z), -1, np.int32)
+    n = int(active.sum())
+    index_vol[active] = np.arange(n, dtype=np.int32)
+    row_bits = rng.integers(0, 2**63, size=n, dtype=np.int64) ^ rng.integers(0, 2, size=n, dtype=np.int64) << 63
+    dense = np.zeros((B,) + dims, bool)
+    b, cx, cy, cz = np.nonzero(active)
+    rb = row_bits.view(np.uint64)
+    for k in range(64):
+        lx, ly, lz = k % 4, (k // 4) % 4, k // 16
+        on = ((rb >> np.uint64(k)) & np.uint64(1)).astype(bool)
+        dense[b[on], 4 * cx[on] + lx, 4 * cy[on] + ly, 4 * cz[on] + lz] = True
+    ref = np.concatenate([FroxelGrid.from_dense(dense[i]).bits for i in range(B)])
+    out = torch.full((ref.size,), 0x5A, dtype=torch.uint8, device="cuda")
+    rbt = torch.from_numpy(row_bits).cuda()
+    ivt = torch.from_numpy(index_vol.ravel()).cuda()
+    _lib.call("fpvs_rowbits_to_grid", _lib.ptr(rbt), _lib.ptr(ivt), B, *dims, 4, _lib.ptr(out), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref)
+    # argument checks: d != 4 and N_x % 32 != 0 are rejected
+    with pytest.raises(Exception):
+        _lib.call("fpvs_rowbits_to_grid", _lib.ptr(rbt), _lib.ptr(ivt), B, *dims, 2, _lib.ptr(out), _lib.stream_ptr())
+    with pytest.raises(Exception):
+        _lib.call("fpvs_rowbits_to_grid", _lib.ptr(rbt), _lib.ptr(ivt), B, 48, 32, 48, 4, _lib.ptr(out),
+                  _lib.stream_ptr())
