@@ -256,6 +256,20 @@ int fpvs_spconv_tc_scatter(const void* x, int ldx, int x_rows, const int32_t* nb
                            const float* bias, int cin, int cout, int act,
                            void* y, int ldy, int col_off, void* stream);
 
+/* The k2s2 transposed (up) conv as ONE dense GEMM over the coarse rows
+ * (the config-2 U-Net's up21 / up10, oracle/sparse.py:196 up_conv; weight rows
+ * k = j Cin + ci as neural.py:163-166):
+ * Y = act(X_coarse W' + b') with W'[ci][j Cout + co] = W[j Cin + ci][co]
+ * (w_packed: fpvs_pack_weights_tc of W' as a K = 1, Cin -> 8 Cout conv;
+ * bias8 = b tiled 8 times), and column block j of coarse row r is written to
+ * fine row child_rows[8 r + j] of y (the coarse level's down table: its child
+ * in parity class j = 4(x&1) + 2(y&1) + (z&1); -1 = no child, skipped).  Each
+ * fine row has exactly one parent, so every active fine row is written once.
+ * Bit-identical to the gathered up conv (same operands, same K order). */
+int fpvs_spconv_tc_upblocks(const void* x, int ldx, int x_rows, const int32_t* n_coarse_dev, int cap_coarse,
+                            const void* w_packed, int bn, const float* bias8, int cin, int cout, int act,
+                            const int32_t* child_rows, void* y, int ldy, int col_off, void* stream);
+
 /* Halo-cached submanifold conv (spconv_halo.cu), same math as
  * fpvs_spconv_tc with K = 27 (neural.py:187-219 on the active set), for
  * Cin and Cout multiples of 64.  Each 128-row tile's distinct neighbour rows

@@ -411,14 +411,18 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, 1) spconv_halo_kernel(con
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u;
     uint32_t sc0 = 0, gc = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      if (lane == 0 && q4 == 0 && bg == 0) HTS(7800 + 2 * gc);
       Unit U;
       get_unit(p, u, cpo, mtiles, U, s_units);
+      if (lane == 0 && q4 == 0 && bg == 0) HTS(7801 + 2 * gc);
       const int nq = U.q1 - U.q0;
       for (int c = U.q0 / U.npres; nq > 0 && c * U.npres < U.q1; ++c) {
         const int qs = max(U.q0, c * U.npres), qe = min(U.q1, (c + 1) * U.npres);
         const int hb = gc % C::NHB;
         const uint32_t hph = (gc / C::NHB) & 1;
+        if (lane == 0 && q4 == 0 && bg == 0) HTS(6000 + 4 * gc);
         mbar_wait(smem_u32(hmeta + hb), hph);
+        if (lane == 0 && q4 == 0 && bg == 0) HTS(6001 + 4 * gc);
         if (gc == 0) {
           // the CTA's first halo: nothing to overlap it with, so the 8 builder
           // warps copy it together with the 2 loader warps (10 warps instead of 2)
@@ -435,8 +439,12 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, 1) spconv_halo_kernel(con
           }
           cp_async_mbar_arrive_noinc(smem_u32(hfull + hb));
         } else {
-          mbar_arrive(smem_u32(hfull + hb));  // builders add no copies to later halos
+          // builders add no copies to later halos: one counted arrival per warp
+          // (measured ~4 us per frame faster than 512 single-thread arrivals)
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cnt(smem_u32(hfull + hb), 32u);
         }
+        if (lane == 0 && q4 == 0 && bg < 2) HTS(257 + 4 * gc + 2 * bg);
         mbar_wait(smem_u32(hfull + hb), hph);
         if (lane == 0 && q4 == 0 && bg < 2) HTS(256 + 4 * gc + 2 * bg);
         const uint8_t* hbuf = smem + hb * HBUF;
@@ -543,8 +551,10 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, 1) spconv_halo_kernel(con
           if (lane == 0) mbar_arrive(smem_u32(full + stage));
           if (lane == 0 && q4 == 0 && bg < 2 && st < 1400) HTS(1024 + 2 * st + bg);
         }
+        if (lane == 0 && q4 == 0 && bg == 0) HTS(6002 + 4 * gc);
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(hempty + hb));
+        if (lane == 0 && q4 == 0 && bg == 0) HTS(6003 + 4 * gc);
         ++gc;
       }
       const uint32_t nst = (nq + C::G - 1) / C::G;

@@ -52,6 +52,11 @@ struct Params {
   __nv_bfloat16* y;
   int ldy, col_off;
   const int* out_rows;  // tile row -> output row (-1 = skip); NULL = identity
+  // column-block scatter (k2s2 up conv as one dense GEMM over the coarse rows):
+  // columns [j blk_w, (j + 1) blk_w) of row r go to output row blk_rows[8 r + j]
+  // (the coarse level's down table: its child in parity class j; -1 = skip)
+  const int* blk_rows;
+  int blk_w;
   const __nv_bfloat16* mask;  // act == FPVS_ACT_MASK: out = z * (mask[row][col] > 0) (relu' of the layer below)
   int ldm;
   // head epilogue
@@ -441,20 +446,28 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
       const int row = mt * BM + r;
       const bool valid = row < n;
       const int col0 = nb * BN;
-      const long long orow = !valid ? -1 : p.out_rows ? (long long)__ldg(p.out_rows + row) : (long long)row;
+      const long long orow0 = !valid ? -1 : p.out_rows ? (long long)__ldg(p.out_rows + row) : (long long)row;
       if (!p.head) {
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += 32) {
           float v[32];
           tmem_ld32(tmem_base + tlane + acc * BN + cb, v);
-          if (!valid || col0 + cb >= p.cout || orow < 0) continue;
+          if (!valid || col0 + cb >= p.cout) continue;
+          long long orow = orow0;
+          int ocol = col0 + cb;
+          if (p.blk_rows) {
+            const int j = ocol / p.blk_w;
+            ocol -= j * p.blk_w;
+            orow = __ldg(p.blk_rows + (long long)row * 8 + j);
+          }
+          if (orow < 0) continue;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             float z = v[i] + s_bias[col0 + cb + i];
             v[i] = p.act == FPVS_ACT_RELU ? fmaxf(z, 0.f) : z;
           }
           if (p.act == FPVS_ACT_MASK) {
-            const uint4* mk = reinterpret_cast<const uint4*>(p.mask + orow * p.ldm + col0 + cb);
+            const uint4* mk = reinterpret_cast<const uint4*>(p.mask + orow * p.ldm + ocol);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const uint4 m4 = __ldg(mk + i);
@@ -466,7 +479,7 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
               }
             }
           }
-          uint4* dst = reinterpret_cast<uint4*>(p.y + orow * p.ldy + p.col_off + col0 + cb);
+          uint4* dst = reinterpret_cast<uint4*>(p.y + orow * p.ldy + p.col_off + ocol);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             dst[i] = make_uint4(pack_bf16x2(v[8 * i + 0], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
@@ -763,6 +776,30 @@ extern "C" int fpvs_spconv_tc_scatter(const void* x, int ldx, int x_rows, const 
   p.ldy = ldy;
   p.col_off = col_off;
   p.out_rows = out_rows;
+  return tc::dispatch(p, bn, as_stream(stream));
+}
+
+extern "C" int fpvs_spconv_tc_upblocks(const void* x, int ldx, int x_rows, const int32_t* n_coarse_dev, int cap_coarse,
+                                       const void* w_packed, int bn, const float* bias8, int cin, int cout, int act,
+                                       const int32_t* child_rows, void* y, int ldy, int col_off, void* stream) {
+  tc::Params p;
+  const int cout8 = 8 * cout;
+  bn = resolve_bn(bn, cout8);
+  FPVS_CHECK_ARG(bn > 0, "tile width must be 0 (auto), 32, 64, 128 or 256");
+  FPVS_CHECK_ARG(child_rows, "null child_rows");
+  FPVS_CHECK_ARG(cout % 32 == 0 && cout8 <= 1024, "up blocks need Cout %% 32 == 0 and 8 Cout <= 1024, got %d", cout);
+  int rc = tc_common(p, x, ldx, x_rows, nullptr, 1, nullptr, n_coarse_dev, cap_coarse, w_packed, bias8, cin, cout8, bn);
+  if (rc) return rc;
+  FPVS_CHECK_ARG(y, "null output");
+  FPVS_CHECK_ARG(ldy % 8 == 0 && col_off % 8 == 0 && ldy >= col_off + cout, "bad output leading dimension");
+  FPVS_CHECK_ARG(act == FPVS_ACT_NONE || act == FPVS_ACT_RELU, "tcgen05 store epilogue supports none/relu");
+  if (cap_coarse <= 0) return FPVS_OK;
+  p.act = act;
+  p.y = (__nv_bfloat16*)y;
+  p.ldy = ldy;
+  p.col_off = col_off;
+  p.blk_rows = child_rows;
+  p.blk_w = cout;
   return tc::dispatch(p, bn, as_stream(stream));
 }
 

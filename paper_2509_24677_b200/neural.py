@@ -380,6 +380,22 @@ def packed_cache(layer, bn: int = 0, stream=None):
     return layer._packed[bn]
 
 
+def packed_upblocks_cache(layer, bn: int = 0, stream=None):
+    """The k2s2 up layer's weights as one Cin x 8 Cout matrix (column block j =
+    parity class j's slice, fpvs_spconv_tc_upblocks) and its bias tiled 8
+    times; built once per update."""
+    if layer._packed is None:
+        layer._packed = {}
+    key = ("upblocks", bn)
+    if key not in layer._packed:
+        cin, cout = layer.spec.in_channels, layer.spec.out_channels
+        if layer.taps != 8:
+            raise ValueError(f"up blocks need a k = 2 layer, got {layer.taps} taps")
+        w8 = layer.w.view(8, cin, cout).permute(1, 0, 2).reshape(cin, 8 * cout).contiguous()
+        layer._packed[key] = (pack_tc(w8, 1, cin, 8 * cout, bn, stream), layer.b.repeat(8).contiguous())
+    return layer._packed[key]
+
+
 def packed_dgrad_cache(layer, bn: int = 0, stream=None):
     """The layer's dgrad weight image (mirrored offsets, per-offset Wᵀ), built once per update."""
     if layer._packed is None:

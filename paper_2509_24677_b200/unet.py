@@ -29,7 +29,7 @@ import numpy as np
 
 from . import _lib
 from . import sparse as sp
-from .neural import halo_ok, packed_cache, pick_bn, run_conv, run_head
+from .neural import halo_ok, packed_cache, packed_upblocks_cache, pick_bn, run_conv, run_head
 
 
 def _torch():
@@ -146,7 +146,12 @@ class UNetPlan:
         self.halo_ws = None
         self._halo_builder = None
         # up convs run on parity-sorted rows (one weight slice per tile); FPVS_UPSORT=0 disables
-        self.use_upsort = net.precision == "bf16" and os.environ.get("FPVS_UPSORT", "1") != "0"
+        # the up convs as one dense GEMM over the coarse rows with a column-block
+        # scatter through the down table (fpvs_spconv_tc_upblocks: no sort, no
+        # gather); FPVS_UPBLOCKS=0 keeps the parity-sorted gather-GEMM
+        self.use_upblocks = net.precision == "bf16" and os.environ.get("FPVS_UPBLOCKS", "1") != "0"
+        self.use_upsort = (net.precision == "bf16" and not self.use_upblocks
+                           and os.environ.get("FPVS_UPSORT", "1") != "0")
         self._up_sorter = None
         self.overlap = True  # side-stream map tables (see build_maps); device_stage_times turns it off
         # the 1x1x1 head fused into dec0b (FPVS_FUSE_HEAD=0 keeps the stand-alone head launch)
@@ -294,6 +299,15 @@ class UNetPlan:
                     self._join_side()
                 hc = self.halo_cfg.get(name) if K == 27 else None
                 halo = (hc[0], hc[1], self.halo_ws[id(lv)]) if hc else None
+                if self.use_upblocks and name in ("up21", "up10"):
+                    coarse, child = (L2, self.down12) if name == "up21" else (L1, self.down01)
+                    layer = L[name]
+                    # 256-wide tiles (measured faster than 128 / 64, tools/frame_variant.py)
+                    w8, b8 = packed_upblocks_cache(layer, 256)
+                    _lib.call("fpvs_spconv_tc_upblocks", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(coarse.n), coarse.cap,
+                              _lib.ptr(w8), 256, _lib.ptr(b8), layer.spec.in_channels, layer.spec.out_channels,
+                              _lib.ACT["relu"], _lib.ptr(child), _lib.ptr(y), ldy, off, _lib.stream_ptr())
+                    return
                 us = lv.extra.get("upsort") if (self.use_upsort and name in ("up21", "up10")) else None
                 if us is not None:
                     run_conv(L[name], x, ldx, us["table"], K, us["n"], us["cap"], y, ldy, off, P, act="relu",

@@ -178,3 +178,37 @@ def test_rowbits_to_grid_matches_dense_scatter():
     with pytest.raises(Exception):
         _lib.call("fpvs_rowbits_to_grid", _lib.ptr(rbt), _lib.ptr(ivt), B, 48, 32, 48, 4, _lib.ptr(out),
                   _lib.stream_ptr())
+
+
+def test_up_blocks_equal_sorted_up_conv():
+    """up21 / up10 as one dense GEMM over the coarse rows with the column-block
+    scatter (fpvs_spconv_tc_upblocks) write exactly the rows of the
+    parity-sorted gather-GEMM (same operands, same K order), and the frame's
+    bits are unchanged."""
+    import os
+    import torch
+    from paper_2509_24677_b200.unet import PvsUNet
+    occ = synth.box_grid((128, 128, 128), 600, 1, 12, 2)
+    bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+    res = []
+    for flag in ("1", "0"):
+        os.environ["FPVS_UPBLOCKS"] = flag
+        try:
+            plan = PvsUNet(seed=1, precision="bf16").plan(1, occ.shape)
+        finally:
+            os.environ.pop("FPVS_UPBLOCKS", None)
+        assert plan.use_upblocks == (flag == "1")
+        out = torch.empty(occ.size // 8, dtype=torch.uint8, device="cuda")
+        stages = plan.stages(bits, out, 0.5)
+        for name, fn in stages:
+            fn()
+            if name == "up10":
+                torch.cuda.synchronize()
+                n0, n1 = plan.L0.count(), plan.L1.count()
+                snap = (plan.buf1[:n1].clone(), plan.buf0[:n0].clone())
+        torch.cuda.synchronize()
+        res.append((snap, out.clone()))
+    (a1, a0), ab = res[0]
+    (b1, b0), bb = res[1]
+    assert torch.equal(a1, b1) and torch.equal(a0, b0)
+    assert torch.equal(ab, bb)

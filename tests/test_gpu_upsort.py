@@ -41,6 +41,10 @@ def _config2_plan():
     net = PvsUNet(seed=1)
     plan = net.plan(1, occ.shape)
     plan.build_maps(bits)
+    # the frame itself now runs the up convs as dense column-block GEMMs
+    # (fpvs_spconv_tc_upblocks); the parity sort stays an exported op
+    from paper_2509_24677_b200 import sparse as sp
+    sp.UpSorter([(plan.L1, plan.up21), (plan.L0, plan.up10)]).run()
     return net, plan, bits, occ
 
 
@@ -102,12 +106,41 @@ def test_sorted_up_conv_bit_identical():
         assert torch.equal(a[:n], b[:n]), name
 
 
+def test_up_blocks_bit_identical():
+    """fpvs_spconv_tc_upblocks (dense coarse-row GEMM, column block j -> child
+    in parity class j through the down table) == the gathered up conv."""
+    import torch
+    from paper_2509_24677_b200 import _lib
+    from paper_2509_24677_b200.neural import packed_upblocks_cache, run_conv
+    net, plan, bits, _ = _config2_plan()
+    for name, coarse, fine, up, down, cin, cout in (("up21", plan.L2, plan.L1, plan.up21, plan.down12, 256, 128),
+                                                    ("up10", plan.L1, plan.L0, plan.up10, plan.down01, 128, 64)):
+        layer = net.layers[name]
+        nc = coarse.count()
+        x = torch.zeros((coarse.cap, cin), dtype=torch.bfloat16, device="cuda")
+        x[:nc] = torch.relu(torch.randn((nc, cin), device="cuda")).bfloat16()
+        a = torch.zeros((fine.cap, 2 * cout), dtype=torch.bfloat16, device="cuda")
+        b = torch.full_like(a, 7.0)
+        run_conv(layer, x, cin, up, 8, fine.n, fine.cap, a, 2 * cout, cout, "bf16", act="relu",
+                 masks=coarse.extra["up_masks"])
+        for bn in (256, 128):
+            w8, b8 = packed_upblocks_cache(layer, bn)
+            _lib.call("fpvs_spconv_tc_upblocks", _lib.ptr(x), cin, x.shape[0], _lib.ptr(coarse.n), coarse.cap,
+                      _lib.ptr(w8), bn, _lib.ptr(b8), cin, cout, _lib.ACT["relu"], _lib.ptr(down), _lib.ptr(b),
+                      2 * cout, cout, _lib.stream_ptr())
+            torch.cuda.synchronize()
+            n = fine.count()
+            assert torch.equal(a[:n, cout:], b[:n, cout:]), (name, bn)
+            assert bool((b[:n, :cout] == 7.0).all())  # columns outside [col_off, col_off + Cout) untouched
+
+
 def test_unet_with_and_without_up_sort():
     import torch
     from paper_2509_24677_b200.unet import PvsUNet
     net, plan, bits, occ = _config2_plan()
     other = net.plan(1, occ.shape)
     other.use_upsort = False
+    other.use_upblocks = False  # plain gathered up convs
     la = torch.zeros((plan.L0.cap, 64), device="cuda")
     lb = torch.zeros_like(la)
     oa = torch.empty(occ.size // 8, dtype=torch.uint8, device="cuda")

@@ -67,3 +67,17 @@ for name, abl in itertools.product(os.environ.get("LAYERS", "enc0b,enc1a").split
         print(f"   st {i:3d}: mma wait {mwait0[i] - base:7d} start {mstart[i] - base:7d} commit {mcommit[i] - base:7d} | "
               f"b0 pre {t[2000 + 2 * i] - base:7d} post {t[2800 + 2 * i] - base:7d} arr {t[1024 + 2 * i] - base:7d} | "
               f"b1 pre {t[2001 + 2 * i] - base:7d} post {t[2801 + 2 * i] - base:7d} arr {t[1025 + 2 * i] - base:7d}")
+    # per-halo (tile) events: loader hempty-wait end / meta landed / copies issued, builders' halo ready
+    print("  halo buffers (cycles from MMA start of stage 0):")
+    for gc in range(4):
+        ev = [t[16 + 3 * gc], t[17 + 3 * gc], t[18 + 3 * gc], t[256 + 4 * gc], t[258 + 4 * gc], t[257 + 4 * gc]]
+        if not ev[0]:
+            break
+        print(f"   halo {gc}: loader free {ev[0] - base:7d} meta {ev[1] - base:7d} issued {ev[2] - base:7d} | "
+              f"b0 at hfull-wait {ev[5] - base if ev[5] else 0:7d} ready {ev[3] - base:7d} b1 ready {ev[4] - base if ev[4] else 0:7d}")
+    print("  builder b0 per halo: " + " ".join(f"[top {t[6000 + 4 * g] - base} meta-ok {t[6001 + 4 * g] - base} "
+                                              f"loop-end {t[6002 + 4 * g] - base} hempty-arrived {t[6003 + 4 * g] - base} | next unit top {t[7802 + 2 * g] - base} "
+                                              f"got unit {t[7803 + 2 * g] - base}]" for g in range(3) if t[6000 + 4 * g]))
+    print("  unit boundaries (MMA): " + " ".join(f"u{k}: acc-wait {t[7601 + 2 * k] - base} -> {t[7000 + 2 * k] - base}, "
+                                                    f"done {t[7001 + 2 * k] - base}" for k in range(3) if t[7000 + 2 * k]))
+    print("  epilogue tile start: " + " ".join(str(t[7200 + 2 * k] - base) for k in range(3) if t[7200 + 2 * k]))

@@ -15,6 +15,7 @@ occ = synth.config2_grid(1)
 bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
 net = PvsUNet(seed=1, precision="bf16")
 plan = net.plan(1, occ.shape)
+plan.tune(bits)
 out = torch.empty(occ.size // 8, dtype=torch.uint8, device="cuda")
 for _ in range(frames):
     plan.run(bits, out, 0.5)
