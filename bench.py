@@ -13,7 +13,7 @@ halo tables), sparse interleave, 14 convs, head.
   step; device time from CUDA events on the launching stream, max over ranks.
 * ``e2e``: the same frames through ``FramePipeline.infer_stream`` — pinned
   host packed grid -> H2D -> frame -> D2H packed PVS for every step, every
-  copy inside the timed region; up to E2E_INFLIGHT = 3 frames compute
+  copy inside the timed region; up to E2E_INFLIGHT = 4 frames compute
   concurrently on separate streams with separate buffers (each frame is
   still one bs1 pass).  ``e2e.latency_ms``: one frame in flight, pinned host
   in -> device -> packed PVS back on the host, synchronised per frame (the
@@ -69,7 +69,7 @@ sys.path.insert(0, ROOT)
 METRIC = "froxel grids/sec and ms/frame (256^3, bs1); % tensor-pipe peak"
 UNIT = "grids/s"
 E2E_FRAMES = 64
-E2E_INFLIGHT = 3  # frames computing concurrently in the streamed e2e (separate buffers per frame)
+E2E_INFLIGHT = 4  # frames computing concurrently in the streamed e2e (separate buffers per frame; tools/e2e_inflight.py: 3 -> 4 +1 %, 6 no better)
 WORKLOAD = "config2: 256^3 froxels, 4000 boxes (edges 1-12, seed 1), d=4, 3-level sparse U-Net 64/128/256, bf16"
 
 

@@ -68,6 +68,7 @@ struct Args {
   long long clear_bytes;
   unsigned* status_all;
   int status_words;
+  int reset_only;  // profiling (FPVS_LV_STOP = 2): K3 runs only the look-back reset
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -88,6 +89,8 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // active child (their arrays are cleared by K3 of the previous frame).
 template <int D, int W>
 __global__ void __launch_bounds__(kThreads) l0_flags_kernel(const Args a) {
+  // K2 is launched programmatically: let it take its tile tickets while we run
+  if (threadIdx.x == 0) pdl_trigger();
   extern __shared__ uint8_t s_flag[];  // [X][33]
   using T = typename std::conditional<W == 4, uint32_t, uint8_t>::type;
   const int X = a.L[0].X, Y = a.L[0].Y, Z = a.L[0].Z;
@@ -161,7 +164,11 @@ __global__ void __launch_bounds__(kThreads) compact_levels_kernel(const Args a) 
   while (l + 1 < a.nlev && (int)blockIdx.x >= a.tile_base[l + 1]) ++l;
   const LevelDev& L = a.L[l];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // the tile ticket counter was re-armed by K3 of the previous frame (complete
+  // before K1 started); the flags below are K1's output: wait for it
   if (tid == 0) s_tile = (int)atomicAdd(L.status + L.ntiles, 1u);
+  pdl_wait();
+  if (tid == 0) pdl_trigger();
   __syncthreads();
   const int tile = s_tile;
   const int X = L.X, Y = L.Y, Z = L.Z;
@@ -427,6 +434,9 @@ __device__ void gather_unit(const Args& a, int n, int tile) {
 constexpr int kClearChunk = kThreads * 64;  // bytes per clear unit
 
 __global__ void __launch_bounds__(kThreads) tables_kernel(const Args a) {
+  // programmatic launch: everything here reads K2's output.  No early trigger:
+  // the first conv's prologue reads the tile masks written here
+  pdl_wait();
   __shared__ uint32_t s_red[kThreads / 32];
   __shared__ __align__(16) int s_tab[kRows * 27];
   __shared__ __align__(16) halob::Smem s_halo;
@@ -439,7 +449,7 @@ __global__ void __launch_bounds__(kThreads) tables_kernel(const Args a) {
     for (int t = 0; t < T_COUNT; ++t)
       for (int l = 0; l < kMaxLev; ++l) {
         int c = 0;
-        if (l < a.nlev) {
+        if (l < a.nlev && (!a.reset_only || t == T_RESET)) {
           const LevelDev& L = a.L[l];
           if (t == T_SUBM && L.nbr) c = (s_nl[l] + kRows - 1) / kRows;
           if (t == T_DOWN && l > 0 && L.down) c = (s_nl[l] + kRows - 1) / kRows;
@@ -604,8 +614,12 @@ extern "C" int fpvs_levels_from_bits(const uint8_t* bits, int B, int Nx, int Ny,
   }
 #undef FPVS_K1
   FPVS_CHECK_LAUNCH("fpvs_levels_from_bits(flags)");
-  lv::compact_levels_kernel<<<tb, lv::kThreads, 0, s>>>(a);
+  const int stop = debug_knob("FPVS_LV_STOP");  // profiling builds: launch K1 (1) or K1 + K2 (2) only
+  if (stop == 1) return FPVS_OK;
+  cudaError_t e = launch_kernel(lv::compact_levels_kernel, dim3(tb), dim3(lv::kThreads), 0, s, a);
+  if (e != cudaSuccess) return set_error(FPVS_ECUDA, "fpvs_levels_from_bits(compact): %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("fpvs_levels_from_bits(compact)");
+  a.reset_only = stop == 2;
   // K3: one resident wave (a second wave of persistent blocks would serialise)
   static int k3_per_sm = 0;
   if (!k3_per_sm) {
@@ -613,7 +627,8 @@ extern "C" int fpvs_levels_from_bits(const uint8_t* bits, int B, int Nx, int Ny,
         k3_per_sm < 1)
       k3_per_sm = 1;
   }
-  lv::tables_kernel<<<kNumSMs * k3_per_sm, lv::kThreads, 0, s>>>(a);
+  e = launch_kernel(lv::tables_kernel, dim3(kNumSMs * k3_per_sm), dim3(lv::kThreads), 0, s, a);
+  if (e != cudaSuccess) return set_error(FPVS_ECUDA, "fpvs_levels_from_bits(tables): %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("fpvs_levels_from_bits(tables)");
   return FPVS_OK;
 }

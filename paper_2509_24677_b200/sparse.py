@@ -283,9 +283,12 @@ class LevelMaps:
     tables and tile masks bit for bit.
     """
 
-    def __init__(self, levels, downs, ups, grid_dims, d: int, with_nbr: bool = True, halo_levels=()):
+    def __init__(self, levels, downs, ups, grid_dims, d: int, with_nbr: bool = True, halo_levels=(),
+                 with_up: bool = True):
         """``halo_levels``: indices of levels whose halo tables (the halo-cached
-        conv's, ``_halo_tables``) are built in the same launch as their maps."""
+        conv's, ``_halo_tables``) are built in the same launch as their maps;
+        ``with_up`` False skips the up tables (the column-block up convs,
+        fpvs_spconv_tc_upblocks, read the down tables instead)."""
         import ctypes as C
         torch = _torch()
         self.levels, self.grid_dims, self.d = list(levels), tuple(grid_dims), d
@@ -306,7 +309,8 @@ class LevelMaps:
                 e.nbr, e.nbr_masks = _lib.ptr(lv.nbr), _lib.ptr(lv.nbr_masks)
             if i > 0:
                 e.down, e.down_masks = _lib.ptr(downs[i - 1]), _lib.ptr(lv.extra["down_masks"])
-                e.up, e.up_masks = _lib.ptr(ups[i - 1]), _lib.ptr(lv.extra["up_masks"])
+                if with_up:
+                    e.up, e.up_masks = _lib.ptr(ups[i - 1]), _lib.ptr(lv.extra["up_masks"])
             if i in halo_levels and with_nbr:
                 h = _halo_tables(lv)
                 e.halo_rows, e.halo_n, e.halo_lnbr = _lib.ptr(h["rows"]), _lib.ptr(h["n"]), _lib.ptr(h["lnbr"])

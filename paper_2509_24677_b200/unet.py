@@ -132,12 +132,18 @@ class UNetPlan:
         # 27-tap layers with 64-multiple channels run the halo-cached kernel
         # (fpvs_spconv_halo); FPVS_HALO=0 keeps them on the plain gather-GEMM
         self.use_halo = net.precision == "bf16" and os.environ.get("FPVS_HALO", "1") != "0"
+        # the up convs as one dense GEMM over the coarse rows with a column-block
+        # scatter through the down table (fpvs_spconv_tc_upblocks: no sort, no
+        # gather); FPVS_UPBLOCKS=0 keeps the parity-sorted gather-GEMM
+        self.use_upblocks = net.precision == "bf16" and os.environ.get("FPVS_UPBLOCKS", "1") != "0"
+        self.use_upsort = (net.precision == "bf16" and not self.use_upblocks
+                           and os.environ.get("FPVS_UPSORT", "1") != "0")
         # the halo tables come out of the fused map build's K3 for the levels in
         # FPVS_MAPS_HALO (default all three: 4 us per frame better than building
         # levels 1 and 2 on the side stream, tools/frame_variant.py)
         self.maps_halo = tuple(int(c) for c in os.environ.get("FPVS_MAPS_HALO", "012")) if self.use_halo else ()
         self.maps = sp.LevelMaps([self.L0, self.L1, self.L2], [self.down01, self.down12], [self.up10, self.up21],
-                                 self.grid_dims, d, halo_levels=self.maps_halo) \
+                                 self.grid_dims, d, halo_levels=self.maps_halo, with_up=not self.use_upblocks) \
             if d in (1, 2, 4, 8) else None
         self.level_of = {"enc0a": self.L0, "enc0b": self.L0, "dec0a": self.L0, "dec0b": self.L0,
                          "enc1a": self.L1, "enc1b": self.L1, "dec1a": self.L1, "dec1b": self.L1,
@@ -145,14 +151,7 @@ class UNetPlan:
         self.halo_cfg = {}
         self.halo_ws = None
         self._halo_builder = None
-        # up convs run on parity-sorted rows (one weight slice per tile); FPVS_UPSORT=0 disables
-        # the up convs as one dense GEMM over the coarse rows with a column-block
-        # scatter through the down table (fpvs_spconv_tc_upblocks: no sort, no
-        # gather); FPVS_UPBLOCKS=0 keeps the parity-sorted gather-GEMM
-        self.use_upblocks = net.precision == "bf16" and os.environ.get("FPVS_UPBLOCKS", "1") != "0"
-        self.use_upsort = (net.precision == "bf16" and not self.use_upblocks
-                           and os.environ.get("FPVS_UPSORT", "1") != "0")
-        self._up_sorter = None
+        self._up_sorter = None  # parity-sorted up tables (FPVS_UPBLOCKS=0 path; FPVS_UPSORT=0 disables)
         self.overlap = True  # side-stream map tables (see build_maps); device_stage_times turns it off
         # the 1x1x1 head fused into dec0b (FPVS_FUSE_HEAD=0 keeps the stand-alone head launch)
         self.fuse_head = net.precision == "bf16" and os.environ.get("FPVS_FUSE_HEAD", "1") != "0"

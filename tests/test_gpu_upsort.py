@@ -38,13 +38,18 @@ def _config2_plan():
     from paper_2509_24677_b200.unet import PvsUNet
     occ = synth.config2_grid(1)
     bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+    import os
     net = PvsUNet(seed=1)
-    plan = net.plan(1, occ.shape)
+    # the default frame runs the up convs as dense column-block GEMMs
+    # (fpvs_spconv_tc_upblocks) and builds no up tables; the parity-sorted
+    # path (up tables + fpvs_up_sort) stays available behind FPVS_UPBLOCKS=0
+    os.environ["FPVS_UPBLOCKS"] = "0"
+    try:
+        plan = net.plan(1, occ.shape)
+    finally:
+        os.environ.pop("FPVS_UPBLOCKS", None)
+    assert plan.use_upsort
     plan.build_maps(bits)
-    # the frame itself now runs the up convs as dense column-block GEMMs
-    # (fpvs_spconv_tc_upblocks); the parity sort stays an exported op
-    from paper_2509_24677_b200 import sparse as sp
-    sp.UpSorter([(plan.L1, plan.up21), (plan.L0, plan.up10)]).run()
     return net, plan, bits, occ
 
 
@@ -138,9 +143,13 @@ def test_unet_with_and_without_up_sort():
     import torch
     from paper_2509_24677_b200.unet import PvsUNet
     net, plan, bits, occ = _config2_plan()
-    other = net.plan(1, occ.shape)
+    import os
+    os.environ["FPVS_UPBLOCKS"] = "0"  # plain gathered up convs (up tables built by the maps)
+    try:
+        other = net.plan(1, occ.shape)
+    finally:
+        os.environ.pop("FPVS_UPBLOCKS", None)
     other.use_upsort = False
-    other.use_upblocks = False  # plain gathered up convs
     la = torch.zeros((plan.L0.cap, 64), device="cuda")
     lb = torch.zeros_like(la)
     oa = torch.empty(occ.size // 8, dtype=torch.uint8, device="cuda")
