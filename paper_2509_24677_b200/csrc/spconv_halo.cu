@@ -186,14 +186,16 @@ struct Unit {
   uint32_t mask;
 };
 
-template <int BN>
+template <int BN, int NBG = 2>
 struct Cfg {
   // chunks per stage: BN 64 runs 4 chunks (16 MMAs) per stage and commit, two
-  // stages deep; BN >= 128: one chunk per stage, deeper weight prefetch
-  static constexpr int G = BN == 64 ? 4 : BN < 64 ? 2 : 1;
+  // stages deep; BN >= 128: one chunk per stage, deeper weight prefetch; with
+  // four builder groups BN 128 runs two chunks (8 MMAs) x two stages
+  static constexpr bool W2 = BN == 128 && NBG == 4;
+  static constexpr int G = BN == 64 ? 4 : BN < 64 ? 2 : W2 ? 2 : 1;
   static constexpr int NACC = BN == 256 ? 1 : 2;
   static constexpr int NHB = BN == 256 ? 1 : 2;
-  static constexpr int NS = BN == 64 ? 2 : 4;
+  static constexpr int NS = BN == 64 || W2 ? 2 : 4;
   static constexpr int B_SUB = BN * 128;
   static constexpr int STAGE_B = G * B_SUB;
   static constexpr int ACOL = NACC * BN;  // TMEM: [accumulators | A slots]
@@ -310,10 +312,11 @@ struct ChunkWalk {
 
 template <int BN, bool PAIR, int NBG>
 __global__ void __launch_bounds__(Roles<NBG>::THREADS, 1) spconv_halo_kernel(const Params p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, NBG>;
   using R = Roles<NBG>;
   constexpr int W_LOAD = R::W_LOAD, W_B = R::W_B, W_MMA = R::W_MMA, W_EPI = R::W_EPI, THREADS = R::THREADS;
-  static_assert(C::G == 1 || C::G % NBG == 0, "a stage's chunk slots split evenly over the builder groups");
+  static_assert(C::G == 1 || C::G % NBG == 0 || NBG % C::G == 0,
+                "a stage's chunk slots split evenly over the builder groups (or groups over stages)");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
@@ -895,7 +898,7 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, 1) spconv_halo_kernel(con
 
 template <int BN, bool PAIR, int NBG>
 int launch(const Params& p, cudaStream_t s) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, NBG>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -911,9 +914,15 @@ int launch(const Params& p, cudaStream_t s) {
   return FPVS_OK;
 }
 
-// 4 builder groups at N = 64 (level 0: the A build paces the MMA issue; at
-// N >= 128 measured no faster, tools/halo_variant.py)
-inline bool default_nbg4(int bn) { return bn == 64; }
+// 4 builder groups at N = 64 (level 0: the A build paces the MMA issue) and
+// at N = 128 with two-chunk stages (levels 1 / 2: 8 MMAs per barrier round
+// instead of 4); measured in-frame with tools/halo_variant.py
+#ifndef FPVS_HALO_NBG4_MASK
+#define FPVS_HALO_NBG4_MASK 1  // bit 0: BN 64, bit 1: BN 128 (tools/build_variant.py A/B builds)
+#endif
+inline bool default_nbg4(int bn) {
+  return (bn == 64 && (FPVS_HALO_NBG4_MASK & 1)) || (bn == 128 && (FPVS_HALO_NBG4_MASK & 2));
+}
 
 inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
