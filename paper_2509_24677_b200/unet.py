@@ -173,15 +173,13 @@ class UNetPlan:
             cin, cout = layer.spec.in_channels, layer.spec.out_channels
             if not halo_ok(27, cin, cout):
                 continue
-            # measured on config 2 (tools/split_sweep.py): 128-wide tiles; a
-            # 2-way K split where the level has well under a wave of tiles, and
-            # split = -2 (only the last partial wave's tiles cut in two) where it
-            # has more tiles than SMs and a long K loop
+            # measured on config 2 in the whole flushed frame (tools/split_frame.py):
+            # 128-wide tiles; a 2-way K split only where the level has well under
+            # a wave of tiles (level 2); every other split, including the
+            # last-wave tail split (-2) of dec0a, costs 4-80 us per frame
             bn = 128 if cout % 128 == 0 else 64
             tiles = max(1, (r + 127) // 128) * (cout // bn)
-            # tail balancing pays where the K loop is long (Cin >= 128); at
-            # Cin = 64 the short tail units cost more than the imbalance
-            split = 2 if tiles * 2 <= 148 else -2 if (tiles > 148 and cin >= 128) else 1
+            split = 2 if tiles * 2 <= 148 else 1
             if cfg and name in cfg:
                 bn, split = cfg[name]
             self.halo_cfg[name] = (bn, split)
