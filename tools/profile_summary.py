@@ -32,20 +32,21 @@ def is_conv(name):
 
 
 def first_frame(ls):
-    """Kernels of the first full eager frame: from the first maps launch to the head (15th conv kernel)."""
+    """Kernels of the first full eager frame: from the first maps launch to the
+    grid writer of the fused head (rowbits_grid_kernel, after the 14th conv)."""
     out, started, nconv = [], False, 0
     for i, name, us in ls:
         if "l0_flags_kernel" in name:
             if started and nconv:
                 break
             started, out, nconv = True, [], 0
-        if not started or "pack_weights" in name:
-            continue
+        if not started or "pack_weights" in name or name.startswith("void at::") or name.startswith("at::"):
+            continue  # one-time weight packing (first eager frame only; never in the graph)
         out.append((i, name, us))
         if is_conv(name):
             nconv += 1
-            if nconv == 15:
-                break
+        if "rowbits_grid" in name or nconv == 15:
+            break
     return out
 
 
@@ -83,8 +84,8 @@ def main(tag, launch_csv, conv_rep, maps_rep=None):
     conv = sum(u for _, n, u in fr if is_conv(n))
     md += [f"Launch list: `{os.path.basename(launch_csv)}` (`ncu --metrics gpu__time_duration.sum "
            "--clock-control none`, cold-cache, serialised).", "",
-           f"First eager frame: {len(fr)} launches, {tot:.1f} us summed; sparse conv kernels (spconv_halo x10 + "
-           f"spconv_tc x4 + head) "
+           f"First eager frame: {len(fr)} launches, {tot:.1f} us summed; sparse conv kernels (spconv_halo x10, "
+           f"dec0b with the head fused, + spconv_tc x4: down01/12 gathers, up21/10 column blocks) "
            f"{conv:.1f} us = {100 * conv / tot:.1f}% of the frame.", "",
            "| # | kernel | us |", "|---|---|---|"]
     md += [f"| {i} | `{n[:70]}` | {u:.2f} |" for i, n, u in fr]
@@ -94,12 +95,12 @@ def main(tag, launch_csv, conv_rep, maps_rep=None):
             "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active"]
     rs = raw(conv_rep, mets)
-    md += ["", f"`--set full` capture `{os.path.basename(conv_rep)}` (first eager frame's 15 conv launches):", "",
+    md += ["", f"`--set full` capture `{os.path.basename(conv_rep)}` (first eager frame's 14 conv launches):", "",
            "| launch | kernel | us | DRAM read MB | DRAM write MB | grid | SM % | L2 % | tensor pipe % (of active SM cycles) |",
            "|---|---|---|---|---|---|---|---|---|"]
     dram = []
     names = ["enc0a", "enc0b", "down01", "enc1a", "enc1b", "down12", "enc2a", "enc2b", "up21", "dec1a", "dec1b",
-             "up10", "dec0a", "dec0b", "head"]
+             "up10", "dec0a", "dec0b+head"]
 
     def mb(v, unit_scale):
         try:
@@ -119,7 +120,8 @@ def main(tag, launch_csv, conv_rep, maps_rep=None):
                   f"{tensor_pct(r)} |")
     if maps_rep:
         mr = raw(maps_rep, mets)
-        md += ["", f"`--set full` capture `{os.path.basename(maps_rep)}` (map kernels: levels, up-sort, halo tables):", "",
+        md += ["", f"`--set full` capture `{os.path.basename(maps_rep)}` (map kernels K1-K3 incl. every level's halo "
+               "tables, and the fused head's grid writer):", "",
                "| kernel | us | DRAM read MB | grid |", "|---|---|---|---|"]
         for r in mr:
             md.append(f"| `{r['name'][:40]}` | {r.get('gpu__time_duration.sum')} | {r.get('dram__bytes_read.sum')} | "

@@ -14,7 +14,7 @@ timeout 600 python $BENCH > gpurun_out/${TAG}_bench_short.json 2> gpurun_out/${T
 timeout 300 python tools/prof_frame.py 1 > gpurun_out/prof_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"spconv_(tc|halo)_kernel" -c 15 \
       -o gpurun_out/conv_full_${TAG} python tools/prof_frame.py 1 > gpurun_out/ncu_conv.log 2>&1
-ncu --set full --clock-control none -k regex:"l0_flags|compact_levels|tables_kernel|count_kernel|place_kernel|halo_build" -c 6 \
+ncu --set full --clock-control none -k regex:"l0_flags|compact_levels|tables_kernel|rowbits_grid" -c 7 \
     -o gpurun_out/maps_full_${TAG} python tools/prof_frame.py 1 > gpurun_out/ncu_maps.log 2>&1
 timeout 300 python tools/interleave_prof.py > gpurun_out/il_plain.log 2>&1 && \
   ncu --set full --clock-control none -k regex:"il_|deil_" -c 8 -o gpurun_out/il_full_${TAG} \
