@@ -186,16 +186,22 @@ struct Unit {
   uint32_t mask;
 };
 
-template <int BN, int NBG = 2>
+template <int BN, int NBG = 2, int MINB = 1>
 struct Cfg {
   // chunks per stage: BN 64 runs 4 chunks (16 MMAs) per stage and commit, two
   // stages deep; BN >= 128: one chunk per stage, deeper weight prefetch; with
-  // four builder groups BN 128 runs two chunks (8 MMAs) x two stages
+  // four builder groups BN 128 runs two chunks (8 MMAs) x two stages.
+  // MINB = 2 (BN 64): two CTAs per SM, each with half the tensor memory, one
+  // halo buffer and two-chunk stages; one CTA's tile-boundary and halo-load
+  // gaps are filled by the other's MMAs.
+  static_assert(MINB == 1 || (MINB == 2 && BN == 64 && NBG == 2), "two CTAs per SM: BN 64, two builder groups");
   static constexpr bool W2 = BN == 128 && NBG == 4;
-  static constexpr int G = BN == 64 ? 4 : BN < 64 ? 2 : W2 ? 2 : 1;
+  static constexpr int G = BN == 64 ? (MINB == 2 ? 2 : 4) : BN < 64 ? 2 : W2 ? 2 : 1;
   static constexpr int NACC = BN == 256 ? 1 : 2;
-  static constexpr int NHB = BN == 256 ? 1 : 2;
+  static constexpr int NHB = BN == 256 || MINB == 2 ? 1 : 2;
   static constexpr int NS = BN == 64 || W2 ? 2 : 4;
+  static constexpr int TMEM_COLS = MINB == 2 ? 256 : 512;
+  static constexpr int BIAS_N = MINB == 2 ? 128 : 1024;  // floats (MINB 2: Cout <= 128, no head)
   static constexpr int B_SUB = BN * 128;
   static constexpr int STAGE_B = G * B_SUB;
   static constexpr int ACOL = NACC * BN;  // TMEM: [accumulators | A slots]
@@ -204,17 +210,17 @@ struct Cfg {
   static constexpr int NBARS = 2 * NS + 2 * NACC + 3 * NHB + 2;  // + fused head: weights landed, head MMA done
   static constexpr int CTRL_OFF = BAR_OFF + 8 * NBARS;
   static constexpr int BIAS_OFF = CTRL_OFF + 64;
-  static constexpr int UC_OFF = BIAS_OFF + 4 * 1024;  // unit cache: Unit [64] + halo sizes [64]
+  static constexpr int UC_OFF = BIAS_OFF + 4 * BIAS_N;  // unit cache: Unit [64] + halo sizes [64]
   static constexpr int UC_END = UC_OFF + kUnitCache * (int)sizeof(Unit) + kUnitCache * 4;
   // fused head (BN = 64 only): 8 KB of packed head weights, 1024-aligned
-  static constexpr bool HEAD = BN == 64;
+  static constexpr bool HEAD = BN == 64 && MINB == 1;
   static constexpr int HW_OFF = (UC_END + 1023) / 1024 * 1024;
   static constexpr int SMEM = 1024 + (HEAD ? HW_OFF + 64 * 128 : UC_END);
   static constexpr int HEAD_A = ACOL + NS * G * 32;  // TMEM: head A operand (32 cols), head accumulator (64 cols)
   static constexpr int HEAD_D = HEAD_A + 32;
-  static_assert(ACOL + NS * G * 32 <= 512, "TMEM columns");
-  static_assert(!HEAD || HEAD_D + 64 <= 512, "TMEM columns (fused head)");
-  static_assert(SMEM <= 232448, "shared memory budget");
+  static_assert(ACOL + NS * G * 32 <= TMEM_COLS, "TMEM columns");
+  static_assert(!HEAD || HEAD_D + 64 <= TMEM_COLS, "TMEM columns (fused head)");
+  static_assert(SMEM <= 232448 && MINB * (SMEM + 1024) <= 233472, "shared memory budget");
 };
 
 
@@ -310,9 +316,9 @@ struct ChunkWalk {
   }
 };
 
-template <int BN, bool PAIR, int NBG>
-__global__ void __launch_bounds__(Roles<NBG>::THREADS, 1) spconv_halo_kernel(const Params p) {
-  using C = Cfg<BN, NBG>;
+template <int BN, bool PAIR, int NBG, int MINB>
+__global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(const Params p) {
+  using C = Cfg<BN, NBG, MINB>;
   using R = Roles<NBG>;
   constexpr int W_LOAD = R::W_LOAD, W_B = R::W_B, W_MMA = R::W_MMA, W_EPI = R::W_EPI, THREADS = R::THREADS;
   static_assert(C::G == 1 || C::G % NBG == 0 || NBG % C::G == 0,
@@ -389,7 +395,8 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, 1) spconv_halo_kernel(con
     s_units[tid] = U;
   }
   if (warp == W_MMA) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                 "n"(C::TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -726,7 +733,7 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, 1) spconv_halo_kernel(con
     const int q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t tlane = (uint32_t)(q4 * 32) << 16;
     const bool fuse_head = C::HEAD && p.head;
-    constexpr int EC = NBG == 4 ? 16 : 32;
+    constexpr int EC = NBG == 4 || MINB == 2 ? 16 : 32;  // 16 where registers are short (768 threads, or 2 CTAs per SM)
     uint32_t head_phase = 0;
     if (fuse_head && warp == W_EPI && lane == 0) {
       // the packed head weights (one 64 x 64 bf16 SW128 chunk), once per CTA
@@ -892,23 +899,28 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, 1) spconv_halo_kernel(con
 #endif
   if (warp == W_MMA) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
+                 : "memory");
   }
 }
 
-template <int BN, bool PAIR, int NBG>
+template <int BN, bool PAIR, int NBG, int MINB = 1>
 int launch(const Params& p, cudaStream_t s) {
-  using C = Cfg<BN, NBG>;
+  using C = Cfg<BN, NBG, MINB>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(spconv_halo_kernel<BN, PAIR, NBG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(spconv_halo_kernel<BN, PAIR, NBG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM);
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     configured = true;
   }
   const long long units = (long long)((p.cap + BM - 1) / BM) * p.nblk * p.smax;
-  const int grid = (int)(units < kNumSMs ? (units < 1 ? 1 : units) : kNumSMs);
-  cudaError_t e = launch_kernel(spconv_halo_kernel<BN, PAIR, NBG>, dim3(grid), dim3(Roles<NBG>::THREADS), C::SMEM, s, p);
+  if (p.cout > C::BIAS_N) return set_error(FPVS_EINVAL, "spconv_halo: Cout %d > %d", p.cout, C::BIAS_N);
+  const long long slots = (long long)kNumSMs * MINB;
+  const int grid = (int)(units < slots ? (units < 1 ? 1 : units) : slots);
+  cudaError_t e = launch_kernel(spconv_halo_kernel<BN, PAIR, NBG, MINB>, dim3(grid), dim3(Roles<NBG>::THREADS), C::SMEM,
+                                s, p);
   if (e != cudaSuccess) return set_error(FPVS_ECUDA, "spconv_halo: %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("spconv_halo");
   return FPVS_OK;
@@ -917,6 +929,9 @@ int launch(const Params& p, cudaStream_t s) {
 // 4 builder groups at N = 64 (level 0: the A build paces the MMA issue) and
 // at N = 128 with two-chunk stages (levels 1 / 2: 8 MMAs per barrier round
 // instead of 4); measured in-frame with tools/halo_variant.py
+#ifndef FPVS_HALO_2CTA
+#define FPVS_HALO_2CTA 0
+#endif
 #ifndef FPVS_HALO_NBG4_MASK
 #define FPVS_HALO_NBG4_MASK 1  // bit 0: BN 64, bit 1: BN 128 (tools/build_variant.py A/B builds)
 #endif
@@ -1074,7 +1089,15 @@ static int halo_conv(const void* x, int ldx, int x_rows, const int32_t* nbr, con
   const int bnbit = bn == 64 ? 1 : bn == 128 ? 2 : 4;
   const bool nbg4 = nbg_knob >= 8 ? ((nbg_knob - 8) & bnbit) != 0 : nbg_knob ? nbg_knob == 4 : halo::default_nbg4(bn);
   if (bn == 32) return halo::launch<32, false, 2>(p, st);
-  if (bn == 64) return nbg4 ? halo::launch<64, false, 4>(p, st) : halo::launch<64, false, 2>(p, st);
+  if (bn == 64) {
+#if FPVS_HALO_2CTA
+    // two CTAs per SM (Cfg MINB = 2) for the plain 64-wide layers: measured
+    // (tools/build_variant.py) equal to one 4-group CTA per SM at Cin 64 and
+    // 4 us slower at Cin 128, so the product build leaves it out
+    if (!head && split == 1 && cout <= 128) return halo::launch<64, false, 2, 2>(p, st);
+#endif
+    return nbg4 ? halo::launch<64, false, 4>(p, st) : halo::launch<64, false, 2>(p, st);
+  }
   if (bn == 128) return nbg4 ? halo::launch<128, false, 4>(p, st) : halo::launch<128, false, 2>(p, st);
   return nbg4 ? halo::launch<256, false, 4>(p, st) : halo::launch<256, false, 2>(p, st);
 }
