@@ -459,10 +459,10 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
         if (lane == 0 && q4 == 0 && bg < 2) HTS(256 + 4 * gc + 2 * bg);
         const uint8_t* hbuf = smem + hb * HBUF;
         const int16_t* ln = reinterpret_cast<const int16_t*>(hbuf + HALO_BYTES) + r * KOFF;
-        int j = first_offset(U.mask, qs - c * U.npres);
-        for (int q = qs; q < qe; ++q, j = next_offset(U.mask, j)) {
+        // one chunk (q = unit chunk index, j = its offset); returns 1 when the
+        // group's partner chunk of the stage was built with it
+        auto chunk = [&](const int q, const int j) -> int {
           const int i = q - U.q0;
-          if (grp(i) != bg) continue;
           const uint32_t st = sc0 + i / C::G;
           const int stage = (int)(st % C::NS);
           uint32_t v[32];
@@ -542,11 +542,7 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
             __syncwarp();
             if (lane == 0) mbar_arrive_cnt(smem_u32(full + stage), two ? 2u : 1u);
             if (lane == 0 && q4 == 0 && bg < 2 && st < 1400) HTS(1024 + 2 * st + bg);
-            if (two) {
-              ++q;  // the partner chunk is done; the loop increment moves past it
-              j = j2;
-            }
-            continue;
+            return two ? 1 : 0;  // the partner chunk is done too
           }
           if (lane == 0 && q4 == 0 && bg < 2 && st < 400) HTS(2000 + 2 * st + bg);
           mbar_wait(smem_u32(empty + stage), ((st / C::NS) & 1) ^ 1);
@@ -560,6 +556,32 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(full + stage));
           if (lane == 0 && q4 == 0 && bg < 2 && st < 1400) HTS(1024 + 2 * st + bg);
+                  return 0;
+        };
+        constexpr bool kTwoG = C::G / NBG >= 2;
+        if constexpr (!kTwoG) {
+          // chunk i goes to group i % NBG: this group's chunks of channel
+          // chunk c are every NBG-th present offset, picked out of the tile
+          // mask once here (walking all chunks and skipping the other groups'
+          // was a dependent bit-scan chain per chunk on every builder warp)
+          const int r0 = (bg - (qs - U.q0)) & (NBG - 1);
+          uint32_t rem = U.mask, own = 0;
+          for (int k = qs - c * U.npres + r0; k > 0; --k) rem &= rem - 1u;  // ranks before this group's first
+          for (int q = qs + r0; q < qe && rem; q += NBG) {
+            own |= rem & (0u - rem);
+#pragma unroll
+            for (int k = 0; k < NBG; ++k) rem &= rem - 1u;
+          }
+          for (int q = qs + r0; own; q += NBG, own &= own - 1u) chunk(q, __ffs(own) - 1);
+        } else {
+          int j = first_offset(U.mask, qs - c * U.npres);
+          for (int q = qs; q < qe; ++q, j = next_offset(U.mask, j)) {
+            if (grp(q - U.q0) != bg) continue;
+            if (chunk(q, j)) {
+              ++q;  // the partner chunk is done; the loop increment moves past it
+              j = next_offset(U.mask, j);
+            }
+          }
         }
         if (lane == 0 && q4 == 0 && bg == 0) HTS(6002 + 4 * gc);
         __syncwarp();
