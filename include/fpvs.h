@@ -53,6 +53,12 @@ enum { FPVS_OK = 0, FPVS_EINVAL = 1, FPVS_ESHAPE = 2, FPVS_ECUDA = 3 };
 enum { FPVS_IN_PACKED = 0, FPVS_IN_U8 = 1, FPVS_IN_F32 = 2, FPVS_IN_F64 = 3 };
 enum { FPVS_F32 = 0, FPVS_BF16 = 1, FPVS_F64 = 2 };
 enum { FPVS_ACT_NONE = 0, FPVS_ACT_RELU = 1, FPVS_ACT_SIGMOID = 2, FPVS_ACT_MASK = 3 };
+/* OR into fpvs_spconv_halo's act when the neighbour / halo tables and tile
+ * masks were written two or more launches earlier on the stream: the conv then
+ * decodes its work units before its programmatic-launch wait (overlapping the
+ * previous kernel's tail).  Without it the decode waits (safe directly after a
+ * table build). */
+#define FPVS_TABLES_SETTLED 0x100
 
 const char* fpvs_last_error(void);
 int fpvs_abi_version(void);

@@ -19,6 +19,7 @@ F32, BF16, F64 = 0, 1, 2
 IN_PACKED, IN_U8, IN_F32, IN_F64 = 0, 1, 2, 3
 EXCHANGE_TAIL = 10  # FPVS_EXCHANGE_TAIL
 ACT = {"none": 0, "relu": 1, "sigmoid": 2}
+TABLES_SETTLED = 0x100  # FPVS_TABLES_SETTLED (fpvs_spconv_halo act flag)
 
 _i, _f, _d, _p, _z = C.c_int, C.c_float, C.c_double, C.c_void_p, C.c_size_t
 

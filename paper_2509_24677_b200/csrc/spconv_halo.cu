@@ -116,6 +116,7 @@ struct Params {
   int* counters;  // [tiles][nblk] arrival counters, zero between launches
   int dbg;        // profiling builds: FPVS_HALO_DEBUG (timestamps)
   int abl;        // profiling builds: FPVS_HALO_ABL (ablations)
+  int settled;    // tables / tile masks are two or more launches old: decode units before the PDL wait
   // fused 1x1x1 head (dec0b of the U-Net, BN = Cout = d^3 = 64, no split):
   // the tile's bf16 activations become the A operand of 4 TS MMAs against the
   // head weights, then the row's 64 [z >= logit(tau)] bits go to row_bits
@@ -386,9 +387,14 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
   if (C::HEAD && p.head)
     for (int c = tid; c < 64; c += THREADS) s_bias[512 + c] = p.head_bias ? p.head_bias[c] : 0.f;
   if (tid < kUnitCache) {
-    // this CTA's units decoded in parallel (the tile masks come from the map
-    // kernels, two or more launches back; the halo sizes may be the previous
-    // launch's output, so the loader warps read them after their PDL wait)
+    // this CTA's units decoded in parallel.  The tile masks are read before
+    // the programmatic-launch wait only when the caller says they are two or
+    // more launches old (FPVS_TABLES_SETTLED: every U-Net conv after the
+    // first); directly after the table build (the first conv of a frame) the
+    // decode waits, since only griddepcontrol.wait makes the immediately
+    // preceding kernel's writes visible.  The halo sizes are read by the
+    // loader warps after their wait.
+    if (!p.settled) pdl_wait();
     const int u = blockIdx.x + tid * gridDim.x;
     Unit U{};
     if (u < nunits) unit_of(p, u, cpo, mtiles, U);
@@ -1043,6 +1049,8 @@ static int halo_conv(const void* x, int ldx, int x_rows, const int32_t* nbr, con
                      void* y, int ldy, int col_off, void* ws, size_t ws_bytes, void* stream, const HeadArgs* head) {
   FPVS_CHECK_ARG(x && nbr && lnbr && halo_rows && halo_n && tile_masks && n_dev && w_packed && y,
                  "null pointer");
+  const int settled = (act & FPVS_TABLES_SETTLED) != 0;
+  act &= ~FPVS_TABLES_SETTLED;
   if (bn == 0) bn = cout % 256 == 0 ? 256 : cout % 128 == 0 ? 128 : cout % 64 == 0 ? 64 : 32;
   if (split == 0) split = 1;
   FPVS_CHECK_ARG(bn == 32 || bn == 64 || bn == 128 || bn == 256, "halo conv tile width must be 32, 64, 128 or 256");
@@ -1086,6 +1094,7 @@ static int halo_conv(const void* x, int ldx, int x_rows, const int32_t* nbr, con
   p.part = (float*)((uint8_t*)ws + halo::align256(items * 4));
   p.dbg = debug_knob("FPVS_HALO_DEBUG");
   p.abl = debug_knob("FPVS_HALO_ABL");
+  p.settled = settled;
   if (head) {
     FPVS_CHECK_ARG(bn == 64 && cout == 64 && split == 1 && cin % 64 == 0,
                    "fused head needs a Cout = 64 layer with 64-wide tiles, no K split and Cin %% 64 == 0");

@@ -480,7 +480,7 @@ def halo_ok(K: int, cin: int, cout: int, dtype=None) -> bool:
 
 def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int, col_off: int = 0,
              precision: str = "fp32", act: str | None = None, stream=None, bn: int = 0, masks=None,
-             halo=None, halo_tabs=None, out_rows=None):
+             halo=None, halo_tabs=None, out_rows=None, settled: bool = False):
     """One sparse conv launch: y[:, col_off:col_off+Cout] = act(gather-GEMM(x, table) + b).
 
     ``masks`` are the table's per-tile offset masks (sparse.tile_masks); the
@@ -488,7 +488,10 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
     (bn, split, workspace) with ``halo_tabs`` (sparse.build_halo) selects the
     halo-cached kernel for 27-tap layers with 64-multiple channels.
     ``out_rows`` (bf16 only) maps tile row i to output row out_rows[i]
-    (-1 = skip): the parity-sorted up conv (sparse.UpSorter).
+    (-1 = skip): the parity-sorted up conv (sparse.UpSorter).  ``settled``:
+    the tables and tile masks were written two or more launches earlier (the
+    halo conv may then decode its units before its programmatic-launch wait,
+    FPVS_TABLES_SETTLED).
     """
     torch = _torch()
     spec = layer.spec
@@ -505,7 +508,8 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
             _lib.call("fpvs_spconv_halo", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), _lib.ptr(halo_tabs["lnbr"]),
                       _lib.ptr(halo_tabs["rows"]), _lib.ptr(halo_tabs["n"]), _lib.ptr(masks), _lib.ptr(n), cap,
                       _lib.ptr(layer.packed(hbn, stream)), hbn, split, _lib.ptr(layer.b), spec.in_channels,
-                      spec.out_channels, a, _lib.ptr(y), ldy, col_off, _lib.ptr(ws), ws.numel(), s)
+                      spec.out_channels, a | (_lib.TABLES_SETTLED if settled else 0), _lib.ptr(y), ldy, col_off,
+                      _lib.ptr(ws), ws.numel(), s)
             return
         if out_rows is not None:
             _lib.call("fpvs_spconv_tc_scatter", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), K, _lib.ptr(masks),

@@ -155,6 +155,8 @@ class UNetPlan:
         self.overlap = True  # side-stream map tables (see build_maps); device_stage_times turns it off
         # the 1x1x1 head fused into dec0b (FPVS_FUSE_HEAD=0 keeps the stand-alone head launch)
         self.fuse_head = net.precision == "bf16" and os.environ.get("FPVS_FUSE_HEAD", "1") != "0"
+        # FPVS_TABLES_SETTLED for the convs after the first (FPVS_SETTLED=0: every conv waits to decode)
+        self.settled = os.environ.get("FPVS_SETTLED", "1") != "0"
         # the fused head's per-row 64-bit cell masks (fpvs_rowbits_to_grid writes the grid from them)
         self.row_bits = torch.empty(k0, dtype=torch.int64, device=device) if self.fuse_head else None
         self._side = None
@@ -310,8 +312,10 @@ class UNetPlan:
                     run_conv(L[name], x, ldx, us["table"], K, us["n"], us["cap"], y, ldy, off, P, act="relu",
                              bn=self.bn.get(name, 0), masks=us["masks"], out_rows=us["perm"])
                     return
+                # every conv but the first reads tables the map build wrote two or more launches back
                 run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu", bn=self.bn.get(name, 0),
-                         masks=masks, halo=halo, halo_tabs=lv.extra.get("halo") if hc else None)
+                         masks=masks, halo=halo, halo_tabs=lv.extra.get("halo") if hc else None,
+                         settled=name != "enc0a" and self.settled)
             out.append((name, launch))
 
         m0, m1, m2 = L0.nbr_masks, L1.nbr_masks, L2.nbr_masks
