@@ -36,6 +36,7 @@ subset of the occupancy, row LBL).
 
 from __future__ import annotations
 
+import os
 from pathlib import Path
 
 import numpy as np
@@ -44,7 +45,7 @@ from . import _lib
 from . import sparse as sp
 from .froxel import FroxelGrid
 from .neural import (ModelConfig, PvsNet, TrainConfig, TrainingDiverged, build_layer_tables, layer_table,
-                     packed_dgrad_cache, run_conv, run_head)
+                     packed_dgrad_cache, run_conv, run_head, halo_ok)
 
 
 def _torch():
@@ -98,9 +99,17 @@ class TrainStep:
             raise ValueError(f"grid dims {self.grid_dims} not divisible by interleave factor {d} (N_x by 8)")
         self.grid_bytes = nx * ny * nz // 8
         self.lv = sp.new_level(B, (nx // d, ny // d, nz // d), device=device)
-        self.maps = sp.LevelMaps([self.lv], [], [], self.grid_dims, d)
-        cap = self.lv.cap
         bf16 = net.precision == "bf16"
+        tc_bw = bf16 and self._tc_backward_ok()
+        # 27-tap layers with Cin = 32 take the halo-cached wgrad (wgrad_halo.cu)
+        # and, where the shapes allow, the halo-cached forward: the level's halo
+        # tables come out of the map build itself (K3), every step
+        self.halo_wgrad = tc_bw and use_halo_wgrad() and any(self._halo_wgrad_ok(L) for L in net.layers)
+        self.halo_fwd = bf16 and os.environ.get("FPVS_TRAIN_HALO_FWD", "1") != "0"
+        want_halo = self.halo_wgrad or (self.halo_fwd and any(
+            L.spec.kernel == 3 and halo_ok(27, L.spec.in_channels, L.spec.out_channels) for L in net.layers[:-1]))
+        self.maps = sp.LevelMaps([self.lv], [], [], self.grid_dims, d, halo_levels=(0,) if want_halo else ())
+        cap = self.lv.cap
         self.adt = torch.bfloat16 if bf16 else torch.float32
         self.x0 = torch.empty((cap, d ** 3), dtype=self.adt, device=device)
         self.acts = [torch.empty((cap, L.spec.out_channels), dtype=self.adt, device=device) for L in net.layers[:-1]]
@@ -110,20 +119,24 @@ class TrainStep:
         widest = max(L.spec.in_channels for L in net.layers)
         self.dx = [torch.empty((cap, widest), dtype=torch.float32, device=device) for _ in range(2)]
         # bf16: the backward runs on tensor cores (tcgen05 dgrad / wgrad) with bf16 gradients
-        self.tc_backward = bf16 and self._tc_backward_ok()
+        self.tc_backward = tc_bw
         if self.tc_backward:
             self.dlog16 = torch.empty((cap, d3), dtype=torch.bfloat16, device=device)
             self.dz16 = [torch.empty((cap, widest), dtype=torch.bfloat16, device=device) for _ in range(2)]
             tws = max(_lib.size("fpvs_wgrad_tc_workspace_size", L.taps, L.spec.in_channels, L.spec.out_channels, cap)
                       for L in net.layers)
             self.wg_tc_ws = torch.empty(tws, dtype=torch.uint8, device=device)
-            # 27-tap layers with Cin = 32 take the halo-cached wgrad (wgrad_halo.cu):
-            # the level's halo tables are rebuilt with the maps every step
-            self.halo_wgrad = use_halo_wgrad() and any(self._halo_wgrad_ok(L) for L in net.layers)
             if self.halo_wgrad:
-                self.halo_builder = sp.HaloBuilder([self.lv])
                 self.wg_halo_ws = torch.empty(_lib.size("fpvs_wgrad_halo_workspace_size", cap), dtype=torch.uint8,
                                               device=device)
+        self.halo_conv_ws = None
+        if want_halo:
+            def auto_bn(c):  # fpvs_spconv_halo's bn = 0 choice
+                return 256 if c % 256 == 0 else 128 if c % 128 == 0 else 64 if c % 64 == 0 else 32
+            need = max([_lib.size("fpvs_spconv_halo_workspace_size", cap, L.spec.out_channels,
+                                  auto_bn(L.spec.out_channels), 1)
+                        for L in net.layers[:-1] if L.spec.out_channels % 32 == 0] + [256])
+            self.halo_conv_ws = torch.zeros(need, dtype=torch.uint8, device=device)
         self.pred_bits = torch.zeros(B * self.grid_bytes, dtype=torch.uint8, device=device)
         # flat master parameters and gradient
         sizes = [(L.w.numel(), L.b.numel()) for L in net.layers]
@@ -165,10 +178,15 @@ class TrainStep:
         self.maps.run(bits, feat=self.x0, clear=self.pred_bits, stream=stream)
         build_layer_tables(lv, net.kernels(), stream)
         x = self.x0
-        for layer, y in zip(net.layers[:-1], self.acts):
+        for li, (layer, y) in enumerate(zip(net.layers[:-1], self.acts)):
             table, K, masks = layer_table(lv, layer.spec.kernel)
+            sp_ = layer.spec
+            halo = None
+            if self.halo_fwd and self.halo_conv_ws is not None and K == 27 and halo_ok(27, sp_.in_channels,
+                                                                                        sp_.out_channels):
+                halo = (0, 1, self.halo_conv_ws)
             run_conv(layer, x, x.shape[1], table, K, lv.n, lv.cap, y, y.shape[1], 0, net.precision, stream=stream,
-                     masks=masks)
+                     masks=masks, halo=halo, halo_tabs=lv.extra.get("halo") if halo else None, settled=li > 0)
             x = y
         run_head(net.layers[-1], x, x.shape[1], lv, d, self.grid_dims, tc.tau, self.pred_bits, self.probs, None,
                  net.precision, stream)
@@ -231,8 +249,7 @@ class TrainStep:
         cap = lv.cap
         halo = None
         if self.halo_wgrad:
-            self.halo_builder.run(stream)
-            halo = sp._halo_tables(lv)
+            halo = sp._halo_tables(lv)  # built by the map build (K3) of this step
         _lib.call("fpvs_cast_bf16_rows", _lib.ptr(self.dlogits), self.dlogits.shape[1], _lib.ptr(lv.n), cap,
                   _lib.ptr(self.dlog16), s)
         dz, lddz = self.dlog16, self.dlog16.shape[1]
