@@ -403,6 +403,17 @@ int fpvs_spconv_wgrad_simt(const void* x, int ldx, int x_dtype, const float* dz,
  * db = sum_i dz[i] on tcgen05 with both operands MN-major (gathered x, dz),
  * fixed-order reduction of per-CTA partials (deterministic). */
 int fpvs_pack_weights_tc_dgrad(const float* w, int K, int cin, int cout, int bn, void* packed, void* stream);
+
+/* Several weight images in ONE launch (the training step re-packs every
+ * layer's forward and dgrad image after each optimizer update): job i is
+ * fpvs_pack_weights_tc (dgrad = 0) or fpvs_pack_weights_tc_dgrad (dgrad = 1)
+ * of (w, K, cin, cout, bn) into packed, byte-identical to the single calls. */
+typedef struct fpvs_pack_job {
+  const float* w;
+  int K, cin, cout, bn, dgrad;
+  void* packed;
+} fpvs_pack_job;
+int fpvs_pack_weights_tc_multi(const fpvs_pack_job* jobs, int njobs, void* stream);
 int fpvs_spconv_tc_dgrad(const void* dz, int lddz, int dz_rows, const int32_t* nbr, int K,
                          const uint32_t* tile_masks, const int32_t* n_dev, int cap,
                          const void* w_packed_dgrad, int bn, int cin, int cout, const void* mask, int ldm,

@@ -56,6 +56,7 @@ SIGNATURES = {
     "fpvs_spconv_halo_head": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _p, _z, _p, _p, _f, _p, _p]),
     "fpvs_rowbits_to_grid": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_pack_weights_tc_dgrad": (_i, [_p, _i, _i, _i, _i, _p, _p]),
+    "fpvs_pack_weights_tc_multi": (_i, [_p, _i, _p]),
     "fpvs_spconv_tc_dgrad": (_i, [_p, _i, _i, _p, _i, _p, _p, _i, _p, _i, _i, _i, _p, _i, _p, _i, _p]),
     "fpvs_wgrad_tc_workspace_size": (_z, [_i, _i, _i, _i]),
     "fpvs_spconv_wgrad_tc": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _p, _p, _p, _z, _p]),
@@ -112,6 +113,11 @@ class Level(C.Structure):
     _fields_ = [("coords", _p), ("index_vol", _p), ("n", _p), ("cap", _i), ("nbr", _p), ("nbr_masks", _p),
                 ("down", _p), ("down_masks", _p), ("up", _p), ("up_masks", _p), ("halo_rows", _p), ("halo_n", _p),
                 ("halo_lnbr", _p)]
+
+
+class PackJob(C.Structure):
+    """struct fpvs_pack_job (include/fpvs.h)."""
+    _fields_ = [("w", _p), ("K", _i), ("cin", _i), ("cout", _i), ("bn", _i), ("dgrad", _i), ("packed", _p)]
 
 
 class Frustum(C.Structure):

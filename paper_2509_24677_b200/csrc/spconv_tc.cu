@@ -591,30 +591,59 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
 // n*128 + ((kk/8) ^ (n%8))*16 + (kk%8)*2 (Swizzle<3,4,3>), value W[c*64+kk][nb*BN + n]
 // dgrad (taps > 0): the packed matrix is W'[(j*cout_src + co)][ci] = W[((taps-1-j)*cin_src + ci)][co]
 // (mirrored offsets, transposed per offset), the forward weight of dx = conv(dz).
+__device__ __forceinline__ void pack_weight_elem(long long t, const float* __restrict__ w, int Ktot, int cout, int BN,
+                                                 int nchunks, __nv_bfloat16* __restrict__ out, int taps, int cin_src,
+                                                 int cout_src) {
+  int kk = t % BK;
+  long long r = t / BK;
+  int nn = r % BN;
+  r /= BN;
+  int c = r % nchunks;
+  int nb = (int)(r / nchunks);
+  int k = c * BK + kk, col = nb * BN + nn;
+  float v = 0.f;
+  if (k < Ktot && col < cout) {
+    if (taps) {
+      const int j = k / cout_src, co = k - j * cout_src;
+      v = w[((long long)(taps - 1 - j) * cin_src + col) * cout_src + co];
+    } else {
+      v = w[(long long)k * cout + col];
+    }
+  }
+  long long byte = (((long long)nb * nchunks + c) * BN + nn) * 128 + (((kk >> 3) ^ (nn & 7)) << 4) + (kk & 7) * 2;
+  out[byte / 2] = __float2bfloat16_rn(v);
+}
+
 __global__ void pack_weights_kernel(const float* __restrict__ w, int Ktot, int cout, int BN, int nchunks, int nblk,
                                     __nv_bfloat16* __restrict__ out, int taps = 0, int cin_src = 0,
                                     int cout_src = 0) {
   const long long total = (long long)nblk * nchunks * BN * BK;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x)
+    pack_weight_elem(t, w, Ktot, cout, BN, nchunks, out, taps, cin_src, cout_src);
+}
+
+// every layer's images in one launch (after an optimizer step)
+constexpr int kMaxPackJobs = 32;
+struct PackJob {
+  const float* w;
+  __nv_bfloat16* out;
+  int Ktot, cout, BN, nchunks, taps, cin_src, cout_src;
+  long long base;  // first element of this job in the concatenated space
+};
+struct PackJobs {
+  PackJob j[kMaxPackJobs];
+  int count;
+  long long total;
+};
+
+__global__ void pack_weights_multi_kernel(const PackJobs J) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < J.total;
        t += (long long)gridDim.x * blockDim.x) {
-    int kk = t % BK;
-    long long r = t / BK;
-    int nn = r % BN;
-    r /= BN;
-    int c = r % nchunks;
-    int nb = (int)(r / nchunks);
-    int k = c * BK + kk, col = nb * BN + nn;
-    float v = 0.f;
-    if (k < Ktot && col < cout) {
-      if (taps) {
-        const int j = k / cout_src, co = k - j * cout_src;
-        v = w[((long long)(taps - 1 - j) * cin_src + col) * cout_src + co];
-      } else {
-        v = w[(long long)k * cout + col];
-      }
-    }
-    long long byte = (((long long)nb * nchunks + c) * BN + nn) * 128 + (((kk >> 3) ^ (nn & 7)) << 4) + (kk & 7) * 2;
-    out[byte / 2] = __float2bfloat16_rn(v);
+    int q = 0;
+    while (q + 1 < J.count && t >= J.j[q + 1].base) ++q;
+    const PackJob& b = J.j[q];
+    pack_weight_elem(t - b.base, b.w, b.Ktot, b.cout, b.BN, b.nchunks, b.out, b.taps, b.cin_src, b.cout_src);
   }
 }
 
@@ -816,6 +845,30 @@ extern "C" int fpvs_pack_weights_tc_dgrad(const float* w, int K, int cin, int co
   tc::pack_weights_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
       w, K * cout, cin, bn, nchunks, nblk, (__nv_bfloat16*)packed, K, cin, cout);
   FPVS_CHECK_LAUNCH("fpvs_pack_weights_tc_dgrad");
+  return FPVS_OK;
+}
+
+extern "C" int fpvs_pack_weights_tc_multi(const fpvs_pack_job* jobs, int njobs, void* stream) {
+  FPVS_CHECK_ARG(jobs && njobs >= 1 && njobs <= tc::kMaxPackJobs, "1..%d pack jobs", tc::kMaxPackJobs);
+  tc::PackJobs J{};
+  J.count = njobs;
+  long long tot = 0;
+  for (int i = 0; i < njobs; ++i) {
+    const fpvs_pack_job& q = jobs[i];
+    FPVS_CHECK_ARG(q.w && q.packed && q.K >= 1 && q.cin >= 1 && q.cout >= 1, "bad pack job %d", i);
+    // a dgrad image is the forward image of the Cout -> Cin conv with mirrored offsets
+    const int kin = q.dgrad ? q.cout : q.cin, kout = q.dgrad ? q.cin : q.cout;
+    const int bn = resolve_bn(q.bn, kout);
+    FPVS_CHECK_ARG(bn > 0, "pack job %d: tile width must be 0 (auto), 32, 64, 128 or 256", i);
+    FPVS_CHECK_ARG(kin % 8 == 0, "pack job %d: tcgen05 path needs the K-side channels %% 8 == 0", i);
+    const int nchunks = (q.K * kin + tc::BK - 1) / tc::BK, nblk = (kout + bn - 1) / bn;
+    J.j[i] = tc::PackJob{q.w, (__nv_bfloat16*)q.packed, q.K * kin, kout, bn, nchunks, q.dgrad ? q.K : 0,
+                         q.dgrad ? q.cin : 0, q.dgrad ? q.cout : 0, tot};
+    tot += (long long)nblk * nchunks * bn * tc::BK;
+  }
+  J.total = tot;
+  tc::pack_weights_multi_kernel<<<grid_for(tot, 256), 256, 0, as_stream(stream)>>>(J);
+  FPVS_CHECK_LAUNCH("fpvs_pack_weights_tc_multi");
   return FPVS_OK;
 }
 

@@ -380,6 +380,33 @@ def packed_cache(layer, bn: int = 0, stream=None):
     return layer._packed[bn]
 
 
+def repack_all(layers, stream=None):
+    """Refresh every cached bf16 weight image of ``layers`` from their (updated)
+    fp32 weights in ONE launch (fpvs_pack_weights_tc_multi) — the training
+    step's re-pack after each optimizer update; images of other kinds are
+    dropped and rebuilt lazily."""
+    import ctypes as C
+    jobs = []
+    for L in layers:
+        cache = getattr(L, "_packed", None)
+        if not cache:
+            continue
+        for key in list(cache):
+            cin, cout = L.spec.in_channels, L.spec.out_channels
+            if isinstance(key, int):
+                jobs.append((L.w, L.taps, cin, cout, key, 0, cache[key]))
+            elif isinstance(key, tuple) and key[0] == "dgrad":
+                jobs.append((L.w, L.taps, cin, cout, key[1], 1, cache[key]))
+            else:
+                del cache[key]
+    for i in range(0, len(jobs), 32):
+        part = jobs[i:i + 32]
+        arr = (_lib.PackJob * len(part))()
+        for e, (w, taps, cin, cout, bn, dg, out) in zip(arr, part):
+            e.w, e.K, e.cin, e.cout, e.bn, e.dgrad, e.packed = _lib.ptr(w), taps, cin, cout, bn, dg, _lib.ptr(out)
+        _lib.call("fpvs_pack_weights_tc_multi", C.addressof(arr), len(part), _lib.stream_ptr(stream))
+
+
 def packed_upblocks_cache(layer, bn: int = 0, stream=None):
     """The k2s2 up layer's weights as one Cin x 8 Cout matrix (column block j =
     parity class j's slice, fpvs_spconv_tc_upblocks) and its bias tiled 8

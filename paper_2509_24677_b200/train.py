@@ -45,7 +45,7 @@ from . import _lib
 from . import sparse as sp
 from .froxel import FroxelGrid
 from .neural import (ModelConfig, PvsNet, TrainConfig, TrainingDiverged, build_layer_tables, layer_table,
-                     packed_dgrad_cache, run_conv, run_head, halo_ok)
+                     packed_dgrad_cache, run_conv, run_head, halo_ok, repack_all)
 
 
 def _torch():
@@ -311,7 +311,8 @@ class TrainStep:
                       _lib.ptr(self.v), n, float(lr), 0.9, 0.999, 1e-8, float(tc.weight_decay), int(step), s)
         else:
             _lib.call("fpvs_sgd_step", _lib.ptr(self.params), _lib.ptr(self.grads), n, float(lr), s)
-        self.net.invalidate()  # the bf16 weight images are re-packed from the new master weights
+        # every cached bf16 weight image re-packed from the new master weights, one launch
+        repack_all(self.net.layers, stream)
 
     def adopt(self, other: "TrainStep"):
         """Share another plan's flat parameters / optimizer state (a different batch size)."""

@@ -260,3 +260,32 @@ def test_dropin_losses_match_reference_golden(golden):
             assert isinstance(gt_, torch.Tensor) and float((gt_.cpu() - torch.as_tensor(g[f"l{i}_{key}_g"])).abs().max()) <= 1e-12
     with pytest.raises(ValueError):
         dice_loss(np.zeros(3), np.zeros(4), 0.1)
+
+
+def test_pack_weights_multi_equals_single_packs():
+    """fpvs_pack_weights_tc_multi (the training step's one-launch re-pack) writes
+    exactly the bytes of the single fpvs_pack_weights_tc / _dgrad calls."""
+    import ctypes as C
+    import torch
+    from paper_2509_24677_b200 import _lib
+    rng = np.random.default_rng(7)
+    specs = [(27, 8, 32, 0, 0), (27, 32, 32, 0, 1), (27, 32, 32, 32, 0), (1, 32, 8, 0, 0), (8, 64, 128, 0, 1),
+             (27, 64, 64, 64, 1)]
+    jobs, refs = [], []
+    for K, cin, cout, bn, dg in specs:
+        w = torch.from_numpy(rng.standard_normal((K * cin, cout)).astype(np.float32)).cuda()
+        fn = "fpvs_pack_weights_tc_dgrad" if dg else "fpvs_pack_weights_tc"
+        n = _lib.size("fpvs_pack_weights_tc_size", K, cout, cin, bn) if dg else \
+            _lib.size("fpvs_pack_weights_tc_size", K, cin, cout, bn)
+        ref = torch.zeros(n, dtype=torch.uint8, device="cuda")
+        _lib.call(fn, _lib.ptr(w), K, cin, cout, bn, _lib.ptr(ref), _lib.stream_ptr())
+        out = torch.full((n,), 0x7F, dtype=torch.uint8, device="cuda")
+        jobs.append((w, K, cin, cout, bn, dg, out))
+        refs.append(ref)
+    arr = (_lib.PackJob * len(jobs))()
+    for e, (w, K, cin, cout, bn, dg, out) in zip(arr, jobs):
+        e.w, e.K, e.cin, e.cout, e.bn, e.dgrad, e.packed = _lib.ptr(w), K, cin, cout, bn, dg, _lib.ptr(out)
+    _lib.call("fpvs_pack_weights_tc_multi", C.addressof(arr), len(jobs), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    for (w, K, cin, cout, bn, dg, out), ref in zip(jobs, refs):
+        assert torch.equal(out, ref), (K, cin, cout, bn, dg)
