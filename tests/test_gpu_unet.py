@@ -212,3 +212,30 @@ def test_up_blocks_equal_sorted_up_conv():
     (b1, b0), bb = res[1]
     assert torch.equal(a1, b1) and torch.equal(a0, b0)
     assert torch.equal(ab, bb)
+
+
+def test_unet_batch_of_two_equals_two_single_frames():
+    """A B = 2 U-Net plan (fused maps over both grids, batch-coordinate rows,
+    column-block up convs, fused head + grid writer per batch plane) gives each
+    grid exactly the bits of its own B = 1 frame."""
+    import torch
+    from paper_2509_24677_b200.unet import PvsUNet
+    dims = (128, 128, 128)
+    occs = [synth.box_grid(dims, 600, 1, 12, s) for s in (11, 12)]
+    net = PvsUNet(seed=1, precision="bf16")
+    singles = []
+    for occ in occs:
+        plan = net.plan(1, dims)
+        bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+        out = torch.full((occ.size // 8,), 0xA5, dtype=torch.uint8, device="cuda")
+        plan.run(bits, out, 0.5)
+        torch.cuda.synchronize()
+        singles.append(out.cpu().numpy())
+    plan2 = net.plan(2, dims)
+    bits2 = torch.from_numpy(np.concatenate([FroxelGrid.from_dense(o).bits for o in occs])).cuda()
+    out2 = torch.full((2 * occs[0].size // 8,), 0x5A, dtype=torch.uint8, device="cuda")
+    plan2.run(bits2, out2, 0.5)
+    torch.cuda.synchronize()
+    got = out2.cpu().numpy().reshape(2, -1)
+    assert np.array_equal(got[0], singles[0]) and np.array_equal(got[1], singles[1])
+    assert int(np.unpackbits(got).sum()) > 0
