@@ -615,8 +615,15 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
     }
   } else if (warp < W_B) {
     // ===================== halo loaders =====================
-    pdl_wait();  // halo rows, sizes and local tables may be the previous launch's output
-    if (tid == W_LOAD * 32) pdl_trigger();
+    // halo sizes, local tables and row lists come from the table build: with
+    // settled tables (two or more launches old) they are read, and the first
+    // halo's table + row list copied, before the wait; the halo ROWS are the
+    // previous launch's output and always wait
+    const bool early = p.settled != 0;
+    if (!early) {
+      pdl_wait();
+      if (tid == W_LOAD * 32) pdl_trigger();
+    }
     const int tl = tid - W_LOAD * 32;
     // the unit cache's halo sizes; the builders read them only after the first
     // hmeta barrier, which loader thread 0 arrives on after this named barrier
@@ -627,6 +634,28 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
     named_bar(2, LOADERS);
     const int pc = tl & 7;
     const uint32_t ldx2 = (uint32_t)p.ldx * 2u;
+    // the tile's local table and its halo row list, one bulk copy each
+    auto issue_meta = [&](const Unit& U, int hb, int H) {
+      const uint32_t rb = (uint32_t)((H * 4 + 15) & ~15);
+      const uint32_t mb = smem_u32(hmeta + hb);
+      uint8_t* hbuf = smem + hb * HBUF;
+      mbar_arrive_expect_tx(mb, LNBR_BYTES + rb);
+      bulk_g2s(smem_u32(hbuf + HALO_BYTES), p.lnbr + (long long)U.mt * BM * KOFF, LNBR_BYTES, mb);
+      if (rb) bulk_g2s(smem_u32(hbuf + ROWS_OFF), p.halo_rows + (long long)U.mt * HMAX, rb, mb);
+    };
+    bool pre = false;  // the first halo's meta copy is already in flight
+    if (early) {
+      if ((int)blockIdx.x < nunits) {
+        Unit U;
+        get_unit(p, blockIdx.x, cpo, mtiles, U, s_units);
+        if (U.q1 > U.q0) {
+          pre = true;
+          if (tl == 0) issue_meta(U, 0, s_uhn[0]);  // buffer 0 is free: nothing has used it yet
+        }
+      }
+      pdl_wait();
+      if (tid == W_LOAD * 32) pdl_trigger();
+    }
     uint32_t gc = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
@@ -639,13 +668,10 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
         uint8_t* hbuf = smem + hb * HBUF;
         const int ku = (u - (int)blockIdx.x) / (int)gridDim.x;
         const int H = ku < kUnitCache ? s_uhn[ku] : __ldg(p.halo_n + U.mt);
-        if (tl == 0) {
-          // the tile's local table and its halo row list, one bulk copy each
-          const uint32_t rb = (uint32_t)((H * 4 + 15) & ~15);
-          const uint32_t mb = smem_u32(hmeta + hb);
-          mbar_arrive_expect_tx(mb, LNBR_BYTES + rb);
-          bulk_g2s(smem_u32(hbuf + HALO_BYTES), p.lnbr + (long long)U.mt * BM * KOFF, LNBR_BYTES, mb);
-          if (rb) bulk_g2s(smem_u32(hbuf + ROWS_OFF), p.halo_rows + (long long)U.mt * HMAX, rb, mb);
+        if (pre) {
+          pre = false;  // gc == 0: issued before the wait
+        } else if (tl == 0) {
+          issue_meta(U, hb, H);
         }
         mbar_wait(smem_u32(hmeta + hb), hph);
         if (tl == 0) HTS(17 + 3 * gc);
