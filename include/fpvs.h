@@ -320,7 +320,8 @@ int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_t* nbr, con
  * operand of the head's tcgen05 MMAs in tensor memory, and active row r's
  * 64 thresholded outputs [sigmoid(z) >= tau] go to row_bits[r] (bit k =
  * channel k = lx + 4 ly + 16 lz); the conv's own output never goes to HBM.
- * Same conv arguments as fpvs_spconv_halo with bn = 64, split = 1;
+ * Same conv arguments as fpvs_spconv_halo with bn = 64, split = 1 (flags:
+ * FPVS_TABLES_SETTLED or 0, as fpvs_spconv_halo's act flag);
  * head_w_packed: the head's fpvs_pack_weights_tc image (K = 1, bn = 64).
  * With fpvs_rowbits_to_grid this replaces the final Conv3d + sigmoid +
  * deinterleave(tau) of the reference (neural.py:513-526, interleave.py:68-80). */
@@ -328,7 +329,7 @@ int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const int32_t* nbr
                           const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
                           const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin,
                           void* ws, size_t ws_bytes, const void* head_w_packed, const float* head_bias,
-                          float tau, uint64_t* row_bits, void* stream);
+                          float tau, uint64_t* row_bits, int flags, void* stream);
 
 /* Per-row 64-bit cell masks (fpvs_spconv_halo_head) -> the packed froxel grid
  * B x Nx x Ny x Nz (FPVS bit order, d = 4, N_x % 32 == 0): every 32-bit word

@@ -1172,11 +1172,11 @@ extern "C" int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const i
                                      const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
                                      const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin,
                                      void* ws, size_t ws_bytes, const void* head_w_packed, const float* head_bias,
-                                     float tau, uint64_t* row_bits, void* stream) {
+                                     float tau, uint64_t* row_bits, int flags, void* stream) {
   const HeadArgs h{head_w_packed, head_bias, tau, reinterpret_cast<unsigned long long*>(row_bits)};
   // the conv's own output is consumed in the epilogue: y is never written
   return halo_conv(x, ldx, x_rows, nbr, lnbr, halo_rows, halo_n, tile_masks, n_dev, cap, w_packed, 64, 1, bias, cin, 64,
-                   FPVS_ACT_RELU, row_bits, 64, 0, ws, ws_bytes, stream, &h);
+                   FPVS_ACT_RELU | (flags & FPVS_TABLES_SETTLED), row_bits, 64, 0, ws, ws_bytes, stream, &h);
 }
 
 namespace fpvs {

@@ -343,7 +343,7 @@ class UNetPlan:
                           _lib.ptr(ht["lnbr"]), _lib.ptr(ht["rows"]), _lib.ptr(ht["n"]), _lib.ptr(m0), _lib.ptr(L0.n),
                           L0.cap, _lib.ptr(L["dec0b"].packed(64)), _lib.ptr(L["dec0b"].b), c0, _lib.ptr(ws), ws.numel(),
                           _lib.ptr(hl.packed(64)), _lib.ptr(hl.b), float(tau), _lib.ptr(self.row_bits),
-                          _lib.stream_ptr())
+                          _lib.TABLES_SETTLED if self.settled else 0, _lib.stream_ptr())
                 _lib.call("fpvs_rowbits_to_grid", _lib.ptr(self.row_bits), _lib.ptr(L0.index_vol), self.B, nx, ny, nz,
                           net.d, _lib.ptr(out_bits), _lib.stream_ptr())
             out.append(("dec0b", dec0b_head))
