@@ -315,13 +315,33 @@ int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_t* nbr, con
                      const float* bias, int cin, int cout, int act, void* y, int ldy, int col_off,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* fpvs_spconv_halo with tile-level dataflow between two convs of ONE level
+ * (same tables; the consumer reads the producer's output):
+ * tile_done_out (int32 [tiles], nullable): the producer's per-tile flags — the
+ * CTA owning tile t zeroes it at its start and sets it to 1 once the tile's
+ * output rows are stored (split must be 1, bn = Cout).  tile_done_in
+ * (nullable): the producer's flags; the consumer, launched right after it
+ * with programmatic dependent launch, then skips the grid-wide wait and each
+ * CTA waits only for the producer tiles holding its tile's halo rows (all of
+ * them when the halo was capped), so its first tiles start on the SMs the
+ * producer's last wave leaves idle.  Requires FPVS_TABLES_SETTLED in act, a
+ * weight image packed before the producer launched, and a y the producer
+ * does not read or write.  With both NULL this is fpvs_spconv_halo. */
+int fpvs_spconv_halo_flow(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
+                          const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
+                          const int32_t* n_dev, int cap, const void* w_packed, int bn, int split,
+                          const float* bias, int cin, int cout, int act, void* y, int ldy, int col_off,
+                          void* ws, size_t ws_bytes, int32_t* tile_done_out, const int32_t* tile_done_in,
+                          void* stream);
+
 /* The U-Net's last level-0 conv (Cout = 64, relu) with the 1x1x1 head fused
  * into its epilogue (d = 4): each tile's bf16 activations become the A
  * operand of the head's tcgen05 MMAs in tensor memory, and active row r's
  * 64 thresholded outputs [sigmoid(z) >= tau] go to row_bits[r] (bit k =
  * channel k = lx + 4 ly + 16 lz); the conv's own output never goes to HBM.
  * Same conv arguments as fpvs_spconv_halo with bn = 64, split = 1 (flags:
- * FPVS_TABLES_SETTLED or 0, as fpvs_spconv_halo's act flag);
+ * FPVS_TABLES_SETTLED or 0, as fpvs_spconv_halo's act flag; tile_done_in:
+ * as fpvs_spconv_halo_flow's consumer side, nullable);
  * head_w_packed: the head's fpvs_pack_weights_tc image (K = 1, bn = 64).
  * With fpvs_rowbits_to_grid this replaces the final Conv3d + sigmoid +
  * deinterleave(tau) of the reference (neural.py:513-526, interleave.py:68-80). */
@@ -329,7 +349,8 @@ int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const int32_t* nbr
                           const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
                           const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin,
                           void* ws, size_t ws_bytes, const void* head_w_packed, const float* head_bias,
-                          float tau, uint64_t* row_bits, int flags, void* stream);
+                          float tau, uint64_t* row_bits, int flags, const int32_t* tile_done_in,
+                          void* stream);
 
 /* Per-row 64-bit cell masks (fpvs_spconv_halo_head) -> the packed froxel grid
  * B x Nx x Ny x Nz (FPVS bit order, d = 4, N_x % 32 == 0): every 32-bit word

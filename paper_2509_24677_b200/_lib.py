@@ -53,7 +53,10 @@ SIGNATURES = {
     "fpvs_spconv_halo_workspace_size": (_z, [_i, _i, _i, _i]),
     "fpvs_spconv_halo": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _i, _i, _p, _i, _i, _i, _p, _i, _i, _p,
                               _z, _p]),
-    "fpvs_spconv_halo_head": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _p, _z, _p, _p, _f, _p, _i, _p]),
+    "fpvs_spconv_halo_head": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _p, _z, _p, _p, _f, _p, _i, _p,
+                                   _p]),
+    "fpvs_spconv_halo_flow": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _i, _i, _p, _i, _i, _i, _p, _i, _i, _p,
+                                   _z, _p, _p, _p]),
     "fpvs_rowbits_to_grid": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_pack_weights_tc_dgrad": (_i, [_p, _i, _i, _i, _i, _p, _p]),
     "fpvs_pack_weights_tc_multi": (_i, [_p, _i, _p]),

@@ -117,6 +117,12 @@ struct Params {
   int dbg;        // profiling builds: FPVS_HALO_DEBUG (timestamps)
   int abl;        // profiling builds: FPVS_HALO_ABL (ablations)
   int settled;    // tables / tile masks are two or more launches old: decode units before the PDL wait
+  // tile-level dataflow between two convs of one level (fpvs_spconv_halo_flow):
+  // done_out[t] = 1 once this launch's output rows of tile t are stored
+  // (zeroed by the owning CTA at its start); with done_in the launch waits for
+  // the producer tiles its halo reads instead of the whole producer grid
+  int* done_out;
+  const int* done_in;
   // fused 1x1x1 head (dec0b of the U-Net, BN = Cout = d^3 = 64, no split):
   // the tile's bf16 activations become the A operand of 4 TS MMAs against the
   // head weights, then the row's 64 [z >= logit(tau)] bits go to row_bits
@@ -159,6 +165,7 @@ __device__ long long g_hclk[2][160];
 // loaded once in the prologue so no role pays a global-memory round trip at a
 // unit boundary (the MMA thread would stall ~1 us on it).
 constexpr int kUnitCache = 64;
+constexpr int kNumSMsForCache = 148;  // persistent grid size the unit-cache bound assumes
 
 constexpr int LOADERS = 64;
 
@@ -208,7 +215,7 @@ struct Cfg {
   static constexpr int ACOL = NACC * BN;  // TMEM: [accumulators | A slots]
   static constexpr int B_OFF = NHB * HBUF;
   static constexpr int BAR_OFF = B_OFF + NS * STAGE_B;
-  static constexpr int NBARS = 2 * NS + 2 * NACC + 3 * NHB + 2;  // + fused head: weights landed, head MMA done
+  static constexpr int NBARS = 2 * NS + 2 * NACC + 3 * NHB + 3;  // + fused head: weights landed, head MMA done; dataflow
   static constexpr int CTRL_OFF = BAR_OFF + 8 * NBARS;
   static constexpr int BIAS_OFF = CTRL_OFF + 64;
   static constexpr int UC_OFF = BIAS_OFF + 4 * BIAS_N;  // unit cache: Unit [64] + halo sizes [64]
@@ -338,6 +345,7 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
   uint64_t* hmeta = hempty + C::NHB;  // the tile's local table + halo row list landed (bulk copy)
   uint64_t* hwbar = hmeta + C::NHB;   // fused head: weights landed
   uint64_t* hdbar = hwbar + 1;        // fused head: the tile's head MMAs done
+  uint64_t* hdep = hdbar + 1;         // dataflow: the first unit's producer tiles are done
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + C::CTRL_OFF);
   volatile int* s_last = reinterpret_cast<volatile int*>(smem + C::CTRL_OFF + 16);
   float* s_bias = reinterpret_cast<float*>(smem + C::BIAS_OFF);
@@ -381,6 +389,7 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
     }
     mbar_init(smem_u32(hwbar), 1);
     mbar_init(smem_u32(hdbar), 1);
+    mbar_init(smem_u32(hdep), 1);
     fence_mbar_init();
   }
   for (int c = tid; c < p.cout; c += THREADS) s_bias[c] = p.bias ? p.bias[c] : 0.f;
@@ -399,7 +408,12 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
     Unit U{};
     if (u < nunits) unit_of(p, u, cpo, mtiles, U);
     s_units[tid] = U;
+    // dataflow producer: this CTA's tiles are not done yet (the consumer
+    // launches only after every CTA of this grid has passed its trigger, which
+    // comes after this store and the fence below)
+    if (p.done_out && u < nunits) p.done_out[U.mt] = 0;
   }
+  if (p.done_out) __threadfence();
   if (warp == W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
                  "n"(C::TMEM_COLS)
@@ -420,7 +434,9 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
     // one empty-wait, two TMEM stores, one store-wait and one counted arrival
     // (measured: a builder's per-chunk sync, not its shared-memory traffic,
     // paced the N = 64 layers); with G = 1 the groups alternate stages.
-    pdl_wait();  // the direct-read path reads x (the previous launch's output)
+    // the direct-read path reads x (the previous launch's output); in dataflow
+    // mode every such read follows the loaders' wait on the producer tiles
+    if (!p.done_in) pdl_wait();
     const int bg = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     auto grp = [](int i) { return C::G >= NBG ? (i % C::G) / (C::G / NBG) : i % NBG; };
     const uint32_t t_a = tmem_base + ((uint32_t)(q4 * 32) << 16) + C::ACOL;
@@ -442,6 +458,7 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
         if (gc == 0) {
           // the CTA's first halo: nothing to overlap it with, so the 8 builder
           // warps copy it together with the 2 loader warps (10 warps instead of 2)
+          if (p.done_in) mbar_wait(smem_u32(hdep), 0);  // its producer tiles are done
           const int ku = (u - (int)blockIdx.x) / (int)gridDim.x;
           const int H = ku < kUnitCache ? s_uhn[ku] : __ldg(p.halo_n + U.mt);
           const int pt = LOADERS + tid, pc = pt & 7;
@@ -620,6 +637,7 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
     // halo's table + row list copied, before the wait; the halo ROWS are the
     // previous launch's output and always wait
     const bool early = p.settled != 0;
+    const bool flow = p.done_in != nullptr;  // dataflow: no grid-wide wait (flow implies settled)
     if (!early) {
       pdl_wait();
       if (tid == W_LOAD * 32) pdl_trigger();
@@ -653,10 +671,13 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
           if (tl == 0) issue_meta(U, 0, s_uhn[0]);  // buffer 0 is free: nothing has used it yet
         }
       }
-      pdl_wait();
-      if (tid == W_LOAD * 32) pdl_trigger();
+      if (!flow) {
+        pdl_wait();
+        if (tid == W_LOAD * 32) pdl_trigger();
+      }
     }
     uint32_t gc = 0;
+    int dep_mt = -1;  // dataflow: the tile whose producer tiles were last waited for
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
       get_unit(p, u, cpo, mtiles, U, s_units);
@@ -676,6 +697,29 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
         mbar_wait(smem_u32(hmeta + hb), hph);
         if (tl == 0) HTS(17 + 3 * gc);
         const int* hr = reinterpret_cast<const int*>(hbuf + ROWS_OFF);
+        if (flow && U.mt != dep_mt) {
+          // the producer tiles holding this tile's halo rows (the sorted row
+          // list's first and last); a capped or windowless halo (rows read
+          // straight from global memory) waits for every producer tile
+          int lo = 0, hi = mtiles - 1;
+          if (H > 0 && H < HMAX) {
+            lo = hr[0] / BM;
+            hi = hr[H - 1] / BM;
+          }
+          for (int t = lo + tl; t <= hi; t += LOADERS) {
+            long long spins = 0;
+            while (ld_acquire_gpu(p.done_in + t) == 0) {
+              __nanosleep(32);
+              if (++spins > (1LL << 26)) __trap();  // a producer that never finishes: fail, do not hang
+            }
+          }
+          named_bar(2, LOADERS);
+          if (gc == 0 && tl == 0) {
+            mbar_arrive(smem_u32(hdep));  // the builders may copy the first halo
+            pdl_trigger();                // dependents launch once every CTA got here
+          }
+          dep_mt = U.mt;
+        }
         const char* xb = reinterpret_cast<const char*>(p.x) + c * 128 + pc * 16;
         const uint32_t hs = smem_u32(hbuf);
         // the first halo is shared with the builders: loader thread tl takes rows
@@ -695,7 +739,9 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
     }
   } else if (warp == W_B) {
     // ===================== weight loader =====================
-    pdl_wait();  // the packed weights may be the previous launch's output (lazy / per-step re-pack)
+    // the packed weights may be the previous launch's output (lazy / per-step
+    // re-pack); a dataflow consumer's weights are packed before the frame
+    if (!p.done_in) pdl_wait();
     if (lane == 0) {
       uint32_t st = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -783,7 +829,9 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
     }
   } else {
     // ===================== epilogue (4 warps) =====================
-    pdl_wait();  // y, partials and counters may be in use by the previous launch
+    // y, partials and counters may be in use by the previous launch (a
+    // dataflow consumer writes a buffer its producer never touches)
+    if (!p.done_in) pdl_wait();
     const int q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t tlane = (uint32_t)(q4 * 32) << 16;
     const bool fuse_head = C::HEAD && p.head;
@@ -834,6 +882,14 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
+        if (p.done_out) {
+          // dataflow producer: the tile's rows are stored (all four epilogue
+          // warps), then published to the consumer grid
+          // (bar.sync orders the four warps' stores before the release; the
+          // release store is cumulative over them at gpu scope)
+          named_bar(1, 128);
+          if (warp == W_EPI && lane == 0) st_release_gpu(p.done_out + U.mt, 1);
+        }
         if constexpr (C::HEAD) {
           if (fuse_head) {
             // head = 1x1x1 conv of the bf16 activations (exactly what the
@@ -1072,7 +1128,8 @@ struct HeadArgs {
 static int halo_conv(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
                      const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks, const int32_t* n_dev,
                      int cap, const void* w_packed, int bn, int split, const float* bias, int cin, int cout, int act,
-                     void* y, int ldy, int col_off, void* ws, size_t ws_bytes, void* stream, const HeadArgs* head) {
+                     void* y, int ldy, int col_off, void* ws, size_t ws_bytes, void* stream, const HeadArgs* head,
+                     int32_t* done_out = nullptr, const int32_t* done_in = nullptr) {
   FPVS_CHECK_ARG(x && nbr && lnbr && halo_rows && halo_n && tile_masks && n_dev && w_packed && y,
                  "null pointer");
   const int settled = (act & FPVS_TABLES_SETTLED) != 0;
@@ -1121,6 +1178,18 @@ static int halo_conv(const void* x, int ldx, int x_rows, const int32_t* nbr, con
   p.dbg = debug_knob("FPVS_HALO_DEBUG");
   p.abl = debug_knob("FPVS_HALO_ABL");
   p.settled = settled;
+  if (done_out || done_in) {
+    // dataflow needs settled tables (the unit decode precedes any wait), one
+    // unit per tile for a producer, and every CTA's units in the unit cache
+    FPVS_CHECK_ARG(settled || !done_in, "a dataflow consumer needs FPVS_TABLES_SETTLED");
+    FPVS_CHECK_ARG(!done_out || split == 1, "a dataflow producer runs unsplit (split = 1)");
+    FPVS_CHECK_ARG((tiles * p.nblk * (split < 0 ? -split : split) + halo::kNumSMsForCache - 1) /
+                           halo::kNumSMsForCache <= halo::kUnitCache,
+                   "dataflow: more units per CTA than the unit cache holds");
+    FPVS_CHECK_ARG(!done_out || p.nblk == 1, "a dataflow producer writes whole rows per unit (Cout = bn)");
+  }
+  p.done_out = done_out;
+  p.done_in = done_in;
   if (head) {
     FPVS_CHECK_ARG(bn == 64 && cout == 64 && split == 1 && cin % 64 == 0,
                    "fused head needs a Cout = 64 layer with 64-wide tiles, no K split and Cin %% 64 == 0");
@@ -1168,15 +1237,27 @@ extern "C" int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_
                    cout, act, y, ldy, col_off, ws, ws_bytes, stream, nullptr);
 }
 
+extern "C" int fpvs_spconv_halo_flow(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
+                                     const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
+                                     const int32_t* n_dev, int cap, const void* w_packed, int bn, int split,
+                                     const float* bias, int cin, int cout, int act, void* y, int ldy, int col_off,
+                                     void* ws, size_t ws_bytes, int32_t* tile_done_out, const int32_t* tile_done_in,
+                                     void* stream) {
+  return halo_conv(x, ldx, x_rows, nbr, lnbr, halo_rows, halo_n, tile_masks, n_dev, cap, w_packed, bn, split, bias, cin,
+                   cout, act, y, ldy, col_off, ws, ws_bytes, stream, nullptr, tile_done_out, tile_done_in);
+}
+
 extern "C" int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
                                      const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
                                      const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin,
                                      void* ws, size_t ws_bytes, const void* head_w_packed, const float* head_bias,
-                                     float tau, uint64_t* row_bits, int flags, void* stream) {
+                                     float tau, uint64_t* row_bits, int flags, const int32_t* done_in,
+                                     void* stream) {
   const HeadArgs h{head_w_packed, head_bias, tau, reinterpret_cast<unsigned long long*>(row_bits)};
   // the conv's own output is consumed in the epilogue: y is never written
   return halo_conv(x, ldx, x_rows, nbr, lnbr, halo_rows, halo_n, tile_masks, n_dev, cap, w_packed, 64, 1, bias, cin, 64,
-                   FPVS_ACT_RELU | (flags & FPVS_TABLES_SETTLED), row_bits, 64, 0, ws, ws_bytes, stream, &h);
+                   FPVS_ACT_RELU | (flags & FPVS_TABLES_SETTLED), row_bits, 64, 0, ws, ws_bytes, stream, &h, nullptr,
+                   done_in);
 }
 
 namespace fpvs {

@@ -507,7 +507,7 @@ def halo_ok(K: int, cin: int, cout: int, dtype=None) -> bool:
 
 def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int, col_off: int = 0,
              precision: str = "fp32", act: str | None = None, stream=None, bn: int = 0, masks=None,
-             halo=None, halo_tabs=None, out_rows=None, settled: bool = False):
+             halo=None, halo_tabs=None, out_rows=None, settled: bool = False, done_out=None, done_in=None):
     """One sparse conv launch: y[:, col_off:col_off+Cout] = act(gather-GEMM(x, table) + b).
 
     ``masks`` are the table's per-tile offset masks (sparse.tile_masks); the
@@ -518,7 +518,8 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
     (-1 = skip): the parity-sorted up conv (sparse.UpSorter).  ``settled``:
     the tables and tile masks were written two or more launches earlier (the
     halo conv may then decode its units before its programmatic-launch wait,
-    FPVS_TABLES_SETTLED).
+    FPVS_TABLES_SETTLED).  ``done_out`` / ``done_in``: per-tile dataflow flags
+    between two halo convs of one level (fpvs_spconv_halo_flow).
     """
     torch = _torch()
     spec = layer.spec
@@ -532,11 +533,15 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
             masks = sp.tile_masks(table, K, n, cap, stream=stream)
         if halo is not None and halo_ok(K, spec.in_channels, spec.out_channels, x.dtype):
             hbn, split, ws = halo
-            _lib.call("fpvs_spconv_halo", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), _lib.ptr(halo_tabs["lnbr"]),
-                      _lib.ptr(halo_tabs["rows"]), _lib.ptr(halo_tabs["n"]), _lib.ptr(masks), _lib.ptr(n), cap,
-                      _lib.ptr(layer.packed(hbn, stream)), hbn, split, _lib.ptr(layer.b), spec.in_channels,
-                      spec.out_channels, a | (_lib.TABLES_SETTLED if settled else 0), _lib.ptr(y), ldy, col_off,
-                      _lib.ptr(ws), ws.numel(), s)
+            args = [_lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), _lib.ptr(halo_tabs["lnbr"]),
+                    _lib.ptr(halo_tabs["rows"]), _lib.ptr(halo_tabs["n"]), _lib.ptr(masks), _lib.ptr(n), cap,
+                    _lib.ptr(layer.packed(hbn, stream)), hbn, split, _lib.ptr(layer.b), spec.in_channels,
+                    spec.out_channels, a | (_lib.TABLES_SETTLED if settled else 0), _lib.ptr(y), ldy, col_off,
+                    _lib.ptr(ws), ws.numel()]
+            if done_out is not None or done_in is not None:
+                _lib.call("fpvs_spconv_halo_flow", *args, _lib.ptr(done_out), _lib.ptr(done_in), s)
+            else:
+                _lib.call("fpvs_spconv_halo", *args, s)
             return
         if out_rows is not None:
             _lib.call("fpvs_spconv_tc_scatter", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), K, _lib.ptr(masks),

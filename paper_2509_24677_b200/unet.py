@@ -157,6 +157,18 @@ class UNetPlan:
         self.fuse_head = net.precision == "bf16" and os.environ.get("FPVS_FUSE_HEAD", "1") != "0"
         # FPVS_TABLES_SETTLED for the convs after the first (FPVS_SETTLED=0: every conv waits to decode)
         self.settled = os.environ.get("FPVS_SETTLED", "1") != "0"
+        # tile-level dataflow between the two convs of a level (fpvs_spconv_halo_flow;
+        # FPVS_FLOW=0: grid-wide waits only): per-tile done flags of each producer
+        self.flow = self.use_halo and self.settled and os.environ.get("FPVS_FLOW", "1") != "0"
+        # level 0 only: its layers run ~2.5 waves of tiles, so the consumer's first
+        # tiles fill the producer's last wave; a level-1 pair runs one wave of
+        # 111 tiles and measured no faster (dec1b 3 us slower: spinning CTAs)
+        self.flow_pairs = {"enc0b": "enc0a", "dec0b": "dec0a"}
+        self.done = {}
+        if self.flow:
+            for cons, prod in self.flow_pairs.items():
+                lv = self.level_of[prod]
+                self.done[prod] = torch.zeros((lv.cap + 127) // 128, dtype=torch.int32, device=device)
         # the fused head's per-row 64-bit cell masks (fpvs_rowbits_to_grid writes the grid from them)
         self.row_bits = torch.empty(k0, dtype=torch.int64, device=device) if self.fuse_head else None
         self._side = None
@@ -292,6 +304,20 @@ class UNetPlan:
             out.append(("gather", lambda: sp.gather_features(bits, L0, self.grid_dims, net.d, self.x0.dtype,
                                                              out=self.x0)))
 
+        # dataflow pairs usable with this plan's tile settings: the producer
+        # runs unsplit full-width tiles, both convs are halo convs, and the
+        # consumer's weights are packed now (before the frame's launches)
+        flow_in = {}
+        if self.flow and fused:
+            for cons, prod in self.flow_pairs.items():
+                pc, cc = self.halo_cfg.get(prod), self.halo_cfg.get(cons)
+                if pc and cc and pc == (L[prod].spec.out_channels, 1):
+                    flow_in[cons] = self.done[prod]
+                    L[cons].packed(cc[0])
+                    if cons == "dec0b":
+                        L["head"].packed(64)  # the fused head's weights (read without a grid-wide wait)
+        flow_out = {self.flow_pairs[c]: self.done[self.flow_pairs[c]] for c in flow_in}
+
         def conv(name, x, ldx, table, K, lv, y, ldy, off=0, masks=None):
             def launch():
                 if name == "enc1a":
@@ -315,7 +341,8 @@ class UNetPlan:
                 # every conv but the first reads tables the map build wrote two or more launches back
                 run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu", bn=self.bn.get(name, 0),
                          masks=masks, halo=halo, halo_tabs=lv.extra.get("halo") if hc else None,
-                         settled=name != "enc0a" and self.settled)
+                         settled=name != "enc0a" and self.settled,
+                         done_out=flow_out.get(name) if hc else None, done_in=flow_in.get(name) if hc else None)
             out.append((name, launch))
 
         m0, m1, m2 = L0.nbr_masks, L1.nbr_masks, L2.nbr_masks
@@ -343,7 +370,8 @@ class UNetPlan:
                           _lib.ptr(ht["lnbr"]), _lib.ptr(ht["rows"]), _lib.ptr(ht["n"]), _lib.ptr(m0), _lib.ptr(L0.n),
                           L0.cap, _lib.ptr(L["dec0b"].packed(64)), _lib.ptr(L["dec0b"].b), c0, _lib.ptr(ws), ws.numel(),
                           _lib.ptr(hl.packed(64)), _lib.ptr(hl.b), float(tau), _lib.ptr(self.row_bits),
-                          _lib.TABLES_SETTLED if self.settled else 0, _lib.stream_ptr())
+                          _lib.TABLES_SETTLED if self.settled else 0, _lib.ptr(flow_in.get("dec0b")),
+                          _lib.stream_ptr())
                 _lib.call("fpvs_rowbits_to_grid", _lib.ptr(self.row_bits), _lib.ptr(L0.index_vol), self.B, nx, ny, nz,
                           net.d, _lib.ptr(out_bits), _lib.stream_ptr())
             out.append(("dec0b", dec0b_head))

@@ -239,3 +239,35 @@ def test_unet_batch_of_two_equals_two_single_frames():
     got = out2.cpu().numpy().reshape(2, -1)
     assert np.array_equal(got[0], singles[0]) and np.array_equal(got[1], singles[1])
     assert int(np.unpackbits(got).sum()) > 0
+
+
+def test_dataflow_pairs_equal_grid_wide_waits():
+    """Tile-level dataflow between the two convs of a level (per-tile done
+    flags, fpvs_spconv_halo_flow) gives the frame of grid-wide waits bit for
+    bit, eagerly and replayed from a CUDA graph."""
+    import os
+    import torch
+    from paper_2509_24677_b200.pipeline import FramePipeline
+    from paper_2509_24677_b200.unet import PvsUNet
+    for dims, boxes in (((256, 256, 256), 4000), ((128, 128, 128), 600)):
+        occ = synth.box_grid(dims, boxes, 1, 12, 5)
+        bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+        outs = []
+        for flag in ("1", "0"):
+            os.environ["FPVS_FLOW"] = flag
+            try:
+                pipe = FramePipeline(PvsUNet(seed=1), 1, occ.shape)
+            finally:
+                os.environ.pop("FPVS_FLOW", None)
+            assert pipe.plan.flow == (flag == "1")
+            pipe.load(bits)
+            pipe.capture()
+            for _ in range(3):
+                pipe.run_device()
+            torch.cuda.synchronize()
+            outs.append(pipe.out_bits.clone())
+            eager = torch.full_like(pipe.out_bits, 0xA5)
+            pipe.plan.run(bits, eager, 0.5)
+            torch.cuda.synchronize()
+            assert torch.equal(eager, outs[-1])
+        assert torch.equal(outs[0], outs[1]), dims
