@@ -254,6 +254,17 @@ int fpvs_up_sort(const int32_t* up, const int32_t* n_fine_dev, int cap_fine, int
                  size_t workspace_bytes, void* stream);
 int fpvs_up_sort_multi(const fpvs_up_sort_job* jobs, int njobs, void* stream);
 
+/* fpvs_spconv_tc as the consumer of tile-level dataflow (see
+ * fpvs_spconv_halo_flow): x is the output of the launch immediately before,
+ * which publishes tile_done_in[t] = 1 per 128-row tile of its level
+ * (done_n_dev: that level's row count); each output tile waits only for the
+ * producer tiles its gathered rows lie in.  The weights must be packed before
+ * the producer launched and y must be disjoint from the producer's buffers. */
+int fpvs_spconv_tc_flow(const void* x, int ldx, int x_rows, const int32_t* nbr, int K,
+                        const uint32_t* tile_masks, const int32_t* n_out_dev, int cap_out, const void* w_packed,
+                        int bn, const float* bias, int cin, int cout, int act, void* y, int ldy, int col_off,
+                        const int32_t* tile_done_in, const int32_t* done_n_dev, void* stream);
+
 /* fpvs_spconv_tc with an output-row map: tile row i is written to row
  * out_rows[i] of y (skipped when -1).  Used with the parity-sorted up conv. */
 int fpvs_spconv_tc_scatter(const void* x, int ldx, int x_rows, const int32_t* nbr, int K,

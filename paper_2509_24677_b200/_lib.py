@@ -69,6 +69,7 @@ SIGNATURES = {
     "fpvs_up_sort": (_i, [_p, _p, _i, _p, _p, _p, _p, _p, _z, _p]),
     "fpvs_up_sort_multi": (_i, [_p, _i, _p]),
     "fpvs_spconv_tc_scatter": (_i, [_p, _i, _i, _p, _i, _p, _p, _i, _p, _p, _i, _p, _i, _i, _i, _p, _i, _i, _p]),
+    "fpvs_spconv_tc_flow": (_i, [_p, _i, _i, _p, _i, _p, _p, _i, _p, _i, _p, _i, _i, _i, _p, _i, _i, _p, _p, _p]),
     "fpvs_spconv_tc_upblocks": (_i, [_p, _i, _i, _p, _i, _p, _i, _p, _i, _i, _i, _p, _p, _i, _i, _p]),
     "fpvs_head_simt": (_i, [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p, _p]),
     "fpvs_head_tc": (_i, [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p, _p, _p]),

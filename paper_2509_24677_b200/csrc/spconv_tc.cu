@@ -68,6 +68,12 @@ struct Params {
   float* probs;
   float* logits;
   int dbg;  // profiling knob (FPVS_TC_DEBUG): 1 = no MMA, 2 = no A gather, 4 = no B copy, 16 = timestamps
+  // tile-level dataflow consumer (fpvs_spconv_tc_flow): x is the output of the
+  // launch just before, which publishes done_in[t] = 1 per 128-row tile of
+  // its level (done_n: that level's row count); each tile waits only for the
+  // producer tiles its gathered rows lie in, instead of the whole grid
+  const int* done_in;
+  const int* done_n;
 };
 
 template <int BN, int G, int PW = 8, int MINB = 1>
@@ -225,8 +231,13 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
 
   if (warp < C::P) {
     // ===================== A-gather warps =====================
-    pdl_wait();  // x is the previous launch's output
-    if (tid == 0) pdl_trigger();
+    const bool flow = p.done_in != nullptr;
+    if (!flow) {
+      pdl_wait();  // x is the previous launch's output
+      if (tid == 0) pdl_trigger();
+    }
+    __shared__ int s_dep[2][C::P];
+    bool triggered = false;
     // All PROD threads gather every chunk: thread t owns column slot t%8 and
     // rows t/8 + RSTEP*i of the 128B-swizzled A chunk; a stage's full barrier
     // completes when every thread's cp.async pieces have landed (noinc arrival).
@@ -259,6 +270,58 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
         if (!ident) mbar_wait(smem_u32(nfull + (mi & 1)), (mi >> 1) & 1);
 #pragma unroll
         for (int i = 0; i < NPT; ++i) live[i] = row0 + rbase + i * RSTEP < n;
+        if (flow) {
+          // the producer tiles this tile's gathered rows lie in: min / max over
+          // the valid rows' table entries (rows past n hold stale entries)
+          const int* nbn = s_nbr + (mi & 1) * nbr_elems;
+          const int nvalid = ident ? 0 : min(BM, n - row0) * p.K;
+          int lo = 0x7fffffff, hi = -1;
+          if (ident) {
+            lo = row0;
+            hi = min(row0 + BM, n) - 1;
+          } else {
+            for (int e = tid; e < nvalid; e += C::PROD) {
+              const int v = nbn[e];
+              if (v >= 0) {
+                lo = min(lo, v);
+                hi = max(hi, v);
+              }
+            }
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+          }
+          if (lane == 0) {
+            s_dep[0][warp] = lo;
+            s_dep[1][warp] = hi;
+          }
+          named_bar(1, C::PROD);
+          lo = 0x7fffffff;
+          hi = -1;
+#pragma unroll
+          for (int w = 0; w < C::P; ++w) {
+            lo = min(lo, s_dep[0][w]);
+            hi = max(hi, s_dep[1][w]);
+          }
+          const int ptiles = (min(*p.done_n, p.x_rows) + BM - 1) / BM;
+          if (hi >= 0) {
+            const int t1 = min(hi / BM, ptiles - 1);
+            for (int t = lo / BM + tid; t <= t1; t += C::PROD) {
+              long long spins = 0;
+              while (ld_acquire_gpu(p.done_in + t) == 0) {
+                __nanosleep(32);
+                if (++spins > (1LL << 26)) __trap();  // a producer that never finishes: fail, do not hang
+              }
+            }
+          }
+          named_bar(1, C::PROD);  // also: every warp read s_dep before the next tile rewrites it
+          if (!triggered) {
+            triggered = true;
+            if (tid == 0) pdl_trigger();
+          }
+        }
       }
       const int* nb_s = s_nbr + (mi & 1) * nbr_elems;
       ChunkIter itr;
@@ -306,8 +369,9 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
     // Streams each stage's weight chunks with bulk copies (TMA engine) and
     // writes the stage flags the MMA issuer reads.  Waits for the previous
     // launch first: the packed weights may be its output (a lazy or per-step
-    // re-pack enqueued right before this conv).
-    pdl_wait();
+    // re-pack enqueued right before this conv); a dataflow consumer's weights
+    // are packed before its producer launched.
+    if (!p.done_in) pdl_wait();
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -432,7 +496,7 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
     }
   } else {
     // ===================== epilogue (4 warps) =====================
-    pdl_wait();  // y may alias a buffer the previous launch reads
+    if (!p.done_in) pdl_wait();  // y may alias a buffer the previous launch reads (not so for a dataflow consumer)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int r = q * 32 + lane;
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
@@ -782,6 +846,31 @@ extern "C" int fpvs_spconv_tc(const void* x, int ldx, int x_rows, const int32_t*
   p.y = (__nv_bfloat16*)y;
   p.ldy = ldy;
   p.col_off = col_off;
+  return tc::dispatch(p, bn, as_stream(stream));
+}
+
+extern "C" int fpvs_spconv_tc_flow(const void* x, int ldx, int x_rows, const int32_t* nbr, int K,
+                                   const uint32_t* tile_masks, const int32_t* n_out_dev, int cap_out,
+                                   const void* w_packed, int bn, const float* bias, int cin, int cout, int act, void* y,
+                                   int ldy, int col_off, const int32_t* tile_done_in, const int32_t* done_n_dev,
+                                   void* stream) {
+  tc::Params p;
+  bn = resolve_bn(bn, cout);
+  FPVS_CHECK_ARG(bn > 0, "tile width must be 0 (auto), 32, 64, 128 or 256");
+  int rc = tc_common(p, x, ldx, x_rows, nbr, K, tile_masks, n_out_dev, cap_out, w_packed, bias, cin, cout, bn);
+  if (rc) return rc;
+  FPVS_CHECK_ARG(y, "null output");
+  FPVS_CHECK_ARG(cout % 32 == 0, "tcgen05 store epilogue needs Cout %% 32 == 0, got %d", cout);
+  FPVS_CHECK_ARG(ldy % 8 == 0 && col_off % 8 == 0 && ldy >= col_off + cout, "bad output leading dimension");
+  FPVS_CHECK_ARG(act == FPVS_ACT_NONE || act == FPVS_ACT_RELU, "tcgen05 store epilogue supports none/relu");
+  FPVS_CHECK_ARG(!tile_done_in || done_n_dev, "tile_done_in needs the producer's row count");
+  if (cap_out <= 0) return FPVS_OK;
+  p.act = act;
+  p.y = (__nv_bfloat16*)y;
+  p.ldy = ldy;
+  p.col_off = col_off;
+  p.done_in = tile_done_in;
+  p.done_n = done_n_dev;
   return tc::dispatch(p, bn, as_stream(stream));
 }
 

@@ -519,7 +519,8 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
     the tables and tile masks were written two or more launches earlier (the
     halo conv may then decode its units before its programmatic-launch wait,
     FPVS_TABLES_SETTLED).  ``done_out`` / ``done_in``: per-tile dataflow flags
-    between two halo convs of one level (fpvs_spconv_halo_flow).
+    between two halo convs of one level (fpvs_spconv_halo_flow); for the plain
+    gather-GEMM ``done_in`` = (flags, producer row count) (fpvs_spconv_tc_flow).
     """
     torch = _torch()
     spec = layer.spec
@@ -548,10 +549,14 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
                       _lib.ptr(n), cap, _lib.ptr(out_rows), _lib.ptr(layer.packed(bn, stream)), bn, _lib.ptr(layer.b),
                       spec.in_channels, spec.out_channels, a, _lib.ptr(y), ldy, col_off, s)
             return
-        _lib.call("fpvs_spconv_tc", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), K, _lib.ptr(masks), _lib.ptr(n),
-                  cap,
-                  _lib.ptr(layer.packed(bn, stream)), bn, _lib.ptr(layer.b), spec.in_channels, spec.out_channels, a,
-                  _lib.ptr(y), ldy, col_off, s)
+        targs = [_lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), K, _lib.ptr(masks), _lib.ptr(n), cap,
+                 _lib.ptr(layer.packed(bn, stream)), bn, _lib.ptr(layer.b), spec.in_channels, spec.out_channels, a,
+                 _lib.ptr(y), ldy, col_off]
+        if done_in is not None:
+            done_flags, done_n = done_in
+            _lib.call("fpvs_spconv_tc_flow", *targs, _lib.ptr(done_flags), _lib.ptr(done_n), s)
+        else:
+            _lib.call("fpvs_spconv_tc", *targs, s)
     else:
         idt = _lib.BF16 if x.dtype == torch.bfloat16 else _lib.F32
         odt = _lib.BF16 if y.dtype == torch.bfloat16 else _lib.F32

@@ -164,9 +164,13 @@ class UNetPlan:
         # tiles fill the producer's last wave; a level-1 pair runs one wave of
         # 111 tiles and measured no faster (dec1b 3 us slower: spinning CTAs)
         self.flow_pairs = {"enc0b": "enc0a", "dec0b": "dec0a"}
+        # the first down conv (a plain gather-GEMM) as a consumer of enc0b
+        # (fpvs_spconv_tc_flow): measured 2 us slower per frame (enc0b's
+        # per-tile publishing outweighs down01's head start), so opt-in only
+        self.flow_tc = {"down01": "enc0b"} if os.environ.get("FPVS_FLOW_TC", "0") == "1" else {}
         self.done = {}
         if self.flow:
-            for cons, prod in self.flow_pairs.items():
+            for prod in list(self.flow_pairs.values()) + list(self.flow_tc.values()):
                 lv = self.level_of[prod]
                 self.done[prod] = torch.zeros((lv.cap + 127) // 128, dtype=torch.int32, device=device)
         # the fused head's per-row 64-bit cell masks (fpvs_rowbits_to_grid writes the grid from them)
@@ -317,6 +321,14 @@ class UNetPlan:
                     if cons == "dec0b":
                         L["head"].packed(64)  # the fused head's weights (read without a grid-wide wait)
         flow_out = {self.flow_pairs[c]: self.done[self.flow_pairs[c]] for c in flow_in}
+        flow_tc = {}
+        if self.flow and fused:
+            for cons, prod in self.flow_tc.items():
+                pc = self.halo_cfg.get(prod)
+                if pc and pc == (L[prod].spec.out_channels, 1):
+                    flow_tc[cons] = (self.done[prod], self.level_of[prod].n)
+                    flow_out[prod] = self.done[prod]
+                    L[cons].packed(self.bn.get(cons, 0))
 
         def conv(name, x, ldx, table, K, lv, y, ldy, off=0, masks=None):
             def launch():
@@ -342,7 +354,8 @@ class UNetPlan:
                 run_conv(L[name], x, ldx, table, K, lv.n, lv.cap, y, ldy, off, P, act="relu", bn=self.bn.get(name, 0),
                          masks=masks, halo=halo, halo_tabs=lv.extra.get("halo") if hc else None,
                          settled=name != "enc0a" and self.settled,
-                         done_out=flow_out.get(name) if hc else None, done_in=flow_in.get(name) if hc else None)
+                         done_out=flow_out.get(name) if hc else None,
+                         done_in=flow_in.get(name) if hc else flow_tc.get(name))
             out.append((name, launch))
 
         m0, m1, m2 = L0.nbr_masks, L1.nbr_masks, L2.nbr_masks

@@ -253,13 +253,15 @@ def test_dataflow_pairs_equal_grid_wide_waits():
         occ = synth.box_grid(dims, boxes, 1, 12, 5)
         bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
         outs = []
-        for flag in ("1", "0"):
-            os.environ["FPVS_FLOW"] = flag
+        # level-0 halo pairs (default), + the down conv as a gather-GEMM consumer, off
+        for flag, tc in (("1", "0"), ("1", "1"), ("0", "0")):
+            os.environ["FPVS_FLOW"], os.environ["FPVS_FLOW_TC"] = flag, tc
             try:
                 pipe = FramePipeline(PvsUNet(seed=1), 1, occ.shape)
             finally:
                 os.environ.pop("FPVS_FLOW", None)
-            assert pipe.plan.flow == (flag == "1")
+                os.environ.pop("FPVS_FLOW_TC", None)
+            assert pipe.plan.flow == (flag == "1") and bool(pipe.plan.flow_tc) == (tc == "1")
             pipe.load(bits)
             pipe.capture()
             for _ in range(3):
@@ -270,4 +272,4 @@ def test_dataflow_pairs_equal_grid_wide_waits():
             pipe.plan.run(bits, eager, 0.5)
             torch.cuda.synchronize()
             assert torch.equal(eager, outs[-1])
-        assert torch.equal(outs[0], outs[1]), dims
+        assert torch.equal(outs[0], outs[2]) and torch.equal(outs[1], outs[2]), dims
