@@ -256,7 +256,7 @@ int fpvs_up_sort_multi(const fpvs_up_sort_job* jobs, int njobs, void* stream);
 
 /* fpvs_spconv_tc as the consumer of tile-level dataflow (see
  * fpvs_spconv_halo_flow): x is the output of the launch immediately before,
- * which publishes tile_done_in[t] = 1 per 128-row tile of its level
+ * which publishes tile_done_in[t] = 4 per 128-row tile of its level
  * (done_n_dev: that level's row count); each output tile waits only for the
  * producer tiles its gathered rows lie in.  The weights must be packed before
  * the producer launched and y must be disjoint from the producer's buffers. */
@@ -329,8 +329,9 @@ int fpvs_spconv_halo(const void* x, int ldx, int x_rows, const int32_t* nbr, con
 /* fpvs_spconv_halo with tile-level dataflow between two convs of ONE level
  * (same tables; the consumer reads the producer's output):
  * tile_done_out (int32 [tiles], nullable): the producer's per-tile flags — the
- * CTA owning tile t zeroes it at its start and sets it to 1 once the tile's
- * output rows are stored (split must be 1, bn = Cout).  tile_done_in
+ * CTA owning tile t zeroes it at its start and it reaches 4 once the tile's
+ * output rows are stored (one release add per epilogue warp; split must be 1,
+ * bn = Cout).  tile_done_in
  * (nullable): the producer's flags; the consumer, launched right after it
  * with programmatic dependent launch, then skips the grid-wide wait and each
  * CTA waits only for the producer tiles holding its tile's halo rows (all of

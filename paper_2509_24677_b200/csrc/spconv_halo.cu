@@ -118,7 +118,7 @@ struct Params {
   int abl;        // profiling builds: FPVS_HALO_ABL (ablations)
   int settled;    // tables / tile masks are two or more launches old: decode units before the PDL wait
   // tile-level dataflow between two convs of one level (fpvs_spconv_halo_flow):
-  // done_out[t] = 1 once this launch's output rows of tile t are stored
+  // done_out[t] reaches 4 (one release add per epilogue warp) once this launch's rows of tile t are stored
   // (zeroed by the owning CTA at its start); with done_in the launch waits for
   // the producer tiles its halo reads instead of the whole producer grid
   int* done_out;
@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
           }
           for (int t = lo + tl; t <= hi; t += LOADERS) {
             long long spins = 0;
-            while (ld_acquire_gpu(p.done_in + t) == 0) {
+            while (ld_acquire_gpu(p.done_in + t) < 4) {
               __nanosleep(32);
               if (++spins > (1LL << 26)) __trap();  // a producer that never finishes: fail, do not hang
             }
@@ -883,12 +883,11 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
         if (p.done_out) {
-          // dataflow producer: the tile's rows are stored (all four epilogue
-          // warps), then published to the consumer grid
-          // (bar.sync orders the four warps' stores before the release; the
-          // release store is cumulative over them at gpu scope)
-          named_bar(1, 128);
-          if (warp == W_EPI && lane == 0) st_release_gpu(p.done_out + U.mt, 1);
+          // dataflow producer: each epilogue warp publishes its 32 rows with a
+          // release add once they are stored (__syncwarp orders the lanes'
+          // stores before lane 0's cumulative release); 4 = the tile is done
+          __syncwarp();
+          if (lane == 0) red_add_release_gpu(p.done_out + U.mt, 1);
         }
         if constexpr (C::HEAD) {
           if (fuse_head) {

@@ -69,7 +69,7 @@ struct Params {
   float* logits;
   int dbg;  // profiling knob (FPVS_TC_DEBUG): 1 = no MMA, 2 = no A gather, 4 = no B copy, 16 = timestamps
   // tile-level dataflow consumer (fpvs_spconv_tc_flow): x is the output of the
-  // launch just before, which publishes done_in[t] = 1 per 128-row tile of
+  // launch just before, which publishes done_in[t] = 4 per 128-row tile of
   // its level (done_n: that level's row count); each tile waits only for the
   // producer tiles its gathered rows lie in, instead of the whole grid
   const int* done_in;
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(Cfg<BN, G, PW, MINB>::THREADS, MINB) spconv_tc
             const int t1 = min(hi / BM, ptiles - 1);
             for (int t = lo / BM + tid; t <= t1; t += C::PROD) {
               long long spins = 0;
-              while (ld_acquire_gpu(p.done_in + t) == 0) {
+              while (ld_acquire_gpu(p.done_in + t) < 4) {  // four epilogue warps per producer tile
                 __nanosleep(32);
                 if (++spins > (1LL << 26)) __trap();  // a producer that never finishes: fail, do not hang
               }
