@@ -507,7 +507,8 @@ def halo_ok(K: int, cin: int, cout: int, dtype=None) -> bool:
 
 def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int, col_off: int = 0,
              precision: str = "fp32", act: str | None = None, stream=None, bn: int = 0, masks=None,
-             halo=None, halo_tabs=None, out_rows=None, settled: bool = False, done_out=None, done_in=None):
+             halo=None, halo_tabs=None, out_rows=None, settled: bool = False, done_out=None, done_in=None,
+             done_n=None):
     """One sparse conv launch: y[:, col_off:col_off+Cout] = act(gather-GEMM(x, table) + b).
 
     ``masks`` are the table's per-tile offset masks (sparse.tile_masks); the
@@ -519,8 +520,9 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
     the tables and tile masks were written two or more launches earlier (the
     halo conv may then decode its units before its programmatic-launch wait,
     FPVS_TABLES_SETTLED).  ``done_out`` / ``done_in``: per-tile dataflow flags
-    between two halo convs of one level (fpvs_spconv_halo_flow); for the plain
-    gather-GEMM ``done_in`` = (flags, producer row count) (fpvs_spconv_tc_flow).
+    between two halo convs of one level (fpvs_spconv_halo_flow); the plain
+    gather-GEMM takes ``done_in`` with ``done_n``, the producer level's row
+    count (fpvs_spconv_tc_flow).
     """
     torch = _torch()
     spec = layer.spec
@@ -553,8 +555,9 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
                  _lib.ptr(layer.packed(bn, stream)), bn, _lib.ptr(layer.b), spec.in_channels, spec.out_channels, a,
                  _lib.ptr(y), ldy, col_off]
         if done_in is not None:
-            done_flags, done_n = done_in
-            _lib.call("fpvs_spconv_tc_flow", *targs, _lib.ptr(done_flags), _lib.ptr(done_n), s)
+            if done_n is None:
+                raise ValueError("a gather-GEMM dataflow consumer needs the producer's row count (done_n)")
+            _lib.call("fpvs_spconv_tc_flow", *targs, _lib.ptr(done_in), _lib.ptr(done_n), s)
         else:
             _lib.call("fpvs_spconv_tc", *targs, s)
     else:

@@ -321,12 +321,13 @@ class UNetPlan:
                     if cons == "dec0b":
                         L["head"].packed(64)  # the fused head's weights (read without a grid-wide wait)
         flow_out = {self.flow_pairs[c]: self.done[self.flow_pairs[c]] for c in flow_in}
-        flow_tc = {}
+        flow_tc, flow_n = {}, {}
         if self.flow and fused:
             for cons, prod in self.flow_tc.items():
                 pc = self.halo_cfg.get(prod)
                 if pc and pc == (L[prod].spec.out_channels, 1):
-                    flow_tc[cons] = (self.done[prod], self.level_of[prod].n)
+                    flow_tc[cons] = self.done[prod]
+                    flow_n[cons] = self.level_of[prod].n
                     flow_out[prod] = self.done[prod]
                     L[cons].packed(self.bn.get(cons, 0))
 
@@ -355,7 +356,7 @@ class UNetPlan:
                          masks=masks, halo=halo, halo_tabs=lv.extra.get("halo") if hc else None,
                          settled=name != "enc0a" and self.settled,
                          done_out=flow_out.get(name) if hc else None,
-                         done_in=flow_in.get(name) if hc else flow_tc.get(name))
+                         done_in=flow_in.get(name) if hc else flow_tc.get(name), done_n=flow_n.get(name))
             out.append((name, launch))
 
         m0, m1, m2 = L0.nbr_masks, L1.nbr_masks, L2.nbr_masks
