@@ -1,6 +1,8 @@
 // Shared helpers for libfpvs (sm_100a).
 #pragma once
 
+#include <mutex>
+
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -85,6 +87,16 @@ inline int debug_knob(const char* name) {
 #define FPVS_KNOB(p) 0
 inline int debug_knob(const char*) { return 0; }
 #endif
+
+// The kernel's dynamic shared-memory ceiling, set once per process and kernel
+// (thread-safe: the C ABI may be called from several host threads).
+template <auto Kernel>
+inline cudaError_t set_smem_once(int bytes) {
+  static std::once_flag flag;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(flag, [&] { err = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
+  return err;
+}
 
 inline int grid_for(long long work, int block, int per_sm = 8) {
   long long g = (work + block - 1) / block;

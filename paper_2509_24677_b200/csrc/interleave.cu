@@ -692,11 +692,7 @@ int launch_il_tile(const void* in, int B, int Nx, int Ny, int Nz, void* out, uin
   const int nzc = (Nz + zt - 1) / zt;
   const long long ntiles = (long long)B * (Nx / D) * (Ny / D) * nzc;
   const size_t smem = 2 * (size_t)D * D * (zt + pad_elems<32, Tin>()) * sizeof(Tin);
-  static bool cfg = false;
-  if (!cfg) {
-    cudaFuncSetAttribute(il_tma_kernel<Tin, Tout, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cfg = true;
-  }
+  set_smem_once<il_tma_kernel<Tin, Tout, D>>(64 * 1024);
   const long long grid = ntiles < (long long)kNumSMs * 6 ? ntiles : (long long)kNumSMs * 6;
   il_tma_kernel<Tin, Tout, D><<<(unsigned)grid, kTileThreads, smem, s>>>((const Tin*)in, Nx, Ny, Nz, zt, ntiles,
                                                                          (Tout*)out, cell_active);
@@ -724,11 +720,7 @@ int launch_deil_tile(const void* in, int B, int X, int Y, int Z, void* out, cuda
   const int nzc = (Nz + zt - 1) / zt;
   const long long ntiles = (long long)B * X * Y * nzc;
   const size_t smem = 2 * (size_t)zt * D * D * sizeof(Tin) + (size_t)D * D * (zt + pad_elems<32, Tout>()) * sizeof(Tout);
-  static bool cfg = false;
-  if (!cfg) {
-    cudaFuncSetAttribute(deil_tma_kernel<Tin, Tout, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cfg = true;
-  }
+  set_smem_once<deil_tma_kernel<Tin, Tout, D>>(96 * 1024);
   const long long grid = ntiles < (long long)kNumSMs * 4 ? ntiles : (long long)kNumSMs * 4;
   deil_tma_kernel<Tin, Tout, D><<<(unsigned)grid, kTileThreads, smem, s>>>((const Tin*)in, X, Y, Z, zt, ntiles,
                                                                            (Tout*)out);

@@ -621,12 +621,12 @@ extern "C" int fpvs_levels_from_bits(const uint8_t* bits, int B, int Nx, int Ny,
   FPVS_CHECK_LAUNCH("fpvs_levels_from_bits(compact)");
   a.reset_only = stop == 2;
   // K3: one resident wave (a second wave of persistent blocks would serialise)
-  static int k3_per_sm = 0;
-  if (!k3_per_sm) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k3_per_sm, lv::tables_kernel, lv::kThreads, 0) != cudaSuccess ||
-        k3_per_sm < 1)
-      k3_per_sm = 1;
-  }
+  static const int k3_per_sm = [] {  // thread-safe one-time occupancy query
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, lv::tables_kernel, lv::kThreads, 0) != cudaSuccess || v < 1)
+      v = 1;
+    return v;
+  }();
   e = launch_kernel(lv::tables_kernel, dim3(kNumSMs * k3_per_sm), dim3(lv::kThreads), 0, s, a);
   if (e != cudaSuccess) return set_error(FPVS_ECUDA, "fpvs_levels_from_bits(tables): %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("fpvs_levels_from_bits(tables)");

@@ -1016,13 +1016,9 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
 template <int BN, bool PAIR, int NBG, int MINB = 1>
 int launch(const Params& p, cudaStream_t s) {
   using C = Cfg<BN, NBG, MINB>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(spconv_halo_kernel<BN, PAIR, NBG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::SMEM);
+  {
+    const cudaError_t e = set_smem_once<spconv_halo_kernel<BN, PAIR, NBG, MINB>>(C::SMEM);
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    configured = true;
   }
   const long long units = (long long)((p.cap + BM - 1) / BM) * p.nblk * p.smax;
   if (p.cout > C::BIAS_N) return set_error(FPVS_EINVAL, "spconv_halo: Cout %d > %d", p.cout, C::BIAS_N);

@@ -630,19 +630,11 @@ static int launch_simt(const void* x, int ldx, int in_dtype, const int32_t* nbr,
     const int g2 = grid_for((cap + kT2M - 1) / kT2M, 1, 8);
     const size_t sh = sizeof(float) * (2 * kT2CinMax * (kT2M + 4) + 2 * kT2CinMax * cout) + sizeof(int) * kT2M * K;
     if (cout == 32) {
-      static bool cfg32 = false;
-      if (!cfg32) {
-        cudaFuncSetAttribute(spconv_simt_tap_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        cfg32 = true;
-      }
+      set_smem_once<spconv_simt_tap_kernel<32>>(96 * 1024);
       spconv_simt_tap_kernel<32><<<g2, kT2M * 32 / 16, sh, s>>>((const float*)x, ldx, nbr, K, n_dev, cap, w, bias, cin,
                                                               cout, act, (float*)y, ldy, col_off);
     } else {
-      static bool cfg64 = false;
-      if (!cfg64) {
-        cudaFuncSetAttribute(spconv_simt_tap_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        cfg64 = true;
-      }
+      set_smem_once<spconv_simt_tap_kernel<64>>(96 * 1024);
       spconv_simt_tap_kernel<64><<<g2, kT2M * 64 / 16, sh, s>>>((const float*)x, ldx, nbr, K, n_dev, cap, w, bias, cin,
                                                               cout, act, (float*)y, ldy, col_off);
     }

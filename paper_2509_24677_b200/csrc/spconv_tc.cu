@@ -723,12 +723,9 @@ inline bool valid_bn(int bn) { return bn == 32 || bn == 64 || bn == 128 || bn ==
 template <int BN, int G, int PW, int MINB>
 int launch_cfg(const Params& p, cudaStream_t s) {
   using C = Cfg<BN, G, PW, MINB>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(spconv_tc_kernel<BN, G, PW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM);
+  {
+    const cudaError_t e = set_smem_once<spconv_tc_kernel<BN, G, PW, MINB>>(C::SMEM);
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    configured = true;
   }
   long long tiles = (long long)((p.cap + BM - 1) / BM) * p.nblk;
   long long slots = (long long)kNumSMs * MINB;

@@ -373,11 +373,9 @@ extern "C" int fpvs_spconv_wgrad_halo(const void* x, int ldx, const void* dz, in
   FPVS_CHECK_ARG(ldx % 8 == 0 && ldx >= cin && lddz % 8 == 0 && lddz >= cout, "row strides must be multiples of 8");
   FPVS_CHECK_ARG(workspace_bytes >= fpvs_wgrad_halo_workspace_size(cap), "workspace too small");
   if (cap <= 0) return FPVS_OK;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(wgh::wgrad_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wgh::SMEM);
+  {
+    const cudaError_t e = set_smem_once<wgh::wgrad_halo_kernel>(wgh::SMEM);
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    configured = true;
   }
   wgh::Params p{};
   p.x = (const __nv_bfloat16*)x;

@@ -341,11 +341,9 @@ template <int NPAD>
 int launch(const Params& p, cudaStream_t s) {
   constexpr int B_STAGE = (NPAD / 8) * 1024;
   constexpr int SMEM = 1024 + NS * (A_STAGE + B_STAGE) + 1024 + KC * 32 * 4;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(wgrad_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  {
+    const cudaError_t e = set_smem_once<wgrad_tc_kernel<NPAD>>(SMEM);
     if (e != cudaSuccess) return set_error(FPVS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    configured = true;
   }
   cudaError_t e = launch_kernel(wgrad_tc_kernel<NPAD>, dim3(p.nmb * p.nsplit), dim3(THREADS), SMEM, s, p);
   if (e != cudaSuccess) return set_error(FPVS_ECUDA, "wgrad_tc: %s", cudaGetErrorString(e));
