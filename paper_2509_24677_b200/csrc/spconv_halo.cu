@@ -1258,12 +1258,16 @@ extern "C" int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const i
 namespace fpvs {
 namespace halo {
 // Per-row head bits -> the packed froxel grid (d = 4).  Block = (b, cell row
-// cy, RZ cells of z); its cells' 64-bit masks are staged in shared memory
+// cy, RZ = 4 cells of z: 1024 small blocks keep more gathers in flight than
+// fewer, larger ones); its cells' 64-bit masks are staged in shared memory
 // (level-0 index volume, coalesced along z, read before the PDL wait: it is
 // the map kernels' output), then thread (z cell, 32-froxel word w) assembles
 // the 16 words of its 8 cells' (ly, lz) voxel rows: every word of the grid is
 // written exactly once, no atomics and no clear.
-constexpr int RZ = 16;
+#ifndef FPVS_ROWBITS_RZ
+#define FPVS_ROWBITS_RZ 4  // measured 16 / 8 / 4 / 2 / 1: 313.3 / 311.3 / 309.3 / 311.3 / 313.3 us per frame
+#endif
+constexpr int RZ = FPVS_ROWBITS_RZ;  // z cells per grid-writer block
 __device__ __forceinline__ unsigned long long ld_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
