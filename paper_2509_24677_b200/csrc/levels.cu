@@ -8,7 +8,7 @@
 // three launches:
 //
 //   K1  level-0 active flags from the packed bits (one block per
-//       (b, cell-row y, 32 cells of z): lanes read contiguous bytes of a voxel
+//       (b, cell-row y, kZC = 16 cells of z): lanes read contiguous bytes of a voxel
 //       row, the d^2 rows of a cell are loaded back to back (d is a template
 //       parameter, so the loads are independent and in flight together));
 //   K2  single-pass compaction of EVERY level (decoupled look-back with a
@@ -34,6 +34,10 @@ constexpr int kThreads = 256;
 constexpr int kPer = 16;                    // cells per scan thread
 constexpr int kTileCells = kThreads * kPer;  // 4096
 constexpr int kRows = 128;                  // table rows per K3 unit (one conv tile)
+#ifndef FPVS_K1_ZC
+#define FPVS_K1_ZC 16  // measured 32 / 16 / 8: 309-311 / 307 / 307 us per frame (more blocks in flight)
+#endif
+constexpr int kZC = FPVS_K1_ZC;             // K1: level-0 z cells per block
 constexpr unsigned kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValMask = (1u << 30) - 1u;
 
 struct LevelDev {
@@ -91,16 +95,16 @@ template <int D, int W>
 __global__ void __launch_bounds__(kThreads) l0_flags_kernel(const Args a) {
   // K2 is launched programmatically: let it take its tile tickets while we run
   if (threadIdx.x == 0) pdl_trigger();
-  extern __shared__ uint8_t s_flag[];  // [X][33]
+  extern __shared__ uint8_t s_flag[];  // [X][kZC + 1]
   using T = typename std::conditional<W == 4, uint32_t, uint8_t>::type;
   const int X = a.L[0].X, Y = a.L[0].Y, Z = a.L[0].Z;
-  const int nzc = (Z + 31) / 32;
+  const int nzc = (Z + kZC - 1) / kZC;
   int blk = blockIdx.x;
   const int zc = blk % nzc;
   blk /= nzc;
   const int cy = blk % Y;
   const int b = blk / Y;
-  const int cz0 = zc * 32, nz = min(32, Z - cz0);
+  const int cz0 = zc * kZC, nz = min(kZC, Z - cz0);
   const int roww = a.Nx / (8 * W);  // words per voxel row
   const long long plane = (long long)(a.Nx >> 3) * a.Ny * a.Nz;
   const T* gb = reinterpret_cast<const T*>(a.bits + b * plane);
@@ -120,13 +124,13 @@ __global__ void __launch_bounds__(kThreads) l0_flags_kernel(const Args a) {
     for (int i = 0; i < D * D; ++i) o |= (uint32_t)v[i];
     constexpr uint32_t M = D >= 32 ? 0xffffffffu : (1u << D) - 1u;
 #pragma unroll
-    for (int i = 0; i < CPW; ++i) s_flag[(xw * CPW + i) * 33 + czl] = ((o >> (i * D)) & M) ? 1 : 0;
+    for (int i = 0; i < CPW; ++i) s_flag[(xw * CPW + i) * (kZC + 1) + czl] = ((o >> (i * D)) & M) ? 1 : 0;
   }
   __syncthreads();
   const long long rowbase = ((long long)b * X) * Y * Z;
   for (int u = threadIdx.x; u < X * nz; u += kThreads) {
     const int cx = u / nz, zl = u - cx * nz;
-    a.act[0][rowbase + ((long long)cx * Y + cy) * Z + cz0 + zl] = s_flag[cx * 33 + zl];
+    a.act[0][rowbase + ((long long)cx * Y + cy) * Z + cz0 + zl] = s_flag[cx * (kZC + 1) + zl];
   }
   for (int l = 1; l < a.nlev; ++l) {
     const int F = 1 << l, Xl = X >> l, Yl = Y >> l, Zl = Z >> l, nzl = nz >> l;
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) l0_flags_kernel(const Args a) {
       const int cx = u / nzl, zl = u - cx * nzl;
       uint32_t any = 0;
       for (int dx = 0; dx < F; ++dx)
-        for (int dz = 0; dz < F; ++dz) any |= s_flag[(cx * F + dx) * 33 + zl * F + dz];
+        for (int dz = 0; dz < F; ++dz) any |= s_flag[(cx * F + dx) * (kZC + 1) + zl * F + dz];
       if (any) a.act[l][(((long long)b * Xl + cx) * Yl + (cy >> l)) * Zl + (cz0 >> l) + zl] = 1;
     }
   }
@@ -551,7 +555,7 @@ extern "C" int fpvs_levels_from_bits(const uint8_t* bits, int B, int Nx, int Ny,
   const long long nc0 = (long long)B * X * Y * Z;
   FPVS_CHECK_ARG(nc0 < (1LL << 30), "cell grid too large (%lld cells)", nc0);
   FPVS_CHECK_ARG(workspace_bytes >= fpvs_levels_workspace_size(B, Nx, Ny, Nz, d, nlev), "workspace too small");
-  FPVS_CHECK_ARG((X * 33) <= 48 * 1024, "N_x / d too large for the flag transpose");
+  FPVS_CHECK_ARG((X * (lv::kZC + 1)) <= 48 * 1024, "N_x / d too large for the flag transpose");
   FPVS_CHECK_ARG(!feat || (feat_dtype == FPVS_F32 || feat_dtype == FPVS_BF16), "bad feature dtype");
   FPVS_CHECK_ARG(!feat || ldf >= d * d * d, "feature ld %d < d^3", ldf);
   lv::Args a{};
@@ -601,8 +605,8 @@ extern "C" int fpvs_levels_from_bits(const uint8_t* bits, int B, int Nx, int Ny,
   a.clear = clear_bits;
   a.clear_bytes = clear_bits ? (long long)clear_bytes : 0;
   cudaStream_t s = as_stream(stream);
-  const unsigned k1 = (unsigned)((long long)B * Y * ((Z + 31) / 32));
-  const size_t smem1 = (size_t)X * 33;
+  const unsigned k1 = (unsigned)((long long)B * Y * ((Z + lv::kZC - 1) / lv::kZC));
+  const size_t smem1 = (size_t)X * (lv::kZC + 1);
 #define FPVS_K1(D)                                                                      \
   if (Nx % 32 == 0) lv::l0_flags_kernel<D, 4><<<k1, lv::kThreads, smem1, s>>>(a);        \
   else lv::l0_flags_kernel<D, 1><<<k1, lv::kThreads, smem1, s>>>(a);
