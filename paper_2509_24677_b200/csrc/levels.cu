@@ -32,7 +32,11 @@ namespace lv {
 constexpr int kMaxLev = 4;
 constexpr int kThreads = 256;
 constexpr int kPer = 16;                    // cells per scan thread
-constexpr int kTileCells = kThreads * kPer;  // 4096
+#ifndef FPVS_K2_THREADS
+#define FPVS_K2_THREADS 256  // measured 64 / 128 / 256 / 512 / 1024: 317 / 310 / 307 / 309 / 311 us per frame
+#endif
+constexpr int kThreads2 = FPVS_K2_THREADS;   // K2 block size (scan tile = kThreads2 * kPer cells)
+constexpr int kTileCells = kThreads2 * kPer;
 constexpr int kRows = 128;                  // table rows per K3 unit (one conv tile)
 #ifndef FPVS_K1_ZC
 #define FPVS_K1_ZC 16  // measured 32 / 16 / 8: 309-311 / 307 / 307 us per frame (more blocks in flight)
@@ -161,9 +165,9 @@ __device__ __forceinline__ uint32_t level_flags16(const Args& a, int l, int r0, 
   return f;
 }
 
-__global__ void __launch_bounds__(kThreads) compact_levels_kernel(const Args a) {
+__global__ void __launch_bounds__(kThreads2) compact_levels_kernel(const Args a) {
   __shared__ int s_tile, s_prefix;
-  __shared__ int s_warp[kThreads / 32];
+  __shared__ int s_warp[kThreads2 / 32];
   int l = 0;
   while (l + 1 < a.nlev && (int)blockIdx.x >= a.tile_base[l + 1]) ++l;
   const LevelDev& L = a.L[l];
@@ -189,14 +193,14 @@ __global__ void __launch_bounds__(kThreads) compact_levels_kernel(const Args a) 
   if (lane == 31) s_warp[wid] = incl;
   __syncthreads();
   if (wid == 0) {
-    const int w = lane < kThreads / 32 ? s_warp[lane] : 0;
+    const int w = lane < kThreads2 / 32 ? s_warp[lane] : 0;
     int wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int t = __shfl_up_sync(0xffffffffu, wi, o);
       if (lane >= o) wi += t;
     }
-    if (lane < kThreads / 32) s_warp[lane] = wi - w;
+    if (lane < kThreads2 / 32) s_warp[lane] = wi - w;
     const unsigned agg = (unsigned)__shfl_sync(0xffffffffu, wi, 31);
     unsigned prefix = 0;
     if (tile == 0) {
@@ -437,7 +441,10 @@ __device__ void gather_unit(const Args& a, int n, int tile) {
 
 constexpr int kClearChunk = kThreads * 64;  // bytes per clear unit
 
-__global__ void __launch_bounds__(kThreads) tables_kernel(const Args a) {
+#ifndef FPVS_K3_MINB
+#define FPVS_K3_MINB 4  // >= 4 resident blocks per SM (without it ptxas takes 109 registers: 2 blocks, +6 us per frame)
+#endif
+__global__ void __launch_bounds__(kThreads, FPVS_K3_MINB) tables_kernel(const Args a) {
   // programmatic launch: everything here reads K2's output.  No early trigger:
   // the first conv's prologue reads the tile masks written here
   pdl_wait();
@@ -620,7 +627,7 @@ extern "C" int fpvs_levels_from_bits(const uint8_t* bits, int B, int Nx, int Ny,
   FPVS_CHECK_LAUNCH("fpvs_levels_from_bits(flags)");
   const int stop = debug_knob("FPVS_LV_STOP");  // profiling builds: launch K1 (1) or K1 + K2 (2) only
   if (stop == 1) return FPVS_OK;
-  cudaError_t e = launch_kernel(lv::compact_levels_kernel, dim3(tb), dim3(lv::kThreads), 0, s, a);
+  cudaError_t e = launch_kernel(lv::compact_levels_kernel, dim3(tb), dim3(lv::kThreads2), 0, s, a);
   if (e != cudaSuccess) return set_error(FPVS_ECUDA, "fpvs_levels_from_bits(compact): %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("fpvs_levels_from_bits(compact)");
   a.reset_only = stop == 2;
