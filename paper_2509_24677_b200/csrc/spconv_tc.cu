@@ -737,11 +737,15 @@ int launch_cfg(const Params& p, cudaStream_t s) {
   return FPVS_OK;
 }
 
+#ifndef FPVS_TC_MINB2_BN
+#define FPVS_TC_MINB2_BN 32  // 32-wide tiles (the chain nets) run two CTAs per SM: config-5 step 692 -> 652 us; wider ones measured slower (U-Net +8 us)
+#endif
 template <int BN>
 int launch(const Params& p, cudaStream_t s) {
   // two K chunks per stage halve the per-stage barrier/commit overhead where
   // the stage still fits >= 4 times in shared memory
-  return launch_cfg<BN, (BN <= 128 ? 2 : 1), 8, 1>(p, s);
+  constexpr bool two = BN <= FPVS_TC_MINB2_BN;
+  return launch_cfg<BN, (two ? 1 : BN <= 128 ? 2 : 1), 8, (two ? 2 : 1)>(p, s);
 }
 
 int dispatch(Params& p, int bn, cudaStream_t s) {
