@@ -273,3 +273,32 @@ def test_dataflow_pairs_equal_grid_wide_waits():
             torch.cuda.synchronize()
             assert torch.equal(eager, outs[-1])
         assert torch.equal(outs[0], outs[2]) and torch.equal(outs[1], outs[2]), dims
+
+
+def test_empty_and_single_cell_frames():
+    """Frames with no active cell (every kernel runs on zero rows: the dataflow
+    pairs wait for nothing, the grid writer writes zeros) and with one active
+    cell run through the captured graph without hanging and give the eager
+    bits."""
+    import torch
+    from paper_2509_24677_b200.pipeline import FramePipeline
+    from paper_2509_24677_b200.unet import PvsUNet
+    dims = (256, 256, 256)
+    one = np.zeros(dims, bool)
+    one[100:102, 50:53, 7] = True
+    pipe = FramePipeline(PvsUNet(seed=1), 1, dims)
+    pipe.load(torch.from_numpy(FroxelGrid.from_dense(synth.config2_grid(1)).bits).cuda())
+    pipe.capture()
+    for occ in (np.zeros(dims, bool), one):
+        bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+        pipe.in_bits.copy_(bits)
+        pipe.out_bits.fill_(0xA5)
+        pipe.run_device()
+        torch.cuda.synchronize()
+        graph_out = pipe.out_bits.clone()
+        eager = torch.full_like(graph_out, 0x5A)
+        pipe.plan.run(bits, eager, 0.5)
+        torch.cuda.synchronize()
+        assert torch.equal(graph_out, eager)
+        if not occ.any():
+            assert int(graph_out.count_nonzero()) == 0
