@@ -305,7 +305,11 @@ class FramePipeline:
 
     # -- streaming: frames in flight on separate compute streams ------------
     # Lane k (k < inflight) is a FramePipeline with its own buffers, CUDA graph
-    # and compute stream (lane 0 is this one); frame i runs on lane i % inflight.
+    # and compute stream; frame i runs on lane i % inflight.  With several
+    # frames in flight the lanes run WITHOUT the level-0 tile dataflow: its
+    # early-resident consumer CTAs wait on SMs another frame would use
+    # (measured 3980 -> 4035 grids/s at 4 in flight); one frame in flight keeps
+    # this pipeline (dataflow on, the lower latency).
     # Uploads and downloads go through two shared copy streams, so frame i's
     # compute overlaps frame i+1's upload, frame i-1's download and, with
     # inflight >= 2, the other lanes' compute: the level-1/2 convs leave SMs
@@ -317,9 +321,14 @@ class FramePipeline:
         torch = _torch()
         if self.graph is None:
             self.capture(tune=False)
-        pipes = [self]
-        for _ in range(1, inflight):
+        if inflight == 1 or not getattr(self.plan, "flow", False):
+            pipes = [self]
+        else:
+            pipes = []
+        while len(pipes) < inflight:
             p = FramePipeline(self.net, self.B, self.grid_dims, self.tau, graph=self._use_graph)
+            if inflight > 1:
+                p.plan.flow = False
             p.in_bits.copy_(self.in_bits)
             p.capture()
             pipes.append(p)
