@@ -150,6 +150,12 @@ class UNetPlan:
                          "enc2a": self.L2, "enc2b": self.L2}
         self.halo_cfg = {}
         self.halo_ws = None
+        # K splits for levels with under a wave of tiles (FPVS_SPLIT=0: none).
+        # Unsplit, the streamed e2e gains 2.6 % (4034 -> 4140 grids/s: no
+        # partial-sum traffic, other frames fill the idle SMs) but one frame
+        # loses 16 us and the fp32 sums change order, so streamed bits would
+        # differ near the threshold from the single-frame path; kept on.
+        self.allow_split = os.environ.get("FPVS_SPLIT", "1") != "0"
         self._halo_builder = None
         self._up_sorter = None  # parity-sorted up tables (FPVS_UPBLOCKS=0 path; FPVS_UPSORT=0 disables)
         self.overlap = True  # side-stream map tables (see build_maps); device_stage_times turns it off
@@ -197,7 +203,7 @@ class UNetPlan:
             # last-wave tail split (-2) of dec0a, costs 4-80 us per frame
             bn = 128 if cout % 128 == 0 else 64
             tiles = max(1, (r + 127) // 128) * (cout // bn)
-            split = 2 if tiles * 2 <= 148 else 1
+            split = 2 if (tiles * 2 <= 148 and self.allow_split) else 1
             if cfg and name in cfg:
                 bn, split = cfg[name]
             self.halo_cfg[name] = (bn, split)
