@@ -21,6 +21,7 @@
 //
 // Everything is sized from device counters: the three launches are
 // graph-capturable and never synchronise.
+#include <cooperative_groups.h>
 #include <type_traits>
 
 #include "common.cuh"
@@ -96,14 +97,10 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // go out in 32-byte runs; coarser levels get a 1 for every parent with an
 // active child (their arrays are cleared by K3 of the previous frame).
 template <int D, int W>
-__global__ void __launch_bounds__(kThreads) l0_flags_kernel(const Args a) {
-  // K2 is launched programmatically: let it take its tile tickets while we run
-  if (threadIdx.x == 0) pdl_trigger();
-  extern __shared__ uint8_t s_flag[];  // [X][kZC + 1]
+__device__ __forceinline__ void l0_flags_body(const Args& a, int blk, uint8_t* s_flag) {  // s_flag: [X][kZC + 1]
   using T = typename std::conditional<W == 4, uint32_t, uint8_t>::type;
   const int X = a.L[0].X, Y = a.L[0].Y, Z = a.L[0].Z;
   const int nzc = (Z + kZC - 1) / kZC;
-  int blk = blockIdx.x;
   const int zc = blk % nzc;
   blk /= nzc;
   const int cy = blk % Y;
@@ -148,6 +145,14 @@ __global__ void __launch_bounds__(kThreads) l0_flags_kernel(const Args a) {
   }
 }
 
+template <int D, int W>
+__global__ void __launch_bounds__(kThreads) l0_flags_kernel(const Args a) {
+  // K2 is launched programmatically: let it take its tile tickets while we run
+  if (threadIdx.x == 0) pdl_trigger();
+  extern __shared__ uint8_t s_flag[];
+  l0_flags_body<D, W>(a, blockIdx.x, s_flag);
+}
+
 // ------------------------------------------------------------------ K2
 // flags of 16 consecutive C-order cells of level l (base linear index r0)
 __device__ __forceinline__ uint32_t level_flags16(const Args& a, int l, int r0, int ncell) {
@@ -165,18 +170,23 @@ __device__ __forceinline__ uint32_t level_flags16(const Args& a, int l, int r0, 
   return f;
 }
 
-__global__ void __launch_bounds__(kThreads2) compact_levels_kernel(const Args a) {
+// pdl: launched programmatically after K1 (false inside the cooperative
+// single-launch build, where a grid barrier orders the phases)
+template <bool PDL>
+__device__ __forceinline__ void compact_body(const Args& a, int blk) {
   __shared__ int s_tile, s_prefix;
   __shared__ int s_warp[kThreads2 / 32];
   int l = 0;
-  while (l + 1 < a.nlev && (int)blockIdx.x >= a.tile_base[l + 1]) ++l;
+  while (l + 1 < a.nlev && blk >= a.tile_base[l + 1]) ++l;
   const LevelDev& L = a.L[l];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // the tile ticket counter was re-armed by K3 of the previous frame (complete
   // before K1 started); the flags below are K1's output: wait for it
   if (tid == 0) s_tile = (int)atomicAdd(L.status + L.ntiles, 1u);
-  pdl_wait();
-  if (tid == 0) pdl_trigger();
+  if constexpr (PDL) {
+    pdl_wait();
+    if (tid == 0) pdl_trigger();
+  }
   __syncthreads();
   const int tile = s_tile;
   const int X = L.X, Y = L.Y, Z = L.Z;
@@ -255,6 +265,8 @@ __global__ void __launch_bounds__(kThreads2) compact_levels_kernel(const Args a)
     }
   }
 }
+
+__global__ void __launch_bounds__(kThreads2) compact_levels_kernel(const Args a) { compact_body<true>(a, blockIdx.x); }
 
 // ------------------------------------------------------------------ K3
 enum Task { T_SUBM = 0, T_DOWN, T_UP, T_GATHER, T_CLEAR, T_RESET, T_COUNT };
@@ -444,10 +456,11 @@ constexpr int kClearChunk = kThreads * 64;  // bytes per clear unit
 #ifndef FPVS_K3_MINB
 #define FPVS_K3_MINB 4  // >= 4 resident blocks per SM (without it ptxas takes 109 registers: 2 blocks, +6 us per frame)
 #endif
-__global__ void __launch_bounds__(kThreads, FPVS_K3_MINB) tables_kernel(const Args a) {
+template <bool PDL>
+__device__ __forceinline__ void tables_body(const Args& a) {
   // programmatic launch: everything here reads K2's output.  No early trigger:
   // the first conv's prologue reads the tile masks written here
-  pdl_wait();
+  if constexpr (PDL) pdl_wait();
   __shared__ uint32_t s_red[kThreads / 32];
   __shared__ __align__(16) int s_tab[kRows * 27];
   __shared__ __align__(16) halob::Smem s_halo;
@@ -515,6 +528,66 @@ __global__ void __launch_bounds__(kThreads, FPVS_K3_MINB) tables_kernel(const Ar
         break;
     }
   }
+}
+
+__global__ void __launch_bounds__(kThreads, FPVS_K3_MINB) tables_kernel(const Args a) { tables_body<true>(a); }
+
+// All three as ONE cooperative launch (grid = every resident block; phases
+// ordered by grid barriers instead of kernel boundaries): K1's units, K2's
+// tiles, then K3's persistent loop.  Co-residency is guaranteed by the
+// cooperative launch, so the barriers cannot deadlock against other work.
+template <int D, int W>
+__global__ void __launch_bounds__(kThreads, FPVS_K3_MINB) maps_fused_kernel(const Args a, int k1_blocks, int k2_blocks) {
+  extern __shared__ uint8_t s_flag[];
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  for (int blk = blockIdx.x; blk < k1_blocks; blk += gridDim.x) {
+    l0_flags_body<D, W>(a, blk, s_flag);
+    __syncthreads();
+  }
+  grid.sync();
+  for (int blk = blockIdx.x; blk < k2_blocks; blk += gridDim.x) {
+    compact_body<false>(a, blk);
+    __syncthreads();
+  }
+  grid.sync();
+  tables_body<false>(a);
+}
+
+// the cooperative single launch measured 8 us SLOWER per frame than the three
+// launches (308 -> 317 us: two grid barriers and a 592-block grid for phases
+// that use 256 and 73 blocks cost more than the launch gaps they remove), so it
+// is off unless FPVS_MAPS_FUSED=1
+#ifndef FPVS_MAPS_FUSED
+#define FPVS_MAPS_FUSED 0
+#endif
+inline bool maps_fused_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FPVS_MAPS_FUSED");  // read once: A/B switch (0 = three launches)
+    return e ? atoi(e) != 0 : FPVS_MAPS_FUSED != 0;
+  }();
+  return on;
+}
+
+template <int D, int W>
+inline cudaError_t launch_fused(const Args& a, int k1_blocks, int k2_blocks, size_t smem1, cudaStream_t s) {
+  static const int per_sm = [smem1] {
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, maps_fused_kernel<D, W>, kThreads, smem1) != cudaSuccess)
+      v = 0;
+    return v;
+  }();
+  if (per_sm < 1) return cudaErrorNotSupported;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kNumSMs * per_sm);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem1;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, maps_fused_kernel<D, W>, a, k1_blocks, k2_blocks);
 }
 
 }  // namespace lv
@@ -614,6 +687,25 @@ extern "C" int fpvs_levels_from_bits(const uint8_t* bits, int B, int Nx, int Ny,
   cudaStream_t s = as_stream(stream);
   const unsigned k1 = (unsigned)((long long)B * Y * ((Z + lv::kZC - 1) / lv::kZC));
   const size_t smem1 = (size_t)X * (lv::kZC + 1);
+  if (lv::maps_fused_enabled() && debug_knob("FPVS_LV_STOP") == 0) {
+    // one cooperative launch for K1 + K2 + K3 (falls through to three
+    // launches when the device cannot hold the whole grid at once)
+    cudaError_t e = cudaErrorNotSupported;
+#define FPVS_KF(D)                                                                              \
+  e = Nx % 32 == 0 ? lv::launch_fused<D, 4>(a, (int)k1, tb, smem1, s) : lv::launch_fused<D, 1>(a, (int)k1, tb, smem1, s);
+    switch (d) {
+      case 1: FPVS_KF(1); break;
+      case 2: FPVS_KF(2); break;
+      case 4: FPVS_KF(4); break;
+      default: FPVS_KF(8); break;
+    }
+#undef FPVS_KF
+    if (e == cudaSuccess) {
+      FPVS_CHECK_LAUNCH("fpvs_levels_from_bits(fused)");
+      return FPVS_OK;
+    }
+    (void)cudaGetLastError();  // a failed cooperative launch leaves no sticky error
+  }
 #define FPVS_K1(D)                                                                      \
   if (Nx % 32 == 0) lv::l0_flags_kernel<D, 4><<<k1, lv::kThreads, smem1, s>>>(a);        \
   else lv::l0_flags_kernel<D, 1><<<k1, lv::kThreads, smem1, s>>>(a);
