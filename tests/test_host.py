@@ -49,6 +49,37 @@ def test_argument_errors_map_to_valueerror():
         _lib.call("fpvs_spconv_tc", 1, 64, 10, None, 27, None, 1, 10, 1, 0, None, 64, 64, 1, 1, 64, 0, None)
 
 
+def test_round2_entry_points_validate_before_launching():
+    """The round-2 entry points reject bad arguments on the host (no GPU)."""
+    p = 256  # a non-null dummy address: never dereferenced, the checks fail first
+    # the grid writer: d must be 4, N_x a multiple of 32
+    with pytest.raises(ValueError, match="d = 4"):
+        _lib.call("fpvs_rowbits_to_grid", p, p, 1, 64, 64, 64, 2, p, None)
+    with pytest.raises(ValueError, match="N_x"):
+        _lib.call("fpvs_rowbits_to_grid", p, p, 1, 48, 64, 64, 4, p, None)
+    with pytest.raises(ValueError, match="null"):
+        _lib.call("fpvs_rowbits_to_grid", None, p, 1, 64, 64, 64, 4, p, None)
+    # column-block up conv: Cout % 32, 8 Cout <= 1024, a child table
+    with pytest.raises(ValueError, match="Cout"):
+        _lib.call("fpvs_spconv_tc_upblocks", p, 64, 10, p, 10, p, 0, p, 64, 48, 1, p, p, 96, 0, None)
+    with pytest.raises(ValueError, match="child_rows"):
+        _lib.call("fpvs_spconv_tc_upblocks", p, 64, 10, p, 10, p, 0, p, 64, 64, 1, None, p, 128, 0, None)
+    # dataflow consumer without settled tables; producer with a K split
+    halo = [p, 64, 10, p, p, p, p, p, p, 10, p, 64, 1, p, 64, 64]
+    with pytest.raises(ValueError, match="SETTLED"):
+        _lib.call("fpvs_spconv_halo_flow", *halo, 1, p, 64, 0, p, 1 << 20, None, p, None)
+    halo_split = halo[:12] + [2] + halo[13:]
+    with pytest.raises(ValueError, match="unsplit"):
+        _lib.call("fpvs_spconv_halo_flow", *halo_split, 1 | _lib.TABLES_SETTLED, p, 64, 0, p, 1 << 20, p, None,
+                  None)
+    # gather-GEMM consumer needs the producer's row count
+    with pytest.raises(ValueError, match="row count"):
+        _lib.call("fpvs_spconv_tc_flow", p, 64, 10, p, 27, p, p, 10, p, 0, p, 64, 64, 1, p, 64, 0, p, None, None)
+    # multi-pack: 1..32 jobs
+    with pytest.raises(ValueError, match="pack jobs"):
+        _lib.call("fpvs_pack_weights_tc_multi", None, 0, None)
+
+
 # -------------------------------------------------------- FPVS boundary format
 
 
