@@ -302,3 +302,35 @@ def test_empty_and_single_cell_frames():
         assert torch.equal(graph_out, eager)
         if not occ.any():
             assert int(graph_out.count_nonzero()) == 0
+
+
+@pytest.mark.slow
+def test_unet_non_cubic_bits_only_frame_matches_oracle():
+    """A non-cubic grid (256 x 128 x 256) through the bits-only frame — the
+    head fused into dec0b, the grid writer, the level-0 dataflow pairs and the
+    column-block up convs all active — against the oracle's bf16 emulation:
+    no mask difference outside the threshold band."""
+    import torch
+    from paper_2509_24677_b200.unet import PvsUNet
+    dims = (256, 128, 256)
+    occ = synth.box_grid(dims, 3000, 1, 12, 9)
+    net = PvsUNet(seed=1, precision="bf16")
+    plan = net.plan(1, dims)
+    bits = torch.from_numpy(FroxelGrid.from_dense(occ).bits).cuda()
+    plan.tune(bits)
+    out = torch.full((occ.size // 8,), 0xA5, dtype=torch.uint8, device="cuda")
+    names = [n for n, _ in plan.stages(bits, out, 0.5)]
+    plan.run(bits, out, 0.5)
+    torch.cuda.synchronize()
+    assert "head" not in names, "expected the fused head at this size"
+    assert plan.flow and plan.halo_cfg["dec0b"] == (64, 1)
+    cells = osp.interleave(occ.astype(np.float64), 4)[None]
+    coords, z = osp.unet_forward(cells, osp.unet_init(1), bf16=True, return_logits=True)
+    assert plan.L0.count() == len(coords)
+    prob = osp.sigmoid(z)
+    dense = osp.deinterleave(osp.scatter_cells(coords, prob, (1,) + plan.L0.dims)[0], 4)
+    got = FroxelGrid(occ.shape, bits=out.cpu().numpy()).to_dense()
+    diff = got != (dense >= 0.5)
+    hard = int((diff & (np.abs(dense - 0.5) >= BAND)).sum())
+    assert hard == 0, (hard, int(diff.sum()))
+    assert int(got.sum()) > 0
