@@ -78,7 +78,15 @@ struct Args {
   unsigned* status_all;
   int status_words;
   int reset_only;  // profiling (FPVS_LV_STOP = 2): K3 runs only the look-back reset
+  int k2_abl;      // profiling builds (FPVS_K2_ABL, wrong results): 1 no look-back, 2 no index_vol
+                   // stores, 4 no coords stores, 8 no flag loads, 16 no ticket atomic
 };
+
+#ifdef FPVS_PROFILE
+#define K2ABL(bit) (a.k2_abl & (bit))
+#else
+#define K2ABL(bit) 0
+#endif
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -182,7 +190,7 @@ __device__ __forceinline__ void compact_body(const Args& a, int blk) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // the tile ticket counter was re-armed by K3 of the previous frame (complete
   // before K1 started); the flags below are K1's output: wait for it
-  if (tid == 0) s_tile = (int)atomicAdd(L.status + L.ntiles, 1u);
+  if (tid == 0) s_tile = K2ABL(16) ? blk - a.tile_base[l] : (int)atomicAdd(L.status + L.ntiles, 1u);
   if constexpr (PDL) {
     pdl_wait();
     if (tid == 0) pdl_trigger();
@@ -192,7 +200,7 @@ __device__ __forceinline__ void compact_body(const Args& a, int blk) {
   const int X = L.X, Y = L.Y, Z = L.Z;
   const int ncell = a.B * X * Y * Z;
   const int r0 = tile * kTileCells + tid * kPer;
-  const uint32_t f = r0 < ncell ? level_flags16(a, l, r0, ncell) : 0u;
+  const uint32_t f = r0 < ncell ? (K2ABL(8) ? 0x1111u : level_flags16(a, l, r0, ncell)) : 0u;
   const int cnt = __popc(f);
   int incl = cnt;
 #pragma unroll
@@ -213,8 +221,8 @@ __device__ __forceinline__ void compact_body(const Args& a, int blk) {
     if (lane < kThreads2 / 32) s_warp[lane] = wi - w;
     const unsigned agg = (unsigned)__shfl_sync(0xffffffffu, wi, 31);
     unsigned prefix = 0;
-    if (tile == 0) {
-      if (lane == 0) st_release(L.status, kFlagPrefix | agg);
+    if (tile == 0 || K2ABL(1)) {
+      if (lane == 0) st_release(L.status + tile, kFlagPrefix | agg);
     } else {
       if (lane == 0) st_release(L.status + tile, kFlagAgg | agg);
       // look back 32 predecessors at a time
@@ -245,14 +253,15 @@ __device__ __forceinline__ void compact_body(const Args& a, int blk) {
     rows[i] = (on && rank < L.cap) ? rank : -1;
     rank += on ? 1 : 0;
   }
-  if (r0 + kPer <= ncell) {
+  if (K2ABL(2)) {
+  } else if (r0 + kPer <= ncell) {
     int4* dst = reinterpret_cast<int4*>(L.index_vol + r0);
 #pragma unroll
     for (int q = 0; q < 4; ++q) dst[q] = make_int4(rows[4 * q], rows[4 * q + 1], rows[4 * q + 2], rows[4 * q + 3]);
   } else {
     for (int i = 0; i < kPer && r0 + i < ncell; ++i) L.index_vol[r0 + i] = rows[i];
   }
-  if (f) {
+  if (f && !K2ABL(4)) {
     int r = r0;
     int z = r % Z; r /= Z;
     int y = r % Y; r /= Y;
@@ -719,6 +728,7 @@ extern "C" int fpvs_levels_from_bits(const uint8_t* bits, int B, int Nx, int Ny,
   FPVS_CHECK_LAUNCH("fpvs_levels_from_bits(flags)");
   const int stop = debug_knob("FPVS_LV_STOP");  // profiling builds: launch K1 (1) or K1 + K2 (2) only
   if (stop == 1) return FPVS_OK;
+  a.k2_abl = debug_knob("FPVS_K2_ABL");
   cudaError_t e = launch_kernel(lv::compact_levels_kernel, dim3(tb), dim3(lv::kThreads2), 0, s, a);
   if (e != cudaSuccess) return set_error(FPVS_ECUDA, "fpvs_levels_from_bits(compact): %s", cudaGetErrorString(e));
   FPVS_CHECK_LAUNCH("fpvs_levels_from_bits(compact)");
