@@ -346,6 +346,24 @@ int fpvs_spconv_halo_flow(const void* x, int ldx, int x_rows, const int32_t* nbr
                           void* ws, size_t ws_bytes, int32_t* tile_done_out, const int32_t* tile_done_in,
                           void* stream);
 
+/* Submanifold 3x3x3 conv over DENSE BRICKS of 1 x 16 x 8 cells of a level
+ * (B x X x Y x Z cells, C order; index_vol[cell] = the cell's row of x or -1),
+ * for well-filled levels: every brick is an M = 128 tile whose 27 tap
+ * operands are shifted views of one dense halo brick in shared memory
+ * (tcgen05 SS MMAs, no gather builders).  Computes the same rows as
+ * fpvs_spconv_halo (reference Conv3d.forward, neural.py:187-219, on the
+ * active set): y[row] for every active cell; inactive cells read as zero and
+ * are not written.  w_packed: fpvs_pack_weights_tc image (K = 27, bn).
+ * split (dividing Cin / 64) cuts the channel chunks over CTAs with fp32
+ * partials in ws (fpvs_spconv_brick_workspace_size bytes, zeroed once; the
+ * kernel leaves its counters zero); split = 1 needs no workspace.  act may
+ * carry FPVS_TABLES_SETTLED (index_vol written two or more launches back:
+ * its lookups start before the programmatic-launch wait). */
+size_t fpvs_spconv_brick_workspace_size(int B, int X, int Y, int Z, int cout, int bn, int split);
+int fpvs_spconv_brick(const void* x, int ldx, int x_rows, const int32_t* index_vol, int B, int X, int Y, int Z,
+                      const void* w_packed, int bn, int split, const float* bias, int cin, int cout, int act,
+                      void* y, int ldy, int col_off, void* ws, size_t ws_bytes, void* stream);
+
 /* The U-Net's last level-0 conv (Cout = 64, relu) with the 1x1x1 head fused
  * into its epilogue (d = 4): each tile's bf16 activations become the A
  * operand of the head's tcgen05 MMAs in tensor memory, and active row r's

@@ -57,6 +57,9 @@ SIGNATURES = {
                                    _p]),
     "fpvs_spconv_halo_flow": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _i, _i, _p, _i, _i, _i, _p, _i, _i, _p,
                                    _z, _p, _p, _p]),
+    "fpvs_spconv_brick_workspace_size": (_z, [_i, _i, _i, _i, _i, _i, _i]),
+    "fpvs_spconv_brick": (_i, [_p, _i, _i, _p, _i, _i, _i, _i, _p, _i, _i, _p, _i, _i, _i, _p, _i, _i, _p, _z,
+                               _p]),
     "fpvs_rowbits_to_grid": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p]),
     "fpvs_pack_weights_tc_dgrad": (_i, [_p, _i, _i, _i, _i, _p, _p]),
     "fpvs_pack_weights_tc_multi": (_i, [_p, _i, _p]),

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfpvs.so")
 PROFILE_LIB = os.path.join(HERE, "libfpvs_prof.so")  # -DFPVS_PROFILE: timestamps + ablation knobs (tools/ only)
-SOURCES = ["capi.cu", "interleave.cu", "kmap.cu", "kmap_pairs.cu", "levels.cu", "spconv_simt.cu", "spconv_tc.cu", "spconv_halo.cu", "upsort.cu", "wgrad_tc.cu", "wgrad_halo.cu", "optim.cu", "froxelize.cu"]
+SOURCES = ["capi.cu", "interleave.cu", "kmap.cu", "kmap_pairs.cu", "levels.cu", "spconv_simt.cu", "spconv_tc.cu", "spconv_halo.cu", "spconv_brick.cu", "upsort.cu", "wgrad_tc.cu", "wgrad_halo.cu", "optim.cu", "froxelize.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-diag-suppress", "177"]

@@ -26,4 +26,4 @@ bool pdl_enabled() {
 }  // namespace fpvs
 
 extern "C" const char* fpvs_last_error(void) { return fpvs::g_err; }
-extern "C" int fpvs_abi_version(void) { return 3; }  // 2: f64 interleave, double tau, exchange, k^3 maps; 3: row-bits head
+extern "C" int fpvs_abi_version(void) { return 4; }  // 2: f64 interleave, double tau, exchange, k^3 maps; 3: row-bits head; 4: brick conv

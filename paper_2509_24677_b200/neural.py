@@ -505,10 +505,18 @@ def halo_ok(K: int, cin: int, cout: int, dtype=None) -> bool:
     return K == 27 and (cin % 64 == 0 or cin == 32) and cout % 32 == 0 and cout <= 1024
 
 
+def brick_ok(K: int, cin: int, cout: int, dtype=None) -> bool:
+    """Shapes the dense-brick conv takes (fpvs_spconv_brick)."""
+    torch = _torch()
+    if dtype is not None and dtype != torch.bfloat16:
+        return False
+    return K == 27 and cin % 64 == 0 and cout % 64 == 0 and cout <= 1024
+
+
 def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int, col_off: int = 0,
              precision: str = "fp32", act: str | None = None, stream=None, bn: int = 0, masks=None,
              halo=None, halo_tabs=None, out_rows=None, settled: bool = False, done_out=None, done_in=None,
-             done_n=None):
+             done_n=None, brick=None):
     """One sparse conv launch: y[:, col_off:col_off+Cout] = act(gather-GEMM(x, table) + b).
 
     ``masks`` are the table's per-tile offset masks (sparse.tile_masks); the
@@ -522,7 +530,9 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
     FPVS_TABLES_SETTLED).  ``done_out`` / ``done_in``: per-tile dataflow flags
     between two halo convs of one level (fpvs_spconv_halo_flow); the plain
     gather-GEMM takes ``done_in`` with ``done_n``, the producer level's row
-    count (fpvs_spconv_tc_flow).
+    count (fpvs_spconv_tc_flow).  ``brick`` = (bn, split, workspace, level):
+    the dense-brick kernel for a well-filled level (fpvs_spconv_brick; reads
+    the level's index volume instead of ``table``).
     """
     torch = _torch()
     spec = layer.spec
@@ -534,6 +544,14 @@ def run_conv(layer: Conv3d, x, ldx: int, table, K: int, n, cap: int, y, ldy: int
     if precision == "bf16":
         if table is not None and masks is None:
             masks = sp.tile_masks(table, K, n, cap, stream=stream)
+        if brick is not None and brick_ok(K, spec.in_channels, spec.out_channels, x.dtype):
+            bbn, bsplit, ws, lv = brick
+            X, Y, Z = lv.dims
+            _lib.call("fpvs_spconv_brick", _lib.ptr(x), ldx, x.shape[0], _lib.ptr(lv.index_vol), lv.B, X, Y, Z,
+                      _lib.ptr(layer.packed(bbn, stream)), bbn, bsplit, _lib.ptr(layer.b), spec.in_channels,
+                      spec.out_channels, a | (_lib.TABLES_SETTLED if settled else 0), _lib.ptr(y), ldy, col_off, _lib.ptr(ws), 0 if ws is None else ws.numel(),
+                      s)
+            return
         if halo is not None and halo_ok(K, spec.in_channels, spec.out_channels, x.dtype):
             hbn, split, ws = halo
             args = [_lib.ptr(x), ldx, x.shape[0], _lib.ptr(table), _lib.ptr(halo_tabs["lnbr"]),

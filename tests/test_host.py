@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
         assert hasattr(lib, name), name
     assert set(names) == set(_lib.SIGNATURES), "ctypes table out of sync with include/fpvs.h"
     lib = _lib.load()
-    assert lib.fpvs_abi_version() == 3
+    assert lib.fpvs_abi_version() == 4
     # size queries are pure host arithmetic
     assert _lib.size("fpvs_pack_weights_tc_size", 27, 64, 64, 0) == 27 * 64 * 128
     assert _lib.size("fpvs_pack_weights_tc_size", 27, 8, 32, 0) == 4 * 32 * 128
