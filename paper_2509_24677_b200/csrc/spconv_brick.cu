@@ -86,6 +86,7 @@ struct Params {
   int* counters;         // [items], zero between launches
   int settled;           // index_vol is two or more launches old: read before the PDL wait
   int abl;               // profiling builds (FPVS_BRICK_ABL, wrong results): 1 weights only for the first stages
+  int slot;              // profiling builds: timestamp slot of this launch
 };
 
 struct Unit {
@@ -124,15 +125,16 @@ __device__ __forceinline__ uint64_t sw128_desc_sbo(uint32_t saddr, uint32_t sbo)
 // first halo landed, first MMA issued, last MMA committed, epilogue start /
 // end of its last unit) — tools/brick_timeline.py
 #ifdef FPVS_PROFILE
-__device__ unsigned long long g_bts[160][8];
-__device__ long long g_bclk[160][8];
+__device__ unsigned long long g_bts[2][160][8];  // [launch slot][CTA][event]
+__device__ long long g_bclk[2][160][8];
+static int g_bslot = 0;  // host: launch counter (slot = parity, so two consecutive launches keep their stamps)
 #define BTS(i)                                                                      \
   do {                                                                              \
     if (blockIdx.x < 160) {                                                         \
       unsigned long long t_;                                                        \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
-      g_bts[blockIdx.x][i] = t_;                                                    \
-      g_bclk[blockIdx.x][i] = clock64();                                            \
+      g_bts[p.slot][blockIdx.x][i] = t_;                                            \
+      g_bclk[p.slot][blockIdx.x][i] = clock64();                                    \
     }                                                                               \
   } while (0)
 #else
@@ -247,7 +249,6 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_brick_kernel(const Params p
   // map build's, read before the wait only when the caller says it is two or
   // more launches old (FPVS_TABLES_SETTLED)
   if (!p.settled) pdl_wait();
-  if (tid == 0) BTS(1);
 
   if (warp < 4 || warp == 6 || warp == 7) {
     // ===================== halo-brick loaders =====================
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(THREADS, 1) spconv_brick_kernel(const Params p
     }
     pdl_wait();
     if (lt == 0) pdl_trigger();
+    if (lt == 0) BTS(1);
     uint32_t gc = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       Unit U;
@@ -570,12 +572,13 @@ inline bool cluster_enabled() {
 using namespace fpvs;
 
 #ifdef FPVS_PROFILE
-extern "C" int fpvs_debug_brick_times(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, brick::g_bts, sizeof(unsigned long long) * 160 * 8) == cudaSuccess ? 0 : 3;
+extern "C" int fpvs_debug_brick_times(unsigned long long* host) {  // [2][160][8]
+  return cudaMemcpyFromSymbol(host, brick::g_bts, sizeof(unsigned long long) * 2 * 160 * 8) == cudaSuccess ? 0 : 3;
 }
 extern "C" int fpvs_debug_brick_clocks(long long* host) {
-  return cudaMemcpyFromSymbol(host, brick::g_bclk, sizeof(long long) * 160 * 8) == cudaSuccess ? 0 : 3;
+  return cudaMemcpyFromSymbol(host, brick::g_bclk, sizeof(long long) * 2 * 160 * 8) == cudaSuccess ? 0 : 3;
 }
+extern "C" void fpvs_debug_brick_reset_slot(void) { brick::g_bslot = 0; }
 #endif
 
 extern "C" size_t fpvs_spconv_brick_workspace_size(int B, int X, int Y, int Z, int cout, int bn, int split) {
@@ -629,6 +632,9 @@ extern "C" int fpvs_spconv_brick(const void* x, int ldx, int x_rows, const int32
   const long long items = (long long)B * X * p.nby * p.nbz * p.nblk;
   p.settled = settled;
   p.abl = debug_knob("FPVS_BRICK_ABL");
+#ifdef FPVS_PROFILE
+  p.slot = brick::g_bslot++ & 1;
+#endif
   p.counters = (int*)ws;
   p.part = ws ? (float*)((uint8_t*)ws + brick::align256((size_t)items * 4)) : nullptr;
   const long long units = items * split;

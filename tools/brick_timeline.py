@@ -31,13 +31,14 @@ stages = dict(plan.stages(bits, out, 0.5))
 name = os.environ.get("LAYER", "enc2a")
 print("brick cfg", plan.brick_of.get(name))
 lib = _lib.load()
-buf = (ctypes.c_ulonglong * (160 * 8))()
+buf = (ctypes.c_ulonglong * (2 * 160 * 8))()
 if os.environ.get("INFRAME"):
     # the frame's stages up to LAYER as one graph after an L2 flush (the
     # layer's real predecessors, programmatic launches and cache state)
     from paper_2509_24677_b200.pipeline import no_gc
     order = [n for n, _ in plan.stages(bits, out, 0.5)]
     pre = order[:order.index(name) + 1]
+    lib.fpvs_debug_brick_reset_slot()
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
@@ -58,10 +59,23 @@ else:
         stages[name]()
         torch.cuda.synchronize()
 lib.fpvs_debug_brick_times(buf)
-clk = (ctypes.c_longlong * (160 * 8))()
+clk = (ctypes.c_longlong * (2 * 160 * 8))()
 lib.fpvs_debug_brick_clocks(clk)
-ck = np.frombuffer(clk, dtype=np.int64).reshape(160, 8)
-t = np.frombuffer(buf, dtype=np.uint64).reshape(160, 8).astype(np.int64)
+# in-frame: the brick launches of the captured prefix alternate slots 0, 1 (capture order);
+# SLOT picks one (default: the last brick launch of the prefix)
+allt = np.frombuffer(buf, dtype=np.uint64).reshape(2, 160, 8).astype(np.int64)
+allc = np.frombuffer(clk, dtype=np.int64).reshape(2, 160, 8)
+slot = int(os.environ.get("SLOT", "-1"))
+if slot < 0:
+    slot = int(np.argmax([allt[k, :, 0].max() for k in (0, 1)]))
+t, ck = allt[slot], allc[slot]
+if (allt[0, :, 0] > 0).any() and (allt[1, :, 0] > 0).any():
+    a, b = (allt[0], allt[1]) if allt[0, :, 0].max() < allt[1, :, 0].max() else (allt[1], allt[0])
+    a, b = a[a[:, 0] > 0], b[b[:, 0] > 0]
+    print("two launches: first ends (last epilogue) %.2f us before the second's first CTA start; "
+          "second's data wait ends %.2f us after the first's end; second's first MMA %.2f us after" % (
+              (b[:, 0].min() - a[:, 6].max()) / -1e3, (np.median(b[:, 1]) - a[:, 6].max()) / 1e3,
+              (np.median(b[:, 3]) - a[:, 6].max()) / 1e3))
 ok = t[:, 0] > 0
 t = t[ok]
 ck = ck[ok]
@@ -73,7 +87,7 @@ mma = (ck[:, 4] - ck[:, 3]).astype(np.float64)
 print("MMA phase: %.0f SM cycles (median) over %.2f us -> %.0f MHz" % (
     np.median(mma), np.median(t[:, 4] - t[:, 3]) / 1e3, np.median(mma / ((t[:, 4] - t[:, 3]) / 1e3))))
 t0 = t[:, 0].min()
-labels = ["start", "pdl", "halo0", "mma0", "commit", "epi0", "epi1", "chunk0"]
+labels = ["start", "data", "halo0", "mma0", "commit", "epi0", "epi1", "chunk0"]
 print("CTAs", len(t), "| kernel span (first start -> last epilogue end) %.2f us" % ((t[:, 6].max() - t0) / 1e3))
 for i, lab in enumerate(labels):
     v = (t[:, i] - t0) / 1e3
