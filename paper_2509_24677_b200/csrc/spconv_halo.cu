@@ -115,6 +115,7 @@ struct Params {
   float* part;    // [tiles][nblk][split][128][BN] fp32 partials (split > 1)
   int* counters;  // [tiles][nblk] arrival counters, zero between launches
   int dbg;        // profiling builds: FPVS_HALO_DEBUG (timestamps)
+  int hslot;      // profiling builds: per-CTA span slot of this launch
   int abl;        // profiling builds: FPVS_HALO_ABL (ablations)
   int settled;    // tables / tile masks are two or more launches old: decode units before the PDL wait
   // tile-level dataflow between two convs of one level (fpvs_spconv_halo_flow):
@@ -141,7 +142,9 @@ struct Params {
 // tcgen05.st, 19 loaders skip the halo row copies, 20 no MMAs.
 #ifdef FPVS_PROFILE
 __device__ unsigned long long g_hts[2][8192];   // CTAs (dbg >> 8) and (dbg >> 8) + 1
-__device__ unsigned long long g_hcta[2][160];  // per-CTA start / end
+constexpr int kSpanSlots = 32;
+__device__ unsigned long long g_hcta[kSpanSlots][3][160];  // [launch slot][start / end / loaders' wait done][CTA]
+static int g_hslot = 0;                                    // host: halo launch counter (slot = count mod 32)
 __device__ unsigned g_hsm[160];
 __device__ long long g_hclk[2][160];
 #define HTS(slot)                                                                        \
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
     unsigned sm_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));
-    g_hcta[0][blockIdx.x] = t_;
+    g_hcta[p.hslot][0][blockIdx.x] = t_;
     g_hsm[blockIdx.x] = sm_;
     g_hclk[0][blockIdx.x] = clock64();
   }
@@ -676,6 +679,13 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
         if (tid == W_LOAD * 32) pdl_trigger();
       }
     }
+#ifdef FPVS_PROFILE
+    if (p.dbg && tid == W_LOAD * 32 && blockIdx.x < 160) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      g_hcta[p.hslot][2][blockIdx.x] = t_;
+    }
+#endif
     uint32_t gc = 0;
     int dep_mt = -1;  // dataflow: the tile whose producer tiles were last waited for
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -1002,7 +1012,7 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
   if (p.dbg && tid == 0 && blockIdx.x < 160) {
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-    g_hcta[1][blockIdx.x] = t_;
+    g_hcta[p.hslot][1][blockIdx.x] = t_;
     g_hclk[1][blockIdx.x] = clock64();
   }
 #endif
@@ -1057,9 +1067,18 @@ extern "C" int fpvs_debug_halo_timestamps(unsigned long long* host, int n) {
   if (n > 2 * 8192) n = 2 * 8192;
   return cudaMemcpyFromSymbol(host, halo::g_hts, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 3;
 }
-extern "C" int fpvs_debug_halo_cta_times(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, halo::g_hcta, sizeof(unsigned long long) * 320) == cudaSuccess ? 0 : 3;
+extern "C" int fpvs_debug_halo_cta_times(unsigned long long* host) {  // [32][3][160]
+  return cudaMemcpyFromSymbol(host, halo::g_hcta, sizeof(halo::g_hcta)) == cudaSuccess ? 0 : 3;
 }
+// resets the launch counter (returns the launches counted since the last reset) and clears the spans
+extern "C" int fpvs_debug_halo_reset_slot(void) {
+  const int n = halo::g_hslot;
+  halo::g_hslot = 0;
+  static const unsigned long long zeros[halo::kSpanSlots * 3 * 160] = {};
+  cudaMemcpyToSymbol(halo::g_hcta, zeros, sizeof(zeros));
+  return n;
+}
+extern "C" int fpvs_debug_halo_slot_count(void) { return halo::g_hslot; }
 extern "C" int fpvs_debug_halo_clk(long long* host) {
   return cudaMemcpyFromSymbol(host, halo::g_hclk, sizeof(long long) * 320) == cudaSuccess ? 0 : 3;
 }
@@ -1171,6 +1190,9 @@ static int halo_conv(const void* x, int ldx, int x_rows, const int32_t* nbr, con
   p.counters = (int*)ws;
   p.part = (float*)((uint8_t*)ws + halo::align256(items * 4));
   p.dbg = debug_knob("FPVS_HALO_DEBUG");
+#ifdef FPVS_PROFILE
+  p.hslot = halo::g_hslot++ % halo::kSpanSlots;
+#endif
   p.abl = debug_knob("FPVS_HALO_ABL");
   p.settled = settled;
   if (done_out || done_in) {

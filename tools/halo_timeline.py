@@ -38,10 +38,11 @@ for name in os.environ.get("LAYERS", "enc0b,enc1a,enc2a").split(","):
         stages[name]()
         torch.cuda.synchronize()
     lib.fpvs_debug_halo_timestamps(buf, 2 * 8192)
-    cta = (ctypes.c_ulonglong * 320)()
+    cta = (ctypes.c_ulonglong * (32 * 3 * 160))()
     if hasattr(lib, "fpvs_debug_halo_cta_times"):
         lib.fpvs_debug_halo_cta_times(cta)
-    ca = np.frombuffer(cta, dtype=np.uint64).astype(np.int64).reshape(2, 160)
+    spans = np.frombuffer(cta, dtype=np.uint64).astype(np.int64).reshape(32, 3, 160)
+    ca = spans[int(np.argmax(spans[:, 0].max(axis=1)))]  # the latest launch's slot
     ok = (ca[0] > 0) & (ca[1] > ca[0])
     st_, en_ = ca[0][ok], ca[1][ok]
     if len(st_):
