@@ -78,6 +78,23 @@ def test_round2_entry_points_validate_before_launching():
     # multi-pack: 1..32 jobs
     with pytest.raises(ValueError, match="pack jobs"):
         _lib.call("fpvs_pack_weights_tc_multi", None, 0, None)
+    # dense-brick conv: tile width, Cin % 64, a split dividing Cin / 64, the workspace of a split
+    brick = [p, 128, 10, p, 1, 16, 16, 16, p]
+    with pytest.raises(ValueError, match="tile width"):
+        _lib.call("fpvs_spconv_brick", *brick, 96, 1, p, 128, 192, 1, p, 192, 0, None, 0, None)
+    with pytest.raises(ValueError, match="Cin"):
+        _lib.call("fpvs_spconv_brick", p, 96, 10, p, 1, 16, 16, 16, p, 128, 1, p, 96, 128, 1, p, 128, 0, None, 0,
+                  None)
+    with pytest.raises(ValueError, match="split"):
+        _lib.call("fpvs_spconv_brick", *brick, 128, 3, p, 128, 128, 1, p, 128, 0, p, 1 << 30, None)
+    with pytest.raises(ValueError, match="workspace"):
+        _lib.call("fpvs_spconv_brick", *brick, 128, 2, p, 128, 128, 1, p, 128, 0, p, 16, None)
+    with pytest.raises(ValueError, match="null"):
+        _lib.call("fpvs_spconv_brick", None, 128, 10, p, 1, 16, 16, 16, p, 128, 1, p, 128, 128, 1, p, 128, 0, None,
+                  0, None)
+    assert _lib.size("fpvs_spconv_brick_workspace_size", 1, 16, 16, 16, 256, 128, 2) == \
+        256 + 32 * 2 * 2 * 128 * 128 * 4  # 32 bricks x 2 column blocks: counters, then 2 partials each
+    assert _lib.size("fpvs_spconv_brick_workspace_size", 1, 16, 16, 16, 256, 96, 1) == 0
 
 
 # -------------------------------------------------------- FPVS boundary format
