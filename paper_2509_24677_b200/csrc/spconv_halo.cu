@@ -197,6 +197,9 @@ struct Unit {
   uint32_t mask;
 };
 
+#ifndef FPVS_HALO_NS128
+#define FPVS_HALO_NS128 4  // stages at BN 128 (one chunk each; tools/build_variant.py A/B)
+#endif
 template <int BN, int NBG = 2, int MINB = 1>
 struct Cfg {
   // chunks per stage: BN 64 runs 4 chunks (16 MMAs) per stage and commit, two
@@ -210,7 +213,7 @@ struct Cfg {
   static constexpr int G = BN == 64 ? (MINB == 2 ? 2 : 4) : BN < 64 ? 2 : W2 ? 2 : 1;
   static constexpr int NACC = BN == 256 ? 1 : 2;
   static constexpr int NHB = BN == 256 || MINB == 2 ? 1 : 2;
-  static constexpr int NS = BN == 64 || W2 ? 2 : 4;
+  static constexpr int NS = BN == 64 || W2 ? 2 : BN == 128 ? FPVS_HALO_NS128 : 4;
   static constexpr int TMEM_COLS = MINB == 2 ? 256 : 512;
   static constexpr int BIAS_N = MINB == 2 ? 128 : 1024;  // floats (MINB 2: Cout <= 128, no head)
   static constexpr int B_SUB = BN * 128;
