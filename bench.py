@@ -821,9 +821,11 @@ def run_ours(args):
     hbm_peak, tf_peak, peak_kind = peaks()
     tc_ms = sum(conv_ms.values())
     tc_flops = sum(layer_flops[k] for k in conv_ms)
-    achieved = tc_flops / (tc_ms * 1e-3) / 1e12
+    # (a stage can difference to 0 when timed under a profiler: no rate then)
+    achieved = tc_flops / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else None
     n_tc_launches = len(conv_ms)
-    per_layer = {k: {"ms": round(conv_ms[k], 5), "tflops": round(layer_flops[k] / (conv_ms[k] * 1e-3) / 1e12, 2)}
+    per_layer = {k: {"ms": round(conv_ms[k], 5),
+                     "tflops": round(layer_flops[k] / (conv_ms[k] * 1e-3) / 1e12, 2) if conv_ms[k] > 0 else None}
                  for k in conv_ms}
     stage_ms = {k: round(v, 5) for k, v in stage_dev.items()}
     traffic = None
@@ -867,10 +869,11 @@ def run_ours(args):
                 "latency_ms": latency},
         "roofline": {"bound": "tensor",
                      "kernel": "tcgen05 sparse conv: spconv_halo (10 subm convs, halo-cached, A in TMEM; the 1x1x1 "
-                               "head fused into dec0b's epilogue) + spconv_tc (2 down + 2 parity-sorted up gather-GEMMs) "
+                               "head fused into dec0b's epilogue) + spconv_tc (2 down gather-GEMMs + 2 column-block up GEMMs) "
                                "per frame",
                      "head_fused": head_fused,
-                     "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s", "frac": achieved / tf_peak,
+                     "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s",
+                     "frac": achieved / tf_peak if achieved is not None else None,
                      "peak_kind": f"{peak_kind} bf16 burst", "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch (mean over the 14 conv launches, ncu --set full)",
                      "flops_per_frame": tc_flops, "launches_per_frame": n_tc_launches,
