@@ -382,12 +382,29 @@ int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const int32_t* nbr
                           float tau, uint64_t* row_bits, int flags, const int32_t* tile_done_in,
                           void* stream);
 
+/* fpvs_spconv_halo_head that also publishes tile_done_out[t] = 4 once the
+ * row masks of 128-row tile t are stored (as fpvs_spconv_halo_flow's
+ * producer side; zeroed by the launch itself), for
+ * fpvs_rowbits_to_grid_flow. */
+int fpvs_spconv_halo_head_flow(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
+                               const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
+                               const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin,
+                               void* ws, size_t ws_bytes, const void* head_w_packed, const float* head_bias,
+                               float tau, uint64_t* row_bits, int flags, const int32_t* tile_done_in,
+                               int32_t* tile_done_out, void* stream);
+
 /* Per-row 64-bit cell masks (fpvs_spconv_halo_head) -> the packed froxel grid
  * B x Nx x Ny x Nz (FPVS bit order, d = 4, N_x % 32 == 0): every 32-bit word
  * of out_bits is written exactly once (no clear needed); cells whose
  * level-0 index_vol entry is -1 are 0. */
 int fpvs_rowbits_to_grid(const uint64_t* row_bits, const int32_t* index_vol, int B, int Nx, int Ny, int Nz, int d,
                          uint8_t* out_bits, void* stream);
+/* The same grid as a dataflow consumer of fpvs_spconv_halo_head_flow launched
+ * immediately before: each block (an 8-cell x octet of one cell row) waits
+ * only for the done flags of the tiles holding its cells' rows (N_z <= 1024).
+ * index_vol must be two or more launches old. */
+int fpvs_rowbits_to_grid_flow(const uint64_t* row_bits, const int32_t* index_vol, int B, int Nx, int Ny, int Nz,
+                              int d, uint8_t* out_bits, const int32_t* tile_done_in, void* stream);
 
 /* Fused head (replaces the final Conv3d + sigmoid + deinterleave(tau),
  * neural.py:513-526): 1x1x1 conv Cin -> d^3, sigmoid, [p >= tau], packed-bit

@@ -61,6 +61,9 @@ SIGNATURES = {
     "fpvs_spconv_brick": (_i, [_p, _i, _i, _p, _i, _i, _i, _i, _p, _i, _i, _p, _i, _i, _i, _p, _i, _i, _p, _z,
                                _p]),
     "fpvs_rowbits_to_grid": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p]),
+    "fpvs_rowbits_to_grid_flow": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _p]),
+    "fpvs_spconv_halo_head_flow": (_i, [_p, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _p, _z, _p, _p, _f, _p, _i,
+                                        _p, _p, _p]),
     "fpvs_pack_weights_tc_dgrad": (_i, [_p, _i, _i, _i, _i, _p, _p]),
     "fpvs_pack_weights_tc_multi": (_i, [_p, _i, _p]),
     "fpvs_spconv_tc_dgrad": (_i, [_p, _i, _i, _p, _i, _p, _p, _i, _p, _i, _i, _i, _p, _i, _p, _i, _p]),

@@ -895,10 +895,11 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(tempty + acc));
-        if (p.done_out) {
+        if (p.done_out && !fuse_head) {
           // dataflow producer: each epilogue warp publishes its 32 rows with a
           // release add once they are stored (__syncwarp orders the lanes'
           // stores before lane 0's cumulative release); 4 = the tile is done
+          // (with the fused head: once its row masks are stored, below)
           __syncwarp();
           if (lane == 0) red_add_release_gpu(p.done_out + U.mt, 1);
         }
@@ -938,6 +939,10 @@ __global__ void __launch_bounds__(Roles<NBG>::THREADS, MINB) spconv_halo_kernel(
                 rb |= (unsigned long long)(v[i] + s_bias[512 + cb + i] >= p.zt ? 1u : 0u) << (cb + i);
             }
             if (valid && !ABL(21)) p.row_bits[row] = rb;
+            if (p.done_out) {  // the grid writer's dataflow: this warp's row masks are stored
+              __syncwarp();
+              if (lane == 0) red_add_release_gpu(p.done_out + U.mt, 1);
+            }
             tc_fence_before();  // the next tile's head A store / MMA come after these reads
             named_bar(3, 128);
           }
@@ -1267,6 +1272,19 @@ extern "C" int fpvs_spconv_halo_flow(const void* x, int ldx, int x_rows, const i
                    cout, act, y, ldy, col_off, ws, ws_bytes, stream, nullptr, tile_done_out, tile_done_in);
 }
 
+extern "C" int fpvs_spconv_halo_head_flow(const void* x, int ldx, int x_rows, const int32_t* nbr,
+                                          const int16_t* lnbr, const int32_t* halo_rows, const int32_t* halo_n,
+                                          const uint32_t* tile_masks, const int32_t* n_dev, int cap,
+                                          const void* w_packed, const float* bias, int cin, void* ws, size_t ws_bytes,
+                                          const void* head_w_packed, const float* head_bias, float tau,
+                                          uint64_t* row_bits, int flags, const int32_t* done_in, int32_t* done_out,
+                                          void* stream) {
+  const HeadArgs h{head_w_packed, head_bias, tau, reinterpret_cast<unsigned long long*>(row_bits)};
+  return halo_conv(x, ldx, x_rows, nbr, lnbr, halo_rows, halo_n, tile_masks, n_dev, cap, w_packed, 64, 1, bias, cin, 64,
+                   FPVS_ACT_RELU | (flags & FPVS_TABLES_SETTLED), row_bits, 64, 0, ws, ws_bytes, stream, &h, done_out,
+                   done_in);
+}
+
 extern "C" int fpvs_spconv_halo_head(const void* x, int ldx, int x_rows, const int32_t* nbr, const int16_t* lnbr,
                                      const int32_t* halo_rows, const int32_t* halo_n, const uint32_t* tile_masks,
                                      const int32_t* n_dev, int cap, const void* w_packed, const float* bias, int cin,
@@ -1364,8 +1382,95 @@ __global__ void __launch_bounds__(128) rowbits_grid_kernel(const RowBitsArgs a) 
       }
   }
 }
+// The grid writer as a dataflow consumer of the fused-head conv: block =
+// (b, x octet w = the 8 cells of one 32-froxel word column, cell row cy),
+// all z; its cells' rows lie in 8 consecutive x slabs, i.e. a contiguous
+// range of 128-row tiles, so it waits (acquire polling) only for those
+// tiles' done flags instead of the whole conv grid, and the blocks of the
+// low x octets run in the conv's last wave.  Words are the plain writer's.
+constexpr int kFlowMaxZ = 256;  // cells along z per block (Nz <= 1024)
+__global__ void __launch_bounds__(256) rowbits_grid_flow_kernel(const RowBitsArgs a, const int* done_in) {
+  __shared__ unsigned long long s_rb[8][kFlowMaxZ];
+  __shared__ int s_lo, s_hi;
+  const int nw = a.X / 8;
+  int blk = blockIdx.x;
+  const int w = blk % nw;
+  blk /= nw;
+  const int cy = blk % a.Y, b = blk / a.Y;
+  if (threadIdx.x == 0) {
+    s_lo = INT_MAX;
+    s_hi = -1;
+  }
+  __syncthreads();
+  // the cells' rows (the map build's index volume: two or more launches old)
+  int lo = INT_MAX, hi = -1;
+  for (int c = threadIdx.x; c < 8 * a.Z; c += blockDim.x) {
+    const int i = c / a.Z, cz = c - i * a.Z;
+    const int r = __ldg(a.index_vol + (((long long)b * a.X + 8 * w + i) * a.Y + cy) * a.Z + cz);
+    s_rb[i][cz] = (unsigned long long)(long long)r;  // row index for now
+    if (r >= 0) {
+      lo = min(lo, r);
+      hi = max(hi, r);
+    }
+  }
+  if (lo <= hi) {
+    atomicMin(&s_lo, lo);
+    atomicMax(&s_hi, hi);
+  }
+  __syncthreads();
+  // wait for the producer tiles holding those rows (bounded spin: a producer
+  // that never finishes fails the launch instead of hanging it)
+  if (s_hi >= 0)
+    for (int t = s_lo / 128 + (int)threadIdx.x; t <= s_hi / 128; t += blockDim.x) {
+      long long spins = 0;
+      while (ld_acquire_gpu(done_in + t) < 4) {
+        __nanosleep(32);
+        if (++spins > (1LL << 26)) __trap();
+      }
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) pdl_trigger();  // after this block's waits, as every kernel here
+  for (int c = threadIdx.x; c < 8 * a.Z; c += blockDim.x) {
+    const int i = c / a.Z, cz = c - i * a.Z;
+    const long long r = (long long)s_rb[i][cz];
+    s_rb[i][cz] = r >= 0 ? ld_u64(a.row_bits + r) : 0ull;
+  }
+  __syncthreads();
+  const int wpr = a.Nx >> 5;
+  const long long plane = (long long)wpr * a.Ny * a.Nz;
+  // 16 words per z cell: (ly, lz) voxel rows of the 8 cells' 4-bit x runs
+  for (int t = threadIdx.x; t < 16 * a.Z; t += blockDim.x) {
+    const int cz = t >> 4, ly = t & 3, lz = (t >> 2) & 3;
+    const int sh = 4 * (ly + 4 * lz);
+    uint32_t word = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) word |= (uint32_t)((s_rb[i][cz] >> sh) & 0xFull) << (4 * i);
+    a.out[b * plane + w + (long long)wpr * ((4 * cy + ly) + (long long)a.Ny * (4 * cz + lz))] = word;
+  }
+}
+
 }  // namespace halo
 }  // namespace fpvs
+
+extern "C" int fpvs_rowbits_to_grid_flow(const uint64_t* row_bits, const int32_t* index_vol, int B, int Nx, int Ny,
+                                         int Nz, int d, uint8_t* out_bits, const int32_t* tile_done_in,
+                                         void* stream) {
+  FPVS_CHECK_ARG(row_bits && index_vol && out_bits && tile_done_in, "null pointer");
+  FPVS_CHECK_ARG(d == 4, "fpvs_rowbits_to_grid_flow: d = 4 (64 bits per cell), got %d", d);
+  FPVS_CHECK_ARG(B >= 1 && Nx > 0 && Ny > 0 && Nz > 0 && Nx % 32 == 0 && Ny % 4 == 0 && Nz % 4 == 0,
+                 "grid must be B x Nx x Ny x Nz with N_x %% 32 == 0 and N_y, N_z %% 4 == 0");
+  FPVS_CHECK_ARG(Nz / 4 <= halo::kFlowMaxZ, "N_z <= %d", 4 * halo::kFlowMaxZ);
+  FPVS_CHECK_ARG(((uintptr_t)out_bits & 3) == 0, "out_bits must be 4-byte aligned");
+  halo::RowBitsArgs a{reinterpret_cast<const unsigned long long*>(row_bits), index_vol, B, Nx / 4, Ny / 4, Nz / 4,
+                      Nx, Ny, Nz, reinterpret_cast<uint32_t*>(out_bits)};
+  const long long blocks = (long long)B * (a.X / 8) * a.Y;
+  FPVS_CHECK_ARG(blocks < (1LL << 31), "grid too large");
+  cudaError_t e = launch_kernel(halo::rowbits_grid_flow_kernel, dim3((unsigned)blocks), dim3(256), 0,
+                                as_stream(stream), a, tile_done_in);
+  if (e != cudaSuccess) return set_error(FPVS_ECUDA, "fpvs_rowbits_to_grid_flow: %s", cudaGetErrorString(e));
+  FPVS_CHECK_LAUNCH("fpvs_rowbits_to_grid_flow");
+  return FPVS_OK;
+}
 
 extern "C" int fpvs_rowbits_to_grid(const uint64_t* row_bits, const int32_t* index_vol, int B, int Nx, int Ny, int Nz,
                                     int d, uint8_t* out_bits, void* stream) {

@@ -174,9 +174,13 @@ class UNetPlan:
         # (fpvs_spconv_tc_flow): measured 2 us slower per frame (enc0b's
         # per-tile publishing outweighs down01's head start), so opt-in only
         self.flow_tc = {"down01": "enc0b"} if os.environ.get("FPVS_FLOW_TC", "0") == "1" else {}
+        # the grid writer as a dataflow consumer of dec0b + head
+        # (fpvs_rowbits_to_grid_flow; FPVS_GRID_FLOW=0: after dec0b's grid)
+        self.grid_flow = self.flow and os.environ.get("FPVS_GRID_FLOW", "1") != "0"
         self.done = {}
         if self.flow:
-            for prod in list(self.flow_pairs.values()) + list(self.flow_tc.values()):
+            for prod in list(self.flow_pairs.values()) + list(self.flow_tc.values()) + \
+                    (["dec0b"] if self.grid_flow else []):
                 lv = self.level_of[prod]
                 self.done[prod] = torch.zeros((lv.cap + 127) // 128, dtype=torch.int32, device=device)
         # the fused head's per-row 64-bit cell masks (fpvs_rowbits_to_grid writes the grid from them)
@@ -427,15 +431,28 @@ class UNetPlan:
                 hl = L["head"]
                 ht = L0.extra["halo"]
                 ws = self.halo_ws[id(L0)]
-                _lib.call("fpvs_spconv_halo_head", _lib.ptr(self.t0a), c0, self.t0a.shape[0], _lib.ptr(L0.nbr),
-                          _lib.ptr(ht["lnbr"]), _lib.ptr(ht["rows"]), _lib.ptr(ht["n"]), _lib.ptr(m0), _lib.ptr(L0.n),
-                          L0.cap, _lib.ptr(L["dec0b"].packed(64)), _lib.ptr(L["dec0b"].b), c0, _lib.ptr(ws), ws.numel(),
-                          _lib.ptr(hl.packed(64)), _lib.ptr(hl.b), float(tau), _lib.ptr(self.row_bits),
-                          _lib.TABLES_SETTLED if self.settled else 0, _lib.ptr(flow_in.get("dec0b")),
-                          _lib.stream_ptr())
-                _lib.call("fpvs_rowbits_to_grid", _lib.ptr(self.row_bits), _lib.ptr(L0.index_vol), self.B, nx, ny, nz,
-                          net.d, _lib.ptr(out_bits), _lib.stream_ptr())
+                args = [_lib.ptr(self.t0a), c0, self.t0a.shape[0], _lib.ptr(L0.nbr), _lib.ptr(ht["lnbr"]),
+                        _lib.ptr(ht["rows"]), _lib.ptr(ht["n"]), _lib.ptr(m0), _lib.ptr(L0.n), L0.cap,
+                        _lib.ptr(L["dec0b"].packed(64)), _lib.ptr(L["dec0b"].b), c0, _lib.ptr(ws), ws.numel(),
+                        _lib.ptr(hl.packed(64)), _lib.ptr(hl.b), float(tau), _lib.ptr(self.row_bits),
+                        _lib.TABLES_SETTLED if self.settled else 0, _lib.ptr(flow_in.get("dec0b"))]
+                if grid_done is not None:
+                    _lib.call("fpvs_spconv_halo_head_flow", *args, _lib.ptr(grid_done), _lib.stream_ptr())
+                else:
+                    _lib.call("fpvs_spconv_halo_head", *args, _lib.stream_ptr())
+
+            # the grid writer waits only for the dec0b tiles its cells' rows lie in
+            grid_done = self.done.get("dec0b") if (self.grid_flow and self.settled and nz // 4 <= 256) else None
+
+            def grid_writer():
+                if grid_done is not None:
+                    _lib.call("fpvs_rowbits_to_grid_flow", _lib.ptr(self.row_bits), _lib.ptr(L0.index_vol), self.B,
+                              nx, ny, nz, net.d, _lib.ptr(out_bits), _lib.ptr(grid_done), _lib.stream_ptr())
+                else:
+                    _lib.call("fpvs_rowbits_to_grid", _lib.ptr(self.row_bits), _lib.ptr(L0.index_vol), self.B, nx,
+                              ny, nz, net.d, _lib.ptr(out_bits), _lib.stream_ptr())
             out.append(("dec0b", dec0b_head))
+            out.append(("grid", grid_writer))  # its own stage: per-stage times keep it out of dec0b's
             return out
         conv("dec0b", self.t0a, c0, L0.nbr, 27, L0, self.t0b, c0, masks=m0)
 

@@ -172,6 +172,13 @@ def test_rowbits_to_grid_matches_dense_scatter():
     _lib.call("fpvs_rowbits_to_grid", _lib.ptr(rbt), _lib.ptr(ivt), B, *dims, 4, _lib.ptr(out), _lib.stream_ptr())
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), ref)
+    # the dataflow writer (every producer tile already published) writes the same words
+    done = torch.full(((n + 127) // 128,), 4, dtype=torch.int32, device="cuda")
+    out2 = torch.full_like(out, 0xA5)
+    _lib.call("fpvs_rowbits_to_grid_flow", _lib.ptr(rbt), _lib.ptr(ivt), B, *dims, 4, _lib.ptr(out2), _lib.ptr(done),
+              _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(out2.cpu().numpy(), ref)
     # argument checks: d != 4 and N_x % 32 != 0 are rejected
     with pytest.raises(Exception):
         _lib.call("fpvs_rowbits_to_grid", _lib.ptr(rbt), _lib.ptr(ivt), B, *dims, 2, _lib.ptr(out), _lib.stream_ptr())
