@@ -328,7 +328,10 @@ class FramePipeline:
         while len(pipes) < inflight:
             p = FramePipeline(self.net, self.B, self.grid_dims, self.tau, graph=self._use_graph)
             if inflight > 1:
+                # concurrent frames fill each other's idle SMs: no spinning
+                # dataflow consumers (conv pairs, grid writer) in the lanes
                 p.plan.flow = False
+                p.plan.grid_flow = False
             p.in_bits.copy_(self.in_bits)
             p.capture()
             pipes.append(p)
